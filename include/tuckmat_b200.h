@@ -1,0 +1,142 @@
+/*
+ * tuckmat_b200 — C ABI of the B200-native Tucker-compressed coupling matvec.
+ *
+ * Drop-in boundary for the reference library's hot path
+ * (/root/reference/proj/include/tuckmat/matvec.hpp).  The reference exposes
+ * a header-only C++ API with no FFI; each entry point below replaces one
+ * reference function, cited as file:line (paths relative to
+ * /root/reference/proj).  The C++ drop-in that re-declares the reference
+ * signatures on top of this ABI is include/tuckmat_b200/tuckmat.hpp.
+ *
+ * Conventions
+ *   - Complex scalars are interleaved (re, im) pairs: float for TM_C64
+ *     stores, double for TM_C128 stores.  Host-side store payloads are
+ *     always complex128 (the reference's only scalar type,
+ *     include/tuckmat/tensor.hpp:14); a TM_C64 store rounds them once.
+ *   - Multivectors are column-major with a leading dimension (elements),
+ *     like Eigen::MatrixXcd (include/tuckmat/matvec.hpp:13).
+ *   - Rows of the coupling matrix are component-major, voxel index
+ *     f1-fastest (src/compress.cpp:52-65).
+ *   - Every call returns a tm_status; on failure tm_last_error() returns a
+ *     thread-local message.  Status codes map one-to-one onto the reference
+ *     exception types (include/tuckmat/errors.hpp:10-48).
+ *   - There is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point fails with TM_CUDA_ERROR.
+ *   - A store is immutable after creation.  Products on one store are
+ *     serialised by an internal mutex (they share device work buffers);
+ *     products on different stores may run concurrently.
+ */
+#ifndef TUCKMAT_B200_H
+#define TUCKMAT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define TM_API __attribute__((visibility("default")))
+#else
+#define TM_API
+#endif
+
+typedef enum {
+    TM_OK = 0,
+    TM_CONTRACT_VIOLATION = 1, /* tuckmat::ContractViolation  (errors.hpp:16-19) */
+    TM_CAPACITY_ERROR = 2,     /* tuckmat::CapacityError      (errors.hpp:27-30) */
+    TM_PARSE_ERROR = 3,        /* tuckmat::ParseError         (errors.hpp:39-45) */
+    TM_CUDA_ERROR = 6,         /* device / driver failure (no reference analogue) */
+    TM_ERROR = 9               /* tuckmat::Error              (errors.hpp:10-13) */
+} tm_status;
+
+typedef enum { TM_C64 = 0, TM_C128 = 1 } tm_dtype;
+
+typedef enum { TM_HOST = 0, TM_DEVICE = 1 } tm_where;
+
+typedef struct tm_store tm_store;
+
+/*
+ * Store description.  Mirrors CompressedCoupling (include/tuckmat/compress.hpp:14-25)
+ * — `ncols` = m, tensors columns[j][k] — or, for an ACA store, the Tucker U
+ * of AcaFactors (include/tuckmat/aca.hpp:24-41) — `ncols` = r_c, tensors
+ * tucker_u[k][l] listed l-major — plus V.
+ *
+ * ranks:   ncols*q*3 int32, [col][comp][mode].
+ * payload: per tensor, in [col][comp] order, the CTC1 payload layout
+ *          (src/io.cpp:121-129): core r1*r2*r3 f1-fastest, then U1 (n1 x r1),
+ *          U2, U3 column-major; complex128 pairs.
+ * v:       ACA only (else NULL): V, m2 x r_c column-major complex128.
+ */
+typedef struct {
+    int32_t q;
+    int64_t ncols;
+    int64_t dims[3];
+    const int32_t* ranks;
+    const double* payload;
+    int32_t payload_on_device; /* payload is a device pointer on `device` */
+    const double* v;
+    int64_t m2;
+    int32_t v_on_device;
+} tm_store_desc;
+
+/* Build the device-resident store (replaces holding CompressedCoupling /
+ * AcaFactors in host memory; K6 "pack_store").  device = CUDA ordinal. */
+TM_API int tm_store_create(const tm_store_desc* desc, int device, int dtype, tm_store** out);
+
+/* Native ingest of a CTC1 / CTA1 file straight into device memory
+ * (replaces load_ctc1 / load_cta1, src/io.cpp:212-230, 249-279). */
+TM_API int tm_store_load_ctc1(const char* path, int device, int dtype, tm_store** out);
+TM_API int tm_store_load_cta1(const char* path, int device, int dtype, tm_store** out);
+
+TM_API int tm_store_destroy(tm_store* s);
+
+/* q, ncols (m or r_c), dims, dtype, m2 (0 unless ACA), device bytes held. */
+TM_API int tm_store_info(const tm_store* s, int32_t* q, int64_t* ncols, int64_t* dims3, int32_t* dtype,
+                         int64_t* m2, int64_t* device_bytes);
+
+/*
+ * Y = Zbc X  — forward(cc, x, workers, ops) (src/matvec.cpp:132-138) and
+ * stacked_forward (src/matvec.cpp:17-65).  x: xrows x p (xrows must equal
+ * ncols), y: q*n_v x p.  where = TM_HOST: x, y are host pointers, the call
+ * copies in, computes and copies out before returning.  where = TM_DEVICE:
+ * x, y are device pointers on the store's device and the work is enqueued
+ * on `stream` (a cudaStream_t, NULL = legacy default stream).  ops, if not
+ * NULL, is {decompress_madds, accumulate_madds} and is incremented (+=) as
+ * the reference does (src/matvec.cpp:60-63).
+ */
+TM_API int tm_forward(tm_store* s, const void* x, int64_t ldx, int64_t xrows, int64_t p, void* y, int64_t ldy,
+                      int where, void* stream, int64_t* ops);
+
+/* Z = Zbc^H Phi — adjoint(cc, phi, workers, ops) (src/matvec.cpp:140-148)
+ * and stacked_adjoint (src/matvec.cpp:67-102).  phi: q*n_v x p, z: ncols x p. */
+TM_API int tm_adjoint(tm_store* s, const void* phi, int64_t ldphi, int64_t phirows, int64_t p, void* z,
+                      int64_t ldz, int where, void* stream, int64_t* ops);
+
+/* ACA products (src/matvec.cpp:150-175): y = U (V^H x), z = V (U^H phi).
+ * x: m2 x p, y: q*n_v x p; phi: q*n_v x p, z: m2 x p.  No OpCounts, as in
+ * the reference (include/tuckmat/matvec.hpp:54-57). */
+TM_API int tm_aca_forward(tm_store* s, const void* x, int64_t ldx, int64_t xrows, int64_t p, void* y, int64_t ldy,
+                          int where, void* stream);
+TM_API int tm_aca_adjoint(tm_store* s, const void* phi, int64_t ldphi, int64_t phirows, int64_t p, void* z,
+                          int64_t ldz, int where, void* stream);
+
+/* Exact OpCounts of one product at p right-hand sides, without running it
+ * (reconstruct_madds, src/matvec.cpp:10-15; accumulate term :51,95). */
+TM_API int tm_opcounts(const tm_store* s, int64_t p, int64_t* decompress_madds, int64_t* accumulate_madds);
+
+/* Thread-local message of the last failed call on this thread. */
+TM_API const char* tm_last_error(void);
+
+/* Number of CUDA kernels this library has launched in this process
+ * (instrumentation for the bench's gpu_launches claim). */
+TM_API int64_t tm_launch_count(void);
+
+/* ABI version (bumped on incompatible changes). */
+TM_API int tm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TUCKMAT_B200_H */

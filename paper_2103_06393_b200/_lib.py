@@ -1,0 +1,73 @@
+"""ctypes binding of the C ABI (include/tuckmat_b200.h).
+
+Loads the in-tree ``libtuckmat_b200.so``.  There is no fallback: if the
+library is missing or cannot be loaded the import of the product path fails
+loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtuckmat_b200.so")
+
+TM_OK, TM_CONTRACT_VIOLATION, TM_CAPACITY_ERROR, TM_PARSE_ERROR, TM_CUDA_ERROR, TM_ERROR = 0, 1, 2, 3, 6, 9
+TM_C64, TM_C128 = 0, 1
+TM_HOST, TM_DEVICE = 0, 1
+
+EXPORTED = [
+    "tm_store_create", "tm_store_load_ctc1", "tm_store_load_cta1", "tm_store_destroy", "tm_store_info",
+    "tm_forward", "tm_adjoint", "tm_aca_forward", "tm_aca_adjoint", "tm_opcounts", "tm_last_error",
+    "tm_launch_count", "tm_version",
+]
+
+
+class StoreDesc(ctypes.Structure):
+    _fields_ = [
+        ("q", ctypes.c_int32),
+        ("ncols", ctypes.c_int64),
+        ("dims", ctypes.c_int64 * 3),
+        ("ranks", ctypes.c_void_p),
+        ("payload", ctypes.c_void_p),
+        ("payload_on_device", ctypes.c_int32),
+        ("v", ctypes.c_void_p),
+        ("m2", ctypes.c_int64),
+        ("v_on_device", ctypes.c_int32),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """The loaded library (raises if it is not built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build it with `python -m paper_2103_06393_b200.build` "
+                    "(or __graft_entry__.build()); there is no CPU fallback")
+            L = ctypes.CDLL(LIB_PATH)
+            vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+            L.tm_store_create.argtypes = [ctypes.POINTER(StoreDesc), i32, i32, ctypes.POINTER(vp)]
+            L.tm_store_load_ctc1.argtypes = [ctypes.c_char_p, i32, i32, ctypes.POINTER(vp)]
+            L.tm_store_load_cta1.argtypes = [ctypes.c_char_p, i32, i32, ctypes.POINTER(vp)]
+            L.tm_store_destroy.argtypes = [vp]
+            L.tm_store_info.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+            L.tm_forward.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp, vp]
+            L.tm_adjoint.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp, vp]
+            L.tm_aca_forward.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp]
+            L.tm_aca_adjoint.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp]
+            L.tm_opcounts.argtypes = [vp, i64, vp, vp]
+            L.tm_last_error.restype = ctypes.c_char_p
+            L.tm_launch_count.restype = ctypes.c_int64
+            _lib = L
+    return _lib
+
+
+def launch_count():
+    return int(lib().tm_launch_count())

@@ -1,0 +1,624 @@
+// C ABI of the B200 Tucker-compressed coupling matvec (include/tuckmat_b200.h).
+//
+// Host orchestration only: validation with the reference's error messages,
+// the device store (K6 pack), work buffers, and the launch plan of the
+// forward / adjoint / ACA kernels.  No CPU fallback: every product runs on
+// the device or fails with TM_CUDA_ERROR.
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tuckmat_b200.h"
+#include "tm_aux_kernels.cuh"
+#include "tm_common.cuh"
+#include "tm_kernels_cc.cuh"
+
+using namespace tmb;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+
+struct TmError : std::runtime_error {
+    int code;
+    TmError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void contract(const std::string& m) { throw TmError(TM_CONTRACT_VIOLATION, m); }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        if (e == cudaErrorMemoryAllocation)
+            throw TmError(TM_CAPACITY_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+        throw TmError(TM_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+#define CK(x) ck((x), #x)
+
+void launched(cudaError_t e, const char* what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    ck(e == cudaSuccess ? cudaGetLastError() : e, what);
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        CK(cudaGetDevice(&prev));
+        if (prev != dev) CK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* get(size_t need) {
+        if (need > bytes) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            bytes = 0;
+            CK(cudaMalloc(&p, std::max<size_t>(need, 256)));
+            bytes = std::max<size_t>(need, 256);
+        }
+        return p;
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return TM_OK;
+    } catch (const TmError& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return TM_CAPACITY_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return TM_ERROR;
+    }
+}
+
+int64_t align2(int64_t v) { return (v + 1) & ~int64_t(1); }
+
+}  // namespace
+
+struct tm_store {
+    int device = 0;
+    int dtype = TM_C64;
+    int q = 0;
+    int64_t ncols = 0;
+    int64_t dims[3] = {0, 0, 0};
+    int64_t m2 = 0;
+    int rmax[3] = {1, 1, 1};
+    std::vector<int32_t> ranks;  // [col][comp][mode]
+    int64_t dec_madds = 0;
+    TDesc* d_desc = nullptr;
+    void* d_arena = nullptr;
+    int64_t arena_elems = 0;
+    void* d_v = nullptr;
+    int64_t device_bytes = 0;
+    std::mutex mu;
+    DevBuf part, xin, yout, wbuf;
+
+    int64_t nv() const { return dims[0] * dims[1] * dims[2]; }
+    int64_t rows() const { return q * nv(); }
+    size_t csize() const { return dtype == TM_C64 ? sizeof(float2) : sizeof(double2); }
+    ~tm_store() {
+        if (d_desc) cudaFree(d_desc);
+        if (d_arena) cudaFree(d_arena);
+        if (d_v) cudaFree(d_v);
+    }
+};
+
+namespace {
+
+// ------------------------------------------------------------ store build --
+void build_store(tm_store* s, const tm_store_desc& d) {
+    const int64_t n1 = d.dims[0], n2 = d.dims[1], n3 = d.dims[2];
+    const int64_t ntens = s->ncols * s->q;
+    // host-side tensor table: source offsets ([col][comp] order) and
+    // destination descriptors (component-major order)
+    std::vector<int64_t> src_off(static_cast<size_t>(ntens) + 1, 0);
+    std::vector<TDesc> desc(static_cast<size_t>(std::max<int64_t>(ntens, 1)));
+    int64_t doff = 0;
+    for (int g = 0; g < 3; ++g) s->rmax[g] = 1;
+    for (int64_t i = 0; i < ntens; ++i) {
+        const int32_t* r = d.ranks + 3 * i;
+        for (int g = 0; g < 3; ++g) {
+            if (r[g] < 1 || r[g] > d.dims[g])
+                contract("store: tucker rank " + std::to_string(r[g]) + " out of range for mode " +
+                         std::to_string(g + 1));
+            s->rmax[g] = std::max(s->rmax[g], int(r[g]));
+        }
+        const int64_t sz = int64_t(r[0]) * r[1] * r[2] + n1 * r[0] + n2 * r[1] + n3 * r[2];
+        src_off[i + 1] = src_off[i] + sz;
+        const int64_t j = i / s->q, k = i % s->q;
+        TDesc& t = desc[static_cast<size_t>(k * s->ncols + j)];
+        t.r1 = r[0];
+        t.r2 = r[1];
+        t.r3 = r[2];
+        t.pad = 0;
+        t.off_core = doff;
+        doff += align2(int64_t(r[0]) * r[1] * r[2]);
+        t.off_u1 = doff;
+        doff += align2(n1 * r[0]);
+        t.off_u2 = doff;
+        doff += align2(n2 * r[1]);
+        t.off_u3 = doff;
+        doff += align2(n3 * r[2]);
+        s->dec_madds += n1 * r[0] * r[1] * r[2] + n1 * n2 * r[1] * r[2] + n1 * n2 * n3 * r[2];
+    }
+    s->ranks.assign(d.ranks, d.ranks + 3 * ntens);
+    s->arena_elems = std::max<int64_t>(doff, 2);
+    const size_t cs = s->csize();
+    CK(cudaMalloc(&s->d_arena, size_t(s->arena_elems) * cs));
+    CK(cudaMalloc(reinterpret_cast<void**>(&s->d_desc), desc.size() * sizeof(TDesc)));
+    CK(cudaMemcpy(s->d_desc, desc.data(), desc.size() * sizeof(TDesc), cudaMemcpyHostToDevice));
+    s->device_bytes = int64_t(s->arena_elems * cs + desc.size() * sizeof(TDesc));
+
+    // pack in bounded chunks of whole tensors
+    const int64_t total = src_off[static_cast<size_t>(ntens)];
+    const int64_t chunk_cap = int64_t(16) << 20;  // 16 M complex128 = 256 MiB of staging
+    DevBuf stage, jobbuf;
+    int64_t t0 = 0;
+    while (t0 < ntens) {
+        int64_t t1 = t0 + 1;
+        while (t1 < ntens && src_off[t1 + 1] - src_off[t0] <= chunk_cap) ++t1;
+        const int64_t elems = src_off[t1] - src_off[t0];
+        const double2* src;
+        if (d.payload_on_device) {
+            src = reinterpret_cast<const double2*>(d.payload) + src_off[t0];
+        } else {
+            void* st = stage.get(size_t(elems) * sizeof(double2));
+            CK(cudaMemcpy(st, d.payload + 2 * src_off[t0], size_t(elems) * sizeof(double2), cudaMemcpyHostToDevice));
+            src = static_cast<const double2*>(st);
+        }
+        std::vector<PackJob> jobs(static_cast<size_t>(t1 - t0));
+        for (int64_t i = t0; i < t1; ++i) {
+            const int64_t j = i / s->q, k = i % s->q;
+            jobs[static_cast<size_t>(i - t0)] = {src_off[i] - src_off[t0], k * s->ncols + j};
+        }
+        void* jb = jobbuf.get(jobs.size() * sizeof(PackJob));
+        CK(cudaMemcpy(jb, jobs.data(), jobs.size() * sizeof(PackJob), cudaMemcpyHostToDevice));
+        if (s->dtype == TM_C64)
+            pack_kernel<float2><<<unsigned(jobs.size()), 256>>>(src, static_cast<PackJob*>(jb), s->d_desc, int(n1),
+                                                               int(n2), int(n3), static_cast<float2*>(s->d_arena));
+        else
+            pack_kernel<double2><<<unsigned(jobs.size()), 256>>>(src, static_cast<PackJob*>(jb), s->d_desc, int(n1),
+                                                                int(n2), int(n3), static_cast<double2*>(s->d_arena));
+        launched(cudaSuccess, "pack_kernel");
+        CK(cudaDeviceSynchronize());
+        t0 = t1;
+    }
+
+    if (d.v) {
+        if (d.m2 < 1) contract("store: ACA V needs m2 >= 1");
+        s->m2 = d.m2;
+        const int64_t n = d.m2 * s->ncols;
+        CK(cudaMalloc(&s->d_v, size_t(std::max<int64_t>(n, 1)) * cs));
+        s->device_bytes += n * int64_t(cs);
+        if (n > 0) {
+            DevBuf vst;
+            const double2* src;
+            if (d.v_on_device) {
+                src = reinterpret_cast<const double2*>(d.v);
+            } else {
+                void* st = vst.get(size_t(n) * sizeof(double2));
+                CK(cudaMemcpy(st, d.v, size_t(n) * sizeof(double2), cudaMemcpyHostToDevice));
+                src = static_cast<const double2*>(st);
+            }
+            const unsigned grid = unsigned(std::min<int64_t>((n + 255) / 256, 4096));
+            if (s->dtype == TM_C64)
+                convert_kernel<float2><<<grid, 256>>>(src, n, static_cast<float2*>(s->d_v));
+            else
+                convert_kernel<double2><<<grid, 256>>>(src, n, static_cast<double2*>(s->d_v));
+            launched(cudaSuccess, "convert_kernel");
+            CK(cudaDeviceSynchronize());
+        }
+    }
+}
+
+tm_store* create_store(const tm_store_desc& d, int device, int dtype) {
+    if (dtype != TM_C64 && dtype != TM_C128) contract("store: dtype must be TM_C64 or TM_C128");
+    if (d.q < 1 || d.ncols < 0 || d.dims[0] < 1 || d.dims[1] < 1 || d.dims[2] < 1)
+        contract("store: non-positive dimensions");
+    if (d.dims[0] > (1 << 30) || d.dims[1] > (1 << 30) || d.dims[2] > (1 << 30))
+        contract("store: grid dimension too large");
+    if (d.ncols > 0 && (!d.ranks || !d.payload)) contract("store: ranks and payload are required");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw TmError(TM_CUDA_ERROR, "store: no CUDA device " + std::to_string(device));
+    DeviceGuard guard(device);
+    auto* s = new tm_store;
+    s->device = device;
+    s->dtype = dtype;
+    s->q = d.q;
+    s->ncols = d.ncols;
+    for (int g = 0; g < 3; ++g) s->dims[g] = d.dims[g];
+    try {
+        build_store(s, d);
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    return s;
+}
+
+// ------------------------------------------------------------ kernel plan --
+constexpr size_t kSmemBudget = 100 * 1024;  // 2 CTAs / SM
+constexpr size_t kSmemMax = 227 * 1024;
+
+template <typename C, int RM, int CN, int NW, int TI1>
+struct CcPlan {
+    static constexpr int ROWS = RM * NW, TI2 = ROWS / TI1, TI3 = 32 * CN;
+    CcGeom g{};
+    size_t smem = 0;
+    dim3 grid;
+    CcPlan(const tm_store* s, bool adjoint) {
+        g.ncols = s->ncols;
+        g.n1 = int(s->dims[0]);
+        g.n2 = int(s->dims[1]);
+        g.n3 = int(s->dims[2]);
+        g.q = s->q;
+        g.nt1 = int((g.n1 + TI1 - 1) / TI1);
+        g.nt2 = int((g.n2 + TI2 - 1) / TI2);
+        g.rmax1 = s->rmax[0];
+        g.rmax2 = s->rmax[1];
+        g.rmax3 = s->rmax[2];
+        const int nt3 = (g.n3 + TI3 - 1) / TI3;
+        const size_t slot = size_t(cc_slot_elems<TI1, TI2, TI3>(g.rmax1, g.rmax2, g.rmax3)) * sizeof(C);
+        const size_t red = adjoint ? size_t(8 * NW) * sizeof(C) : 0;
+        int jb = 8;
+        while (jb > 1 && slot * jb + red > kSmemBudget) --jb;
+        if (slot * jb + red > kSmemMax)
+            throw TmError(TM_CAPACITY_ERROR,
+                          "tucker ranks (" + std::to_string(g.rmax1) + "," + std::to_string(g.rmax2) + "," +
+                              std::to_string(g.rmax3) + ") exceed the shared-memory plan of the CUDA-core kernel");
+        g.jb = jb;
+        smem = slot * jb + red;
+        grid = dim3(unsigned(int64_t(g.nt1) * g.nt2 * nt3), unsigned(s->q), 1);
+    }
+};
+
+template <typename C, int RM, int CN, int NW, int TI1>
+void run_forward_cc(const tm_store* s, const C* x, int64_t ldx, int64_t p, C* y, int64_t ldy, cudaStream_t st) {
+    CcPlan<C, RM, CN, NW, TI1> plan(s, false);
+    auto kern = fwd_cc_kernel<C, RM, CN, NW, TI1>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan.smem)));
+    for (int64_t c0 = 0; c0 < p; c0 += 65535) {
+        dim3 grid = plan.grid;
+        grid.z = unsigned(std::min<int64_t>(65535, p - c0));
+        kern<<<grid, NW * 32, plan.smem, st>>>(s->d_desc, static_cast<const C*>(s->d_arena), plan.g, x + ldx * c0, ldx,
+                                               y + ldy * c0, ldy);
+        launched(cudaSuccess, "fwd_cc_kernel");
+    }
+}
+
+template <typename C, int RM, int CN, int NW, int TI1>
+void run_adjoint_cc(tm_store* s, const C* phi, int64_t ldphi, int64_t p, C* z, int64_t ldz, cudaStream_t st) {
+    CcPlan<C, RM, CN, NW, TI1> plan(s, true);
+    const int64_t ntiles = plan.grid.x;
+    const int64_t nred = ntiles * s->q;
+    C* part = static_cast<C*>(s->part.get(size_t(s->ncols * p * nred) * sizeof(C)));
+    auto kern = adj_cc_kernel<C, RM, CN, NW, TI1>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan.smem)));
+    for (int64_t c0 = 0; c0 < p; c0 += 65535) {
+        dim3 grid = plan.grid;
+        grid.z = unsigned(std::min<int64_t>(65535, p - c0));
+        kern<<<grid, NW * 32, plan.smem, st>>>(s->d_desc, static_cast<const C*>(s->d_arena), plan.g,
+                                               phi + ldphi * c0, ldphi, part + s->ncols * nred * c0);
+        launched(cudaSuccess, "adj_cc_kernel");
+    }
+    const int64_t warps = s->ncols * p;
+    const unsigned blocks = unsigned((warps * 32 + 255) / 256);
+    adj_reduce_kernel<C><<<blocks, 256, 0, st>>>(part, s->ncols, p, nred, z, ldz);
+    launched(cudaSuccess, "adj_reduce_kernel");
+}
+
+// n3-dependent choice of lanes-per-i3 (CN): smallest padded n3, weighted by
+// the smem-traffic cost of narrow micro-tiles.
+int pick_cn(int64_t n3) {
+    double best = 1e300;
+    int cn = 4;
+    const int cands[3] = {4, 2, 1};
+    const double cost[3] = {1.0, 1.2, 1.6};
+    for (int i = 0; i < 3; ++i) {
+        const int64_t ti3 = 32 * cands[i];
+        const double c = double((n3 + ti3 - 1) / ti3 * ti3) * cost[i];
+        if (c < best - 1e-9) {
+            best = c;
+            cn = cands[i];
+        }
+    }
+    return cn;
+}
+
+void forward_dev(const tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy, cudaStream_t st) {
+    const int cn = pick_cn(s->dims[2]);
+    if (s->dtype == TM_C64) {
+        auto X = static_cast<const float2*>(x);
+        auto Y = static_cast<float2*>(y);
+        if (cn == 4) run_forward_cc<float2, 8, 4, 8, 8>(s, X, ldx, p, Y, ldy, st);
+        else if (cn == 2) run_forward_cc<float2, 8, 2, 8, 8>(s, X, ldx, p, Y, ldy, st);
+        else run_forward_cc<float2, 8, 1, 8, 8>(s, X, ldx, p, Y, ldy, st);
+    } else {
+        auto X = static_cast<const double2*>(x);
+        auto Y = static_cast<double2*>(y);
+        if (cn == 4) run_forward_cc<double2, 4, 4, 8, 8>(s, X, ldx, p, Y, ldy, st);
+        else if (cn == 2) run_forward_cc<double2, 4, 2, 8, 8>(s, X, ldx, p, Y, ldy, st);
+        else run_forward_cc<double2, 4, 1, 8, 8>(s, X, ldx, p, Y, ldy, st);
+    }
+}
+
+void adjoint_dev(tm_store* s, const void* phi, int64_t ldphi, int64_t p, void* z, int64_t ldz, cudaStream_t st) {
+    if (s->ncols == 0 || p == 0) return;
+    const int cn = pick_cn(s->dims[2]);
+    if (s->dtype == TM_C64) {
+        auto P = static_cast<const float2*>(phi);
+        auto Z = static_cast<float2*>(z);
+        if (cn == 4) run_adjoint_cc<float2, 8, 4, 8, 8>(s, P, ldphi, p, Z, ldz, st);
+        else if (cn == 2) run_adjoint_cc<float2, 8, 2, 8, 8>(s, P, ldphi, p, Z, ldz, st);
+        else run_adjoint_cc<float2, 8, 1, 8, 8>(s, P, ldphi, p, Z, ldz, st);
+    } else {
+        auto P = static_cast<const double2*>(phi);
+        auto Z = static_cast<double2*>(z);
+        if (cn == 4) run_adjoint_cc<double2, 4, 4, 8, 8>(s, P, ldphi, p, Z, ldz, st);
+        else if (cn == 2) run_adjoint_cc<double2, 4, 2, 8, 8>(s, P, ldphi, p, Z, ldz, st);
+        else run_adjoint_cc<double2, 4, 1, 8, 8>(s, P, ldphi, p, Z, ldz, st);
+    }
+}
+
+void aca_vhx_dev(const tm_store* s, const void* x, int64_t ldx, int64_t p, void* w, cudaStream_t st) {
+    const int64_t warps = s->ncols * p;
+    if (warps == 0) return;
+    const unsigned blocks = unsigned((warps * 32 + 255) / 256);
+    if (s->dtype == TM_C64)
+        aca_vhx_kernel<float2><<<blocks, 256, 0, st>>>(static_cast<const float2*>(s->d_v), s->m2, s->ncols,
+                                                       static_cast<const float2*>(x), ldx, p, static_cast<float2*>(w));
+    else
+        aca_vhx_kernel<double2><<<blocks, 256, 0, st>>>(static_cast<const double2*>(s->d_v), s->m2, s->ncols,
+                                                        static_cast<const double2*>(x), ldx, p,
+                                                        static_cast<double2*>(w));
+    launched(cudaSuccess, "aca_vhx_kernel");
+}
+
+void aca_vt_dev(const tm_store* s, const void* t, int64_t p, void* z, int64_t ldz, cudaStream_t st) {
+    const int64_t n = s->m2 * p;
+    if (n == 0) return;
+    const unsigned blocks = unsigned((n + 255) / 256);
+    if (s->dtype == TM_C64)
+        aca_vt_kernel<float2><<<blocks, 256, 0, st>>>(static_cast<const float2*>(s->d_v), s->m2, s->ncols,
+                                                      static_cast<const float2*>(t), p, static_cast<float2*>(z), ldz);
+    else
+        aca_vt_kernel<double2><<<blocks, 256, 0, st>>>(static_cast<const double2*>(s->d_v), s->m2, s->ncols,
+                                                       static_cast<const double2*>(t), p, static_cast<double2*>(z),
+                                                       ldz);
+    launched(cudaSuccess, "aca_vt_kernel");
+}
+
+void zero_dev(const tm_store* s, void* y, int64_t rows, int64_t p, int64_t ldy, cudaStream_t st) {
+    if (rows * p == 0) return;
+    const unsigned blocks = unsigned(std::min<int64_t>((rows * p + 255) / 256, 8192));
+    if (s->dtype == TM_C64)
+        zero_kernel<float2><<<blocks, 256, 0, st>>>(static_cast<float2*>(y), rows, p, ldy);
+    else
+        zero_kernel<double2><<<blocks, 256, 0, st>>>(static_cast<double2*>(y), rows, p, ldy);
+    launched(cudaSuccess, "zero_kernel");
+}
+
+// ------------------------------------------------------------ host staging --
+// Runs `body(dev_in, ld_in, dev_out, ld_out)` with host-side in/out blocks
+// staged through the store's work buffers on a private stream.
+template <typename Body>
+void with_host_io(tm_store* s, const void* in, int64_t ldin, int64_t inrows, int64_t p, void* out, int64_t ldout,
+                  int64_t outrows, Body body) {
+    const size_t cs = s->csize();
+    void* din = s->xin.get(size_t(std::max<int64_t>(inrows * p, 1)) * cs);
+    void* dout = s->yout.get(size_t(std::max<int64_t>(outrows * p, 1)) * cs);
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    try {
+        if (inrows * p > 0)
+            CK(cudaMemcpy2DAsync(din, size_t(inrows) * cs, in, size_t(ldin) * cs, size_t(inrows) * cs, size_t(p),
+                                 cudaMemcpyHostToDevice, st));
+        body(din, inrows, dout, outrows, st);
+        if (outrows * p > 0)
+            CK(cudaMemcpy2DAsync(out, size_t(ldout) * cs, dout, size_t(outrows) * cs, size_t(outrows) * cs, size_t(p),
+                                 cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    } catch (...) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+        throw;
+    }
+    CK(cudaStreamDestroy(st));
+}
+
+void check_common(const tm_store* s, int64_t p, int64_t ldin, int64_t inrows, int64_t ldout, int64_t outrows,
+                  int where, const void* in, const void* out) {
+    if (!s) contract("null store");
+    if (p < 0) contract("negative right-hand-side count");
+    if (ldin < std::max<int64_t>(inrows, 1) && p > 0) contract("leading dimension of the input is too small");
+    if (ldout < std::max<int64_t>(outrows, 1) && p > 0) contract("leading dimension of the output is too small");
+    if (where != TM_HOST && where != TM_DEVICE) contract("where must be TM_HOST or TM_DEVICE");
+    if (p > 0 && ((inrows > 0 && !in) || (outrows > 0 && !out))) contract("null input or output pointer");
+}
+
+}  // namespace
+
+// ================================================================== C ABI ==
+extern "C" {
+
+TM_API int tm_version(void) { return 1; }
+
+TM_API const char* tm_last_error(void) { return g_last_error.c_str(); }
+
+void tmb_set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
+
+TM_API int64_t tm_launch_count(void) { return g_launches.load(); }
+
+TM_API int tm_store_create(const tm_store_desc* desc, int device, int dtype, tm_store** out) {
+    return guarded([&] {
+        if (!desc || !out) contract("tm_store_create: null argument");
+        *out = create_store(*desc, device, dtype);
+    });
+}
+
+TM_API int tm_store_destroy(tm_store* s) {
+    return guarded([&] {
+        if (!s) return;
+        DeviceGuard guard(s->device);
+        delete s;
+    });
+}
+
+TM_API int tm_store_info(const tm_store* s, int32_t* q, int64_t* ncols, int64_t* dims3, int32_t* dtype, int64_t* m2,
+                         int64_t* device_bytes) {
+    return guarded([&] {
+        if (!s) contract("null store");
+        if (q) *q = s->q;
+        if (ncols) *ncols = s->ncols;
+        if (dims3)
+            for (int g = 0; g < 3; ++g) dims3[g] = s->dims[g];
+        if (dtype) *dtype = s->dtype;
+        if (m2) *m2 = s->m2;
+        if (device_bytes) *device_bytes = s->device_bytes;
+    });
+}
+
+TM_API int tm_opcounts(const tm_store* s, int64_t p, int64_t* dec, int64_t* acc) {
+    return guarded([&] {
+        if (!s) contract("null store");
+        if (dec) *dec = s->dec_madds;
+        if (acc) *acc = s->ncols * s->q * s->nv() * p;
+    });
+}
+
+TM_API int tm_forward(tm_store* s, const void* x, int64_t ldx, int64_t xrows, int64_t p, void* y, int64_t ldy,
+                      int where, void* stream, int64_t* ops) {
+    return guarded([&] {
+        if (!s) contract("null store");
+        if (xrows != s->ncols)
+            contract("forward: x has " + std::to_string(xrows) + " rows, expected m = " + std::to_string(s->ncols));
+        check_common(s, p, ldx, xrows, ldy, s->rows(), where, x, y);
+        std::lock_guard<std::mutex> lock(s->mu);
+        DeviceGuard guard(s->device);
+        if (p > 0) {
+            if (where == TM_DEVICE)
+                forward_dev(s, x, ldx, p, y, ldy, static_cast<cudaStream_t>(stream));
+            else
+                with_host_io(s, x, ldx, xrows, p, y, ldy, s->rows(),
+                             [&](void* din, int64_t ldi, void* dout, int64_t ldo, cudaStream_t st) {
+                                 forward_dev(s, din, ldi, p, dout, ldo, st);
+                             });
+        }
+        if (ops) {
+            ops[0] += s->dec_madds;
+            ops[1] += s->ncols * s->q * s->nv() * p;
+        }
+    });
+}
+
+TM_API int tm_adjoint(tm_store* s, const void* phi, int64_t ldphi, int64_t phirows, int64_t p, void* z, int64_t ldz,
+                      int where, void* stream, int64_t* ops) {
+    return guarded([&] {
+        if (!s) contract("null store");
+        if (phirows != s->rows())
+            contract("adjoint: phi has " + std::to_string(phirows) + " rows, expected q*n_v = " +
+                     std::to_string(s->rows()));
+        check_common(s, p, ldphi, phirows, ldz, s->ncols, where, phi, z);
+        std::lock_guard<std::mutex> lock(s->mu);
+        DeviceGuard guard(s->device);
+        if (p > 0 && s->ncols > 0) {
+            if (where == TM_DEVICE)
+                adjoint_dev(s, phi, ldphi, p, z, ldz, static_cast<cudaStream_t>(stream));
+            else
+                with_host_io(s, phi, ldphi, phirows, p, z, ldz, s->ncols,
+                             [&](void* din, int64_t ldi, void* dout, int64_t ldo, cudaStream_t st) {
+                                 adjoint_dev(s, din, ldi, p, dout, ldo, st);
+                             });
+        }
+        if (ops) {
+            ops[0] += s->dec_madds;
+            ops[1] += s->ncols * s->q * s->nv() * p;
+        }
+    });
+}
+
+TM_API int tm_aca_forward(tm_store* s, const void* x, int64_t ldx, int64_t xrows, int64_t p, void* y, int64_t ldy,
+                          int where, void* stream) {
+    return guarded([&] {
+        if (!s) contract("null store");
+        if (!s->d_v) contract("aca_forward: store carries no ACA V factor");
+        if (xrows != s->m2)
+            contract("aca_forward: x has " + std::to_string(xrows) + " rows, expected " + std::to_string(s->m2));
+        check_common(s, p, ldx, xrows, ldy, s->rows(), where, x, y);
+        std::lock_guard<std::mutex> lock(s->mu);
+        DeviceGuard guard(s->device);
+        if (p == 0) return;
+        auto body = [&](const void* xin, int64_t ldi, void* yout, int64_t ldo, cudaStream_t st) {
+            if (s->ncols == 0) {
+                zero_dev(s, yout, s->rows(), p, ldo, st);
+                return;
+            }
+            void* w = s->wbuf.get(size_t(s->ncols * p) * s->csize());
+            aca_vhx_dev(s, xin, ldi, p, w, st);
+            forward_dev(s, w, s->ncols, p, yout, ldo, st);
+        };
+        if (where == TM_DEVICE)
+            body(x, ldx, y, ldy, static_cast<cudaStream_t>(stream));
+        else
+            with_host_io(s, x, ldx, xrows, p, y, ldy, s->rows(),
+                         [&](void* din, int64_t ldi, void* dout, int64_t ldo, cudaStream_t st) {
+                             body(din, ldi, dout, ldo, st);
+                         });
+    });
+}
+
+TM_API int tm_aca_adjoint(tm_store* s, const void* phi, int64_t ldphi, int64_t phirows, int64_t p, void* z,
+                          int64_t ldz, int where, void* stream) {
+    return guarded([&] {
+        if (!s) contract("null store");
+        if (!s->d_v) contract("aca_adjoint: store carries no ACA V factor");
+        if (phirows != s->rows())
+            contract("aca_adjoint: phi has " + std::to_string(phirows) + " rows, expected " +
+                     std::to_string(s->rows()));
+        check_common(s, p, ldphi, phirows, ldz, s->m2, where, phi, z);
+        std::lock_guard<std::mutex> lock(s->mu);
+        DeviceGuard guard(s->device);
+        if (p == 0) return;
+        auto body = [&](const void* pin, int64_t ldi, void* zout, int64_t ldo, cudaStream_t st) {
+            if (s->ncols == 0) {
+                zero_dev(s, zout, s->m2, p, ldo, st);
+                return;
+            }
+            void* t = s->wbuf.get(size_t(s->ncols * p) * s->csize());
+            adjoint_dev(s, pin, ldi, p, t, s->ncols, st);
+            aca_vt_dev(s, t, p, zout, ldo, st);
+        };
+        if (where == TM_DEVICE)
+            body(phi, ldphi, z, ldz, static_cast<cudaStream_t>(stream));
+        else
+            with_host_io(s, phi, ldphi, phirows, p, z, ldz, s->m2,
+                         [&](void* din, int64_t ldi, void* dout, int64_t ldo, cudaStream_t st) {
+                             body(din, ldi, dout, ldo, st);
+                         });
+    });
+}
+
+}  // extern "C"

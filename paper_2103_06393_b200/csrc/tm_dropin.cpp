@@ -1,0 +1,424 @@
+// C++ drop-in of the reference matvec API on top of the C ABI
+// (include/tuckmat_b200/tuckmat.hpp).  Host glue only: flatten the
+// reference value types into a tm_store_desc, keep the device store cached
+// by object identity, convert MultiVector blocks to the store precision and
+// map status codes back onto the reference exception types.
+#include "../../include/tuckmat_b200/tuckmat.hpp"
+
+#include <cmath>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "tm_io_internal.hpp"
+
+namespace tuckmat {
+
+double Matrix::norm() const {
+    double s = 0;
+    for (const Complex& z : d_) s += std::norm(z);
+    return std::sqrt(s);
+}
+
+Tensor3::Tensor3(Index n1, Index n2, Index n3) : dims_{n1, n2, n3} {
+    if (n1 <= 0 || n2 <= 0 || n3 <= 0) throw ContractViolation("Tensor3: dimensions must be positive");
+    data_.assign(static_cast<std::size_t>(n1 * n2 * n3), Complex(0));
+}
+
+std::int64_t reconstruct_madds(const TuckerTensor& tt) {
+    const Index n1 = tt.dims[0], n2 = tt.dims[1], n3 = tt.dims[2];
+    const Index r1 = tt.core.dim(1), r2 = tt.core.dim(2), r3 = tt.core.dim(3);
+    return std::int64_t(n1) * r1 * r2 * r3 + std::int64_t(n1) * n2 * r2 * r3 + std::int64_t(n1) * n2 * n3 * r3;
+}
+
+namespace {
+
+[[noreturn]] void rethrow(int st) {
+    const std::string msg = tm_last_error();
+    switch (st) {
+    case TM_CONTRACT_VIOLATION:
+        throw ContractViolation(msg);
+    case TM_CAPACITY_ERROR:
+        throw CapacityError(msg);
+    case TM_PARSE_ERROR: {
+        std::uint64_t off = 0;
+        const auto p = msg.rfind("(byte offset ");
+        if (p != std::string::npos) off = std::strtoull(msg.c_str() + p + 13, nullptr, 10);
+        throw ParseError(msg, off);
+    }
+    default:
+        throw Error(msg);
+    }
+}
+
+void check(int st) {
+    if (st != TM_OK) rethrow(st);
+}
+
+struct Flat {
+    std::vector<std::int32_t> ranks;
+    std::vector<double> payload;
+};
+
+void append_tensor(Flat& f, const TuckerTensor& tt, const Dims3& dims) {
+    for (int g = 0; g < 3; ++g) {
+        if (tt.factors[g].rows() != dims[g] || tt.factors[g].cols() != tt.core.dim(g + 1))
+            throw ContractViolation("TuckerTensor factor " + std::to_string(g + 1) + " does not match the core");
+        f.ranks.push_back(static_cast<std::int32_t>(tt.core.dim(g + 1)));
+    }
+    auto put = [&](const Complex* p, Index n) {
+        for (Index i = 0; i < n; ++i) {
+            f.payload.push_back(p[i].real());
+            f.payload.push_back(p[i].imag());
+        }
+    };
+    put(tt.core.data(), tt.core.size());
+    for (int g = 0; g < 3; ++g) put(tt.factors[g].data(), tt.factors[g].size());
+}
+
+tm_store* make_store(int q, Index ncols, const Dims3& dims,
+                     const std::function<const TuckerTensor&(Index, int)>& at, const Matrix* v, int dtype,
+                     int device) {
+    Flat f;
+    for (Index j = 0; j < ncols; ++j)
+        for (int k = 0; k < q; ++k) append_tensor(f, at(j, k), dims);
+    std::vector<double> vbuf;
+    tm_store_desc d{};
+    d.q = q;
+    d.ncols = ncols;
+    for (int g = 0; g < 3; ++g) d.dims[g] = dims[g];
+    d.ranks = f.ranks.data();
+    d.payload = f.payload.data();
+    if (v) {
+        vbuf.reserve(static_cast<std::size_t>(2 * v->size()));
+        for (Index i = 0; i < v->size(); ++i) {
+            vbuf.push_back(v->data()[i].real());
+            vbuf.push_back(v->data()[i].imag());
+        }
+        d.v = vbuf.data();
+        d.m2 = v->rows();
+    }
+    tm_store* h = nullptr;
+    check(tm_store_create(&d, device, dtype, &h));
+    return h;
+}
+
+// ---- identity cache ------------------------------------------------------
+using Key = std::tuple<const void*, const void*, Index, int, Index, Index, Index, int, int>;
+std::mutex g_mu;
+std::map<Key, std::shared_ptr<tm_store>> g_cache;
+int g_dtype = TM_C128;
+int g_device = -1;
+
+int current_device() {
+    if (g_device >= 0) return g_device;
+    if (const char* e = std::getenv("TUCKMAT_DEVICE")) return std::atoi(e);
+    return 0;
+}
+
+std::shared_ptr<tm_store> cached(const Key& key, const std::function<tm_store*()>& make) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) return it->second;
+    std::shared_ptr<tm_store> s(make(), [](tm_store* p) { tm_store_destroy(p); });
+    g_cache.emplace(key, s);
+    return s;
+}
+
+// ---- products through the C ABI -------------------------------------------
+// dtype-converting host call: MultiVector is complex128; a TM_C64 store takes
+// complex64 blocks.
+template <typename Call>
+MultiVector run(tm_store* s, int dtype, const MultiVector& in, Index outrows, Call call) {
+    const Index p = in.cols();
+    MultiVector out(outrows, p);
+    if (dtype == TM_C128) {
+        check(call(in.data(), std::max<Index>(in.rows(), 1), out.data(), std::max<Index>(outrows, 1)));
+        return out;
+    }
+    std::vector<std::complex<float>> a(static_cast<std::size_t>(in.size())), b(static_cast<std::size_t>(outrows * p));
+    for (Index i = 0; i < in.size(); ++i) a[static_cast<std::size_t>(i)] = std::complex<float>(in.data()[i]);
+    check(call(a.data(), std::max<Index>(in.rows(), 1), b.data(), std::max<Index>(outrows, 1)));
+    for (Index i = 0; i < outrows * p; ++i) out.data()[i] = Complex(b[static_cast<std::size_t>(i)]);
+    (void)s;
+    return out;
+}
+
+Index store_rows(tm_store* s) {
+    std::int32_t q = 0;
+    std::int64_t ncols = 0, dims[3] = {0, 0, 0};
+    check(tm_store_info(s, &q, &ncols, dims, nullptr, nullptr, nullptr));
+    return q * dims[0] * dims[1] * dims[2];
+}
+
+Index store_cols(tm_store* s) {
+    std::int64_t ncols = 0;
+    check(tm_store_info(s, nullptr, &ncols, nullptr, nullptr, nullptr, nullptr));
+    return ncols;
+}
+
+Index store_m2(tm_store* s) {
+    std::int64_t m2 = 0;
+    check(tm_store_info(s, nullptr, nullptr, nullptr, nullptr, &m2, nullptr));
+    return m2;
+}
+
+MultiVector fwd(tm_store* s, int dtype, const MultiVector& x, OpCounts* ops) {
+    std::int64_t o[2] = {0, 0};
+    MultiVector y = run(s, dtype, x, store_rows(s), [&](const void* in, Index ldi, void* out, Index ldo) {
+        return tm_forward(s, in, ldi, x.rows(), x.cols(), out, ldo, TM_HOST, nullptr, o);
+    });
+    if (ops) {
+        ops->decompress_madds += o[0];
+        ops->accumulate_madds += o[1];
+    }
+    return y;
+}
+
+MultiVector adj(tm_store* s, int dtype, const MultiVector& phi, OpCounts* ops) {
+    std::int64_t o[2] = {0, 0};
+    MultiVector z = run(s, dtype, phi, store_cols(s), [&](const void* in, Index ldi, void* out, Index ldo) {
+        return tm_adjoint(s, in, ldi, phi.rows(), phi.cols(), out, ldo, TM_HOST, nullptr, o);
+    });
+    if (ops) {
+        ops->decompress_madds += o[0];
+        ops->accumulate_madds += o[1];
+    }
+    return z;
+}
+
+MultiVector aca_fwd(tm_store* s, int dtype, const MultiVector& x) {
+    return run(s, dtype, x, store_rows(s), [&](const void* in, Index ldi, void* out, Index ldo) {
+        return tm_aca_forward(s, in, ldi, x.rows(), x.cols(), out, ldo, TM_HOST, nullptr);
+    });
+}
+
+MultiVector aca_adj(tm_store* s, int dtype, const MultiVector& phi) {
+    return run(s, dtype, phi, store_m2(s), [&](const void* in, Index ldi, void* out, Index ldo) {
+        return tm_aca_adjoint(s, in, ldi, phi.rows(), phi.cols(), out, ldo, TM_HOST, nullptr);
+    });
+}
+
+Key key_of(const CompressedCoupling& cc) {
+    return Key(&cc, cc.columns.data(), cc.m, cc.q, cc.grid_dims[0], cc.grid_dims[1], cc.grid_dims[2], g_dtype,
+               current_device());
+}
+
+Key key_of(const AcaFactors& f) {
+    return Key(&f, f.tucker_u.data(), f.rank(), f.q, f.grid_dims[0], f.grid_dims[1], f.grid_dims[2], g_dtype,
+               current_device());
+}
+
+std::shared_ptr<tm_store> store_of(const CompressedCoupling& cc) {
+    if (static_cast<Index>(cc.columns.size()) != cc.m) throw ContractViolation("CompressedCoupling: columns != m");
+    return cached(key_of(cc), [&] {
+        return make_store(
+            cc.q, cc.m, cc.grid_dims,
+            [&](Index j, int k) -> const TuckerTensor& {
+                return cc.columns[static_cast<std::size_t>(j)][static_cast<std::size_t>(k)];
+            },
+            nullptr, g_dtype, current_device());
+    });
+}
+
+std::shared_ptr<tm_store> store_of(const AcaFactors& f) {
+    return cached(key_of(f), [&] {
+        return make_store(
+            f.q, f.rank(), f.grid_dims,
+            [&](Index l, int k) -> const TuckerTensor& {
+                return f.tucker_u[static_cast<std::size_t>(k)][static_cast<std::size_t>(l)];
+            },
+            &f.v, g_dtype, current_device());
+    });
+}
+
+// Dense-U ACA products (aca_forward's `fac.dense_u * w` branch,
+// src/matvec.cpp:158,173): small host GEMMs, as in the reference.
+MultiVector host_gemm(const Matrix& a, bool conj_a, const MultiVector& b) {
+    const Index m = conj_a ? a.cols() : a.rows(), k = conj_a ? a.rows() : a.cols();
+    MultiVector c(m, b.cols());
+    for (Index j = 0; j < b.cols(); ++j)
+        for (Index i = 0; i < m; ++i) {
+            Complex s = 0;
+            for (Index l = 0; l < k; ++l) s += (conj_a ? std::conj(a(l, i)) : a(i, l)) * b(l, j);
+            c(i, j) = s;
+        }
+    return c;
+}
+
+}  // namespace
+
+// ---- reference API ----------------------------------------------------------
+MultiVector forward(const CompressedCoupling& cc, const MultiVector& x, int, OpCounts* ops) {
+    if (x.rows() != cc.m)
+        throw ContractViolation("forward: x has " + std::to_string(x.rows()) + " rows, expected m = " +
+                                std::to_string(cc.m));
+    auto s = store_of(cc);
+    return fwd(s.get(), g_dtype, x, ops);
+}
+
+MultiVector adjoint(const CompressedCoupling& cc, const MultiVector& phi, int, OpCounts* ops) {
+    if (phi.rows() != cc.rows())
+        throw ContractViolation("adjoint: phi has " + std::to_string(phi.rows()) + " rows, expected q*n_v = " +
+                                std::to_string(cc.rows()));
+    auto s = store_of(cc);
+    return adj(s.get(), g_dtype, phi, ops);
+}
+
+MultiVector stacked_forward(const TuckerColumns& z, const MultiVector& x, int, OpCounts* ops) {
+    if (x.rows() != z.ncols)
+        throw ContractViolation("stacked_forward: x has " + std::to_string(x.rows()) + " rows, expected " +
+                                std::to_string(z.ncols));
+    b200::DeviceStore s(z, g_dtype, current_device());
+    return fwd(s.handle(), g_dtype, x, ops);
+}
+
+MultiVector stacked_adjoint(const TuckerColumns& z, const MultiVector& x, int, OpCounts* ops) {
+    if (x.rows() != z.rows())
+        throw ContractViolation("stacked_adjoint: x has " + std::to_string(x.rows()) + " rows, expected " +
+                                std::to_string(z.rows()));
+    b200::DeviceStore s(z, g_dtype, current_device());
+    return adj(s.handle(), g_dtype, x, ops);
+}
+
+MultiVector aca_forward(const AcaFactors& fac, const MultiVector& x, int) {
+    if (x.rows() != fac.cols())
+        throw ContractViolation("aca_forward: x has " + std::to_string(x.rows()) + " rows, expected " +
+                                std::to_string(fac.cols()));
+    if (!fac.compressed()) return host_gemm(fac.dense_u, false, host_gemm(fac.v, true, x));
+    auto s = store_of(fac);
+    return aca_fwd(s.get(), g_dtype, x);
+}
+
+MultiVector aca_adjoint(const AcaFactors& fac, const MultiVector& phi, int) {
+    if (phi.rows() != fac.rows())
+        throw ContractViolation("aca_adjoint: phi has " + std::to_string(phi.rows()) + " rows, expected " +
+                                std::to_string(fac.rows()));
+    if (!fac.compressed()) return host_gemm(fac.v, false, host_gemm(fac.dense_u, true, phi));
+    auto s = store_of(fac);
+    return aca_adj(s.get(), g_dtype, phi);
+}
+
+// ---- io ------------------------------------------------------------------
+namespace {
+
+std::vector<std::vector<TuckerTensor>> unpack(const tmb_io::Parsed& p, bool aca) {
+    const Dims3 dims{p.dims[0], p.dims[1], p.dims[2]};
+    std::vector<std::vector<TuckerTensor>> out;
+    if (aca)
+        out.assign(p.q, std::vector<TuckerTensor>(p.m));
+    else
+        out.assign(p.m, std::vector<TuckerTensor>(p.q));
+    std::size_t off = 0;
+    const Complex* src = reinterpret_cast<const Complex*>(p.payload.data());
+    for (std::uint32_t j = 0; j < p.m; ++j)
+        for (std::uint32_t k = 0; k < p.q; ++k) {
+            TuckerTensor& tt = aca ? out[k][j] : out[j][k];
+            const std::int32_t* r = &p.ranks[3 * (std::size_t(j) * p.q + k)];
+            tt.dims = dims;
+            tt.core = Tensor3(r[0], r[1], r[2]);
+            for (Index i = 0; i < tt.core.size(); ++i) tt.core[i] = src[off++];
+            for (int g = 0; g < 3; ++g) {
+                tt.factors[g] = Matrix(dims[g], r[g]);
+                for (Index i = 0; i < tt.factors[g].size(); ++i) tt.factors[g].data()[i] = src[off++];
+            }
+        }
+    return out;
+}
+
+template <typename F>
+auto parse_or_throw(F&& f) -> decltype(f()) {
+    try {
+        return f();
+    } catch (const tmb_io::ParseFail& e) {
+        throw ParseError(e.what(), e.offset);
+    }
+}
+
+}  // namespace
+
+CompressedCoupling load_ctc1(const std::string& path) {
+    return parse_or_throw([&] {
+        const tmb_io::Parsed p = tmb_io::parse(path, false);
+        CompressedCoupling cc;
+        cc.grid_dims = {p.dims[0], p.dims[1], p.dims[2]};
+        cc.q = int(p.q);
+        cc.m = p.m;
+        cc.kernel_op = static_cast<KernelOp>(p.op);
+        cc.k0 = p.k0;
+        cc.eps = p.eps;
+        cc.columns = unpack(p, false);
+        return cc;
+    });
+}
+
+Cta1File load_cta1(const std::string& path) {
+    return parse_or_throw([&] {
+        const tmb_io::Parsed p = tmb_io::parse(path, true);
+        Cta1File f;
+        f.k0 = p.k0;
+        f.kernel_op = static_cast<KernelOp>(p.op);
+        AcaFactors& fac = f.factors;
+        fac.grid_dims = {p.dims[0], p.dims[1], p.dims[2]};
+        fac.q = int(p.q);
+        fac.eps = p.eps;
+        fac.tucker_u = unpack(p, true);
+        fac.v = Matrix(Index(p.m2), Index(p.m));
+        const Complex* v = reinterpret_cast<const Complex*>(p.v.data());
+        for (Index i = 0; i < fac.v.size(); ++i) fac.v.data()[i] = v[i];
+        return f;
+    });
+}
+
+// ---- B200 extensions ----------------------------------------------------
+namespace b200 {
+
+void set_default_dtype(int dtype) {
+    if (dtype != TM_C64 && dtype != TM_C128) throw ContractViolation("dtype must be TM_C64 or TM_C128");
+    g_dtype = dtype;
+}
+int default_dtype() { return g_dtype; }
+void set_device(int device) { g_device = device; }
+void clear_cache() {
+    std::lock_guard<std::mutex> lock(g_mu);
+    g_cache.clear();
+}
+
+DeviceStore::DeviceStore(const CompressedCoupling& cc, int dtype, int device) : dtype_(dtype) {
+    h_ = make_store(
+        cc.q, cc.m, cc.grid_dims,
+        [&](Index j, int k) -> const TuckerTensor& {
+            return cc.columns[static_cast<std::size_t>(j)][static_cast<std::size_t>(k)];
+        },
+        nullptr, dtype, device);
+}
+
+DeviceStore::DeviceStore(const AcaFactors& f, int dtype, int device) : dtype_(dtype) {
+    h_ = make_store(
+        f.q, f.rank(), f.grid_dims,
+        [&](Index l, int k) -> const TuckerTensor& {
+            return f.tucker_u[static_cast<std::size_t>(k)][static_cast<std::size_t>(l)];
+        },
+        &f.v, dtype, device);
+}
+
+DeviceStore::DeviceStore(const TuckerColumns& z, int dtype, int device) : dtype_(dtype) {
+    h_ = make_store(z.q, z.ncols, z.grid_dims, z.tensor, nullptr, dtype, device);
+}
+
+DeviceStore::~DeviceStore() {
+    if (h_) tm_store_destroy(h_);
+}
+
+MultiVector forward(const DeviceStore& s, const MultiVector& x, OpCounts* ops) {
+    return fwd(s.handle(), s.dtype(), x, ops);
+}
+MultiVector adjoint(const DeviceStore& s, const MultiVector& phi, OpCounts* ops) {
+    return adj(s.handle(), s.dtype(), phi, ops);
+}
+MultiVector aca_forward(const DeviceStore& s, const MultiVector& x) { return aca_fwd(s.handle(), s.dtype(), x); }
+MultiVector aca_adjoint(const DeviceStore& s, const MultiVector& phi) { return aca_adj(s.handle(), s.dtype(), phi); }
+
+}  // namespace b200
+}  // namespace tuckmat

@@ -1,0 +1,30 @@
+// Host-side CTC1 / CTA1 parser shared by the C ABI loaders and the C++
+// drop-in (reference byte layout: src/io.cpp:121-194, 198-279).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace tmb_io {
+
+struct ParseFail : std::runtime_error {
+    std::uint64_t offset;
+    ParseFail(const std::string& m, std::uint64_t off) : std::runtime_error(m), offset(off) {}
+};
+
+struct Parsed {
+    std::uint32_t q = 0, m = 0, dims[3] = {0, 0, 0};
+    double k0 = 0, eps = 0;
+    std::uint8_t op = 0;
+    std::vector<std::int32_t> ranks;  // [col][comp][mode]
+    std::vector<double> payload;      // CTC1 tensor payloads, complex128 pairs
+    std::vector<double> v;            // CTA1 only: V, m2 x r_c column-major
+    std::uint64_t m2 = 0;
+};
+
+// aca = false: "CTC1"; aca = true: "CTA1".  Throws ParseFail.
+Parsed parse(const std::string& path, bool aca);
+
+}  // namespace tmb_io

@@ -1,0 +1,214 @@
+"""GPU parity of the CUDA path against the CPU oracle (reference restatement).
+
+Tolerances (north_star): relative Frobenius error <= 1e-12 for complex128
+stores, <= 1e-5 for complex64 stores; the oracle always computes in complex128
+on the same (rounded) factors and inputs.  The reference's own matvec tests
+(proj/tests/test_matvec.cpp) are restated here against the GPU operator.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel
+from helpers import cn01, ragged_store
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c128": 1e-12, "c64": 1e-5}
+
+
+def _loop_scene(O, n, seg, d, h=0.05):
+    g = O.make_centered_grid((0, 0, 0), h, (n, n, n) if np.isscalar(n) else n)
+    return O.make_loop_scene(0.5, (0, d, 0), seg, g, 0, O.wavenumber_from_mhz(298.06), 3)
+
+
+def _pair(O, P, cc, dtype):
+    ref = cc.rounded_c64() if dtype == "c64" else cc
+    return O.OracleStore(ref), P.DeviceStore.from_compressed(cc, dtype), ref
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("p", [1, 3, 8])
+def test_forward_adjoint_physics_scene(oracle, product, dtype, p):
+    O, P = oracle, product
+    cc = O.compress_matrix(_loop_scene(O, 8, 10, 0.8), 1e-6)
+    os_, ds, _ = _pair(O, P, cc, dtype)
+    x = cn01(cc.m, p, 31)
+    phi = cn01(cc.rows, p, 77)
+    if dtype == "c64":
+        x = x.astype(np.complex64).astype(np.complex128)
+        phi = phi.astype(np.complex64).astype(np.complex128)
+    assert rel(ds.forward(x), os_.forward(x)) <= TOL[dtype]
+    assert rel(ds.adjoint(phi), os_.adjoint(phi)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("dims,q,m,rmin,rmax", [
+    ((7, 5, 9), 3, 13, 1, 5),          # ragged, tiny, non-multiples of every tile
+    ((24, 24, 24), 3, 40, 6, 11),      # config-1 shape
+    ((33, 17, 130), 2, 9, 2, 12),      # n3 > 128 (two i3 tiles), odd n1/n2
+    ((64, 64, 64), 12, 6, 4, 8),       # config-5 shape (q = 12)
+    ((1, 1, 1), 3, 4, 1, 1),           # single voxel
+    ((12, 40, 3), 1, 17, 1, 20),       # tall ranks clipped to the grid, q = 1
+])
+def test_ragged_stores(oracle, product, dtype, dims, q, m, rmin, rmax):
+    O, P = oracle, product
+    cc = ragged_store(dims, q, m, rmin, rmax, seed=sum(dims) + m)
+    os_, ds, _ = _pair(O, P, cc, dtype)
+    for p in (1, 2):
+        x = cn01(m, p, 5 + p)
+        phi = cn01(cc.rows, p, 9 + p)
+        if dtype == "c64":
+            x = x.astype(np.complex64).astype(np.complex128)
+            phi = phi.astype(np.complex64).astype(np.complex128)
+        assert rel(ds.forward(x), os_.forward(x)) <= TOL[dtype]
+        assert rel(ds.adjoint(phi), os_.adjoint(phi)) <= TOL[dtype]
+
+
+def test_basis_vector_extracts_column(oracle, product):
+    """forward(e_j) == decompressed column j (test_matvec.cpp:38-48)."""
+    O, P = oracle, product
+    cc = O.compress_matrix(_loop_scene(O, 6, 8, 0.8), 1e-6)
+    os_ = O.OracleStore(cc)
+    ds = P.DeviceStore.from_compressed(cc, "c128")
+    for j in range(cc.m):
+        e = np.zeros((cc.m, 1), complex)
+        e[j] = 1.0
+        assert rel(ds.forward(e)[:, 0], os_.column(j)) <= 1e-14
+
+
+def test_zero_block_is_exactly_zero(oracle, product):
+    """test_matvec.cpp:60-66."""
+    O, P = oracle, product
+    cc = O.compress_matrix(_loop_scene(O, 5, 6, 0.9), 1e-6)
+    for dtype in ("c128", "c64"):
+        ds = P.DeviceStore.from_compressed(cc, dtype)
+        y = ds.forward(np.zeros((cc.m, 3), complex))
+        assert y.shape == (cc.rows, 3)
+        assert np.count_nonzero(y) == 0
+        z = ds.adjoint(np.zeros((cc.rows, 2), complex))
+        assert np.count_nonzero(z) == 0
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_adjoint_identity(oracle, product, dtype):
+    """<F x, phi> = <x, F^H phi> (test_matvec.cpp:68-75); 1e-12 at c128."""
+    O, P = oracle, product
+    cc = O.compress_matrix(_loop_scene(O, 6, 9, 0.8), 1e-6)
+    ds = P.DeviceStore.from_compressed(cc, dtype)
+    x = O.random_multivector(cc.m, 4, 7)
+    phi = O.random_multivector(cc.rows, 4, 8)
+    lhs = np.trace(ds.forward(x).conj().T @ phi)
+    rhs = np.trace(x.conj().T @ ds.adjoint(phi))
+    assert abs(lhs - rhs) <= (1e-12 if dtype == "c128" else 1e-5) * abs(lhs)
+
+
+def test_dense_oracle_and_squared_norm(oracle, product):
+    """Forward/adjoint vs the dense matrix within 5 eps (test_matvec.cpp:50-58,77-98)."""
+    O, P = oracle, product
+    eps = 1e-6
+    sc = _loop_scene(O, 8, 10, 0.8)
+    cc = O.compress_matrix(sc, eps)
+    ds = P.DeviceStore.from_compressed(cc, "c128")
+    x = O.random_multivector(cc.m, 8, 31)
+    assert rel(ds.forward(x), O.dense_forward(sc, x)) <= 5 * eps
+    phi = O.random_multivector(cc.rows, 8, 77)
+    assert rel(ds.adjoint(phi), O.dense_adjoint(sc, phi)) <= 5 * eps
+    cc8 = O.compress_matrix(_loop_scene(O, 6, 8, 0.8), 1e-8)
+    ds8 = P.DeviceStore.from_compressed(cc8, "c128")
+    col = O.OracleStore(cc8).column(3)
+    y = ds8.adjoint(col.reshape(-1, 1))
+    sq = float(np.vdot(col, col).real)
+    assert abs(y[3, 0] - sq) <= 1e-12 * sq
+
+
+def test_linearity(oracle, product):
+    """test_matvec.cpp:117-132."""
+    O, P = oracle, product
+    cc = O.compress_matrix(_loop_scene(O, 6, 7, 0.9), 1e-8)
+    ds = P.DeviceStore.from_compressed(cc, "c128")
+    x1 = O.random_multivector(cc.m, 2, 1)
+    x2 = O.random_multivector(cc.m, 2, 2)
+    a, b = 0.7 - 0.3j, -1.1 + 0.2j
+    lhs = ds.forward(a * x1 + b * x2)
+    rhs = a * ds.forward(x1) + b * ds.forward(x2)
+    assert rel(lhs, rhs) <= 1e-12
+
+
+def test_shape_errors(oracle, product):
+    """ContractViolation on row-count mismatch (test_matvec.cpp:134-140)."""
+    O, P = oracle, product
+    cc = O.compress_matrix(_loop_scene(O, 4, 5, 0.9), 1e-6)
+    ds = P.DeviceStore.from_compressed(cc, "c128")
+    with pytest.raises(P.ContractViolation, match="forward: x has 6 rows, expected m = 5"):
+        ds.forward(np.zeros((cc.m + 1, 1), complex))
+    with pytest.raises(P.ContractViolation, match="adjoint: phi has"):
+        ds.adjoint(np.zeros((cc.rows - 1, 1), complex))
+
+
+def test_determinism(oracle, product):
+    """Fixed column-to-CTA assignment and ordered reductions: bitwise repeatable."""
+    O, P = oracle, product
+    cc = ragged_store((24, 20, 40), 3, 30, 3, 9, seed=3)
+    ds = P.DeviceStore.from_compressed(cc, "c64")
+    x = cn01(cc.m, 2, 1)
+    phi = cn01(cc.rows, 2, 2)
+    y1, y2 = ds.forward(x), ds.forward(x)
+    z1, z2 = ds.adjoint(phi), ds.adjoint(phi)
+    assert np.array_equal(y1, y2) and np.array_equal(z1, z2)
+
+
+def test_opcounts(oracle, product):
+    """Exact OpCounts formula (test_matvec.cpp:170-220)."""
+    O, P = oracle, product
+    n = 26
+    cc = O.synthetic_compression(n, 4, 2, 9)
+    ds = P.DeviceStore.from_compressed(cc, "c128")
+    ops = P.OpCounts()
+    ds.forward(O.random_multivector(cc.m, 2, 3), ops)
+    assert ops.decompress_madds == 4 * 3 * (n * 8 + n * n * 4 + n * n * n * 2)
+    assert ops.accumulate_madds == 4 * 3 * n * n * n * 2
+    assert ds.opcounts(2) == O.OracleStore(cc).opcounts(2)
+    ds.forward(O.random_multivector(cc.m, 2, 3), ops)   # counts accumulate (+=)
+    assert ops.decompress_madds == 2 * 4 * 3 * (n * 8 + n * n * 4 + n * n * n * 2)
+
+
+def test_device_tensors_match_host(oracle, product):
+    """TM_DEVICE path (torch CUDA tensors on the current stream) == TM_HOST path."""
+    import torch
+    O, P = oracle, product
+    cc = ragged_store((16, 12, 20), 3, 11, 2, 6, seed=11)
+    ds = P.DeviceStore.from_compressed(cc, "c64")
+    x = cn01(cc.m, 3, 4).astype(np.complex64)
+    phi = cn01(cc.rows, 3, 5).astype(np.complex64)
+    yh = ds.forward(x)
+    zh = ds.adjoint(phi)
+    xd = torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t()
+    pd = torch.from_numpy(np.ascontiguousarray(phi.T)).cuda().t()
+    yd = ds.forward(xd)
+    zd = ds.adjoint(pd)
+    torch.cuda.synchronize()
+    assert np.array_equal(yd.cpu().numpy(), yh)
+    assert np.array_equal(zd.cpu().numpy(), zh)
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_aca_products(oracle, product, dtype):
+    """aca_forward / aca_adjoint vs the oracle on a Tucker-ACA store (matvec.cpp:150-175)."""
+    O, P = oracle, product
+    g = O.make_centered_grid((0, 0, 0), 0.04, (8, 8, 8))
+    sc = O.make_loop_scene(0.5, (0, 0.9, 0), 12, g, 0, O.wavenumber_from_mhz(123.0), 3)
+    row, col, m1, m2 = O.coupling_oracle(sc)
+    fac = O.tucker_aca(row, col, m1, m2, sc.dims, 3, 1e-4)
+    assert fac.rank >= 2
+    ref = fac.rounded_c64() if dtype == "c64" else fac
+    ds = P.DeviceStore.from_compressed(fac, dtype)
+    x = cn01(m2, 4, 17)
+    phi = cn01(m1, 4, 18)
+    if dtype == "c64":
+        x = x.astype(np.complex64).astype(np.complex128)
+        phi = phi.astype(np.complex64).astype(np.complex128)
+    assert rel(ds.aca_forward(x), O.aca_forward(ref, x)) <= TOL[dtype]
+    assert rel(ds.aca_adjoint(phi), O.aca_adjoint(ref, phi)) <= TOL[dtype]
+    # and the operator stays within a decade of the ACA tolerance (test_aca.cpp:134-139)
+    z = O.assemble_full(sc)
+    assert rel(ds.aca_forward(x), z @ x) <= 10 * 1e-4
