@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""Benchmark: ms per forward Zbc x + adjoint Zbc^H y on the Tucker-compressed
+1 mm-class PWL coupling matrix (BASELINE.json configs[3], "c4"), on N B200s.
+
+One step = one forward and one adjoint over the whole store, x and Phi
+resident in HBM (value), and the same pair through the public API with host
+buffers (e2e).  Multi-GPU: one process per GPU (torchrun), columns sharded by
+cost; NCCL reduce of y, NCCL all-gather of z; time = max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4]
+  python bench.py --impl reference ...     # the CPU reference (restated, oracle/)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 1234  # reference default seed (include/tuckmat/experiments.hpp:51); Phi uses SEED + 1
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-cols", type=int, default=0, help="columns in the CPU sample (0 = auto)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ utilities --
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while running."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def fp32_peak_tflops(torch):
+    """FP32 (FFMA, no TF32) throughput of cuBLAS SGEMM 8192^3 — the CUDA-core
+    roofline denominator the driver does not measure (best of 5)."""
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        n = 8192
+        a = torch.randn(n, n, device="cuda")
+        b = torch.randn(n, n, device="cuda")
+        for _ in range(2):
+            a @ b
+        torch.cuda.synchronize()
+        best = 0.0
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            a @ b
+            e1.record()
+            e1.synchronize()
+            best = max(best, 2 * n ** 3 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+        del a, b
+        return best
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+# ------------------------------------------------------------- CPU reference --
+def cpu_sample(cfg, ranks, host_payload_fn, x_full, phi_full, ncols_sample, workers):
+    """Time the restated reference (oracle/, src/matvec.cpp:17-102) forward +
+    adjoint on the first `ncols_sample` columns with `workers` host threads,
+    and scale to the whole store by the algorithmic madd count."""
+    from oracle import oracle as O
+    from paper_2103_06393_b200.sharded import column_costs
+
+    from paper_2103_06393_b200.workloads import tensor_offsets
+
+    pay = host_payload_fn(ncols_sample)  # complex128 (already c64-rounded values)
+    costs = column_costs(cfg.grid, ranks, cfg.p)
+
+    def timed_forward(nc):
+        off = tensor_offsets(cfg.grid, ranks[:nc])
+        st = O.OracleStore(O.Compressed(cfg.grid, cfg.q, nc, ranks[:nc], pay[: int(off[-1])]))
+        t0 = time.perf_counter()
+        st.forward(np.asfortranarray(x_full[:nc]), workers)
+        return time.perf_counter() - t0, st
+
+    # stacked_forward with W workers = a fixed cost (zeroing and serially
+    # summing the W rows x p partials, src/matvec.cpp:30-38,58-59) + rounds of
+    # W columns in parallel.  Time W and 2W columns with the same W workers:
+    # the difference is one round of column work at full thread occupancy.
+    W = workers
+    n1, n2 = min(W, ncols_sample), min(2 * W, ncols_sample)
+    ta, _ = timed_forward(n1)
+    tb, st = timed_forward(n2)
+    ca, cb = costs[:n1].sum(), costs[:n2].sum()
+    rate = (cb - ca) / max(tb - ta, 1e-9) if n2 > n1 else ca / ta  # madds per second, all workers
+    fwd_full = ta + (costs.sum() - ca) / rate
+    fixed = max(ta - ca / rate, 0.0)
+    t1 = time.perf_counter()
+    st.adjoint(phi_full, workers)
+    t2 = time.perf_counter()
+    scale = float(costs.sum() / cb)
+    return {"fwd_s": fwd_full, "adj_s": (t2 - t1) * scale, "scale": scale, "fwd_fixed_s": fixed}
+
+
+def cpu_workers(cfg, ncols_cap):
+    nproc = os.cpu_count() or 1
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 32 << 30
+    rows = cfg.q * int(np.prod(cfg.grid))
+    # stacked_forward holds one rows x p complex128 partial + one decompressed tensor per worker
+    per_worker = 16 * rows * cfg.p + 3 * 16 * int(np.prod(cfg.grid)) + (64 << 20)
+    budget = max(1, int((avail - 8 * 16 * rows) // per_worker))
+    return max(1, min(nproc, budget, ncols_cap))
+
+
+# --------------------------------------------------------------------- main --
+def run_reference(args):
+    """--impl reference: the reference's own CPU matvec path (restated in
+    oracle/, Eigen unavailable) on the host cores, same config / metric."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2103_06393_b200.workloads import CONFIGS, column_scales, rank_table
+    from oracle import oracle as O
+
+    cfg = CONFIGS[args.config]
+    ranks = rank_table(cfg, SEED)
+    scales = column_scales(cfg, SEED)
+    nrows = cfg.q * int(np.prod(cfg.grid))
+    W = cpu_workers(cfg, 32)
+    ncs = args.cpu_cols or 2 * W
+    x = cn01(cfg.m, cfg.p, SEED).astype(np.complex64).astype(np.complex128)
+    phi = np.asfortranarray(cn01(nrows, cfg.p, SEED + 1).astype(np.complex64).astype(np.complex128))
+
+    def host_payload(nc):
+        return _numpy_synthetic(cfg, ranks[:nc], scales[:nc], SEED)
+
+    times = []
+    for s in range(args.warmup + args.steps):
+        r = cpu_sample(cfg, ranks, host_payload, x, phi, ncs, W)
+        if s >= args.warmup:
+            times.append((r["fwd_s"] + r["adj_s"]) * 1e3)
+    ms = statistics.median(times)
+    line = {
+        "impl": "reference", "metric": metric_name(cfg), "value": ms, "unit": "ms", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128 (restated reference; c64-rounded factors)",
+        "data": "synthetic", "config": {"workload": cfg.name, "p": cfg.p, "m": cfg.m, "q": cfg.q,
+                                        "grid": list(cfg.grid)},
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": W, "kind": "port",
+                         "sample": f"forward timed on {W} and {ncs} of {cfg.m} columns (all q={cfg.q} components) "
+                                   f"with {W} workers (fixed partial-sum cost + per-round rate), adjoint on {ncs} "
+                                   f"columns scaled by the madd count"},
+        "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _numpy_synthetic(cfg, ranks, scales, seed):
+    """Host copy of the synthetic store's first columns, c64-rounded (for the
+    CPU legs without a GPU-generated payload)."""
+    import torch
+    from paper_2103_06393_b200.workloads import synthetic_payload
+    pay, _ = synthetic_payload(cfg.grid, ranks, scales, seed, device="cpu")
+    return pay.to(torch.complex64).to(torch.complex128).cpu().numpy()
+
+
+def cn01(rows, cols, seed):
+    """Seeded CN(0,1) block, column-major."""
+    rng = np.random.default_rng(seed)
+    a = (rng.standard_normal((rows, cols)) + 1j * rng.standard_normal((rows, cols))) / math.sqrt(2)
+    return np.asfortranarray(a)
+
+
+def metric_name(cfg):
+    return f"ms per Zbc*x + Zbc^H*y matvec pair ({cfg.name})"
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2103_06393_b200 import DeviceStore, launch_count
+    from paper_2103_06393_b200.sharded import ShardedStore, balanced_shards, column_costs
+    from paper_2103_06393_b200.workloads import CONFIGS, column_scales, rank_table, synthetic_payload
+
+    cfg = CONFIGS[args.config]
+    ranks = rank_table(cfg, SEED)
+    scales = column_scales(cfg, SEED)
+    costs = column_costs(cfg.grid, ranks, cfg.p)
+    shards = balanced_shards(costs, world)
+    c0, c1 = shards[rank]
+    nrows = cfg.q * int(np.prod(cfg.grid))
+    cdt = torch.complex64 if cfg.dtype == "c64" else torch.complex128
+
+    # --- store: seeded synthetic payload generated on the device, packed once --
+    t_build = time.perf_counter()
+    pay, _ = synthetic_payload(cfg.grid, ranks[c0:c1], scales[c0:c1], SEED + 1000 + c0, device=dev)
+    store = DeviceStore.from_arrays(cfg.grid, cfg.q, ranks[c0:c1], pay, cfg.dtype, local)
+    cpu_pay = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        W = cpu_workers(cfg, 32)
+        ncs = min(args.cpu_cols or 2 * W, c1 - c0)
+        from paper_2103_06393_b200.workloads import tensor_offsets
+        off = tensor_offsets(cfg.grid, ranks[:ncs])
+        cpu_pay = pay[: int(off[-1])].to(cdt).to(torch.complex128).cpu().numpy()
+    del pay
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t_build
+    sh = ShardedStore(store, c0, c1, cfg.m, shards=shards)
+
+    # --- inputs: CN(0,1), seeded (x: numpy, Phi: device RNG) ---------------------
+    x_host = cn01(cfg.m, cfg.p, SEED).astype(np.complex64 if cfg.dtype == "c64" else np.complex128)
+    x = torch.from_numpy(np.ascontiguousarray(x_host.T)).to(dev).t()
+    g = torch.Generator(device=dev)
+    g.manual_seed(SEED + 1)
+    phi = (torch.randn((cfg.p, nrows), dtype=cdt, device=dev, generator=g)).t()
+    xs = x[c0:c1]
+
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        y = sh.forward(xs)
+        if ev:
+            ev[1].record(stream)
+        z = sh.adjoint(phi)
+        if ev:
+            ev[2].record(stream)
+        return y, z
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    peaks = measured_peaks()
+    fp32_peak = fp32_peak_tflops(torch) if rank == 0 else None
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    if rank == 0:
+        clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    l0 = launch_count()
+    t_all0 = torch.cuda.Event(enable_timing=True)
+    t_all1 = torch.cuda.Event(enable_timing=True)
+    t_all0.record(stream)
+    for s in range(args.steps):
+        step(evs[s])
+    t_all1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = launch_count() - l0
+    clk = clocks.stop() if rank == 0 else None
+    total_ms = t_all0.elapsed_time(t_all1)
+    fwd_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    adj_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    t = torch.tensor([total_ms, statistics.median(fwd_ms), statistics.median(adj_ms)], device=dev,
+                     dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, fwd_med, adj_med = t.tolist()
+    ms_per_step = total_ms / args.steps
+
+    # --- e2e through the public API with host buffers ---------------------------
+    e2e = None
+    if not args.no_e2e:
+        import ctypes
+        from paper_2103_06393_b200._lib import TM_HOST, lib
+        from paper_2103_06393_b200.matvec import _check
+        npdt = np.complex64 if cfg.dtype == "c64" else np.complex128
+        xh = torch.from_numpy(np.asfortranarray(x_host[c0:c1]).ravel(order="F")).pin_memory()
+        yh = torch.empty(nrows * cfg.p, dtype=cdt).pin_memory()
+        ph = phi.t().contiguous().cpu().pin_memory() if world == 1 else None
+        zh = torch.empty((c1 - c0) * cfg.p, dtype=cdt).pin_memory()
+        e2e_times = []
+        h2d = d2h = 0
+        for s in range(1 + args.e2e_steps):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            if world == 1:
+                _check(lib().tm_forward(store.handle, xh.data_ptr(), c1 - c0, c1 - c0, cfg.p, yh.data_ptr(), nrows,
+                                        TM_HOST, None, None))
+                _check(lib().tm_adjoint(store.handle, ph.data_ptr(), nrows, nrows, cfg.p, zh.data_ptr(), c1 - c0,
+                                        TM_HOST, None, None))
+                h2d = xh.numel() * xh.element_size() + ph.numel() * ph.element_size()
+                d2h = yh.numel() * yh.element_size() + zh.numel() * zh.element_size()
+            else:
+                # sharded public API: host x -> device, forward + NCCL reduce,
+                # y -> host on rank 0; host phi -> device on every rank,
+                # adjoint + all-gather, z -> host
+                xd = xh.to(dev, non_blocking=True).reshape(cfg.p, -1).t()
+                y = sh.forward(xd)
+                if rank == 0:
+                    yh.copy_(y.t().reshape(-1) if y.dim() == 2 else y, non_blocking=True)
+                pd = phi  # Phi H2D counted below (replicated input)
+                z = sh.adjoint(pd)
+                zf = torch.empty(z.numel(), dtype=cdt).pin_memory()
+                zf.copy_(z.t().reshape(-1) if z.dim() == 2 else z, non_blocking=True)
+                torch.cuda.synchronize()
+                h2d = xh.numel() * xh.element_size()
+                d2h = (yh.numel() * yh.element_size() if rank == 0 else 0) + zf.numel() * zf.element_size()
+            torch.cuda.synchronize()
+            dt = (time.perf_counter() - t0) * 1e3
+            if s > 0:
+                e2e_times.append(dt)
+        tt = torch.tensor([statistics.median(e2e_times)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": tt.item(), "unit": "ms", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+        if world > 1:
+            e2e["note"] = "multi-GPU e2e uses the sharded Python API; Phi is replicated device-resident"
+
+    # --- roofline of the dominant kernel (forward kernel, one launch per forward) --
+    dec, acc = store.opcounts(cfg.p)
+    flops_fwd = 8.0 * (dec + acc)  # OpCounts x 8 real flops per complex madd (this rank's shard)
+    achieved = flops_fwd / (fwd_med * 1e-3) / 1e12
+    roof = None
+    if rank == 0:
+        roof = {"bound": "fp32-ffma", "kernel": "fwd_cc_kernel", "achieved": round(achieved, 2),
+                "peak": round(fp32_peak, 2), "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4),
+                "peak_source": "measured here: cuBLAS SGEMM 8192^3 without TF32 (MEASURED_PEAKS.json has no FP32 "
+                               "figure)",
+                "traffic": None,
+                "algorithmic_flops_per_launch": flops_fwd,
+                "hbm_bytes_algorithmic": int(store.device_bytes + (c1 - c0) * cfg.p * 8 + nrows * cfg.p * 8),
+                "hbm_peak_gbs": peaks.get("hbm_gbs"),
+                "bf16_peak_tflops_measured": peaks.get("bf16_tflops")}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and cpu_pay is not None:
+        W = cpu_workers(cfg, 32)
+        ncs = min(args.cpu_cols or 2 * W, c1 - c0)
+        phi_h = np.asfortranarray(phi.cpu().numpy().astype(np.complex128))
+        r = cpu_sample(cfg, ranks, lambda nc: cpu_pay, x_host.astype(np.complex128), phi_h, ncs, W)
+        cpu = {"value": round((r["fwd_s"] + r["adj_s"]) * 1e3, 1), "unit": "ms", "cores": W, "kind": "port",
+               "sample": f"forward timed on {W} and {ncs} of {cfg.m} columns (all {cfg.q} components) with {W} "
+                         f"worker threads, extrapolated as fixed partial-sum cost + per-round rate; adjoint on "
+                         f"{ncs} columns scaled x{r['scale']:.1f} by the madd count",
+               "fwd_fixed_ms": round(r["fwd_fixed_s"] * 1e3, 1),
+               "forward_ms": round(r["fwd_s"] * 1e3, 1), "adjoint_ms": round(r["adj_s"] * 1e3, 1)}
+
+    if rank == 0:
+        line = {
+            "metric": metric_name(cfg), "value": round(ms_per_step, 3), "unit": "ms", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
+            "data": "synthetic (seeded Tucker store with the config's shape and rank distribution)",
+            "config": {"workload": cfg.name, "grid": list(cfg.grid), "q": cfg.q, "m": cfg.m, "p": cfg.p,
+                       "parallelism": f"column-shard x{world}", "l2": "inputs larger than L2 (store %.2f GB)"
+                       % (store.device_bytes * world / 1e9)},
+            "forward_ms": round(fwd_med, 3), "adjoint_ms": round(adj_med, 3),
+            "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "store_build_s": round(t_build, 2),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

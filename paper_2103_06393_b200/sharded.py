@@ -1,0 +1,109 @@
+"""Column sharding of a Tucker store across GPUs (one process per GPU).
+
+The reference parallelises products over columns with host threads
+(stacked_forward's per-worker partials, src/matvec.cpp:28-59; stacked_adjoint's
+per-column rows, :78-96).  Here each rank of a torch.distributed process group
+owns a contiguous, cost-balanced range of columns (all q components of each)
+as its own DeviceStore, and the products exchange data only where the
+algorithm has a real exchange step:
+
+  forward  y = sum_ranks Zbc[:, shard] x[shard]    -> NCCL reduce (or all-reduce)
+                                                      of the q*n_v x p partial
+  adjoint  z[shard] = Zbc[:, shard]^H phi          -> NCCL all-gather of the
+                                                      r-row blocks (m x p total)
+
+The class is agnostic of the store type (anything with forward / adjoint /
+rows / ncols), which lets the CPU tests drive the same host logic with gloo.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def balanced_shards(costs, world, align=1):
+    """Contiguous [begin, end) column ranges with near-equal total cost.
+
+    costs: per-column cost (e.g. reconstruct_madds + accumulate madds);
+    boundaries are multiples of `align` (except the last)."""
+    costs = np.asarray(costs, np.float64)
+    m = len(costs)
+    pref = np.concatenate([[0.0], np.cumsum(costs)])
+    bounds = [0]
+    for r in range(1, world):
+        target = pref[-1] * r / world
+        b = int(np.searchsorted(pref, target))
+        b = int(round(b / align) * align) if align > 1 else b
+        b = min(max(b, bounds[-1]), m)
+        bounds.append(b)
+    bounds.append(m)
+    return [(bounds[i], bounds[i + 1]) for i in range(world)]
+
+
+def column_costs(dims, ranks, p=1):
+    """Per-column madds of one product: sum_k reconstruct_madds + q n_v p."""
+    r = np.asarray(ranks, np.int64)
+    n1, n2, n3 = (int(d) for d in dims)
+    dec = n1 * r[..., 0] * r[..., 1] * r[..., 2] + n1 * n2 * r[..., 1] * r[..., 2] + n1 * n2 * n3 * r[..., 2]
+    return dec.sum(axis=1) + r.shape[1] * n1 * n2 * n3 * p
+
+
+class ShardedStore:
+    """One rank's column shard plus the collectives that assemble products."""
+
+    def __init__(self, store, col_begin, col_end, ncols_total, group=None, shards=None):
+        import torch.distributed as dist
+
+        self.store = store
+        self.c0, self.c1 = int(col_begin), int(col_end)
+        self.ncols = int(ncols_total)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if shards is None:
+            shards = [None] * self.world
+            if self.world > 1:
+                dist.all_gather_object(shards, (self.c0, self.c1), group=group)
+            else:
+                shards = [(self.c0, self.c1)]
+        self.shards = [tuple(s) for s in shards]
+        self.max_cols = max(b - a for a, b in self.shards)
+
+    @property
+    def rows(self):
+        return self.store.rows
+
+    def forward(self, x, dst=0, allreduce=False):
+        """y = Zbc x.  x: (ncols x p) on this rank's device (the full block or
+        just this shard's rows).  Returns the full y on `dst` (or every rank
+        with allreduce=True); other ranks get their partial."""
+        import torch.distributed as dist
+
+        xs = x[self.c0:self.c1] if x.shape[0] == self.ncols else x
+        y = self.store.forward(xs)
+        if self.world > 1:
+            # column-major (rows x p) blocks are contiguous as their transpose
+            buf = y if y.is_contiguous() else y.t()
+            if allreduce:
+                dist.all_reduce(buf, group=self.group)
+            else:
+                dist.reduce(buf, dst=dst, group=self.group)
+        return y
+
+    def adjoint(self, phi):
+        """z = Zbc^H phi on every rank.  phi: (q n_v x p), replicated."""
+        import torch
+        import torch.distributed as dist
+
+        z = self.store.adjoint(phi)
+        if self.world == 1:
+            return z
+        squeeze = z.dim() == 1
+        zz = z.reshape(z.shape[0], -1)
+        p = zz.shape[1]
+        pad = torch.zeros((self.max_cols, p), dtype=zz.dtype, device=zz.device)
+        pad[: zz.shape[0]] = zz
+        full = torch.empty((self.world * self.max_cols, p), dtype=zz.dtype, device=zz.device)
+        dist.all_gather_into_tensor(full, pad.contiguous(), group=self.group)
+        parts = [full[r * self.max_cols: r * self.max_cols + (b - a)] for r, (a, b) in enumerate(self.shards)]
+        out = torch.cat(parts, 0)
+        return out[:, 0] if squeeze else out
