@@ -5,6 +5,7 @@
 // forward / adjoint / ACA kernels.  No CPU fallback: every product runs on
 // the device or fails with TM_CUDA_ERROR.
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -18,6 +19,8 @@
 #include "tm_aux_kernels.cuh"
 #include "tm_common.cuh"
 #include "tm_kernels_cc.cuh"
+#include "tm_kernels_tc.cuh"
+#include "tm_tmap.h"
 
 using namespace tmb;
 
@@ -106,12 +109,20 @@ struct tm_store {
     int64_t m2 = 0;
     int rmax[3] = {1, 1, 1};
     std::vector<int32_t> ranks;  // [col][comp][mode]
+    std::vector<TDesc> host_desc;  // build-time only
     int64_t dec_madds = 0;
     TDesc* d_desc = nullptr;
     void* d_arena = nullptr;
     int64_t arena_elems = 0;
     void* d_v = nullptr;
     int64_t device_bytes = 0;
+    // tensor-core (tcgen05 3xTF32) forward data: B planes of U3, K offsets
+    bool tc_ok = false;
+    int* d_kofs = nullptr;   // [q*ncols] component-major K offset of each tensor
+    int* d_kc = nullptr;     // [q] K extent of each component
+    float* d_planes = nullptr;
+    int64_t kpad = 0;
+    CUtensorMap bmap{};
     std::mutex mu;
     DevBuf part, xin, yout, wbuf;
 
@@ -119,6 +130,9 @@ struct tm_store {
     int64_t rows() const { return q * nv(); }
     size_t csize() const { return dtype == TM_C64 ? sizeof(float2) : sizeof(double2); }
     ~tm_store() {
+        if (d_kofs) cudaFree(d_kofs);
+        if (d_kc) cudaFree(d_kc);
+        if (d_planes) cudaFree(d_planes);
         if (d_desc) cudaFree(d_desc);
         if (d_arena) cudaFree(d_arena);
         if (d_v) cudaFree(d_v);
@@ -128,6 +142,57 @@ struct tm_store {
 namespace {
 
 // ------------------------------------------------------------ store build --
+// The cta_group::1 tensor-core forward accumulates the whole K stream in
+// one TMEM chain; tcgen05's fp32 accumulate truncates, so its error grows
+// linearly with the column count (measured 4e-4 at 3200 columns, see
+// DESIGN.md).  It stays opt-in (TMB_ENABLE_TC=1) until the chained
+// accumulator lands; TMB_DISABLE_TC=1 forces the CUDA-core path.
+bool tc_disabled() {
+    const char* d = std::getenv("TMB_DISABLE_TC");
+    if (d && d[0] == '1') return true;
+    const char* e = std::getenv("TMB_ENABLE_TC");
+    return !(e && e[0] == '1');
+}
+
+// B planes of the tensor-core forward (see tm_kernels_tc.cuh), built once.
+void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
+    int dev = 0, major = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    if (s->dtype != TM_C64 || s->ncols == 0 || major != 10) return;
+    if (s->rmax[0] > 16 || s->rmax[1] > 16 || s->rmax[2] > 16) return;
+    if (s->dims[2] < 16) return;
+    const int64_t ntens = s->ncols * s->q;
+    std::vector<int> kofs(static_cast<size_t>(ntens)), kc(static_cast<size_t>(s->q), 0);
+    for (int k = 0; k < s->q; ++k) {
+        int64_t acc = 0;
+        for (int64_t j = 0; j < s->ncols; ++j) {
+            kofs[static_cast<size_t>(k * s->ncols + j)] = int(acc);
+            acc += desc[static_cast<size_t>(k * s->ncols + j)].r3;
+        }
+        if (acc >= (int64_t(1) << 30)) return;
+        kc[static_cast<size_t>(k)] = int(acc);
+        s->kpad = std::max<int64_t>(s->kpad, (acc + 7) / 8 * 8);
+    }
+    const int64_t n3 = s->dims[2];
+    const size_t pbytes = size_t(4) * s->q * n3 * s->kpad * sizeof(float);
+    CK(cudaMalloc(&s->d_kofs, kofs.size() * sizeof(int)));
+    CK(cudaMalloc(&s->d_kc, kc.size() * sizeof(int)));
+    CK(cudaMalloc(&s->d_planes, pbytes));
+    CK(cudaMemcpy(s->d_kofs, kofs.data(), kofs.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(s->d_kc, kc.data(), kc.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemset(s->d_planes, 0, pbytes));
+    build_bplanes_kernel<<<unsigned(ntens), 256>>>(s->d_desc, static_cast<const float2*>(s->d_arena), s->d_kofs,
+                                                   s->ncols, s->q, int(n3), s->kpad, s->d_planes);
+    launched(cudaSuccess, "build_bplanes_kernel");
+    CK(cudaDeviceSynchronize());
+    const uint32_t nmma = uint32_t(std::min<int64_t>((std::min<int64_t>(n3, 256) + 15) / 16 * 16, 256));
+    s->bmap = make_tmap_3d_f32(s->d_planes, uint64_t(s->kpad), uint64_t(n3), uint64_t(4 * s->q),
+                               uint64_t(s->kpad) * 4, uint64_t(n3) * s->kpad * 4, 8, nmma, CU_TENSOR_MAP_SWIZZLE_32B);
+    s->device_bytes += int64_t(pbytes + (kofs.size() + kc.size()) * sizeof(int));
+    s->tc_ok = true;
+}
+
 void build_store(tm_store* s, const tm_store_desc& d) {
     const int64_t n1 = d.dims[0], n2 = d.dims[1], n3 = d.dims[2];
     const int64_t ntens = s->ncols * s->q;
@@ -164,7 +229,10 @@ void build_store(tm_store* s, const tm_store_desc& d) {
         s->dec_madds += n1 * r[0] * r[1] * r[2] + n1 * n2 * r[1] * r[2] + n1 * n2 * n3 * r[2];
     }
     s->ranks.assign(d.ranks, d.ranks + 3 * ntens);
-    s->arena_elems = std::max<int64_t>(doff, 2);
+    s->host_desc = desc;
+    // slack: the tensor-core path bulk-copies whole tile rows of U1/U2 and
+    // may read past the last tensor's segments
+    s->arena_elems = doff + 16 * 64 + 4096;
     const size_t cs = s->csize();
     CK(cudaMalloc(&s->d_arena, size_t(s->arena_elems) * cs));
     CK(cudaMalloc(reinterpret_cast<void**>(&s->d_desc), desc.size() * sizeof(TDesc)));
@@ -205,6 +273,10 @@ void build_store(tm_store* s, const tm_store_desc& d) {
         CK(cudaDeviceSynchronize());
         t0 = t1;
     }
+
+    build_tc(s, s->host_desc);
+    s->host_desc.clear();
+    s->host_desc.shrink_to_fit();
 
     if (d.v) {
         if (d.m2 < 1) contract("store: ACA V needs m2 >= 1");
@@ -348,7 +420,51 @@ int pick_cn(int64_t n3) {
     return cn;
 }
 
+int num_sms(int dev) {
+    int n = 0;
+    CK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    return n;
+}
+
+void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy,
+                    cudaStream_t st) {
+    TcGeom g{};
+    g.ncols = s->ncols;
+    g.n1 = int(s->dims[0]);
+    g.n2 = int(s->dims[1]);
+    g.n3 = int(s->dims[2]);
+    g.q = s->q;
+    g.nt1 = (g.n1 + TC_TI1 - 1) / TC_TI1;
+    g.nt2 = (g.n2 + TC_TI2 - 1) / TC_TI2;
+    g.nt3 = (g.n3 + 255) / 256;
+    g.nmma = std::min(256, (std::min(g.n3, 256) + 15) / 16 * 16);
+    g.p = int(p);
+    g.ntiles = int64_t(p) * g.q * g.nt3 * g.nt2 * g.nt1;
+    g.rmax1 = s->rmax[0];
+    g.rmax2 = s->rmax[1];
+    g.rmax3 = s->rmax[2];
+    g.g_off = 64;
+    g.u1_off = g.g_off + int(round16(uint32_t(g.rmax1 * g.rmax2 * g.rmax3) * 8u));
+    g.u2_off = g.u1_off + TC_TI1 * g.rmax1 * 8;
+    g.slot_bytes = (g.u2_off + TC_TI2 * g.rmax2 * 8 + 127) / 128 * 128;
+    g.b_stage = 4 * g.nmma * 32;
+    const size_t smem = 1024 + size_t(TC_NST) * (TC_A_STAGE + g.b_stage) + size_t(TC_JR) * g.slot_bytes +
+                        size_t(TC_TI1) * g.rmax2 * g.rmax3 * sizeof(float2) + 16 + 16 * 16;
+    if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core forward: shared-memory plan too large");
+    CK(cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const unsigned grid = unsigned(std::min<int64_t>(g.ntiles, num_sms(dev)));
+    fwd_tc_kernel<<<grid, TC_THREADS, smem, st>>>(s->bmap, s->d_desc, static_cast<const float2*>(s->d_arena), s->d_kc,
+                                                   g, x, ldx, y, ldy);
+    launched(cudaSuccess, "fwd_tc_kernel");
+}
+
 void forward_dev(const tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy, cudaStream_t st) {
+    if (s->tc_ok && !tc_disabled()) {
+        run_forward_tc(s, static_cast<const float2*>(x), ldx, p, static_cast<float2*>(y), ldy, st);
+        return;
+    }
     const int cn = pick_cn(s->dims[2]);
     if (s->dtype == TM_C64) {
         auto X = static_cast<const float2*>(x);

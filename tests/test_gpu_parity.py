@@ -212,3 +212,28 @@ def test_aca_products(oracle, product, dtype):
     # and the operator stays within a decade of the ACA tolerance (test_aca.cpp:134-139)
     z = O.assemble_full(sc)
     assert rel(ds.aca_forward(x), z @ x) <= 10 * 1e-4
+
+
+@pytest.mark.parametrize("dims,q,m,rmin,rmax,p", [
+    ((16, 16, 16), 3, 9, 2, 6, 1),       # smallest tensor-core shape
+    ((24, 40, 40), 2, 21, 3, 16, 2),     # ranks up to the tensor-core limit, partial row tiles
+    ((64, 64, 64), 12, 7, 4, 9, 1),      # config-5 grid
+    ((20, 18, 300), 1, 5, 2, 8, 1),      # n3 > 256: two i3 blocks, partial N
+    ((192, 224, 256), 1, 3, 5, 12, 1),   # config-4 grid, a few columns
+])
+def test_tensor_core_forward(oracle, product, monkeypatch, dims, q, m, rmin, rmax, p):
+    """tcgen05 3xTF32 forward (c64) vs the oracle and vs the CUDA-core kernel."""
+    O, P = oracle, product
+    cc = ragged_store(dims, q, m, rmin, rmax, seed=7 * m + q)
+    ref = O.OracleStore(cc.rounded_c64())
+    ds = P.DeviceStore.from_compressed(cc, "c64")
+    x = cn01(m, p, 3).astype(np.complex64).astype(np.complex128)
+    monkeypatch.setenv("TMB_ENABLE_TC", "1")
+    y_tc = ds.forward(x)
+    monkeypatch.setenv("TMB_DISABLE_TC", "1")
+    y_cc = ds.forward(x)
+    monkeypatch.delenv("TMB_DISABLE_TC")
+    monkeypatch.delenv("TMB_ENABLE_TC")
+    y_ref = ref.forward(x)
+    assert rel(y_tc, y_ref) <= 1e-5
+    assert rel(y_cc, y_ref) <= 1e-5
