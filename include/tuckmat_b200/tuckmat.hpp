@@ -34,6 +34,9 @@
 
 #include "../tuckmat_b200.h"
 
+// The drop-in's symbols are part of the library's public ABI.
+#pragma GCC visibility push(default)
+
 namespace tuckmat {
 
 using Complex = std::complex<double>;
@@ -231,3 +234,5 @@ MultiVector aca_adjoint(const DeviceStore& s, const MultiVector& phi);
 
 }  // namespace b200
 }  // namespace tuckmat
+
+#pragma GCC visibility pop

@@ -312,6 +312,15 @@ tm_store* create_store(const tm_store_desc& d, int device, int dtype) {
     if (d.dims[0] > (1 << 30) || d.dims[1] > (1 << 30) || d.dims[2] > (1 << 30))
         contract("store: grid dimension too large");
     if (d.ncols > 0 && (!d.ranks || !d.payload)) contract("store: ranks and payload are required");
+    if (d.v && d.m2 < 1) contract("store: ACA V needs m2 >= 1");
+    // validate every rank before touching the device (reference: read_tucker,
+    // src/io.cpp:133-139, and the TuckerTensor invariant 1 <= r_g <= n_g)
+    for (int64_t i = 0; i < d.ncols * d.q; ++i)
+        for (int g = 0; g < 3; ++g) {
+            const int32_t r = d.ranks[3 * i + g];
+            if (r < 1 || r > d.dims[g])
+                contract("store: tucker rank " + std::to_string(r) + " out of range for mode " + std::to_string(g + 1));
+        }
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) throw TmError(TM_CUDA_ERROR, "store: no CUDA device " + std::to_string(device));

@@ -1,0 +1,111 @@
+"""Multi-GPU column sharding, host logic on CPU with gloo (world_size 2 and 3).
+
+Each rank wraps an oracle-backed store over its cost-balanced column shard;
+ShardedStore must reproduce the single-process products: the forward by a
+sum-reduce of the partial y blocks, the adjoint by an all-gather of the shard
+rows of z.  (On the GPU box the same class runs DeviceStore shards over NCCL.)
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+
+class OracleShard:
+    """Store-like wrapper (rows / forward / adjoint on torch CPU tensors)."""
+
+    def __init__(self, cc):
+        from oracle import oracle as O
+        self.st = O.OracleStore(cc)
+        self.rows = self.st.rows
+
+    def forward(self, x):
+        import torch
+        y = self.st.forward(x.numpy())
+        return torch.from_numpy(np.ascontiguousarray(y))
+
+    def adjoint(self, phi):
+        import torch
+        return torch.from_numpy(np.ascontiguousarray(self.st.adjoint(phi.numpy())))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_q):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch
+    import torch.distributed as dist
+    from helpers import ragged_store
+    from oracle import oracle as O
+    from paper_2103_06393_b200.sharded import ShardedStore, balanced_shards, column_costs
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cc = ragged_store((9, 7, 11), 3, 13, 1, 5, seed=42)
+        shards = balanced_shards(column_costs(cc.grid_dims, cc.ranks, 2), world)
+        c0, c1 = shards[rank]
+        off = O.tensor_offsets(cc.grid_dims, cc.ranks)
+        sub = O.Compressed(cc.grid_dims, cc.q, c1 - c0, cc.ranks[c0:c1],
+                           cc.payload[off[c0 * cc.q]:off[c1 * cc.q]])
+        sh = ShardedStore(OracleShard(sub), c0, c1, cc.m)
+        assert sh.shards == [tuple(s) for s in shards]
+        rng = np.random.default_rng(3)
+        x = rng.standard_normal((cc.m, 2)) + 1j * rng.standard_normal((cc.m, 2))
+        phi = rng.standard_normal((cc.rows, 2)) + 1j * rng.standard_normal((cc.rows, 2))
+        y = sh.forward(torch.from_numpy(x), dst=0)
+        ya = sh.forward(torch.from_numpy(x), allreduce=True)
+        z = sh.adjoint(torch.from_numpy(phi))
+        full = O.OracleStore(cc)
+        res = {"rank": rank,
+               "ya": float(np.linalg.norm(ya.numpy() - full.forward(x)) / np.linalg.norm(full.forward(x))),
+               "z": float(np.linalg.norm(z.numpy() - full.adjoint(phi)) / np.linalg.norm(full.adjoint(phi)))}
+        if rank == 0:
+            res["y"] = float(np.linalg.norm(y.numpy() - full.forward(x)) / np.linalg.norm(full.forward(x)))
+        out_q.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_products_gloo(world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    res = [q.get(timeout=10) for _ in range(world)]
+    for r in res:
+        assert r["ya"] < 1e-13 and r["z"] < 1e-13
+        if r["rank"] == 0:
+            assert r["y"] < 1e-13
+
+
+def test_balanced_shards():
+    from paper_2103_06393_b200.sharded import balanced_shards
+    costs = np.array([5, 1, 1, 1, 1, 1, 5, 5, 1, 1], float)
+    for world in (1, 2, 3, 4, 8):
+        sh = balanced_shards(costs, world)
+        assert sh[0][0] == 0 and sh[-1][1] == len(costs)
+        assert all(a <= b for a, b in sh) and all(sh[i][1] == sh[i + 1][0] for i in range(world - 1))
+    big = np.random.default_rng(0).uniform(1, 2.3, 5000)
+    sh = balanced_shards(big, 8)
+    loads = [big[a:b].sum() for a, b in sh]
+    assert max(loads) / min(loads) < 1.01

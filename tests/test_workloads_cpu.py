@@ -1,0 +1,46 @@
+"""Benchmark workload definitions (BASELINE.json configs) on CPU."""
+import numpy as np
+
+from paper_2103_06393_b200.sharded import column_costs
+from paper_2103_06393_b200.workloads import CONFIGS, rank_table, synthetic_payload, tensor_offsets
+
+
+def test_configs_match_baseline():
+    c4 = CONFIGS["c4"]
+    assert c4.grid == (192, 224, 256) and c4.q == 12 and c4.m == 5000 and c4.dtype == "c64"
+    assert CONFIGS["c1"].grid == (24, 24, 24) and CONFIGS["c1"].dtype == "c128" and CONFIGS["c1"].m == 128
+    assert CONFIGS["c5"].p == 32 and CONFIGS["c5"].q == 12
+    assert CONFIGS["c3"].aca_m2 == 2048
+
+
+def test_rank_model_matches_survey_probes():
+    """config-4 ranks 5-12, mean about 9; store about 3.1 GB (c64)."""
+    r = rank_table(CONFIGS["c4"])
+    assert r.min() >= 4 and r.max() <= 13
+    assert 7.5 <= r.mean() <= 9.5
+    n = np.array(CONFIGS["c4"].grid)
+    scalars = (r[..., 0] * r[..., 1] * r[..., 2] + r @ n).sum()
+    assert 2.5e9 < 8 * scalars < 3.6e9
+
+
+def test_column_costs_are_opcounts(oracle):
+    cc = oracle.synthetic_compression(6, 3, 2, 1)
+    st = oracle.OracleStore(cc)
+    dec, acc = st.opcounts(4)
+    assert column_costs(cc.grid_dims, cc.ranks, 4).sum() == dec + acc
+
+
+def test_synthetic_payload_layout_cpu(oracle):
+    """The device generator's CTC1 layout on CPU: orthonormal factors, seeded."""
+    import torch
+    cfg = CONFIGS["c1"]
+    ranks = rank_table(cfg)[:3]
+    pay, off = synthetic_payload(cfg.grid, ranks, np.ones(3), 5, device="cpu")
+    pay2, _ = synthetic_payload(cfg.grid, ranks, np.ones(3), 5, device="cpu")
+    assert torch.equal(pay, pay2)
+    assert off[-1] == tensor_offsets(cfg.grid, ranks)[-1] == pay.numel()
+    p = pay.numpy()
+    for i in range(ranks.shape[0] * ranks.shape[1]):
+        core, u1, u2, u3 = oracle.split_tensor(cfg.grid, ranks.reshape(-1, 3)[i], p[off[i]:off[i + 1]])
+        for u in (u1, u2, u3):
+            assert np.linalg.norm(u.conj().T @ u - np.eye(u.shape[1])) < 1e-12
