@@ -334,6 +334,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    torch.cuda.profiler.start()  # ncu --profile-from-start off captures exactly the timed region
     l0 = launch_count()
     t_all0 = torch.cuda.Event(enable_timing=True)
     t_all1 = torch.cuda.Event(enable_timing=True)
@@ -342,6 +343,7 @@ def main():
         step(evs[s])
     t_all1.record(stream)
     torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     if world > 1:
         dist.barrier()
     launches = launch_count() - l0

@@ -1,0 +1,48 @@
+#!/usr/bin/env python
+"""Profiling driver: build a bench store unprofiled, then run exactly one
+forward and one adjoint between cudaProfilerStart / Stop, so that
+`ncu --profile-from-start off` sees only the product kernels."""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--cols", type=int, default=0, help="use only the first N columns (0 = all)")
+    ap.add_argument("--tc", action="store_true", help="enable the tensor-core forward")
+    args = ap.parse_args()
+    import torch
+    from paper_2103_06393_b200 import DeviceStore
+    from paper_2103_06393_b200.workloads import CONFIGS, column_scales, rank_table, synthetic_payload
+    if args.tc:
+        os.environ["TMB_ENABLE_TC"] = "1"
+    cfg = CONFIGS[args.config]
+    m = args.cols or cfg.m
+    ranks = rank_table(cfg, 1234)[:m]
+    pay, _ = synthetic_payload(cfg.grid, ranks, column_scales(cfg, 1234)[:m], 2234, device="cuda")
+    s = DeviceStore.from_arrays(cfg.grid, cfg.q, ranks, pay, cfg.dtype, 0)
+    del pay
+    rows = cfg.q * int(np.prod(cfg.grid))
+    cdt = torch.complex64 if cfg.dtype == "c64" else torch.complex128
+    x = torch.randn((cfg.p, m), dtype=cdt, device="cuda").t()
+    phi = torch.randn((cfg.p, rows), dtype=cdt, device="cuda").t()
+    s.forward(x)
+    s.adjoint(phi)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    s.forward(x)
+    s.adjoint(phi)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    print("prof_run done", cfg.name, "cols", m)
+
+
+if __name__ == "__main__":
+    main()
