@@ -142,16 +142,19 @@ struct tm_store {
 namespace {
 
 // ------------------------------------------------------------ store build --
-// The cta_group::1 tensor-core forward accumulates the whole K stream in
-// one TMEM chain; tcgen05's fp32 accumulate truncates, so its error grows
-// linearly with the column count (measured 4e-4 at 3200 columns, see
-// DESIGN.md).  It stays opt-in (TMB_ENABLE_TC=1) until the chained
-// accumulator lands; TMB_DISABLE_TC=1 forces the CUDA-core path.
+// c64 stores run the forward on the tcgen05 3xTF32 kernel (chained TMEM
+// accumulation, tm_kernels_tc.cuh) whenever the store qualifies;
+// TMB_DISABLE_TC=1 forces the CUDA-core kernel (used by the tests to check
+// one against the other).
 bool tc_disabled() {
     const char* d = std::getenv("TMB_DISABLE_TC");
-    if (d && d[0] == '1') return true;
-    const char* e = std::getenv("TMB_ENABLE_TC");
-    return !(e && e[0] == '1');
+    return d && d[0] == '1';
+}
+
+int tc_chain() {
+    const char* e = std::getenv("TMB_TC_CHAIN");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? v : 12;
 }
 
 // B planes of the tensor-core forward (see tm_kernels_tc.cuh), built once.
@@ -160,7 +163,7 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
     if (s->dtype != TM_C64 || s->ncols == 0 || major != 10) return;
-    if (s->rmax[0] > 16 || s->rmax[1] > 16 || s->rmax[2] > 16) return;
+    if (s->rmax[0] > TC_RMAX || s->rmax[1] > TC_RMAX || s->rmax[2] > TC_RMAX) return;
     if (s->dims[2] < 16) return;
     const int64_t ntens = s->ncols * s->q;
     std::vector<int> kofs(static_cast<size_t>(ntens)), kc(static_cast<size_t>(s->q), 0);
@@ -186,7 +189,7 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
                                                    s->ncols, s->q, int(n3), s->kpad, s->d_planes);
     launched(cudaSuccess, "build_bplanes_kernel");
     CK(cudaDeviceSynchronize());
-    const uint32_t nmma = uint32_t(std::min<int64_t>((std::min<int64_t>(n3, 256) + 15) / 16 * 16, 256));
+    const uint32_t nmma = uint32_t(std::min<int64_t>((n3 + 15) / 16 * 16, TC_NMAX));
     s->bmap = make_tmap_3d_f32(s->d_planes, uint64_t(s->kpad), uint64_t(n3), uint64_t(4 * s->q),
                                uint64_t(s->kpad) * 4, uint64_t(n3) * s->kpad * 4, 8, nmma, CU_TENSOR_MAP_SWIZZLE_32B);
     s->device_bytes += int64_t(pbytes + (kofs.size() + kc.size()) * sizeof(int));
@@ -445,8 +448,8 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     g.q = s->q;
     g.nt1 = (g.n1 + TC_TI1 - 1) / TC_TI1;
     g.nt2 = (g.n2 + TC_TI2 - 1) / TC_TI2;
-    g.nt3 = (g.n3 + 255) / 256;
-    g.nmma = std::min(256, (std::min(g.n3, 256) + 15) / 16 * 16);
+    g.nmma = std::min(TC_NMAX, (g.n3 + 15) / 16 * 16);
+    g.nt3 = (g.n3 + g.nmma - 1) / g.nmma;
     g.p = int(p);
     g.ntiles = int64_t(p) * g.q * g.nt3 * g.nt2 * g.nt1;
     g.rmax1 = s->rmax[0];
@@ -457,8 +460,15 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     g.u2_off = g.u1_off + TC_TI1 * g.rmax1 * 8;
     g.slot_bytes = (g.u2_off + TC_TI2 * g.rmax2 * 8 + 127) / 128 * 128;
     g.b_stage = 4 * g.nmma * 32;
-    const size_t smem = 1024 + size_t(TC_NST) * (TC_A_STAGE + g.b_stage) + size_t(TC_JR) * g.slot_bytes +
-                        size_t(TC_TI1) * g.rmax2 * g.rmax3 * sizeof(float2) + 16 + 16 * 16;
+    g.chain = tc_chain();
+    g.v_stride = TC_TI1 * g.rmax2 * g.rmax3;
+    auto smem_for = [&](int nst) {
+        return 1024 + size_t(nst) * (TC_A_STAGE + g.b_stage) + size_t(TC_JR) * g.slot_bytes +
+               size_t(2) * g.v_stride * sizeof(float4) + (2 * TC_NST_MAX + 2 * TC_JR + 2) * 8 + 16;
+    };
+    g.nst = TC_NST_MAX;
+    while (g.nst > 2 && smem_for(g.nst) > kSmemMax) --g.nst;
+    const size_t smem = smem_for(g.nst);
     if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core forward: shared-memory plan too large");
     CK(cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int dev = 0;

@@ -218,22 +218,49 @@ def test_aca_products(oracle, product, dtype):
     ((16, 16, 16), 3, 9, 2, 6, 1),       # smallest tensor-core shape
     ((24, 40, 40), 2, 21, 3, 16, 2),     # ranks up to the tensor-core limit, partial row tiles
     ((64, 64, 64), 12, 7, 4, 9, 1),      # config-5 grid
-    ((20, 18, 300), 1, 5, 2, 8, 1),      # n3 > 256: two i3 blocks, partial N
+    ((20, 18, 300), 1, 5, 2, 8, 1),      # n3 > 256: three i3 blocks, partial N
     ((192, 224, 256), 1, 3, 5, 12, 1),   # config-4 grid, a few columns
+    ((9, 70, 20), 2, 40, 1, 13, 3),      # many short chains, ragged ranks from 1
 ])
 def test_tensor_core_forward(oracle, product, monkeypatch, dims, q, m, rmin, rmax, p):
-    """tcgen05 3xTF32 forward (c64) vs the oracle and vs the CUDA-core kernel."""
+    """tcgen05 3xTF32 forward (c64, the default c64 forward) vs the oracle and
+    vs the CUDA-core kernel (TMB_DISABLE_TC=1)."""
     O, P = oracle, product
     cc = ragged_store(dims, q, m, rmin, rmax, seed=7 * m + q)
     ref = O.OracleStore(cc.rounded_c64())
     ds = P.DeviceStore.from_compressed(cc, "c64")
     x = cn01(m, p, 3).astype(np.complex64).astype(np.complex128)
-    monkeypatch.setenv("TMB_ENABLE_TC", "1")
     y_tc = ds.forward(x)
     monkeypatch.setenv("TMB_DISABLE_TC", "1")
     y_cc = ds.forward(x)
     monkeypatch.delenv("TMB_DISABLE_TC")
-    monkeypatch.delenv("TMB_ENABLE_TC")
     y_ref = ref.forward(x)
     assert rel(y_tc, y_ref) <= 1e-5
     assert rel(y_cc, y_ref) <= 1e-5
+
+
+@pytest.mark.parametrize("chain", ["", "1", "3"])
+def test_tensor_core_long_k(product, monkeypatch, chain):
+    """Accumulation over a long K stream (2 500 columns, K ~ 21 000 per
+    component): the chained TMEM accumulation must stay within 1e-5 of the
+    complex128 GPU forward on the same rounded factors (the c128 kernels are
+    pinned to the oracle at 1e-12 above).  An unchained accumulator drifts
+    to ~3e-4 here."""
+    import torch
+    from paper_2103_06393_b200.workloads import Config, rank_table, synthetic_payload
+    P = product
+    cfg = Config("longk", (32, 32, 128), 2, 2500, "c64", 1, (3.0, 50.0))
+    ranks = rank_table(cfg, 5)
+    pay, _ = synthetic_payload(cfg.grid, ranks, np.ones(cfg.m), 9, device="cuda")
+    p64 = pay.to(torch.complex64).to(torch.complex128)
+    s64 = P.DeviceStore.from_arrays(cfg.grid, cfg.q, ranks, pay, "c64", 0)
+    s128 = P.DeviceStore.from_arrays(cfg.grid, cfg.q, ranks, p64, "c128", 0)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    x = torch.randn((1, cfg.m), dtype=torch.complex64, device="cuda", generator=g).t()
+    if chain:
+        monkeypatch.setenv("TMB_TC_CHAIN", chain)
+    y64 = s64.forward(x).to(torch.complex128)
+    y128 = s128.forward(x.to(torch.complex128))
+    err = float(torch.linalg.vector_norm(y64 - y128) / torch.linalg.vector_norm(y128))
+    assert err <= 1e-5, err

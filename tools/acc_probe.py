@@ -29,9 +29,7 @@ def main():
             g.manual_seed(3)
             x = torch.randn((1, m), dtype=torch.complex64, device="cuda", generator=g).t()
             yr = s128.forward(x.to(torch.complex128))
-            os.environ["TMB_ENABLE_TC"] = "1"
             yt = s64.forward(x)
-            os.environ.pop("TMB_ENABLE_TC")
             os.environ["TMB_DISABLE_TC"] = "1"
             yc = s64.forward(x)
             os.environ.pop("TMB_DISABLE_TC")

@@ -16,13 +16,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c4")
     ap.add_argument("--cols", type=int, default=0, help="use only the first N columns (0 = all)")
-    ap.add_argument("--tc", action="store_true", help="enable the tensor-core forward")
+    ap.add_argument("--cc", action="store_true", help="force the CUDA-core forward (TMB_DISABLE_TC=1)")
     args = ap.parse_args()
     import torch
     from paper_2103_06393_b200 import DeviceStore
     from paper_2103_06393_b200.workloads import CONFIGS, column_scales, rank_table, synthetic_payload
-    if args.tc:
-        os.environ["TMB_ENABLE_TC"] = "1"
+    if args.cc:
+        os.environ["TMB_DISABLE_TC"] = "1"
     cfg = CONFIGS[args.config]
     m = args.cols or cfg.m
     ranks = rank_table(cfg, 1234)[:m]
