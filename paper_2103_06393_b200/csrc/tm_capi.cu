@@ -121,6 +121,9 @@ struct tm_store {
     int* d_kofs = nullptr;   // [q*ncols] component-major K offset of each tensor
     int* d_kc = nullptr;     // [q] K extent of each component
     float* d_planes = nullptr;
+    TcDesc* d_tcd = nullptr;  // [q*ncols] tensor-core descriptors
+    float4* d_varena = nullptr;  // mode-1 products V = U1 x_1 G (FFMA2 form)
+    float2* d_u2arena = nullptr;  // U2 with odd row strides
     int64_t kpad = 0;
     CUtensorMap bmap{};
     std::mutex mu;
@@ -133,6 +136,9 @@ struct tm_store {
         if (d_kofs) cudaFree(d_kofs);
         if (d_kc) cudaFree(d_kc);
         if (d_planes) cudaFree(d_planes);
+        if (d_tcd) cudaFree(d_tcd);
+        if (d_varena) cudaFree(d_varena);
+        if (d_u2arena) cudaFree(d_u2arena);
         if (d_desc) cudaFree(d_desc);
         if (d_arena) cudaFree(d_arena);
         if (d_v) cudaFree(d_v);
@@ -178,21 +184,49 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
         s->kpad = std::max<int64_t>(s->kpad, (acc + 7) / 8 * 8);
     }
     const int64_t n3 = s->dims[2];
-    const size_t pbytes = size_t(4) * s->q * n3 * s->kpad * sizeof(float);
+    const size_t pbytes = size_t(TC_BPLANES) * s->q * n3 * s->kpad * sizeof(float);
+    // V arena: per tensor ceil(n1/4)*4 x r2 x r3 float4
+    const int64_t n1p = (s->dims[0] + 3) / 4 * 4;
+    std::vector<TcDesc> tcd(static_cast<size_t>(ntens));
+    int64_t voff = 0, u2off = 0;
+    const int64_t n2p = (s->dims[1] + TC_TI2 - 1) / TC_TI2 * TC_TI2;
+    for (int64_t t = 0; t < ntens; ++t) {
+        const TDesc& d = desc[static_cast<size_t>(t)];
+        TcDesc& c = tcd[static_cast<size_t>(t)];
+        c.off_v = voff;
+        c.off_u2 = u2off;
+        u2off += n2p * (d.r2 | 1);
+        c.r2 = d.r2;
+        c.r3 = d.r3;
+        c.pad0 = c.pad1 = 0;
+        voff += n1p * d.r2 * d.r3;
+    }
+    const size_t vbytes = size_t(voff) * sizeof(float4);
+    const size_t u2bytes = size_t(u2off) * sizeof(float2);
     CK(cudaMalloc(&s->d_kofs, kofs.size() * sizeof(int)));
     CK(cudaMalloc(&s->d_kc, kc.size() * sizeof(int)));
     CK(cudaMalloc(&s->d_planes, pbytes));
+    CK(cudaMalloc(&s->d_tcd, tcd.size() * sizeof(TcDesc)));
+    CK(cudaMalloc(&s->d_varena, std::max<size_t>(vbytes, 16)));
+    CK(cudaMalloc(&s->d_u2arena, std::max<size_t>(u2bytes, 16)));
     CK(cudaMemcpy(s->d_kofs, kofs.data(), kofs.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(s->d_kc, kc.data(), kc.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(s->d_tcd, tcd.data(), tcd.size() * sizeof(TcDesc), cudaMemcpyHostToDevice));
     CK(cudaMemset(s->d_planes, 0, pbytes));
     build_bplanes_kernel<<<unsigned(ntens), 256>>>(s->d_desc, static_cast<const float2*>(s->d_arena), s->d_kofs,
                                                    s->ncols, s->q, int(n3), s->kpad, s->d_planes);
     launched(cudaSuccess, "build_bplanes_kernel");
+    build_v_kernel<<<unsigned(ntens), 256>>>(s->d_desc, static_cast<const float2*>(s->d_arena), s->d_tcd,
+                                             int(s->dims[0]), s->d_varena);
+    launched(cudaSuccess, "build_v_kernel");
+    build_u2_kernel<<<unsigned(ntens), 256>>>(s->d_desc, static_cast<const float2*>(s->d_arena), s->d_tcd,
+                                              int(s->dims[1]), s->d_u2arena);
+    launched(cudaSuccess, "build_u2_kernel");
     CK(cudaDeviceSynchronize());
     const uint32_t nmma = uint32_t(std::min<int64_t>((n3 + 15) / 16 * 16, TC_NMAX));
-    s->bmap = make_tmap_3d_f32(s->d_planes, uint64_t(s->kpad), uint64_t(n3), uint64_t(4 * s->q),
+    s->bmap = make_tmap_3d_f32(s->d_planes, uint64_t(s->kpad), uint64_t(n3), uint64_t(TC_BPLANES * s->q),
                                uint64_t(s->kpad) * 4, uint64_t(n3) * s->kpad * 4, 8, nmma, CU_TENSOR_MAP_SWIZZLE_32B);
-    s->device_bytes += int64_t(pbytes + (kofs.size() + kc.size()) * sizeof(int));
+    s->device_bytes += int64_t(pbytes + vbytes + u2bytes + tcd.size() * sizeof(TcDesc) + (kofs.size() + kc.size()) * sizeof(int));
     s->tc_ok = true;
 }
 
@@ -452,30 +486,26 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     g.nt3 = (g.n3 + g.nmma - 1) / g.nmma;
     g.p = int(p);
     g.ntiles = int64_t(p) * g.q * g.nt3 * g.nt2 * g.nt1;
-    g.rmax1 = s->rmax[0];
     g.rmax2 = s->rmax[1];
     g.rmax3 = s->rmax[2];
-    g.g_off = 64;
-    g.u1_off = g.g_off + int(round16(uint32_t(g.rmax1 * g.rmax2 * g.rmax3) * 8u));
-    g.u2_off = g.u1_off + TC_TI1 * g.rmax1 * 8;
-    g.slot_bytes = (g.u2_off + TC_TI2 * g.rmax2 * 8 + 127) / 128 * 128;
-    g.b_stage = 4 * g.nmma * 32;
+    g.u2_off = TC_SLOT_V + TC_TI1 * g.rmax2 * g.rmax3 * 16;
+    g.slot_bytes = (g.u2_off + TC_TI2 * (g.rmax2 | 1) * 8 + 127) / 128 * 128;
+    g.b_stage = TC_BPLANES * g.nmma * 32;
     g.chain = tc_chain();
-    g.v_stride = TC_TI1 * g.rmax2 * g.rmax3;
     auto smem_for = [&](int nst) {
         return 1024 + size_t(nst) * (TC_A_STAGE + g.b_stage) + size_t(TC_JR) * g.slot_bytes +
-               size_t(2) * g.v_stride * sizeof(float4) + (2 * TC_NST_MAX + 2 * TC_JR + 2) * 8 + 16;
+               (2 * TC_NST_MAX + 2 * TC_JR + 2) * 8 + 16;
     };
     g.nst = TC_NST_MAX;
-    while (g.nst > 2 && smem_for(g.nst) > kSmemMax) --g.nst;
+    while (g.nst > 3 && smem_for(g.nst) > kSmemMax) --g.nst;
     const size_t smem = smem_for(g.nst);
     if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core forward: shared-memory plan too large");
     CK(cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int dev = 0;
     CK(cudaGetDevice(&dev));
     const unsigned grid = unsigned(std::min<int64_t>(g.ntiles, num_sms(dev)));
-    fwd_tc_kernel<<<grid, TC_THREADS, smem, st>>>(s->bmap, s->d_desc, static_cast<const float2*>(s->d_arena), s->d_kc,
-                                                   g, x, ldx, y, ldy);
+    fwd_tc_kernel<<<grid, TC_THREADS, smem, st>>>(s->bmap, s->d_tcd, s->d_varena, s->d_u2arena, s->d_kc, g, x, ldx,
+                                                   y, ldy);
     launched(cudaSuccess, "fwd_tc_kernel");
 }
 

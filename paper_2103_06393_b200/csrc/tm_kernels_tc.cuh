@@ -13,8 +13,11 @@
 // (U3 of every column, concatenated along K) is pre-split at store creation
 // into four fp32 planes {Re hi, Re lo, Im hi, Im lo} (hi = tf32(x),
 // lo = tf32(x - hi)), laid out [plane][k][i3][K] and streamed by TMA
-// (SWIZZLE_32B, 8 K per stage).  The A operand W is produced on the fly by 8
-// producer warps (FFMA2 mode products) into the same four-plane split in
+// (SWIZZLE_32B, 8 K per stage; see build_bplanes_kernel for the 6-plane
+// complex-as-real layout).  The mode-1 products V_j = U1_j x_1 G_j are
+// formed once per store (build_v_kernel; per tile they would be recomputed
+// n2/TI2 x n3/NMMA times).  The A operand W is produced on the fly by 8
+// producer warps (FFMA2 mode-2 products) into the same four-plane split in
 // shared memory (hi = W with the low 13 mantissa bits cleared, lo = W - hi),
 // so no decompressed column is ever written anywhere.  Per 8-wide K step the
 // MMA warp issues 12 tcgen05.mma (M=128, N=NMMA, K=8):
@@ -33,10 +36,10 @@
 // Warp roles (512 threads, 1 CTA / SM, persistent over tiles):
 //   warp 0      TMA producer of the B planes
 //   warp 1      MMA issuer (one elected thread)
-//   warp 2      factor loader: per column, bulk-copies {TDesc, G, U1 rows,
-//               U2 rows} of the tile into a 2-deep shared-memory ring
+//   warp 2      factor loader: per column, bulk-copies {TcDesc, V rows,
+//               U2 rows} of the tile into a 3-deep shared-memory ring
 //   warp 3      TMEM allocator
-//   warps 4-11  A producers (mode-1 V, mode-2 W, hi/lo split)
+//   warps 4-11  A producers (mode-2 W, x_j scale, hi/lo split)
 //   warps 12-15 chain fold + epilogue (TMEM -> registers -> y)
 // Pipelines: A/B stage ring (full: 1 TMA arrive+tx + 8 producer-warp
 // arrivals; empty: tcgen05.commit), factor ring (full: bulk-copy tx; empty:
@@ -51,7 +54,7 @@ namespace tmb {
 
 constexpr int TC_TI1 = 4, TC_TI2 = 32, TC_ROWS = 128;
 constexpr int TC_NST_MAX = 4;   // A/B stages (8 K each)
-constexpr int TC_JR = 2;        // factor-ring slots
+constexpr int TC_JR = 3;        // factor-ring slots
 constexpr int TC_THREADS = 512;
 constexpr int TC_NPW = 8;       // producer warps
 constexpr int TC_PW0 = 4;       // first producer warp
@@ -61,6 +64,21 @@ constexpr int TC_RMAX = 16;     // rank bound of the tensor-core path
 constexpr int TC_A_PLANE = TC_ROWS * 32;     // bytes (128 rows x 8 tf32)
 constexpr int TC_A_STAGE = 4 * TC_A_PLANE;   // 16 KB
 constexpr uint32_t TC_RUN_COL = 256;         // TMEM column of the running sum
+constexpr int TC_SLOT_V = 128;               // byte offset of the V block in a factor slot
+constexpr int TC_BPLANES = 6;                // B planes: [-U3i, U3r, U3i] x {hi, lo}
+
+// Per-tensor descriptor of the tensor-core forward (component-major like
+// TDesc).  off_v: float4 offset of the tensor's mode-1 product
+// V = U1 x_1 G in the V arena, laid out [i1/4][b + r2 c][i1 % 4] with each
+// complex stored as (vr, vi, -vi, vr) (the FFMA2 operand form); off_u2:
+// float2 offset of the tensor's U2 copy in the U2 arena, n2 rounded up to
+// TI2 rows (zero rows past n2) with an odd row stride r2 | 1 (conflict-free
+// 32-lane row loads).
+struct TcDesc {
+    int64_t off_v;
+    int64_t off_u2;
+    int32_t r2, r3, pad0, pad1;
+};
 
 struct TcGeom {
     int64_t ncols;
@@ -69,13 +87,12 @@ struct TcGeom {
     int nmma;       // N per MMA = i3 per tile (multiple of 16, <= 128)
     int p;          // right-hand sides
     int64_t ntiles;
-    int rmax1, rmax2, rmax3;
+    int rmax2, rmax3;
     int slot_bytes;             // factor slot size (multiple of 128)
-    int g_off, u1_off, u2_off;  // byte offsets in a slot (TDesc at 0)
+    int u2_off;                 // byte offset of the U2 rows in a slot
     int b_stage;                // bytes of one B stage (4 planes x nmma x 32)
-    int nst;                    // A/B stages in the ring (<= TC_NST_MAX)
+    int nst;                    // A/B stages in the ring (3..TC_NST_MAX)
     int chain;                  // K stages per TMEM accumulation chain
-    int v_stride;               // float4 elements per V buffer
 };
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -113,21 +130,107 @@ __device__ __forceinline__ TcTile tc_tile(const TcGeom& g, int64_t t) {
     return r;
 }
 
+// Producer-side state of the A stage ring: the current (open) stage's ring
+// slot and phase, and the next free K position inside it.
+struct ARing {
+    uint32_t st, ph, kpos;
+};
+
+// Ring slot / phase `i` stages ahead of the current one (i < nst).
+__device__ __forceinline__ void ring_ahead(const ARing& r, uint32_t i, uint32_t nst, uint32_t& s, uint32_t& ph) {
+    s = r.st + i;
+    ph = r.ph;
+    if (s >= nst) {
+        s -= nst;
+        ph ^= 1u;
+    }
+}
+
+// One column of one tile for the producer thread (row, c parity h): mode 2
+// (W[row, c] = x_j sum_b V[i1, b, c] U2[i2, b] for c = 2u + h) and the
+// 3xTF32 hi/lo split of W into its K slots of the A ring.  NU = ceil(r3/2).
+// All lanes of a producer warp share i1 (lane = i2), so the V operand of
+// each FFMA2 is a warp-uniform shared-memory broadcast.
+template <int NU>
+__device__ __forceinline__ void tc_produce_column(const float4* __restrict__ V, const float2* __restrict__ U2, int r2,
+                                                  int ld2, int r3, int h, float2 xj, uint64_t* fempty_s,
+                                                  uint64_t* empty, uint64_t* full, unsigned char* sA,
+                                                  uint32_t rowbase, uint32_t xorv, int lane, uint32_t nst,
+                                                  ARing& ring) {
+    using namespace sm100;
+    uint64_t w[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) w[u] = 0;
+    // V[(b + r2 c) * 4 + il]: c = 2u + h  ->  stride 8 r2 float4 per u
+    const float4* vp = V + 4 * r2 * h;
+    const float2* up = U2 + lane * ld2;
+    for (int b = 0; b < r2; ++b) {
+        const float2 ub = up[b];
+#pragma unroll
+        for (int u = 0; u < NU; ++u)
+            if (u < NU - 1 || 2 * u + h < r3) cfma2(w[u], vp[4 * b + 8 * r2 * u], ub);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(fempty_s);  // this warp no longer reads the slot
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        const float2 v = cmul(f2_unpack(w[u]), xj);
+        w[u] = f2_pack(v.x, v.y);
+    }
+    // wait for every stage this column opens, write, close completed stages
+    const uint32_t kend = ring.kpos + uint32_t(r3);
+    const uint32_t ns = (kend + 7) >> 3;
+    for (uint32_t i = ring.kpos == 0 ? 0u : 1u; i < ns; ++i) {
+        uint32_t s, ph;
+        ring_ahead(ring, i, nst, s, ph);
+        mbar_wait(&empty[s], ph ^ 1u);
+    }
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        const int c = 2 * u + h;
+        if (u < NU - 1 || c < r3) {
+            const uint32_t K = ring.kpos + uint32_t(c);
+            uint32_t s, ph;
+            ring_ahead(ring, K >> 3, nst, s, ph);
+            const float2 wv = f2_unpack(w[u]);
+            const float hr = __uint_as_float(__float_as_uint(wv.x) & 0xFFFFE000u);
+            const float hi = __uint_as_float(__float_as_uint(wv.y) & 0xFFFFE000u);
+            float* a = reinterpret_cast<float*>(sA + s * TC_A_STAGE + rowbase + (((K & 7u) * 4u) ^ xorv));
+            a[0] = hr;
+            a[TC_A_PLANE / 4] = wv.x - hr;
+            a[2 * TC_A_PLANE / 4] = hi;
+            a[3 * TC_A_PLANE / 4] = wv.y - hi;
+        }
+    }
+    const uint32_t nc = kend >> 3;  // stages completed by this column
+    if (nc) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0)
+            for (uint32_t i = 0; i < nc; ++i) {
+                uint32_t s, ph;
+                ring_ahead(ring, i, nst, s, ph);
+                mbar_arrive(&full[s]);
+            }
+        ring_ahead(ring, nc, nst, ring.st, ring.ph);
+    }
+    ring.kpos = kend & 7u;
+}
+
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    fwd_tc_kernel(const __grid_constant__ CUtensorMap bmap, const TDesc* __restrict__ td,
-                  const float2* __restrict__ arena, const int* __restrict__ kc, TcGeom g,
-                  const float2* __restrict__ x, int64_t ldx, float2* __restrict__ y, int64_t ldy) {
+    fwd_tc_kernel(const __grid_constant__ CUtensorMap bmap, const TcDesc* __restrict__ tcd,
+                  const float4* __restrict__ varena, const float2* __restrict__ u2arena, const int* __restrict__ kc,
+                  TcGeom g, const float2* __restrict__ x, int64_t ldx, float2* __restrict__ y, int64_t ldy) {
     using namespace sm100;
     extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
     // align to 1024 B by offsetting the shared array itself (keeps the
     // shared address space visible to the compiler: LDS/STS, not generic)
     unsigned char* sm = tc_smem_raw + ((1024u - (smem_u32(tc_smem_raw) & 1023u)) & 1023u);
-    const int nst = g.nst;
+    const uint32_t nst = uint32_t(g.nst);
     unsigned char* sA = sm;
     unsigned char* sB = sA + nst * TC_A_STAGE;
     unsigned char* sSlot = sB + nst * g.b_stage;
-    float4* sV = reinterpret_cast<float4*>(sSlot + TC_JR * g.slot_bytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * g.v_stride);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sSlot + TC_JR * g.slot_bytes);
     uint64_t* full = bars;                 // [nst]
     uint64_t* empty = full + TC_NST_MAX;   // [nst]
     uint64_t* ffull = empty + TC_NST_MAX;  // [JR]
@@ -138,7 +241,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < nst; ++s) {
+        for (uint32_t s = 0; s < nst; ++s) {
             mbar_init(&full[s], 1 + TC_NPW);
             mbar_init(&empty[s], 1);
         }
@@ -160,65 +263,70 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (warp == 0) {
         // ------------------------------------------------ B-plane TMA producer
         if (elect_one()) {
-            uint32_t ks = 0;
-            const int plane_bytes = g.b_stage / 4;
+            uint32_t s = 0, ph = 0;
+            const int plane_bytes = g.b_stage / TC_BPLANES;
             for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
                 const TcTile tl = tc_tile(g, t);
                 const int nks = (kc[tl.k] + 7) >> 3;
-                for (int kk = 0; kk < nks; ++kk, ++ks) {
-                    const uint32_t s = ks % nst, ph = (ks / nst) & 1;
+                for (int kk = 0; kk < nks; ++kk) {
                     mbar_wait(&empty[s], ph ^ 1);
                     mbar_arrive_expect_tx(&full[s], uint32_t(g.b_stage));
                     unsigned char* dst = sB + s * g.b_stage;
 #pragma unroll
-                    for (int pl = 0; pl < 4; ++pl)
+                    for (int pl = 0; pl < TC_BPLANES; ++pl)
                         tma_load_3d(dst + pl * plane_bytes, &bmap, &full[s], kk * 8, tl.i3_0, pl * g.q + tl.k);
+                    if (++s == nst) {
+                        s = 0;
+                        ph ^= 1;
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer
         if (elect_one()) {
-            const uint32_t id_pp = umma_idesc_tf32(TC_ROWS, g.nmma, false, false);
-            const uint32_t id_np = umma_idesc_tf32(TC_ROWS, g.nmma, true, false);
-            const int plane_b = g.b_stage / 4;
-            const uint32_t yr = tmem, yi = tmem + TC_NMAX;
-            uint32_t ks = 0, gch = 0;
+            // complex product as one real GEMM of width 2 NMMA:
+            //   [Yr | Yi] += Ar . [U3r | U3i] + Ai . [-U3i | U3r]
+            // with the B planes staged [-U3i][U3r][U3i] (hi) and the same
+            // (lo), so both operands are contiguous 2-plane windows.
+            const uint32_t idesc = umma_idesc_tf32(TC_ROWS, 2 * g.nmma, false, false);
+            const int plane_b = g.b_stage / TC_BPLANES;
+            const uint32_t yd = tmem;
+            uint32_t s = 0, ph = 0, gch = 0;
             for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
                 const TcTile tl = tc_tile(g, t);
                 const int nks = (kc[tl.k] + 7) >> 3;
                 int cpos = 0;  // stage position inside the current chain
-                for (int kk = 0; kk < nks; ++kk, ++ks) {
+                for (int kk = 0; kk < nks; ++kk) {
                     if (cpos == 0) {
                         mbar_wait(cfree, (gch & 1) ^ 1);  // the previous chain has been folded
                         tc_fence_after();
                     }
-                    const uint32_t s = ks % nst, ph = (ks / nst) & 1;
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + s * TC_A_STAGE);
                     const uint32_t b0 = smem_u32(sB + s * g.b_stage);
-                    uint64_t A[4], B[4];
+                    // A planes: 0 = re hi, 1 = re lo, 2 = im hi, 3 = im lo
+                    uint64_t A[4];
 #pragma unroll
-                    for (int pl = 0; pl < 4; ++pl) {
-                        A[pl] = umma_smem_desc(a0 + pl * TC_A_PLANE, 256, 6);
-                        B[pl] = umma_smem_desc(b0 + pl * plane_b, 256, 6);
-                    }
+                    for (int pl = 0; pl < 4; ++pl) A[pl] = umma_smem_desc(a0 + pl * TC_A_PLANE, 256, 6);
+                    // B windows: hi [U3r|U3i] at plane 1, [-U3i|U3r] at plane 0; lo at +3
+                    const uint64_t B1h = umma_smem_desc(b0 + 1 * plane_b, 256, 6);
+                    const uint64_t B2h = umma_smem_desc(b0 + 0 * plane_b, 256, 6);
+                    const uint64_t B1l = umma_smem_desc(b0 + 4 * plane_b, 256, 6);
+                    const uint64_t B2l = umma_smem_desc(b0 + 3 * plane_b, 256, 6);
                     const uint32_t acc = cpos > 0 ? 1u : 0u;
-                    // planes: 0 = re hi, 1 = re lo, 2 = im hi, 3 = im lo
-                    mma_tf32(yr, A[0], B[0], id_pp, acc);
-                    mma_tf32(yr, A[0], B[1], id_pp, 1);
-                    mma_tf32(yr, A[1], B[0], id_pp, 1);
-                    mma_tf32(yr, A[2], B[2], id_np, 1);
-                    mma_tf32(yr, A[2], B[3], id_np, 1);
-                    mma_tf32(yr, A[3], B[2], id_np, 1);
-                    mma_tf32(yi, A[0], B[2], id_pp, acc);
-                    mma_tf32(yi, A[0], B[3], id_pp, 1);
-                    mma_tf32(yi, A[1], B[2], id_pp, 1);
-                    mma_tf32(yi, A[2], B[0], id_pp, 1);
-                    mma_tf32(yi, A[2], B[1], id_pp, 1);
-                    mma_tf32(yi, A[3], B[0], id_pp, 1);
+                    mma_tf32(yd, A[0], B1h, idesc, acc);
+                    mma_tf32(yd, A[0], B1l, idesc, 1);
+                    mma_tf32(yd, A[1], B1h, idesc, 1);
+                    mma_tf32(yd, A[2], B2h, idesc, 1);
+                    mma_tf32(yd, A[2], B2l, idesc, 1);
+                    mma_tf32(yd, A[3], B2h, idesc, 1);
                     mma_commit(&empty[s]);
+                    if (++s == nst) {
+                        s = 0;
+                        ph ^= 1;
+                    }
                     if (++cpos == g.chain || kk == nks - 1) {
                         mma_commit(cfull);
                         cpos = 0;
@@ -231,127 +339,85 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     } else if (warp == 2) {
         // ---------------------------------------------------- factor loader
         if (elect_one()) {
-            uint32_t jc = 0;
+            uint32_t s = 0, ph = 0;
             for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
                 const TcTile tl = tc_tile(g, t);
-                const TDesc* tdk = td + int64_t(tl.k) * g.ncols;
-                for (int64_t j = 0; j < g.ncols; ++j, ++jc) {
-                    const uint32_t s = jc % TC_JR, ph = (jc / TC_JR) & 1;
+                const TcDesc* tdk = tcd + int64_t(tl.k) * g.ncols;
+                for (int64_t j = 0; j < g.ncols; ++j) {
                     mbar_wait(&fempty[s], ph ^ 1);
-                    const TDesc d = tdk[j];
+                    const TcDesc d = tdk[j];
                     unsigned char* slot = sSlot + s * g.slot_bytes;
-                    const uint32_t bg = round16(uint32_t(d.r1 * d.r2 * d.r3) * 8u);
-                    const uint32_t b1 = uint32_t(TC_TI1 * d.r1) * 8u;
-                    const uint32_t b2 = uint32_t(TC_TI2 * d.r2) * 8u;
-                    mbar_arrive_expect_tx(&ffull[s], uint32_t(sizeof(TDesc)) + bg + b1 + b2);
-                    bulk_g2s(slot, tdk + j, uint32_t(sizeof(TDesc)), &ffull[s]);
-                    bulk_g2s(slot + g.g_off, arena + d.off_core, bg, &ffull[s]);
-                    bulk_g2s(slot + g.u1_off, arena + d.off_u1 + int64_t(tl.i1_0) * d.r1, b1, &ffull[s]);
-                    bulk_g2s(slot + g.u2_off, arena + d.off_u2 + int64_t(tl.i2_0) * d.r2, b2, &ffull[s]);
+                    const uint32_t r23 = uint32_t(d.r2 * d.r3);
+                    const uint32_t ld2 = uint32_t(d.r2 | 1);
+                    const uint32_t bv = uint32_t(TC_TI1) * r23 * 16u;
+                    const uint32_t b2 = uint32_t(TC_TI2) * ld2 * 8u;
+                    mbar_arrive_expect_tx(&ffull[s], uint32_t(sizeof(TcDesc)) + bv + b2);
+                    bulk_g2s(slot, tdk + j, uint32_t(sizeof(TcDesc)), &ffull[s]);
+                    bulk_g2s(slot + TC_SLOT_V, varena + d.off_v + int64_t(tl.i1_0) * r23, bv, &ffull[s]);
+                    bulk_g2s(slot + g.u2_off, u2arena + d.off_u2 + int64_t(tl.i2_0) * ld2, b2, &ffull[s]);
+                    if (++s == TC_JR) {
+                        s = 0;
+                        ph ^= 1;
+                    }
                 }
             }
         }
     } else if (warp >= TC_PW0 && warp < TC_FW0) {
         // ------------------------------------------------------ A producers
-        const int pt = threadIdx.x - TC_PW0 * 32;  // 0..255
-        const int row = pt & (TC_ROWS - 1);
-        const int h = pt >> 7;                      // c parity handled by this thread
-        const int i1l = row & (TC_TI1 - 1), i2l = row / TC_TI1;
-        uint32_t ks = 0, jc = 0;
+        // warp pw: i1 = pw & 3 (warp-uniform), c parity h = pw >> 2, lane = i2;
+        // tile row = i2 + 32 i1 (= TMEM lane of the accumulator)
+        const int pw = warp - TC_PW0;
+        const int i1l = pw & (TC_TI1 - 1), h = pw >> 2;
+        const int row = lane + 32 * i1l;
+        const uint32_t rowbase = uint32_t(row) * 32u, xorv = (uint32_t(row) & 4u) << 2;
+        ARing ring{0, 0, 0};
+        uint32_t fs = 0, fph = 0;
         for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
             const TcTile tl = tc_tile(g, t);
-            const bool row_ok = (tl.i1_0 + i1l < g.n1) && (tl.i2_0 + i2l < g.n2);
             const float2* xc = x + ldx * tl.c;
-            uint32_t kpos = 0;  // K slot inside the current stage
-            for (int64_t j = 0; j < g.ncols; ++j, ++jc) {
-                const uint32_t s = jc % TC_JR, ph = (jc / TC_JR) & 1;
+            for (int64_t j = 0; j < g.ncols; ++j) {
                 const float2 xj = xc[j];
-                mbar_wait(&ffull[s], ph);
-                const unsigned char* slot = sSlot + s * g.slot_bytes;
-                const TDesc d = *reinterpret_cast<const TDesc*>(slot);
-                const float2* G = reinterpret_cast<const float2*>(slot + g.g_off);
-                const float2* U1 = reinterpret_cast<const float2*>(slot + g.u1_off);
+                mbar_wait(&ffull[fs], fph);
+                const unsigned char* slot = sSlot + fs * g.slot_bytes;
+                const int r2 = reinterpret_cast<const TcDesc*>(slot)->r2;
+                const int r3 = reinterpret_cast<const TcDesc*>(slot)->r3;
+                const float4* V = reinterpret_cast<const float4*>(slot + TC_SLOT_V) + i1l;
                 const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
-                const int r1 = d.r1, r2 = d.r2, r3 = d.r3;
-                float4* V = sV + (jc & 1) * g.v_stride;
-                // mode 1 (+ x_j): V[(b + r2 c) * 4 + i1l] = x_j sum_a U1[i1l][a] G[a + r1 (b + r2 c)],
-                // stored as (vr, vi, -vi, vr) for the FFMA2 mode-2 product
-                const int nv = TC_TI1 * r2 * r3;
-                for (int e = pt; e < nv; e += TC_NPW * 32) {
-                    const int il = e & (TC_TI1 - 1), bc = e >> 2;
-                    const float2* gp = G + r1 * bc;
-                    const float2* up = U1 + il * r1;
-                    float2 acc = make_float2(0.f, 0.f);
-                    for (int a = 0; a < r1; ++a) cfma(acc, up[a], gp[a]);
-                    const float2 v = cmul(acc, xj);
-                    V[e] = make_float4(v.x, v.y, -v.y, v.x);
+#define TC_COL(NU)                                                                                              \
+    tc_produce_column<NU>(V, U2, r2, r2 | 1, r3, h, xj, &fempty[fs], empty, full, sA, rowbase, xorv, lane, nst, \
+                          ring)
+                switch ((r3 + 1) >> 1) {
+                    case 1: TC_COL(1); break;
+                    case 2: TC_COL(2); break;
+                    case 3: TC_COL(3); break;
+                    case 4: TC_COL(4); break;
+                    case 5: TC_COL(5); break;
+                    case 6: TC_COL(6); break;
+                    case 7: TC_COL(7); break;
+                    default: TC_COL(8); break;
                 }
-                // my row of U2 into registers
-                float2 u2[TC_RMAX];
-#pragma unroll
-                for (int b = 0; b < TC_RMAX; ++b) u2[b] = b < r2 ? U2[i2l * r2 + b] : make_float2(0.f, 0.f);
-                named_bar_sync(1, TC_NPW * 32);  // V complete; the slot is no longer read
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&fempty[s]);
-                // mode 2 for c = 2u + h: W[row, c] = sum_b V[i1l, b, c] U2[i2l, b]
-                uint64_t w[TC_RMAX / 2];
-#pragma unroll
-                for (int u = 0; u < TC_RMAX / 2; ++u) {
-                    const int c = 2 * u + h;
-                    w[u] = 0;
-                    if (c < r3) {
-                        const float4* vp = V + r2 * c * 4 + i1l;
-#pragma unroll
-                        for (int b = 0; b < TC_RMAX; ++b)
-                            if (b < r2) cfma2(w[u], vp[b * 4], u2[b]);
-                    }
-                    if (!row_ok) w[u] = 0;
-                }
-                // scatter into the K stream (uniform stage bookkeeping)
-#pragma unroll
-                for (int c = 0; c < TC_RMAX; ++c) {
-                    if (c < r3) {
-                        const uint32_t st = ks % nst;
-                        if (kpos == 0) mbar_wait(&empty[st], ((ks / nst) & 1) ^ 1);
-                        if ((c & 1) == h) {
-                            const float2 wv = f2_unpack(w[c >> 1]);
-                            const float hr = __uint_as_float(__float_as_uint(wv.x) & 0xFFFFE000u);
-                            const float hi = __uint_as_float(__float_as_uint(wv.y) & 0xFFFFE000u);
-                            unsigned char* a = sA + st * TC_A_STAGE + sw_offset(row, kpos, 32);
-                            *reinterpret_cast<float*>(a) = hr;
-                            *reinterpret_cast<float*>(a + TC_A_PLANE) = wv.x - hr;
-                            *reinterpret_cast<float*>(a + 2 * TC_A_PLANE) = hi;
-                            *reinterpret_cast<float*>(a + 3 * TC_A_PLANE) = wv.y - hi;
-                        }
-                        if (++kpos == 8) {
-                            fence_proxy_async_smem();
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive(&full[st]);
-                            kpos = 0;
-                            ++ks;
-                        }
-                    }
+#undef TC_COL
+                if (++fs == TC_JR) {
+                    fs = 0;
+                    fph ^= 1;
                 }
             }
-            if (kpos != 0) {  // zero the tail of the last stage and close it
-                const uint32_t st = ks % nst;
+            if (ring.kpos != 0) {  // zero the tail of the last stage and close it
                 if (h == 0)
-                    for (uint32_t kq = kpos; kq < 8; ++kq) {
-                        unsigned char* a = sA + st * TC_A_STAGE + sw_offset(row, kq, 32);
+                    for (uint32_t kq = ring.kpos; kq < 8; ++kq) {
+                        float* a = reinterpret_cast<float*>(sA + ring.st * TC_A_STAGE + rowbase + ((kq * 4u) ^ xorv));
 #pragma unroll
-                        for (int pl = 0; pl < 4; ++pl) *reinterpret_cast<float*>(a + pl * TC_A_PLANE) = 0.f;
+                        for (int pl = 0; pl < 4; ++pl) a[pl * TC_A_PLANE / 4] = 0.f;
                     }
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&full[st]);
-                kpos = 0;
-                ++ks;
+                if (lane == 0) mbar_arrive(&full[ring.st]);
+                ring_ahead(ring, 1, nst, ring.st, ring.ph);
+                ring.kpos = 0;
             }
         }
     } else if (warp >= TC_FW0) {
-        // ------------------------------------------ chain fold + epilogue
         const int quarter = warp & 3;             // TMEM lane quarter
-        const int erow = quarter * 32 + lane;     // TMEM lane = tile row
         const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
         const uint32_t tC = tmem + lane_addr, tR = tmem + lane_addr + TC_RUN_COL;
         const int64_t nv3 = int64_t(g.n1) * g.n2 * g.n3;
@@ -360,7 +426,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const TcTile tl = tc_tile(g, t);
             const int nks = (kc[tl.k] + 7) >> 3;
             const int nch = (nks + g.chain - 1) / g.chain;
-            const int ei1 = tl.i1_0 + (erow & (TC_TI1 - 1)), ei2 = tl.i2_0 + erow / TC_TI1;
+            const int ei1 = tl.i1_0 + quarter, ei2 = tl.i2_0 + lane;  // row = i2 + 32 i1
             const bool eok = ei1 < g.n1 && ei2 < g.n2;
             float2* yp = y + ldy * tl.c + int64_t(tl.k) * nv3 + ei1 + int64_t(g.n1) * ei2;
             const int64_t pl = int64_t(g.n1) * g.n2;
@@ -371,11 +437,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 for (int cb = 0; cb < g.nmma; cb += 16) {
                     uint32_t cr[16], ci[16];
                     tmem_ld16(tC + uint32_t(cb), cr);
-                    tmem_ld16(tC + uint32_t(TC_NMAX + cb), ci);
+                    tmem_ld16(tC + uint32_t(g.nmma + cb), ci);
                     if (ch > 0) {
                         uint32_t rr[16], ri[16];
                         tmem_ld16(tR + uint32_t(cb), rr);
-                        tmem_ld16(tR + uint32_t(TC_NMAX + cb), ri);
+                        tmem_ld16(tR + uint32_t(g.nmma + cb), ri);
                         tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
@@ -387,7 +453,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     }
                     if (!last) {
                         tmem_st16(tR + uint32_t(cb), cr);
-                        tmem_st16(tR + uint32_t(TC_NMAX + cb), ci);
+                        tmem_st16(tR + uint32_t(g.nmma + cb), ci);
                     } else if (eok) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
@@ -409,8 +475,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (warp == 3) tmem_dealloc(tmem, 512);
 }
 
+// ------------------------------------------------- store-side V arena (K6'')
+// V_t[i1][b][c] = sum_a U1t[i1][a] G[a + r1 (b + r2 c)] for every tensor t
+// (the reference's mode-1 product, src/tensor.cpp:106-108, done once per
+// store instead of once per tile), accumulated in fp64 from the c64 factors
+// and stored [i1/4][b + r2 c][i1 % 4] as (vr, vi, -vi, vr); rows i1 >= n1 of
+// the last group of four are zero.
+__global__ void build_v_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena,
+                               const TcDesc* __restrict__ tcd, int n1, float4* __restrict__ varena) {
+    const int64_t t = blockIdx.x;
+    const TDesc d = td[t];
+    const int r23 = d.r2 * d.r3;
+    const int n1p = (n1 + 3) & ~3;
+    float4* out = varena + tcd[t].off_v;
+    for (int e = threadIdx.x; e < n1p * r23; e += blockDim.x) {
+        const int i1 = e / r23, bc = e - i1 * r23;
+        double vr = 0.0, vi = 0.0;
+        if (i1 < n1) {
+            const float2* u = arena + d.off_u1 + int64_t(i1) * d.r1;
+            const float2* gp = arena + d.off_core + int64_t(bc) * d.r1;
+            for (int a = 0; a < d.r1; ++a) {
+                const float2 ua = u[a], ga = gp[a];
+                vr += double(ua.x) * ga.x - double(ua.y) * ga.y;
+                vi += double(ua.x) * ga.y + double(ua.y) * ga.x;
+            }
+        }
+        const float fr = float(vr), fi = float(vi);
+        out[int64_t(i1 >> 2) * 4 * r23 + int64_t(bc) * 4 + (i1 & 3)] = make_float4(fr, fi, -fi, fr);
+    }
+}
+
 // ------------------------------------------------- store-side B planes (K6')
-// planes[p][k][i3][K], K = kofs[k][j] + r:  p = 0 re hi, 1 re lo, 2 im hi, 3 im lo.
+// planes[p][k][i3][K], K = kofs[k][j] + r, in the order
+//   0: -U3i hi, 1: U3r hi, 2: U3i hi, 3: -U3i lo, 4: U3r lo, 5: U3i lo
+// (hi = tf32(x), lo = tf32(x - hi)), so that the windows [U3r | U3i] and
+// [-U3i | U3r] of two consecutive planes are the B operands of the
+// complex-as-real forward MMA.
 __global__ void build_bplanes_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena,
                                      const int* __restrict__ kofs, int64_t ncols, int q, int n3, int64_t kpad,
                                      float* __restrict__ planes) {
@@ -423,11 +523,30 @@ __global__ void build_bplanes_kernel(const TDesc* __restrict__ td, const float2*
         const int i3 = e / d.r3, r = e - i3 * d.r3;
         const float2 u = arena[d.off_u3 + e];
         const float rh = sm100::tf32_round(u.x), ih = sm100::tf32_round(u.y);
+        const float rl = sm100::tf32_round(u.x - rh), il = sm100::tf32_round(u.y - ih);
         const int64_t o = (int64_t(k) * n3 + i3) * kpad + k0 + r;
-        planes[o] = rh;
-        planes[plane + o] = sm100::tf32_round(u.x - rh);
+        planes[o] = -ih;
+        planes[plane + o] = rh;
         planes[2 * plane + o] = ih;
-        planes[3 * plane + o] = sm100::tf32_round(u.y - ih);
+        planes[3 * plane + o] = -il;
+        planes[4 * plane + o] = rl;
+        planes[5 * plane + o] = il;
+    }
+}
+
+// ------------------------------------------------ store-side U2 arena (K6 U2)
+// U2 of every tensor with an odd row stride r2 | 1 and n2 rounded up to TI2
+// rows (the padding rows and columns are zero).
+__global__ void build_u2_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena,
+                                const TcDesc* __restrict__ tcd, int n2, float2* __restrict__ u2arena) {
+    const int64_t t = blockIdx.x;
+    const TDesc d = td[t];
+    const int ld2 = d.r2 | 1;
+    const int n2p = (n2 + TC_TI2 - 1) / TC_TI2 * TC_TI2;
+    float2* out = u2arena + tcd[t].off_u2;
+    for (int e = threadIdx.x; e < n2p * ld2; e += blockDim.x) {
+        const int i2 = e / ld2, b = e - i2 * ld2;
+        out[e] = (i2 < n2 && b < d.r2) ? arena[d.off_u2 + int64_t(i2) * d.r2 + b] : make_float2(0.f, 0.f);
     }
 }
 
