@@ -1,0 +1,414 @@
+// Tensor-core (tcgen05, kind::tf32, 3xTF32 split) adjoint kernel, complex64.
+//
+// The reference's stacked_adjoint (src/matvec.cpp:67-102) forms, per column
+// j and component k, z_j += vec(T_jk)^H Phi_k.  With T_jk[row, i3] =
+// sum_c W_j[row, c] U3_j[i3, c] (row = (i1, i2), W as in the forward) this is
+//
+//   z_j = sum_rows sum_c conj(W_j[row, c]) Q[row, (j, c)],
+//   Q[row, (j, c)] = sum_i3 Phi[row, i3] conj(U3_j[i3, c]),
+//
+// i.e. one GEMM per 128-row tile, M = rows, K = i3 (all n3), N = the (j, c)
+// slots of component k in chunks of 128 (whole columns per chunk, zero
+// padded), followed by a per-column contraction with conj(W).  The complex
+// product runs as one real GEMM of width 256:
+//   [Qi | Qr] += Phir . [-U3i | U3r] + Phii . [U3r | U3i]
+// with the B planes staged [-U3i][U3r][U3i] (hi and lo, i3-contiguous
+// chunk-aligned copy built once per store) and the A planes the 3xTF32
+// split of the Phi tile (built per call by adj_split_phi_kernel).  Both
+// operands arrive by TMA; Q is accumulated in TMEM (two 256-column buffers,
+// ping-pong over chunks).
+//
+// Warp roles (512 threads, 1 CTA / SM, persistent over row tiles):
+//   warp 0      TMA producer of the A (Phi) and B (U3) planes
+//   warp 1      MMA issuer
+//   warp 2      factor loader (TcDesc, V rows, U2 rows per column)
+//   warp 3      TMEM allocator
+//   warps 4-11  consumers: per column, W = V x_2 U2 for the tile rows
+//               (FFMA2), Q from TMEM, conj(W) . Q, warp-shuffle reduction
+//               over the 32 rows of the warp, fixed-order sum over the 8
+//               warps -> one partial z_j per (tile, component)
+// A second kernel (adj_reduce_kernel) sums the partials in a fixed order,
+// so results are bitwise reproducible.
+#pragma once
+
+#include "tm_common.cuh"
+#include "tm_kernels_tc.cuh"
+#include "tm_sm100.cuh"
+
+namespace tmb {
+
+constexpr int AJ_NST = 4;        // A/B stages (8 i3 each)
+constexpr int AJ_CH = 128;       // (j, c) slots per chunk
+constexpr int AJ_APLANES = 4;    // Phi planes: re hi, re lo, im hi, im lo
+constexpr int AJ_A_PLANE = TC_ROWS * 32;
+constexpr int AJ_A_STAGE = AJ_APLANES * AJ_A_PLANE;       // 16 KB
+constexpr int AJ_B_PLANE = AJ_CH * 32;
+constexpr int AJ_B_STAGE = TC_BPLANES * AJ_B_PLANE;       // 24 KB
+constexpr int AJ_MAXCOLS = 128;  // columns per chunk (r3 >= 1)
+
+struct AjGeom {
+    int64_t ncols;
+    int n1, n2, n3, q;
+    int nt1, nt2;
+    int p;
+    int64_t nrt;     // row tiles per component
+    int64_t ntiles;  // p * q * nrt
+    int nks;         // K steps (8 i3 each) per chunk
+    int rmax2, rmax3;
+    int slot_bytes, u2_off;
+    int maxch;       // chunk stride of the chunk-start table
+};
+
+struct AjTile {
+    int c, k, i1_0, i2_0;
+    int64_t rt;  // row tile inside the component
+};
+
+__device__ __forceinline__ AjTile aj_tile(const AjGeom& g, int64_t t) {
+    AjTile r;
+    const int64_t per_c = int64_t(g.q) * g.nrt;
+    r.c = int(t / per_c);
+    int64_t rem = t - int64_t(r.c) * per_c;
+    r.k = int(rem / g.nrt);
+    r.rt = rem - int64_t(r.k) * g.nrt;
+    const int t2 = int(r.rt / g.nt1), t1 = int(r.rt - int64_t(t2) * g.nt1);
+    r.i1_0 = t1 * TC_TI1;
+    r.i2_0 = t2 * TC_TI2;
+    return r;
+}
+
+// One column of a chunk for the consumer thread (row = lane + 32 il, c parity
+// h): W = V x_2 U2 (no x_j in the adjoint), Q[row, soff + c] from TMEM, and
+// the partial sum_c conj(W) Q of this thread's row.
+template <int NU>
+__device__ __forceinline__ float2 aj_consume_column(const float4* __restrict__ V, const float2* __restrict__ U2,
+                                                    int r2, int ld2, int r3, int h, int lane, uint32_t qaddr,
+                                                    uint64_t* fempty_s) {
+    using namespace sm100;
+    uint64_t w[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) w[u] = 0;
+    const float4* vp = V + 4 * r2 * h;
+    const float2* up = U2 + lane * ld2;
+    for (int b = 0; b < r2; ++b) {
+        const float2 ub = up[b];
+#pragma unroll
+        for (int u = 0; u < NU; ++u)
+            if (u < NU - 1 || 2 * u + h < r3) cfma2(w[u], vp[4 * b + 8 * r2 * u], ub);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(fempty_s);
+    // Q columns: Qi at qaddr + s, Qr at qaddr + AJ_CH + s
+    uint32_t qi[NU], qr[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        // (a slot past this column's last c reads slot 0 and is ignored: it
+        // may lie past the end of the TMEM allocation)
+        const uint32_t s = (u < NU - 1 || 2 * u + h < r3) ? uint32_t(2 * u + h) : 0u;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(qi[u]) : "r"(qaddr + s));
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(qr[u]) : "r"(qaddr + AJ_CH + s));
+    }
+    tmem_ld_wait();
+    float ar = 0.f, ai = 0.f;
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        if (u < NU - 1 || 2 * u + h < r3) {
+            const float2 wv = f2_unpack(w[u]);
+            const float qre = __uint_as_float(qr[u]), qim = __uint_as_float(qi[u]);
+            // conj(W) Q = (Wr Qr + Wi Qi) + i (Wr Qi - Wi Qr)
+            ar = fmaf(wv.x, qre, fmaf(wv.y, qim, ar));
+            ai = fmaf(wv.x, qim, fmaf(-wv.y, qre, ai));
+        }
+    }
+    return make_float2(ar, ai);
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    adj_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                  const TcDesc* __restrict__ tcd, const float4* __restrict__ varena,
+                  const float2* __restrict__ u2arena, const int* __restrict__ nch, const int* __restrict__ cstart,
+                  AjGeom g, float2* __restrict__ part) {
+    using namespace sm100;
+    extern __shared__ __align__(1024) unsigned char aj_smem_raw[];
+    unsigned char* sm = aj_smem_raw + ((1024u - (smem_u32(aj_smem_raw) & 1023u)) & 1023u);
+    unsigned char* sA = sm;
+    unsigned char* sB = sA + AJ_NST * AJ_A_STAGE;
+    unsigned char* sSlot = sB + AJ_NST * AJ_B_STAGE;
+    float2* red = reinterpret_cast<float2*>(sSlot + TC_JR * g.slot_bytes);  // [2][AJ_MAXCOLS][8]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * AJ_MAXCOLS * TC_NPW);
+    uint64_t* full = bars;                // [NST]
+    uint64_t* empty = full + AJ_NST;      // [NST]
+    uint64_t* ffull = empty + AJ_NST;     // [JR]
+    uint64_t* fempty = ffull + TC_JR;     // [JR]
+    uint64_t* qfull = fempty + TC_JR;     // [2]
+    uint64_t* qfree = qfull + 2;          // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qfree + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < AJ_NST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < TC_JR; ++s) {
+            mbar_init(&ffull[s], 1);
+            mbar_init(&fempty[s], TC_NPW);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&qfull[s], 1);
+            mbar_init(&qfree[s], TC_NPW);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 3) tmem_alloc(tmem_slot, 512);
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&amap);
+        tma_prefetch_desc(&bmap);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------- TMA producer
+        if (elect_one()) {
+            uint32_t s = 0, ph = 0;
+            for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+                const AjTile tl = aj_tile(g, t);
+                const int nc = nch[tl.k];
+                const int arow = int(tl.rt * TC_ROWS);
+                for (int n = 0; n < nc; ++n) {
+                    for (int kk = 0; kk < g.nks; ++kk) {
+                        mbar_wait(&empty[s], ph ^ 1);
+                        mbar_arrive_expect_tx(&full[s], uint32_t(AJ_A_STAGE + AJ_B_STAGE));
+                        unsigned char* da = sA + s * AJ_A_STAGE;
+                        unsigned char* db = sB + s * AJ_B_STAGE;
+#pragma unroll
+                        for (int pl = 0; pl < AJ_APLANES; ++pl)
+                            tma_load_3d(da + pl * AJ_A_PLANE, &amap, &full[s], kk * 8, arow,
+                                        (pl * g.p + tl.c) * g.q + tl.k);
+#pragma unroll
+                        for (int pl = 0; pl < TC_BPLANES; ++pl)
+                            tma_load_3d(db + pl * AJ_B_PLANE, &bmap, &full[s], kk * 8, n * AJ_CH, pl * g.q + tl.k);
+                        if (++s == AJ_NST) {
+                            s = 0;
+                            ph ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------- MMA issuer
+        if (elect_one()) {
+            const uint32_t idesc = umma_idesc_tf32(TC_ROWS, 2 * AJ_CH, false, false);
+            uint32_t s = 0, ph = 0, nq = 0;
+            for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+                const AjTile tl = aj_tile(g, t);
+                const int nc = nch[tl.k];
+                for (int n = 0; n < nc; ++n, ++nq) {
+                    const uint32_t qb = nq & 1, qph = (nq >> 1) & 1;
+                    mbar_wait(&qfree[qb], qph ^ 1);  // consumers are done with this buffer
+                    tc_fence_after();
+                    const uint32_t qd = tmem + qb * 256u;
+                    for (int kk = 0; kk < g.nks; ++kk) {
+                        mbar_wait(&full[s], ph);
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(sA + s * AJ_A_STAGE);
+                        const uint32_t b0 = smem_u32(sB + s * AJ_B_STAGE);
+                        uint64_t A[4];
+#pragma unroll
+                        for (int pl = 0; pl < 4; ++pl) A[pl] = umma_smem_desc(a0 + pl * AJ_A_PLANE, 256, 6);
+                        // B windows: [-U3i|U3r] at plane 0 / 3 (hi / lo), [U3r|U3i] at plane 1 / 4
+                        const uint64_t B2h = umma_smem_desc(b0 + 0 * AJ_B_PLANE, 256, 6);
+                        const uint64_t B1h = umma_smem_desc(b0 + 1 * AJ_B_PLANE, 256, 6);
+                        const uint64_t B2l = umma_smem_desc(b0 + 3 * AJ_B_PLANE, 256, 6);
+                        const uint64_t B1l = umma_smem_desc(b0 + 4 * AJ_B_PLANE, 256, 6);
+                        const uint32_t acc = kk > 0 ? 1u : 0u;
+                        // [Qi | Qr] += Phir . [-U3i | U3r] + Phii . [U3r | U3i]
+                        mma_tf32(qd, A[0], B2h, idesc, acc);
+                        mma_tf32(qd, A[0], B2l, idesc, 1);
+                        mma_tf32(qd, A[1], B2h, idesc, 1);
+                        mma_tf32(qd, A[2], B1h, idesc, 1);
+                        mma_tf32(qd, A[2], B1l, idesc, 1);
+                        mma_tf32(qd, A[3], B1h, idesc, 1);
+                        mma_commit(&empty[s]);
+                        if (++s == AJ_NST) {
+                            s = 0;
+                            ph ^= 1;
+                        }
+                    }
+                    mma_commit(&qfull[qb]);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 2) {
+        // ---------------------------------------------------- factor loader
+        if (elect_one()) {
+            uint32_t s = 0, ph = 0;
+            for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+                const AjTile tl = aj_tile(g, t);
+                const TcDesc* tdk = tcd + int64_t(tl.k) * g.ncols;
+                for (int64_t j = 0; j < g.ncols; ++j) {
+                    mbar_wait(&fempty[s], ph ^ 1);
+                    const TcDesc d = tdk[j];
+                    unsigned char* slot = sSlot + s * g.slot_bytes;
+                    const uint32_t r23 = uint32_t(d.r2 * d.r3);
+                    const uint32_t ld2 = uint32_t(d.r2 | 1);
+                    const uint32_t bv = uint32_t(TC_TI1) * r23 * 16u;
+                    const uint32_t b2 = uint32_t(TC_TI2) * ld2 * 8u;
+                    mbar_arrive_expect_tx(&ffull[s], uint32_t(sizeof(TcDesc)) + bv + b2);
+                    bulk_g2s(slot, tdk + j, uint32_t(sizeof(TcDesc)), &ffull[s]);
+                    bulk_g2s(slot + TC_SLOT_V, varena + d.off_v + int64_t(tl.i1_0) * r23, bv, &ffull[s]);
+                    bulk_g2s(slot + g.u2_off, u2arena + d.off_u2 + int64_t(tl.i2_0) * ld2, b2, &ffull[s]);
+                    if (++s == TC_JR) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp >= TC_PW0 && warp < TC_PW0 + TC_NPW) {
+        // -------------------------------------------------------- consumers
+        const int pw = warp - TC_PW0;
+        const int i1l = pw & (TC_TI1 - 1), h = pw >> 2;
+        const int ctid = threadIdx.x - TC_PW0 * 32;  // 0..255
+        const uint32_t lane_addr = uint32_t(i1l * 32) << 16;
+        uint32_t fs = 0, fph = 0, nq = 0;
+        for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+            const AjTile tl = aj_tile(g, t);
+            const int nc = nch[tl.k];
+            const int* cs = cstart + int64_t(tl.k) * (g.maxch + 1);
+            for (int n = 0; n < nc; ++n, ++nq) {
+                const uint32_t qb = nq & 1, qph = (nq >> 1) & 1;
+                const int j0 = cs[n], j1 = cs[n + 1];
+                float2* rb = red + (nq & 1) * AJ_MAXCOLS * TC_NPW;
+                mbar_wait(&qfull[qb], qph);
+                tc_fence_after();
+                const uint32_t qbase = tmem + lane_addr + qb * 256u;
+                for (int j = j0; j < j1; ++j) {
+                    mbar_wait(&ffull[fs], fph);
+                    const unsigned char* slot = sSlot + fs * g.slot_bytes;
+                    const TcDesc* dd = reinterpret_cast<const TcDesc*>(slot);
+                    const int r2 = dd->r2, r3 = dd->r3, soff = dd->pad0;
+                    const float4* V = reinterpret_cast<const float4*>(slot + TC_SLOT_V) + i1l;
+                    const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
+                    float2 a;
+#define AJ_COL(NU) a = aj_consume_column<NU>(V, U2, r2, r2 | 1, r3, h, lane, qbase + uint32_t(soff), &fempty[fs])
+                    switch ((r3 + 1) >> 1) {
+                        case 1: AJ_COL(1); break;
+                        case 2: AJ_COL(2); break;
+                        case 3: AJ_COL(3); break;
+                        case 4: AJ_COL(4); break;
+                        case 5: AJ_COL(5); break;
+                        case 6: AJ_COL(6); break;
+                        case 7: AJ_COL(7); break;
+                        default: AJ_COL(8); break;
+                    }
+#undef AJ_COL
+                    if (++fs == TC_JR) {
+                        fs = 0;
+                        fph ^= 1;
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+                        a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+                    }
+                    if (lane == 0) rb[(j - j0) * TC_NPW + pw] = a;
+                }
+                // Q buffer no longer read by this warp
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&qfree[qb]);
+                named_bar_sync(1, TC_NPW * 32);  // all partials of the chunk are in rb
+                for (int jj = ctid; jj < j1 - j0; jj += TC_NPW * 32) {
+                    float sx = 0.f, sy = 0.f;
+#pragma unroll
+                    for (int w = 0; w < TC_NPW; ++w) {
+                        sx += rb[jj * TC_NPW + w].x;
+                        sy += rb[jj * TC_NPW + w].y;
+                    }
+                    part[((int64_t(tl.c) * g.ncols + j0 + jj) * g.q + tl.k) * g.nrt + tl.rt] = make_float2(sx, sy);
+                }
+                // rb (this parity) is rewritten two chunks later, after the
+                // next chunk's named barrier: no second barrier needed
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 3) tmem_dealloc(tmem, 512);
+}
+
+// Phi (c64, [c][k n_v + v]) -> 3xTF32 planes [pl][c][k][row-tile order][n3p]
+// (n3p = n3 rounded up to 4 for the TMA row pitch),
+// pl = re hi, re lo, im hi, im lo; tile rows are (i2 + 32 i1) of the
+// (TI1 x TI2) row tiles, rows outside the grid are zero.  One block per
+// (row tile, 32 i3, k, c), transposed through shared memory so both the
+// read (voxel-contiguous) and the write (i3-contiguous) are coalesced.
+__global__ void __launch_bounds__(256) adj_split_phi_kernel(const float2* __restrict__ phi, int64_t ldphi, int n1,
+                                                            int n2, int n3, int n3p, int q, int p, int nt1,
+                                                            int64_t nrt, float* __restrict__ planes) {
+    __shared__ float2 tile[TC_ROWS][33];
+    const int64_t rt = blockIdx.x;
+    const int i3b = blockIdx.y * 32;
+    const int k = blockIdx.z % q, c = blockIdx.z / q;
+    const int t2 = int(rt / nt1), t1 = int(rt - int64_t(t2) * nt1);
+    const int64_t nv = int64_t(n1) * n2 * n3;
+    const float2* src = phi + ldphi * c + int64_t(k) * nv;
+    // load: thread -> (row = i1l + 4 i2l in voxel order for coalescing)
+    for (int e = threadIdx.x; e < TC_ROWS * 32; e += 256) {
+        const int vr = e & (TC_ROWS - 1), i3l = e >> 7;
+        const int i1l = vr & 3, i2l = vr >> 2;
+        const int i1 = t1 * TC_TI1 + i1l, i2 = t2 * TC_TI2 + i2l, i3 = i3b + i3l;
+        float2 v = make_float2(0.f, 0.f);
+        if (i1 < n1 && i2 < n2 && i3 < n3) v = src[i1 + int64_t(n1) * (i2 + int64_t(n2) * i3)];
+        tile[i2l + 32 * i1l][i3l] = v;
+    }
+    __syncthreads();
+    const int64_t R = nrt * TC_ROWS;
+    const int64_t plane = int64_t(p) * q * R * n3p;
+    for (int e = threadIdx.x; e < TC_ROWS * 32; e += 256) {
+        const int i3l = e & 31, row = e >> 5;
+        const int i3 = i3b + i3l;
+        if (i3 >= n3p) continue;
+        const float2 v = tile[row][i3l];
+        const float rh = sm100::tf32_round(v.x), ih = sm100::tf32_round(v.y);
+        const int64_t o = ((int64_t(c) * q + k) * R + rt * TC_ROWS + row) * n3p + i3;
+        planes[o] = rh;
+        planes[plane + o] = sm100::tf32_round(v.x - rh);
+        planes[2 * plane + o] = ih;
+        planes[3 * plane + o] = sm100::tf32_round(v.y - ih);
+    }
+}
+
+// U3 planes for the adjoint: [pl][k][slot][n3] (i3-contiguous), slot =
+// chunk * 128 + offset of the (j, c) pair inside its chunk; same 6-plane
+// order as build_bplanes_kernel.
+__global__ void build_adj_bplanes_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena,
+                                         const int* __restrict__ aslot, int64_t ncols, int q, int n3, int n3p,
+                                         int64_t nslots, float* __restrict__ planes) {
+    const int64_t t = blockIdx.x;
+    const int k = int(t / ncols);
+    const TDesc d = td[t];
+    const int64_t s0 = aslot[t];
+    const int64_t plane = int64_t(q) * nslots * n3p;
+    for (int e = threadIdx.x; e < n3 * d.r3; e += blockDim.x) {
+        const int i3 = e / d.r3, r = e - i3 * d.r3;
+        const float2 u = arena[d.off_u3 + e];
+        const float rh = sm100::tf32_round(u.x), ih = sm100::tf32_round(u.y);
+        const float rl = sm100::tf32_round(u.x - rh), il = sm100::tf32_round(u.y - ih);
+        const int64_t o = (int64_t(k) * nslots + s0 + r) * n3p + i3;
+        planes[o] = -ih;
+        planes[plane + o] = rh;
+        planes[2 * plane + o] = ih;
+        planes[3 * plane + o] = -il;
+        planes[4 * plane + o] = rl;
+        planes[5 * plane + o] = il;
+    }
+}
+
+}  // namespace tmb

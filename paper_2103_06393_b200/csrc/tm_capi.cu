@@ -20,6 +20,7 @@
 #include "tm_common.cuh"
 #include "tm_kernels_cc.cuh"
 #include "tm_kernels_tc.cuh"
+#include "tm_adj_tc.cuh"
 #include "tm_tmap.h"
 
 using namespace tmb;
@@ -124,10 +125,18 @@ struct tm_store {
     TcDesc* d_tcd = nullptr;  // [q*ncols] tensor-core descriptors
     float4* d_varena = nullptr;  // mode-1 products V = U1 x_1 G (FFMA2 form)
     float2* d_u2arena = nullptr;  // U2 with odd row strides
+    // tensor-core adjoint: chunk-aligned, i3-contiguous U3 planes
+    bool tca_ok = false;
+    float* d_aplanes = nullptr;
+    int* d_nch = nullptr;     // [q] chunks per component
+    int* d_cstart = nullptr;  // [q][maxch + 1] first column of each chunk
+    int maxch = 0;
+    int64_t nslots = 0;       // slots per component (maxch * 128)
+    CUtensorMap adj_bmap{};
     int64_t kpad = 0;
     CUtensorMap bmap{};
     std::mutex mu;
-    DevBuf part, xin, yout, wbuf;
+    DevBuf part, xin, yout, wbuf, phiplanes;
 
     int64_t nv() const { return dims[0] * dims[1] * dims[2]; }
     int64_t rows() const { return q * nv(); }
@@ -139,6 +148,9 @@ struct tm_store {
         if (d_tcd) cudaFree(d_tcd);
         if (d_varena) cudaFree(d_varena);
         if (d_u2arena) cudaFree(d_u2arena);
+        if (d_aplanes) cudaFree(d_aplanes);
+        if (d_nch) cudaFree(d_nch);
+        if (d_cstart) cudaFree(d_cstart);
         if (d_desc) cudaFree(d_desc);
         if (d_arena) cudaFree(d_arena);
         if (d_v) cudaFree(d_v);
@@ -201,6 +213,34 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
         c.pad0 = c.pad1 = 0;
         voff += n1p * d.r2 * d.r3;
     }
+    // adjoint chunks: whole columns, at most AJ_CH (j, c) slots each
+    std::vector<int> aslot(static_cast<size_t>(ntens), 0), nch(static_cast<size_t>(s->q), 0);
+    std::vector<std::vector<int>> cst(static_cast<size_t>(s->q));
+    for (int k = 0; k < s->q; ++k) {
+        int fill = AJ_CH, chunk = -1;
+        for (int64_t j = 0; j < s->ncols; ++j) {
+            const size_t t = static_cast<size_t>(k * s->ncols + j);
+            const int r3 = desc[t].r3;
+            if (fill + r3 > AJ_CH || int64_t(cst[k].size()) == 0 ||
+                (j - cst[static_cast<size_t>(k)].back()) >= AJ_MAXCOLS) {
+                ++chunk;
+                fill = 0;
+                cst[static_cast<size_t>(k)].push_back(int(j));
+            }
+            aslot[t] = chunk * AJ_CH + fill;
+            tcd[t].pad0 = fill;
+            fill += r3;
+        }
+        nch[static_cast<size_t>(k)] = chunk + 1;
+        s->maxch = std::max(s->maxch, chunk + 1);
+    }
+    s->nslots = int64_t(s->maxch) * AJ_CH;
+    std::vector<int> cstart(static_cast<size_t>(s->q) * (s->maxch + 1), int(s->ncols));
+    for (int k = 0; k < s->q; ++k)
+        for (size_t n = 0; n < cst[static_cast<size_t>(k)].size(); ++n)
+            cstart[static_cast<size_t>(k) * (s->maxch + 1) + n] = cst[static_cast<size_t>(k)][n];
+    const int64_t n3p = (n3 + 3) / 4 * 4;
+    const size_t abytes = size_t(TC_BPLANES) * s->q * s->nslots * n3p * sizeof(float);
     const size_t vbytes = size_t(voff) * sizeof(float4);
     const size_t u2bytes = size_t(u2off) * sizeof(float2);
     CK(cudaMalloc(&s->d_kofs, kofs.size() * sizeof(int)));
@@ -209,6 +249,25 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
     CK(cudaMalloc(&s->d_tcd, tcd.size() * sizeof(TcDesc)));
     CK(cudaMalloc(&s->d_varena, std::max<size_t>(vbytes, 16)));
     CK(cudaMalloc(&s->d_u2arena, std::max<size_t>(u2bytes, 16)));
+    CK(cudaMalloc(&s->d_aplanes, abytes));
+    CK(cudaMalloc(&s->d_nch, nch.size() * sizeof(int)));
+    CK(cudaMalloc(&s->d_cstart, cstart.size() * sizeof(int)));
+    CK(cudaMemcpy(s->d_nch, nch.data(), nch.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(s->d_cstart, cstart.data(), cstart.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemset(s->d_aplanes, 0, abytes));
+    {
+        DevBuf as;
+        int* d_as = static_cast<int*>(as.get(aslot.size() * sizeof(int)));
+        CK(cudaMemcpy(d_as, aslot.data(), aslot.size() * sizeof(int), cudaMemcpyHostToDevice));
+        build_adj_bplanes_kernel<<<unsigned(ntens), 256>>>(s->d_desc, static_cast<const float2*>(s->d_arena), d_as,
+                                                           s->ncols, s->q, int(n3), int(n3p), s->nslots, s->d_aplanes);
+        launched(cudaSuccess, "build_adj_bplanes_kernel");
+        CK(cudaDeviceSynchronize());
+    }
+    s->adj_bmap = make_tmap_3d_f32(s->d_aplanes, uint64_t(n3), uint64_t(s->nslots), uint64_t(TC_BPLANES * s->q),
+                                   uint64_t(n3p) * 4, uint64_t(s->nslots) * n3p * 4, 8, AJ_CH,
+                                   CU_TENSOR_MAP_SWIZZLE_32B);
+    s->tca_ok = true;
     CK(cudaMemcpy(s->d_kofs, kofs.data(), kofs.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(s->d_kc, kc.data(), kc.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(s->d_tcd, tcd.data(), tcd.size() * sizeof(TcDesc), cudaMemcpyHostToDevice));
@@ -226,7 +285,7 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
     const uint32_t nmma = uint32_t(std::min<int64_t>((n3 + 15) / 16 * 16, TC_NMAX));
     s->bmap = make_tmap_3d_f32(s->d_planes, uint64_t(s->kpad), uint64_t(n3), uint64_t(TC_BPLANES * s->q),
                                uint64_t(s->kpad) * 4, uint64_t(n3) * s->kpad * 4, 8, nmma, CU_TENSOR_MAP_SWIZZLE_32B);
-    s->device_bytes += int64_t(pbytes + vbytes + u2bytes + tcd.size() * sizeof(TcDesc) + (kofs.size() + kc.size()) * sizeof(int));
+    s->device_bytes += int64_t(pbytes + vbytes + u2bytes + abytes + tcd.size() * sizeof(TcDesc) + (kofs.size() + kc.size()) * sizeof(int));
     s->tc_ok = true;
 }
 
@@ -530,8 +589,68 @@ void forward_dev(const tm_store* s, const void* x, int64_t ldx, int64_t p, void*
     }
 }
 
+size_t adj_tc_smem(const tm_store* s) {
+    const int u2_off = TC_SLOT_V + TC_TI1 * s->rmax[1] * s->rmax[2] * 16;
+    const int slot = (u2_off + TC_TI2 * (s->rmax[1] | 1) * 8 + 127) / 128 * 128;
+    return 1024 + size_t(AJ_NST) * (AJ_A_STAGE + AJ_B_STAGE) + size_t(TC_JR) * slot +
+           size_t(2) * AJ_MAXCOLS * TC_NPW * sizeof(float2) + (2 * AJ_NST + 2 * TC_JR + 4) * 8 + 16;
+}
+
+void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, float2* z, int64_t ldz,
+                    cudaStream_t st) {
+    AjGeom g{};
+    g.ncols = s->ncols;
+    g.n1 = int(s->dims[0]);
+    g.n2 = int(s->dims[1]);
+    g.n3 = int(s->dims[2]);
+    g.q = s->q;
+    g.nt1 = (g.n1 + TC_TI1 - 1) / TC_TI1;
+    g.nt2 = (g.n2 + TC_TI2 - 1) / TC_TI2;
+    g.p = int(p);
+    g.nrt = int64_t(g.nt1) * g.nt2;
+    g.ntiles = int64_t(p) * g.q * g.nrt;
+    g.nks = (g.n3 + 7) / 8;
+    g.rmax2 = s->rmax[1];
+    g.rmax3 = s->rmax[2];
+    g.u2_off = TC_SLOT_V + TC_TI1 * g.rmax2 * g.rmax3 * 16;
+    g.slot_bytes = (g.u2_off + TC_TI2 * (g.rmax2 | 1) * 8 + 127) / 128 * 128;
+    g.maxch = s->maxch;
+    const size_t smem = 1024 + size_t(AJ_NST) * (AJ_A_STAGE + AJ_B_STAGE) + size_t(TC_JR) * g.slot_bytes +
+                        size_t(2) * AJ_MAXCOLS * TC_NPW * sizeof(float2) + (2 * AJ_NST + 2 * TC_JR + 4) * 8 + 16;
+    if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: shared-memory plan too large");
+    // Phi -> 3xTF32 planes (per call)
+    const int64_t n3p = (g.n3 + 3) / 4 * 4;
+    const int64_t R = g.nrt * TC_ROWS;
+    float* planes = static_cast<float*>(s->phiplanes.get(size_t(AJ_APLANES) * p * g.q * R * n3p * sizeof(float)));
+    if (int64_t(p) * g.q > 65535) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: too many right-hand sides");
+    dim3 sgrid(unsigned(g.nrt), unsigned((n3p + 31) / 32), unsigned(p * g.q));
+    adj_split_phi_kernel<<<sgrid, 256, 0, st>>>(phi, ldphi, g.n1, g.n2, g.n3, int(n3p), g.q, int(p), g.nt1, g.nrt,
+                                                planes);
+    launched(cudaSuccess, "adj_split_phi_kernel");
+    const CUtensorMap amap = make_tmap_3d_f32(planes, uint64_t(g.n3), uint64_t(R), uint64_t(AJ_APLANES * p * g.q),
+                                              uint64_t(n3p) * 4, uint64_t(R) * n3p * 4, 8, TC_ROWS,
+                                              CU_TENSOR_MAP_SWIZZLE_32B);
+    const int64_t nred = g.nrt * g.q;
+    float2* part = static_cast<float2*>(s->part.get(size_t(s->ncols * p * nred) * sizeof(float2)));
+    CK(cudaFuncSetAttribute(adj_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const unsigned grid = unsigned(std::min<int64_t>(g.ntiles, num_sms(dev)));
+    adj_tc_kernel<<<grid, TC_THREADS, smem, st>>>(amap, s->adj_bmap, s->d_tcd, s->d_varena, s->d_u2arena, s->d_nch,
+                                                   s->d_cstart, g, part);
+    launched(cudaSuccess, "adj_tc_kernel");
+    const int64_t warps = s->ncols * p;
+    const unsigned blocks = unsigned((warps * 32 + 255) / 256);
+    adj_reduce_kernel<float2><<<blocks, 256, 0, st>>>(part, s->ncols, p, nred, z, ldz);
+    launched(cudaSuccess, "adj_reduce_kernel");
+}
+
 void adjoint_dev(tm_store* s, const void* phi, int64_t ldphi, int64_t p, void* z, int64_t ldz, cudaStream_t st) {
     if (s->ncols == 0 || p == 0) return;
+    if (s->tca_ok && !tc_disabled() && adj_tc_smem(s) <= kSmemMax && int64_t(p) * s->q <= 65535) {
+        run_adjoint_tc(s, static_cast<const float2*>(phi), ldphi, p, static_cast<float2*>(z), ldz, st);
+        return;
+    }
     const int cn = pick_cn(s->dims[2]);
     if (s->dtype == TM_C64) {
         auto P = static_cast<const float2*>(phi);

@@ -223,20 +223,23 @@ def test_aca_products(oracle, product, dtype):
     ((9, 70, 20), 2, 40, 1, 13, 3),      # many short chains, ragged ranks from 1
 ])
 def test_tensor_core_forward(oracle, product, monkeypatch, dims, q, m, rmin, rmax, p):
-    """tcgen05 3xTF32 forward (c64, the default c64 forward) vs the oracle and
-    vs the CUDA-core kernel (TMB_DISABLE_TC=1)."""
+    """tcgen05 3xTF32 forward and adjoint (c64, the default c64 path) vs the
+    oracle and vs the CUDA-core kernels (TMB_DISABLE_TC=1)."""
     O, P = oracle, product
     cc = ragged_store(dims, q, m, rmin, rmax, seed=7 * m + q)
     ref = O.OracleStore(cc.rounded_c64())
     ds = P.DeviceStore.from_compressed(cc, "c64")
     x = cn01(m, p, 3).astype(np.complex64).astype(np.complex128)
-    y_tc = ds.forward(x)
+    phi = cn01(cc.rows, p, 4).astype(np.complex64).astype(np.complex128)
+    y_tc, z_tc = ds.forward(x), ds.adjoint(phi)
     monkeypatch.setenv("TMB_DISABLE_TC", "1")
-    y_cc = ds.forward(x)
+    y_cc, z_cc = ds.forward(x), ds.adjoint(phi)
     monkeypatch.delenv("TMB_DISABLE_TC")
-    y_ref = ref.forward(x)
+    y_ref, z_ref = ref.forward(x), ref.adjoint(phi)
     assert rel(y_tc, y_ref) <= 1e-5
     assert rel(y_cc, y_ref) <= 1e-5
+    assert rel(z_tc, z_ref) <= 1e-5
+    assert rel(z_cc, z_ref) <= 1e-5
 
 
 @pytest.mark.parametrize("chain", ["", "1", "3"])
@@ -263,4 +266,9 @@ def test_tensor_core_long_k(product, monkeypatch, chain):
     y64 = s64.forward(x).to(torch.complex128)
     y128 = s128.forward(x.to(torch.complex128))
     err = float(torch.linalg.vector_norm(y64 - y128) / torch.linalg.vector_norm(y128))
+    assert err <= 1e-5, err
+    phi = torch.randn((1, y128.shape[0]), dtype=torch.complex64, device="cuda", generator=g).t()
+    z64 = s64.adjoint(phi).to(torch.complex128)
+    z128 = s128.adjoint(phi.to(torch.complex128))
+    err = float(torch.linalg.vector_norm(z64 - z128) / torch.linalg.vector_norm(z128))
     assert err <= 1e-5, err
