@@ -113,11 +113,12 @@ def measured_peaks():
         return {}
 
 
-def fp32_peak_tflops(torch):
-    """FP32 (FFMA, no TF32) throughput of cuBLAS SGEMM 8192^3 — the CUDA-core
-    roofline denominator the driver does not measure (best of 5)."""
+def fp32_peak_tflops(torch, tf32=False):
+    """cuBLAS SGEMM 8192^3 throughput (best of 5): plain FP32 (FFMA) or with
+    TF32 tensor cores — the roofline denominators the driver does not measure
+    (MEASURED_PEAKS.json has HBM and bf16 only)."""
     prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = tf32
     try:
         n = 8192
         a = torch.randn(n, n, device="cuda")
@@ -251,6 +252,16 @@ def cn01(rows, cols, seed):
     return np.asfortranarray(a)
 
 
+def compressed_bytes(cfg, ranks):
+    """Bytes of the compressed store proper (cores + factors, c64): the
+    roofline's B_alg term, without the derived tensor-core
+    operand copies."""
+    r = np.asarray(ranks, np.int64).reshape(-1, 3)
+    n1, n2, n3 = cfg.grid
+    scalars = (r[:, 0] * r[:, 1] * r[:, 2] + n1 * r[:, 0] + n2 * r[:, 1] + n3 * r[:, 2]).sum()
+    return int(scalars) * (8 if cfg.dtype == "c64" else 16)
+
+
 def metric_name(cfg):
     return f"ms per Zbc*x + Zbc^H*y matvec pair ({cfg.name})"
 
@@ -325,6 +336,7 @@ def main():
 
     peaks = measured_peaks()
     fp32_peak = fp32_peak_tflops(torch) if rank == 0 else None
+    tf32_peak = fp32_peak_tflops(torch, tf32=True) if rank == 0 else None
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -409,21 +421,35 @@ def main():
         if world > 1:
             e2e["note"] = "multi-GPU e2e uses the sharded Python API; Phi is replicated device-resident"
 
-    # --- roofline of the dominant kernel (forward kernel, one launch per forward) --
+    # --- roofline of the dominant kernels (one tensor-core launch per forward;
+    # the adjoint is Phi split + tensor-core kernel + partial reduction) ------
     dec, acc = store.opcounts(cfg.p)
-    flops_fwd = 8.0 * (dec + acc)  # OpCounts x 8 real flops per complex madd (this rank's shard)
-    achieved = flops_fwd / (fwd_med * 1e-3) / 1e12
+    flops = 8.0 * (dec + acc)  # OpCounts x 8 real flops per complex madd (this rank's shard)
+    tc = cfg.dtype == "c64" and os.environ.get("TMB_DISABLE_TC", "0") != "1"
     roof = None
     if rank == 0:
-        roof = {"bound": "fp32-ffma", "kernel": "fwd_cc_kernel", "achieved": round(achieved, 2),
-                "peak": round(fp32_peak, 2), "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4),
-                "peak_source": "measured here: cuBLAS SGEMM 8192^3 without TF32 (MEASURED_PEAKS.json has no FP32 "
-                               "figure)",
-                "traffic": None,
-                "algorithmic_flops_per_launch": flops_fwd,
-                "hbm_bytes_algorithmic": int(store.device_bytes + (c1 - c0) * cfg.p * 8 + nrows * cfg.p * 8),
-                "hbm_peak_gbs": peaks.get("hbm_gbs"),
-                "bf16_peak_tflops_measured": peaks.get("bf16_tflops")}
+        if tc:
+            # complex64 on 3xTF32: every real fp32 multiply-add costs three
+            # TF32 tensor-core multiply-adds, so the compute roofline of the
+            # algorithmic (fp32-equivalent) flops is the TF32 peak / 3
+            peak = tf32_peak / 3.0
+            bound, unit_src = "tensor", ("measured here: cuBLAS TF32 GEMM 8192^3 = %.1f TFLOP/s, / 3 for the 3xTF32 "
+                                         "split (bf16 measured in MEASURED_PEAKS.json: %s TFLOP/s)"
+                                         % (tf32_peak, peaks.get("bf16_tflops")))
+            kernels = ("fwd_tc_kernel", "adj_tc_kernel (+ adj_split_phi_kernel, adj_reduce_kernel)")
+        else:
+            peak = fp32_peak
+            bound, unit_src = "fp32-ffma", "measured here: cuBLAS SGEMM 8192^3 without TF32"
+            kernels = ("fwd_cc_kernel", "adj_cc_kernel (+ adj_reduce_kernel)")
+        fa, aa = flops / (fwd_med * 1e-3) / 1e12, flops / (adj_med * 1e-3) / 1e12
+        roof = {"bound": bound, "kernel": kernels[0], "achieved": round(fa, 2), "peak": round(peak, 2),
+                "unit": "TFLOP/s", "frac": round(fa / peak, 4), "peak_source": unit_src, "traffic": None,
+                "algorithmic_flops_per_launch": flops,
+                "adjoint": {"kernel": kernels[1], "achieved": round(aa, 2), "frac": round(aa / peak, 4)},
+                "hbm_bytes_algorithmic": int(compressed_bytes(cfg, ranks[c0:c1]) + (c1 - c0) * cfg.p * 8
+                                             + nrows * cfg.p * 8),
+                "hbm_peak_gbs": peaks.get("hbm_gbs"), "fp32_ffma_peak_tflops": round(fp32_peak, 2),
+                "tf32_peak_tflops": round(tf32_peak, 2), "bf16_peak_tflops_measured": peaks.get("bf16_tflops")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and cpu_pay is not None:

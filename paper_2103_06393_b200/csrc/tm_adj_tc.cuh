@@ -45,6 +45,9 @@ constexpr int AJ_A_STAGE = AJ_APLANES * AJ_A_PLANE;       // 16 KB
 constexpr int AJ_B_PLANE = AJ_CH * 32;
 constexpr int AJ_B_STAGE = TC_BPLANES * AJ_B_PLANE;       // 24 KB
 constexpr int AJ_MAXCOLS = 128;  // columns per chunk (r3 >= 1)
+constexpr int AJ_NPW = 8;        // consumer warps (4 i1 rows x 2 c parities)
+constexpr int AJ_NH = AJ_NPW / TC_TI1;
+constexpr int AJ_THREADS = (TC_PW0 + AJ_NPW) * 32;
 
 struct AjGeom {
     int64_t ncols;
@@ -90,11 +93,12 @@ __device__ __forceinline__ float2 aj_consume_column(const float4* __restrict__ V
     for (int u = 0; u < NU; ++u) w[u] = 0;
     const float4* vp = V + 4 * r2 * h;
     const float2* up = U2 + lane * ld2;
+#pragma unroll 2
     for (int b = 0; b < r2; ++b) {
         const float2 ub = up[b];
 #pragma unroll
         for (int u = 0; u < NU; ++u)
-            if (u < NU - 1 || 2 * u + h < r3) cfma2(w[u], vp[4 * b + 8 * r2 * u], ub);
+            if (u < NU - 1 || AJ_NH * u + h < r3) cfma2(w[u], vp[4 * b + 4 * AJ_NH * r2 * u], ub);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(fempty_s);
@@ -104,7 +108,7 @@ __device__ __forceinline__ float2 aj_consume_column(const float4* __restrict__ V
     for (int u = 0; u < NU; ++u) {
         // (a slot past this column's last c reads slot 0 and is ignored: it
         // may lie past the end of the TMEM allocation)
-        const uint32_t s = (u < NU - 1 || 2 * u + h < r3) ? uint32_t(2 * u + h) : 0u;
+        const uint32_t s = (u < NU - 1 || AJ_NH * u + h < r3) ? uint32_t(AJ_NH * u + h) : 0u;
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(qi[u]) : "r"(qaddr + s));
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(qr[u]) : "r"(qaddr + AJ_CH + s));
     }
@@ -112,7 +116,7 @@ __device__ __forceinline__ float2 aj_consume_column(const float4* __restrict__ V
     float ar = 0.f, ai = 0.f;
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
-        if (u < NU - 1 || 2 * u + h < r3) {
+        if (u < NU - 1 || AJ_NH * u + h < r3) {
             const float2 wv = f2_unpack(w[u]);
             const float qre = __uint_as_float(qr[u]), qim = __uint_as_float(qi[u]);
             // conj(W) Q = (Wr Qr + Wi Qi) + i (Wr Qi - Wi Qr)
@@ -123,7 +127,7 @@ __device__ __forceinline__ float2 aj_consume_column(const float4* __restrict__ V
     return make_float2(ar, ai);
 }
 
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(AJ_THREADS, 1)
     adj_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                   const TcDesc* __restrict__ tcd, const float4* __restrict__ varena,
                   const float2* __restrict__ u2arena, const int* __restrict__ nch, const int* __restrict__ cstart,
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     unsigned char* sB = sA + AJ_NST * AJ_A_STAGE;
     unsigned char* sSlot = sB + AJ_NST * AJ_B_STAGE;
     float2* red = reinterpret_cast<float2*>(sSlot + TC_JR * g.slot_bytes);  // [2][AJ_MAXCOLS][8]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * AJ_MAXCOLS * TC_NPW);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * AJ_MAXCOLS * AJ_NPW);
     uint64_t* full = bars;                // [NST]
     uint64_t* empty = full + AJ_NST;      // [NST]
     uint64_t* ffull = empty + AJ_NST;     // [JR]
@@ -152,11 +156,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         for (int s = 0; s < TC_JR; ++s) {
             mbar_init(&ffull[s], 1);
-            mbar_init(&fempty[s], TC_NPW);
+            mbar_init(&fempty[s], AJ_NPW);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&qfull[s], 1);
-            mbar_init(&qfree[s], TC_NPW);
+            mbar_init(&qfree[s], AJ_NPW);
         }
         fence_mbar_init();
     }
@@ -270,10 +274,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 }
             }
         }
-    } else if (warp >= TC_PW0 && warp < TC_PW0 + TC_NPW) {
+    } else if (warp >= TC_PW0 && warp < TC_PW0 + AJ_NPW) {
         // -------------------------------------------------------- consumers
         const int pw = warp - TC_PW0;
-        const int i1l = pw & (TC_TI1 - 1), h = pw >> 2;
+        const int i1l = pw & (TC_TI1 - 1), h = pw / TC_TI1;
         const int ctid = threadIdx.x - TC_PW0 * 32;  // 0..255
         const uint32_t lane_addr = uint32_t(i1l * 32) << 16;
         uint32_t fs = 0, fph = 0, nq = 0;
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int n = 0; n < nc; ++n, ++nq) {
                 const uint32_t qb = nq & 1, qph = (nq >> 1) & 1;
                 const int j0 = cs[n], j1 = cs[n + 1];
-                float2* rb = red + (nq & 1) * AJ_MAXCOLS * TC_NPW;
+                float2* rb = red + (nq & 1) * AJ_MAXCOLS * AJ_NPW;
                 mbar_wait(&qfull[qb], qph);
                 tc_fence_after();
                 const uint32_t qbase = tmem + lane_addr + qb * 256u;
@@ -297,7 +301,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
                     float2 a;
 #define AJ_COL(NU) a = aj_consume_column<NU>(V, U2, r2, r2 | 1, r3, h, lane, qbase + uint32_t(soff), &fempty[fs])
-                    switch ((r3 + 1) >> 1) {
+                    switch ((r3 + AJ_NH - 1) / AJ_NH) {
                         case 1: AJ_COL(1); break;
                         case 2: AJ_COL(2); break;
                         case 3: AJ_COL(3); break;
@@ -317,19 +321,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
                         a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
                     }
-                    if (lane == 0) rb[(j - j0) * TC_NPW + pw] = a;
+                    if (lane == 0) rb[(j - j0) * AJ_NPW + pw] = a;
                 }
                 // Q buffer no longer read by this warp
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&qfree[qb]);
-                named_bar_sync(1, TC_NPW * 32);  // all partials of the chunk are in rb
-                for (int jj = ctid; jj < j1 - j0; jj += TC_NPW * 32) {
+                named_bar_sync(1, AJ_NPW * 32);  // all partials of the chunk are in rb
+                for (int jj = ctid; jj < j1 - j0; jj += AJ_NPW * 32) {
                     float sx = 0.f, sy = 0.f;
 #pragma unroll
-                    for (int w = 0; w < TC_NPW; ++w) {
-                        sx += rb[jj * TC_NPW + w].x;
-                        sy += rb[jj * TC_NPW + w].y;
+                    for (int w = 0; w < AJ_NPW; ++w) {
+                        sx += rb[jj * AJ_NPW + w].x;
+                        sy += rb[jj * AJ_NPW + w].y;
                     }
                     part[((int64_t(tl.c) * g.ncols + j0 + jj) * g.q + tl.k) * g.nrt + tl.rt] = make_float2(sx, sy);
                 }

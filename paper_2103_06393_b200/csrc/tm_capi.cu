@@ -551,6 +551,10 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     g.slot_bytes = (g.u2_off + TC_TI2 * (g.rmax2 | 1) * 8 + 127) / 128 * 128;
     g.b_stage = TC_BPLANES * g.nmma * 32;
     g.chain = tc_chain();
+    {
+        const char* dbg = std::getenv("TMB_TC_DEBUG");
+        g.debug = dbg ? std::atoi(dbg) : 0;
+    }
     auto smem_for = [&](int nst) {
         return 1024 + size_t(nst) * (TC_A_STAGE + g.b_stage) + size_t(TC_JR) * g.slot_bytes +
                (2 * TC_NST_MAX + 2 * TC_JR + 2) * 8 + 16;
@@ -593,7 +597,7 @@ size_t adj_tc_smem(const tm_store* s) {
     const int u2_off = TC_SLOT_V + TC_TI1 * s->rmax[1] * s->rmax[2] * 16;
     const int slot = (u2_off + TC_TI2 * (s->rmax[1] | 1) * 8 + 127) / 128 * 128;
     return 1024 + size_t(AJ_NST) * (AJ_A_STAGE + AJ_B_STAGE) + size_t(TC_JR) * slot +
-           size_t(2) * AJ_MAXCOLS * TC_NPW * sizeof(float2) + (2 * AJ_NST + 2 * TC_JR + 4) * 8 + 16;
+           size_t(2) * AJ_MAXCOLS * AJ_NPW * sizeof(float2) + (2 * AJ_NST + 2 * TC_JR + 4) * 8 + 16;
 }
 
 void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, float2* z, int64_t ldz,
@@ -616,7 +620,7 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     g.slot_bytes = (g.u2_off + TC_TI2 * (g.rmax2 | 1) * 8 + 127) / 128 * 128;
     g.maxch = s->maxch;
     const size_t smem = 1024 + size_t(AJ_NST) * (AJ_A_STAGE + AJ_B_STAGE) + size_t(TC_JR) * g.slot_bytes +
-                        size_t(2) * AJ_MAXCOLS * TC_NPW * sizeof(float2) + (2 * AJ_NST + 2 * TC_JR + 4) * 8 + 16;
+                        size_t(2) * AJ_MAXCOLS * AJ_NPW * sizeof(float2) + (2 * AJ_NST + 2 * TC_JR + 4) * 8 + 16;
     if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: shared-memory plan too large");
     // Phi -> 3xTF32 planes (per call)
     const int64_t n3p = (g.n3 + 3) / 4 * 4;
@@ -636,7 +640,7 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     int dev = 0;
     CK(cudaGetDevice(&dev));
     const unsigned grid = unsigned(std::min<int64_t>(g.ntiles, num_sms(dev)));
-    adj_tc_kernel<<<grid, TC_THREADS, smem, st>>>(amap, s->adj_bmap, s->d_tcd, s->d_varena, s->d_u2arena, s->d_nch,
+    adj_tc_kernel<<<grid, AJ_THREADS, smem, st>>>(amap, s->adj_bmap, s->d_tcd, s->d_varena, s->d_u2arena, s->d_nch,
                                                    s->d_cstart, g, part);
     launched(cudaSuccess, "adj_tc_kernel");
     const int64_t warps = s->ncols * p;

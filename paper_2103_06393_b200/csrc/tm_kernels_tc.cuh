@@ -33,17 +33,17 @@
 // fold warps; the tile's last chain is added to the running sum on its way
 // to y.  The error is then set by the chain length, not by K.
 //
-// Warp roles (512 threads, 1 CTA / SM, persistent over tiles):
+// Warp roles (640 threads, 1 CTA / SM, persistent over tiles):
 //   warp 0      TMA producer of the B planes
 //   warp 1      MMA issuer (one elected thread)
 //   warp 2      factor loader: per column, bulk-copies {TcDesc, V rows,
 //               U2 rows} of the tile into a 3-deep shared-memory ring
 //   warp 3      TMEM allocator
-//   warps 4-11  A producers (mode-2 W, x_j scale, hi/lo split)
-//   warps 12-15 chain fold + epilogue (TMEM -> registers -> y)
-// Pipelines: A/B stage ring (full: 1 TMA arrive+tx + 8 producer-warp
+//   warps 4-15  A producers (mode-2 W, x_j scale, hi/lo split)
+//   warps 16-19 chain fold + epilogue (TMEM -> registers -> y)
+// Pipelines: A/B stage ring (full: 1 TMA arrive+tx + 12 producer-warp
 // arrivals; empty: tcgen05.commit), factor ring (full: bulk-copy tx; empty:
-// 8 producer warps), chain (full: commit after the chain's last K step;
+// 12 producer warps), chain (full: commit after the chain's last K step;
 // free: 4 fold warps).
 #pragma once
 
@@ -55,10 +55,11 @@ namespace tmb {
 constexpr int TC_TI1 = 4, TC_TI2 = 32, TC_ROWS = 128;
 constexpr int TC_NST_MAX = 4;   // A/B stages (8 K each)
 constexpr int TC_JR = 3;        // factor-ring slots
-constexpr int TC_THREADS = 512;
-constexpr int TC_NPW = 8;       // producer warps
+constexpr int TC_NPW = 12;      // producer warps: 4 i1 rows x TC_NH c partitions
+constexpr int TC_NH = TC_NPW / TC_TI1;
 constexpr int TC_PW0 = 4;       // first producer warp
-constexpr int TC_FW0 = 12;      // first fold / epilogue warp
+constexpr int TC_FW0 = TC_PW0 + TC_NPW;   // first fold / epilogue warp
+constexpr int TC_THREADS = (TC_FW0 + 4) * 32;
 constexpr int TC_NMAX = 128;    // i3 per tile (N per MMA)
 constexpr int TC_RMAX = 16;     // rank bound of the tensor-core path
 constexpr int TC_A_PLANE = TC_ROWS * 32;     // bytes (128 rows x 8 tf32)
@@ -93,6 +94,7 @@ struct TcGeom {
     int b_stage;                // bytes of one B stage (4 planes x nmma x 32)
     int nst;                    // A/B stages in the ring (3..TC_NST_MAX)
     int chain;                  // K stages per TMEM accumulation chain
+    int debug;                  // diagnostics (TMB_TC_DEBUG): 1 = no mode-2 work, 2 = no B loads
 };
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -146,9 +148,9 @@ __device__ __forceinline__ void ring_ahead(const ARing& r, uint32_t i, uint32_t 
     }
 }
 
-// One column of one tile for the producer thread (row, c parity h): mode 2
-// (W[row, c] = x_j sum_b V[i1, b, c] U2[i2, b] for c = 2u + h) and the
-// 3xTF32 hi/lo split of W into its K slots of the A ring.  NU = ceil(r3/2).
+// One column of one tile for the producer thread (row, c partition h): mode 2
+// (W[row, c] = x_j sum_b V[i1, b, c] U2[i2, b] for c = NH u + h) and the
+// 3xTF32 hi/lo split of W into its K slots of the A ring.  NU = ceil(r3/NH).
 // All lanes of a producer warp share i1 (lane = i2), so the V operand of
 // each FFMA2 is a warp-uniform shared-memory broadcast.
 template <int NU>
@@ -161,14 +163,15 @@ __device__ __forceinline__ void tc_produce_column(const float4* __restrict__ V, 
     uint64_t w[NU];
 #pragma unroll
     for (int u = 0; u < NU; ++u) w[u] = 0;
-    // V[(b + r2 c) * 4 + il]: c = 2u + h  ->  stride 8 r2 float4 per u
+    // V[(b + r2 c) * 4 + il]: c = NH u + h  ->  stride 4 NH r2 float4 per u
     const float4* vp = V + 4 * r2 * h;
     const float2* up = U2 + lane * ld2;
+#pragma unroll 2
     for (int b = 0; b < r2; ++b) {
         const float2 ub = up[b];
 #pragma unroll
         for (int u = 0; u < NU; ++u)
-            if (u < NU - 1 || 2 * u + h < r3) cfma2(w[u], vp[4 * b + 8 * r2 * u], ub);
+            if (u < NU - 1 || TC_NH * u + h < r3) cfma2(w[u], vp[4 * b + 4 * TC_NH * r2 * u], ub);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(fempty_s);  // this warp no longer reads the slot
@@ -187,7 +190,7 @@ __device__ __forceinline__ void tc_produce_column(const float4* __restrict__ V, 
     }
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
-        const int c = 2 * u + h;
+        const int c = TC_NH * u + h;
         if (u < NU - 1 || c < r3) {
             const uint32_t K = ring.kpos + uint32_t(c);
             uint32_t s, ph;
@@ -270,11 +273,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int nks = (kc[tl.k] + 7) >> 3;
                 for (int kk = 0; kk < nks; ++kk) {
                     mbar_wait(&empty[s], ph ^ 1);
-                    mbar_arrive_expect_tx(&full[s], uint32_t(g.b_stage));
-                    unsigned char* dst = sB + s * g.b_stage;
+                    if (g.debug & 2) {
+                        mbar_arrive(&full[s]);
+                    } else {
+                        mbar_arrive_expect_tx(&full[s], uint32_t(g.b_stage));
+                        unsigned char* dst = sB + s * g.b_stage;
 #pragma unroll
-                    for (int pl = 0; pl < TC_BPLANES; ++pl)
-                        tma_load_3d(dst + pl * plane_bytes, &bmap, &full[s], kk * 8, tl.i3_0, pl * g.q + tl.k);
+                        for (int pl = 0; pl < TC_BPLANES; ++pl)
+                            tma_load_3d(dst + pl * plane_bytes, &bmap, &full[s], kk * 8, tl.i3_0, pl * g.q + tl.k);
+                    }
                     if (++s == nst) {
                         s = 0;
                         ph ^= 1;
@@ -363,11 +370,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
         }
     } else if (warp >= TC_PW0 && warp < TC_FW0) {
+        static_assert(TC_NH * 6 >= TC_RMAX, "producer switch covers ceil(TC_RMAX / TC_NH)");
         // ------------------------------------------------------ A producers
-        // warp pw: i1 = pw & 3 (warp-uniform), c parity h = pw >> 2, lane = i2;
+        // warp pw: i1 = pw & 3 (warp-uniform), c partition h = pw / 4, lane = i2;
         // tile row = i2 + 32 i1 (= TMEM lane of the accumulator)
         const int pw = warp - TC_PW0;
-        const int i1l = pw & (TC_TI1 - 1), h = pw >> 2;
+        const int i1l = pw & (TC_TI1 - 1), h = pw / TC_TI1;
         const int row = lane + 32 * i1l;
         const uint32_t rowbase = uint32_t(row) * 32u, xorv = (uint32_t(row) & 4u) << 2;
         ARing ring{0, 0, 0};
@@ -384,17 +392,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const float4* V = reinterpret_cast<const float4*>(slot + TC_SLOT_V) + i1l;
                 const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
 #define TC_COL(NU)                                                                                              \
-    tc_produce_column<NU>(V, U2, r2, r2 | 1, r3, h, xj, &fempty[fs], empty, full, sA, rowbase, xorv, lane, nst, \
+    tc_produce_column<NU>(V, U2, (g.debug & 1) ? 0 : r2, r2 | 1, r3, h, xj, &fempty[fs], empty, full, sA, rowbase, xorv, lane, nst, \
                           ring)
-                switch ((r3 + 1) >> 1) {
+                switch ((r3 + TC_NH - 1) / TC_NH) {
                     case 1: TC_COL(1); break;
                     case 2: TC_COL(2); break;
                     case 3: TC_COL(3); break;
                     case 4: TC_COL(4); break;
                     case 5: TC_COL(5); break;
-                    case 6: TC_COL(6); break;
-                    case 7: TC_COL(7); break;
-                    default: TC_COL(8); break;
+                    default: TC_COL(6); break;
                 }
 #undef TC_COL
                 if (++fs == TC_JR) {
