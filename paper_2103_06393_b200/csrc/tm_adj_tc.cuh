@@ -74,7 +74,8 @@ __device__ __forceinline__ AjTile aj_tile(const AjGeom& g, int64_t t) {
     int64_t rem = t - int64_t(r.c) * per_c;
     r.k = int(rem / g.nrt);
     r.rt = rem - int64_t(r.k) * g.nrt;
-    const int t2 = int(r.rt / g.nt1), t1 = int(r.rt - int64_t(t2) * g.nt1);
+    // i2 block fastest: the resident CTAs share the V rows of one i1 block
+    const int t1 = int(r.rt / g.nt2), t2 = int(r.rt - int64_t(t1) * g.nt2);
     r.i1_0 = t1 * TC_TI1;
     r.i2_0 = t2 * TC_TI2;
     return r;
@@ -354,13 +355,13 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
 // (row tile, 32 i3, k, c), transposed through shared memory so both the
 // read (voxel-contiguous) and the write (i3-contiguous) are coalesced.
 __global__ void __launch_bounds__(256) adj_split_phi_kernel(const float2* __restrict__ phi, int64_t ldphi, int n1,
-                                                            int n2, int n3, int n3p, int q, int p, int nt1,
+                                                            int n2, int n3, int n3p, int q, int p, int nt2,
                                                             int64_t nrt, float* __restrict__ planes) {
     __shared__ float2 tile[TC_ROWS][33];
     const int64_t rt = blockIdx.x;
     const int i3b = blockIdx.y * 32;
     const int k = blockIdx.z % q, c = blockIdx.z / q;
-    const int t2 = int(rt / nt1), t1 = int(rt - int64_t(t2) * nt1);
+    const int t1 = int(rt / nt2), t2 = int(rt - int64_t(t1) * nt2);  // as aj_tile
     const int64_t nv = int64_t(n1) * n2 * n3;
     const float2* src = phi + ldphi * c + int64_t(k) * nv;
     // load: thread -> (row = i1l + 4 i2l in voxel order for coalescing)

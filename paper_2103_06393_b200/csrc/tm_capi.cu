@@ -628,7 +628,7 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     float* planes = static_cast<float*>(s->phiplanes.get(size_t(AJ_APLANES) * p * g.q * R * n3p * sizeof(float)));
     if (int64_t(p) * g.q > 65535) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: too many right-hand sides");
     dim3 sgrid(unsigned(g.nrt), unsigned((n3p + 31) / 32), unsigned(p * g.q));
-    adj_split_phi_kernel<<<sgrid, 256, 0, st>>>(phi, ldphi, g.n1, g.n2, g.n3, int(n3p), g.q, int(p), g.nt1, g.nrt,
+    adj_split_phi_kernel<<<sgrid, 256, 0, st>>>(phi, ldphi, g.n1, g.n2, g.n3, int(n3p), g.q, int(p), g.nt2, g.nrt,
                                                 planes);
     launched(cudaSuccess, "adj_split_phi_kernel");
     const CUtensorMap amap = make_tmap_3d_f32(planes, uint64_t(g.n3), uint64_t(R), uint64_t(AJ_APLANES * p * g.q),

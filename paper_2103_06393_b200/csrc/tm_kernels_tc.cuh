@@ -111,9 +111,11 @@ struct TcTile {
     int c, k, i1_0, i2_0, i3_0;
 };
 
-// Tile order: (i1, i2) fastest, then i3, component, right-hand side — the
-// CTAs resident at one time share (k, i3-block) and so stream the same B
-// planes through L2.
+// Tile order: i3 block fastest, then i2 block, then i1 block, component,
+// right-hand side.  The CTAs resident at one time then share the V rows
+// of their i1 block (read by all n2/TI2 x n3/NMMA tiles of that block —
+// re-reading them from HBM per tile would cost ~200 GB per config-4
+// forward) and stream the same B planes of component k through L2.
 __device__ __forceinline__ TcTile tc_tile(const TcGeom& g, int64_t t) {
     const int64_t per_c = int64_t(g.q) * g.nt3 * g.nt2 * g.nt1;
     TcTile r;
@@ -122,10 +124,10 @@ __device__ __forceinline__ TcTile tc_tile(const TcGeom& g, int64_t t) {
     const int64_t per_k = int64_t(g.nt3) * g.nt2 * g.nt1;
     r.k = int(rem / per_k);
     rem -= int64_t(r.k) * per_k;
-    const int t3 = int(rem / (int64_t(g.nt2) * g.nt1));
-    rem -= int64_t(t3) * g.nt2 * g.nt1;
-    const int t2 = int(rem / g.nt1);
-    const int t1 = int(rem - int64_t(t2) * g.nt1);
+    const int t1 = int(rem / (int64_t(g.nt2) * g.nt3));
+    rem -= int64_t(t1) * g.nt2 * g.nt3;
+    const int t2 = int(rem / g.nt3);
+    const int t3 = int(rem - int64_t(t2) * g.nt3);
     r.i1_0 = t1 * TC_TI1;
     r.i2_0 = t2 * TC_TI2;
     r.i3_0 = t3 * g.nmma;
