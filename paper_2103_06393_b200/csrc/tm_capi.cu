@@ -21,6 +21,7 @@
 #include "tm_kernels_cc.cuh"
 #include "tm_kernels_tc.cuh"
 #include "tm_adj_tc.cuh"
+#include "tm_mrhs_tc.cuh"
 #include "tm_tmap.h"
 
 using namespace tmb;
@@ -136,7 +137,7 @@ struct tm_store {
     int64_t kpad = 0;
     CUtensorMap bmap{};
     std::mutex mu;
-    DevBuf part, xin, yout, wbuf, phiplanes;
+    DevBuf part, xin, yout, wbuf, phiplanes, xplanes;
 
     int64_t nv() const { return dims[0] * dims[1] * dims[2]; }
     int64_t rows() const { return q * nv(); }
@@ -207,10 +208,11 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
         TcDesc& c = tcd[static_cast<size_t>(t)];
         c.off_v = voff;
         c.off_u2 = u2off;
+        c.off_u3 = d.off_u3;
         u2off += n2p * (d.r2 | 1);
         c.r2 = d.r2;
         c.r3 = d.r3;
-        c.pad0 = c.pad1 = 0;
+        c.pad0 = c.pad1 = c.pad2 = c.pad3 = 0;
         voff += n1p * d.r2 * d.r3;
     }
     // adjoint chunks: whole columns, at most AJ_CH (j, c) slots each
@@ -572,7 +574,59 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     launched(cudaSuccess, "fwd_tc_kernel");
 }
 
-void forward_dev(const tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy, cudaStream_t st) {
+// Batched multi-RHS forward (tm_mrhs_tc.cuh) for c64 stores at p >= 3,
+// in blocks of MR_P right-hand sides.
+bool mrhs_ok(const tm_store* s, int64_t p) {
+    const char* e = std::getenv("TMB_DISABLE_MRHS");
+    if (e && e[0] == '1') return false;
+    return s->tc_ok && p >= 3;
+}
+
+void run_forward_mrhs(tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy, cudaStream_t st) {
+    MrGeom g{};
+    g.ncols = s->ncols;
+    g.n1 = int(s->dims[0]);
+    g.n2 = int(s->dims[1]);
+    g.n3 = int(s->dims[2]);
+    g.q = s->q;
+    g.nt2 = (g.n2 + MR_TI2 - 1) / MR_TI2;
+    g.nt3 = (g.n3 + MR_TI3 - 1) / MR_TI3;
+    g.ntiles = int64_t(g.q) * g.n1 * g.nt2 * g.nt3;
+    g.nks = int((s->ncols + 7) / 8);
+    g.chain = tc_chain();
+    g.v_off = 64;
+    g.u2_off = g.v_off + TC_TI1 * s->rmax[1] * s->rmax[2] * 16;
+    g.u3_off = g.u2_off + MR_TI2 * (s->rmax[1] | 1) * 8;
+    g.slot_bytes = (g.u3_off + int(round16(uint32_t(MR_TI3 * s->rmax[2]) * 8u)) + 127) / 128 * 128;
+    const size_t smem = 1024 + size_t(MR_NST) * (MR_A_STAGE + MR_B_STAGE) + size_t(MR_JR) * g.slot_bytes +
+                        size_t(2) * MR_TI2 * MR_WLD * sizeof(float4) + (2 * MR_NST + 2 * MR_JR + 2) * 8 + 16;
+    if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "batched forward: shared-memory plan too large");
+    CK(cudaFuncSetAttribute(fwd_mrhs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const int64_t mp = (s->ncols + 3) / 4 * 4;
+    float* planes = static_cast<float*>(s->xplanes.get(size_t(TC_BPLANES) * MR_P * mp * sizeof(float)));
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const unsigned grid = unsigned(std::min<int64_t>(g.ntiles, num_sms(dev)));
+    for (int64_t c0 = 0; c0 < p; c0 += MR_P) {
+        const int pb = int(std::min<int64_t>(MR_P, p - c0));
+        const unsigned sblocks = unsigned(std::min<int64_t>((MR_P * mp + 255) / 256, 4096));
+        mrhs_split_x_kernel<<<sblocks, 256, 0, st>>>(x + ldx * c0, ldx, s->ncols, pb, mp, planes);
+        launched(cudaSuccess, "mrhs_split_x_kernel");
+        const CUtensorMap xmap = make_tmap_3d_f32(planes, uint64_t(mp), uint64_t(MR_P), uint64_t(TC_BPLANES),
+                                                  uint64_t(mp) * 4, uint64_t(MR_P) * mp * 4, 8, MR_P,
+                                                  CU_TENSOR_MAP_SWIZZLE_32B);
+        fwd_mrhs_kernel<<<grid, MR_THREADS, smem, st>>>(xmap, s->d_tcd, s->d_varena, s->d_u2arena,
+                                                         static_cast<const float2*>(s->d_arena), g, y + ldy * c0, ldy,
+                                                         pb);
+        launched(cudaSuccess, "fwd_mrhs_kernel");
+    }
+}
+
+void forward_dev(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy, cudaStream_t st) {
+    if (s->tc_ok && !tc_disabled() && mrhs_ok(s, p)) {
+        run_forward_mrhs(s, static_cast<const float2*>(x), ldx, p, static_cast<float2*>(y), ldy, st);
+        return;
+    }
     if (s->tc_ok && !tc_disabled()) {
         run_forward_tc(s, static_cast<const float2*>(x), ldx, p, static_cast<float2*>(y), ldy, st);
         return;

@@ -74,12 +74,15 @@ constexpr int TC_BPLANES = 6;                // B planes: [-U3i, U3r, U3i] x {hi
 // complex stored as (vr, vi, -vi, vr) (the FFMA2 operand form); off_u2:
 // float2 offset of the tensor's U2 copy in the U2 arena, n2 rounded up to
 // TI2 rows (zero rows past n2) with an odd row stride r2 | 1 (conflict-free
-// 32-lane row loads).
+// 32-lane row loads); pad0: the (j, c) slot of the column inside its
+// adjoint chunk.
 struct TcDesc {
     int64_t off_v;
     int64_t off_u2;
-    int32_t r2, r3, pad0, pad1;
+    int64_t off_u3;  // float2 offset of U3t (n3 x r3 row-major) in the store arena
+    int32_t r2, r3, pad0, pad1, pad2, pad3;
 };
+static_assert(sizeof(TcDesc) % 16 == 0, "TcDesc is bulk-copied (16-byte granularity)");
 
 struct TcGeom {
     int64_t ncols;
