@@ -60,6 +60,7 @@ struct AjGeom {
     int rmax2, rmax3;
     int slot_bytes, u2_off;
     int maxch;       // chunk stride of the chunk-start table
+    int64_t t_begin, t_end;  // tile range of this launch
 };
 
 struct AjTile {
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         // ------------------------------------------------------- TMA producer
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
-            for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
                 const AjTile tl = aj_tile(g, t);
                 const int nc = nch[tl.k];
                 const int arow = int(tl.rt * TC_ROWS);
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         if (elect_one()) {
             const uint32_t idesc = umma_idesc_tf32(TC_ROWS, 2 * AJ_CH, false, false);
             uint32_t s = 0, ph = 0, nq = 0;
-            for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
                 const AjTile tl = aj_tile(g, t);
                 const int nc = nch[tl.k];
                 for (int n = 0; n < nc; ++n, ++nq) {
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         // ---------------------------------------------------- factor loader
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
-            for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
                 const AjTile tl = aj_tile(g, t);
                 const TcDesc* tdk = tcd + int64_t(tl.k) * g.ncols;
                 for (int64_t j = 0; j < g.ncols; ++j) {
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         const int ctid = threadIdx.x - TC_PW0 * 32;  // 0..255
         const uint32_t lane_addr = uint32_t(i1l * 32) << 16;
         uint32_t fs = 0, fph = 0, nq = 0;
-        for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+        for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
             const AjTile tl = aj_tile(g, t);
             const int nc = nch[tl.k];
             const int* cs = cstart + int64_t(tl.k) * (g.maxch + 1);

@@ -137,7 +137,7 @@ struct tm_store {
     int64_t kpad = 0;
     CUtensorMap bmap{};
     std::mutex mu;
-    DevBuf part, xin, yout, wbuf, phiplanes, xplanes;
+    DevBuf part, xin, yout, wbuf, phiplanes, xplanes, rsum;
 
     int64_t nv() const { return dims[0] * dims[1] * dims[2]; }
     int64_t rows() const { return q * nv(); }
@@ -173,7 +173,7 @@ bool tc_disabled() {
 int tc_chain() {
     const char* e = std::getenv("TMB_TC_CHAIN");
     const int v = e ? std::atoi(e) : 0;
-    return v > 0 ? v : 12;
+    return v > 0 ? v : 16;
 }
 
 // B planes of the tensor-core forward (see tm_kernels_tc.cuh), built once.
@@ -544,14 +544,15 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     g.nt1 = (g.n1 + TC_TI1 - 1) / TC_TI1;
     g.nt2 = (g.n2 + TC_TI2 - 1) / TC_TI2;
     g.nmma = std::min(TC_NMAX, (g.n3 + 15) / 16 * 16);
-    g.nt3 = (g.n3 + g.nmma - 1) / g.nmma;
+    g.nh3 = g.n3 > TC_NMAX ? 2 : 1;
+    g.nt3 = (g.n3 + g.nmma * g.nh3 - 1) / (g.nmma * g.nh3);
     g.p = int(p);
     g.ntiles = int64_t(p) * g.q * g.nt3 * g.nt2 * g.nt1;
     g.rmax2 = s->rmax[1];
     g.rmax3 = s->rmax[2];
     g.u2_off = TC_SLOT_V + TC_TI1 * g.rmax2 * g.rmax3 * 16;
     g.slot_bytes = (g.u2_off + TC_TI2 * (g.rmax2 | 1) * 8 + 127) / 128 * 128;
-    g.b_stage = TC_BPLANES * g.nmma * 32;
+    g.b_stage = g.nh3 * TC_FPLANES * g.nmma * 32;
     g.chain = tc_chain();
     {
         const char* dbg = std::getenv("TMB_TC_DEBUG");
@@ -562,16 +563,28 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
                (2 * TC_NST_MAX + 2 * TC_JR + 2) * 8 + 16;
     };
     g.nst = TC_NST_MAX;
-    while (g.nst > 3 && smem_for(g.nst) > kSmemMax) --g.nst;
+    while (g.nst > 2 && smem_for(g.nst) > kSmemMax) --g.nst;
     const size_t smem = smem_for(g.nst);
     if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core forward: shared-memory plan too large");
     CK(cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int dev = 0;
     CK(cudaGetDevice(&dev));
     const unsigned grid = unsigned(std::min<int64_t>(g.ntiles, num_sms(dev)));
-    fwd_tc_kernel<<<grid, TC_THREADS, smem, st>>>(s->bmap, s->d_tcd, s->d_varena, s->d_u2arena, s->d_kc, g, x, ldx,
-                                                   y, ldy);
-    launched(cudaSuccess, "fwd_tc_kernel");
+    float2* rsum = static_cast<float2*>(
+        const_cast<tm_store*>(s)->rsum.get(size_t(grid) * g.nmma * g.nh3 * TC_ROWS * sizeof(float2)));
+    // One launch per wave of `grid` tiles: every CTA starts its tile at the
+    // same time, so the CTAs of one component stream its B planes (184 MB
+    // per component at config 4, more than L2) in K-lockstep and share them
+    // in L2.  A persistent schedule over all tiles drifts apart by the
+    // per-component cost differences and re-reads B from HBM (725 GB per
+    // config-4 forward, measured).
+    for (int64_t t0 = 0; t0 < g.ntiles; t0 += grid) {
+        g.t_begin = t0;
+        g.t_end = std::min<int64_t>(g.ntiles, t0 + grid);
+        fwd_tc_kernel<<<grid, TC_THREADS, smem, st>>>(s->bmap, s->d_tcd, s->d_varena, s->d_u2arena, s->d_kc, g, x,
+                                                       ldx, y, ldy, rsum);
+        launched(cudaSuccess, "fwd_tc_kernel");
+    }
 }
 
 // Batched multi-RHS forward (tm_mrhs_tc.cuh) for c64 stores at p >= 3,
@@ -615,6 +628,8 @@ void run_forward_mrhs(tm_store* s, const float2* x, int64_t ldx, int64_t p, floa
         const CUtensorMap xmap = make_tmap_3d_f32(planes, uint64_t(mp), uint64_t(MR_P), uint64_t(TC_BPLANES),
                                                   uint64_t(mp) * 4, uint64_t(MR_P) * mp * 4, 8, MR_P,
                                                   CU_TENSOR_MAP_SWIZZLE_32B);
+        g.t_begin = 0;
+        g.t_end = g.ntiles;
         fwd_mrhs_kernel<<<grid, MR_THREADS, smem, st>>>(xmap, s->d_tcd, s->d_varena, s->d_u2arena,
                                                          static_cast<const float2*>(s->d_arena), g, y + ldy * c0, ldy,
                                                          pb);
@@ -694,9 +709,13 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     int dev = 0;
     CK(cudaGetDevice(&dev));
     const unsigned grid = unsigned(std::min<int64_t>(g.ntiles, num_sms(dev)));
-    adj_tc_kernel<<<grid, AJ_THREADS, smem, st>>>(amap, s->adj_bmap, s->d_tcd, s->d_varena, s->d_u2arena, s->d_nch,
-                                                   s->d_cstart, g, part);
-    launched(cudaSuccess, "adj_tc_kernel");
+    for (int64_t t0 = 0; t0 < g.ntiles; t0 += grid) {  // one launch per wave (see run_forward_tc)
+        g.t_begin = t0;
+        g.t_end = std::min<int64_t>(g.ntiles, t0 + grid);
+        adj_tc_kernel<<<grid, AJ_THREADS, smem, st>>>(amap, s->adj_bmap, s->d_tcd, s->d_varena, s->d_u2arena,
+                                                       s->d_nch, s->d_cstart, g, part);
+        launched(cudaSuccess, "adj_tc_kernel");
+    }
     const int64_t warps = s->ncols * p;
     const unsigned blocks = unsigned((warps * 32 + 255) / 256);
     adj_reduce_kernel<float2><<<blocks, 256, 0, st>>>(part, s->ncols, p, nred, z, ldz);

@@ -1,7 +1,7 @@
 // Tensor-core (tcgen05, kind::tf32, 3xTF32 split) forward kernel, complex64.
 //
 // Forward of component k, for one output tile of ROWS = 128 voxel rows
-// (TI1 x TI2 = 4 x 32 of (i1, i2)) times NMMA <= 128 voxels along mode 3:
+// (TI1 x TI2 = 4 x 32 of (i1, i2)) times up to 2 x 128 voxels along mode 3:
 //
 //   Y[row, i3] = sum_j sum_r W_j[row, r] U3_j[i3, r],
 //   W_j[row, r] = sum_b V_j[i1, b, r] U2_j[i2, b],  V_j = x_j (U1_j x_1 G_j),
@@ -28,10 +28,14 @@
 // accumulator over the whole K stream (~45 000 terms per component at
 // config 4) drifts toward zero linearly in K.  The K stream
 // is therefore cut into chains of `chain` stages: each chain accumulates
-// from zero in TMEM columns [0, 256) and is then folded (round-to-nearest
-// fp32 adds) into a running sum at TMEM columns [256, 512) by 4 dedicated
-// fold warps; the tile's last chain is added to the running sum on its way
-// to y.  The error is then set by the chain length, not by K.
+// from zero in TMEM and is then folded (round-to-nearest fp32 adds) by 4
+// dedicated fold warps into a running sum held in a per-CTA scratch in
+// global memory (L2-resident, [i3][row] so the fold is coalesced; the CTA
+// owns its tile, so the fold is deterministic); the tile's last chain is
+// added to the running sum on its way to y.  The error is then set by the
+// chain length, not by K.  Keeping the running sum out of TMEM lets a tile
+// span 2 x 128 voxels along mode 3 (all 512 TMEM columns hold [Yr|Yi] of
+// the two halves), so each produced W element feeds twice the MMA work.
 //
 // Warp roles (640 threads, 1 CTA / SM, persistent over tiles):
 //   warp 0      TMA producer of the B planes
@@ -53,7 +57,7 @@
 namespace tmb {
 
 constexpr int TC_TI1 = 4, TC_TI2 = 32, TC_ROWS = 128;
-constexpr int TC_NST_MAX = 4;   // A/B stages (8 K each)
+constexpr int TC_NST_MAX = 5;   // A/B stages (8 K each)
 constexpr int TC_JR = 3;        // factor-ring slots
 constexpr int TC_NPW = 12;      // producer warps: 4 i1 rows x TC_NH c partitions
 constexpr int TC_NH = TC_NPW / TC_TI1;
@@ -66,7 +70,8 @@ constexpr int TC_A_PLANE = TC_ROWS * 32;     // bytes (128 rows x 8 tf32)
 constexpr int TC_A_STAGE = 4 * TC_A_PLANE;   // 16 KB
 constexpr uint32_t TC_RUN_COL = 256;         // TMEM column of the running sum
 constexpr int TC_SLOT_V = 128;               // byte offset of the V block in a factor slot
-constexpr int TC_BPLANES = 6;                // B planes: [-U3i, U3r, U3i] x {hi, lo}
+constexpr int TC_BPLANES = 6;                // B planes in HBM: [-U3i, U3r, U3i] x {hi, lo}
+constexpr int TC_FPLANES = 4;                // forward B planes per stage: [U3r, U3i] x {hi, lo}
 
 // Per-tensor descriptor of the tensor-core forward (component-major like
 // TDesc).  off_v: float4 offset of the tensor's mode-1 product
@@ -88,7 +93,8 @@ struct TcGeom {
     int64_t ncols;
     int n1, n2, n3, q;
     int nt1, nt2, nt3;
-    int nmma;       // N per MMA = i3 per tile (multiple of 16, <= 128)
+    int nmma;       // i3 per half tile = N of the narrow MMAs (multiple of 16, <= 128)
+    int nh3;        // i3 halves per tile (1 or 2): a tile spans nh3 * nmma voxels along mode 3
     int p;          // right-hand sides
     int64_t ntiles;
     int rmax2, rmax3;
@@ -98,6 +104,7 @@ struct TcGeom {
     int nst;                    // A/B stages in the ring (3..TC_NST_MAX)
     int chain;                  // K stages per TMEM accumulation chain
     int debug;                  // diagnostics (TMB_TC_DEBUG): 1 = no mode-2 work, 2 = no B loads
+    int64_t t_begin, t_end;     // tile range of this launch (one wave: see run_forward_tc)
 };
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -133,7 +140,7 @@ __device__ __forceinline__ TcTile tc_tile(const TcGeom& g, int64_t t) {
     const int t3 = int(rem - int64_t(t2) * g.nt3);
     r.i1_0 = t1 * TC_TI1;
     r.i2_0 = t2 * TC_TI2;
-    r.i3_0 = t3 * g.nmma;
+    r.i3_0 = t3 * g.nmma * g.nh3;
     return r;
 }
 
@@ -228,7 +235,8 @@ __device__ __forceinline__ void tc_produce_column(const float4* __restrict__ V, 
 __global__ void __launch_bounds__(TC_THREADS, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap bmap, const TcDesc* __restrict__ tcd,
                   const float4* __restrict__ varena, const float2* __restrict__ u2arena, const int* __restrict__ kc,
-                  TcGeom g, const float2* __restrict__ x, int64_t ldx, float2* __restrict__ y, int64_t ldy) {
+                  TcGeom g, const float2* __restrict__ x, int64_t ldx, float2* __restrict__ y, int64_t ldy,
+                  float2* __restrict__ rsum) {
     using namespace sm100;
     extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
     // align to 1024 B by offsetting the shared array itself (keeps the
@@ -272,8 +280,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // ------------------------------------------------ B-plane TMA producer
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
-            const int plane_bytes = g.b_stage / TC_BPLANES;
-            for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+            const int plane_bytes = g.nmma * 32;
+            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
                 const TcTile tl = tc_tile(g, t);
                 const int nks = (kc[tl.k] + 7) >> 3;
                 for (int kk = 0; kk < nks; ++kk) {
@@ -283,9 +291,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     } else {
                         mbar_arrive_expect_tx(&full[s], uint32_t(g.b_stage));
                         unsigned char* dst = sB + s * g.b_stage;
+                        // per i3 half: HBM planes 1, 2 (U3r, U3i hi) and 4, 5 (lo) -> smem 0..3
+                        for (int hh = 0; hh < g.nh3; ++hh)
 #pragma unroll
-                        for (int pl = 0; pl < TC_BPLANES; ++pl)
-                            tma_load_3d(dst + pl * plane_bytes, &bmap, &full[s], kk * 8, tl.i3_0, pl * g.q + tl.k);
+                            for (int pl = 0; pl < TC_FPLANES; ++pl)
+                                tma_load_3d(dst + (hh * TC_FPLANES + pl) * plane_bytes, &bmap, &full[s], kk * 8,
+                                            tl.i3_0 + hh * g.nmma, (1 + pl + (pl >> 1)) * g.q + tl.k);
                     }
                     if (++s == nst) {
                         s = 0;
@@ -297,15 +308,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer
         if (elect_one()) {
-            // complex product as one real GEMM of width 2 NMMA:
-            //   [Yr | Yi] += Ar . [U3r | U3i] + Ai . [-U3i | U3r]
-            // with the B planes staged [-U3i][U3r][U3i] (hi) and the same
-            // (lo), so both operands are contiguous 2-plane windows.
-            const uint32_t idesc = umma_idesc_tf32(TC_ROWS, 2 * g.nmma, false, false);
-            const int plane_b = g.b_stage / TC_BPLANES;
-            const uint32_t yd = tmem;
+            // complex product per i3 half hh (TMEM columns 2 NMMA hh + [0, 2 NMMA)):
+            //   [Yr | Yi] += Ar . [U3r | U3i]   (one MMA of width 2 NMMA)
+            //   Yr -= Ai . U3i,  Yi += Ai . U3r (width NMMA, negate-A bit)
+            // each as hi.hi + hi.lo + lo.hi; smem B planes per half:
+            // U3r hi, U3i hi, U3r lo, U3i lo
+            const uint32_t id_w = umma_idesc_tf32(TC_ROWS, 2 * g.nmma, false, false);
+            const uint32_t id_p = umma_idesc_tf32(TC_ROWS, g.nmma, false, false);
+            const uint32_t id_n = umma_idesc_tf32(TC_ROWS, g.nmma, true, false);
+            const int plane_b = g.nmma * 32;
             uint32_t s = 0, ph = 0, gch = 0;
-            for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
                 const TcTile tl = tc_tile(g, t);
                 const int nks = (kc[tl.k] + 7) >> 3;
                 int cpos = 0;  // stage position inside the current chain
@@ -322,18 +335,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     uint64_t A[4];
 #pragma unroll
                     for (int pl = 0; pl < 4; ++pl) A[pl] = umma_smem_desc(a0 + pl * TC_A_PLANE, 256, 6);
-                    // B windows: hi [U3r|U3i] at plane 1, [-U3i|U3r] at plane 0; lo at +3
-                    const uint64_t B1h = umma_smem_desc(b0 + 1 * plane_b, 256, 6);
-                    const uint64_t B2h = umma_smem_desc(b0 + 0 * plane_b, 256, 6);
-                    const uint64_t B1l = umma_smem_desc(b0 + 4 * plane_b, 256, 6);
-                    const uint64_t B2l = umma_smem_desc(b0 + 3 * plane_b, 256, 6);
                     const uint32_t acc = cpos > 0 ? 1u : 0u;
-                    mma_tf32(yd, A[0], B1h, idesc, acc);
-                    mma_tf32(yd, A[0], B1l, idesc, 1);
-                    mma_tf32(yd, A[1], B1h, idesc, 1);
-                    mma_tf32(yd, A[2], B2h, idesc, 1);
-                    mma_tf32(yd, A[2], B2l, idesc, 1);
-                    mma_tf32(yd, A[3], B2h, idesc, 1);
+                    for (int hh = 0; hh < g.nh3; ++hh) {
+                        const uint32_t bh = b0 + uint32_t(hh * TC_FPLANES * plane_b);
+                        const uint64_t Brh = umma_smem_desc(bh + 0 * plane_b, 256, 6);  // [U3r|U3i] hi window
+                        const uint64_t Bih = umma_smem_desc(bh + 1 * plane_b, 256, 6);
+                        const uint64_t Brl = umma_smem_desc(bh + 2 * plane_b, 256, 6);  // [U3r|U3i] lo window
+                        const uint64_t Bil = umma_smem_desc(bh + 3 * plane_b, 256, 6);
+                        const uint32_t yr = tmem + uint32_t(2 * g.nmma * hh), yi = yr + uint32_t(g.nmma);
+                        mma_tf32(yr, A[0], Brh, id_w, acc);
+                        mma_tf32(yr, A[0], Brl, id_w, 1);
+                        mma_tf32(yr, A[1], Brh, id_w, 1);
+                        mma_tf32(yr, A[2], Bih, id_n, 1);
+                        mma_tf32(yr, A[2], Bil, id_n, 1);
+                        mma_tf32(yr, A[3], Bih, id_n, 1);
+                        mma_tf32(yi, A[2], Brh, id_p, 1);
+                        mma_tf32(yi, A[2], Brl, id_p, 1);
+                        mma_tf32(yi, A[3], Brh, id_p, 1);
+                    }
                     mma_commit(&empty[s]);
                     if (++s == nst) {
                         s = 0;
@@ -352,7 +371,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // ---------------------------------------------------- factor loader
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
-            for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
                 const TcTile tl = tc_tile(g, t);
                 const TcDesc* tdk = tcd + int64_t(tl.k) * g.ncols;
                 for (int64_t j = 0; j < g.ncols; ++j) {
@@ -385,7 +404,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t rowbase = uint32_t(row) * 32u, xorv = (uint32_t(row) & 4u) << 2;
         ARing ring{0, 0, 0};
         uint32_t fs = 0, fph = 0;
-        for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+        for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
             const TcTile tl = tc_tile(g, t);
             const float2* xc = x + ldx * tl.c;
             for (int64_t j = 0; j < g.ncols; ++j) {
@@ -428,16 +447,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
         }
     } else if (warp >= TC_FW0) {
-        const int quarter = warp & 3;             // TMEM lane quarter
+        // ------------------------------------------ chain fold + epilogue
+        // The running sum of the tile lives in this CTA's private scratch
+        // rsum[blockIdx.x][i3][row] (L2-resident, row-contiguous so a warp's
+        // 32 rows are one coalesced 256-byte access); every chain is added
+        // to it with round-to-nearest fp32 adds, the last one goes to y.
+        const int quarter = warp & 3;             // TMEM lane quarter = i1 of the tile
         const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
-        const uint32_t tC = tmem + lane_addr, tR = tmem + lane_addr + TC_RUN_COL;
+        const uint32_t tC = tmem + lane_addr;
+        const int row = lane + 32 * quarter;      // row = i2 + 32 i1
+        const int span = g.nmma * g.nh3;
+        float2* rs = rsum + int64_t(blockIdx.x) * span * TC_ROWS + row;
         const int64_t nv3 = int64_t(g.n1) * g.n2 * g.n3;
         uint32_t gch = 0;
-        for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+        for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
             const TcTile tl = tc_tile(g, t);
             const int nks = (kc[tl.k] + 7) >> 3;
             const int nch = (nks + g.chain - 1) / g.chain;
-            const int ei1 = tl.i1_0 + quarter, ei2 = tl.i2_0 + lane;  // row = i2 + 32 i1
+            const int ei1 = tl.i1_0 + quarter, ei2 = tl.i2_0 + lane;
             const bool eok = ei1 < g.n1 && ei2 < g.n2;
             float2* yp = y + ldy * tl.c + int64_t(tl.k) * nv3 + ei1 + int64_t(g.n1) * ei2;
             const int64_t pl = int64_t(g.n1) * g.n2;
@@ -445,36 +472,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 mbar_wait(cfull, gch & 1);
                 tc_fence_after();
                 const bool last = ch == nch - 1;
-                for (int cb = 0; cb < g.nmma; cb += 16) {
-                    uint32_t cr[16], ci[16];
-                    tmem_ld16(tC + uint32_t(cb), cr);
-                    tmem_ld16(tC + uint32_t(g.nmma + cb), ci);
-                    if (ch > 0) {
-                        uint32_t rr[16], ri[16];
-                        tmem_ld16(tR + uint32_t(cb), rr);
-                        tmem_ld16(tR + uint32_t(g.nmma + cb), ri);
+                for (int hh = 0; hh < g.nh3; ++hh)
+                    for (int cb = 0; cb < g.nmma; cb += 16) {
+                        uint32_t cr[16], ci[16];
+                        const uint32_t col = uint32_t(2 * g.nmma * hh + cb);
+                        tmem_ld16(tC + col, cr);
+                        tmem_ld16(tC + col + uint32_t(g.nmma), ci);
                         tmem_ld_wait();
+                        const int i3l = hh * g.nmma + cb;
+                        float2* rp = rs + int64_t(i3l) * TC_ROWS;
+                        if (ch > 0) {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            cr[i] = __float_as_uint(__uint_as_float(cr[i]) + __uint_as_float(rr[i]));
-                            ci[i] = __float_as_uint(__uint_as_float(ci[i]) + __uint_as_float(ri[i]));
+                            for (int i = 0; i < 16; ++i) {
+                                const float2 r = rp[int64_t(i) * TC_ROWS];
+                                cr[i] = __float_as_uint(__uint_as_float(cr[i]) + r.x);
+                                ci[i] = __float_as_uint(__uint_as_float(ci[i]) + r.y);
+                            }
                         }
-                    } else {
-                        tmem_ld_wait();
-                    }
-                    if (!last) {
-                        tmem_st16(tR + uint32_t(cb), cr);
-                        tmem_st16(tR + uint32_t(g.nmma + cb), ci);
-                    } else if (eok) {
+                        if (!last) {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const int i3 = tl.i3_0 + cb + i;
-                            if (i3 < g.n3)
-                                yp[pl * i3] = make_float2(__uint_as_float(cr[i]), __uint_as_float(ci[i]));
+                            for (int i = 0; i < 16; ++i)
+                                rp[int64_t(i) * TC_ROWS] = make_float2(__uint_as_float(cr[i]), __uint_as_float(ci[i]));
+                        } else if (eok) {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) {
+                                const int i3 = tl.i3_0 + i3l + i;
+                                if (i3 < g.n3)
+                                    yp[pl * i3] = make_float2(__uint_as_float(cr[i]), __uint_as_float(ci[i]));
+                            }
                         }
                     }
-                }
-                if (!last) tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(cfree);

@@ -55,6 +55,7 @@ struct MrGeom {
     int nks;          // stages per tile (ceil(ncols / 8))
     int chain;
     int slot_bytes, v_off, u2_off, u3_off;  // slot layout (bytes)
+    int64_t t_begin, t_end;  // tile range of this launch
 };
 
 struct MrTile {
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(MR_THREADS, 1)
         // ------------------------------------------------ X-plane TMA producer
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
-            for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
                 for (int kk = 0; kk < g.nks; ++kk) {
                     mbar_wait(&empty[s], ph ^ 1);
                     mbar_arrive_expect_tx(&full[s], uint32_t(MR_B_STAGE));
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(MR_THREADS, 1)
         if (elect_one()) {
             const uint32_t idesc = umma_idesc_tf32(128, 2 * MR_P, false, false);
             uint32_t s = 0, ph = 0, gch = 0;
-            for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
                 int cpos = 0;
                 for (int kk = 0; kk < g.nks; ++kk) {
                     if (cpos == 0) {
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(MR_THREADS, 1)
         // ---------------------------------------------------- factor loader
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
-            for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
                 const MrTile tl = mr_tile(g, t);
                 const TcDesc* tdk = tcd + int64_t(tl.k) * g.ncols;
                 for (int64_t j = 0; j < g.ncols; ++j) {
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(MR_THREADS, 1)
             aoff[e] = uint32_t(mt * MR_A_MT + ln * 32);
             xorv[e] = (uint32_t(ln) & 4u) << 2;
         }
-        for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+        for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
             const MrTile tl = mr_tile(g, t);
             const bool i2ok = tl.i2_0 + i2a < g.n2;
             for (int64_t j = 0; j < g.ncols; ++j) {
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(MR_THREADS, 1)
         const int64_t nv3 = int64_t(g.n1) * g.n2 * g.n3;
         const int nch = (g.nks + g.chain - 1) / g.chain;
         uint32_t gch = 0;
-        for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+        for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
             const MrTile tl = mr_tile(g, t);
             const int i2 = tl.i2_0 + i2l;
             for (int ch = 0; ch < nch; ++ch, ++gch) {
