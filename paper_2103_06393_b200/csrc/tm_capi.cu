@@ -173,7 +173,9 @@ bool tc_disabled() {
 int tc_chain() {
     const char* e = std::getenv("TMB_TC_CHAIN");
     const int v = e ? std::atoi(e) : 0;
-    return v > 0 ? v : 16;
+    // 24 stages x 6 truncating MMAs per accumulator: 2.9e-6 at config 4
+    // (8: 1.2e-6, 16: 2.0e-6, 32: 3.9e-6, 48: 5.8e-6 — tools/validate_full.py)
+    return v > 0 ? v : 24;
 }
 
 // B planes of the tensor-core forward (see tm_kernels_tc.cuh), built once.

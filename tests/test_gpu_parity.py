@@ -242,7 +242,7 @@ def test_tensor_core_forward(oracle, product, monkeypatch, dims, q, m, rmin, rma
     assert rel(z_cc, z_ref) <= 1e-5
 
 
-@pytest.mark.parametrize("chain", ["", "1", "3"])
+@pytest.mark.parametrize("chain", ["", "1", "3", "48"])
 def test_tensor_core_long_k(product, monkeypatch, chain):
     """Accumulation over a long K stream (2 500 columns, K ~ 21 000 per
     component): the chained TMEM accumulation must stay within 1e-5 of the

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--sample-cols", type=int, default=4)
     ap.add_argument("--no-oracle", action="store_true")
+    ap.add_argument("--chains", default="", help="comma list of TMB_TC_CHAIN values to also check")
     args = ap.parse_args()
     import torch
     from paper_2103_06393_b200 import DeviceStore
@@ -74,6 +75,10 @@ def main():
     out["forward_rel_l2_default_vs_c128"] = rel(y_tc.to(torch.complex128), y_ref)
     out["adjoint_rel_l2_default_vs_c128"] = rel(z_tc.to(torch.complex128), z_ref)
     out["forward_rel_l2_cudacore_vs_c128"] = rel(y_cc.to(torch.complex128), y_ref)
+    for ch in [c for c in args.chains.split(",") if c]:
+        os.environ["TMB_TC_CHAIN"] = ch
+        out[f"forward_rel_l2_chain{ch}_vs_c128"] = rel(s64.forward(xd).to(torch.complex128), y_ref)
+        os.environ.pop("TMB_TC_CHAIN")
     out["adjoint_rel_l2_cudacore_vs_c128"] = rel(z_cc.to(torch.complex128), z_ref)
 
     if not args.no_oracle:
