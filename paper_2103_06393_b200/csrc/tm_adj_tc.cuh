@@ -13,8 +13,11 @@
 // product runs as one real GEMM of width 256:
 //   [Qi | Qr] += Phir . [-U3i | U3r] + Phii . [U3r | U3i]
 // with the B planes staged [-U3i][U3r][U3i] (hi and lo, i3-contiguous
-// chunk-aligned copy built once per store) and the A planes the 3xTF32
-// split of the Phi tile (built per call by adj_split_phi_kernel).  Both
+// chunk-aligned copy built once per store) and the A planes the split of
+// the Phi tile (built per call by adj_split_phi_kernel), both as scaled
+// 2-term fp16 splits on tcgen05.mma.kind::f16 (K = 16 per MMA: half the
+// MMAs and half the operand bytes of 3xTF32 at the same 22-bit operand
+// precision; products hi.hi + hi.lo + lo.hi accumulate in fp32).  Both
 // operands arrive by TMA; Q is accumulated in TMEM (two 256-column buffers,
 // ping-pong over chunks).
 //
@@ -31,11 +34,28 @@
 // so results are bitwise reproducible.
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "tm_common.cuh"
 #include "tm_kernels_tc.cuh"
 #include "tm_sm100.cuh"
 
 namespace tmb {
+
+// fp16 operand scaling of the adjoint GEMM.  Both operands are stored as a
+// 2-term fp16 split (hi = fp16(v), lo = fp16(v - hi): 22 significant bits,
+// the class of the 3xTF32 split) scaled by powers of two so their values sit
+// inside fp16's normal range: U3 (orthonormal columns, |u| <= 1) by 2^12,
+// Phi by 2^(14 - e) with max|Phi| < 2^e (measured per call).  Q in TMEM is
+// then scaled by both factors, undone exactly on the fp32 partial sums.
+constexpr float AJ_U3_SCALE = 4096.f;
+__host__ __device__ inline float aj_phi_scale(float amax) {
+    if (!(amax > 0.f) || !(amax < 3.0e38f)) return 1.f;
+    int e = 0;
+    frexpf(amax, &e);  // amax < 2^e
+    e = e < -100 ? -100 : (e > 100 ? 100 : e);
+    return ldexpf(1.f, 14 - e);
+}
 
 constexpr int AJ_NST = 4;        // A/B stages (8 i3 each)
 constexpr int AJ_CH = 128;       // (j, c) slots per chunk
@@ -56,7 +76,7 @@ struct AjGeom {
     int p;
     int64_t nrt;     // row tiles per component
     int64_t ntiles;  // p * q * nrt
-    int nks;         // K steps (8 i3 each) per chunk
+    int nks;         // K steps (16 i3 each) per chunk
     int rmax2, rmax3;
     int slot_bytes, u2_off;
     int maxch;       // chunk stride of the chunk-start table
@@ -133,7 +153,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
     adj_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                   const TcDesc* __restrict__ tcd, const float4* __restrict__ varena,
                   const float2* __restrict__ u2arena, const int* __restrict__ nch, const int* __restrict__ cstart,
-                  AjGeom g, float2* __restrict__ part) {
+                  AjGeom g, const float* __restrict__ phimax, float2* __restrict__ part) {
     using namespace sm100;
     extern __shared__ __align__(1024) unsigned char aj_smem_raw[];
     unsigned char* sm = aj_smem_raw + ((1024u - (smem_u32(aj_smem_raw) & 1023u)) & 1023u);
@@ -192,11 +212,11 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                         unsigned char* db = sB + s * AJ_B_STAGE;
 #pragma unroll
                         for (int pl = 0; pl < AJ_APLANES; ++pl)
-                            tma_load_3d(da + pl * AJ_A_PLANE, &amap, &full[s], kk * 8, arow,
+                            tma_load_3d(da + pl * AJ_A_PLANE, &amap, &full[s], kk * 16, arow,
                                         (pl * g.p + tl.c) * g.q + tl.k);
 #pragma unroll
                         for (int pl = 0; pl < TC_BPLANES; ++pl)
-                            tma_load_3d(db + pl * AJ_B_PLANE, &bmap, &full[s], kk * 8, n * AJ_CH, pl * g.q + tl.k);
+                            tma_load_3d(db + pl * AJ_B_PLANE, &bmap, &full[s], kk * 16, n * AJ_CH, pl * g.q + tl.k);
                         if (++s == AJ_NST) {
                             s = 0;
                             ph ^= 1;
@@ -208,7 +228,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
     } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer
         if (elect_one()) {
-            const uint32_t idesc = umma_idesc_tf32(TC_ROWS, 2 * AJ_CH, false, false);
+            const uint32_t idesc = umma_idesc_f16(TC_ROWS, 2 * AJ_CH, false, false);
             uint32_t s = 0, ph = 0, nq = 0;
             for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
                 const AjTile tl = aj_tile(g, t);
@@ -233,12 +253,12 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                         const uint64_t B1l = umma_smem_desc(b0 + 4 * AJ_B_PLANE, 256, 6);
                         const uint32_t acc = kk > 0 ? 1u : 0u;
                         // [Qi | Qr] += Phir . [-U3i | U3r] + Phii . [U3r | U3i]
-                        mma_tf32(qd, A[0], B2h, idesc, acc);
-                        mma_tf32(qd, A[0], B2l, idesc, 1);
-                        mma_tf32(qd, A[1], B2h, idesc, 1);
-                        mma_tf32(qd, A[2], B1h, idesc, 1);
-                        mma_tf32(qd, A[2], B1l, idesc, 1);
-                        mma_tf32(qd, A[3], B1h, idesc, 1);
+                        mma_f16(qd, A[0], B2h, idesc, acc);
+                        mma_f16(qd, A[0], B2l, idesc, 1);
+                        mma_f16(qd, A[1], B2h, idesc, 1);
+                        mma_f16(qd, A[2], B1h, idesc, 1);
+                        mma_f16(qd, A[2], B1l, idesc, 1);
+                        mma_f16(qd, A[3], B1h, idesc, 1);
                         mma_commit(&empty[s]);
                         if (++s == AJ_NST) {
                             s = 0;
@@ -282,6 +302,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         const int i1l = pw & (TC_TI1 - 1), h = pw / TC_TI1;
         const int ctid = threadIdx.x - TC_PW0 * 32;  // 0..255
         const uint32_t lane_addr = uint32_t(i1l * 32) << 16;
+        const float inv_scale = 1.f / (aj_phi_scale(*phimax) * AJ_U3_SCALE);  // exact power of two
         uint32_t fs = 0, fph = 0, nq = 0;
         for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
             const AjTile tl = aj_tile(g, t);
@@ -337,7 +358,8 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                         sx += rb[jj * AJ_NPW + w].x;
                         sy += rb[jj * AJ_NPW + w].y;
                     }
-                    part[((int64_t(tl.c) * g.ncols + j0 + jj) * g.q + tl.k) * g.nrt + tl.rt] = make_float2(sx, sy);
+                    part[((int64_t(tl.c) * g.ncols + j0 + jj) * g.q + tl.k) * g.nrt + tl.rt] =
+                        make_float2(sx * inv_scale, sy * inv_scale);
                 }
                 // rb (this parity) is rewritten two chunks later, after the
                 // next chunk's named barrier: no second barrier needed
@@ -349,15 +371,31 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
     if (warp == 3) tmem_dealloc(tmem, 512);
 }
 
-// Phi (c64, [c][k n_v + v]) -> 3xTF32 planes [pl][c][k][row-tile order][n3p]
-// (n3p = n3 rounded up to 4 for the TMA row pitch),
-// pl = re hi, re lo, im hi, im lo; tile rows are (i2 + 32 i1) of the
-// (TI1 x TI2) row tiles, rows outside the grid are zero.  One block per
-// (row tile, 32 i3, k, c), transposed through shared memory so both the
-// read (voxel-contiguous) and the write (i3-contiguous) are coalesced.
+// max |Re|, |Im| of Phi (the fp16 scale of its planes), by an order-free
+// atomicMax on the bit patterns of non-negative floats.
+__global__ void absmax_kernel(const float2* __restrict__ phi, int64_t ldphi, int64_t rows, int64_t p,
+                              float* __restrict__ out) {
+    float m = 0.f;
+    for (int64_t c = 0; c < p; ++c)
+        for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows; e += int64_t(gridDim.x) * blockDim.x) {
+            const float2 v = phi[ldphi * c + e];
+            m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned int*>(out), __float_as_uint(m));
+}
+
+// Phi (c64, [c][k n_v + v]) -> scaled 2-term fp16 planes [pl][c][k][row-tile
+// order][n3p] (n3p = n3 rounded up to 8 for the TMA row pitch), pl = re hi,
+// re lo, im hi, im lo; tile rows are (i2 + 32 i1) of the (TI1 x TI2) row
+// tiles, rows outside the grid are zero.  One block per (row tile, 32 i3,
+// k, c), transposed through shared memory so both the read
+// (voxel-contiguous) and the write (i3-contiguous) are coalesced.
 __global__ void __launch_bounds__(256) adj_split_phi_kernel(const float2* __restrict__ phi, int64_t ldphi, int n1,
                                                             int n2, int n3, int n3p, int q, int p, int nt2,
-                                                            int64_t nrt, float* __restrict__ planes) {
+                                                            int64_t nrt, const float* __restrict__ phimax,
+                                                            __half* __restrict__ planes) {
     __shared__ float2 tile[TC_ROWS][33];
     const int64_t rt = blockIdx.x;
     const int i3b = blockIdx.y * 32;
@@ -365,14 +403,14 @@ __global__ void __launch_bounds__(256) adj_split_phi_kernel(const float2* __rest
     const int t1 = int(rt / nt2), t2 = int(rt - int64_t(t1) * nt2);  // as aj_tile
     const int64_t nv = int64_t(n1) * n2 * n3;
     const float2* src = phi + ldphi * c + int64_t(k) * nv;
-    // load: thread -> (row = i1l + 4 i2l in voxel order for coalescing)
+    const float sc = aj_phi_scale(*phimax);
     for (int e = threadIdx.x; e < TC_ROWS * 32; e += 256) {
         const int vr = e & (TC_ROWS - 1), i3l = e >> 7;
         const int i1l = vr & 3, i2l = vr >> 2;
         const int i1 = t1 * TC_TI1 + i1l, i2 = t2 * TC_TI2 + i2l, i3 = i3b + i3l;
         float2 v = make_float2(0.f, 0.f);
         if (i1 < n1 && i2 < n2 && i3 < n3) v = src[i1 + int64_t(n1) * (i2 + int64_t(n2) * i3)];
-        tile[i2l + 32 * i1l][i3l] = v;
+        tile[i2l + 32 * i1l][i3l] = make_float2(v.x * sc, v.y * sc);
     }
     __syncthreads();
     const int64_t R = nrt * TC_ROWS;
@@ -382,21 +420,22 @@ __global__ void __launch_bounds__(256) adj_split_phi_kernel(const float2* __rest
         const int i3 = i3b + i3l;
         if (i3 >= n3p) continue;
         const float2 v = tile[row][i3l];
-        const float rh = sm100::tf32_round(v.x), ih = sm100::tf32_round(v.y);
+        const __half rh = __float2half_rn(v.x), ih = __float2half_rn(v.y);
         const int64_t o = ((int64_t(c) * q + k) * R + rt * TC_ROWS + row) * n3p + i3;
         planes[o] = rh;
-        planes[plane + o] = sm100::tf32_round(v.x - rh);
+        planes[plane + o] = __float2half_rn(v.x - __half2float(rh));
         planes[2 * plane + o] = ih;
-        planes[3 * plane + o] = sm100::tf32_round(v.y - ih);
+        planes[3 * plane + o] = __float2half_rn(v.y - __half2float(ih));
     }
 }
 
-// U3 planes for the adjoint: [pl][k][slot][n3] (i3-contiguous), slot =
-// chunk * 128 + offset of the (j, c) pair inside its chunk; same 6-plane
-// order as build_bplanes_kernel.
+// U3 planes for the adjoint: [pl][k][slot][n3p] fp16 (i3-contiguous), slot
+// = chunk * 128 + offset of the (j, c) pair inside its chunk; values scaled
+// by AJ_U3_SCALE, 2-term fp16 split, in the 6-plane order of
+// build_bplanes_kernel (-U3i, U3r, U3i hi; the same lo).
 __global__ void build_adj_bplanes_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena,
                                          const int* __restrict__ aslot, int64_t ncols, int q, int n3, int n3p,
-                                         int64_t nslots, float* __restrict__ planes) {
+                                         int64_t nslots, __half* __restrict__ planes) {
     const int64_t t = blockIdx.x;
     const int k = int(t / ncols);
     const TDesc d = td[t];
@@ -404,14 +443,15 @@ __global__ void build_adj_bplanes_kernel(const TDesc* __restrict__ td, const flo
     const int64_t plane = int64_t(q) * nslots * n3p;
     for (int e = threadIdx.x; e < n3 * d.r3; e += blockDim.x) {
         const int i3 = e / d.r3, r = e - i3 * d.r3;
-        const float2 u = arena[d.off_u3 + e];
-        const float rh = sm100::tf32_round(u.x), ih = sm100::tf32_round(u.y);
-        const float rl = sm100::tf32_round(u.x - rh), il = sm100::tf32_round(u.y - ih);
+        const float2 u0 = arena[d.off_u3 + e];
+        const float2 u = make_float2(u0.x * AJ_U3_SCALE, u0.y * AJ_U3_SCALE);
+        const __half rh = __float2half_rn(u.x), ih = __float2half_rn(u.y);
+        const __half rl = __float2half_rn(u.x - __half2float(rh)), il = __float2half_rn(u.y - __half2float(ih));
         const int64_t o = (int64_t(k) * nslots + s0 + r) * n3p + i3;
-        planes[o] = -ih;
+        planes[o] = __hneg(ih);
         planes[plane + o] = rh;
         planes[2 * plane + o] = ih;
-        planes[3 * plane + o] = -il;
+        planes[3 * plane + o] = __hneg(il);
         planes[4 * plane + o] = rl;
         planes[5 * plane + o] = il;
     }

@@ -128,7 +128,7 @@ struct tm_store {
     float2* d_u2arena = nullptr;  // U2 with odd row strides
     // tensor-core adjoint: chunk-aligned, i3-contiguous U3 planes
     bool tca_ok = false;
-    float* d_aplanes = nullptr;
+    __half* d_aplanes = nullptr;
     int* d_nch = nullptr;     // [q] chunks per component
     int* d_cstart = nullptr;  // [q][maxch + 1] first column of each chunk
     int maxch = 0;
@@ -137,7 +137,7 @@ struct tm_store {
     int64_t kpad = 0;
     CUtensorMap bmap{};
     std::mutex mu;
-    DevBuf part, xin, yout, wbuf, phiplanes, xplanes, rsum;
+    DevBuf part, xin, yout, wbuf, phiplanes, xplanes, rsum, scal;
 
     int64_t nv() const { return dims[0] * dims[1] * dims[2]; }
     int64_t rows() const { return q * nv(); }
@@ -243,8 +243,8 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
     for (int k = 0; k < s->q; ++k)
         for (size_t n = 0; n < cst[static_cast<size_t>(k)].size(); ++n)
             cstart[static_cast<size_t>(k) * (s->maxch + 1) + n] = cst[static_cast<size_t>(k)][n];
-    const int64_t n3p = (n3 + 3) / 4 * 4;
-    const size_t abytes = size_t(TC_BPLANES) * s->q * s->nslots * n3p * sizeof(float);
+    const int64_t n3p = (n3 + 7) / 8 * 8;
+    const size_t abytes = size_t(TC_BPLANES) * s->q * s->nslots * n3p * sizeof(__half);
     const size_t vbytes = size_t(voff) * sizeof(float4);
     const size_t u2bytes = size_t(u2off) * sizeof(float2);
     CK(cudaMalloc(&s->d_kofs, kofs.size() * sizeof(int)));
@@ -268,8 +268,8 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
         launched(cudaSuccess, "build_adj_bplanes_kernel");
         CK(cudaDeviceSynchronize());
     }
-    s->adj_bmap = make_tmap_3d_f32(s->d_aplanes, uint64_t(n3), uint64_t(s->nslots), uint64_t(TC_BPLANES * s->q),
-                                   uint64_t(n3p) * 4, uint64_t(s->nslots) * n3p * 4, 8, AJ_CH,
+    s->adj_bmap = make_tmap_3d_f16(s->d_aplanes, uint64_t(n3), uint64_t(s->nslots), uint64_t(TC_BPLANES * s->q),
+                                   uint64_t(n3p) * 2, uint64_t(s->nslots) * n3p * 2, 16, AJ_CH,
                                    CU_TENSOR_MAP_SWIZZLE_32B);
     s->tca_ok = true;
     CK(cudaMemcpy(s->d_kofs, kofs.data(), kofs.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -684,7 +684,6 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     g.p = int(p);
     g.nrt = int64_t(g.nt1) * g.nt2;
     g.ntiles = int64_t(p) * g.q * g.nrt;
-    g.nks = (g.n3 + 7) / 8;
     g.rmax2 = s->rmax[1];
     g.rmax3 = s->rmax[2];
     g.u2_off = TC_SLOT_V + TC_TI1 * g.rmax2 * g.rmax3 * 16;
@@ -693,17 +692,22 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     const size_t smem = 1024 + size_t(AJ_NST) * (AJ_A_STAGE + AJ_B_STAGE) + size_t(TC_JR) * g.slot_bytes +
                         size_t(2) * AJ_MAXCOLS * AJ_NPW * sizeof(float2) + (2 * AJ_NST + 2 * TC_JR + 4) * 8 + 16;
     if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: shared-memory plan too large");
-    // Phi -> 3xTF32 planes (per call)
-    const int64_t n3p = (g.n3 + 3) / 4 * 4;
+    // Phi -> scaled 2-term fp16 planes (per call)
+    g.nks = (g.n3 + 15) / 16;
+    const int64_t n3p = (g.n3 + 7) / 8 * 8;
     const int64_t R = g.nrt * TC_ROWS;
-    float* planes = static_cast<float*>(s->phiplanes.get(size_t(AJ_APLANES) * p * g.q * R * n3p * sizeof(float)));
     if (int64_t(p) * g.q > 65535) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: too many right-hand sides");
+    __half* planes = static_cast<__half*>(s->phiplanes.get(size_t(AJ_APLANES) * p * g.q * R * n3p * sizeof(__half)));
+    float* phimax = static_cast<float*>(s->scal.get(sizeof(float)));
+    CK(cudaMemsetAsync(phimax, 0, sizeof(float), st));
+    absmax_kernel<<<1184, 256, 0, st>>>(phi, ldphi, s->rows(), p, phimax);
+    launched(cudaSuccess, "absmax_kernel");
     dim3 sgrid(unsigned(g.nrt), unsigned((n3p + 31) / 32), unsigned(p * g.q));
     adj_split_phi_kernel<<<sgrid, 256, 0, st>>>(phi, ldphi, g.n1, g.n2, g.n3, int(n3p), g.q, int(p), g.nt2, g.nrt,
-                                                planes);
+                                                phimax, planes);
     launched(cudaSuccess, "adj_split_phi_kernel");
-    const CUtensorMap amap = make_tmap_3d_f32(planes, uint64_t(g.n3), uint64_t(R), uint64_t(AJ_APLANES * p * g.q),
-                                              uint64_t(n3p) * 4, uint64_t(R) * n3p * 4, 8, TC_ROWS,
+    const CUtensorMap amap = make_tmap_3d_f16(planes, uint64_t(g.n3), uint64_t(R), uint64_t(AJ_APLANES * p * g.q),
+                                              uint64_t(n3p) * 2, uint64_t(R) * n3p * 2, 16, TC_ROWS,
                                               CU_TENSOR_MAP_SWIZZLE_32B);
     const int64_t nred = g.nrt * g.q;
     float2* part = static_cast<float2*>(s->part.get(size_t(s->ncols * p * nred) * sizeof(float2)));
@@ -715,7 +719,7 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
         g.t_begin = t0;
         g.t_end = std::min<int64_t>(g.ntiles, t0 + grid);
         adj_tc_kernel<<<grid, AJ_THREADS, smem, st>>>(amap, s->adj_bmap, s->d_tcd, s->d_varena, s->d_u2arena,
-                                                       s->d_nch, s->d_cstart, g, part);
+                                                       s->d_nch, s->d_cstart, g, phimax, part);
         launched(cudaSuccess, "adj_tc_kernel");
     }
     const int64_t warps = s->ncols * p;

@@ -105,6 +105,19 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64
         : "memory");
 }
 
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (fp16 / bf16 operands, K = 16).
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // Arrive (once) on `bar` when all previously issued tcgen05.mma of this
 // thread have completed (implicitly fences before_thread_sync).
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -220,6 +233,16 @@ __host__ __device__ constexpr uint32_t umma_idesc_tf32(int M, int N, bool neg_a 
            | (0u << 15) | (0u << 16)     // a, b K-major
            | (uint32_t(N >> 3) << 17)    // n_dim
            | (uint32_t(M >> 4) << 24);   // m_dim
+}
+
+// Instruction descriptor for kind::f16 with fp16 A and B, f32 accumulate,
+// K-major A and B.
+__host__ __device__ constexpr uint32_t umma_idesc_f16(int M, int N, bool neg_a = false, bool neg_b = false) {
+    return (1u << 4)                     // c_format = F32
+           | (0u << 7)                   // a_format = F16
+           | (0u << 10)                  // b_format = F16
+           | (uint32_t(neg_a) << 13) | (uint32_t(neg_b) << 14) | (0u << 15) | (0u << 16) |
+           (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
 // Byte offset of element (row, k) (4-byte elements) inside a K-major tile
