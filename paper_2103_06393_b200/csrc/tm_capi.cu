@@ -122,7 +122,8 @@ struct tm_store {
     bool tc_ok = false;
     int* d_kofs = nullptr;   // [q*ncols] component-major K offset of each tensor
     int* d_kc = nullptr;     // [q] K extent of each component
-    float* d_planes = nullptr;
+    __half* d_planes = nullptr;
+    float* d_vbound = nullptr;  // [q*ncols] per-tensor bound of |W| / |x_j|
     TcDesc* d_tcd = nullptr;  // [q*ncols] tensor-core descriptors
     float4* d_varena = nullptr;  // mode-1 products V = U1 x_1 G (FFMA2 form)
     float2* d_u2arena = nullptr;  // U2 with odd row strides
@@ -146,6 +147,7 @@ struct tm_store {
         if (d_kofs) cudaFree(d_kofs);
         if (d_kc) cudaFree(d_kc);
         if (d_planes) cudaFree(d_planes);
+        if (d_vbound) cudaFree(d_vbound);
         if (d_tcd) cudaFree(d_tcd);
         if (d_varena) cudaFree(d_varena);
         if (d_u2arena) cudaFree(d_u2arena);
@@ -196,10 +198,10 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
         }
         if (acc >= (int64_t(1) << 30)) return;
         kc[static_cast<size_t>(k)] = int(acc);
-        s->kpad = std::max<int64_t>(s->kpad, (acc + 7) / 8 * 8);
+        s->kpad = std::max<int64_t>(s->kpad, (acc + 15) / 16 * 16);
     }
     const int64_t n3 = s->dims[2];
-    const size_t pbytes = size_t(TC_BPLANES) * s->q * n3 * s->kpad * sizeof(float);
+    const size_t pbytes = size_t(TC_BPLANES) * s->q * n3 * s->kpad * sizeof(__half);
     // V arena: per tensor ceil(n1/4)*4 x r2 x r3 float4
     const int64_t n1p = (s->dims[0] + 3) / 4 * 4;
     std::vector<TcDesc> tcd(static_cast<size_t>(ntens));
@@ -285,10 +287,13 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
     build_u2_kernel<<<unsigned(ntens), 256>>>(s->d_desc, static_cast<const float2*>(s->d_arena), s->d_tcd,
                                               int(s->dims[1]), s->d_u2arena);
     launched(cudaSuccess, "build_u2_kernel");
+    CK(cudaMalloc(&s->d_vbound, size_t(ntens) * sizeof(float)));
+    vbound_kernel<<<unsigned(ntens), 256>>>(s->d_desc, s->d_tcd, s->d_varena, int(s->dims[0]), s->d_vbound);
+    launched(cudaSuccess, "vbound_kernel");
     CK(cudaDeviceSynchronize());
     const uint32_t nmma = uint32_t(std::min<int64_t>((n3 + 15) / 16 * 16, TC_NMAX));
-    s->bmap = make_tmap_3d_f32(s->d_planes, uint64_t(s->kpad), uint64_t(n3), uint64_t(TC_BPLANES * s->q),
-                               uint64_t(s->kpad) * 4, uint64_t(n3) * s->kpad * 4, 8, nmma, CU_TENSOR_MAP_SWIZZLE_32B);
+    s->bmap = make_tmap_3d_f16(s->d_planes, uint64_t(s->kpad), uint64_t(n3), uint64_t(TC_BPLANES * s->q),
+                               uint64_t(s->kpad) * 2, uint64_t(n3) * s->kpad * 2, 16, nmma, CU_TENSOR_MAP_SWIZZLE_32B);
     s->device_bytes += int64_t(pbytes + vbytes + u2bytes + abytes + tcd.size() * sizeof(TcDesc) + (kofs.size() + kc.size()) * sizeof(int));
     s->tc_ok = true;
 }
@@ -572,8 +577,13 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     int dev = 0;
     CK(cudaGetDevice(&dev));
     const unsigned grid = unsigned(std::min<int64_t>(g.ntiles, num_sms(dev)));
-    float2* rsum = static_cast<float2*>(
-        const_cast<tm_store*>(s)->rsum.get(size_t(grid) * g.nmma * g.nh3 * TC_ROWS * sizeof(float2)));
+    tm_store* ms = const_cast<tm_store*>(s);
+    float2* rsum = static_cast<float2*>(ms->rsum.get(size_t(grid) * g.nmma * g.nh3 * TC_ROWS * sizeof(float2)));
+    float* wmax = static_cast<float*>(ms->scal.get(2 * sizeof(float))) + 1;
+    CK(cudaMemsetAsync(wmax, 0, sizeof(float), st));
+    wmax_kernel<<<unsigned(std::min<int64_t>((s->ncols * p + 255) / 256, 1184)), 256, 0, st>>>(x, ldx, s->ncols, p,
+                                                                                              s->q, s->d_vbound, wmax);
+    launched(cudaSuccess, "wmax_kernel");
     // One launch per wave of `grid` tiles: every CTA starts its tile at the
     // same time, so the CTAs of one component stream its B planes (184 MB
     // per component at config 4, more than L2) in K-lockstep and share them
@@ -584,7 +594,7 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
         g.t_begin = t0;
         g.t_end = std::min<int64_t>(g.ntiles, t0 + grid);
         fwd_tc_kernel<<<grid, TC_THREADS, smem, st>>>(s->bmap, s->d_tcd, s->d_varena, s->d_u2arena, s->d_kc, g, x,
-                                                       ldx, y, ldy, rsum);
+                                                       ldx, y, ldy, rsum, wmax);
         launched(cudaSuccess, "fwd_tc_kernel");
     }
 }
@@ -698,7 +708,7 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     const int64_t R = g.nrt * TC_ROWS;
     if (int64_t(p) * g.q > 65535) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: too many right-hand sides");
     __half* planes = static_cast<__half*>(s->phiplanes.get(size_t(AJ_APLANES) * p * g.q * R * n3p * sizeof(__half)));
-    float* phimax = static_cast<float*>(s->scal.get(sizeof(float)));
+    float* phimax = static_cast<float*>(s->scal.get(2 * sizeof(float)));
     CK(cudaMemsetAsync(phimax, 0, sizeof(float), st));
     absmax_kernel<<<1184, 256, 0, st>>>(phi, ldphi, s->rows(), p, phimax);
     launched(cudaSuccess, "absmax_kernel");

@@ -51,10 +51,28 @@
 // free: 4 fold warps).
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "tm_common.cuh"
 #include "tm_sm100.cuh"
 
 namespace tmb {
+
+// fp16 operand scaling (see also tm_adj_tc.cuh): operands are stored as a
+// 2-term fp16 split (hi = fp16(v), lo = fp16(v - hi): 22 significant bits)
+// of values scaled by powers of two into fp16's normal range — U3
+// (orthonormal columns, |u| <= 1) by 2^12, data-dependent operands by
+// 2^(14 - e) where 2^e bounds their magnitude (fp16_scale).  The products
+// hi.hi + hi.lo + lo.hi run on tcgen05.mma.kind::f16 (K = 16) with fp32
+// accumulation; the scale is undone exactly on the fp32 results.
+constexpr float TC_U3_SCALE = 4096.f;
+__host__ __device__ inline float fp16_scale(float amax) {
+    if (!(amax > 0.f) || !(amax < 3.0e38f)) return 1.f;
+    int e = 0;
+    frexpf(amax, &e);  // amax < 2^e
+    e = e < -100 ? -100 : (e > 100 ? 100 : e);
+    return ldexpf(1.f, 14 - e);
+}
 
 constexpr int TC_TI1 = 4, TC_TI2 = 32, TC_ROWS = 128;
 constexpr int TC_NST_MAX = 5;   // A/B stages (8 K each)
@@ -66,7 +84,7 @@ constexpr int TC_FW0 = TC_PW0 + TC_NPW;   // first fold / epilogue warp
 constexpr int TC_THREADS = (TC_FW0 + 4) * 32;
 constexpr int TC_NMAX = 128;    // i3 per tile (N per MMA)
 constexpr int TC_RMAX = 16;     // rank bound of the tensor-core path
-constexpr int TC_A_PLANE = TC_ROWS * 32;     // bytes (128 rows x 8 tf32)
+constexpr int TC_A_PLANE = TC_ROWS * 32;     // bytes (128 rows x 16 fp16 = one K16 stage)
 constexpr int TC_A_STAGE = 4 * TC_A_PLANE;   // 16 KB
 constexpr uint32_t TC_RUN_COL = 256;         // TMEM column of the running sum
 constexpr int TC_SLOT_V = 128;               // byte offset of the V block in a factor slot
@@ -192,9 +210,9 @@ __device__ __forceinline__ void tc_produce_column(const float4* __restrict__ V, 
         const float2 v = cmul(f2_unpack(w[u]), xj);
         w[u] = f2_pack(v.x, v.y);
     }
-    // wait for every stage this column opens, write, close completed stages
+    // wait for every stage (16 K) this column opens, write, close completed stages
     const uint32_t kend = ring.kpos + uint32_t(r3);
-    const uint32_t ns = (kend + 7) >> 3;
+    const uint32_t ns = (kend + 15) >> 4;
     for (uint32_t i = ring.kpos == 0 ? 0u : 1u; i < ns; ++i) {
         uint32_t s, ph;
         ring_ahead(ring, i, nst, s, ph);
@@ -206,18 +224,17 @@ __device__ __forceinline__ void tc_produce_column(const float4* __restrict__ V, 
         if (u < NU - 1 || c < r3) {
             const uint32_t K = ring.kpos + uint32_t(c);
             uint32_t s, ph;
-            ring_ahead(ring, K >> 3, nst, s, ph);
+            ring_ahead(ring, K >> 4, nst, s, ph);
             const float2 wv = f2_unpack(w[u]);
-            const float hr = __uint_as_float(__float_as_uint(wv.x) & 0xFFFFE000u);
-            const float hi = __uint_as_float(__float_as_uint(wv.y) & 0xFFFFE000u);
-            float* a = reinterpret_cast<float*>(sA + s * TC_A_STAGE + rowbase + (((K & 7u) * 4u) ^ xorv));
+            const __half hr = __float2half_rn(wv.x), hi = __float2half_rn(wv.y);
+            __half* a = reinterpret_cast<__half*>(sA + s * TC_A_STAGE + rowbase + (((K & 15u) * 2u) ^ xorv));
             a[0] = hr;
-            a[TC_A_PLANE / 4] = wv.x - hr;
-            a[2 * TC_A_PLANE / 4] = hi;
-            a[3 * TC_A_PLANE / 4] = wv.y - hi;
+            a[TC_A_PLANE / 2] = __float2half_rn(wv.x - __half2float(hr));
+            a[2 * TC_A_PLANE / 2] = hi;
+            a[3 * TC_A_PLANE / 2] = __float2half_rn(wv.y - __half2float(hi));
         }
     }
-    const uint32_t nc = kend >> 3;  // stages completed by this column
+    const uint32_t nc = kend >> 4;  // stages completed by this column
     if (nc) {
         fence_proxy_async_smem();
         __syncwarp();
@@ -229,14 +246,14 @@ __device__ __forceinline__ void tc_produce_column(const float4* __restrict__ V, 
             }
         ring_ahead(ring, nc, nst, ring.st, ring.ph);
     }
-    ring.kpos = kend & 7u;
+    ring.kpos = kend & 15u;
 }
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap bmap, const TcDesc* __restrict__ tcd,
                   const float4* __restrict__ varena, const float2* __restrict__ u2arena, const int* __restrict__ kc,
                   TcGeom g, const float2* __restrict__ x, int64_t ldx, float2* __restrict__ y, int64_t ldy,
-                  float2* __restrict__ rsum) {
+                  float2* __restrict__ rsum, const float* __restrict__ wmax) {
     using namespace sm100;
     extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
     // align to 1024 B by offsetting the shared array itself (keeps the
@@ -283,7 +300,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int plane_bytes = g.nmma * 32;
             for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
                 const TcTile tl = tc_tile(g, t);
-                const int nks = (kc[tl.k] + 7) >> 3;
+                const int nks = (kc[tl.k] + 15) >> 4;
                 for (int kk = 0; kk < nks; ++kk) {
                     mbar_wait(&empty[s], ph ^ 1);
                     if (g.debug & 2) {
@@ -295,7 +312,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         for (int hh = 0; hh < g.nh3; ++hh)
 #pragma unroll
                             for (int pl = 0; pl < TC_FPLANES; ++pl)
-                                tma_load_3d(dst + (hh * TC_FPLANES + pl) * plane_bytes, &bmap, &full[s], kk * 8,
+                                tma_load_3d(dst + (hh * TC_FPLANES + pl) * plane_bytes, &bmap, &full[s], kk * 16,
                                             tl.i3_0 + hh * g.nmma, (1 + pl + (pl >> 1)) * g.q + tl.k);
                     }
                     if (++s == nst) {
@@ -313,14 +330,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             //   Yr -= Ai . U3i,  Yi += Ai . U3r (width NMMA, negate-A bit)
             // each as hi.hi + hi.lo + lo.hi; smem B planes per half:
             // U3r hi, U3i hi, U3r lo, U3i lo
-            const uint32_t id_w = umma_idesc_tf32(TC_ROWS, 2 * g.nmma, false, false);
-            const uint32_t id_p = umma_idesc_tf32(TC_ROWS, g.nmma, false, false);
-            const uint32_t id_n = umma_idesc_tf32(TC_ROWS, g.nmma, true, false);
+            const uint32_t id_w = umma_idesc_f16(TC_ROWS, 2 * g.nmma, false, false);
+            const uint32_t id_p = umma_idesc_f16(TC_ROWS, g.nmma, false, false);
+            const uint32_t id_n = umma_idesc_f16(TC_ROWS, g.nmma, true, false);
             const int plane_b = g.nmma * 32;
             uint32_t s = 0, ph = 0, gch = 0;
             for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
                 const TcTile tl = tc_tile(g, t);
-                const int nks = (kc[tl.k] + 7) >> 3;
+                const int nks = (kc[tl.k] + 15) >> 4;
                 int cpos = 0;  // stage position inside the current chain
                 for (int kk = 0; kk < nks; ++kk) {
                     if (cpos == 0) {
@@ -343,15 +360,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         const uint64_t Brl = umma_smem_desc(bh + 2 * plane_b, 256, 6);  // [U3r|U3i] lo window
                         const uint64_t Bil = umma_smem_desc(bh + 3 * plane_b, 256, 6);
                         const uint32_t yr = tmem + uint32_t(2 * g.nmma * hh), yi = yr + uint32_t(g.nmma);
-                        mma_tf32(yr, A[0], Brh, id_w, acc);
-                        mma_tf32(yr, A[0], Brl, id_w, 1);
-                        mma_tf32(yr, A[1], Brh, id_w, 1);
-                        mma_tf32(yr, A[2], Bih, id_n, 1);
-                        mma_tf32(yr, A[2], Bil, id_n, 1);
-                        mma_tf32(yr, A[3], Bih, id_n, 1);
-                        mma_tf32(yi, A[2], Brh, id_p, 1);
-                        mma_tf32(yi, A[2], Brl, id_p, 1);
-                        mma_tf32(yi, A[3], Brh, id_p, 1);
+                        mma_f16(yr, A[0], Brh, id_w, acc);
+                        mma_f16(yr, A[0], Brl, id_w, 1);
+                        mma_f16(yr, A[1], Brh, id_w, 1);
+                        mma_f16(yr, A[2], Bih, id_n, 1);
+                        mma_f16(yr, A[2], Bil, id_n, 1);
+                        mma_f16(yr, A[3], Bih, id_n, 1);
+                        mma_f16(yi, A[2], Brh, id_p, 1);
+                        mma_f16(yi, A[2], Brl, id_p, 1);
+                        mma_f16(yi, A[3], Brh, id_p, 1);
                     }
                     mma_commit(&empty[s]);
                     if (++s == nst) {
@@ -404,11 +421,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t rowbase = uint32_t(row) * 32u, xorv = (uint32_t(row) & 4u) << 2;
         ARing ring{0, 0, 0};
         uint32_t fs = 0, fph = 0;
+        const float sw = fp16_scale(*wmax);  // W x sw fits fp16 (wmax bounds |W| over the store)
         for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
             const TcTile tl = tc_tile(g, t);
             const float2* xc = x + ldx * tl.c;
             for (int64_t j = 0; j < g.ncols; ++j) {
-                const float2 xj = xc[j];
+                const float2 x0 = xc[j];
+                const float2 xj = make_float2(x0.x * sw, x0.y * sw);
                 mbar_wait(&ffull[fs], fph);
                 const unsigned char* slot = sSlot + fs * g.slot_bytes;
                 const int r2 = reinterpret_cast<const TcDesc*>(slot)->r2;
@@ -434,10 +453,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
             if (ring.kpos != 0) {  // zero the tail of the last stage and close it
                 if (h == 0)
-                    for (uint32_t kq = ring.kpos; kq < 8; ++kq) {
-                        float* a = reinterpret_cast<float*>(sA + ring.st * TC_A_STAGE + rowbase + ((kq * 4u) ^ xorv));
+                    for (uint32_t kq = ring.kpos; kq < 16; ++kq) {
+                        __half* a = reinterpret_cast<__half*>(sA + ring.st * TC_A_STAGE + rowbase + ((kq * 2u) ^ xorv));
 #pragma unroll
-                        for (int pl = 0; pl < 4; ++pl) a[pl * TC_A_PLANE / 4] = 0.f;
+                        for (int pl = 0; pl < 4; ++pl) a[pl * TC_A_PLANE / 2] = __float2half_rn(0.f);
                     }
                 fence_proxy_async_smem();
                 __syncwarp();
@@ -459,10 +478,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int span = g.nmma * g.nh3;
         float2* rs = rsum + int64_t(blockIdx.x) * span * TC_ROWS + row;
         const int64_t nv3 = int64_t(g.n1) * g.n2 * g.n3;
+        const float inv = 1.f / (fp16_scale(*wmax) * TC_U3_SCALE);  // exact power of two
         uint32_t gch = 0;
         for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
             const TcTile tl = tc_tile(g, t);
-            const int nks = (kc[tl.k] + 7) >> 3;
+            const int nks = (kc[tl.k] + 15) >> 4;
             const int nch = (nks + g.chain - 1) / g.chain;
             const int ei1 = tl.i1_0 + quarter, ei2 = tl.i2_0 + lane;
             const bool eok = ei1 < g.n1 && ei2 < g.n2;
@@ -498,7 +518,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             for (int i = 0; i < 16; ++i) {
                                 const int i3 = tl.i3_0 + i3l + i;
                                 if (i3 < g.n3)
-                                    yp[pl * i3] = make_float2(__uint_as_float(cr[i]), __uint_as_float(ci[i]));
+                                    yp[pl * i3] = make_float2(__uint_as_float(cr[i]) * inv, __uint_as_float(ci[i]) * inv);
                             }
                         }
                     }
@@ -544,14 +564,12 @@ __global__ void build_v_kernel(const TDesc* __restrict__ td, const float2* __res
 }
 
 // ------------------------------------------------- store-side B planes (K6')
-// planes[p][k][i3][K], K = kofs[k][j] + r, in the order
-//   0: -U3i hi, 1: U3r hi, 2: U3i hi, 3: -U3i lo, 4: U3r lo, 5: U3i lo
-// (hi = tf32(x), lo = tf32(x - hi)), so that the windows [U3r | U3i] and
-// [-U3i | U3r] of two consecutive planes are the B operands of the
-// complex-as-real forward MMA.
+// planes[p][k][i3][K] fp16, K = kofs[k][j] + r, values U3 x TC_U3_SCALE in
+// the order 0: -U3i hi, 1: U3r hi, 2: U3i hi, 3: -U3i lo, 4: U3r lo,
+// 5: U3i lo (2-term fp16 split).  The forward streams planes 1, 2, 4, 5.
 __global__ void build_bplanes_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena,
                                      const int* __restrict__ kofs, int64_t ncols, int q, int n3, int64_t kpad,
-                                     float* __restrict__ planes) {
+                                     __half* __restrict__ planes) {
     const int64_t t = blockIdx.x;  // tensor index k*ncols + j
     const int k = int(t / ncols);
     const TDesc d = td[t];
@@ -559,17 +577,66 @@ __global__ void build_bplanes_kernel(const TDesc* __restrict__ td, const float2*
     const int64_t plane = int64_t(q) * n3 * kpad;
     for (int e = threadIdx.x; e < n3 * d.r3; e += blockDim.x) {
         const int i3 = e / d.r3, r = e - i3 * d.r3;
-        const float2 u = arena[d.off_u3 + e];
-        const float rh = sm100::tf32_round(u.x), ih = sm100::tf32_round(u.y);
-        const float rl = sm100::tf32_round(u.x - rh), il = sm100::tf32_round(u.y - ih);
+        const float2 u0 = arena[d.off_u3 + e];
+        const float2 u = make_float2(u0.x * TC_U3_SCALE, u0.y * TC_U3_SCALE);
+        const __half rh = __float2half_rn(u.x), ih = __float2half_rn(u.y);
+        const __half rl = __float2half_rn(u.x - __half2float(rh)), il = __float2half_rn(u.y - __half2float(ih));
         const int64_t o = (int64_t(k) * n3 + i3) * kpad + k0 + r;
-        planes[o] = -ih;
+        planes[o] = __hneg(ih);
         planes[plane + o] = rh;
         planes[2 * plane + o] = ih;
-        planes[3 * plane + o] = -il;
+        planes[3 * plane + o] = __hneg(il);
         planes[4 * plane + o] = rl;
         planes[5 * plane + o] = il;
     }
+}
+
+// Per tensor: max over (i1, c) of the 2-norm over b of V[i1, b, c] — a
+// bound on |W[row, c]| / |x_j| because every row of U2 has norm <= 1.
+__global__ void vbound_kernel(const TDesc* __restrict__ td, const TcDesc* __restrict__ tcd,
+                              const float4* __restrict__ varena, int n1, float* __restrict__ vbound) {
+    const int64_t t = blockIdx.x;
+    const int r2 = tcd[t].r2, r3 = tcd[t].r3;
+    const float4* v = varena + tcd[t].off_v;
+    float m = 0.f;
+    for (int e = threadIdx.x; e < n1 * r3; e += blockDim.x) {
+        const int i1 = e / r3, c = e - i1 * r3;
+        float s2 = 0.f;
+        for (int b = 0; b < r2; ++b) {
+            const float4 x = v[int64_t(i1 >> 2) * 4 * r2 * r3 + int64_t(b + r2 * c) * 4 + (i1 & 3)];
+            s2 += x.x * x.x + x.y * x.y;
+        }
+        m = fmaxf(m, sqrtf(s2));
+    }
+    __shared__ float red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float r = 0.f;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) r = fmaxf(r, red[w]);
+        vbound[t] = r * 1.0001f;  // margin for the fp32 norm's rounding
+    }
+    (void)td;
+}
+
+// wmax = max over (k, j, c) of |x[j, c]| * vbound[k ncols + j] (atomicMax on
+// the bits of non-negative floats: order-free).
+__global__ void wmax_kernel(const float2* __restrict__ x, int64_t ldx, int64_t ncols, int64_t p, int q,
+                            const float* __restrict__ vbound, float* __restrict__ out) {
+    float m = 0.f;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < ncols * p; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t j = e % ncols, c = e / ncols;
+        const float2 xv = x[j + ldx * c];
+        const float ax = sqrtf(xv.x * xv.x + xv.y * xv.y);
+        float vb = 0.f;
+        for (int k = 0; k < q; ++k) vb = fmaxf(vb, vbound[int64_t(k) * ncols + j]);
+        m = fmaxf(m, ax * vb * 1.0001f);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned int*>(out), __float_as_uint(m));
 }
 
 // ------------------------------------------------ store-side U2 arena (K6 U2)
