@@ -302,12 +302,13 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         const int i1l = pw & (TC_TI1 - 1), h = pw / TC_TI1;
         const int ctid = threadIdx.x - TC_PW0 * 32;  // 0..255
         const uint32_t lane_addr = uint32_t(i1l * 32) << 16;
-        const float inv_scale = 1.f / (aj_phi_scale(*phimax) * AJ_U3_SCALE);  // exact power of two
         uint32_t fs = 0, fph = 0, nq = 0;
         for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
             const AjTile tl = aj_tile(g, t);
             const int nc = nch[tl.k];
             const int* cs = cstart + int64_t(tl.k) * (g.maxch + 1);
+            // exact power of two: undoes the (rhs, component) Phi scale and the U3 scale
+            const float inv_scale = 1.f / (aj_phi_scale(phimax[int64_t(tl.c) * g.q + tl.k]) * AJ_U3_SCALE);
             for (int n = 0; n < nc; ++n, ++nq) {
                 const uint32_t qb = nq & 1, qph = (nq >> 1) & 1;
                 const int j0 = cs[n], j1 = cs[n + 1];
@@ -371,19 +372,22 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
     if (warp == 3) tmem_dealloc(tmem, 512);
 }
 
-// max |Re|, |Im| of Phi (the fp16 scale of its planes), by an order-free
-// atomicMax on the bit patterns of non-negative floats.
-__global__ void absmax_kernel(const float2* __restrict__ phi, int64_t ldphi, int64_t rows, int64_t p,
+// max |Re|, |Im| of each (right-hand side, component) block of Phi — the
+// fp16 scale of its planes — by an order-free atomicMax on the bit
+// patterns of non-negative floats.  blockIdx.y = block index - b0.
+__global__ void absmax_kernel(const float2* __restrict__ phi, int64_t ldphi, int64_t nv, int q, int64_t b0,
                               float* __restrict__ out) {
+    const int64_t b = b0 + blockIdx.y;
+    const int64_t c = b / q, k = b - c * q;
+    const float2* src = phi + ldphi * c + k * nv;
     float m = 0.f;
-    for (int64_t c = 0; c < p; ++c)
-        for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows; e += int64_t(gridDim.x) * blockDim.x) {
-            const float2 v = phi[ldphi * c + e];
-            m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
-        }
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nv; e += int64_t(gridDim.x) * blockDim.x) {
+        const float2 v = src[e];
+        m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned int*>(out), __float_as_uint(m));
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned int*>(out + b), __float_as_uint(m));
 }
 
 // Phi (c64, [c][k n_v + v]) -> scaled 2-term fp16 planes [pl][c][k][row-tile
@@ -394,16 +398,17 @@ __global__ void absmax_kernel(const float2* __restrict__ phi, int64_t ldphi, int
 // (voxel-contiguous) and the write (i3-contiguous) are coalesced.
 __global__ void __launch_bounds__(256) adj_split_phi_kernel(const float2* __restrict__ phi, int64_t ldphi, int n1,
                                                             int n2, int n3, int n3p, int q, int p, int nt2,
-                                                            int64_t nrt, const float* __restrict__ phimax,
+                                                            int64_t nrt, int64_t b0, const float* __restrict__ phimax,
                                                             __half* __restrict__ planes) {
     __shared__ float2 tile[TC_ROWS][33];
     const int64_t rt = blockIdx.x;
     const int i3b = blockIdx.y * 32;
-    const int k = blockIdx.z % q, c = blockIdx.z / q;
+    const int64_t b = b0 + blockIdx.z;  // (rhs, component) block
+    const int k = int(b % q), c = int(b / q);
     const int t1 = int(rt / nt2), t2 = int(rt - int64_t(t1) * nt2);  // as aj_tile
     const int64_t nv = int64_t(n1) * n2 * n3;
     const float2* src = phi + ldphi * c + int64_t(k) * nv;
-    const float sc = aj_phi_scale(*phimax);
+    const float sc = aj_phi_scale(phimax[b]);
     for (int e = threadIdx.x; e < TC_ROWS * 32; e += 256) {
         const int vr = e & (TC_ROWS - 1), i3l = e >> 7;
         const int i1l = vr & 3, i2l = vr >> 2;

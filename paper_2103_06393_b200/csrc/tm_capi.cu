@@ -540,8 +540,18 @@ int num_sms(int dev) {
     return n;
 }
 
+// Host I/O overlapped with the tensor-core kernels, per (rhs, component)
+// block of q*n_v rows: the forward copies each finished block of y to the
+// host while later waves compute; the adjoint copies Phi in block by block
+// ahead of the waves that need it (tm_forward / tm_adjoint with TM_HOST).
+struct HostPipe {
+    cudaStream_t copy = nullptr;
+    void* host = nullptr;  // forward: y (out); adjoint: phi (in)
+    int64_t ldhost = 0;
+};
+
 void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy,
-                    cudaStream_t st) {
+                    cudaStream_t st, const HostPipe* hp = nullptr) {
     TcGeom g{};
     g.ncols = s->ncols;
     g.n1 = int(s->dims[0]);
@@ -590,12 +600,29 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     // in L2.  A persistent schedule over all tiles drifts apart by the
     // per-component cost differences and re-reads B from HBM (725 GB per
     // config-4 forward, measured).
+    const int64_t tpb = g.ntiles / (int64_t(p) * g.q);  // tiles per (rhs, component) block
+    const int64_t nv = s->nv();
+    int64_t bdone = 0;
     for (int64_t t0 = 0; t0 < g.ntiles; t0 += grid) {
         g.t_begin = t0;
         g.t_end = std::min<int64_t>(g.ntiles, t0 + grid);
         fwd_tc_kernel<<<grid, TC_THREADS, smem, st>>>(s->bmap, s->d_tcd, s->d_varena, s->d_u2arena, s->d_kc, g, x,
                                                        ldx, y, ldy, rsum, wmax);
         launched(cudaSuccess, "fwd_tc_kernel");
+        const int64_t bnow = g.t_end / tpb;
+        if (hp && bnow > bdone) {
+            cudaEvent_t ev;
+            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            CK(cudaEventRecord(ev, st));
+            CK(cudaStreamWaitEvent(hp->copy, ev, 0));
+            CK(cudaEventDestroy(ev));
+            for (int64_t b = bdone; b < bnow; ++b) {
+                const int64_t c = b / g.q, k = b - c * g.q;
+                CK(cudaMemcpyAsync(static_cast<float2*>(hp->host) + hp->ldhost * c + k * nv, y + ldy * c + k * nv,
+                                   size_t(nv) * sizeof(float2), cudaMemcpyDeviceToHost, hp->copy));
+            }
+            bdone = bnow;
+        }
     }
 }
 
@@ -682,7 +709,7 @@ size_t adj_tc_smem(const tm_store* s) {
 }
 
 void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, float2* z, int64_t ldz,
-                    cudaStream_t st) {
+                    cudaStream_t st, const HostPipe* hp = nullptr) {
     AjGeom g{};
     g.ncols = s->ncols;
     g.n1 = int(s->dims[0]);
@@ -708,14 +735,35 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     const int64_t R = g.nrt * TC_ROWS;
     if (int64_t(p) * g.q > 65535) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: too many right-hand sides");
     __half* planes = static_cast<__half*>(s->phiplanes.get(size_t(AJ_APLANES) * p * g.q * R * n3p * sizeof(__half)));
-    float* phimax = static_cast<float*>(s->scal.get(2 * sizeof(float)));
-    CK(cudaMemsetAsync(phimax, 0, sizeof(float), st));
-    absmax_kernel<<<1184, 256, 0, st>>>(phi, ldphi, s->rows(), p, phimax);
-    launched(cudaSuccess, "absmax_kernel");
-    dim3 sgrid(unsigned(g.nrt), unsigned((n3p + 31) / 32), unsigned(p * g.q));
-    adj_split_phi_kernel<<<sgrid, 256, 0, st>>>(phi, ldphi, g.n1, g.n2, g.n3, int(n3p), g.q, int(p), g.nt2, g.nrt,
-                                                phimax, planes);
-    launched(cudaSuccess, "adj_split_phi_kernel");
+    const int64_t nblk = int64_t(p) * g.q;  // (rhs, component) blocks
+    const int64_t nv = s->nv();
+    float* scal = static_cast<float*>(s->scal.get(size_t(nblk + 2) * sizeof(float)));
+    float* phimax = scal + 2;  // [p][q]
+    CK(cudaMemsetAsync(phimax, 0, size_t(nblk) * sizeof(float), st));
+    // prepare (absmax, split) blocks [b0, b1) of Phi on the compute stream
+    auto prepare = [&](int64_t b0, int64_t b1) {
+        if (b1 <= b0) return;
+        absmax_kernel<<<dim3(148, unsigned(b1 - b0)), 256, 0, st>>>(phi, ldphi, nv, g.q, b0, phimax);
+        launched(cudaSuccess, "absmax_kernel");
+        dim3 sgrid(unsigned(g.nrt), unsigned((n3p + 31) / 32), unsigned(b1 - b0));
+        adj_split_phi_kernel<<<sgrid, 256, 0, st>>>(phi, ldphi, g.n1, g.n2, g.n3, int(n3p), g.q, int(p), g.nt2,
+                                                    g.nrt, b0, phimax, planes);
+        launched(cudaSuccess, "adj_split_phi_kernel");
+    };
+    std::vector<cudaEvent_t> arrived;
+    if (hp) {  // host Phi: copy every block in ahead of the waves, on the copy stream
+        arrived.resize(size_t(nblk));
+        for (int64_t b = 0; b < nblk; ++b) {
+            const int64_t c = b / g.q, k = b - c * g.q;
+            CK(cudaMemcpyAsync(const_cast<float2*>(phi) + ldphi * c + k * nv,
+                               static_cast<const float2*>(hp->host) + hp->ldhost * c + k * nv,
+                               size_t(nv) * sizeof(float2), cudaMemcpyHostToDevice, hp->copy));
+            CK(cudaEventCreateWithFlags(&arrived[size_t(b)], cudaEventDisableTiming));
+            CK(cudaEventRecord(arrived[size_t(b)], hp->copy));
+        }
+    } else {
+        prepare(0, nblk);
+    }
     const CUtensorMap amap = make_tmap_3d_f16(planes, uint64_t(g.n3), uint64_t(R), uint64_t(AJ_APLANES * p * g.q),
                                               uint64_t(n3p) * 2, uint64_t(R) * n3p * 2, 16, TC_ROWS,
                                               CU_TENSOR_MAP_SWIZZLE_32B);
@@ -725,13 +773,20 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     int dev = 0;
     CK(cudaGetDevice(&dev));
     const unsigned grid = unsigned(std::min<int64_t>(g.ntiles, num_sms(dev)));
+    int64_t bready = hp ? 0 : nblk;
     for (int64_t t0 = 0; t0 < g.ntiles; t0 += grid) {  // one launch per wave (see run_forward_tc)
         g.t_begin = t0;
         g.t_end = std::min<int64_t>(g.ntiles, t0 + grid);
+        const int64_t bneed = (g.t_end - 1) / g.nrt + 1;  // blocks this wave reads
+        for (; bready < bneed; ++bready) {
+            CK(cudaStreamWaitEvent(st, arrived[size_t(bready)], 0));
+            prepare(bready, bready + 1);
+        }
         adj_tc_kernel<<<grid, AJ_THREADS, smem, st>>>(amap, s->adj_bmap, s->d_tcd, s->d_varena, s->d_u2arena,
                                                        s->d_nch, s->d_cstart, g, phimax, part);
         launched(cudaSuccess, "adj_tc_kernel");
     }
+    for (cudaEvent_t e : arrived) CK(cudaEventDestroy(e));
     const int64_t warps = s->ncols * p;
     const unsigned blocks = unsigned((warps * 32 + 255) / 256);
     adj_reduce_kernel<float2><<<blocks, 256, 0, st>>>(part, s->ncols, p, nred, z, ldz);
@@ -826,6 +881,72 @@ void with_host_io(tm_store* s, const void* in, int64_t ldin, int64_t inrows, int
     CK(cudaStreamDestroy(st));
 }
 
+// TM_HOST products on the tensor-core path: host I/O overlapped with the
+// kernels block by block (HostPipe).  Returns false when the product does
+// not take the tensor-core path (the caller then uses with_host_io).
+bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy) {
+    if (!(s->tc_ok && !tc_disabled() && !mrhs_ok(s, p))) return false;
+    const size_t cs = s->csize();
+    void* din = s->xin.get(size_t(std::max<int64_t>(s->ncols * p, 1)) * cs);
+    void* dout = s->yout.get(size_t(std::max<int64_t>(s->rows() * p, 1)) * cs);
+    cudaStream_t st, cp;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+    auto done = [&]() {
+        cudaStreamSynchronize(st);
+        cudaStreamSynchronize(cp);
+        cudaStreamDestroy(st);
+        cudaStreamDestroy(cp);
+    };
+    try {
+        CK(cudaMemcpy2DAsync(din, size_t(s->ncols) * cs, x, size_t(ldx) * cs, size_t(s->ncols) * cs, size_t(p),
+                             cudaMemcpyHostToDevice, st));
+        HostPipe hp;
+        hp.copy = cp;
+        hp.host = y;
+        hp.ldhost = ldy;
+        run_forward_tc(s, static_cast<const float2*>(din), s->ncols, p, static_cast<float2*>(dout), s->rows(), st, &hp);
+        CK(cudaStreamSynchronize(st));
+        CK(cudaStreamSynchronize(cp));
+    } catch (...) {
+        done();
+        throw;
+    }
+    done();
+    return true;
+}
+
+bool adjoint_host_pipelined(tm_store* s, const void* phi, int64_t ldphi, int64_t p, void* z, int64_t ldz) {
+    if (!(s->tca_ok && !tc_disabled() && adj_tc_smem(s) <= kSmemMax && int64_t(p) * s->q <= 65535)) return false;
+    const size_t cs = s->csize();
+    void* din = s->xin.get(size_t(std::max<int64_t>(s->rows() * p, 1)) * cs);
+    void* dout = s->yout.get(size_t(std::max<int64_t>(s->ncols * p, 1)) * cs);
+    cudaStream_t st, cp;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+    auto done = [&]() {
+        cudaStreamSynchronize(st);
+        cudaStreamSynchronize(cp);
+        cudaStreamDestroy(st);
+        cudaStreamDestroy(cp);
+    };
+    try {
+        HostPipe hp;
+        hp.copy = cp;
+        hp.host = const_cast<void*>(phi);
+        hp.ldhost = ldphi;
+        run_adjoint_tc(s, static_cast<const float2*>(din), s->rows(), p, static_cast<float2*>(dout), s->ncols, st, &hp);
+        CK(cudaMemcpy2DAsync(z, size_t(ldz) * cs, dout, size_t(s->ncols) * cs, size_t(s->ncols) * cs, size_t(p),
+                             cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    } catch (...) {
+        done();
+        throw;
+    }
+    done();
+    return true;
+}
+
 void check_common(const tm_store* s, int64_t p, int64_t ldin, int64_t inrows, int64_t ldout, int64_t outrows,
                   int where, const void* in, const void* out) {
     if (!s) contract("null store");
@@ -898,7 +1019,7 @@ TM_API int tm_forward(tm_store* s, const void* x, int64_t ldx, int64_t xrows, in
         if (p > 0) {
             if (where == TM_DEVICE)
                 forward_dev(s, x, ldx, p, y, ldy, static_cast<cudaStream_t>(stream));
-            else
+            else if (!forward_host_pipelined(s, x, ldx, p, y, ldy))
                 with_host_io(s, x, ldx, xrows, p, y, ldy, s->rows(),
                              [&](void* din, int64_t ldi, void* dout, int64_t ldo, cudaStream_t st) {
                                  forward_dev(s, din, ldi, p, dout, ldo, st);
@@ -924,7 +1045,7 @@ TM_API int tm_adjoint(tm_store* s, const void* phi, int64_t ldphi, int64_t phiro
         if (p > 0 && s->ncols > 0) {
             if (where == TM_DEVICE)
                 adjoint_dev(s, phi, ldphi, p, z, ldz, static_cast<cudaStream_t>(stream));
-            else
+            else if (!adjoint_host_pipelined(s, phi, ldphi, p, z, ldz))
                 with_host_io(s, phi, ldphi, phirows, p, z, ldz, s->ncols,
                              [&](void* din, int64_t ldi, void* dout, int64_t ldo, cudaStream_t st) {
                                  adjoint_dev(s, din, ldi, p, dout, ldo, st);
