@@ -201,7 +201,7 @@ __device__ __forceinline__ void tc_produce_column(const float4* __restrict__ V, 
         const float2 ub = up[b];
 #pragma unroll
         for (int u = 0; u < NU; ++u)
-            if (u < NU - 1 || TC_NH * u + h < r3) cfma2(w[u], vp[4 * b + 4 * TC_NH * r2 * u], ub);
+            if (u < NU - 2 || TC_NH * u + h < r3) cfma2(w[u], vp[4 * b + 4 * TC_NH * r2 * u], ub);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(fempty_s);  // this warp no longer reads the slot
@@ -221,7 +221,7 @@ __device__ __forceinline__ void tc_produce_column(const float4* __restrict__ V, 
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
         const int c = TC_NH * u + h;
-        if (u < NU - 1 || c < r3) {
+        if (u < NU - 2 || c < r3) {
             const uint32_t K = ring.kpos + uint32_t(c);
             uint32_t s, ph;
             ring_ahead(ring, K >> 4, nst, s, ph);
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
         }
     } else if (warp >= TC_PW0 && warp < TC_FW0) {
-        static_assert(TC_NH * 6 >= TC_RMAX, "producer switch covers ceil(TC_RMAX / TC_NH)");
+        static_assert(TC_NH * 16 >= TC_RMAX, "producer switch covers ceil(TC_RMAX / TC_NH)");
         // ------------------------------------------------------ A producers
         // warp pw: i1 = pw & 3 (warp-uniform), c partition h = pw / 4, lane = i2;
         // tile row = i2 + 32 i1 (= TMEM lane of the accumulator)
@@ -437,13 +437,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #define TC_COL(NU)                                                                                              \
     tc_produce_column<NU>(V, U2, (g.debug & 1) ? 0 : r2, r2 | 1, r3, h, xj, &fempty[fs], empty, full, sA, rowbase, xorv, lane, nst, \
                           ring)
+                // NU = ceil(r3 / NH) rounded up to even above 4 (fewer
+                // instantiations; the last u is predicated by c < r3)
                 switch ((r3 + TC_NH - 1) / TC_NH) {
                     case 1: TC_COL(1); break;
                     case 2: TC_COL(2); break;
                     case 3: TC_COL(3); break;
                     case 4: TC_COL(4); break;
-                    case 5: TC_COL(5); break;
-                    default: TC_COL(6); break;
+                    case 5: case 6: TC_COL(6); break;
+                    case 7: case 8: TC_COL(8); break;
+                    case 9: case 10: TC_COL(10); break;
+                    case 11: case 12: TC_COL(12); break;
+                    case 13: case 14: TC_COL(14); break;
+                    default: TC_COL(16); break;
                 }
 #undef TC_COL
                 if (++fs == TC_JR) {
@@ -468,15 +474,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     } else if (warp >= TC_FW0) {
         // ------------------------------------------ chain fold + epilogue
         // The running sum of the tile lives in this CTA's private scratch
-        // rsum[blockIdx.x][i3][row] (L2-resident, row-contiguous so a warp's
-        // 32 rows are one coalesced 256-byte access); every chain is added
-        // to it with round-to-nearest fp32 adds, the last one goes to y.
+        // rsum[blockIdx.x][i3 / 2][row] as float4 (re, im of i3 and i3 + 1;
+        // L2-resident, a warp's 32 rows are one coalesced 512-byte access).
+        // The fold is fire-and-forget so the accumulator is released as soon
+        // as TMEM has been read: the first chain of a tile stores, later
+        // chains add with red.global.add.v4.f32 (round-to-nearest; every
+        // element is only ever touched by this thread, in program order, so
+        // the sum is deterministic), and the last chain reads the running sum
+        // back and writes y.
         const int quarter = warp & 3;             // TMEM lane quarter = i1 of the tile
         const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
         const uint32_t tC = tmem + lane_addr;
         const int row = lane + 32 * quarter;      // row = i2 + 32 i1
         const int span = g.nmma * g.nh3;
-        float2* rs = rsum + int64_t(blockIdx.x) * span * TC_ROWS + row;
+        float4* rs = reinterpret_cast<float4*>(rsum) + int64_t(blockIdx.x) * (span / 2) * TC_ROWS + row;
         const int64_t nv3 = int64_t(g.n1) * g.n2 * g.n3;
         const float inv = 1.f / (fp16_scale(*wmax) * TC_U3_SCALE);  // exact power of two
         uint32_t gch = 0;
@@ -499,26 +510,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         tmem_ld16(tC + col, cr);
                         tmem_ld16(tC + col + uint32_t(g.nmma), ci);
                         tmem_ld_wait();
-                        const int i3l = hh * g.nmma + cb;
-                        float2* rp = rs + int64_t(i3l) * TC_ROWS;
-                        if (ch > 0) {
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) {
-                                const float2 r = rp[int64_t(i) * TC_ROWS];
-                                cr[i] = __float_as_uint(__uint_as_float(cr[i]) + r.x);
-                                ci[i] = __float_as_uint(__uint_as_float(ci[i]) + r.y);
-                            }
-                        }
+                        const int i3l = hh * g.nmma + cb;  // even
+                        float4* rp = rs + int64_t(i3l / 2) * TC_ROWS;
                         if (!last) {
 #pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                rp[int64_t(i) * TC_ROWS] = make_float2(__uint_as_float(cr[i]), __uint_as_float(ci[i]));
-                        } else if (eok) {
+                            for (int m = 0; m < 8; ++m) {
+                                float4* a = rp + int64_t(m) * TC_ROWS;
+                                const float4 v = make_float4(__uint_as_float(cr[2 * m]), __uint_as_float(ci[2 * m]),
+                                                             __uint_as_float(cr[2 * m + 1]),
+                                                             __uint_as_float(ci[2 * m + 1]));
+                                if (ch == 0)
+                                    *a = v;
+                                else
+                                    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(a), "f"(v.x),
+                                                 "f"(v.y), "f"(v.z), "f"(v.w)
+                                                 : "memory");
+                            }
+                        } else {
+                            float4 r[8];
+                            if (ch > 0) {
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) {
-                                const int i3 = tl.i3_0 + i3l + i;
-                                if (i3 < g.n3)
-                                    yp[pl * i3] = make_float2(__uint_as_float(cr[i]) * inv, __uint_as_float(ci[i]) * inv);
+                                for (int m = 0; m < 8; ++m) r[m] = rp[int64_t(m) * TC_ROWS];
+                            } else {
+#pragma unroll
+                                for (int m = 0; m < 8; ++m) r[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            }
+                            if (eok) {
+#pragma unroll
+                                for (int m = 0; m < 8; ++m) {
+                                    const int i3 = tl.i3_0 + i3l + 2 * m;
+                                    if (i3 < g.n3)
+                                        yp[pl * i3] = make_float2((__uint_as_float(cr[2 * m]) + r[m].x) * inv,
+                                                                  (__uint_as_float(ci[2 * m]) + r[m].y) * inv);
+                                    if (i3 + 1 < g.n3)
+                                        yp[pl * (i3 + 1)] = make_float2((__uint_as_float(cr[2 * m + 1]) + r[m].z) * inv,
+                                                                        (__uint_as_float(ci[2 * m + 1]) + r[m].w) * inv);
+                                }
                             }
                         }
                     }
