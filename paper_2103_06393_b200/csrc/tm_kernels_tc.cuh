@@ -308,11 +308,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     } else {
                         mbar_arrive_expect_tx(&full[s], uint32_t(g.b_stage));
                         unsigned char* dst = sB + s * g.b_stage;
-                        // per i3 half: HBM planes 1, 2 (U3r, U3i hi) and 4, 5 (lo) -> smem 0..3
+                        // smem plane pl = (U3r hi, U3i hi, U3r lo, U3i lo) holds both i3 halves
+                        // contiguously ([pl][hh][nmma rows]): HBM planes 1, 2, 4, 5
                         for (int hh = 0; hh < g.nh3; ++hh)
 #pragma unroll
                             for (int pl = 0; pl < TC_FPLANES; ++pl)
-                                tma_load_3d(dst + (hh * TC_FPLANES + pl) * plane_bytes, &bmap, &full[s], kk * 16,
+                                tma_load_3d(dst + (pl * g.nh3 + hh) * plane_bytes, &bmap, &full[s], kk * 16,
                                             tl.i3_0 + hh * g.nmma, (1 + pl + (pl >> 1)) * g.q + tl.k);
                     }
                     if (++s == nst) {
@@ -325,15 +326,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer
         if (elect_one()) {
-            // complex product per i3 half hh (TMEM columns 2 NMMA hh + [0, 2 NMMA)):
-            //   [Yr | Yi] += Ar . [U3r | U3i]   (one MMA of width 2 NMMA)
-            //   Yr -= Ai . U3i,  Yi += Ai . U3r (width NMMA, negate-A bit)
-            // each as hi.hi + hi.lo + lo.hi; smem B planes per half:
-            // U3r hi, U3i hi, U3r lo, U3i lo
-            const uint32_t id_w = umma_idesc_f16(TC_ROWS, 2 * g.nmma, false, false);
-            const uint32_t id_p = umma_idesc_f16(TC_ROWS, g.nmma, false, false);
-            const uint32_t id_n = umma_idesc_f16(TC_ROWS, g.nmma, true, false);
-            const int plane_b = g.nmma * 32;
+            // complex product over the tile's span = nh3 * NMMA voxels along i3
+            // (TMEM: Yr at [0, span), Yi at [span, 2 span)), four real products
+            // of full width N = span, each as hi.hi + hi.lo + lo.hi:
+            //   Yr += Ar.U3r,  Yr -= Ai.U3i (negate-A bit),  Yi += Ar.U3i,  Yi += Ai.U3r
+            const int span = g.nmma * g.nh3;
+            const uint32_t id_p = umma_idesc_f16(TC_ROWS, span, false, false);
+            const uint32_t id_n = umma_idesc_f16(TC_ROWS, span, true, false);
+            const int plane_b = span * 32;  // one smem B plane (all i3 of the tile)
             uint32_t s = 0, ph = 0, gch = 0;
             for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
                 const TcTile tl = tc_tile(g, t);
@@ -353,23 +353,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
                     for (int pl = 0; pl < 4; ++pl) A[pl] = umma_smem_desc(a0 + pl * TC_A_PLANE, 256, 6);
                     const uint32_t acc = cpos > 0 ? 1u : 0u;
-                    for (int hh = 0; hh < g.nh3; ++hh) {
-                        const uint32_t bh = b0 + uint32_t(hh * TC_FPLANES * plane_b);
-                        const uint64_t Brh = umma_smem_desc(bh + 0 * plane_b, 256, 6);  // [U3r|U3i] hi window
-                        const uint64_t Bih = umma_smem_desc(bh + 1 * plane_b, 256, 6);
-                        const uint64_t Brl = umma_smem_desc(bh + 2 * plane_b, 256, 6);  // [U3r|U3i] lo window
-                        const uint64_t Bil = umma_smem_desc(bh + 3 * plane_b, 256, 6);
-                        const uint32_t yr = tmem + uint32_t(2 * g.nmma * hh), yi = yr + uint32_t(g.nmma);
-                        mma_f16(yr, A[0], Brh, id_w, acc);
-                        mma_f16(yr, A[0], Brl, id_w, 1);
-                        mma_f16(yr, A[1], Brh, id_w, 1);
-                        mma_f16(yr, A[2], Bih, id_n, 1);
-                        mma_f16(yr, A[2], Bil, id_n, 1);
-                        mma_f16(yr, A[3], Bih, id_n, 1);
-                        mma_f16(yi, A[2], Brh, id_p, 1);
-                        mma_f16(yi, A[2], Brl, id_p, 1);
-                        mma_f16(yi, A[3], Brh, id_p, 1);
-                    }
+                    const uint64_t Brh = umma_smem_desc(b0 + 0 * plane_b, 256, 6);
+                    const uint64_t Bih = umma_smem_desc(b0 + 1 * plane_b, 256, 6);
+                    const uint64_t Brl = umma_smem_desc(b0 + 2 * plane_b, 256, 6);
+                    const uint64_t Bil = umma_smem_desc(b0 + 3 * plane_b, 256, 6);
+                    const uint32_t yr = tmem, yi = tmem + uint32_t(span);
+                    mma_f16(yr, A[0], Brh, id_p, acc);
+                    mma_f16(yr, A[0], Brl, id_p, 1);
+                    mma_f16(yr, A[1], Brh, id_p, 1);
+                    mma_f16(yr, A[2], Bih, id_n, 1);
+                    mma_f16(yr, A[2], Bil, id_n, 1);
+                    mma_f16(yr, A[3], Bih, id_n, 1);
+                    mma_f16(yi, A[0], Bih, id_p, acc);
+                    mma_f16(yi, A[0], Bil, id_p, 1);
+                    mma_f16(yi, A[1], Bih, id_p, 1);
+                    mma_f16(yi, A[2], Brh, id_p, 1);
+                    mma_f16(yi, A[2], Brl, id_p, 1);
+                    mma_f16(yi, A[3], Brh, id_p, 1);
                     mma_commit(&empty[s]);
                     if (++s == nst) {
                         s = 0;
@@ -506,11 +506,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 for (int hh = 0; hh < g.nh3; ++hh)
                     for (int cb = 0; cb < g.nmma; cb += 16) {
                         uint32_t cr[16], ci[16];
-                        const uint32_t col = uint32_t(2 * g.nmma * hh + cb);
-                        tmem_ld16(tC + col, cr);
-                        tmem_ld16(tC + col + uint32_t(g.nmma), ci);
+                        const int i3l = hh * g.nmma + cb;  // even; Yr at column i3l, Yi at span + i3l
+                        tmem_ld16(tC + uint32_t(i3l), cr);
+                        tmem_ld16(tC + uint32_t(span + i3l), ci);
                         tmem_ld_wait();
-                        const int i3l = hh * g.nmma + cb;  // even
                         float4* rp = rs + int64_t(i3l / 2) * TC_ROWS;
                         if (!last) {
 #pragma unroll
