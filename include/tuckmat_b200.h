@@ -121,6 +121,15 @@ TM_API int tm_aca_forward(tm_store* s, const void* x, int64_t ldx, int64_t xrows
 TM_API int tm_aca_adjoint(tm_store* s, const void* phi, int64_t ldphi, int64_t phirows, int64_t p, void* z,
                           int64_t ldz, int where, void* stream);
 
+/* Rows of the stored operator at the requested global rows (host array,
+ * rows[r] = k*n_v + v, v = i1 + n1*(i2 + n2*i3)): out[r + ldout*j] =
+ * T_jk[v] for every column j — element() (src/tensor.cpp:183-196) per
+ * column, i.e. row_of_compressed_u (src/aca.cpp:234-244) for an ACA store.
+ * out is nrows x ncols, host or device per `where`.  An index outside
+ * [0, q*n_v) is a contract violation ("element: index out of range"). */
+TM_API int tm_rows(tm_store* s, const int64_t* rows, int64_t nrows, void* out, int64_t ldout, int where,
+                   void* stream);
+
 /* Exact OpCounts of one product at p right-hand sides, without running it
  * (reconstruct_madds, src/matvec.cpp:10-15; accumulate term :51,95). */
 TM_API int tm_opcounts(const tm_store* s, int64_t p, int64_t* decompress_madds, int64_t* accumulate_madds);

@@ -198,6 +198,12 @@ MultiVector adjoint(const CompressedCoupling& cc, const MultiVector& phi, int wo
 MultiVector aca_forward(const AcaFactors& fac, const MultiVector& x, int workers = 1);
 MultiVector aca_adjoint(const AcaFactors& fac, const MultiVector& phi, int workers = 1);
 
+// tensor.hpp:105 / src/tensor.cpp:183-196 and aca.hpp:57 / src/aca.cpp:234-244,
+// evaluated on the device (tm_rows).  row_of_compressed_u returns a 1 x rank
+// MultiVector (the reference returns Eigen::RowVectorXcd).
+Complex element(const TuckerTensor& tt, Index i1, Index i2, Index i3);
+MultiVector row_of_compressed_u(const AcaFactors& fac, Index i);
+
 // ------------------------------------------------------ B200 extensions --
 namespace b200 {
 

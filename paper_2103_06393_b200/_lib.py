@@ -19,7 +19,7 @@ TM_HOST, TM_DEVICE = 0, 1
 
 EXPORTED = [
     "tm_store_create", "tm_store_load_ctc1", "tm_store_load_cta1", "tm_store_destroy", "tm_store_info",
-    "tm_forward", "tm_adjoint", "tm_aca_forward", "tm_aca_adjoint", "tm_opcounts", "tm_last_error",
+    "tm_forward", "tm_adjoint", "tm_aca_forward", "tm_aca_adjoint", "tm_opcounts", "tm_rows", "tm_last_error",
     "tm_launch_count", "tm_version",
 ]
 
@@ -63,6 +63,7 @@ def lib():
             L.tm_aca_forward.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp]
             L.tm_aca_adjoint.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp]
             L.tm_opcounts.argtypes = [vp, i64, vp, vp]
+            L.tm_rows.argtypes = [vp, vp, i64, vp, i64, i32, vp]
             L.tm_last_error.restype = ctypes.c_char_p
             L.tm_launch_count.restype = ctypes.c_int64
             _lib = L

@@ -102,4 +102,40 @@ __global__ void zero_kernel(C* __restrict__ y, int64_t rows, int64_t p, int64_t 
         y[(i % rows) + ldy * (i / rows)] = cmake<C>(R(0), R(0));
 }
 
+// Batched element extraction: out[r + ldout j] = T_jk[v] for
+// the requested global rows rows[r] = k n_v + v, v = i1 + n1 (i2 + n2 i3) —
+// the reference's element() (src/tensor.cpp:183-196) for every column j, i.e.
+// row_of_compressed_u (src/aca.cpp:234-244) on ACA stores.  One thread per
+// (row, column): the three factor rows contracted into the core, O(r1 r2 r3).
+// Accumulation in double for the c128 store, float for c64 (as the products).
+template <typename C>
+__global__ void rows_kernel(const TDesc* __restrict__ td, const C* __restrict__ arena, int64_t ncols, int64_t n1,
+                            int64_t n2, int64_t nv, const int64_t* __restrict__ rows, C* __restrict__ out,
+                            int64_t ldout) {
+    using R = decltype(C{}.x);
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t r = blockIdx.y;
+    if (j >= ncols) return;
+    const int64_t row = rows[r];
+    const int64_t k = row / nv, v = row - k * nv;
+    const int64_t i1 = v % n1, i2 = (v / n1) % n2, i3 = v / (n1 * n2);
+    const TDesc d = td[k * ncols + j];
+    const C* G = arena + d.off_core;
+    const C* u1 = arena + d.off_u1 + i1 * d.r1;
+    const C* u2 = arena + d.off_u2 + i2 * d.r2;
+    const C* u3 = arena + d.off_u3 + i3 * d.r3;
+    C e = cmake<C>(R(0), R(0));
+    for (int c = 0; c < d.r3; ++c) {
+        C sc = cmake<C>(R(0), R(0));
+        for (int b = 0; b < d.r2; ++b) {
+            C sb = cmake<C>(R(0), R(0));
+            const C* g = G + int64_t(d.r1) * (b + int64_t(d.r2) * c);
+            for (int a = 0; a < d.r1; ++a) cfma(sb, u1[a], g[a]);
+            cfma(sc, u2[b], sb);
+        }
+        cfma(e, u3[c], sc);
+    }
+    out[r + ldout * j] = e;
+}
+
 }  // namespace tmb

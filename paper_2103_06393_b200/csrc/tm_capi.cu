@@ -999,6 +999,57 @@ TM_API int tm_store_info(const tm_store* s, int32_t* q, int64_t* ncols, int64_t*
     });
 }
 
+TM_API int tm_rows(tm_store* s, const int64_t* rows, int64_t nrows, void* out, int64_t ldout, int where,
+                   void* stream) {
+    return guarded([&] {
+        if (!s) contract("null store");
+        if (nrows < 0) contract("negative row count");
+        if (where != TM_HOST && where != TM_DEVICE) contract("where must be TM_HOST or TM_DEVICE");
+        if (nrows > 0 && (!rows || !out)) contract("null rows or output pointer");
+        if (nrows > 0 && ldout < nrows) contract("leading dimension of the output is too small");
+        for (int64_t r = 0; r < nrows; ++r)
+            if (rows[r] < 0 || rows[r] >= s->rows()) contract("element: index out of range");
+        if (nrows == 0 || s->ncols == 0) return;
+        if (nrows > 65535) contract("tm_rows: at most 65535 rows per call");
+        std::lock_guard<std::mutex> lock(s->mu);
+        DeviceGuard guard(s->device);
+        const size_t cs = s->csize();
+        cudaStream_t st = where == TM_DEVICE ? static_cast<cudaStream_t>(stream) : nullptr;
+        bool own = false;
+        if (where == TM_HOST) {
+            CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            own = true;
+        }
+        try {
+            int64_t* d_rows = static_cast<int64_t*>(s->wbuf.get(size_t(nrows) * sizeof(int64_t)));
+            CK(cudaMemcpyAsync(d_rows, rows, size_t(nrows) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+            void* dout = where == TM_DEVICE ? out : s->yout.get(size_t(nrows * s->ncols) * cs);
+            const int64_t ld = where == TM_DEVICE ? ldout : nrows;
+            const dim3 grid(unsigned((s->ncols + 127) / 128), unsigned(nrows));
+            if (s->dtype == TM_C64)
+                rows_kernel<float2><<<grid, 128, 0, st>>>(s->d_desc, static_cast<const float2*>(s->d_arena), s->ncols,
+                                                          s->dims[0], s->dims[1], s->nv(), d_rows,
+                                                          static_cast<float2*>(dout), ld);
+            else
+                rows_kernel<double2><<<grid, 128, 0, st>>>(s->d_desc, static_cast<const double2*>(s->d_arena),
+                                                           s->ncols, s->dims[0], s->dims[1], s->nv(), d_rows,
+                                                           static_cast<double2*>(dout), ld);
+            launched(cudaSuccess, "rows_kernel");
+            if (where == TM_HOST)
+                CK(cudaMemcpy2DAsync(out, size_t(ldout) * cs, dout, size_t(nrows) * cs, size_t(nrows) * cs,
+                                     size_t(s->ncols), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        } catch (...) {
+            if (own) {
+                cudaStreamSynchronize(st);
+                cudaStreamDestroy(st);
+            }
+            throw;
+        }
+        if (own) CK(cudaStreamDestroy(st));
+    });
+}
+
 TM_API int tm_opcounts(const tm_store* s, int64_t p, int64_t* dec, int64_t* acc) {
     return guarded([&] {
         if (!s) contract("null store");

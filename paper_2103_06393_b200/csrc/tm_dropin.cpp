@@ -282,6 +282,45 @@ MultiVector stacked_adjoint(const TuckerColumns& z, const MultiVector& x, int, O
     return adj(s.handle(), g_dtype, x, ops);
 }
 
+namespace {
+// One row of a store through tm_rows, in the store's dtype, as complex<double>.
+std::vector<Complex> store_row(tm_store* s, int dtype, Index row, Index ncols) {
+    std::vector<Complex> r(static_cast<std::size_t>(ncols));
+    const std::int64_t idx = row;
+    if (dtype == TM_C128) {
+        check(tm_rows(s, &idx, 1, r.data(), 1, TM_HOST, nullptr));
+    } else {
+        std::vector<std::complex<float>> f(static_cast<std::size_t>(ncols));
+        check(tm_rows(s, &idx, 1, f.data(), 1, TM_HOST, nullptr));
+        for (std::size_t i = 0; i < f.size(); ++i) r[i] = Complex(f[i].real(), f[i].imag());
+    }
+    return r;
+}
+}  // namespace
+
+Complex element(const TuckerTensor& tt, Index i1, Index i2, Index i3) {
+    const Dims3 d = tt.dims;
+    if (i1 < 0 || i1 >= d[0] || i2 < 0 || i2 >= d[1] || i3 < 0 || i3 >= d[2])
+        throw ContractViolation("element: index out of range");
+    TuckerColumns z;
+    z.ncols = 1;
+    z.q = 1;
+    z.grid_dims = d;
+    z.tensor = [&](Index, int) -> const TuckerTensor& { return tt; };
+    b200::DeviceStore s(z, g_dtype, current_device());
+    return store_row(s.handle(), g_dtype, i1 + d[0] * (i2 + d[1] * i3), 1)[0];
+}
+
+MultiVector row_of_compressed_u(const AcaFactors& fac, Index i) {
+    if (!fac.compressed()) throw ContractViolation("row_of_compressed_u: U is stored dense");
+    if (i < 0 || i >= fac.rows()) throw ContractViolation("element: index out of range");
+    auto s = store_of(fac);
+    const std::vector<Complex> r = store_row(s.get(), g_dtype, i, fac.rank());
+    MultiVector out(1, fac.rank());
+    for (Index l = 0; l < fac.rank(); ++l) out(0, l) = r[static_cast<std::size_t>(l)];
+    return out;
+}
+
 MultiVector aca_forward(const AcaFactors& fac, const MultiVector& x, int) {
     if (x.rows() != fac.cols())
         throw ContractViolation("aca_forward: x has " + std::to_string(x.rows()) + " rows, expected " +

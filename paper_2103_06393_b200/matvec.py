@@ -197,6 +197,24 @@ class DeviceStore:
     def np_dtype(self):
         return _NP[self.dtype]
 
+    def row_block(self, indices):
+        """Rows of the stored operator at global row indices (k*n_v + v):
+        an (len(indices), ncols) array with entry [r, j] = T_jk[v] — the
+        reference's element() per column (src/tensor.cpp:183-196), i.e.
+        row_of_compressed_u (src/aca.cpp:234-244) on an ACA store."""
+        idx = np.ascontiguousarray(np.asarray(indices, dtype=np.int64).reshape(-1))
+        out = np.zeros((idx.size, self.ncols), dtype=self.np_dtype, order="F")
+        _check(lib().tm_rows(self.handle, idx.ctypes.data, idx.size, out.ctypes.data, max(idx.size, 1), TM_HOST,
+                             None))
+        return out
+
+    def element(self, j, k, i1, i2, i3):
+        """element(tucker_jk, i1, i2, i3) (src/tensor.cpp:183-196)."""
+        n1, n2, n3 = self.dims
+        if not (0 <= j < self.ncols and 0 <= k < self.q and 0 <= i1 < n1 and 0 <= i2 < n2 and 0 <= i3 < n3):
+            raise ContractViolation("element: index out of range")
+        return self.row_block([k * self.num_voxels + i1 + n1 * (i2 + n2 * i3)])[0, j]
+
     def opcounts(self, p=1):
         """Exact OpCounts of one product at p right-hand sides (matvec.cpp:10-15,50-51)."""
         dec = ctypes.c_int64()

@@ -137,6 +137,14 @@ int main(int argc, char** argv) {
                     (long long)ops.decompress_madds);
         MultiVector z = adjoint(cc, y, 1, &ops);
         std::printf("gpu adjoint ok norm=%.17g\n", z.norm());
+        const Complex e = element(cc.columns[3][1], 2, 5, 7);
+        std::printf("element %.17g %.17g\n", e.real(), e.imag());
+        try {
+            element(cc.columns[3][1], 2, 5, 99);
+            return 6;
+        } catch (const ContractViolation& e2) {
+            std::printf("contract: %s\n", e2.what());
+        }
     } catch (const Error& e) {
         std::printf("device error: %s\n", e.what());
         return 5;

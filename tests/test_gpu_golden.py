@@ -60,6 +60,14 @@ def test_cpp_dropin_on_gpu(product, tmp_path):
     r = subprocess.run([str(exe), os.path.join(GOLD, "loop8.ctc1")], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "gpu forward ok rows=1536" in r.stdout and "gpu adjoint ok" in r.stdout
+    assert "contract: element: index out of range" in r.stdout
+    # element(tensor (j=3, k=1), 2, 5, 7) vs the oracle's element()
+    from oracle import oracle as O
+    cc = O.load_ctc1(os.path.join(GOLD, "loop8.ctc1"))
+    want = O.OracleStore(cc).element(3, 1, 2, 5, 7)
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("element ")][0].split()
+    got = complex(float(line[1]), float(line[2]))
+    assert abs(got - want) <= 1e-12 * max(abs(want), 1e-30)
 
 
 def test_umma_probe():

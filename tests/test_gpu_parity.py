@@ -299,3 +299,50 @@ def test_batched_forward(oracle, product, monkeypatch, dims, q, m, rmin, rmax, p
     # single-RHS product of column c
     y1 = ds.forward(x[:, p - 1:p])
     assert rel(y_b[:, p - 1:p], y1) <= 1e-5
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_rows_and_element(oracle, product, dtype):
+    """Batched element() / row_of_compressed_u: rows of the
+    stored operator vs the oracle's element() and vs columns of the forward."""
+    O, P = oracle, product
+    cc = ragged_store((13, 11, 20), 3, 9, 1, 7, seed=5)
+    ref = O.OracleStore(cc.rounded_c64() if dtype == "c64" else cc)
+    ds = P.DeviceStore.from_compressed(cc, dtype)
+    n1, n2, n3 = cc.grid_dims
+    nv = n1 * n2 * n3
+    rng = np.random.default_rng(3)
+    rows = rng.integers(0, 3 * nv, size=17)
+    got = ds.row_block(rows)
+    want = np.zeros_like(got, dtype=np.complex128)
+    for r, g in enumerate(rows):
+        k, v = divmod(int(g), nv)
+        i1, i2, i3 = v % n1, (v // n1) % n2, v // (n1 * n2)
+        for j in range(cc.m):
+            want[r, j] = ref.element(j, k, i1, i2, i3)
+    tol = TOL[dtype]
+    assert rel(got, want) <= tol
+    # the same rows of Z from the product with basis vectors (test_matvec.cpp:38-48)
+    y = ds.forward(np.eye(cc.m))
+    assert rel(got, y[rows, :]) <= tol
+    assert abs(ds.element(4, 2, 1, 2, 3) - ref.element(4, 2, 1, 2, 3)) <= 10 * tol * np.abs(want).max()
+    with pytest.raises(P.ContractViolation, match="index out of range"):
+        ds.row_block([3 * nv])
+    with pytest.raises(P.ContractViolation, match="index out of range"):
+        ds.element(0, 0, n1, 0, 0)
+
+
+def test_row_of_compressed_u_aca(oracle, product):
+    """row_of_compressed_u on an ACA store (src/aca.cpp:234-244)."""
+    O, P = oracle, product
+    import os
+    GOLD = os.path.join(os.path.dirname(__file__), "golden")
+    ds = P.DeviceStore.load_cta1(os.path.join(GOLD, "aca8.cta1"), "c128")
+    fac = O.load_cta1(os.path.join(GOLD, "aca8.cta1"))[0]
+    i = 5 + ds.num_voxels  # component 1
+    got = ds.row_block([i])[0]
+    st = O.OracleStore(fac)
+    n1, n2, _ = ds.dims
+    v = i - ds.num_voxels
+    want = np.array([st.element(l, 1, v % n1, (v // n1) % n2, v // (n1 * n2)) for l in range(ds.ncols)])
+    assert rel(got, want) <= 1e-12
