@@ -106,21 +106,21 @@ __device__ __forceinline__ AjTile aj_tile(const AjGeom& g, int64_t t) {
 // h): W = V x_2 U2 (no x_j in the adjoint), Q[row, soff + c] from TMEM, and
 // the partial sum_c conj(W) Q of this thread's row.
 template <int NU>
-__device__ __forceinline__ float2 aj_consume_column(const float4* __restrict__ V, const float2* __restrict__ U2,
+__device__ __forceinline__ float2 aj_consume_column(const float2* __restrict__ V, const float2* __restrict__ U2,
                                                     int r2, int ld2, int r3, int h, int lane, uint32_t qaddr,
                                                     uint64_t* fempty_s) {
     using namespace sm100;
     uint64_t w[NU];
 #pragma unroll
     for (int u = 0; u < NU; ++u) w[u] = 0;
-    const float4* vp = V + 4 * r2 * h;
+    const float2* vp = V + 4 * r2 * h;
     const float2* up = U2 + lane * ld2;
 #pragma unroll 2
     for (int b = 0; b < r2; ++b) {
         const float2 ub = up[b];
 #pragma unroll
         for (int u = 0; u < NU; ++u)
-            if (u < NU - 1 || AJ_NH * u + h < r3) cfma2(w[u], vp[4 * b + 4 * AJ_NH * r2 * u], ub);
+            if (u < NU - 1 || AJ_NH * u + h < r3) cfma2v(w[u], vp[4 * b + 4 * AJ_NH * r2 * u], ub);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(fempty_s);
@@ -151,7 +151,7 @@ __device__ __forceinline__ float2 aj_consume_column(const float4* __restrict__ V
 
 __global__ void __launch_bounds__(AJ_THREADS, 1)
     adj_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
-                  const TcDesc* __restrict__ tcd, const float4* __restrict__ varena,
+                  const TcDesc* __restrict__ tcd, const float2* __restrict__ varena,
                   const float2* __restrict__ u2arena, const int* __restrict__ nch, const int* __restrict__ cstart,
                   AjGeom g, const float* __restrict__ phimax, float2* __restrict__ part) {
     using namespace sm100;
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                     unsigned char* slot = sSlot + s * g.slot_bytes;
                     const uint32_t r23 = uint32_t(d.r2 * d.r3);
                     const uint32_t ld2 = uint32_t(d.r2 | 1);
-                    const uint32_t bv = uint32_t(TC_TI1) * r23 * 16u;
+                    const uint32_t bv = round16(uint32_t(TC_TI1) * r23 * 8u);
                     const uint32_t b2 = uint32_t(TC_TI2) * ld2 * 8u;
                     mbar_arrive_expect_tx(&ffull[s], uint32_t(sizeof(TcDesc)) + bv + b2);
                     bulk_g2s(slot, tdk + j, uint32_t(sizeof(TcDesc)), &ffull[s]);
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                     const unsigned char* slot = sSlot + fs * g.slot_bytes;
                     const TcDesc* dd = reinterpret_cast<const TcDesc*>(slot);
                     const int r2 = dd->r2, r3 = dd->r3, soff = dd->pad0;
-                    const float4* V = reinterpret_cast<const float4*>(slot + TC_SLOT_V) + i1l;
+                    const float2* V = reinterpret_cast<const float2*>(slot + TC_SLOT_V) + i1l;
                     const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
                     float2 a;
 #define AJ_COL(NU) a = aj_consume_column<NU>(V, U2, r2, r2 | 1, r3, h, lane, qbase + uint32_t(soff), &fempty[fs])

@@ -125,7 +125,7 @@ struct tm_store {
     __half* d_planes = nullptr;
     float* d_vbound = nullptr;  // [q*ncols] per-tensor bound of |W| / |x_j|
     TcDesc* d_tcd = nullptr;  // [q*ncols] tensor-core descriptors
-    float4* d_varena = nullptr;  // mode-1 products V = U1 x_1 G (FFMA2 form)
+    float2* d_varena = nullptr;  // mode-1 products V = U1 x_1 G
     float2* d_u2arena = nullptr;  // U2 with odd row strides
     // tensor-core adjoint: chunk-aligned, i3-contiguous U3 planes
     bool tca_ok = false;
@@ -247,7 +247,7 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
             cstart[static_cast<size_t>(k) * (s->maxch + 1) + n] = cst[static_cast<size_t>(k)][n];
     const int64_t n3p = (n3 + 7) / 8 * 8;
     const size_t abytes = size_t(TC_BPLANES) * s->q * s->nslots * n3p * sizeof(__half);
-    const size_t vbytes = size_t(voff) * sizeof(float4);
+    const size_t vbytes = size_t(voff) * sizeof(float2);
     const size_t u2bytes = size_t(u2off) * sizeof(float2);
     CK(cudaMalloc(&s->d_kofs, kofs.size() * sizeof(int)));
     CK(cudaMalloc(&s->d_kc, kc.size() * sizeof(int)));
@@ -567,7 +567,7 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     g.ntiles = int64_t(p) * g.q * g.nt3 * g.nt2 * g.nt1;
     g.rmax2 = s->rmax[1];
     g.rmax3 = s->rmax[2];
-    g.u2_off = TC_SLOT_V + TC_TI1 * g.rmax2 * g.rmax3 * 16;
+    g.u2_off = TC_SLOT_V + int(round16(uint32_t(TC_TI1 * g.rmax2 * g.rmax3 * 8)));
     g.slot_bytes = (g.u2_off + TC_TI2 * (g.rmax2 | 1) * 8 + 127) / 128 * 128;
     g.b_stage = g.nh3 * TC_FPLANES * g.nmma * 32;
     g.chain = tc_chain();
@@ -647,7 +647,7 @@ void run_forward_mrhs(tm_store* s, const float2* x, int64_t ldx, int64_t p, floa
     g.nks = int((s->ncols + 7) / 8);
     g.chain = tc_chain();
     g.v_off = 64;
-    g.u2_off = g.v_off + TC_TI1 * s->rmax[1] * s->rmax[2] * 16;
+    g.u2_off = g.v_off + int(round16(uint32_t(TC_TI1 * s->rmax[1] * s->rmax[2] * 8)));
     g.u3_off = g.u2_off + MR_TI2 * (s->rmax[1] | 1) * 8;
     g.slot_bytes = (g.u3_off + int(round16(uint32_t(MR_TI3 * s->rmax[2]) * 8u)) + 127) / 128 * 128;
     const size_t smem = 1024 + size_t(MR_NST) * (MR_A_STAGE + MR_B_STAGE) + size_t(MR_JR) * g.slot_bytes +
@@ -702,7 +702,7 @@ void forward_dev(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, in
 }
 
 size_t adj_tc_smem(const tm_store* s) {
-    const int u2_off = TC_SLOT_V + TC_TI1 * s->rmax[1] * s->rmax[2] * 16;
+    const int u2_off = TC_SLOT_V + int(round16(uint32_t(TC_TI1 * s->rmax[1] * s->rmax[2] * 8)));
     const int slot = (u2_off + TC_TI2 * (s->rmax[1] | 1) * 8 + 127) / 128 * 128;
     return 1024 + size_t(AJ_NST) * (AJ_A_STAGE + AJ_B_STAGE) + size_t(TC_JR) * slot +
            size_t(2) * AJ_MAXCOLS * AJ_NPW * sizeof(float2) + (2 * AJ_NST + 2 * TC_JR + 4) * 8 + 16;
@@ -723,7 +723,7 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     g.ntiles = int64_t(p) * g.q * g.nrt;
     g.rmax2 = s->rmax[1];
     g.rmax3 = s->rmax[2];
-    g.u2_off = TC_SLOT_V + TC_TI1 * g.rmax2 * g.rmax3 * 16;
+    g.u2_off = TC_SLOT_V + int(round16(uint32_t(TC_TI1 * g.rmax2 * g.rmax3 * 8)));
     g.slot_bytes = (g.u2_off + TC_TI2 * (g.rmax2 | 1) * 8 + 127) / 128 * 128;
     g.maxch = s->maxch;
     const size_t smem = 1024 + size_t(AJ_NST) * (AJ_A_STAGE + AJ_B_STAGE) + size_t(TC_JR) * g.slot_bytes +

@@ -92,9 +92,8 @@ constexpr int TC_BPLANES = 6;                // B planes in HBM: [-U3i, U3r, U3i
 constexpr int TC_FPLANES = 4;                // forward B planes per stage: [U3r, U3i] x {hi, lo}
 
 // Per-tensor descriptor of the tensor-core forward (component-major like
-// TDesc).  off_v: float4 offset of the tensor's mode-1 product
-// V = U1 x_1 G in the V arena, laid out [i1/4][b + r2 c][i1 % 4] with each
-// complex stored as (vr, vi, -vi, vr) (the FFMA2 operand form); off_u2:
+// TDesc).  off_v: float2 offset of the tensor's mode-1 product
+// V = U1 x_1 G in the V arena, laid out [i1/4][b + r2 c][i1 % 4]; off_u2:
 // float2 offset of the tensor's U2 copy in the U2 arena, n2 rounded up to
 // TI2 rows (zero rows past n2) with an odd row stride r2 | 1 (conflict-free
 // 32-lane row loads); pad0: the (j, c) slot of the column inside its
@@ -184,7 +183,7 @@ __device__ __forceinline__ void ring_ahead(const ARing& r, uint32_t i, uint32_t 
 // All lanes of a producer warp share i1 (lane = i2), so the V operand of
 // each FFMA2 is a warp-uniform shared-memory broadcast.
 template <int NU>
-__device__ __forceinline__ void tc_produce_column(const float4* __restrict__ V, const float2* __restrict__ U2, int r2,
+__device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, const float2* __restrict__ U2, int r2,
                                                   int ld2, int r3, int h, float2 xj, uint64_t* fempty_s,
                                                   uint64_t* empty, uint64_t* full, unsigned char* sA,
                                                   uint32_t rowbase, uint32_t xorv, int lane, uint32_t nst,
@@ -193,15 +192,15 @@ __device__ __forceinline__ void tc_produce_column(const float4* __restrict__ V, 
     uint64_t w[NU];
 #pragma unroll
     for (int u = 0; u < NU; ++u) w[u] = 0;
-    // V[(b + r2 c) * 4 + il]: c = NH u + h  ->  stride 4 NH r2 float4 per u
-    const float4* vp = V + 4 * r2 * h;
+    // V[(b + r2 c) * 4 + il]: c = NH u + h  ->  stride 4 NH r2 float2 per u
+    const float2* vp = V + 4 * r2 * h;
     const float2* up = U2 + lane * ld2;
 #pragma unroll 2
     for (int b = 0; b < r2; ++b) {
         const float2 ub = up[b];
 #pragma unroll
         for (int u = 0; u < NU; ++u)
-            if (u < NU - 2 || TC_NH * u + h < r3) cfma2(w[u], vp[4 * b + 4 * TC_NH * r2 * u], ub);
+            if (u < NU - 2 || TC_NH * u + h < r3) cfma2v(w[u], vp[4 * b + 4 * TC_NH * r2 * u], ub);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(fempty_s);  // this warp no longer reads the slot
@@ -251,7 +250,7 @@ __device__ __forceinline__ void tc_produce_column(const float4* __restrict__ V, 
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap bmap, const TcDesc* __restrict__ tcd,
-                  const float4* __restrict__ varena, const float2* __restrict__ u2arena, const int* __restrict__ kc,
+                  const float2* __restrict__ varena, const float2* __restrict__ u2arena, const int* __restrict__ kc,
                   TcGeom g, const float2* __restrict__ x, int64_t ldx, float2* __restrict__ y, int64_t ldy,
                   float2* __restrict__ rsum, const float* __restrict__ wmax) {
     using namespace sm100;
@@ -397,7 +396,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     unsigned char* slot = sSlot + s * g.slot_bytes;
                     const uint32_t r23 = uint32_t(d.r2 * d.r3);
                     const uint32_t ld2 = uint32_t(d.r2 | 1);
-                    const uint32_t bv = uint32_t(TC_TI1) * r23 * 16u;
+                    const uint32_t bv = round16(uint32_t(TC_TI1) * r23 * 8u);
                     const uint32_t b2 = uint32_t(TC_TI2) * ld2 * 8u;
                     mbar_arrive_expect_tx(&ffull[s], uint32_t(sizeof(TcDesc)) + bv + b2);
                     bulk_g2s(slot, tdk + j, uint32_t(sizeof(TcDesc)), &ffull[s]);
@@ -432,7 +431,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const unsigned char* slot = sSlot + fs * g.slot_bytes;
                 const int r2 = reinterpret_cast<const TcDesc*>(slot)->r2;
                 const int r3 = reinterpret_cast<const TcDesc*>(slot)->r3;
-                const float4* V = reinterpret_cast<const float4*>(slot + TC_SLOT_V) + i1l;
+                const float2* V = reinterpret_cast<const float2*>(slot + TC_SLOT_V) + i1l;
                 const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
 #define TC_COL(NU)                                                                                              \
     tc_produce_column<NU>(V, U2, (g.debug & 1) ? 0 : r2, r2 | 1, r3, h, xj, &fempty[fs], empty, full, sA, rowbase, xorv, lane, nst, \
@@ -563,15 +562,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 // V_t[i1][b][c] = sum_a U1t[i1][a] G[a + r1 (b + r2 c)] for every tensor t
 // (the reference's mode-1 product, src/tensor.cpp:106-108, done once per
 // store instead of once per tile), accumulated in fp64 from the c64 factors
-// and stored [i1/4][b + r2 c][i1 % 4] as (vr, vi, -vi, vr); rows i1 >= n1 of
-// the last group of four are zero.
+// and stored [i1/4][b + r2 c][i1 % 4] as float2; rows i1 >= n1 of the last
+// group of four are zero.
 __global__ void build_v_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena,
-                               const TcDesc* __restrict__ tcd, int n1, float4* __restrict__ varena) {
+                               const TcDesc* __restrict__ tcd, int n1, float2* __restrict__ varena) {
     const int64_t t = blockIdx.x;
     const TDesc d = td[t];
     const int r23 = d.r2 * d.r3;
     const int n1p = (n1 + 3) & ~3;
-    float4* out = varena + tcd[t].off_v;
+    float2* out = varena + tcd[t].off_v;
     for (int e = threadIdx.x; e < n1p * r23; e += blockDim.x) {
         const int i1 = e / r23, bc = e - i1 * r23;
         double vr = 0.0, vi = 0.0;
@@ -585,7 +584,7 @@ __global__ void build_v_kernel(const TDesc* __restrict__ td, const float2* __res
             }
         }
         const float fr = float(vr), fi = float(vi);
-        out[int64_t(i1 >> 2) * 4 * r23 + int64_t(bc) * 4 + (i1 & 3)] = make_float4(fr, fi, -fi, fr);
+        out[int64_t(i1 >> 2) * 4 * r23 + int64_t(bc) * 4 + (i1 & 3)] = make_float2(fr, fi);
     }
 }
 
@@ -620,16 +619,16 @@ __global__ void build_bplanes_kernel(const TDesc* __restrict__ td, const float2*
 // Per tensor: max over (i1, c) of the 2-norm over b of V[i1, b, c] — a
 // bound on |W[row, c]| / |x_j| because every row of U2 has norm <= 1.
 __global__ void vbound_kernel(const TDesc* __restrict__ td, const TcDesc* __restrict__ tcd,
-                              const float4* __restrict__ varena, int n1, float* __restrict__ vbound) {
+                              const float2* __restrict__ varena, int n1, float* __restrict__ vbound) {
     const int64_t t = blockIdx.x;
     const int r2 = tcd[t].r2, r3 = tcd[t].r3;
-    const float4* v = varena + tcd[t].off_v;
+    const float2* v = varena + tcd[t].off_v;
     float m = 0.f;
     for (int e = threadIdx.x; e < n1 * r3; e += blockDim.x) {
         const int i1 = e / r3, c = e - i1 * r3;
         float s2 = 0.f;
         for (int b = 0; b < r2; ++b) {
-            const float4 x = v[int64_t(i1 >> 2) * 4 * r2 * r3 + int64_t(b + r2 * c) * 4 + (i1 & 3)];
+            const float2 x = v[int64_t(i1 >> 2) * 4 * r2 * r3 + int64_t(b + r2 * c) * 4 + (i1 & 3)];
             s2 += x.x * x.x + x.y * x.y;
         }
         m = fmaxf(m, sqrtf(s2));

@@ -78,7 +78,7 @@ __device__ __forceinline__ MrTile mr_tile(const MrGeom& g, int64_t t) {
 
 __global__ void __launch_bounds__(MR_THREADS, 1)
     fwd_mrhs_kernel(const __grid_constant__ CUtensorMap xmap, const TcDesc* __restrict__ tcd,
-                    const float4* __restrict__ varena, const float2* __restrict__ u2arena,
+                    const float2* __restrict__ varena, const float2* __restrict__ u2arena,
                     const float2* __restrict__ arena, MrGeom g, float2* __restrict__ y, int64_t ldy, int p) {
     using namespace sm100;
     extern __shared__ __align__(1024) unsigned char mr_smem_raw[];
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(MR_THREADS, 1)
                     unsigned char* slot = sSlot + s * g.slot_bytes;
                     const uint32_t r23 = uint32_t(d.r2 * d.r3);
                     const uint32_t ld2 = uint32_t(d.r2 | 1);
-                    const uint32_t bv = uint32_t(TC_TI1) * r23 * 16u;  // the 4-row V group of i1
+                    const uint32_t bv = round16(uint32_t(TC_TI1) * r23 * 8u);  // the 4-row V group of i1
                     const uint32_t b2 = uint32_t(MR_TI2) * ld2 * 8u;
                     const uint32_t b3 = round16(uint32_t(MR_TI3 * d.r3) * 8u);
                     mbar_arrive_expect_tx(&ffull[s], uint32_t(sizeof(TcDesc)) + bv + b2 + b3);
@@ -238,16 +238,16 @@ __global__ void __launch_bounds__(MR_THREADS, 1)
                 const unsigned char* slot = sSlot + fs * g.slot_bytes;
                 const int r2 = reinterpret_cast<const TcDesc*>(slot)->r2;
                 const int r3 = reinterpret_cast<const TcDesc*>(slot)->r3;
-                const float4* V = reinterpret_cast<const float4*>(slot + g.v_off) + (tl.i1 & 3);
+                const float2* V = reinterpret_cast<const float2*>(slot + g.v_off) + (tl.i1 & 3);
                 const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
                 const float2* U3 = reinterpret_cast<const float2*>(slot + g.u3_off);
                 float4* W = sW + wb * MR_TI2 * MR_WLD;
                 // phase A: W[i2, c] = sum_b V[i1, b, c] U2[i2, b]  -> (wr, wi, -wi, wr)
                 if (ca < r3) {
                     uint64_t acc = 0;
-                    const float4* vp = V + 4 * r2 * ca;
+                    const float2* vp = V + 4 * r2 * ca;
                     const float2* up = U2 + i2a * (r2 | 1);
-                    for (int b = 0; b < r2; ++b) cfma2(acc, vp[4 * b], up[b]);
+                    for (int b = 0; b < r2; ++b) cfma2v(acc, vp[4 * b], up[b]);
                     float2 w = f2_unpack(acc);
                     if (!i2ok) w = make_float2(0.f, 0.f);
                     W[i2a * MR_WLD + ca] = make_float4(w.x, w.y, -w.y, w.x);

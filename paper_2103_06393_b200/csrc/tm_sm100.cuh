@@ -203,6 +203,16 @@ __device__ __forceinline__ float2 f2_unpack(uint64_t r) {
     asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
     return v;
 }
+// acc += v * u with v = (vr, vi) as stored: (vr, vi) * ur + (vi, vr) * (-ui, ui);
+// ptxas folds the swap and the partial negation into FFMA2 operand modifiers
+// (-R.F32x2.LO_HI.NP) and ur / ui into scalar broadcasts: two FFMA2.
+__device__ __forceinline__ void cfma2v(uint64_t& acc, const float2& v, const float2& u) {
+    const uint64_t p = f2_pack(v.x, v.y), sw = f2_pack(v.y, v.x);
+    const uint64_t ur = f2_pack(u.x, u.x), nu = f2_pack(-u.y, u.y);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(p), "l"(ur));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(sw), "l"(nu));
+}
+
 __device__ __forceinline__ void cfma2(uint64_t& acc, const float4& v, const float2& u) {
     const uint64_t p = f2_pack(v.x, v.y), q = f2_pack(v.z, v.w);
     const uint64_t ur = f2_pack(u.x, u.x), ui = f2_pack(u.y, u.y);
