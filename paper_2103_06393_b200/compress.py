@@ -1,0 +1,208 @@
+"""GPU compressor: column assembly + truncated HOSVD on the device.
+
+Replaces the reference's producer path compress_matrix (src/compress.cpp:7-35):
+assemble_column (src/scene.cpp:127-150, kernels :84-118) and hosvd
+(src/tensor.cpp:122-174) per column, on one B200, writing the compressed
+store straight into HBM (or a CTC1 file, src/io.cpp:121-210).
+
+* Assembly: the E-/H-field kernels evaluated for a batch of columns over all
+  voxel centres in complex128 (q = 3: the reference's point-collocated
+  piecewise-constant column; q = 12: this build's piecewise-linear stand-in,
+  2x2x2 Gauss moments against {1, x~, y~, z~} — the same definition as the
+  oracle's voxel_field).
+* HOSVD: per tensor and mode g, the Gram matrix A_g A_g^H of the mode-g
+  unfolding (n_g x n_g, cuBLAS zgemm) and its Hermitian eigendecomposition
+  (cuSOLVER, batched); squared singular values are the eigenvalues, the
+  truncation follows the reference's per-mode rule (smallest rank whose
+  discarded energy stays below eps^2/3 |T|^2), the factors are the leading
+  eigenvectors and the core is T x_1 U1^H x_2 U2^H x_3 U3^H.  Singular
+  vectors differ from an SVD's by a phase per column, which changes no
+  product (the factors only enter through U diag G U^H-type contractions).
+  The Gram route squares the condition number; with eps >= 1e-8 the kept
+  spectrum lies far above fp64's resolution of it.
+
+The result is the reference's CompressedCoupling layout: ranks (m, q, 3) and
+the concatenated CTC1 tensor payloads, on the device.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+_SINGULAR = 1e-12  # kSingularRadius of the reference kernels (src/scene.cpp)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def voxel_centers(origin, spacing, dims, device):
+    """Voxel centres, f1-fastest (v = i1 + n1 (i2 + n2 i3)), shape (n_v, 3)."""
+    torch = _torch()
+    ax = [torch.arange(int(dims[a]), device=device, dtype=torch.float64) for a in range(3)]
+    i3, i2, i1 = torch.meshgrid(ax[2], ax[1], ax[0], indexing="ij")
+    c = torch.stack([origin[0] + spacing * (i1 + 0.5), origin[1] + spacing * (i2 + 0.5),
+                     origin[2] + spacing * (i3 + 0.5)], dim=-1)
+    return c.reshape(-1, 3)
+
+
+def _kernel(op, k0, src, obs):
+    """Field of sources src (B, 7) at points obs (n, 3) -> (B, n, 3) complex128:
+    efield_kernel (src/scene.cpp:84-103) or hfield_kernel (:105-118)."""
+    torch = _torch()
+    mid, d, w = src[:, None, 0:3], src[:, None, 3:6], src[:, None, 6:7]
+    rv = obs[None, :, :] - mid
+    R = torch.linalg.vector_norm(rv, dim=-1, keepdim=True)
+    if bool((R < _SINGULAR).any()):
+        raise RuntimeError("field kernel: observation point hits the source")
+    rh = rv / R
+    g = torch.polar(1.0 / (4.0 * math.pi * R), -k0 * R)
+    if op == 0:
+        R2 = R * R
+        a = g * torch.complex(k0 * k0 - 1.0 / R2, -k0 / R)
+        b = g * torch.complex(-(k0 * k0) + 3.0 / R2, 3.0 * k0 / R)
+        pr = (rh * d).sum(-1, keepdim=True)
+        return w * (a * d + b * pr * rh)
+    gc = -g * torch.complex(1.0 / R, torch.full_like(R, k0))
+    cr = torch.linalg.cross(rh.expand_as(rv), d.expand_as(rv), dim=-1)
+    return (w * gc) * cr
+
+
+def assemble_columns(scene, cols, device="cuda"):
+    """assemble_column (src/scene.cpp:127-150) for the columns `cols`:
+    (len(cols), q, n_v) complex128 on the device, component-major rows."""
+    torch = _torch()
+    src = torch.as_tensor(np.asarray(scene.sources)[list(cols)], dtype=torch.float64, device=device)
+    cen = voxel_centers(scene.origin, scene.spacing, scene.dims, device)
+    if scene.q == 3:
+        return _kernel(scene.op, scene.k0, src, cen).permute(0, 2, 1).contiguous()
+    if scene.q != 12:
+        raise ValueError("q must be 3 (PWC) or 12 (PWL stand-in)")
+    off = 0.5 / math.sqrt(3.0)
+    out = torch.zeros((src.shape[0], 12, cen.shape[0]), dtype=torch.complex128, device=device)
+    for gz in (0, 1):
+        for gy in (0, 1):
+            for gx in (0, 1):
+                lx, ly, lz = (off if gx else -off), (off if gy else -off), (off if gz else -off)
+                pt = cen + scene.spacing * torch.tensor([lx, ly, lz], dtype=torch.float64, device=device)
+                f = _kernel(scene.op, scene.k0, src, pt)  # (B, n, 3)
+                phi = (1.0, lx, ly, lz)
+                for c in range(3):
+                    for mu in range(4):
+                        out[:, 4 * c + mu, :] += (0.125 * phi[mu]) * f[:, :, c]
+    return out
+
+
+def _unfold(t, mode):
+    """unfold (src/tensor.cpp:67-87) of a batch t (B, n1, n2, n3) stored
+    f1-fastest, i.e. torch shape (B, n3, n2, n1): mode-g rows."""
+    if mode == 1:
+        return t.permute(0, 3, 2, 1).reshape(t.shape[0], t.shape[3], -1)
+    if mode == 2:
+        return t.permute(0, 2, 3, 1).reshape(t.shape[0], t.shape[2], -1)
+    return t.reshape(t.shape[0], t.shape[1], -1)
+
+
+def hosvd_batch(t, eps):
+    """Truncated HOSVD of a batch of tensors t (B, n3, n2, n1) complex128
+    (f1-fastest): list of (core (r1, r2, r3) f1-fastest as a torch tensor of
+    shape (r3, r2, r1), U1, U2, U3) per tensor — the reference's hosvd
+    (src/tensor.cpp:122-174) with Gram eigendecompositions for the SVDs."""
+    torch = _torch()
+    if not 0.0 < eps < 1.0:
+        raise ValueError("hosvd: eps must lie in (0,1)")
+    B = t.shape[0]
+    fro2 = (t.abs() ** 2).reshape(B, -1).sum(-1)
+    budget = (eps * eps / 3.0) * fro2
+    facs = []
+    for mode in (1, 2, 3):
+        a = _unfold(t, mode)
+        gram = a @ a.conj().transpose(1, 2)
+        lam, vec = torch.linalg.eigh(gram)  # ascending
+        lam = lam.clamp(min=0.0)
+        # smallest rank whose discarded energy (sum of the smallest eigenvalues) <= budget
+        csum = torch.cumsum(lam, dim=-1)  # csum[i] = energy of the i+1 smallest
+        n = lam.shape[-1]
+        keep_small = (csum <= budget[:, None]).sum(-1)  # how many smallest may be discarded
+        ranks = torch.clamp(n - keep_small, min=1)
+        facs.append((vec, ranks))
+    out = []
+    ranks_cpu = [f[1].cpu().numpy() for f in facs]
+    zero = (fro2.sqrt() < 1e-300).cpu().numpy()  # the reference's |t|_F < 1e-300
+    for b in range(B):
+        if zero[b]:
+            dims = (t.shape[3], t.shape[2], t.shape[1])
+            us = []
+            for g in range(3):
+                u = torch.zeros((dims[g], 1), dtype=torch.complex128, device=t.device)
+                u[0, 0] = 1.0
+                us.append(u)
+            out.append((torch.zeros((1, 1, 1), dtype=torch.complex128, device=t.device), *us))
+            continue
+        us = []
+        for g in range(3):
+            vec = facs[g][0][b]
+            r = int(ranks_cpu[g][b])
+            us.append(torch.flip(vec[:, -r:], dims=[1]))  # leading eigenvectors, descending
+        # core[c3, c2, c1] = sum t[i3, i2, i1] conj(U1[i1,c1]) conj(U2[i2,c2]) conj(U3[i3,c3])
+        core = torch.einsum("zyx,xa,yb,zc->cba", t[b], us[0].conj(), us[1].conj(), us[2].conj())
+        out.append((core, us[0], us[1], us[2]))
+    return out
+
+
+def compress_scene(scene, eps, device="cuda", batch=None):
+    """compress_matrix (src/compress.cpp:7-35) on the device.  Returns
+    (ranks (m, q, 3) int32 numpy, payload complex128 torch tensor on the
+    device in the CTC1 tensor layout, concatenated [col][comp])."""
+    torch = _torch()
+    m, q = scene.num_sources, scene.q
+    n1, n2, n3 = (int(d) for d in scene.dims)
+    nv = n1 * n2 * n3
+    if batch is None:
+        batch = max(1, min(m, int((1 << 30) // (q * nv * 16 * 6))))
+    ranks = np.zeros((m, q, 3), np.int32)
+    parts = []
+    for j0 in range(0, m, batch):
+        cols = list(range(j0, min(m, j0 + batch)))
+        f = assemble_columns(scene, cols, device)  # (B, q, nv)
+        t = f.reshape(len(cols) * q, n3, n2, n1)
+        res = hosvd_batch(t, eps)
+        for i, (core, u1, u2, u3) in enumerate(res):
+            j, k = cols[i // q], i % q
+            ranks[j, k] = (u1.shape[1], u2.shape[1], u3.shape[1])
+            # CTC1 tensor payload: core f1-fastest, then U1, U2, U3 column-major
+            parts += [core.reshape(-1), u1.t().reshape(-1), u2.t().reshape(-1), u3.t().reshape(-1)]
+        del f, t, res
+    payload = torch.cat(parts) if parts else torch.zeros(0, dtype=torch.complex128, device=device)
+    return ranks, payload
+
+
+def compress_to_store(scene, eps, dtype="c64", device=0):
+    """compress_scene straight into a DeviceStore (no host round trip)."""
+    from .matvec import DeviceStore
+    ranks, payload = compress_scene(scene, eps, device=f"cuda:{device}")
+    return DeviceStore.from_arrays(scene.dims, scene.q, ranks, payload, dtype, device)
+
+
+def write_ctc1(path, dims, q, ranks, payload, k0=0.0, eps=0.0, op=0):
+    """save_ctc1 (src/io.cpp:198-210): the 45-byte little-endian header
+    {"CTC1", version 1, q, m, n1, n2, n3, k0, eps, kernel id} then per tensor
+    [col][comp] its ranks (u32 x 3) and complex f64 payload."""
+    import struct
+    ranks = np.asarray(ranks, np.int32).reshape(-1, q, 3)
+    m = ranks.shape[0]
+    pay = payload.detach().cpu().numpy() if hasattr(payload, "detach") else np.asarray(payload)
+    pay = np.ascontiguousarray(pay, dtype=np.complex128)
+    with open(path, "wb") as f:
+        f.write(b"CTC1" + struct.pack("<6I", 1, q, m, int(dims[0]), int(dims[1]), int(dims[2])))
+        f.write(struct.pack("<ddB", float(k0), float(eps), int(op)))
+        pos = 0
+        n1, n2, n3 = (int(d) for d in dims)
+        for r in ranks.reshape(-1, 3):
+            r1, r2, r3 = (int(v) for v in r)
+            size = r1 * r2 * r3 + n1 * r1 + n2 * r2 + n3 * r3
+            f.write(struct.pack("<3I", r1, r2, r3))
+            f.write(pay[pos:pos + size].astype("<c16").tobytes())
+            pos += size
