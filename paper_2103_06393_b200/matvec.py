@@ -252,6 +252,12 @@ class DeviceStore:
             x = x.reshape(-1, 1)
         if x.dtype != td:
             x = x.to(td)
+        # torch's lazy conjugate / negative views keep the raw memory
+        # unconjugated: materialise them before handing the pointer over
+        if x.is_conj():
+            x = x.resolve_conj()
+        if x.is_neg():
+            x = x.resolve_neg()
         if x.stride(0) != 1 or (x.shape[1] > 1 and x.stride(1) < x.shape[0]):
             x = x.t().contiguous().t()
         inrows, p = x.shape
