@@ -80,6 +80,7 @@ struct AjGeom {
     int rmax2, rmax3;
     int slot_bytes, u2_off;
     int maxch;       // chunk stride of the chunk-start table
+    int debug;       // diagnostics (TMB_TC_DEBUG & 4): consumers skip the mode-2 product
     int64_t t_begin, t_end;  // tile range of this launch
 };
 
@@ -324,7 +325,8 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                     const float2* V = reinterpret_cast<const float2*>(slot + TC_SLOT_V) + i1l;
                     const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
                     float2 a;
-#define AJ_COL(NU) a = aj_consume_column<NU>(V, U2, r2, r2 | 1, r3, h, lane, qbase + uint32_t(soff), &fempty[fs])
+#define AJ_COL(NU) \
+    a = aj_consume_column<NU>(V, U2, (g.debug & 4) ? 0 : r2, r2 | 1, r3, h, lane, qbase + uint32_t(soff), &fempty[fs])
                     switch ((r3 + AJ_NH - 1) / AJ_NH) {
                         case 1: AJ_COL(1); break;
                         case 2: AJ_COL(2); break;

@@ -726,6 +726,10 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     g.u2_off = TC_SLOT_V + int(round16(uint32_t(TC_TI1 * g.rmax2 * g.rmax3 * 8)));
     g.slot_bytes = (g.u2_off + TC_TI2 * (g.rmax2 | 1) * 8 + 127) / 128 * 128;
     g.maxch = s->maxch;
+    {
+        const char* dbg = std::getenv("TMB_TC_DEBUG");
+        g.debug = dbg ? std::atoi(dbg) : 0;
+    }
     const size_t smem = 1024 + size_t(AJ_NST) * (AJ_A_STAGE + AJ_B_STAGE) + size_t(TC_JR) * g.slot_bytes +
                         size_t(2) * AJ_MAXCOLS * AJ_NPW * sizeof(float2) + (2 * AJ_NST + 2 * TC_JR + 4) * 8 + 16;
     if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: shared-memory plan too large");
