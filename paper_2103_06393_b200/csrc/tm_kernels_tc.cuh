@@ -37,17 +37,17 @@
 // span 2 x 128 voxels along mode 3 (all 512 TMEM columns hold [Yr|Yi] of
 // the two halves), so each produced W element feeds twice the MMA work.
 //
-// Warp roles (640 threads, 1 CTA / SM, persistent over tiles):
+// Warp roles (512 threads, 1 CTA / SM, persistent over tiles):
 //   warp 0      TMA producer of the B planes
 //   warp 1      MMA issuer (one elected thread)
 //   warp 2      factor loader: per column, bulk-copies {TcDesc, V rows,
 //               U2 rows} of the tile into a 3-deep shared-memory ring
 //   warp 3      TMEM allocator
-//   warps 4-15  A producers (mode-2 W, x_j scale, hi/lo split)
-//   warps 16-19 chain fold + epilogue (TMEM -> registers -> y)
-// Pipelines: A/B stage ring (full: 1 TMA arrive+tx + 12 producer-warp
+//   warps 4-11  A producers (mode-2 W, x_j scale, hi/lo split)
+//   warps 12-15 chain fold + epilogue (TMEM -> registers -> y)
+// Pipelines: A/B stage ring (full: 1 TMA arrive+tx + 8 producer-warp
 // arrivals; empty: tcgen05.commit), factor ring (full: bulk-copy tx; empty:
-// 12 producer warps), chain (full: commit after the chain's last K step;
+// 8 producer warps), chain (full: commit after the chain's last K step;
 // free: 4 fold warps).
 #pragma once
 
@@ -77,8 +77,8 @@ __host__ __device__ inline float fp16_scale(float amax) {
 constexpr int TC_TI1 = 4, TC_TI2 = 32, TC_ROWS = 128;
 constexpr int TC_NST_MAX = 5;   // A/B stages (8 K each)
 constexpr int TC_JR = 3;        // factor-ring slots
-constexpr int TC_NPW = 12;      // producer warps: 4 i1 rows x TC_NH c partitions
-constexpr int TC_NH = TC_NPW / TC_TI1;
+constexpr int TC_NPW = 8;       // producer warps: 4 i1 rows x 2 halves of the 32 i2
+constexpr int TC_NH = 4;        // c partition across lanes: c = 4 u + (lane & 3)
 constexpr int TC_PW0 = 4;       // first producer warp
 constexpr int TC_FW0 = TC_PW0 + TC_NPW;   // first fold / epilogue warp
 constexpr int TC_THREADS = (TC_FW0 + 4) * 32;
@@ -177,73 +177,82 @@ __device__ __forceinline__ void ring_ahead(const ARing& r, uint32_t i, uint32_t 
     }
 }
 
-// One column of one tile for the producer thread (row, c partition h): mode 2
-// (W[row, c] = x_j sum_b V[i1, b, c] U2[i2, b] for c = NH u + h) and the
-// 3xTF32 hi/lo split of W into its K slots of the A ring.  NU = ceil(r3/NH).
-// All lanes of a producer warp share i1 (lane = i2), so the V operand of
-// each FFMA2 is a warp-uniform shared-memory broadcast.
+// One column of one tile for the producer thread: two tile rows (i2a, i2a + 8
+// of the warp's i1) and the c values c = 4u + hq (hq = lane & 3).  Mode 2:
+// W[row, c] = x_j sum_b V[i1, b, c] U2[i2, b] (FFMA2, V shared by the two
+// rows, U2 by the NU values of c), then the scaled fp16 hi/lo split of W
+// into its K slots of the A ring.  The four lanes of a row write four
+// consecutive K slots (8 bytes of one 32-byte K-major row), so a warp's
+// 2-byte plane stores hit 16 distinct banks: conflict-free.  NU = ceil(r3/4).
 template <int NU>
 __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, const float2* __restrict__ U2, int r2,
-                                                  int ld2, int r3, int h, float2 xj, uint64_t* fempty_s,
+                                                  int ld2, int r3, int hq, int i2a, float2 xj, uint64_t* fempty_s,
                                                   uint64_t* empty, uint64_t* full, unsigned char* sA,
-                                                  uint32_t rowbase, uint32_t xorv, int lane, uint32_t nst,
-                                                  ARing& ring) {
+                                                  const uint32_t (&rowbase)[2], const uint32_t (&xorv)[2], int lane,
+                                                  uint32_t nst, ARing& ring) {
     using namespace sm100;
-    uint64_t w[NU];
+    uint64_t w[2][NU];
 #pragma unroll
-    for (int u = 0; u < NU; ++u) w[u] = 0;
-    // V[(b + r2 c) * 4 + il]: c = NH u + h  ->  stride 4 NH r2 float2 per u
-    const float2* vp = V + 4 * r2 * h;
-    const float2* up = U2 + lane * ld2;
+    for (int u = 0; u < NU; ++u) w[0][u] = w[1][u] = 0;
+    // V[(b + r2 c) * 4 + il]: c = 4u + hq  ->  stride 16 r2 float2 per u
+    const float2* vp = V + 4 * r2 * hq;
+    const float2* upa = U2 + i2a * ld2;
+    const float2* upb = upa + 8 * ld2;
 #pragma unroll 2
     for (int b = 0; b < r2; ++b) {
-        const float2 ub = up[b];
+        const float2 ua = upa[b], ub = upb[b];
 #pragma unroll
         for (int u = 0; u < NU; ++u)
-            if (u < NU - 2 || TC_NH * u + h < r3) cfma2v(w[u], vp[4 * b + 4 * TC_NH * r2 * u], ub);
+            if (u < NU - 1 || TC_NH * u + hq < r3) {
+                const float2 v = vp[4 * b + 16 * r2 * u];
+                cfma2v(w[0][u], v, ua);
+                cfma2v(w[1][u], v, ub);
+            }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(fempty_s);  // this warp no longer reads the slot
 #pragma unroll
-    for (int u = 0; u < NU; ++u) {
-        const float2 v = cmul(f2_unpack(w[u]), xj);
-        w[u] = f2_pack(v.x, v.y);
-    }
-    // wait for every stage (16 K) this column opens, write, close completed stages
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+            const float2 v = cmul(f2_unpack(w[e][u]), xj);
+            w[e][u] = f2_pack(v.x, v.y);
+        }
+    // wait for every stage (16 K) this column opens (at most two: r3 <= 16)
     const uint32_t kend = ring.kpos + uint32_t(r3);
-    const uint32_t ns = (kend + 15) >> 4;
-    for (uint32_t i = ring.kpos == 0 ? 0u : 1u; i < ns; ++i) {
+    if (ring.kpos == 0) mbar_wait(&empty[ring.st], ring.ph ^ 1u);
+    if (kend > 16) {
         uint32_t s, ph;
-        ring_ahead(ring, i, nst, s, ph);
+        ring_ahead(ring, 1, nst, s, ph);
         mbar_wait(&empty[s], ph ^ 1u);
     }
+    uint32_t s1, ph1;
+    ring_ahead(ring, 1, nst, s1, ph1);
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
-        const int c = TC_NH * u + h;
-        if (u < NU - 2 || c < r3) {
+        const int c = TC_NH * u + hq;
+        if (u < NU - 1 || c < r3) {
             const uint32_t K = ring.kpos + uint32_t(c);
-            uint32_t s, ph;
-            ring_ahead(ring, K >> 4, nst, s, ph);
-            const float2 wv = f2_unpack(w[u]);
-            const __half hr = __float2half_rn(wv.x), hi = __float2half_rn(wv.y);
-            __half* a = reinterpret_cast<__half*>(sA + s * TC_A_STAGE + rowbase + (((K & 15u) * 2u) ^ xorv));
-            a[0] = hr;
-            a[TC_A_PLANE / 2] = __float2half_rn(wv.x - __half2float(hr));
-            a[2 * TC_A_PLANE / 2] = hi;
-            a[3 * TC_A_PLANE / 2] = __float2half_rn(wv.y - __half2float(hi));
+            const uint32_t s = K < 16 ? ring.st : s1;
+            unsigned char* st = sA + s * TC_A_STAGE;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const float2 wv = f2_unpack(w[e][u]);
+                const __half hr = __float2half_rn(wv.x), hi = __float2half_rn(wv.y);
+                __half* a = reinterpret_cast<__half*>(st + rowbase[e] + (((K & 15u) * 2u) ^ xorv[e]));
+                a[0] = hr;
+                a[TC_A_PLANE / 2] = __float2half_rn(wv.x - __half2float(hr));
+                a[2 * TC_A_PLANE / 2] = hi;
+                a[3 * TC_A_PLANE / 2] = __float2half_rn(wv.y - __half2float(hi));
+            }
         }
     }
-    const uint32_t nc = kend >> 4;  // stages completed by this column
-    if (nc) {
+    if (kend >= 16) {  // the current stage is complete (and maybe the next one too, kend == 32 is impossible)
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0)
-            for (uint32_t i = 0; i < nc; ++i) {
-                uint32_t s, ph;
-                ring_ahead(ring, i, nst, s, ph);
-                mbar_arrive(&full[s]);
-            }
-        ring_ahead(ring, nc, nst, ring.st, ring.ph);
+        if (lane == 0) mbar_arrive(&full[ring.st]);
+        ring.st = s1;
+        ring.ph = ph1;
     }
     ring.kpos = kend & 15u;
 }
@@ -410,14 +419,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
         }
     } else if (warp >= TC_PW0 && warp < TC_FW0) {
-        static_assert(TC_NH * 16 >= TC_RMAX, "producer switch covers ceil(TC_RMAX / TC_NH)");
+        static_assert(TC_NH * 4 >= TC_RMAX, "producer switch covers ceil(TC_RMAX / TC_NH)");
         // ------------------------------------------------------ A producers
-        // warp pw: i1 = pw & 3 (warp-uniform), c partition h = pw / 4, lane = i2;
+        // warp pw: i1 = pw / 2 (warp-uniform), rows i2 in [16 (pw & 1), +16);
+        // lane: rows i2a = 16 (pw & 1) + lane / 4 and i2a + 8, c = 4u + (lane & 3);
         // tile row = i2 + 32 i1 (= TMEM lane of the accumulator)
         const int pw = warp - TC_PW0;
-        const int i1l = pw & (TC_TI1 - 1), h = pw / TC_TI1;
-        const int row = lane + 32 * i1l;
-        const uint32_t rowbase = uint32_t(row) * 32u, xorv = (uint32_t(row) & 4u) << 2;
+        const int i1l = pw >> 1, hq = lane & 3;
+        const int i2a = 16 * (pw & 1) + (lane >> 2);
+        uint32_t rowbase[2], xorv[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const uint32_t row = uint32_t(i2a + 8 * e + 32 * i1l);
+            rowbase[e] = row * 32u;
+            xorv[e] = (row & 4u) << 2;
+        }
         ARing ring{0, 0, 0};
         uint32_t fs = 0, fph = 0;
         const float sw = fp16_scale(*wmax);  // W x sw fits fp16 (wmax bounds |W| over the store)
@@ -433,22 +449,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int r3 = reinterpret_cast<const TcDesc*>(slot)->r3;
                 const float2* V = reinterpret_cast<const float2*>(slot + TC_SLOT_V) + i1l;
                 const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
-#define TC_COL(NU)                                                                                              \
-    tc_produce_column<NU>(V, U2, (g.debug & 1) ? 0 : r2, r2 | 1, r3, h, xj, &fempty[fs], empty, full, sA, rowbase, xorv, lane, nst, \
-                          ring)
-                // NU = ceil(r3 / NH) rounded up to even above 4 (fewer
-                // instantiations; the last u is predicated by c < r3)
+#define TC_COL(NU)                                                                                             \
+    tc_produce_column<NU>(V, U2, (g.debug & 1) ? 0 : r2, r2 | 1, r3, hq, i2a, xj, &fempty[fs], empty, full, sA, \
+                          rowbase, xorv, lane, nst, ring)
                 switch ((r3 + TC_NH - 1) / TC_NH) {
                     case 1: TC_COL(1); break;
                     case 2: TC_COL(2); break;
                     case 3: TC_COL(3); break;
-                    case 4: TC_COL(4); break;
-                    case 5: case 6: TC_COL(6); break;
-                    case 7: case 8: TC_COL(8); break;
-                    case 9: case 10: TC_COL(10); break;
-                    case 11: case 12: TC_COL(12); break;
-                    case 13: case 14: TC_COL(14); break;
-                    default: TC_COL(16); break;
+                    default: TC_COL(4); break;
                 }
 #undef TC_COL
                 if (++fs == TC_JR) {
@@ -457,9 +465,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 }
             }
             if (ring.kpos != 0) {  // zero the tail of the last stage and close it
-                if (h == 0)
-                    for (uint32_t kq = ring.kpos; kq < 16; ++kq) {
-                        __half* a = reinterpret_cast<__half*>(sA + ring.st * TC_A_STAGE + rowbase + ((kq * 2u) ^ xorv));
+                unsigned char* st = sA + ring.st * TC_A_STAGE;
+                for (uint32_t kq = ring.kpos + uint32_t(hq); kq < 16; kq += 4)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        __half* a = reinterpret_cast<__half*>(st + rowbase[e] + ((kq * 2u) ^ xorv[e]));
 #pragma unroll
                         for (int pl = 0; pl < 4; ++pl) a[pl * TC_A_PLANE / 2] = __float2half_rn(0.f);
                     }
