@@ -93,7 +93,9 @@ constexpr int TC_FPLANES = 4;                // forward B planes per stage: [U3r
 
 // Per-tensor descriptor of the tensor-core forward (component-major like
 // TDesc).  off_v: float2 offset of the tensor's mode-1 product
-// V = U1 x_1 G in the V arena, laid out [i1/4][b + r2 c][i1 % 4]; off_u2:
+// V = U1 x_1 G in the V arena, laid out [i1/4][c + r3 b][i1 % 4] (c innermost:
+// the four consecutive c of one producer warp's lanes are bank-conflict
+// free for every r2); off_u2:
 // float2 offset of the tensor's U2 copy in the U2 arena, n2 rounded up to
 // TI2 rows (zero rows past n2) with an odd row stride r2 | 1 (conflict-free
 // 32-lane row loads); pad0: the (j, c) slot of the column inside its
@@ -194,8 +196,8 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
     uint64_t w[2][NU];
 #pragma unroll
     for (int u = 0; u < NU; ++u) w[0][u] = w[1][u] = 0;
-    // V[(b + r2 c) * 4 + il]: c = 4u + hq  ->  stride 16 r2 float2 per u
-    const float2* vp = V + 4 * r2 * hq;
+    // V[(c + r3 b) * 4 + il]: c = 4u + hq  ->  stride 16 float2 per u, 4 r3 per b
+    const float2* vp = V + 4 * hq;
     const float2* upa = U2 + i2a * ld2;
     const float2* upb = upa + 8 * ld2;
 #pragma unroll 2
@@ -204,7 +206,7 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
 #pragma unroll
         for (int u = 0; u < NU; ++u)
             if (u < NU - 1 || TC_NH * u + hq < r3) {
-                const float2 v = vp[4 * b + 16 * r2 * u];
+                const float2 v = vp[4 * r3 * b + 16 * u];
                 cfma2v(w[0][u], v, ua);
                 cfma2v(w[1][u], v, ub);
             }
@@ -572,7 +574,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 // V_t[i1][b][c] = sum_a U1t[i1][a] G[a + r1 (b + r2 c)] for every tensor t
 // (the reference's mode-1 product, src/tensor.cpp:106-108, done once per
 // store instead of once per tile), accumulated in fp64 from the c64 factors
-// and stored [i1/4][b + r2 c][i1 % 4] as float2; rows i1 >= n1 of the last
+// and stored [i1/4][c + r3 b][i1 % 4] as float2; rows i1 >= n1 of the last
 // group of four are zero.
 __global__ void build_v_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena,
                                const TcDesc* __restrict__ tcd, int n1, float2* __restrict__ varena) {
@@ -594,7 +596,8 @@ __global__ void build_v_kernel(const TDesc* __restrict__ td, const float2* __res
             }
         }
         const float fr = float(vr), fi = float(vi);
-        out[int64_t(i1 >> 2) * 4 * r23 + int64_t(bc) * 4 + (i1 & 3)] = make_float2(fr, fi);
+        const int b = bc % d.r2, c = bc / d.r2;  // bc = b + r2 c (core order)
+        out[int64_t(i1 >> 2) * 4 * r23 + int64_t(c + d.r3 * b) * 4 + (i1 & 3)] = make_float2(fr, fi);
     }
 }
 
@@ -638,7 +641,7 @@ __global__ void vbound_kernel(const TDesc* __restrict__ td, const TcDesc* __rest
         const int i1 = e / r3, c = e - i1 * r3;
         float s2 = 0.f;
         for (int b = 0; b < r2; ++b) {
-            const float2 x = v[int64_t(i1 >> 2) * 4 * r2 * r3 + int64_t(b + r2 * c) * 4 + (i1 & 3)];
+            const float2 x = v[int64_t(i1 >> 2) * 4 * r2 * r3 + int64_t(c + r3 * b) * 4 + (i1 & 3)];
             s2 += x.x * x.x + x.y * x.y;
         }
         m = fmaxf(m, sqrtf(s2));

@@ -245,9 +245,9 @@ __global__ void __launch_bounds__(MR_THREADS, 1)
                 // phase A: W[i2, c] = sum_b V[i1, b, c] U2[i2, b]  -> (wr, wi, -wi, wr)
                 if (ca < r3) {
                     uint64_t acc = 0;
-                    const float2* vp = V + 4 * r2 * ca;
+                    const float2* vp = V + 4 * ca;  // V[(c + r3 b) * 4 + il]
                     const float2* up = U2 + i2a * (r2 | 1);
-                    for (int b = 0; b < r2; ++b) cfma2v(acc, vp[4 * b], up[b]);
+                    for (int b = 0; b < r2; ++b) cfma2v(acc, vp[4 * r3 * b], up[b]);
                     float2 w = f2_unpack(acc);
                     if (!i2ok) w = make_float2(0.f, 0.f);
                     W[i2a * MR_WLD + ca] = make_float4(w.x, w.y, -w.y, w.x);
