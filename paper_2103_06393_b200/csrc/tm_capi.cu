@@ -202,7 +202,7 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
     }
     const int64_t n3 = s->dims[2];
     const size_t pbytes = size_t(TC_BPLANES) * s->q * n3 * s->kpad * sizeof(__half);
-    // V arena: per tensor ceil(n1/4)*4 x r2 x r3 float4
+    // V arena: per tensor ceil(n1/4)*4 x r2 x r3 float2, [i1/4][c + r3 b][i1%4]
     const int64_t n1p = (s->dims[0] + 3) / 4 * 4;
     std::vector<TcDesc> tcd(static_cast<size_t>(ntens));
     int64_t voff = 0, u2off = 0;
