@@ -196,30 +196,32 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
     uint64_t w[2][NU];
 #pragma unroll
     for (int u = 0; u < NU; ++u) w[0][u] = w[1][u] = 0;
-    // V[(c + r3 b) * 4 + il]: c = 4u + hq  ->  stride 16 float2 per u, 4 r3 per b
+    // V[(c + r3 b) * 4 + il]: c = 4u + hq  ->  stride 16 float2 per u, 4 r3 per b.
+    // Every lane computes all NU values: for c >= r3 the loads read
+    // neighbouring V entries (or the slot's U2 rows past the V block — at
+    // most 12 float2 beyond it, inside the slot) and the products are never
+    // stored, so the inner loop carries no predicates.
     const float2* vp = V + 4 * hq;
     const float2* upa = U2 + i2a * ld2;
     const float2* upb = upa + 8 * ld2;
+    const int vstep = 4 * r3;
 #pragma unroll 2
     for (int b = 0; b < r2; ++b) {
         const float2 ua = upa[b], ub = upb[b];
 #pragma unroll
-        for (int u = 0; u < NU; ++u)
-            if (u < NU - 1 || TC_NH * u + hq < r3) {
-                const float2 v = vp[4 * r3 * b + 16 * u];
-                cfma2v(w[0][u], v, ua);
-                cfma2v(w[1][u], v, ub);
-            }
+        for (int u = 0; u < NU; ++u) {
+            const float2 v = vp[16 * u];
+            cfma2v(w[0][u], v, ua);
+            cfma2v(w[1][u], v, ub);
+        }
+        vp += vstep;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(fempty_s);  // this warp no longer reads the slot
 #pragma unroll
     for (int e = 0; e < 2; ++e)
 #pragma unroll
-        for (int u = 0; u < NU; ++u) {
-            const float2 v = cmul(f2_unpack(w[e][u]), xj);
-            w[e][u] = f2_pack(v.x, v.y);
-        }
+        for (int u = 0; u < NU; ++u) w[e][u] = cmul2(w[e][u], xj);
     // wait for every stage (16 K) this column opens (at most two: r3 <= 16)
     const uint32_t kend = ring.kpos + uint32_t(r3);
     if (ring.kpos == 0) mbar_wait(&empty[ring.st], ring.ph ^ 1u);
@@ -239,13 +241,13 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
             unsigned char* st = sA + s * TC_A_STAGE;
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const float2 wv = f2_unpack(w[e][u]);
-                const __half hr = __float2half_rn(wv.x), hi = __float2half_rn(wv.y);
-                __half* a = reinterpret_cast<__half*>(st + rowbase[e] + (((K & 15u) * 2u) ^ xorv[e]));
-                a[0] = hr;
-                a[TC_A_PLANE / 2] = __float2half_rn(wv.x - __half2float(hr));
-                a[2 * TC_A_PLANE / 2] = hi;
-                a[3 * TC_A_PLANE / 2] = __float2half_rn(wv.y - __half2float(hi));
+                uint32_t hi, lo;
+                f16_split2(w[e][u], hi, lo);
+                unsigned short* a = reinterpret_cast<unsigned short*>(st + rowbase[e] + (((K & 15u) * 2u) ^ xorv[e]));
+                a[0] = static_cast<unsigned short>(hi);                      // Re hi
+                a[TC_A_PLANE / 2] = static_cast<unsigned short>(lo);         // Re lo
+                a[2 * TC_A_PLANE / 2] = static_cast<unsigned short>(hi >> 16);  // Im hi
+                a[3 * TC_A_PLANE / 2] = static_cast<unsigned short>(lo >> 16);  // Im lo
             }
         }
     }

@@ -213,6 +213,29 @@ __device__ __forceinline__ void cfma2v(uint64_t& acc, const float2& v, const flo
     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(sw), "l"(nu));
 }
 
+// Scaled complex W -> its 2-term fp16 split, packed: hi = (fp16(re), fp16(im)),
+// lo = (fp16(re - hi.re), fp16(im - hi.im)); the low halves hold Re.
+__device__ __forceinline__ void f16_split2(uint64_t w, uint32_t& hi, uint32_t& lo) {
+    const float2 v = f2_unpack(w);
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(v.y), "f"(v.x));
+    float hr, hm;
+    asm("{.reg .f16 a, b;\n\tmov.b32 {a, b}, %2;\n\tcvt.f32.f16 %0, a;\n\tcvt.f32.f16 %1, b;\n\t}"
+        : "=f"(hr), "=f"(hm) : "r"(hi));
+    uint64_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(w), "l"(f2_pack(hr, hm)));
+    const float2 r = f2_unpack(d);
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(r.y), "f"(r.x));
+}
+
+// w * x for packed complex w and x (two FFMA2-class ops).
+__device__ __forceinline__ uint64_t cmul2(uint64_t w, const float2& x) {
+    const float2 v = f2_unpack(w);
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(v.x, v.x)), "l"(f2_pack(x.x, x.y)));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(r) : "l"(f2_pack(v.y, v.y)), "l"(f2_pack(-x.y, x.x)));
+    return r;
+}
+
 __device__ __forceinline__ void cfma2(uint64_t& acc, const float4& v, const float2& u) {
     const uint64_t p = f2_pack(v.x, v.y), q = f2_pack(v.z, v.w);
     const uint64_t ur = f2_pack(u.x, u.x), ui = f2_pack(u.y, u.y);
