@@ -180,12 +180,12 @@ __device__ __forceinline__ void ring_ahead(const ARing& r, uint32_t i, uint32_t 
 }
 
 // One column of one tile for the producer thread: two tile rows (i2a, i2a + 8
-// of the warp's i1) and the c values c = 4u + hq (hq = lane & 3).  Mode 2:
+// of the warp's i1) and the c values c = 4u + hq.  Mode 2:
 // W[row, c] = x_j sum_b V[i1, b, c] U2[i2, b] (FFMA2, V shared by the two
 // rows, U2 by the NU values of c), then the scaled fp16 hi/lo split of W
-// into its K slots of the A ring.  The four lanes of a row write four
-// consecutive K slots (8 bytes of one 32-byte K-major row), so a warp's
-// 2-byte plane stores hit 16 distinct banks: conflict-free.  NU = ceil(r3/4).
+// into its K slots of the A ring.  A warp's 2-byte plane stores cover 8 rows
+// x 4 consecutive K slots (8 bytes of each 32-byte K-major row, swizzled):
+// conflict-free, one wavefront.  NU = ceil(r3/4).
 template <int NU>
 __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, const float2* __restrict__ U2, int r2,
                                                   int ld2, int r3, int hq, int i2a, float2 xj, uint64_t* fempty_s,
@@ -426,11 +426,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         static_assert(TC_NH * 4 >= TC_RMAX, "producer switch covers ceil(TC_RMAX / TC_NH)");
         // ------------------------------------------------------ A producers
         // warp pw: i1 = pw / 2 (warp-uniform), rows i2 in [16 (pw & 1), +16);
-        // lane: rows i2a = 16 (pw & 1) + lane / 4 and i2a + 8, c = 4u + (lane & 3);
+        // lane: row lane rl in [0, 8) (rows i2a = 16 (pw & 1) + rl and i2a + 8)
+        // and c = 4u + hq.  Each quad of lanes is 2 row lanes x 2 hq, so a
+        // quad's V and U2 loads touch 2 addresses each: one shared-memory
+        // wavefront per LDS.64 for both (lanes of a quad on 4 distinct
+        // addresses cost two; tools/smem_probe.cu).
         // tile row = i2 + 32 i1 (= TMEM lane of the accumulator)
         const int pw = warp - TC_PW0;
-        const int i1l = pw >> 1, hq = lane & 3;
-        const int i2a = 16 * (pw & 1) + (lane >> 2);
+        const int rl = 2 * ((lane >> 2) & 3) + (lane & 1);
+        const int i1l = pw >> 1, hq = 2 * (lane >> 4) + ((lane >> 1) & 1);
+        const int i2a = 16 * (pw & 1) + rl;
         uint32_t rowbase[2], xorv[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--cols", type=int, default=400)
     ap.add_argument("--settings", default="0,1,2,3")
+    ap.add_argument("--reps", type=int, default=11)
     args = ap.parse_args()
     import torch
     from paper_2103_06393_b200 import DeviceStore
@@ -38,15 +39,19 @@ def main():
         for name, fn in (("forward", lambda: s.forward(x)), ("adjoint", lambda: s.adjoint(phi))):
             fn()
             torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(3):
+            ts = []
+            for _ in range(args.reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
                 fn()
-            e1.record()
-            e1.synchronize()
-            ms = e0.elapsed_time(e1) / 3
-            print(json.dumps({"debug": st, "op": name, "cols": m, "ms": round(ms, 3),
-                              "tflops": round(flops / (ms * 1e-3) / 1e12, 1)}), flush=True)
+                e1.record()
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ts.sort()
+            ms = ts[len(ts) // 2]
+            print(json.dumps({"debug": st, "op": name, "cols": m, "ms": round(ms, 3), "ms_min": round(ts[0], 3),
+                              "tflops": round(flops / (ms * 1e-3) / 1e12, 1),
+                              "tflops_best": round(flops / (ts[0] * 1e-3) / 1e12, 1)}), flush=True)
     os.environ.pop("TMB_TC_DEBUG")
 
 
