@@ -12,6 +12,9 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtuckmat_b200.so")
+# A/B experiments: load an alternative in-tree build (e.g. libtuckmat_b200_a.so)
+if os.environ.get("TMB_LIB_VARIANT"):
+    LIB_PATH = os.path.join(HERE, "libtuckmat_b200_%s.so" % os.environ["TMB_LIB_VARIANT"])
 
 TM_OK, TM_CONTRACT_VIOLATION, TM_CAPACITY_ERROR, TM_PARSE_ERROR, TM_CUDA_ERROR, TM_ERROR = 0, 1, 2, 3, 6, 9
 TM_C64, TM_C128 = 0, 1

@@ -114,14 +114,19 @@ __device__ __forceinline__ float2 aj_consume_column(const float2* __restrict__ V
     uint64_t w[NU];
 #pragma unroll
     for (int u = 0; u < NU; ++u) w[u] = 0;
-    const float2* vp = V + 4 * h;  // V[(c + r3 b) * 4 + il], c = NH u + h
+    // V[(c + r3 b) * 4 + il], c = NH u + h.  The loop computes all NU values
+    // unpredicated: for c = r3 (odd r3, h = 1) the load reads the next V entry
+    // (at most 4 float2 past the V block, inside the slot) and the product is
+    // dropped below.
+    const float2* vp = V + 4 * h;
     const float2* up = U2 + lane * ld2;
+    const int vstep = 4 * r3;
 #pragma unroll 2
     for (int b = 0; b < r2; ++b) {
         const float2 ub = up[b];
 #pragma unroll
-        for (int u = 0; u < NU; ++u)
-            if (u < NU - 1 || AJ_NH * u + h < r3) cfma2v(w[u], vp[4 * r3 * b + 4 * AJ_NH * u], ub);
+        for (int u = 0; u < NU; ++u) cfma2v(w[u], vp[4 * AJ_NH * u], ub);
+        vp += vstep;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(fempty_s);
