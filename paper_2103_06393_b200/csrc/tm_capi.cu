@@ -564,12 +564,24 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     g.nh3 = g.n3 > TC_NMAX ? 2 : 1;
     g.nt3 = (g.n3 + g.nmma * g.nh3 - 1) / (g.nmma * g.nh3);
     g.p = int(p);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const int nsm = num_sms(dev);
+    // CTA-pair kernel (cta_group::2, M = 256 over two i1 blocks, each CTA
+    // holding half of the 256-voxel i3 span of B): halves the B-operand
+    // shared-memory reads per MMA and the B stage.  Needs full 256-voxel i3
+    // tiles and an even number of i1 blocks.
+    {
+        const char* e = std::getenv("TMB_DISABLE_PAIR");
+        g.pair = (!(e && *e && *e != '0') && g.nmma == TC_NMAX && g.nh3 == 2 && g.nt1 % 2 == 0 && nsm >= 2) ? 1 : 0;
+    }
+    if (g.pair) g.nt1 /= 2;
     g.ntiles = int64_t(p) * g.q * g.nt3 * g.nt2 * g.nt1;
     g.rmax2 = s->rmax[1];
     g.rmax3 = s->rmax[2];
     g.u2_off = TC_SLOT_V + int(round16(uint32_t(TC_TI1 * g.rmax2 * g.rmax3 * 8)));
     g.slot_bytes = (g.u2_off + TC_TI2 * (g.rmax2 | 1) * 8 + 127) / 128 * 128;
-    g.b_stage = g.nh3 * TC_FPLANES * g.nmma * 32;
+    g.b_stage = (g.pair ? 1 : g.nh3) * TC_FPLANES * g.nmma * 32;
     g.chain = tc_chain();
     {
         const char* dbg = std::getenv("TMB_TC_DEBUG");
@@ -583,10 +595,12 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     while (g.nst > 2 && smem_for(g.nst) > kSmemMax) --g.nst;
     const size_t smem = smem_for(g.nst);
     if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core forward: shared-memory plan too large");
-    CK(cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    const unsigned grid = unsigned(std::min<int64_t>(g.ntiles, num_sms(dev)));
+    CK(cudaFuncSetAttribute(fwd_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CK(cudaFuncSetAttribute(fwd_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    // grid: CTAs; a wave covers `wave` tiles (pair tiles in pair mode)
+    const unsigned grid = g.pair ? unsigned(std::min<int64_t>(2 * g.ntiles, nsm & ~1))
+                                 : unsigned(std::min<int64_t>(g.ntiles, nsm));
+    const int64_t wave = g.pair ? grid / 2 : grid;
     tm_store* ms = const_cast<tm_store*>(s);
     float2* rsum = static_cast<float2*>(ms->rsum.get(size_t(grid) * g.nmma * g.nh3 * TC_ROWS * sizeof(float2)));
     float* wmax = static_cast<float*>(ms->scal.get(2 * sizeof(float))) + 1;
@@ -603,12 +617,32 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     const int64_t tpb = g.ntiles / (int64_t(p) * g.q);  // tiles per (rhs, component) block
     const int64_t nv = s->nv();
     int64_t bdone = 0;
-    for (int64_t t0 = 0; t0 < g.ntiles; t0 += grid) {
+    for (int64_t t0 = 0; t0 < g.ntiles; t0 += wave) {
         g.t_begin = t0;
-        g.t_end = std::min<int64_t>(g.ntiles, t0 + grid);
-        fwd_tc_kernel<<<grid, TC_THREADS, smem, st>>>(s->bmap, s->d_tcd, s->d_varena, s->d_u2arena, s->d_kc, g, x,
-                                                       ldx, y, ldy, rsum, wmax);
-        launched(cudaSuccess, "fwd_tc_kernel");
+        g.t_end = std::min<int64_t>(g.ntiles, t0 + wave);
+        if (g.pair) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(TC_THREADS);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            launched(cudaLaunchKernelEx(&cfg, fwd_tc_kernel<true>, s->bmap, static_cast<const TcDesc*>(s->d_tcd),
+                                        static_cast<const float2*>(s->d_varena),
+                                        static_cast<const float2*>(s->d_u2arena), static_cast<const int*>(s->d_kc),
+                                        g, x, ldx, y, ldy, rsum, static_cast<const float*>(wmax)),
+                     "fwd_tc_kernel<pair>");
+        } else {
+            fwd_tc_kernel<false><<<grid, TC_THREADS, smem, st>>>(s->bmap, s->d_tcd, s->d_varena, s->d_u2arena,
+                                                                  s->d_kc, g, x, ldx, y, ldy, rsum, wmax);
+            launched(cudaSuccess, "fwd_tc_kernel");
+        }
         const int64_t bnow = g.t_end / tpb;
         if (hp && bnow > bdone) {
             cudaEvent_t ev;

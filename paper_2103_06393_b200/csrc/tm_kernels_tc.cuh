@@ -123,6 +123,7 @@ struct TcGeom {
     int nst;                    // A/B stages in the ring (3..TC_NST_MAX)
     int chain;                  // K stages per TMEM accumulation chain
     int debug;                  // diagnostics (TMB_TC_DEBUG): 1 = no mode-2 work, 2 = no B loads
+    int pair;                   // 1: CTA-pair kernel (cta_group::2, M = 256), nt1 counts pairs of i1 blocks
     int64_t t_begin, t_end;     // tile range of this launch (one wave: see run_forward_tc)
 };
 
@@ -145,7 +146,7 @@ struct TcTile {
 // of their i1 block (read by all n2/TI2 x n3/NMMA tiles of that block —
 // re-reading them from HBM per tile would cost ~200 GB per config-4
 // forward) and stream the same B planes of component k through L2.
-__device__ __forceinline__ TcTile tc_tile(const TcGeom& g, int64_t t) {
+__device__ __forceinline__ TcTile tc_tile(const TcGeom& g, int64_t t, uint32_t rank = 0) {
     const int64_t per_c = int64_t(g.q) * g.nt3 * g.nt2 * g.nt1;
     TcTile r;
     r.c = int(t / per_c);
@@ -157,7 +158,7 @@ __device__ __forceinline__ TcTile tc_tile(const TcGeom& g, int64_t t) {
     rem -= int64_t(t1) * g.nt2 * g.nt3;
     const int t2 = int(rem / g.nt3);
     const int t3 = int(rem - int64_t(t2) * g.nt3);
-    r.i1_0 = t1 * TC_TI1;
+    r.i1_0 = (t1 * (1 + g.pair) + int(rank)) * TC_TI1;  // a pair tile spans 2 i1 blocks, one per CTA
     r.i2_0 = t2 * TC_TI2;
     r.i3_0 = t3 * g.nmma * g.nh3;
     return r;
@@ -186,7 +187,7 @@ __device__ __forceinline__ void ring_ahead(const ARing& r, uint32_t i, uint32_t 
 // into its K slots of the A ring.  A warp's 2-byte plane stores cover 8 rows
 // x 4 consecutive K slots (8 bytes of each 32-byte K-major row, swizzled):
 // conflict-free, one wavefront.  NU = ceil(r3/4).
-template <int NU>
+template <int NU, bool PAIR>
 __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, const float2* __restrict__ U2, int r2,
                                                   int ld2, int r3, int hq, int i2a, float2 xj, uint64_t* fempty_s,
                                                   uint64_t* empty, uint64_t* full, unsigned char* sA,
@@ -224,11 +225,11 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
         for (int u = 0; u < NU; ++u) w[e][u] = cmul2(w[e][u], xj);
     // wait for every stage (16 K) this column opens (at most two: r3 <= 16)
     const uint32_t kend = ring.kpos + uint32_t(r3);
-    if (ring.kpos == 0) mbar_wait(&empty[ring.st], ring.ph ^ 1u);
+    if (ring.kpos == 0) mbar_wait<PAIR>(&empty[ring.st], ring.ph ^ 1u);
     if (kend > 16) {
         uint32_t s, ph;
         ring_ahead(ring, 1, nst, s, ph);
-        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_wait<PAIR>(&empty[s], ph ^ 1u);
     }
     uint32_t s1, ph1;
     ring_ahead(ring, 1, nst, s1, ph1);
@@ -254,13 +255,19 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
     if (kend >= 16) {  // the current stage is complete (and maybe the next one too, kend == 32 is impossible)
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&full[ring.st]);
+        if (lane == 0) {
+            if (PAIR)
+                mbar_arrive_cluster(mapa_shared(smem_u32(&full[ring.st]), 0));  // the even CTA issues the MMAs
+            else
+                mbar_arrive(&full[ring.st]);
+        }
         ring.st = s1;
         ring.ph = ph1;
     }
     ring.kpos = kend & 15u;
 }
 
+template <bool PAIR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap bmap, const TcDesc* __restrict__ tcd,
                   const float2* __restrict__ varena, const float2* __restrict__ u2arena, const int* __restrict__ kc,
@@ -285,9 +292,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfree + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // CTA pairs (PAIR): both CTAs walk the same pair tiles; rank 0 issues the
+    // cta_group::2 MMAs, so its full / cfree barriers count the peer's
+    // producer and fold warps too (remote arrivals), and its commits
+    // multicast to the empty / cfull barriers of both CTAs.
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    const int64_t tstart = g.t_begin + (PAIR ? (blockIdx.x >> 1) : blockIdx.x);
+    const int64_t tstep = PAIR ? (gridDim.x >> 1) : gridDim.x;
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < nst; ++s) {
-            mbar_init(&full[s], 1 + TC_NPW);
+            mbar_init(&full[s], 1 + TC_NPW * (PAIR ? 2 : 1));
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < TC_JR; ++s) {
@@ -295,13 +309,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mbar_init(&fempty[s], TC_NPW);
         }
         mbar_init(cfull, 1);
-        mbar_init(cfree, 4);
+        mbar_init(cfree, 4 * (PAIR ? 2 : 1));
         fence_mbar_init();
     }
-    if (warp == 3) tmem_alloc(tmem_slot, 512);
+    if (warp == 3) {
+        if (PAIR)
+            tmem_alloc_pair(tmem_slot, 512);
+        else
+            tmem_alloc(tmem_slot, 512);
+    }
     if (warp == 0 && lane == 0) tma_prefetch_desc(&bmap);
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync();  // barriers of both CTAs initialised before any remote arrival
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -310,12 +330,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
             const int plane_bytes = g.nmma * 32;
-            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
-                const TcTile tl = tc_tile(g, t);
+            for (int64_t t = tstart; t < g.t_end; t += tstep) {
+                const TcTile tl = tc_tile(g, t, rank);
                 const int nks = (kc[tl.k] + 15) >> 4;
                 for (int kk = 0; kk < nks; ++kk) {
-                    mbar_wait(&empty[s], ph ^ 1);
-                    if (g.debug & 2) {
+                    mbar_wait<PAIR>(&empty[s], ph ^ 1);
+                    if (PAIR) {
+                        // each CTA loads its half of the i3 span (B rows [rank nmma, +nmma) of the
+                        // M = 256 MMA); the bytes of both halves complete on rank 0's barrier
+                        if (rank == 0) {
+                            if (g.debug & 2)
+                                mbar_arrive(&full[s]);
+                            else
+                                mbar_arrive_expect_tx(&full[s], 2u * uint32_t(g.b_stage));
+                        }
+                        if (!(g.debug & 2)) {
+                            unsigned char* dst = sB + s * g.b_stage;
+                            const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+#pragma unroll
+                            for (int pl = 0; pl < TC_FPLANES; ++pl)
+                                tma_load_3d_pair(dst + pl * plane_bytes, &bmap, fb, kk * 16,
+                                                 tl.i3_0 + int(rank) * g.nmma, (1 + pl + (pl >> 1)) * g.q + tl.k);
+                        }
+                    } else if (g.debug & 2) {
                         mbar_arrive(&full[s]);
                     } else {
                         mbar_arrive_expect_tx(&full[s], uint32_t(g.b_stage));
@@ -337,26 +374,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer
-        if (elect_one()) {
+        if ((!PAIR || rank == 0) && elect_one()) {
             // complex product over the tile's span = nh3 * NMMA voxels along i3
             // (TMEM: Yr at [0, span), Yi at [span, 2 span)), four real products
             // of full width N = span, each as hi.hi + hi.lo + lo.hi:
             //   Yr += Ar.U3r,  Yr -= Ai.U3i (negate-A bit),  Yi += Ar.U3i,  Yi += Ai.U3r
             const int span = g.nmma * g.nh3;
-            const uint32_t id_p = umma_idesc_f16(TC_ROWS, span, false, false);
-            const uint32_t id_n = umma_idesc_f16(TC_ROWS, span, true, false);
-            const int plane_b = span * 32;  // one smem B plane (all i3 of the tile)
+            const uint32_t id_p = umma_idesc_f16(TC_ROWS * (PAIR ? 2 : 1), span, false, false);
+            const uint32_t id_n = umma_idesc_f16(TC_ROWS * (PAIR ? 2 : 1), span, true, false);
+            const int plane_b = (PAIR ? span / 2 : span) * 32;  // one smem B plane (this CTA's i3 rows)
             uint32_t s = 0, ph = 0, gch = 0;
-            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
-                const TcTile tl = tc_tile(g, t);
+            for (int64_t t = tstart; t < g.t_end; t += tstep) {
+                const TcTile tl = tc_tile(g, t, rank);
                 const int nks = (kc[tl.k] + 15) >> 4;
                 int cpos = 0;  // stage position inside the current chain
                 for (int kk = 0; kk < nks; ++kk) {
                     if (cpos == 0) {
-                        mbar_wait(cfree, (gch & 1) ^ 1);  // the previous chain has been folded
+                        mbar_wait<PAIR>(cfree, (gch & 1) ^ 1);  // the previous chain has been folded
                         tc_fence_after();
                     }
-                    mbar_wait(&full[s], ph);
+                    mbar_wait<PAIR>(&full[s], ph);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + s * TC_A_STAGE);
                     const uint32_t b0 = smem_u32(sB + s * g.b_stage);
@@ -370,38 +407,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     const uint64_t Brl = umma_smem_desc(b0 + 2 * plane_b, 256, 6);
                     const uint64_t Bil = umma_smem_desc(b0 + 3 * plane_b, 256, 6);
                     const uint32_t yr = tmem, yi = tmem + uint32_t(span);
-                    mma_f16(yr, A[0], Brh, id_p, acc);
-                    mma_f16(yr, A[0], Brl, id_p, 1);
-                    mma_f16(yr, A[1], Brh, id_p, 1);
-                    mma_f16(yr, A[2], Bih, id_n, 1);
-                    mma_f16(yr, A[2], Bil, id_n, 1);
-                    mma_f16(yr, A[3], Bih, id_n, 1);
-                    mma_f16(yi, A[0], Bih, id_p, acc);
-                    mma_f16(yi, A[0], Bil, id_p, 1);
-                    mma_f16(yi, A[1], Bih, id_p, 1);
-                    mma_f16(yi, A[2], Brh, id_p, 1);
-                    mma_f16(yi, A[2], Brl, id_p, 1);
-                    mma_f16(yi, A[3], Brh, id_p, 1);
-                    mma_commit(&empty[s]);
+#define MMA(...) (PAIR ? mma_f16_pair(__VA_ARGS__) : mma_f16(__VA_ARGS__))
+#define COMMIT(b) (PAIR ? mma_commit_pair(b) : mma_commit(b))
+                    MMA(yr, A[0], Brh, id_p, acc);
+                    MMA(yr, A[0], Brl, id_p, 1);
+                    MMA(yr, A[1], Brh, id_p, 1);
+                    MMA(yr, A[2], Bih, id_n, 1);
+                    MMA(yr, A[2], Bil, id_n, 1);
+                    MMA(yr, A[3], Bih, id_n, 1);
+                    MMA(yi, A[0], Bih, id_p, acc);
+                    MMA(yi, A[0], Bil, id_p, 1);
+                    MMA(yi, A[1], Bih, id_p, 1);
+                    MMA(yi, A[2], Brh, id_p, 1);
+                    MMA(yi, A[2], Brl, id_p, 1);
+                    MMA(yi, A[3], Brh, id_p, 1);
+                    COMMIT(&empty[s]);
                     if (++s == nst) {
                         s = 0;
                         ph ^= 1;
                     }
                     if (++cpos == g.chain || kk == nks - 1) {
-                        mma_commit(cfull);
+                        COMMIT(cfull);
                         cpos = 0;
                         ++gch;
                     }
                 }
             }
         }
+#undef MMA
+#undef COMMIT
         __syncwarp();
     } else if (warp == 2) {
         // ---------------------------------------------------- factor loader
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
-            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
-                const TcTile tl = tc_tile(g, t);
+            for (int64_t t = tstart; t < g.t_end; t += tstep) {
+                const TcTile tl = tc_tile(g, t, rank);
                 const TcDesc* tdk = tcd + int64_t(tl.k) * g.ncols;
                 for (int64_t j = 0; j < g.ncols; ++j) {
                     mbar_wait(&fempty[s], ph ^ 1);
@@ -446,8 +487,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         ARing ring{0, 0, 0};
         uint32_t fs = 0, fph = 0;
         const float sw = fp16_scale(*wmax);  // W x sw fits fp16 (wmax bounds |W| over the store)
-        for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
-            const TcTile tl = tc_tile(g, t);
+        for (int64_t t = tstart; t < g.t_end; t += tstep) {
+            const TcTile tl = tc_tile(g, t, rank);
             const float2* xc = x + ldx * tl.c;
             for (int64_t j = 0; j < g.ncols; ++j) {
                 const float2 x0 = xc[j];
@@ -459,7 +500,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const float2* V = reinterpret_cast<const float2*>(slot + TC_SLOT_V) + i1l;
                 const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
 #define TC_COL(NU)                                                                                             \
-    tc_produce_column<NU>(V, U2, (g.debug & 1) ? 0 : r2, r2 | 1, r3, hq, i2a, xj, &fempty[fs], empty, full, sA, \
+    tc_produce_column<NU, PAIR>(V, U2, (g.debug & 1) ? 0 : r2, r2 | 1, r3, hq, i2a, xj, &fempty[fs], empty, full, sA, \
                           rowbase, xorv, lane, nst, ring)
                 switch ((r3 + TC_NH - 1) / TC_NH) {
                     case 1: TC_COL(1); break;
@@ -484,7 +525,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     }
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&full[ring.st]);
+                if (lane == 0) {
+                    if (PAIR)
+                        mbar_arrive_cluster(mapa_shared(smem_u32(&full[ring.st]), 0));
+                    else
+                        mbar_arrive(&full[ring.st]);
+                }
                 ring_ahead(ring, 1, nst, ring.st, ring.ph);
                 ring.kpos = 0;
             }
@@ -509,8 +555,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int64_t nv3 = int64_t(g.n1) * g.n2 * g.n3;
         const float inv = 1.f / (fp16_scale(*wmax) * TC_U3_SCALE);  // exact power of two
         uint32_t gch = 0;
-        for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
-            const TcTile tl = tc_tile(g, t);
+        for (int64_t t = tstart; t < g.t_end; t += tstep) {
+            const TcTile tl = tc_tile(g, t, rank);
             const int nks = (kc[tl.k] + 15) >> 4;
             const int nch = (nks + g.chain - 1) / g.chain;
             const int ei1 = tl.i1_0 + quarter, ei2 = tl.i2_0 + lane;
@@ -518,7 +564,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             float2* yp = y + ldy * tl.c + int64_t(tl.k) * nv3 + ei1 + int64_t(g.n1) * ei2;
             const int64_t pl = int64_t(g.n1) * g.n2;
             for (int ch = 0; ch < nch; ++ch, ++gch) {
-                mbar_wait(cfull, gch & 1);
+                mbar_wait<PAIR>(cfull, gch & 1);
                 tc_fence_after();
                 const bool last = ch == nch - 1;
                 for (int hh = 0; hh < g.nh3; ++hh)
@@ -568,13 +614,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(cfree);
+                if (lane == 0) {
+                    if (PAIR)
+                        mbar_arrive_cluster(mapa_shared(smem_u32(cfree), 0));
+                    else
+                        mbar_arrive(cfree);
+                }
             }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 3) tmem_dealloc(tmem, 512);
+    if (PAIR) cluster_sync();  // the peer no longer arrives on this CTA's barriers / uses the pair's TMEM
+    if (warp == 3) {
+        if (PAIR)
+            tmem_dealloc_pair(tmem, 512);
+        else
+            tmem_dealloc(tmem, 512);
+    }
 }
 
 // ------------------------------------------------- store-side V arena (K6'')
