@@ -206,9 +206,11 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
     const float2* upa = U2 + i2a * ld2;
     const float2* upb = upa + 8 * ld2;
     const int vstep = 4 * r3;
-#pragma unroll 2
+    const float2* pa = upa;
+    const float2* pb = upb;
+#pragma unroll 4
     for (int b = 0; b < r2; ++b) {
-        const float2 ua = upa[b], ub = upb[b];
+        const float2 ua = *pa++, ub = *pb++;
 #pragma unroll
         for (int u = 0; u < NU; ++u) {
             const float2 v = vp[16 * u];
