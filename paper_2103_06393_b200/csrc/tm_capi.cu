@@ -601,6 +601,11 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     const unsigned grid = g.pair ? unsigned(std::min<int64_t>(2 * g.ntiles, nsm & ~1))
                                  : unsigned(std::min<int64_t>(g.ntiles, nsm));
     const int64_t wave = g.pair ? grid / 2 : grid;
+    g.prof = nullptr;
+    if (g.debug & 8) {
+        CK(cudaMalloc(&g.prof, 16 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(g.prof, 0, 16 * sizeof(unsigned long long), st));
+    }
     tm_store* ms = const_cast<tm_store*>(s);
     float2* rsum = static_cast<float2*>(ms->rsum.get(size_t(grid) * g.nmma * g.nh3 * TC_ROWS * sizeof(float2)));
     float* wmax = static_cast<float*>(ms->scal.get(2 * sizeof(float))) + 1;
@@ -657,6 +662,18 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
             }
             bdone = bnow;
         }
+    }
+    if (g.prof) {  // wait profile: mean cycles per recording thread, per role
+        unsigned long long h[16];
+        CK(cudaMemcpyAsync(h, g.prof, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        CK(cudaFree(g.prof));
+        static const char* names[5] = {"tma", "mma", "loader", "producers", "fold"};
+        static const char* w1[5] = {"empty", "cfree", "fempty", "ffull", "cfull"};
+        static const char* w2[5] = {"-", "full", "-", "empty", "-"};
+        for (int r = 0; r < 5; ++r)
+            std::fprintf(stderr, "[tc-prof] %-9s total %14llu  wait %-6s %14llu  wait %-5s %14llu\n", names[r], h[3 * r],
+                         w1[r], h[3 * r + 1], w2[r], h[3 * r + 2]);
     }
 }
 

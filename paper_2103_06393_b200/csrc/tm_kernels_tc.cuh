@@ -77,7 +77,8 @@ __host__ __device__ inline float fp16_scale(float amax) {
 constexpr int TC_TI1 = 4, TC_TI2 = 32, TC_ROWS = 128;
 constexpr int TC_NST_MAX = 5;   // A/B stages (8 K each)
 constexpr int TC_JR = 3;        // factor-ring slots
-constexpr int TC_NPW = 8;       // producer warps: 4 i1 rows x 2 halves of the 32 i2
+constexpr int TC_NR = 2;        // tile rows per producer lane (rows i2a + 8 e, e < TC_NR)
+constexpr int TC_NPW = 16 / TC_NR;  // producer warps: 4 i1 rows x (4 / TC_NR) blocks of 8 TC_NR i2
 constexpr int TC_NH = 4;        // c partition across lanes: c = 4 u + (lane & 3)
 constexpr int TC_PW0 = 4;       // first producer warp
 constexpr int TC_FW0 = TC_PW0 + TC_NPW;   // first fold / epilogue warp
@@ -124,6 +125,7 @@ struct TcGeom {
     int chain;                  // K stages per TMEM accumulation chain
     int debug;                  // diagnostics (TMB_TC_DEBUG): 1 = no mode-2 work, 2 = no B loads
     int pair;                   // 1: CTA-pair kernel (cta_group::2, M = 256), nt1 counts pairs of i1 blocks
+    unsigned long long* prof;   // diagnostics (TMB_TC_DEBUG & 8): per-role barrier-wait cycles, else null
     int64_t t_begin, t_end;     // tile range of this launch (one wave: see run_forward_tc)
 };
 
@@ -136,6 +138,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 __host__ __device__ inline uint32_t round16(uint32_t b) { return (b + 15u) & ~15u; }
+
+// Barrier wait, timed into `acc` (cycles) when the wait profile is on.
+#define TC_TWAIT(on, acc, call)                  \
+    do {                                         \
+        if (on) {                                \
+            const long long t0_ = clock64();     \
+            call;                                \
+            (acc) += uint64_t(clock64() - t0_);  \
+        } else {                                 \
+            call;                                \
+        }                                        \
+    } while (0)
 
 struct TcTile {
     int c, k, i1_0, i2_0, i3_0;
@@ -191,47 +205,50 @@ template <int NU, bool PAIR>
 __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, const float2* __restrict__ U2, int r2,
                                                   int ld2, int r3, int hq, int i2a, float2 xj, uint64_t* fempty_s,
                                                   uint64_t* empty, uint64_t* full, unsigned char* sA,
-                                                  const uint32_t (&rowbase)[2], const uint32_t (&xorv)[2], int lane,
-                                                  uint32_t nst, ARing& ring) {
+                                                  const uint32_t (&rowbase)[TC_NR], const uint32_t (&xorv)[TC_NR],
+                                                  int lane, uint32_t nst, ARing& ring, bool prof, uint64_t& t_empty) {
     using namespace sm100;
-    uint64_t w[2][NU];
+    uint64_t w[TC_NR][NU];
 #pragma unroll
-    for (int u = 0; u < NU; ++u) w[0][u] = w[1][u] = 0;
+    for (int e = 0; e < TC_NR; ++e)
+#pragma unroll
+        for (int u = 0; u < NU; ++u) w[e][u] = 0;
     // V[(c + r3 b) * 4 + il]: c = 4u + hq  ->  stride 16 float2 per u, 4 r3 per b.
     // Every lane computes all NU values: for c >= r3 the loads read
     // neighbouring V entries (or the slot's U2 rows past the V block — at
     // most 12 float2 beyond it, inside the slot) and the products are never
     // stored, so the inner loop carries no predicates.
     const float2* vp = V + 4 * hq;
-    const float2* upa = U2 + i2a * ld2;
-    const float2* upb = upa + 8 * ld2;
     const int vstep = 4 * r3;
-    const float2* pa = upa;
-    const float2* pb = upb;
+    const float2* pu[TC_NR];
+#pragma unroll
+    for (int e = 0; e < TC_NR; ++e) pu[e] = U2 + (i2a + 8 * e) * ld2;
 #pragma unroll 4
     for (int b = 0; b < r2; ++b) {
-        const float2 ua = *pa++, ub = *pb++;
+        float2 ue[TC_NR];
+#pragma unroll
+        for (int e = 0; e < TC_NR; ++e) ue[e] = *pu[e]++;
 #pragma unroll
         for (int u = 0; u < NU; ++u) {
             const float2 v = vp[16 * u];
-            cfma2v(w[0][u], v, ua);
-            cfma2v(w[1][u], v, ub);
+#pragma unroll
+            for (int e = 0; e < TC_NR; ++e) cfma2v(w[e][u], v, ue[e]);
         }
         vp += vstep;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(fempty_s);  // this warp no longer reads the slot
 #pragma unroll
-    for (int e = 0; e < 2; ++e)
+    for (int e = 0; e < TC_NR; ++e)
 #pragma unroll
         for (int u = 0; u < NU; ++u) w[e][u] = cmul2(w[e][u], xj);
     // wait for every stage (16 K) this column opens (at most two: r3 <= 16)
     const uint32_t kend = ring.kpos + uint32_t(r3);
-    if (ring.kpos == 0) mbar_wait<PAIR>(&empty[ring.st], ring.ph ^ 1u);
+    if (ring.kpos == 0) TC_TWAIT(prof, t_empty, (mbar_wait<PAIR>(&empty[ring.st], ring.ph ^ 1u)));
     if (kend > 16) {
         uint32_t s, ph;
         ring_ahead(ring, 1, nst, s, ph);
-        mbar_wait<PAIR>(&empty[s], ph ^ 1u);
+        TC_TWAIT(prof, t_empty, (mbar_wait<PAIR>(&empty[s], ph ^ 1u)));
     }
     uint32_t s1, ph1;
     ring_ahead(ring, 1, nst, s1, ph1);
@@ -243,7 +260,7 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
             const uint32_t s = K < 16 ? ring.st : s1;
             unsigned char* st = sA + s * TC_A_STAGE;
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
+            for (int e = 0; e < TC_NR; ++e) {
                 uint32_t hi, lo;
                 f16_split2(w[e][u], hi, lo);
                 unsigned short* a = reinterpret_cast<unsigned short*>(st + rowbase[e] + (((K & 15u) * 2u) ^ xorv[e]));
@@ -326,17 +343,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (PAIR) cluster_sync();  // barriers of both CTAs initialised before any remote arrival
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // wait profile (g.prof): per role, cycles spent in barrier waits
+    uint64_t t_w = 0, t_w2 = 0;
+    bool rec = false;
+    const long long t_role = clock64();
 
     if (warp == 0) {
         // ------------------------------------------------ B-plane TMA producer
         if (elect_one()) {
+            rec = true;
             uint32_t s = 0, ph = 0;
             const int plane_bytes = g.nmma * 32;
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
                 const TcTile tl = tc_tile(g, t, rank);
                 const int nks = (kc[tl.k] + 15) >> 4;
                 for (int kk = 0; kk < nks; ++kk) {
-                    mbar_wait<PAIR>(&empty[s], ph ^ 1);
+                    TC_TWAIT(g.prof, t_w, (mbar_wait<PAIR>(&empty[s], ph ^ 1)));
                     if (PAIR) {
                         // each CTA loads its half of the i3 span (B rows [rank nmma, +nmma) of the
                         // M = 256 MMA); the bytes of both halves complete on rank 0's barrier
@@ -377,6 +399,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer
         if ((!PAIR || rank == 0) && elect_one()) {
+            rec = true;
             // complex product over the tile's span = nh3 * NMMA voxels along i3
             // (TMEM: Yr at [0, span), Yi at [span, 2 span)), four real products
             // of full width N = span, each as hi.hi + hi.lo + lo.hi:
@@ -392,10 +415,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 int cpos = 0;  // stage position inside the current chain
                 for (int kk = 0; kk < nks; ++kk) {
                     if (cpos == 0) {
-                        mbar_wait<PAIR>(cfree, (gch & 1) ^ 1);  // the previous chain has been folded
+                        TC_TWAIT(g.prof, t_w, (mbar_wait<PAIR>(cfree, (gch & 1) ^ 1)));  // previous chain folded
                         tc_fence_after();
                     }
-                    mbar_wait<PAIR>(&full[s], ph);
+                    TC_TWAIT(g.prof, t_w2, (mbar_wait<PAIR>(&full[s], ph)));
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + s * TC_A_STAGE);
                     const uint32_t b0 = smem_u32(sB + s * g.b_stage);
@@ -442,12 +465,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     } else if (warp == 2) {
         // ---------------------------------------------------- factor loader
         if (elect_one()) {
+            rec = true;
             uint32_t s = 0, ph = 0;
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
                 const TcTile tl = tc_tile(g, t, rank);
                 const TcDesc* tdk = tcd + int64_t(tl.k) * g.ncols;
                 for (int64_t j = 0; j < g.ncols; ++j) {
-                    mbar_wait(&fempty[s], ph ^ 1);
+                    TC_TWAIT(g.prof, t_w, (mbar_wait(&fempty[s], ph ^ 1)));
                     const TcDesc d = tdk[j];
                     unsigned char* slot = sSlot + s * g.slot_bytes;
                     const uint32_t r23 = uint32_t(d.r2 * d.r3);
@@ -468,20 +492,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     } else if (warp >= TC_PW0 && warp < TC_FW0) {
         static_assert(TC_NH * 4 >= TC_RMAX, "producer switch covers ceil(TC_RMAX / TC_NH)");
         // ------------------------------------------------------ A producers
-        // warp pw: i1 = pw / 2 (warp-uniform), rows i2 in [16 (pw & 1), +16);
-        // lane: row lane rl in [0, 8) (rows i2a = 16 (pw & 1) + rl and i2a + 8)
-        // and c = 4u + hq.  Each quad of lanes is 2 row lanes x 2 hq, so a
+        // warp pw: i1 = pw / (4 / NR) (warp-uniform), rows i2 in a block of 8 NR;
+        // lane: row lane rl in [0, 8) (rows i2a = block base + rl, + 8 e for
+        // e < NR) and c = 4u + hq.  Each quad of lanes is 2 row lanes x 2 hq, so a
         // quad's V and U2 loads touch 2 addresses each: one shared-memory
         // wavefront per LDS.64 for both (lanes of a quad on 4 distinct
         // addresses cost two; tools/smem_probe.cu).
         // tile row = i2 + 32 i1 (= TMEM lane of the accumulator)
+        rec = lane == 0;
         const int pw = warp - TC_PW0;
         const int rl = 2 * ((lane >> 2) & 3) + (lane & 1);
-        const int i1l = pw >> 1, hq = 2 * (lane >> 4) + ((lane >> 1) & 1);
-        const int i2a = 16 * (pw & 1) + rl;
-        uint32_t rowbase[2], xorv[2];
+        constexpr int wpi = 4 / TC_NR;  // producer warps per i1 row of the tile
+        const int i1l = pw / wpi, hq = 2 * (lane >> 4) + ((lane >> 1) & 1);
+        const int i2a = 8 * TC_NR * (pw % wpi) + rl;
+        uint32_t rowbase[TC_NR], xorv[TC_NR];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
+        for (int e = 0; e < TC_NR; ++e) {
             const uint32_t row = uint32_t(i2a + 8 * e + 32 * i1l);
             rowbase[e] = row * 32u;
             xorv[e] = (row & 4u) << 2;
@@ -492,10 +518,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int64_t t = tstart; t < g.t_end; t += tstep) {
             const TcTile tl = tc_tile(g, t, rank);
             const float2* xc = x + ldx * tl.c;
+            // x_j is prefetched one column ahead: its global-load latency
+            // hides behind a whole column of mode-2 work
+            float2 xn = xc[0];
             for (int64_t j = 0; j < g.ncols; ++j) {
-                const float2 x0 = xc[j];
+                const float2 x0 = xn;
+                if (j + 1 < g.ncols) xn = xc[j + 1];
                 const float2 xj = make_float2(x0.x * sw, x0.y * sw);
-                mbar_wait(&ffull[fs], fph);
+                TC_TWAIT(g.prof, t_w, (mbar_wait(&ffull[fs], fph)));
                 const unsigned char* slot = sSlot + fs * g.slot_bytes;
                 const int r2 = reinterpret_cast<const TcDesc*>(slot)->r2;
                 const int r3 = reinterpret_cast<const TcDesc*>(slot)->r3;
@@ -503,7 +533,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
 #define TC_COL(NU)                                                                                             \
     tc_produce_column<NU, PAIR>(V, U2, (g.debug & 1) ? 0 : r2, r2 | 1, r3, hq, i2a, xj, &fempty[fs], empty, full, sA, \
-                          rowbase, xorv, lane, nst, ring)
+                          rowbase, xorv, lane, nst, ring, g.prof != nullptr, t_w2)
                 switch ((r3 + TC_NH - 1) / TC_NH) {
                     case 1: TC_COL(1); break;
                     case 2: TC_COL(2); break;
@@ -520,7 +550,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 unsigned char* st = sA + ring.st * TC_A_STAGE;
                 for (uint32_t kq = ring.kpos + uint32_t(hq); kq < 16; kq += 4)
 #pragma unroll
-                    for (int e = 0; e < 2; ++e) {
+                    for (int e = 0; e < TC_NR; ++e) {
                         __half* a = reinterpret_cast<__half*>(st + rowbase[e] + ((kq * 2u) ^ xorv[e]));
 #pragma unroll
                         for (int pl = 0; pl < 4; ++pl) a[pl * TC_A_PLANE / 2] = __float2half_rn(0.f);
@@ -548,6 +578,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // element is only ever touched by this thread, in program order, so
         // the sum is deterministic), and the last chain reads the running sum
         // back and writes y.
+        rec = lane == 0;
         const int quarter = warp & 3;             // TMEM lane quarter = i1 of the tile
         const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
         const uint32_t tC = tmem + lane_addr;
@@ -566,7 +597,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             float2* yp = y + ldy * tl.c + int64_t(tl.k) * nv3 + ei1 + int64_t(g.n1) * ei2;
             const int64_t pl = int64_t(g.n1) * g.n2;
             for (int ch = 0; ch < nch; ++ch, ++gch) {
-                mbar_wait<PAIR>(cfull, gch & 1);
+                TC_TWAIT(g.prof, t_w, (mbar_wait<PAIR>(cfull, gch & 1)));
                 tc_fence_after();
                 const bool last = ch == nch - 1;
                 for (int hh = 0; hh < g.nh3; ++hh)
@@ -624,6 +655,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 }
             }
         }
+    }
+    if (g.prof && rec) {
+        const int role = warp < 3 ? warp : (warp < TC_FW0 ? 3 : 4);
+        atomicAdd(g.prof + 3 * role, static_cast<unsigned long long>(clock64() - t_role));
+        atomicAdd(g.prof + 3 * role + 1, static_cast<unsigned long long>(t_w));
+        atomicAdd(g.prof + 3 * role + 2, static_cast<unsigned long long>(t_w2));
     }
     tc_fence_before();
     __syncthreads();

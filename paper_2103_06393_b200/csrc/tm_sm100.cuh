@@ -65,9 +65,30 @@ template <bool CLUSTER = false>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     if (mbar_try<CLUSTER>(a, parity)) return;
+    uint32_t n = 0;
+    uint64_t t0 = 0;
+    while (!mbar_try<CLUSTER>(a, parity)) {
+        if ((++n & 0x3FFu) == 0) {  // the clock is read only every 1024 unsuccessful polls
+            const uint64_t t = globaltimer_ns();
+            if (t0 == 0)
+                t0 = t;
+            else if (t - t0 > 20000000000ull)
+                __trap();
+        }
+    }
+}
+// Same, for waits off the critical path (ring producers far ahead, fold
+// warps between chains): back off `ns` nanoseconds between polls so the
+// waiting warp does not take issue slots from the compute warps.
+template <bool CLUSTER = false>
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    const uint32_t a = smem_u32(bar);
+    if (mbar_try<CLUSTER>(a, parity)) return;
     const uint64_t t0 = globaltimer_ns();
-    while (!mbar_try<CLUSTER>(a, parity))
+    while (!mbar_try<CLUSTER>(a, parity)) {
+        __nanosleep(ns);
         if (globaltimer_ns() - t0 > 20000000000ull) __trap();
+    }
 }
 
 // ------------------------------------------------ clusters (CTA pairs) --
