@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const TcTile tl = tc_tile(g, t, rank);
                 const int nks = (kc[tl.k] + 15) >> 4;
                 for (int kk = 0; kk < nks; ++kk) {
-                    TC_TWAIT(g.prof, t_w, (mbar_wait<PAIR>(&empty[s], ph ^ 1)));
+                    TC_TWAIT(g.prof, t_w, (mbar_wait_backoff<PAIR>(&empty[s], ph ^ 1, 128)));
                     if (PAIR) {
                         // each CTA loads its half of the i3 span (B rows [rank nmma, +nmma) of the
                         // M = 256 MMA); the bytes of both halves complete on rank 0's barrier
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const TcTile tl = tc_tile(g, t, rank);
                 const TcDesc* tdk = tcd + int64_t(tl.k) * g.ncols;
                 for (int64_t j = 0; j < g.ncols; ++j) {
-                    TC_TWAIT(g.prof, t_w, (mbar_wait(&fempty[s], ph ^ 1)));
+                    TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(&fempty[s], ph ^ 1, 128)));
                     const TcDesc d = tdk[j];
                     unsigned char* slot = sSlot + s * g.slot_bytes;
                     const uint32_t r23 = uint32_t(d.r2 * d.r3);
@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             float2* yp = y + ldy * tl.c + int64_t(tl.k) * nv3 + ei1 + int64_t(g.n1) * ei2;
             const int64_t pl = int64_t(g.n1) * g.n2;
             for (int ch = 0; ch < nch; ++ch, ++gch) {
-                TC_TWAIT(g.prof, t_w, (mbar_wait<PAIR>(cfull, gch & 1)));
+                TC_TWAIT(g.prof, t_w, (mbar_wait_backoff<PAIR>(cfull, gch & 1, 256)));
                 tc_fence_after();
                 const bool last = ch == nch - 1;
                 for (int hh = 0; hh < g.nh3; ++hh)
