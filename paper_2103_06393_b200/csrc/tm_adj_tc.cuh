@@ -57,7 +57,8 @@ __host__ __device__ inline float aj_phi_scale(float amax) {
     return ldexpf(1.f, 14 - e);
 }
 
-constexpr int AJ_NST = 4;        // A/B stages (8 i3 each)
+constexpr int AJ_NST = 4;        // A/B stages (16 i3 each)
+constexpr int AJ_NST2 = 5;       // stages of the CTA-pair kernel (half-size B stage)
 constexpr int AJ_CH = 128;       // (j, c) slots per chunk
 constexpr int AJ_APLANES = 4;    // Phi planes: re hi, re lo, im hi, im lo
 constexpr int AJ_A_PLANE = TC_ROWS * 32;
@@ -81,6 +82,7 @@ struct AjGeom {
     int slot_bytes, u2_off;
     int maxch;       // chunk stride of the chunk-start table
     int debug;       // diagnostics (TMB_TC_DEBUG & 4): consumers skip the mode-2 product
+    int pair;        // 1: CTA-pair kernel (cta_group::2, M = 256 over two row tiles); tiles count pairs
     int64_t t_begin, t_end;  // tile range of this launch
 };
 
@@ -89,13 +91,14 @@ struct AjTile {
     int64_t rt;  // row tile inside the component
 };
 
-__device__ __forceinline__ AjTile aj_tile(const AjGeom& g, int64_t t) {
+__device__ __forceinline__ AjTile aj_tile(const AjGeom& g, int64_t t, uint32_t rank = 0) {
     AjTile r;
-    const int64_t per_c = int64_t(g.q) * g.nrt;
+    const int64_t tpk = g.nrt >> g.pair;  // (pair) tiles per component
+    const int64_t per_c = int64_t(g.q) * tpk;
     r.c = int(t / per_c);
     int64_t rem = t - int64_t(r.c) * per_c;
-    r.k = int(rem / g.nrt);
-    r.rt = rem - int64_t(r.k) * g.nrt;
+    r.k = int(rem / tpk);
+    r.rt = ((rem - int64_t(r.k) * tpk) << g.pair) + rank;  // a pair tile = row tiles 2 pt, 2 pt + 1
     // i2 block fastest: the resident CTAs share the V rows of one i1 block
     const int t1 = int(r.rt / g.nt2), t2 = int(r.rt - int64_t(t1) * g.nt2);
     r.i1_0 = t1 * TC_TI1;
@@ -155,6 +158,7 @@ __device__ __forceinline__ float2 aj_consume_column(const float2* __restrict__ V
     return make_float2(ar, ai);
 }
 
+template <bool PAIR>
 __global__ void __launch_bounds__(AJ_THREADS, 1)
     adj_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                   const TcDesc* __restrict__ tcd, const float2* __restrict__ varena,
@@ -163,22 +167,30 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
     using namespace sm100;
     extern __shared__ __align__(1024) unsigned char aj_smem_raw[];
     unsigned char* sm = aj_smem_raw + ((1024u - (smem_u32(aj_smem_raw) & 1023u)) & 1023u);
+    // PAIR: the M = 256 MMA takes B rows [0, 128) of each N = 256 window from
+    // the even CTA and [128, 256) from the odd one: the even CTA holds planes
+    // (-U3i, U3r), the odd one (U3r, U3i), hi and lo — 4 planes per stage.
+    constexpr int NST = PAIR ? AJ_NST2 : AJ_NST;
+    constexpr int BSTAGE = PAIR ? 4 * AJ_B_PLANE : AJ_B_STAGE;
     unsigned char* sA = sm;
-    unsigned char* sB = sA + AJ_NST * AJ_A_STAGE;
-    unsigned char* sSlot = sB + AJ_NST * AJ_B_STAGE;
+    unsigned char* sB = sA + NST * AJ_A_STAGE;
+    unsigned char* sSlot = sB + NST * BSTAGE;
     float2* red = reinterpret_cast<float2*>(sSlot + TC_JR * g.slot_bytes);  // [2][AJ_MAXCOLS][8]
     uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * AJ_MAXCOLS * AJ_NPW);
     uint64_t* full = bars;                // [NST]
-    uint64_t* empty = full + AJ_NST;      // [NST]
-    uint64_t* ffull = empty + AJ_NST;     // [JR]
+    uint64_t* empty = full + NST;         // [NST]
+    uint64_t* ffull = empty + NST;        // [JR]
     uint64_t* fempty = ffull + TC_JR;     // [JR]
     uint64_t* qfull = fempty + TC_JR;     // [2]
     uint64_t* qfree = qfull + 2;          // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qfree + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    const int64_t tstart = g.t_begin + (PAIR ? (blockIdx.x >> 1) : blockIdx.x);
+    const int64_t tstep = PAIR ? (gridDim.x >> 1) : gridDim.x;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < AJ_NST; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -188,17 +200,23 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&qfull[s], 1);
-            mbar_init(&qfree[s], AJ_NPW);
+            mbar_init(&qfree[s], AJ_NPW * (PAIR ? 2 : 1));  // PAIR: the peer's consumers too
         }
         fence_mbar_init();
     }
-    if (warp == 3) tmem_alloc(tmem_slot, 512);
+    if (warp == 3) {
+        if (PAIR)
+            tmem_alloc_pair(tmem_slot, 512);
+        else
+            tmem_alloc(tmem_slot, 512);
+    }
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&amap);
         tma_prefetch_desc(&bmap);
     }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -206,24 +224,40 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         // ------------------------------------------------------- TMA producer
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
-            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
-                const AjTile tl = aj_tile(g, t);
+            for (int64_t t = tstart; t < g.t_end; t += tstep) {
+                const AjTile tl = aj_tile(g, t, rank);
                 const int nc = nch[tl.k];
                 const int arow = int(tl.rt * TC_ROWS);
                 for (int n = 0; n < nc; ++n) {
                     for (int kk = 0; kk < g.nks; ++kk) {
-                        mbar_wait(&empty[s], ph ^ 1);
-                        mbar_arrive_expect_tx(&full[s], uint32_t(AJ_A_STAGE + AJ_B_STAGE));
+                        mbar_wait_backoff<PAIR>(&empty[s], ph ^ 1, 64);
                         unsigned char* da = sA + s * AJ_A_STAGE;
-                        unsigned char* db = sB + s * AJ_B_STAGE;
+                        unsigned char* db = sB + s * BSTAGE;
+                        if (PAIR) {
+                            // both CTAs' bytes complete on the even CTA's barrier
+                            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2u * uint32_t(AJ_A_STAGE + BSTAGE));
+                            const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
 #pragma unroll
-                        for (int pl = 0; pl < AJ_APLANES; ++pl)
-                            tma_load_3d(da + pl * AJ_A_PLANE, &amap, &full[s], kk * 16, arow,
-                                        (pl * g.p + tl.c) * g.q + tl.k);
+                            for (int pl = 0; pl < AJ_APLANES; ++pl)
+                                tma_load_3d_pair(da + pl * AJ_A_PLANE, &amap, fb, kk * 16, arow,
+                                                 (pl * g.p + tl.c) * g.q + tl.k);
+                            // smem B slots (W1 hi, W2 hi, W1 lo, W2 lo) <- HBM planes rank + {0, 1} (+3 for lo)
 #pragma unroll
-                        for (int pl = 0; pl < TC_BPLANES; ++pl)
-                            tma_load_3d(db + pl * AJ_B_PLANE, &bmap, &full[s], kk * 16, n * AJ_CH, pl * g.q + tl.k);
-                        if (++s == AJ_NST) {
+                            for (int sl = 0; sl < 4; ++sl)
+                                tma_load_3d_pair(db + sl * AJ_B_PLANE, &bmap, fb, kk * 16, n * AJ_CH,
+                                                 (int(rank) + (sl & 1) + 3 * (sl >> 1)) * g.q + tl.k);
+                        } else {
+                            mbar_arrive_expect_tx(&full[s], uint32_t(AJ_A_STAGE + AJ_B_STAGE));
+#pragma unroll
+                            for (int pl = 0; pl < AJ_APLANES; ++pl)
+                                tma_load_3d(da + pl * AJ_A_PLANE, &amap, &full[s], kk * 16, arow,
+                                            (pl * g.p + tl.c) * g.q + tl.k);
+#pragma unroll
+                            for (int pl = 0; pl < TC_BPLANES; ++pl)
+                                tma_load_3d(db + pl * AJ_B_PLANE, &bmap, &full[s], kk * 16, n * AJ_CH,
+                                            pl * g.q + tl.k);
+                        }
+                        if (++s == NST) {
                             s = 0;
                             ph ^= 1;
                         }
@@ -233,45 +267,50 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer
-        if (elect_one()) {
-            const uint32_t idesc = umma_idesc_f16(TC_ROWS, 2 * AJ_CH, false, false);
+        if ((!PAIR || rank == 0) && elect_one()) {
+            const uint32_t idesc = umma_idesc_f16(TC_ROWS * (PAIR ? 2 : 1), 2 * AJ_CH, false, false);
             uint32_t s = 0, ph = 0, nq = 0;
-            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
-                const AjTile tl = aj_tile(g, t);
+            for (int64_t t = tstart; t < g.t_end; t += tstep) {
+                const AjTile tl = aj_tile(g, t, rank);
                 const int nc = nch[tl.k];
                 for (int n = 0; n < nc; ++n, ++nq) {
                     const uint32_t qb = nq & 1, qph = (nq >> 1) & 1;
-                    mbar_wait(&qfree[qb], qph ^ 1);  // consumers are done with this buffer
+                    mbar_wait<PAIR>(&qfree[qb], qph ^ 1);  // consumers are done with this buffer
                     tc_fence_after();
                     const uint32_t qd = tmem + qb * 256u;
                     for (int kk = 0; kk < g.nks; ++kk) {
-                        mbar_wait(&full[s], ph);
+                        mbar_wait<PAIR>(&full[s], ph);
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + s * AJ_A_STAGE);
-                        const uint32_t b0 = smem_u32(sB + s * AJ_B_STAGE);
+                        const uint32_t b0 = smem_u32(sB + s * BSTAGE);
                         uint64_t A[4];
 #pragma unroll
                         for (int pl = 0; pl < 4; ++pl) A[pl] = umma_smem_desc(a0 + pl * AJ_A_PLANE, 256, 6);
                         // B windows: [-U3i|U3r] at plane 0 / 3 (hi / lo), [U3r|U3i] at plane 1 / 4
+                        // (PAIR: smem slots 0 / 2 and 1 / 3 of each CTA, half a window each)
                         const uint64_t B2h = umma_smem_desc(b0 + 0 * AJ_B_PLANE, 256, 6);
                         const uint64_t B1h = umma_smem_desc(b0 + 1 * AJ_B_PLANE, 256, 6);
-                        const uint64_t B2l = umma_smem_desc(b0 + 3 * AJ_B_PLANE, 256, 6);
-                        const uint64_t B1l = umma_smem_desc(b0 + 4 * AJ_B_PLANE, 256, 6);
+                        const uint64_t B2l = umma_smem_desc(b0 + (PAIR ? 2 : 3) * AJ_B_PLANE, 256, 6);
+                        const uint64_t B1l = umma_smem_desc(b0 + (PAIR ? 3 : 4) * AJ_B_PLANE, 256, 6);
                         const uint32_t acc = kk > 0 ? 1u : 0u;
                         // [Qi | Qr] += Phir . [-U3i | U3r] + Phii . [U3r | U3i]
-                        mma_f16(qd, A[0], B2h, idesc, acc);
-                        mma_f16(qd, A[0], B2l, idesc, 1);
-                        mma_f16(qd, A[1], B2h, idesc, 1);
-                        mma_f16(qd, A[2], B1h, idesc, 1);
-                        mma_f16(qd, A[2], B1l, idesc, 1);
-                        mma_f16(qd, A[3], B1h, idesc, 1);
-                        mma_commit(&empty[s]);
-                        if (++s == AJ_NST) {
+#define MMA(...) (PAIR ? mma_f16_pair(__VA_ARGS__) : mma_f16(__VA_ARGS__))
+#define COMMIT(b) (PAIR ? mma_commit_pair(b) : mma_commit(b))
+                        MMA(qd, A[0], B2h, idesc, acc);
+                        MMA(qd, A[0], B2l, idesc, 1);
+                        MMA(qd, A[1], B2h, idesc, 1);
+                        MMA(qd, A[2], B1h, idesc, 1);
+                        MMA(qd, A[2], B1l, idesc, 1);
+                        MMA(qd, A[3], B1h, idesc, 1);
+                        COMMIT(&empty[s]);
+                        if (++s == NST) {
                             s = 0;
                             ph ^= 1;
                         }
                     }
-                    mma_commit(&qfull[qb]);
+                    COMMIT(&qfull[qb]);
+#undef MMA
+#undef COMMIT
                 }
             }
         }
@@ -280,11 +319,11 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         // ---------------------------------------------------- factor loader
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
-            for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
-                const AjTile tl = aj_tile(g, t);
+            for (int64_t t = tstart; t < g.t_end; t += tstep) {
+                const AjTile tl = aj_tile(g, t, rank);
                 const TcDesc* tdk = tcd + int64_t(tl.k) * g.ncols;
                 for (int64_t j = 0; j < g.ncols; ++j) {
-                    mbar_wait(&fempty[s], ph ^ 1);
+                    mbar_wait_backoff(&fempty[s], ph ^ 1, 64);
                     const TcDesc d = tdk[j];
                     unsigned char* slot = sSlot + s * g.slot_bytes;
                     const uint32_t r23 = uint32_t(d.r2 * d.r3);
@@ -309,8 +348,8 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         const int ctid = threadIdx.x - TC_PW0 * 32;  // 0..255
         const uint32_t lane_addr = uint32_t(i1l * 32) << 16;
         uint32_t fs = 0, fph = 0, nq = 0;
-        for (int64_t t = g.t_begin + blockIdx.x; t < g.t_end; t += gridDim.x) {
-            const AjTile tl = aj_tile(g, t);
+        for (int64_t t = tstart; t < g.t_end; t += tstep) {
+            const AjTile tl = aj_tile(g, t, rank);
             const int nc = nch[tl.k];
             const int* cs = cstart + int64_t(tl.k) * (g.maxch + 1);
             // exact power of two: undoes the (rhs, component) Phi scale and the U3 scale
@@ -319,7 +358,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                 const uint32_t qb = nq & 1, qph = (nq >> 1) & 1;
                 const int j0 = cs[n], j1 = cs[n + 1];
                 float2* rb = red + (nq & 1) * AJ_MAXCOLS * AJ_NPW;
-                mbar_wait(&qfull[qb], qph);
+                mbar_wait<PAIR>(&qfull[qb], qph);
                 tc_fence_after();
                 const uint32_t qbase = tmem + lane_addr + qb * 256u;
                 for (int j = j0; j < j1; ++j) {
@@ -357,7 +396,12 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                 // Q buffer no longer read by this warp
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&qfree[qb]);
+                if (lane == 0) {
+                    if (PAIR)
+                        mbar_arrive_cluster(mapa_shared(smem_u32(&qfree[qb]), 0));
+                    else
+                        mbar_arrive(&qfree[qb]);
+                }
                 named_bar_sync(1, AJ_NPW * 32);  // all partials of the chunk are in rb
                 for (int jj = ctid; jj < j1 - j0; jj += AJ_NPW * 32) {
                     float sx = 0.f, sy = 0.f;
@@ -376,7 +420,13 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 3) tmem_dealloc(tmem, 512);
+    if (PAIR) cluster_sync();
+    if (warp == 3) {
+        if (PAIR)
+            tmem_dealloc_pair(tmem, 512);
+        else
+            tmem_dealloc(tmem, 512);
+    }
 }
 
 // max |Re|, |Im| of each (right-hand side, component) block of Phi — the

@@ -771,7 +771,14 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     g.nt2 = (g.n2 + TC_TI2 - 1) / TC_TI2;
     g.p = int(p);
     g.nrt = int64_t(g.nt1) * g.nt2;
-    g.ntiles = int64_t(p) * g.q * g.nrt;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const int nsm = num_sms(dev);
+    {  // CTA-pair kernel (cta_group::2 over two row tiles): half the B reads per MMA
+        const char* e = std::getenv("TMB_DISABLE_PAIR");
+        g.pair = (!(e && *e && *e != '0') && g.nrt % 2 == 0 && nsm >= 2) ? 1 : 0;
+    }
+    g.ntiles = int64_t(p) * g.q * (g.nrt >> g.pair);
     g.rmax2 = s->rmax[1];
     g.rmax3 = s->rmax[2];
     g.u2_off = TC_SLOT_V + int(round16(uint32_t(TC_TI1 * g.rmax2 * g.rmax3 * 8)));
@@ -781,8 +788,10 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
         const char* dbg = std::getenv("TMB_TC_DEBUG");
         g.debug = dbg ? std::atoi(dbg) : 0;
     }
-    const size_t smem = 1024 + size_t(AJ_NST) * (AJ_A_STAGE + AJ_B_STAGE) + size_t(TC_JR) * g.slot_bytes +
-                        size_t(2) * AJ_MAXCOLS * AJ_NPW * sizeof(float2) + (2 * AJ_NST + 2 * TC_JR + 4) * 8 + 16;
+    const int nst = g.pair ? AJ_NST2 : AJ_NST;
+    const size_t bstage = g.pair ? size_t(4) * AJ_B_PLANE : size_t(AJ_B_STAGE);
+    const size_t smem = 1024 + size_t(nst) * (AJ_A_STAGE + bstage) + size_t(TC_JR) * g.slot_bytes +
+                        size_t(2) * AJ_MAXCOLS * AJ_NPW * sizeof(float2) + (2 * nst + 2 * TC_JR + 4) * 8 + 16;
     if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: shared-memory plan too large");
     // Phi -> scaled 2-term fp16 planes (per call)
     g.nks = (g.n3 + 15) / 16;
@@ -824,22 +833,46 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
                                               CU_TENSOR_MAP_SWIZZLE_32B);
     const int64_t nred = g.nrt * g.q;
     float2* part = static_cast<float2*>(s->part.get(size_t(s->ncols * p * nred) * sizeof(float2)));
-    CK(cudaFuncSetAttribute(adj_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    const unsigned grid = unsigned(std::min<int64_t>(g.ntiles, num_sms(dev)));
+    CK(cudaFuncSetAttribute(adj_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CK(cudaFuncSetAttribute(adj_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const unsigned grid = g.pair ? unsigned(std::min<int64_t>(2 * g.ntiles, nsm & ~1))
+                                 : unsigned(std::min<int64_t>(g.ntiles, nsm));
+    const int64_t wave = g.pair ? grid / 2 : grid;
+    const int64_t tpb = g.nrt >> g.pair;  // tiles per (rhs, component) block
     int64_t bready = hp ? 0 : nblk;
-    for (int64_t t0 = 0; t0 < g.ntiles; t0 += grid) {  // one launch per wave (see run_forward_tc)
+    for (int64_t t0 = 0; t0 < g.ntiles; t0 += wave) {  // one launch per wave (see run_forward_tc)
         g.t_begin = t0;
-        g.t_end = std::min<int64_t>(g.ntiles, t0 + grid);
-        const int64_t bneed = (g.t_end - 1) / g.nrt + 1;  // blocks this wave reads
+        g.t_end = std::min<int64_t>(g.ntiles, t0 + wave);
+        const int64_t bneed = (g.t_end - 1) / tpb + 1;  // blocks this wave reads
         for (; bready < bneed; ++bready) {
             CK(cudaStreamWaitEvent(st, arrived[size_t(bready)], 0));
             prepare(bready, bready + 1);
         }
-        adj_tc_kernel<<<grid, AJ_THREADS, smem, st>>>(amap, s->adj_bmap, s->d_tcd, s->d_varena, s->d_u2arena,
-                                                       s->d_nch, s->d_cstart, g, phimax, part);
-        launched(cudaSuccess, "adj_tc_kernel");
+        if (g.pair) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(AJ_THREADS);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            launched(cudaLaunchKernelEx(&cfg, adj_tc_kernel<true>, amap, s->adj_bmap,
+                                        static_cast<const TcDesc*>(s->d_tcd), static_cast<const float2*>(s->d_varena),
+                                        static_cast<const float2*>(s->d_u2arena), static_cast<const int*>(s->d_nch),
+                                        static_cast<const int*>(s->d_cstart), g, static_cast<const float*>(phimax),
+                                        part),
+                     "adj_tc_kernel<pair>");
+        } else {
+            adj_tc_kernel<false><<<grid, AJ_THREADS, smem, st>>>(amap, s->adj_bmap, s->d_tcd, s->d_varena,
+                                                                  s->d_u2arena, s->d_nch, s->d_cstart, g, phimax,
+                                                                  part);
+            launched(cudaSuccess, "adj_tc_kernel");
+        }
     }
     for (cudaEvent_t e : arrived) CK(cudaEventDestroy(e));
     const int64_t warps = s->ncols * p;
