@@ -242,6 +242,33 @@ def test_tensor_core_forward(oracle, product, monkeypatch, dims, q, m, rmin, rma
     assert rel(z_cc, z_ref) <= 1e-5
 
 
+@pytest.mark.parametrize("dims,q,m,rmin,rmax,p", [
+    ((24, 18, 300), 2, 11, 2, 12, 1),    # forward pairs over a partial second i3 tile, nrt = 6
+    ((16, 40, 200), 1, 17, 1, 16, 2),    # nt1 = 4 (two i1 pairs), partial i2 tiles, two RHS
+    ((8, 64, 130), 3, 6, 3, 9, 1),       # nt1 = 2: one pair; adjoint nrt = 4
+])
+def test_cta_pair_kernels(oracle, product, monkeypatch, dims, q, m, rmin, rmax, p):
+    """The CTA-pair (cta_group::2) forward and adjoint against the oracle and
+    against the single-CTA kernels (TMB_DISABLE_PAIR=1) on shapes that take
+    the pair path (even i1-block / row-tile counts, 256-voxel i3 tiles)."""
+    O, P = oracle, product
+    cc = ragged_store(dims, q, m, rmin, rmax, seed=11 * m + q)
+    ref = O.OracleStore(cc.rounded_c64())
+    ds = P.DeviceStore.from_compressed(cc, "c64")
+    x = cn01(m, p, 5).astype(np.complex64).astype(np.complex128)
+    phi = cn01(cc.rows, p, 6).astype(np.complex64).astype(np.complex128)
+    y2, z2 = ds.forward(x), ds.adjoint(phi)
+    monkeypatch.setenv("TMB_DISABLE_PAIR", "1")
+    y1, z1 = ds.forward(x), ds.adjoint(phi)
+    monkeypatch.delenv("TMB_DISABLE_PAIR")
+    y_ref, z_ref = ref.forward(x), ref.adjoint(phi)
+    for got in (y1, y2):
+        assert rel(got, y_ref) <= 1e-5
+    for got in (z1, z2):
+        assert rel(got, z_ref) <= 1e-5
+    assert rel(y2, y1) <= 1e-6 and rel(z2, z1) <= 1e-6
+
+
 @pytest.mark.parametrize("chain", ["", "1", "3", "48"])
 def test_tensor_core_long_k(product, monkeypatch, chain):
     """Accumulation over a long K stream (2 500 columns, K ~ 21 000 per
