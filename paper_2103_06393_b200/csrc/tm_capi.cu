@@ -23,6 +23,7 @@
 #include "tm_adj_tc.cuh"
 #include "tm_mrhs_tc.cuh"
 #include "tm_tmap.h"
+#include "tm_io_internal.hpp"
 
 using namespace tmb;
 
@@ -89,6 +90,9 @@ int guarded(F&& f) {
     } catch (const TmError& e) {
         g_last_error = e.what();
         return e.code;
+    } catch (const tmb_io::ParseFail& e) {  // streaming ingest (tm_io.cpp)
+        g_last_error = e.what();
+        return TM_PARSE_ERROR;
     } catch (const std::bad_alloc&) {
         g_last_error = "host allocation failed";
         return TM_CAPACITY_ERROR;
@@ -298,7 +302,7 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
     s->tc_ok = true;
 }
 
-void build_store(tm_store* s, const tm_store_desc& d) {
+void build_store(tm_store* s, const tm_store_desc& d, const tmb_io::PayloadFill* fill = nullptr) {
     const int64_t n1 = d.dims[0], n2 = d.dims[1], n3 = d.dims[2];
     const int64_t ntens = s->ncols * s->q;
     // host-side tensor table: source offsets ([col][comp] order) and
@@ -346,37 +350,103 @@ void build_store(tm_store* s, const tm_store_desc& d) {
 
     // pack in bounded chunks of whole tensors
     const int64_t total = src_off[static_cast<size_t>(ntens)];
+    (void)total;
     const int64_t chunk_cap = int64_t(16) << 20;  // 16 M complex128 = 256 MiB of staging
-    DevBuf stage, jobbuf;
-    int64_t t0 = 0;
-    while (t0 < ntens) {
+    auto chunk_end = [&](int64_t t0) {
         int64_t t1 = t0 + 1;
         while (t1 < ntens && src_off[t1 + 1] - src_off[t0] <= chunk_cap) ++t1;
-        const int64_t elems = src_off[t1] - src_off[t0];
-        const double2* src;
-        if (d.payload_on_device) {
-            src = reinterpret_cast<const double2*>(d.payload) + src_off[t0];
-        } else {
-            void* st = stage.get(size_t(elems) * sizeof(double2));
-            CK(cudaMemcpy(st, d.payload + 2 * src_off[t0], size_t(elems) * sizeof(double2), cudaMemcpyHostToDevice));
-            src = static_cast<const double2*>(st);
-        }
-        std::vector<PackJob> jobs(static_cast<size_t>(t1 - t0));
+        return t1;
+    };
+    auto make_jobs = [&](int64_t t0, int64_t t1, PackJob* jobs) {
         for (int64_t i = t0; i < t1; ++i) {
             const int64_t j = i / s->q, k = i % s->q;
-            jobs[static_cast<size_t>(i - t0)] = {src_off[i] - src_off[t0], k * s->ncols + j};
+            jobs[i - t0] = {src_off[i] - src_off[t0], k * s->ncols + j};
         }
-        void* jb = jobbuf.get(jobs.size() * sizeof(PackJob));
-        CK(cudaMemcpy(jb, jobs.data(), jobs.size() * sizeof(PackJob), cudaMemcpyHostToDevice));
+    };
+    auto pack = [&](const double2* src, const PackJob* jb, int64_t njobs, cudaStream_t st) {
         if (s->dtype == TM_C64)
-            pack_kernel<float2><<<unsigned(jobs.size()), 256>>>(src, static_cast<PackJob*>(jb), s->d_desc, int(n1),
-                                                               int(n2), int(n3), static_cast<float2*>(s->d_arena));
+            pack_kernel<float2><<<unsigned(njobs), 256, 0, st>>>(src, jb, s->d_desc, int(n1), int(n2), int(n3),
+                                                                 static_cast<float2*>(s->d_arena));
         else
-            pack_kernel<double2><<<unsigned(jobs.size()), 256>>>(src, static_cast<PackJob*>(jb), s->d_desc, int(n1),
-                                                                int(n2), int(n3), static_cast<double2*>(s->d_arena));
+            pack_kernel<double2><<<unsigned(njobs), 256, 0, st>>>(src, jb, s->d_desc, int(n1), int(n2), int(n3),
+                                                                  static_cast<double2*>(s->d_arena));
         launched(cudaSuccess, "pack_kernel");
-        CK(cudaDeviceSynchronize());
-        t0 = t1;
+    };
+    if (fill) {
+        // Streaming ingest: the host reads chunk c into pinned buffer c % 2
+        // while the copy + pack of chunk c - 1 run on the stream; no host copy
+        // of the whole payload ever exists.
+        struct Pipe {
+            void* h[2] = {nullptr, nullptr};
+            PackJob* hj[2] = {nullptr, nullptr};
+            cudaEvent_t done[2] = {nullptr, nullptr};
+            cudaStream_t st = nullptr;
+            ~Pipe() {
+                if (st) cudaStreamSynchronize(st);
+                for (int b = 0; b < 2; ++b) {
+                    if (h[b]) cudaFreeHost(h[b]);
+                    if (hj[b]) cudaFreeHost(hj[b]);
+                    if (done[b]) cudaEventDestroy(done[b]);
+                }
+                if (st) cudaStreamDestroy(st);
+            }
+        } pp;
+        int64_t maxjobs = 1, maxel = 1;
+        for (int64_t t0 = 0; t0 < ntens;) {
+            const int64_t t1 = chunk_end(t0);
+            maxjobs = std::max(maxjobs, t1 - t0);
+            maxel = std::max(maxel, src_off[t1] - src_off[t0]);
+            t0 = t1;
+        }
+        DevBuf dstage[2], djobs[2];
+        CK(cudaStreamCreateWithFlags(&pp.st, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaHostAlloc(&pp.h[b], size_t(maxel) * sizeof(double2), cudaHostAllocDefault));
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&pp.hj[b]), size_t(maxjobs) * sizeof(PackJob),
+                             cudaHostAllocDefault));
+            CK(cudaEventCreateWithFlags(&pp.done[b], cudaEventDisableTiming));
+            dstage[b].get(size_t(maxel) * sizeof(double2));
+            djobs[b].get(size_t(maxjobs) * sizeof(PackJob));
+        }
+        int c = 0;
+        for (int64_t t0 = 0; t0 < ntens; ++c) {
+            const int64_t t1 = chunk_end(t0);
+            const int b = c & 1;
+            if (c >= 2) CK(cudaEventSynchronize(pp.done[b]));  // buffer b's previous chunk is packed
+            const int64_t elems = src_off[t1] - src_off[t0];
+            (*fill)(t0, t1, static_cast<double*>(pp.h[b]));
+            make_jobs(t0, t1, pp.hj[b]);
+            CK(cudaMemcpyAsync(dstage[b].p, pp.h[b], size_t(elems) * sizeof(double2), cudaMemcpyHostToDevice, pp.st));
+            CK(cudaMemcpyAsync(djobs[b].p, pp.hj[b], size_t(t1 - t0) * sizeof(PackJob), cudaMemcpyHostToDevice,
+                               pp.st));
+            pack(static_cast<const double2*>(dstage[b].p), static_cast<const PackJob*>(djobs[b].p), t1 - t0, pp.st);
+            CK(cudaEventRecord(pp.done[b], pp.st));
+            t0 = t1;
+        }
+        CK(cudaStreamSynchronize(pp.st));
+    } else {
+        DevBuf stage, jobbuf;
+        int64_t t0 = 0;
+        while (t0 < ntens) {
+            const int64_t t1 = chunk_end(t0);
+            const int64_t elems = src_off[t1] - src_off[t0];
+            const double2* src;
+            if (d.payload_on_device) {
+                src = reinterpret_cast<const double2*>(d.payload) + src_off[t0];
+            } else {
+                void* st = stage.get(size_t(elems) * sizeof(double2));
+                CK(cudaMemcpy(st, d.payload + 2 * src_off[t0], size_t(elems) * sizeof(double2),
+                              cudaMemcpyHostToDevice));
+                src = static_cast<const double2*>(st);
+            }
+            std::vector<PackJob> jobs(static_cast<size_t>(t1 - t0));
+            make_jobs(t0, t1, jobs.data());
+            void* jb = jobbuf.get(jobs.size() * sizeof(PackJob));
+            CK(cudaMemcpy(jb, jobs.data(), jobs.size() * sizeof(PackJob), cudaMemcpyHostToDevice));
+            pack(src, static_cast<const PackJob*>(jb), t1 - t0, nullptr);
+            CK(cudaDeviceSynchronize());
+            t0 = t1;
+        }
     }
 
     build_tc(s, s->host_desc);
@@ -410,13 +480,13 @@ void build_store(tm_store* s, const tm_store_desc& d) {
     }
 }
 
-tm_store* create_store(const tm_store_desc& d, int device, int dtype) {
+tm_store* create_store(const tm_store_desc& d, int device, int dtype, const tmb_io::PayloadFill* fill = nullptr) {
     if (dtype != TM_C64 && dtype != TM_C128) contract("store: dtype must be TM_C64 or TM_C128");
     if (d.q < 1 || d.ncols < 0 || d.dims[0] < 1 || d.dims[1] < 1 || d.dims[2] < 1)
         contract("store: non-positive dimensions");
     if (d.dims[0] > (1 << 30) || d.dims[1] > (1 << 30) || d.dims[2] > (1 << 30))
         contract("store: grid dimension too large");
-    if (d.ncols > 0 && (!d.ranks || !d.payload)) contract("store: ranks and payload are required");
+    if (d.ncols > 0 && (!d.ranks || (!d.payload && !fill))) contract("store: ranks and payload are required");
     if (d.v && d.m2 < 1) contract("store: ACA V needs m2 >= 1");
     // validate every rank before touching the device (reference: read_tucker,
     // src/io.cpp:133-139, and the TuckerTensor invariant 1 <= r_g <= n_g)
@@ -437,7 +507,7 @@ tm_store* create_store(const tm_store_desc& d, int device, int dtype) {
     s->ncols = d.ncols;
     for (int g = 0; g < 3; ++g) s->dims[g] = d.dims[g];
     try {
-        build_store(s, d);
+        build_store(s, d, fill);
     } catch (...) {
         delete s;
         throw;
@@ -1259,3 +1329,10 @@ TM_API int tm_aca_adjoint(tm_store* s, const void* phi, int64_t ldphi, int64_t p
 }
 
 }  // extern "C"
+
+// Streaming CTC1 / CTA1 ingest (tm_io.cpp): `d` carries the ranks (and V),
+// the payload comes chunk by chunk from `fill`.
+int tmb_io::create_store_streaming(const tm_store_desc* d, const PayloadFill& fill, int device, int dtype,
+                                   tm_store** out) {
+    return guarded([&] { *out = create_store(*d, device, dtype, &fill); });
+}

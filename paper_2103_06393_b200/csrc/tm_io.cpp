@@ -28,6 +28,7 @@ struct Reader {
     std::vector<char> buf;
     uint64_t pos = 0;
 
+    Reader() = default;
     explicit Reader(const std::string& p) : path(p) {
         std::ifstream in(p, std::ios::binary | std::ios::ate);
         if (!in) fail_at("cannot open '" + p + "'", 0);
@@ -142,6 +143,93 @@ Parsed parse(const std::string& path, bool aca) {
     return out;
 }
 
+namespace {
+
+// Streaming reader: the header and the 12-byte rank triplet of every record
+// are read up front (seeking over the payloads), the payloads later on
+// demand, straight into the builder's pinned staging buffers.
+struct StreamScan {
+    std::string path;
+    std::ifstream in;
+    uint64_t size = 0;
+    Header h{};
+    std::vector<int32_t> ranks;
+    std::vector<uint64_t> pay_off;   // file offset of each record's payload
+    std::vector<uint64_t> pay_len;   // complex elements
+    std::vector<double> v;
+    uint64_t m2 = 0;
+
+    [[noreturn]] void fail(const std::string& m, uint64_t off) const {
+        throw ParseFail("'" + path + "': " + m + " (byte offset " + std::to_string(off) + ")", off);
+    }
+    void read_at(uint64_t off, void* dst, uint64_t n, const char* what) {
+        if (off + n > size) fail(std::string("truncated while reading ") + what, off > size ? size : off);
+        in.seekg(std::streamoff(off));
+        in.read(static_cast<char*>(dst), std::streamsize(n));
+        if (!in) fail(std::string("read error in ") + what, off);
+    }
+
+    StreamScan(const std::string& p, bool aca) : path(p) {
+        in.open(p, std::ios::binary | std::ios::ate);
+        if (!in) throw ParseFail("cannot open '" + p + "' (byte offset 0)", 0);
+        size = uint64_t(in.tellg());
+        // the header through the common Reader logic (45 bytes)
+        unsigned char hb[45];
+        read_at(0, hb, std::min<uint64_t>(45, size), "header");
+        Reader r;
+        r.path = p;
+        r.buf.assign(reinterpret_cast<char*>(hb), reinterpret_cast<char*>(hb) + std::min<uint64_t>(45, size));
+        h = read_header(r, aca ? "CTA1" : "CTC1");
+        const uint64_t count = uint64_t(h.m) * h.q;
+        ranks.reserve(size_t(3 * count));
+        pay_off.reserve(size_t(count));
+        pay_len.reserve(size_t(count));
+        uint64_t pos = 45;
+        for (uint64_t i = 0; i < count; ++i) {
+            unsigned char rb[12];
+            if (pos + 12 > size) fail("truncated while reading u32", pos + 4 * ((size - pos) / 4));
+            read_at(pos, rb, 12, "u32");
+            uint32_t rk[3];
+            for (int g = 0; g < 3; ++g) {
+                rk[g] = uint32_t(rb[4 * g]) | uint32_t(rb[4 * g + 1]) << 8 | uint32_t(rb[4 * g + 2]) << 16 |
+                        uint32_t(rb[4 * g + 3]) << 24;
+                if (rk[g] == 0 || rk[g] > h.dims[g])
+                    fail("tucker rank " + std::to_string(rk[g]) + " out of range for mode " + std::to_string(g + 1),
+                         pos + 4 * uint64_t(g) + 4);
+                ranks.push_back(int32_t(rk[g]));
+            }
+            pos += 12;
+            const uint64_t n = uint64_t(rk[0]) * rk[1] * rk[2] + uint64_t(h.dims[0]) * rk[0] +
+                               uint64_t(h.dims[1]) * rk[1] + uint64_t(h.dims[2]) * rk[2];
+            if (pos + 16 * n > size) fail("truncated while reading f64", pos);
+            pay_off.push_back(pos);
+            pay_len.push_back(n);
+            pos += 16 * n;
+        }
+        if (!aca) {
+            if (pos != size) fail(std::to_string(size - pos) + " trailing bytes", pos);
+            return;
+        }
+        const uint64_t rest = size - pos;
+        const uint64_t col_bytes = 16ull * h.m;
+        if (col_bytes == 0 || rest % col_bytes != 0 || rest / col_bytes == 0)
+            fail("V block of " + std::to_string(rest) + " bytes is not a positive multiple of 16*r_c", pos);
+        m2 = rest / col_bytes;
+        v.resize(size_t(2 * m2 * h.m));
+        read_at(pos, v.data(), rest, "f64");
+    }
+
+    // payloads of records [t0, t1), contiguous, into dst
+    void fill(int64_t t0, int64_t t1, double* dst) {
+        for (int64_t i = t0; i < t1; ++i) {
+            read_at(pay_off[size_t(i)], dst, 16 * pay_len[size_t(i)], "f64");
+            dst += 2 * pay_len[size_t(i)];
+        }
+    }
+};
+
+}  // namespace
+
 }  // namespace tmb_io
 
 namespace {
@@ -173,18 +261,38 @@ int create_from(const tmb_io::Parsed& p, int device, int dtype, tm_store** out) 
     return tm_store_create(&d, device, dtype, out);
 }
 
+int create_streamed(const std::string& path, bool aca, int device, int dtype, tm_store** out) {
+    tmb_io::StreamScan sc(path, aca);
+    tm_store_desc d{};
+    d.q = int32_t(sc.h.q);
+    d.ncols = sc.h.m;
+    for (int g = 0; g < 3; ++g) d.dims[g] = sc.h.dims[g];
+    d.ranks = sc.ranks.data();
+    d.payload = nullptr;
+    if (aca) {
+        d.v = sc.v.data();
+        d.m2 = int64_t(sc.m2);
+    }
+    return tmb_io::create_store_streaming(
+        &d, [&](std::int64_t t0, std::int64_t t1, double* dst) { sc.fill(t0, t1, dst); }, device, dtype, out);
+}
+
 }  // namespace
 
 extern "C" {
 
-// load_ctc1 (src/io.cpp:212-230) into a device store.
+// load_ctc1 (src/io.cpp:212-230) into a device store, streamed (SURVEY
+// §8f-3): only the rank triplets are read up front; payloads go from the file
+// through two pinned 256 MiB staging buffers to the device in bounded chunks
+// (read of chunk c overlapping the copy + pack of chunk c - 1), converted to
+// the store's precision on the device — no whole-file host buffer.
 TM_API int tm_store_load_ctc1(const char* path, int device, int dtype, tm_store** out) {
-    return guarded_io([&]() -> int { return create_from(tmb_io::parse(path ? path : "", false), device, dtype, out); });
+    return guarded_io([&]() -> int { return create_streamed(path ? path : "", false, device, dtype, out); });
 }
 
-// load_cta1 (src/io.cpp:249-279) into a device store carrying V.
+// load_cta1 (src/io.cpp:249-279) into a device store carrying V, streamed.
 TM_API int tm_store_load_cta1(const char* path, int device, int dtype, tm_store** out) {
-    return guarded_io([&]() -> int { return create_from(tmb_io::parse(path ? path : "", true), device, dtype, out); });
+    return guarded_io([&]() -> int { return create_streamed(path ? path : "", true, device, dtype, out); });
 }
 
 }  // extern "C"

@@ -3,9 +3,12 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
+
+#include "../../include/tuckmat_b200.h"
 
 namespace tmb_io {
 
@@ -26,5 +29,14 @@ struct Parsed {
 
 // aca = false: "CTC1"; aca = true: "CTA1".  Throws ParseFail.
 Parsed parse(const std::string& path, bool aca);
+
+// Streaming ingest: the store builder asks for the payloads
+// of tensors [t0, t1) ([col][comp] order, complex128 pairs, contiguous) in
+// bounded chunks; `dst` is pinned host memory.  Throws ParseFail.
+using PayloadFill = std::function<void(std::int64_t t0, std::int64_t t1, double* dst)>;
+
+// Build a device store from `d` (ranks, optional V; payload unused) with the
+// payload streamed through `fill` (tm_capi.cu).  Returns a TM_* status.
+int create_store_streaming(const tm_store_desc* d, const PayloadFill& fill, int device, int dtype, tm_store** out);
 
 }  // namespace tmb_io
