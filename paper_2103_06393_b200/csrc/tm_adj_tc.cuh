@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                 const int arow = int(tl.rt * TC_ROWS);
                 for (int n = 0; n < nc; ++n) {
                     for (int kk = 0; kk < g.nks; ++kk) {
-                        mbar_wait_backoff<PAIR>(&empty[s], ph ^ 1, 64);
+                        mbar_wait_backoff(&empty[s], ph ^ 1, 64);
                         unsigned char* da = sA + s * AJ_A_STAGE;
                         unsigned char* db = sB + s * BSTAGE;
                         if (PAIR) {
@@ -275,11 +275,11 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                 const int nc = nch[tl.k];
                 for (int n = 0; n < nc; ++n, ++nq) {
                     const uint32_t qb = nq & 1, qph = (nq >> 1) & 1;
-                    mbar_wait<PAIR>(&qfree[qb], qph ^ 1);  // consumers are done with this buffer
+                    mbar_wait(&qfree[qb], qph ^ 1);  // consumers are done with this buffer
                     tc_fence_after();
                     const uint32_t qd = tmem + qb * 256u;
                     for (int kk = 0; kk < g.nks; ++kk) {
-                        mbar_wait<PAIR>(&full[s], ph);
+                        mbar_wait(&full[s], ph);
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + s * AJ_A_STAGE);
                         const uint32_t b0 = smem_u32(sB + s * BSTAGE);
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                 const uint32_t qb = nq & 1, qph = (nq >> 1) & 1;
                 const int j0 = cs[n], j1 = cs[n + 1];
                 float2* rb = red + (nq & 1) * AJ_MAXCOLS * AJ_NPW;
-                mbar_wait<PAIR>(&qfull[qb], qph);
+                mbar_wait(&qfull[qb], qph);
                 tc_fence_after();
                 const uint32_t qbase = tmem + lane_addr + qb * 256u;
                 for (int j = j0; j < j1; ++j) {

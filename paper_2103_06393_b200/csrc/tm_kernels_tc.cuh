@@ -244,11 +244,11 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
         for (int u = 0; u < NU; ++u) w[e][u] = cmul2(w[e][u], xj);
     // wait for every stage (16 K) this column opens (at most two: r3 <= 16)
     const uint32_t kend = ring.kpos + uint32_t(r3);
-    if (ring.kpos == 0) TC_TWAIT(prof, t_empty, (mbar_wait<PAIR>(&empty[ring.st], ring.ph ^ 1u)));
+    if (ring.kpos == 0) TC_TWAIT(prof, t_empty, (mbar_wait(&empty[ring.st], ring.ph ^ 1u)));
     if (kend > 16) {
         uint32_t s, ph;
         ring_ahead(ring, 1, nst, s, ph);
-        TC_TWAIT(prof, t_empty, (mbar_wait<PAIR>(&empty[s], ph ^ 1u)));
+        TC_TWAIT(prof, t_empty, (mbar_wait(&empty[s], ph ^ 1u)));
     }
     uint32_t s1, ph1;
     ring_ahead(ring, 1, nst, s1, ph1);
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const TcTile tl = tc_tile(g, t, rank);
                 const int nks = (kc[tl.k] + 15) >> 4;
                 for (int kk = 0; kk < nks; ++kk) {
-                    TC_TWAIT(g.prof, t_w, (mbar_wait_backoff<PAIR>(&empty[s], ph ^ 1, 128)));
+                    TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(&empty[s], ph ^ 1, 128)));
                     if (PAIR) {
                         // each CTA loads its half of the i3 span (B rows [rank nmma, +nmma) of the
                         // M = 256 MMA); the bytes of both halves complete on rank 0's barrier
@@ -415,10 +415,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 int cpos = 0;  // stage position inside the current chain
                 for (int kk = 0; kk < nks; ++kk) {
                     if (cpos == 0) {
-                        TC_TWAIT(g.prof, t_w, (mbar_wait<PAIR>(cfree, (gch & 1) ^ 1)));  // previous chain folded
+                        TC_TWAIT(g.prof, t_w, (mbar_wait(cfree, (gch & 1) ^ 1)));  // previous chain folded
                         tc_fence_after();
                     }
-                    TC_TWAIT(g.prof, t_w2, (mbar_wait<PAIR>(&full[s], ph)));
+                    TC_TWAIT(g.prof, t_w2, (mbar_wait(&full[s], ph)));
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + s * TC_A_STAGE);
                     const uint32_t b0 = smem_u32(sB + s * g.b_stage);
@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             float2* yp = y + ldy * tl.c + int64_t(tl.k) * nv3 + ei1 + int64_t(g.n1) * ei2;
             const int64_t pl = int64_t(g.n1) * g.n2;
             for (int ch = 0; ch < nch; ++ch, ++gch) {
-                TC_TWAIT(g.prof, t_w, (mbar_wait_backoff<PAIR>(cfull, gch & 1, 256)));
+                TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(cfull, gch & 1, 256)));
                 tc_fence_after();
                 const bool last = ch == nch - 1;
                 for (int hh = 0; hh < g.nh3; ++hh)

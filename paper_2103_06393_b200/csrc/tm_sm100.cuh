@@ -61,6 +61,11 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // cluster scope, for barriers that receive arrivals from the peer CTA).  A
 // barrier that has not completed after 20 s means a protocol bug (or a dead
 // peer CTA): trap instead of hanging the GPU.
+// Note: the CTA-pair kernels wait with CLUSTER = false too (as CUTLASS's
+// 2-SM pipelines do): a cluster-scope acquire invalidates the whole L1 (CCTL.IVALL)
+// on every completed wait, and every operand the peer hands over is either
+// TMA-written or read by the peer's own tensor core after its
+// fence.proxy.async.
 template <bool CLUSTER = false>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
