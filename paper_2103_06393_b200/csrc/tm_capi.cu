@@ -673,8 +673,8 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     const int64_t wave = g.pair ? grid / 2 : grid;
     g.prof = nullptr;
     if (g.debug & 8) {
-        CK(cudaMalloc(&g.prof, 16 * sizeof(unsigned long long)));
-        CK(cudaMemsetAsync(g.prof, 0, 16 * sizeof(unsigned long long), st));
+        CK(cudaMalloc(&g.prof, 32 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(g.prof, 0, 32 * sizeof(unsigned long long), st));
     }
     tm_store* ms = const_cast<tm_store*>(s);
     float2* rsum = static_cast<float2*>(ms->rsum.get(size_t(grid) * g.nmma * g.nh3 * TC_ROWS * sizeof(float2)));
@@ -734,7 +734,7 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
         }
     }
     if (g.prof) {  // wait profile: mean cycles per recording thread, per role
-        unsigned long long h[16];
+        unsigned long long h[32];
         CK(cudaMemcpyAsync(h, g.prof, sizeof(h), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         CK(cudaFree(g.prof));
@@ -744,6 +744,7 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
         for (int r = 0; r < 5; ++r)
             std::fprintf(stderr, "[tc-prof] %-9s total %14llu  wait %-6s %14llu  wait %-5s %14llu\n", names[r], h[3 * r],
                          w1[r], h[3 * r + 1], w2[r], h[3 * r + 2]);
+        std::fprintf(stderr, "[tc-prof] producer phases: mode-2 loop %llu  scale/split/store %llu\n", h[15], h[16]);
     }
 }
 
