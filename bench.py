@@ -113,6 +113,21 @@ def measured_peaks():
         return {}
 
 
+def committed_traffic(cfg):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu --set full capture (profiles/traffic.json), when it was
+    taken on this config; else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+    except (OSError, ValueError):
+        return None
+    if not cfg.name.startswith(t.get("config", "") + ":"):
+        return None
+    v = t.get("dram_bytes_per_launch") or []
+    return int(sum(v) / len(v)) if v else None
+
+
 def f16_peak_tflops(torch):
     """cuBLAS fp16 GEMM 8192^3 throughput measured in this run (best of 5),
     beside MEASURED_PEAKS.json's bf16 figures (same tensor-core rate)."""
@@ -468,7 +483,8 @@ def main():
             kernels = ("fwd_cc_kernel", "adj_cc_kernel (+ adj_reduce_kernel)")
         fa, aa = flops / (fwd_med * 1e-3) / 1e12, flops / (adj_med * 1e-3) / 1e12
         roof = {"bound": bound, "kernel": kernels[0], "achieved": round(fa, 2), "peak": round(peak, 2),
-                "unit": "TFLOP/s", "frac": round(fa / peak, 4), "peak_source": unit_src, "traffic": None,
+                "unit": "TFLOP/s", "frac": round(fa / peak, 4), "peak_source": unit_src, "traffic": committed_traffic(cfg),
+                "traffic_unit": "bytes per launch (DRAM read + write; profiles/traffic.json)",
                 "algorithmic_flops_per_launch": flops,
                 "adjoint": {"kernel": kernels[1], "achieved": round(aa, 2), "frac": round(aa / peak, 4)},
                 "hbm_bytes_algorithmic": int(compressed_bytes(cfg, ranks[c0:c1]) + (c1 - c0) * cfg.p * 8
