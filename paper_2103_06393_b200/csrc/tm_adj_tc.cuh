@@ -83,16 +83,27 @@ struct AjGeom {
     int maxch;       // chunk stride of the chunk-start table
     int debug;       // diagnostics (TMB_TC_DEBUG & 4): consumers skip the mode-2 product
     int pair;        // 1: CTA-pair kernel (cta_group::2, M = 256 over two row tiles); tiles count pairs
-    int64_t t_begin, t_end;  // tile range of this launch
+    int split;       // work items per tile in this launch (chunk ranges; > 1 only for a final partial wave)
+    int64_t tile0;   // first tile of this launch: item t is tile tile0 + t / split, part t % split
+    int64_t t_begin, t_end;  // item range of this launch
 };
 
 struct AjTile {
     int c, k, i1_0, i2_0;
     int64_t rt;  // row tile inside the component
+    int part;    // chunk range part (of g.split)
 };
 
-__device__ __forceinline__ AjTile aj_tile(const AjGeom& g, int64_t t, uint32_t rank = 0) {
+// Chunk range [n0, n1) of a work item over a tile of nc chunks.
+__device__ __forceinline__ void aj_chunks(const AjGeom& g, const AjTile& tl, int nc, int& n0, int& n1) {
+    n0 = int(int64_t(nc) * tl.part / g.split);
+    n1 = int(int64_t(nc) * (tl.part + 1) / g.split);
+}
+
+__device__ __forceinline__ AjTile aj_tile(const AjGeom& g, int64_t item, uint32_t rank = 0) {
     AjTile r;
+    const int64_t t = g.tile0 + item / g.split;
+    r.part = int(item % g.split);
     const int64_t tpk = g.nrt >> g.pair;  // (pair) tiles per component
     const int64_t per_c = int64_t(g.q) * tpk;
     r.c = int(t / per_c);
@@ -226,9 +237,10 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
             uint32_t s = 0, ph = 0;
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
                 const AjTile tl = aj_tile(g, t, rank);
-                const int nc = nch[tl.k];
+                int n0, n1;
+                aj_chunks(g, tl, nch[tl.k], n0, n1);
                 const int arow = int(tl.rt * TC_ROWS);
-                for (int n = 0; n < nc; ++n) {
+                for (int n = n0; n < n1; ++n) {
                     for (int kk = 0; kk < g.nks; ++kk) {
                         mbar_wait_backoff(&empty[s], ph ^ 1, 64);
                         unsigned char* da = sA + s * AJ_A_STAGE;
@@ -272,8 +284,9 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
             uint32_t s = 0, ph = 0, nq = 0;
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
                 const AjTile tl = aj_tile(g, t, rank);
-                const int nc = nch[tl.k];
-                for (int n = 0; n < nc; ++n, ++nq) {
+                int n0, n1;
+                aj_chunks(g, tl, nch[tl.k], n0, n1);
+                for (int n = n0; n < n1; ++n, ++nq) {
                     const uint32_t qb = nq & 1, qph = (nq >> 1) & 1;
                     mbar_wait(&qfree[qb], qph ^ 1);  // consumers are done with this buffer
                     tc_fence_after();
@@ -322,7 +335,10 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
                 const AjTile tl = aj_tile(g, t, rank);
                 const TcDesc* tdk = tcd + int64_t(tl.k) * g.ncols;
-                for (int64_t j = 0; j < g.ncols; ++j) {
+                int n0, n1;
+                aj_chunks(g, tl, nch[tl.k], n0, n1);
+                const int* cs = cstart + int64_t(tl.k) * (g.maxch + 1);
+                for (int64_t j = cs[n0]; j < cs[n1]; ++j) {
                     mbar_wait_backoff(&fempty[s], ph ^ 1, 64);
                     const TcDesc d = tdk[j];
                     unsigned char* slot = sSlot + s * g.slot_bytes;
@@ -350,11 +366,12 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         uint32_t fs = 0, fph = 0, nq = 0;
         for (int64_t t = tstart; t < g.t_end; t += tstep) {
             const AjTile tl = aj_tile(g, t, rank);
-            const int nc = nch[tl.k];
+            int n0, n1;
+            aj_chunks(g, tl, nch[tl.k], n0, n1);
             const int* cs = cstart + int64_t(tl.k) * (g.maxch + 1);
             // exact power of two: undoes the (rhs, component) Phi scale and the U3 scale
             const float inv_scale = 1.f / (aj_phi_scale(phimax[int64_t(tl.c) * g.q + tl.k]) * AJ_U3_SCALE);
-            for (int n = 0; n < nc; ++n, ++nq) {
+            for (int n = n0; n < n1; ++n, ++nq) {
                 const uint32_t qb = nq & 1, qph = (nq >> 1) & 1;
                 const int j0 = cs[n], j1 = cs[n + 1];
                 float2* rb = red + (nq & 1) * AJ_MAXCOLS * AJ_NPW;

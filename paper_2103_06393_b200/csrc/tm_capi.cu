@@ -912,9 +912,15 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     const int64_t tpb = g.nrt >> g.pair;  // tiles per (rhs, component) block
     int64_t bready = hp ? 0 : nblk;
     for (int64_t t0 = 0; t0 < g.ntiles; t0 += wave) {  // one launch per wave (see run_forward_tc)
-        g.t_begin = t0;
-        g.t_end = std::min<int64_t>(g.ntiles, t0 + wave);
-        const int64_t bneed = (g.t_end - 1) / tpb + 1;  // blocks this wave reads
+        const int64_t tiles = std::min<int64_t>(g.ntiles - t0, wave);
+        // a final partial wave splits each tile's chunk range into parts so the
+        // launch still fills the GPU (partials are per column: no extra reduction)
+        g.split = tiles < wave ? int(std::max<int64_t>(1, std::min<int64_t>(8, wave / tiles))) : 1;
+        if (const char* e = std::getenv("TMB_ADJ_NOSPLIT")) if (*e && *e != '0') g.split = 1;
+        g.tile0 = t0;
+        g.t_begin = 0;
+        g.t_end = tiles * g.split;
+        const int64_t bneed = (t0 + tiles - 1) / tpb + 1;  // blocks this wave reads
         for (; bready < bneed; ++bready) {
             CK(cudaStreamWaitEvent(st, arrived[size_t(bready)], 0));
             prepare(bready, bready + 1);
