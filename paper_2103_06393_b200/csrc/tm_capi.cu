@@ -143,6 +143,7 @@ struct tm_store {
     CUtensorMap bmap{};
     std::mutex mu;
     DevBuf part, xin, yout, wbuf, phiplanes, xplanes, rsum, scal;
+    DevBuf ypart;  // partial tiles of a split final wave of the tensor-core forward
 
     int64_t nv() const { return dims[0] * dims[1] * dims[2]; }
     int64_t rows() const { return q * nv(); }
@@ -692,9 +693,23 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     const int64_t tpb = g.ntiles / (int64_t(p) * g.q);  // tiles per (rhs, component) block
     const int64_t nv = s->nv();
     int64_t bdone = 0;
+    const int span = g.nmma * g.nh3;
     for (int64_t t0 = 0; t0 < g.ntiles; t0 += wave) {
-        g.t_begin = t0;
-        g.t_end = std::min<int64_t>(g.ntiles, t0 + wave);
+        const int64_t tiles = std::min<int64_t>(g.ntiles - t0, wave);
+        // A final partial wave splits each tile's columns into parts (partial tiles
+        // to ypart, summed by fwd_split_reduce_kernel) so the launch fills the GPU.
+        g.split = 1;
+        if (tiles < wave && tiles * 2 <= wave) {
+            g.split = int(std::min<int64_t>({int64_t(8), wave / tiles, std::max<int64_t>(1, s->ncols)}));
+            if (const char* e = std::getenv("TMB_FWD_NOSPLIT")) if (*e && *e != '0') g.split = 1;
+        }
+        g.tile0 = t0;
+        g.t_begin = 0;
+        g.t_end = tiles * g.split;
+        g.ypart = nullptr;
+        if (g.split > 1)
+            g.ypart = static_cast<float2*>(ms->ypart.get(size_t(tiles) * g.split * (1 + g.pair) * span * TC_ROWS *
+                                                         sizeof(float2)));
         if (g.pair) {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(grid);
@@ -711,14 +726,21 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
             launched(cudaLaunchKernelEx(&cfg, fwd_tc_kernel<true>, s->bmap, static_cast<const TcDesc*>(s->d_tcd),
                                         static_cast<const float2*>(s->d_varena),
                                         static_cast<const float2*>(s->d_u2arena), static_cast<const int*>(s->d_kc),
-                                        g, x, ldx, y, ldy, rsum, static_cast<const float*>(wmax)),
+                                        static_cast<const int*>(s->d_kofs), g, x, ldx, y, ldy, rsum,
+                                        static_cast<const float*>(wmax)),
                      "fwd_tc_kernel<pair>");
         } else {
             fwd_tc_kernel<false><<<grid, TC_THREADS, smem, st>>>(s->bmap, s->d_tcd, s->d_varena, s->d_u2arena,
-                                                                  s->d_kc, g, x, ldx, y, ldy, rsum, wmax);
+                                                                  s->d_kc, s->d_kofs, g, x, ldx, y, ldy, rsum, wmax);
             launched(cudaSuccess, "fwd_tc_kernel");
         }
-        const int64_t bnow = g.t_end / tpb;
+        if (g.split > 1) {
+            const int64_t n = tiles * (1 + g.pair) * span * TC_ROWS;
+            fwd_split_reduce_kernel<<<unsigned(std::min<int64_t>((n + 255) / 256, 4096)), 256, 0, st>>>(g, tiles, y,
+                                                                                                     ldy);
+            launched(cudaSuccess, "fwd_split_reduce_kernel");
+        }
+        const int64_t bnow = (t0 + tiles) / tpb;
         if (hp && bnow > bdone) {
             cudaEvent_t ev;
             CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));

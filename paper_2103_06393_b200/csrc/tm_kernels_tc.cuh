@@ -126,6 +126,10 @@ struct TcGeom {
     int debug;                  // diagnostics (TMB_TC_DEBUG): 1 = no mode-2 work, 2 = no B loads
     int pair;                   // 1: CTA-pair kernel (cta_group::2, M = 256), nt1 counts pairs of i1 blocks
     unsigned long long* prof;   // diagnostics (TMB_TC_DEBUG & 8): per-role barrier-wait cycles, else null
+    int split;                  // work items per tile in this launch (column ranges; > 1 only in a final
+                                // partial wave, whose items write partial tiles to ypart)
+    int64_t tile0;              // first tile of the launch: item t = tile tile0 + t / split, part t % split
+    float2* ypart;              // split > 1: [item][rank][span][128 rows] partial results (scaled)
     int64_t t_begin, t_end;     // tile range of this launch (one wave: see run_forward_tc)
 };
 
@@ -153,6 +157,7 @@ __host__ __device__ inline uint32_t round16(uint32_t b) { return (b + 15u) & ~15
 
 struct TcTile {
     int c, k, i1_0, i2_0, i3_0;
+    int part;  // column-range part of the tile (of g.split)
 };
 
 // Tile order: i3 block fastest, then i2 block, then i1 block, component,
@@ -160,9 +165,11 @@ struct TcTile {
 // of their i1 block (read by all n2/TI2 x n3/NMMA tiles of that block —
 // re-reading them from HBM per tile would cost ~200 GB per config-4
 // forward) and stream the same B planes of component k through L2.
-__device__ __forceinline__ TcTile tc_tile(const TcGeom& g, int64_t t, uint32_t rank = 0) {
+__host__ __device__ inline TcTile tc_tile(const TcGeom& g, int64_t item, uint32_t rank = 0) {
+    const int64_t t = g.tile0 + item / g.split;
     const int64_t per_c = int64_t(g.q) * g.nt3 * g.nt2 * g.nt1;
     TcTile r;
+    r.part = int(item % g.split);
     r.c = int(t / per_c);
     int64_t rem = t - int64_t(r.c) * per_c;
     const int64_t per_k = int64_t(g.nt3) * g.nt2 * g.nt1;
@@ -176,6 +183,24 @@ __device__ __forceinline__ TcTile tc_tile(const TcGeom& g, int64_t t, uint32_t r
     r.i2_0 = t2 * TC_TI2;
     r.i3_0 = t3 * g.nmma * g.nh3;
     return r;
+}
+
+// Column range [j0, j1) of a work item and its packed-K range [ka, kb) in
+// the component's K stream (kofs: component-major K offsets, kc: K per
+// component); the item runs stages [ka / 16, ceil(kb / 16)).
+__device__ __forceinline__ void tc_range(const TcGeom& g, const TcTile& tl, const int* __restrict__ kofs,
+                                         const int* __restrict__ kc, int& j0, int& j1, uint32_t& ka, uint32_t& kb) {
+    if (g.split == 1) {  // the common case: the whole column stream
+        j0 = 0;
+        j1 = int(g.ncols);
+        ka = 0u;
+        kb = uint32_t(kc[tl.k]);
+        return;
+    }
+    j0 = int(g.ncols * tl.part / g.split);
+    j1 = int(g.ncols * (tl.part + 1) / g.split);
+    ka = j0 == 0 ? 0u : uint32_t(kofs[int64_t(tl.k) * g.ncols + j0]);
+    kb = j1 == int(g.ncols) ? uint32_t(kc[tl.k]) : uint32_t(kofs[int64_t(tl.k) * g.ncols + j1]);
 }
 
 // Producer-side state of the A stage ring: the current (open) stage's ring
@@ -295,7 +320,7 @@ template <bool PAIR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap bmap, const TcDesc* __restrict__ tcd,
                   const float2* __restrict__ varena, const float2* __restrict__ u2arena, const int* __restrict__ kc,
-                  TcGeom g, const float2* __restrict__ x, int64_t ldx, float2* __restrict__ y, int64_t ldy,
+                  const int* __restrict__ kofs, TcGeom g, const float2* __restrict__ x, int64_t ldx, float2* __restrict__ y, int64_t ldy,
                   float2* __restrict__ rsum, const float* __restrict__ wmax) {
     using namespace sm100;
     extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
@@ -361,8 +386,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int plane_bytes = g.nmma * 32;
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
                 const TcTile tl = tc_tile(g, t, rank);
-                const int nks = (kc[tl.k] + 15) >> 4;
-                for (int kk = 0; kk < nks; ++kk) {
+                int j0, j1;
+                uint32_t ka, kb;
+                tc_range(g, tl, kofs, kc, j0, j1, ka, kb);
+                for (int kk = int(ka >> 4); kk < int((kb + 15) >> 4); ++kk) {
                     TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(&empty[s], ph ^ 1, 128)));
                     if (PAIR) {
                         // each CTA loads its half of the i3 span (B rows [rank nmma, +nmma) of the
@@ -416,7 +443,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             uint32_t s = 0, ph = 0, gch = 0;
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
                 const TcTile tl = tc_tile(g, t, rank);
-                const int nks = (kc[tl.k] + 15) >> 4;
+                int j0, j1;
+                uint32_t ka, kb;
+                tc_range(g, tl, kofs, kc, j0, j1, ka, kb);
+                const int nks = int((kb + 15) >> 4) - int(ka >> 4);
                 int cpos = 0;  // stage position inside the current chain
                 for (int kk = 0; kk < nks; ++kk) {
                     if (cpos == 0) {
@@ -475,7 +505,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
                 const TcTile tl = tc_tile(g, t, rank);
                 const TcDesc* tdk = tcd + int64_t(tl.k) * g.ncols;
-                for (int64_t j = 0; j < g.ncols; ++j) {
+                int j0, j1;
+                uint32_t ka, kb;
+                tc_range(g, tl, kofs, kc, j0, j1, ka, kb);
+                for (int j = j0; j < j1; ++j) {
                     TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(&fempty[s], ph ^ 1, 128)));
                     const TcDesc d = tdk[j];
                     unsigned char* slot = sSlot + s * g.slot_bytes;
@@ -523,12 +556,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int64_t t = tstart; t < g.t_end; t += tstep) {
             const TcTile tl = tc_tile(g, t, rank);
             const float2* xc = x + ldx * tl.c;
+            int j0, j1;
+            uint32_t ka, kb;
+            tc_range(g, tl, kofs, kc, j0, j1, ka, kb);
+            if (ka & 15u) {
+                // a column-range item starting inside a stage: its first K slots belong to
+                // the previous part's columns and are zero here
+                ring.kpos = ka & 15u;
+                TC_TWAIT(g.prof != nullptr, t_w2, (mbar_wait(&empty[ring.st], ring.ph ^ 1u)));
+                unsigned char* st = sA + ring.st * TC_A_STAGE;
+                for (uint32_t kq = uint32_t(hq); kq < ring.kpos; kq += 4)
+#pragma unroll
+                    for (int e = 0; e < TC_NR; ++e) {
+                        __half* a = reinterpret_cast<__half*>(st + rowbase[e] + ((kq * 2u) ^ xorv[e]));
+#pragma unroll
+                        for (int pl = 0; pl < 4; ++pl) a[pl * TC_A_PLANE / 2] = __float2half_rn(0.f);
+                    }
+            }
             // x_j is prefetched one column ahead: its global-load latency
             // hides behind a whole column of mode-2 work
-            float2 xn = xc[0];
-            for (int64_t j = 0; j < g.ncols; ++j) {
+            float2 xn = j0 < j1 ? xc[j0] : make_float2(0.f, 0.f);
+            for (int j = j0; j < j1; ++j) {
                 const float2 x0 = xn;
-                if (j + 1 < g.ncols) xn = xc[j + 1];
+                if (j + 1 < j1) xn = xc[j + 1];
                 const float2 xj = make_float2(x0.x * sw, x0.y * sw);
                 TC_TWAIT(g.prof, t_w, (mbar_wait(&ffull[fs], fph)));
                 const unsigned char* slot = sSlot + fs * g.slot_bytes;
@@ -595,12 +645,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         uint32_t gch = 0;
         for (int64_t t = tstart; t < g.t_end; t += tstep) {
             const TcTile tl = tc_tile(g, t, rank);
-            const int nks = (kc[tl.k] + 15) >> 4;
+            int j0, j1;
+            uint32_t ka, kb;
+            tc_range(g, tl, kofs, kc, j0, j1, ka, kb);
+            const int nks = int((kb + 15) >> 4) - int(ka >> 4);
             const int nch = (nks + g.chain - 1) / g.chain;
             const int ei1 = tl.i1_0 + quarter, ei2 = tl.i2_0 + lane;
-            const bool eok = ei1 < g.n1 && ei2 < g.n2;
-            float2* yp = y + ldy * tl.c + int64_t(tl.k) * nv3 + ei1 + int64_t(g.n1) * ei2;
-            const int64_t pl = int64_t(g.n1) * g.n2;
+            // split items write their partial tile to ypart ([item][rank][i3][row]); the wave's
+            // reduce kernel sums the parts into y in a fixed order
+            const bool part_out = g.split > 1;
+            const bool eok = part_out || (ei1 < g.n1 && ei2 < g.n2);
+            float2* yp = part_out ? g.ypart + ((t * (1 + g.pair) + int64_t(rank)) * span) * TC_ROWS + row
+                                  : y + ldy * tl.c + int64_t(tl.k) * nv3 + ei1 + int64_t(g.n1) * ei2;
+            const int64_t pl = part_out ? int64_t(TC_ROWS) : int64_t(g.n1) * g.n2;
+            const int n3lim = part_out ? span : g.n3 - tl.i3_0;  // i3 bound relative to the tile
             for (int ch = 0; ch < nch; ++ch, ++gch) {
                 TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(cfull, gch & 1, 256)));
                 tc_fence_after();
@@ -639,13 +697,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             if (eok) {
 #pragma unroll
                                 for (int m = 0; m < 8; ++m) {
-                                    const int i3 = tl.i3_0 + i3l + 2 * m;
-                                    if (i3 < g.n3)
-                                        yp[pl * i3] = make_float2((__uint_as_float(cr[2 * m]) + r[m].x) * inv,
-                                                                  (__uint_as_float(ci[2 * m]) + r[m].y) * inv);
-                                    if (i3 + 1 < g.n3)
-                                        yp[pl * (i3 + 1)] = make_float2((__uint_as_float(cr[2 * m + 1]) + r[m].z) * inv,
-                                                                        (__uint_as_float(ci[2 * m + 1]) + r[m].w) * inv);
+                                    const int i3 = i3l + 2 * m;  // relative to the tile
+                                    const int64_t o = part_out ? 0 : int64_t(tl.i3_0);
+                                    if (i3 < n3lim)
+                                        yp[pl * (o + i3)] = make_float2((__uint_as_float(cr[2 * m]) + r[m].x) * inv,
+                                                                        (__uint_as_float(ci[2 * m]) + r[m].y) * inv);
+                                    if (i3 + 1 < n3lim)
+                                        yp[pl * (o + i3 + 1)] =
+                                            make_float2((__uint_as_float(cr[2 * m + 1]) + r[m].z) * inv,
+                                                        (__uint_as_float(ci[2 * m + 1]) + r[m].w) * inv);
                                 }
                             }
                         }
@@ -679,6 +739,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tmem_dealloc_pair(tmem, 512);
         else
             tmem_dealloc(tmem, 512);
+    }
+}
+
+// Sum the column-range parts of a split final wave (fwd_tc_kernel with
+// g.split > 1) into y, in part order (deterministic).  One thread per
+// (tile, CTA rank, i3 of the span, row).
+__global__ void fwd_split_reduce_kernel(TcGeom g, int64_t tiles, float2* __restrict__ y, int64_t ldy) {
+    const int span = g.nmma * g.nh3;
+    const int nr = 1 + g.pair;
+    const int64_t total = tiles * nr * span * TC_ROWS;
+    const int64_t nv3 = int64_t(g.n1) * g.n2 * g.n3;
+    const int64_t pl = int64_t(g.n1) * g.n2;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int row = int(e % TC_ROWS);
+        int64_t rest = e / TC_ROWS;
+        const int i3l = int(rest % span);
+        rest /= span;
+        const int rank = int(rest % nr);
+        const int64_t tt = rest / nr;
+        const TcTile tl = tc_tile(g, tt * g.split, uint32_t(rank));
+        const int i1 = tl.i1_0 + row / 32, i2 = tl.i2_0 + row % 32, i3 = tl.i3_0 + i3l;
+        if (i1 >= g.n1 || i2 >= g.n2 || i3 >= g.n3) continue;
+        float2 acc = make_float2(0.f, 0.f);
+        for (int p = 0; p < g.split; ++p) {
+            const float2 v = g.ypart[(((tt * g.split + p) * nr + rank) * span + i3l) * TC_ROWS + row];
+            acc.x += v.x;
+            acc.y += v.y;
+        }
+        y[ldy * tl.c + int64_t(tl.k) * nv3 + i1 + int64_t(g.n1) * i2 + pl * i3] = acc;
     }
 }
 
