@@ -766,7 +766,6 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
         for (int r = 0; r < 5; ++r)
             std::fprintf(stderr, "[tc-prof] %-9s total %14llu  wait %-6s %14llu  wait %-5s %14llu\n", names[r], h[3 * r],
                          w1[r], h[3 * r + 1], w2[r], h[3 * r + 2]);
-        std::fprintf(stderr, "[tc-prof] producer phases: mode-2 loop %llu  scale/split/store %llu\n", h[15], h[16]);
     }
 }
 

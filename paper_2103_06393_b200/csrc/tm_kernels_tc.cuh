@@ -231,10 +231,8 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
                                                   int ld2, int r3, int hq, int i2a, float2 xj, uint64_t* fempty_s,
                                                   uint64_t* empty, uint64_t* full, unsigned char* sA,
                                                   const uint32_t (&rowbase)[TC_NR], const uint32_t (&xorv)[TC_NR],
-                                                  int lane, uint32_t nst, ARing& ring, bool prof, uint64_t& t_empty,
-                                                  uint64_t* t_phase) {
+                                                  int lane, uint32_t nst, ARing& ring, bool prof, uint64_t& t_empty) {
     using namespace sm100;
-    const long long t_in = prof ? clock64() : 0;
     uint64_t w[TC_NR][NU];
 #pragma unroll
     for (int e = 0; e < TC_NR; ++e)
@@ -265,8 +263,6 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(fempty_s);  // this warp no longer reads the slot
-    const long long t_loop = prof ? clock64() : 0;
-    if (prof) t_phase[0] += uint64_t(t_loop - t_in);
 #pragma unroll
     for (int e = 0; e < TC_NR; ++e)
 #pragma unroll
@@ -313,7 +309,6 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
         ring.ph = ph1;
     }
     ring.kpos = kend & 15u;
-    if (prof) t_phase[1] += uint64_t(clock64() - t_loop);
 }
 
 template <bool PAIR>
@@ -374,7 +369,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     // wait profile (g.prof): per role, cycles spent in barrier waits
-    uint64_t t_w = 0, t_w2 = 0, t_ph[2] = {0, 0};
+    uint64_t t_w = 0, t_w2 = 0;
     bool rec = false;
     const long long t_role = clock64();
 
@@ -588,7 +583,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
 #define TC_COL(NU)                                                                                             \
     tc_produce_column<NU, PAIR>(V, U2, (g.debug & 1) ? 0 : r2, r2 | 1, r3, hq, i2a, xj, &fempty[fs], empty, full, sA, \
-                          rowbase, xorv, lane, nst, ring, g.prof != nullptr, t_w2, t_ph)
+                          rowbase, xorv, lane, nst, ring, g.prof != nullptr, t_w2)
                 switch ((r3 + TC_NH - 1) / TC_NH) {
                     case 1: TC_COL(1); break;
                     case 2: TC_COL(2); break;
@@ -726,10 +721,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         atomicAdd(g.prof + 3 * role, static_cast<unsigned long long>(clock64() - t_role));
         atomicAdd(g.prof + 3 * role + 1, static_cast<unsigned long long>(t_w));
         atomicAdd(g.prof + 3 * role + 2, static_cast<unsigned long long>(t_w2));
-        if (role == 3) {
-            atomicAdd(g.prof + 15, static_cast<unsigned long long>(t_ph[0]));
-            atomicAdd(g.prof + 16, static_cast<unsigned long long>(t_ph[1]));
-        }
+
     }
     tc_fence_before();
     __syncthreads();
