@@ -125,7 +125,7 @@ struct TcGeom {
     int chain;                  // K stages per TMEM accumulation chain
     int debug;                  // diagnostics (TMB_TC_DEBUG): 1 = no mode-2 work, 2 = no B loads
     int pair;                   // 1: CTA-pair kernel (cta_group::2, M = 256), nt1 counts pairs of i1 blocks
-    unsigned long long* prof;   // diagnostics (TMB_TC_DEBUG & 8): per-role barrier-wait cycles, else null
+    unsigned long long* prof;   // diagnostics (TMB_TC_DEBUG & 8, builds with -DTMB_TC_PROFILE): per-role wait cycles
     int split;                  // work items per tile in this launch (column ranges; > 1 only in a final
                                 // partial wave, whose items write partial tiles to ypart)
     int64_t tile0;              // first tile of the launch: item t = tile tile0 + t / split, part t % split
@@ -143,7 +143,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 __host__ __device__ inline uint32_t round16(uint32_t b) { return (b + 15u) & ~15u; }
 
-// Barrier wait, timed into `acc` (cycles) when the wait profile is on.
+// Barrier wait, timed into `acc` (cycles) when the wait profile is on.  The
+// profile is compiled in only with -DTMB_TC_PROFILE (then TMB_TC_DEBUG=8
+// prints it): even disabled, the timing branches cost several percent in
+// the producer warps (measured).
+#ifdef TMB_TC_PROFILE
 #define TC_TWAIT(on, acc, call)                  \
     do {                                         \
         if (on) {                                \
@@ -154,6 +158,12 @@ __host__ __device__ inline uint32_t round16(uint32_t b) { return (b + 15u) & ~15
             call;                                \
         }                                        \
     } while (0)
+#else
+#define TC_TWAIT(on, acc, call) \
+    do {                        \
+        call;                   \
+    } while (0)
+#endif
 
 struct TcTile {
     int c, k, i1_0, i2_0, i3_0;
@@ -269,11 +279,11 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
         for (int u = 0; u < NU; ++u) w[e][u] = cmul2(w[e][u], xj);
     // wait for every stage (16 K) this column opens (at most two: r3 <= 16)
     const uint32_t kend = ring.kpos + uint32_t(r3);
-    if (ring.kpos == 0) TC_TWAIT(prof, t_empty, (mbar_wait(&empty[ring.st], ring.ph ^ 1u)));
+    if (ring.kpos == 0) mbar_wait(&empty[ring.st], ring.ph ^ 1u);
     if (kend > 16) {
         uint32_t s, ph;
         ring_ahead(ring, 1, nst, s, ph);
-        TC_TWAIT(prof, t_empty, (mbar_wait(&empty[s], ph ^ 1u)));
+        mbar_wait(&empty[s], ph ^ 1u);
     }
     uint32_t s1, ph1;
     ring_ahead(ring, 1, nst, s1, ph1);
@@ -716,6 +726,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
         }
     }
+#ifdef TMB_TC_PROFILE
     if (g.prof && rec) {
         const int role = warp < 3 ? warp : (warp < TC_FW0 ? 3 : 4);
         atomicAdd(g.prof + 3 * role, static_cast<unsigned long long>(clock64() - t_role));
@@ -723,6 +734,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         atomicAdd(g.prof + 3 * role + 2, static_cast<unsigned long long>(t_w2));
 
     }
+#endif
     tc_fence_before();
     __syncthreads();
     if (PAIR) cluster_sync();  // the peer no longer arrives on this CTA's barriers / uses the pair's TMEM
