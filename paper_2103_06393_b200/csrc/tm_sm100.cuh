@@ -66,10 +66,10 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // on every completed wait, and every operand the peer hands over is either
 // TMA-written or read by the peer's own tensor core after its
 // fence.proxy.async.
-template <bool CLUSTER = false>
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    const uint32_t a = smem_u32(bar);
-    if (mbar_try<CLUSTER>(a, parity)) return;
+// The polling loop lives out of line: the inlined fast path at every call
+// site is one try_wait and a branch (smaller hot loops in the warp roles).
+template <bool CLUSTER>
+__device__ __noinline__ void mbar_wait_slow(uint32_t a, uint32_t parity) {
     uint32_t n = 0;
     uint64_t t0 = 0;
     while (!mbar_try<CLUSTER>(a, parity)) {
@@ -81,6 +81,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
                 __trap();
         }
     }
+}
+template <bool CLUSTER = false>
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    if (mbar_try<CLUSTER>(a, parity)) return;
+    mbar_wait_slow<CLUSTER>(a, parity);
 }
 // Same, for waits off the critical path (ring producers far ahead, fold
 // warps between chains): back off `ns` nanoseconds between polls so the
