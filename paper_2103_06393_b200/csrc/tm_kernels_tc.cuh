@@ -241,7 +241,7 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
                                                   int ld2, int r3, int hq, int i2a, float2 xj, uint64_t* fempty_s,
                                                   uint64_t* empty, uint64_t* full, unsigned char* sA,
                                                   const uint32_t (&rowbase)[TC_NR], const uint32_t (&xorv)[TC_NR],
-                                                  int lane, uint32_t nst, ARing& ring, bool prof, uint64_t& t_empty) {
+                                                  int lane, uint32_t nst, ARing& ring) {
     using namespace sm100;
     uint64_t w[TC_NR][NU];
 #pragma unroll
@@ -379,9 +379,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     // wait profile (g.prof): per role, cycles spent in barrier waits
-    uint64_t t_w = 0, t_w2 = 0;
-    bool rec = false;
+    [[maybe_unused]] uint64_t t_w = 0, t_w2 = 0;
+    [[maybe_unused]] bool rec = false;
+#ifdef TMB_TC_PROFILE
     const long long t_role = clock64();
+#endif
 
     if (warp == 0) {
         // ------------------------------------------------ B-plane TMA producer
@@ -593,7 +595,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
 #define TC_COL(NU)                                                                                             \
     tc_produce_column<NU, PAIR>(V, U2, (g.debug & 1) ? 0 : r2, r2 | 1, r3, hq, i2a, xj, &fempty[fs], empty, full, sA, \
-                          rowbase, xorv, lane, nst, ring, g.prof != nullptr, t_w2)
+                          rowbase, xorv, lane, nst, ring)
                 switch ((r3 + TC_NH - 1) / TC_NH) {
                     case 1: TC_COL(1); break;
                     case 2: TC_COL(2); break;
