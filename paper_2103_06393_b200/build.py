@@ -58,6 +58,8 @@ def build(force=False, verbose=False, ptxas_verbose=False):
                "-fPIC,-fvisibility=hidden", *inc, "-c", os.path.join(CSRC, src), "-o", obj]
         if ptxas_verbose:
             cmd.insert(1, "-Xptxas=-v")
+        # diagnostics builds, e.g. TMB_NVCC_FLAGS=-DTMB_TC_PROFILE (forward wait profile)
+        cmd[1:1] = os.environ.get("TMB_NVCC_FLAGS", "").split()
         _run(cmd, verbose)
         objs.append(obj)
     for src in CPP_SOURCES:
