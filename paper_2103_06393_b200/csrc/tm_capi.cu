@@ -126,7 +126,7 @@ struct tm_store {
     bool tc_ok = false;
     int* d_kofs = nullptr;   // [q*ncols] component-major K offset of each tensor
     int* d_kc = nullptr;     // [q] K extent of each component
-    __half* d_planes = nullptr;
+    float vmax = 0.f;            // max per-tensor |W| bound (W = V x_2 U2): the fp16 scale of A
     float* d_vbound = nullptr;  // [q*ncols] per-tensor bound of |W| / |x_j|
     TcDesc* d_tcd = nullptr;  // [q*ncols] tensor-core descriptors
     float2* d_varena = nullptr;  // mode-1 products V = U1 x_1 G
@@ -140,7 +140,8 @@ struct tm_store {
     int64_t nslots = 0;       // slots per component (maxch * 128)
     CUtensorMap adj_bmap{};
     int64_t kpad = 0;
-    CUtensorMap bmap{};
+    DevBuf xbplanes;        // the forward's per-call B operand (build_xb_kernel)
+    size_t xb_zeroed = 0;   // bytes of xbplanes zeroed since allocation
     std::mutex mu;
     DevBuf part, xin, yout, wbuf, phiplanes, xplanes, rsum, scal;
     DevBuf ypart;  // partial tiles of a split final wave of the tensor-core forward
@@ -151,7 +152,7 @@ struct tm_store {
     ~tm_store() {
         if (d_kofs) cudaFree(d_kofs);
         if (d_kc) cudaFree(d_kc);
-        if (d_planes) cudaFree(d_planes);
+
         if (d_vbound) cudaFree(d_vbound);
         if (d_tcd) cudaFree(d_tcd);
         if (d_varena) cudaFree(d_varena);
@@ -206,7 +207,6 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
         s->kpad = std::max<int64_t>(s->kpad, (acc + 15) / 16 * 16);
     }
     const int64_t n3 = s->dims[2];
-    const size_t pbytes = size_t(TC_BPLANES) * s->q * n3 * s->kpad * sizeof(__half);
     // V arena: per tensor ceil(n1/4)*4 x r2 x r3 float2, [i1/4][c + r3 b][i1%4]
     const int64_t n1p = (s->dims[0] + 3) / 4 * 4;
     std::vector<TcDesc> tcd(static_cast<size_t>(ntens));
@@ -256,7 +256,6 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
     const size_t u2bytes = size_t(u2off) * sizeof(float2);
     CK(cudaMalloc(&s->d_kofs, kofs.size() * sizeof(int)));
     CK(cudaMalloc(&s->d_kc, kc.size() * sizeof(int)));
-    CK(cudaMalloc(&s->d_planes, pbytes));
     CK(cudaMalloc(&s->d_tcd, tcd.size() * sizeof(TcDesc)));
     CK(cudaMalloc(&s->d_varena, std::max<size_t>(vbytes, 16)));
     CK(cudaMalloc(&s->d_u2arena, std::max<size_t>(u2bytes, 16)));
@@ -282,10 +281,6 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
     CK(cudaMemcpy(s->d_kofs, kofs.data(), kofs.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(s->d_kc, kc.data(), kc.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(s->d_tcd, tcd.data(), tcd.size() * sizeof(TcDesc), cudaMemcpyHostToDevice));
-    CK(cudaMemset(s->d_planes, 0, pbytes));
-    build_bplanes_kernel<<<unsigned(ntens), 256>>>(s->d_desc, static_cast<const float2*>(s->d_arena), s->d_kofs,
-                                                   s->ncols, s->q, int(n3), s->kpad, s->d_planes);
-    launched(cudaSuccess, "build_bplanes_kernel");
     build_v_kernel<<<unsigned(ntens), 256>>>(s->d_desc, static_cast<const float2*>(s->d_arena), s->d_tcd,
                                              int(s->dims[0]), s->d_varena);
     launched(cudaSuccess, "build_v_kernel");
@@ -296,10 +291,12 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
     vbound_kernel<<<unsigned(ntens), 256>>>(s->d_desc, s->d_tcd, s->d_varena, int(s->dims[0]), s->d_vbound);
     launched(cudaSuccess, "vbound_kernel");
     CK(cudaDeviceSynchronize());
-    const uint32_t nmma = uint32_t(std::min<int64_t>((n3 + 15) / 16 * 16, TC_NMAX));
-    s->bmap = make_tmap_3d_f16(s->d_planes, uint64_t(s->kpad), uint64_t(n3), uint64_t(TC_BPLANES * s->q),
-                               uint64_t(s->kpad) * 2, uint64_t(n3) * s->kpad * 2, 16, nmma, CU_TENSOR_MAP_SWIZZLE_32B);
-    s->device_bytes += int64_t(pbytes + vbytes + u2bytes + abytes + tcd.size() * sizeof(TcDesc) + (kofs.size() + kc.size()) * sizeof(int));
+    {  // the A operand's fp16 scale: max over tensors of the |W| bound
+        std::vector<float> vb(static_cast<size_t>(ntens));
+        CK(cudaMemcpy(vb.data(), s->d_vbound, vb.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        for (float v : vb) s->vmax = std::max(s->vmax, v);
+    }
+    s->device_bytes += int64_t(vbytes + u2bytes + abytes + tcd.size() * sizeof(TcDesc) + (kofs.size() + kc.size()) * sizeof(int));
     s->tc_ok = true;
 }
 
@@ -621,20 +618,26 @@ struct HostPipe {
     int64_t ldhost = 0;
 };
 
-void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy,
-                    cudaStream_t st, const HostPipe* hp = nullptr) {
+// One pass of the tensor-core forward over pb right-hand sides: the B
+// operand x (x) U3 of the pass is built per call (build_xb_kernel) and the
+// tiles span the N space n = i3 * pb + c, so W is produced once for all
+// right-hand sides of the pass.
+void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy,
+                      cudaStream_t st, const HostPipe* hp, int64_t hc0) {
     TcGeom g{};
     g.ncols = s->ncols;
     g.n1 = int(s->dims[0]);
     g.n2 = int(s->dims[1]);
     g.n3 = int(s->dims[2]);
     g.q = s->q;
+    g.p = int(p);
+    g.nt = int(int64_t(g.n3) * p);
     g.nt1 = (g.n1 + TC_TI1 - 1) / TC_TI1;
     g.nt2 = (g.n2 + TC_TI2 - 1) / TC_TI2;
-    g.nmma = std::min(TC_NMAX, (g.n3 + 15) / 16 * 16);
-    g.nh3 = g.n3 > TC_NMAX ? 2 : 1;
-    g.nt3 = (g.n3 + g.nmma * g.nh3 - 1) / (g.nmma * g.nh3);
-    g.p = int(p);
+    g.nmma = std::min(TC_NMAX, (g.nt + 15) / 16 * 16);
+    g.nh3 = g.nt > TC_NMAX ? 2 : 1;
+    g.nt3 = (g.nt + g.nmma * g.nh3 - 1) / (g.nmma * g.nh3);
+    g.wsc = fp16_scale(s->vmax * 1.0001f);
     int dev = 0;
     CK(cudaGetDevice(&dev));
     const int nsm = num_sms(dev);
@@ -647,7 +650,7 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
         g.pair = (!(e && *e && *e != '0') && g.nmma == TC_NMAX && g.nh3 == 2 && g.nt1 % 2 == 0 && nsm >= 2) ? 1 : 0;
     }
     if (g.pair) g.nt1 /= 2;
-    g.ntiles = int64_t(p) * g.q * g.nt3 * g.nt2 * g.nt1;
+    g.ntiles = int64_t(g.q) * g.nt3 * g.nt2 * g.nt1;
     g.rmax2 = s->rmax[1];
     g.rmax3 = s->rmax[2];
     g.u2_off = TC_SLOT_V + int(round16(uint32_t(TC_TI1 * g.rmax2 * g.rmax3 * 8)));
@@ -679,18 +682,33 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     }
     tm_store* ms = const_cast<tm_store*>(s);
     float2* rsum = static_cast<float2*>(ms->rsum.get(size_t(grid) * g.nmma * g.nh3 * TC_ROWS * sizeof(float2)));
-    float* wmax = static_cast<float*>(ms->scal.get(2 * sizeof(float))) + 1;
+    // B = sb x (x) U3 for the pass (sb from max |x|), 4 fp16 planes [pl][q][nt][kpad]
+    float* wmax = static_cast<float*>(ms->scal.get(2 * sizeof(float))) + 1;  // max |x| of the pass
     CK(cudaMemsetAsync(wmax, 0, sizeof(float), st));
-    wmax_kernel<<<unsigned(std::min<int64_t>((s->ncols * p + 255) / 256, 1184)), 256, 0, st>>>(x, ldx, s->ncols, p,
-                                                                                              s->q, s->d_vbound, wmax);
-    launched(cudaSuccess, "wmax_kernel");
+    xmax_kernel<<<unsigned(std::min<int64_t>((s->ncols * p + 255) / 256, 1184)), 256, 0, st>>>(x, ldx, s->ncols, p,
+                                                                                              wmax);
+    launched(cudaSuccess, "xmax_kernel");
+    const size_t xbbytes = size_t(TC_FPLANES) * s->q * size_t(g.nt) * s->kpad * sizeof(__half);
+    void* prev = ms->xbplanes.p;
+    __half* xb = static_cast<__half*>(ms->xbplanes.get(xbbytes));
+    if (xb != prev || ms->xb_zeroed < xbbytes) {  // padding rows / K slots must hold finite values
+        CK(cudaMemsetAsync(xb, 0, ms->xbplanes.bytes, st));
+        ms->xb_zeroed = ms->xbplanes.bytes;
+    }
+    build_xb_kernel<<<unsigned(s->ncols * s->q), 256, 0, st>>>(s->d_desc, static_cast<const float2*>(s->d_arena),
+                                                              s->d_kofs, x, ldx, int(p), s->ncols, s->q, g.n3,
+                                                              int64_t(g.nt), s->kpad, wmax, xb);
+    launched(cudaSuccess, "build_xb_kernel");
+    const CUtensorMap bmap = make_tmap_3d_f16(xb, uint64_t(s->kpad), uint64_t(g.nt), uint64_t(TC_FPLANES * s->q),
+                                              uint64_t(s->kpad) * 2, uint64_t(g.nt) * s->kpad * 2, 16,
+                                              uint32_t(g.nmma), CU_TENSOR_MAP_SWIZZLE_32B);
     // One launch per wave of `grid` tiles: every CTA starts its tile at the
     // same time, so the CTAs of one component stream its B planes (184 MB
     // per component at config 4, more than L2) in K-lockstep and share them
     // in L2.  A persistent schedule over all tiles drifts apart by the
     // per-component cost differences and re-reads B from HBM (725 GB per
     // config-4 forward, measured).
-    const int64_t tpb = g.ntiles / (int64_t(p) * g.q);  // tiles per (rhs, component) block
+    const int64_t tpb = g.ntiles / g.q;  // tiles per component (all right-hand sides of the pass)
     const int64_t nv = s->nv();
     int64_t bdone = 0;
     const int span = g.nmma * g.nh3;
@@ -723,14 +741,14 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            launched(cudaLaunchKernelEx(&cfg, fwd_tc_kernel<true>, s->bmap, static_cast<const TcDesc*>(s->d_tcd),
+            launched(cudaLaunchKernelEx(&cfg, fwd_tc_kernel<true>, bmap, static_cast<const TcDesc*>(s->d_tcd),
                                         static_cast<const float2*>(s->d_varena),
                                         static_cast<const float2*>(s->d_u2arena), static_cast<const int*>(s->d_kc),
                                         static_cast<const int*>(s->d_kofs), g, x, ldx, y, ldy, rsum,
                                         static_cast<const float*>(wmax)),
                      "fwd_tc_kernel<pair>");
         } else {
-            fwd_tc_kernel<false><<<grid, TC_THREADS, smem, st>>>(s->bmap, s->d_tcd, s->d_varena, s->d_u2arena,
+            fwd_tc_kernel<false><<<grid, TC_THREADS, smem, st>>>(bmap, s->d_tcd, s->d_varena, s->d_u2arena,
                                                                   s->d_kc, s->d_kofs, g, x, ldx, y, ldy, rsum, wmax);
             launched(cudaSuccess, "fwd_tc_kernel");
         }
@@ -747,11 +765,11 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
             CK(cudaEventRecord(ev, st));
             CK(cudaStreamWaitEvent(hp->copy, ev, 0));
             CK(cudaEventDestroy(ev));
-            for (int64_t b = bdone; b < bnow; ++b) {
-                const int64_t c = b / g.q, k = b - c * g.q;
-                CK(cudaMemcpyAsync(static_cast<float2*>(hp->host) + hp->ldhost * c + k * nv, y + ldy * c + k * nv,
-                                   size_t(nv) * sizeof(float2), cudaMemcpyDeviceToHost, hp->copy));
-            }
+            for (int64_t k = bdone; k < bnow; ++k)  // component k of every right-hand side of the pass
+                for (int64_t c = 0; c < p; ++c)
+                    CK(cudaMemcpyAsync(static_cast<float2*>(hp->host) + hp->ldhost * (hc0 + c) + k * nv,
+                                       y + ldy * c + k * nv, size_t(nv) * sizeof(float2), cudaMemcpyDeviceToHost,
+                                       hp->copy));
             bdone = bnow;
         }
     }
@@ -769,11 +787,25 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     }
 }
 
+// The tensor-core forward: passes of up to pbmax right-hand sides (the B
+// operand of a pass is 4 q n3 kpad fp16 per right-hand side).
+void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy,
+                    cudaStream_t st, const HostPipe* hp = nullptr) {
+    const size_t per_rhs = size_t(TC_FPLANES) * s->q * size_t(s->dims[2]) * s->kpad * sizeof(__half);
+    const int64_t pbmax = std::max<int64_t>(1, std::min<int64_t>(p, int64_t((size_t(4) << 30) / per_rhs)));
+    for (int64_t c0 = 0; c0 < p; c0 += pbmax) {
+        const int64_t pb = std::min<int64_t>(pbmax, p - c0);
+        run_forward_pass(s, x + ldx * c0, ldx, pb, y + ldy * c0, ldy, st, hp, c0);
+    }
+}
+
 // Batched multi-RHS forward (tm_mrhs_tc.cuh) for c64 stores at p >= 3,
 // in blocks of MR_P right-hand sides.
+// The older batched forward (tm_mrhs_tc.cuh) only on request: the x-in-B
+// tensor-core forward shares W across right-hand sides itself.
 bool mrhs_ok(const tm_store* s, int64_t p) {
-    const char* e = std::getenv("TMB_DISABLE_MRHS");
-    if (e && e[0] == '1') return false;
+    const char* e = std::getenv("TMB_USE_MRHS");
+    if (!(e && e[0] == '1')) return false;
     return s->tc_ok && p >= 3;
 }
 

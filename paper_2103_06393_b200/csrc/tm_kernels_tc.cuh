@@ -115,7 +115,9 @@ struct TcGeom {
     int nt1, nt2, nt3;
     int nmma;       // i3 per half tile = N of the narrow MMAs (multiple of 16, <= 128)
     int nh3;        // i3 halves per tile (1 or 2): a tile spans nh3 * nmma voxels along mode 3
-    int p;          // right-hand sides
+    int p;          // right-hand sides of this pass (B rows n = i3 * p + c)
+    int nt;         // B rows = n3 * p: the N space the tiles span (nt3 tiles of nmma * nh3 rows)
+    float wsc;      // fp16 scale of W (power of two from the store's max vbound)
     int64_t ntiles;
     int rmax2, rmax3;
     int slot_bytes;             // factor slot size (multiple of 128)
@@ -177,11 +179,10 @@ struct TcTile {
 // forward) and stream the same B planes of component k through L2.
 __host__ __device__ inline TcTile tc_tile(const TcGeom& g, int64_t item, uint32_t rank = 0) {
     const int64_t t = g.tile0 + item / g.split;
-    const int64_t per_c = int64_t(g.q) * g.nt3 * g.nt2 * g.nt1;
     TcTile r;
     r.part = int(item % g.split);
-    r.c = int(t / per_c);
-    int64_t rem = t - int64_t(r.c) * per_c;
+    r.c = 0;  // the right-hand sides live in the N space (B rows n = i3 * p + c)
+    int64_t rem = t;
     const int64_t per_k = int64_t(g.nt3) * g.nt2 * g.nt1;
     r.k = int(rem / per_k);
     rem -= int64_t(r.k) * per_k;
@@ -238,7 +239,7 @@ __device__ __forceinline__ void ring_ahead(const ARing& r, uint32_t i, uint32_t 
 // conflict-free, one wavefront.  NU = ceil(r3/4).
 template <int NU, bool PAIR>
 __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, const float2* __restrict__ U2, int r2,
-                                                  int ld2, int r3, int hq, int i2a, float2 xj, uint64_t* fempty_s,
+                                                  int ld2, int r3, int hq, int i2a, float wsc, uint64_t* fempty_s,
                                                   uint64_t* empty, uint64_t* full, unsigned char* sA,
                                                   const uint32_t (&rowbase)[TC_NR], const uint32_t (&xorv)[TC_NR],
                                                   int lane, uint32_t nst, ARing& ring) {
@@ -273,10 +274,12 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(fempty_s);  // this warp no longer reads the slot
+    // W x wsc (x_j lives in the B operand: build_xb_kernel)
+    const uint64_t sc2 = f2_pack(wsc, wsc);
 #pragma unroll
     for (int e = 0; e < TC_NR; ++e)
 #pragma unroll
-        for (int u = 0; u < NU; ++u) w[e][u] = cmul2(w[e][u], xj);
+        for (int u = 0; u < NU; ++u) asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(w[e][u]) : "l"(sc2));
     // wait for every stage (16 K) this column opens (at most two: r3 <= 16)
     const uint32_t kend = ring.kpos + uint32_t(r3);
     if (ring.kpos == 0) mbar_wait(&empty[ring.st], ring.ph ^ 1u);
@@ -413,20 +416,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
                             for (int pl = 0; pl < TC_FPLANES; ++pl)
                                 tma_load_3d_pair(dst + pl * plane_bytes, &bmap, fb, kk * 16,
-                                                 tl.i3_0 + int(rank) * g.nmma, (1 + pl + (pl >> 1)) * g.q + tl.k);
+                                                 tl.i3_0 + int(rank) * g.nmma, pl * g.q + tl.k);
                         }
                     } else if (g.debug & 2) {
                         mbar_arrive(&full[s]);
                     } else {
                         mbar_arrive_expect_tx(&full[s], uint32_t(g.b_stage));
                         unsigned char* dst = sB + s * g.b_stage;
-                        // smem plane pl = (U3r hi, U3i hi, U3r lo, U3i lo) holds both i3 halves
-                        // contiguously ([pl][hh][nmma rows]): HBM planes 1, 2, 4, 5
+                        // smem plane pl = (Br hi, Bi hi, Br lo, Bi lo) holds both halves of the
+                        // tile's N rows contiguously ([pl][hh][nmma rows])
                         for (int hh = 0; hh < g.nh3; ++hh)
 #pragma unroll
                             for (int pl = 0; pl < TC_FPLANES; ++pl)
                                 tma_load_3d(dst + (pl * g.nh3 + hh) * plane_bytes, &bmap, &full[s], kk * 16,
-                                            tl.i3_0 + hh * g.nmma, (1 + pl + (pl >> 1)) * g.q + tl.k);
+                                            tl.i3_0 + hh * g.nmma, pl * g.q + tl.k);
                     }
                     if (++s == nst) {
                         s = 0;
@@ -559,10 +562,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         ARing ring{0, 0, 0};
         uint32_t fs = 0, fph = 0;
-        const float sw = fp16_scale(*wmax);  // W x sw fits fp16 (wmax bounds |W| over the store)
         for (int64_t t = tstart; t < g.t_end; t += tstep) {
             const TcTile tl = tc_tile(g, t, rank);
-            const float2* xc = x + ldx * tl.c;
             int j0, j1;
             uint32_t ka, kb;
             tc_range(g, tl, kofs, kc, j0, j1, ka, kb);
@@ -580,13 +581,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         for (int pl = 0; pl < 4; ++pl) a[pl * TC_A_PLANE / 2] = __float2half_rn(0.f);
                     }
             }
-            // x_j is prefetched one column ahead: its global-load latency
-            // hides behind a whole column of mode-2 work
-            float2 xn = j0 < j1 ? xc[j0] : make_float2(0.f, 0.f);
             for (int j = j0; j < j1; ++j) {
-                const float2 x0 = xn;
-                if (j + 1 < j1) xn = xc[j + 1];
-                const float2 xj = make_float2(x0.x * sw, x0.y * sw);
                 TC_TWAIT(g.prof, t_w, (mbar_wait(&ffull[fs], fph)));
                 const unsigned char* slot = sSlot + fs * g.slot_bytes;
                 const int r2 = reinterpret_cast<const TcDesc*>(slot)->r2;
@@ -594,7 +589,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const float2* V = reinterpret_cast<const float2*>(slot + TC_SLOT_V) + i1l;
                 const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
 #define TC_COL(NU)                                                                                             \
-    tc_produce_column<NU, PAIR>(V, U2, (g.debug & 1) ? 0 : r2, r2 | 1, r3, hq, i2a, xj, &fempty[fs], empty, full, sA, \
+    tc_produce_column<NU, PAIR>(V, U2, (g.debug & 1) ? 0 : r2, r2 | 1, r3, hq, i2a, g.wsc, &fempty[fs], empty, full, sA, \
                           rowbase, xorv, lane, nst, ring)
                 switch ((r3 + TC_NH - 1) / TC_NH) {
                     case 1: TC_COL(1); break;
@@ -648,7 +643,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int span = g.nmma * g.nh3;
         float4* rs = reinterpret_cast<float4*>(rsum) + int64_t(blockIdx.x) * (span / 2) * TC_ROWS + row;
         const int64_t nv3 = int64_t(g.n1) * g.n2 * g.n3;
-        const float inv = 1.f / (fp16_scale(*wmax) * TC_U3_SCALE);  // exact power of two
+        const float inv = 1.f / (g.wsc * fp16_scale(*wmax));  // exact power of two (W scale x B scale)
         uint32_t gch = 0;
         for (int64_t t = tstart; t < g.t_end; t += tstep) {
             const TcTile tl = tc_tile(g, t, rank);
@@ -663,9 +658,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const bool part_out = g.split > 1;
             const bool eok = part_out || (ei1 < g.n1 && ei2 < g.n2);
             float2* yp = part_out ? g.ypart + ((t * (1 + g.pair) + int64_t(rank)) * span) * TC_ROWS + row
-                                  : y + ldy * tl.c + int64_t(tl.k) * nv3 + ei1 + int64_t(g.n1) * ei2;
-            const int64_t pl = part_out ? int64_t(TC_ROWS) : int64_t(g.n1) * g.n2;
-            const int n3lim = part_out ? span : g.n3 - tl.i3_0;  // i3 bound relative to the tile
+                                  : y + int64_t(tl.k) * nv3 + ei1 + int64_t(g.n1) * ei2;
+            const int64_t pl = int64_t(g.n1) * g.n2;
+            // output of tile column nl (N row n = i3_0 + nl = i3 * p + c)
+            auto put = [&](int nl, float2 v) {
+                if (part_out) {
+                    yp[int64_t(TC_ROWS) * nl] = v;
+                    return;
+                }
+                const int n = tl.i3_0 + nl;
+                if (n >= g.nt) return;
+                int i3 = n, c = 0;
+                if (g.p > 1) {
+                    i3 = n / g.p;
+                    c = n - i3 * g.p;
+                }
+                yp[ldy * c + pl * i3] = v;
+            };
             for (int ch = 0; ch < nch; ++ch, ++gch) {
                 TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(cfull, gch & 1, 256)));
                 tc_fence_after();
@@ -704,15 +713,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             if (eok) {
 #pragma unroll
                                 for (int m = 0; m < 8; ++m) {
-                                    const int i3 = i3l + 2 * m;  // relative to the tile
-                                    const int64_t o = part_out ? 0 : int64_t(tl.i3_0);
-                                    if (i3 < n3lim)
-                                        yp[pl * (o + i3)] = make_float2((__uint_as_float(cr[2 * m]) + r[m].x) * inv,
-                                                                        (__uint_as_float(ci[2 * m]) + r[m].y) * inv);
-                                    if (i3 + 1 < n3lim)
-                                        yp[pl * (o + i3 + 1)] =
-                                            make_float2((__uint_as_float(cr[2 * m + 1]) + r[m].z) * inv,
-                                                        (__uint_as_float(ci[2 * m + 1]) + r[m].w) * inv);
+                                    put(i3l + 2 * m, make_float2((__uint_as_float(cr[2 * m]) + r[m].x) * inv,
+                                                                 (__uint_as_float(ci[2 * m]) + r[m].y) * inv));
+                                    put(i3l + 2 * m + 1, make_float2((__uint_as_float(cr[2 * m + 1]) + r[m].z) * inv,
+                                                                     (__uint_as_float(ci[2 * m + 1]) + r[m].w) * inv));
                                 }
                             }
                         }
@@ -748,6 +752,53 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
 }
 
+// max |x[j, c]| over the columns and right-hand sides of a pass (the fp16
+// scale of the B operand), by an order-free atomicMax on float bit patterns.
+__global__ void xmax_kernel(const float2* __restrict__ x, int64_t ldx, int64_t ncols, int64_t p, float* __restrict__ out) {
+    float m = 0.f;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < ncols * p; e += int64_t(gridDim.x) * blockDim.x) {
+        const float2 v = x[(e % ncols) + ldx * (e / ncols)];
+        m = fmaxf(m, sqrtf(v.x * v.x + v.y * v.y));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned int*>(out), __float_as_uint(m));
+}
+
+// The forward's B operand for a pass of p right-hand sides:
+// B[k][n = i3 p + c][K = kofs[k][j] + r] = sb x[j, c] U3_j[i3, r] as a 2-term
+// fp16 split in 4 planes [Re hi, Im hi, Re lo, Im lo][q][nt][kpad] (sb =
+// fp16_scale(max |x|); |U3| <= 1).  x_j rides in B so the producers' A
+// operand is x-free and, with p > 1, W = V x_2 U2 is produced once for all
+// right-hand sides (they share the tile's N space).  One block per tensor.
+__global__ void build_xb_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena,
+                                const int* __restrict__ kofs, const float2* __restrict__ x, int64_t ldx, int p,
+                                int64_t ncols, int q, int n3, int64_t nt, int64_t kpad, const float* __restrict__ xmax,
+                                __half* __restrict__ planes) {
+    const int64_t t = blockIdx.x;  // tensor index k*ncols + j
+    const int k = int(t / ncols);
+    const int64_t j = t - int64_t(k) * ncols;
+    const TDesc d = td[t];
+    const int64_t k0 = kofs[t];
+    const int64_t plane = int64_t(q) * nt * kpad;
+    const float sb = fp16_scale(*xmax);
+    for (int e = threadIdx.x; e < n3 * d.r3 * p; e += blockDim.x) {
+        const int c = e / (n3 * d.r3);
+        const int rem = e - c * (n3 * d.r3);
+        const int i3 = rem / d.r3, r = rem - i3 * d.r3;
+        const float2 u = arena[d.off_u3 + rem];
+        const float2 xv = x[j + ldx * c];
+        const float br = (xv.x * u.x - xv.y * u.y) * sb, bi = (xv.x * u.y + xv.y * u.x) * sb;
+        const __half rh = __float2half_rn(br), ih = __float2half_rn(bi);
+        const __half rl = __float2half_rn(br - __half2float(rh)), il = __float2half_rn(bi - __half2float(ih));
+        const int64_t o = (int64_t(k) * nt + int64_t(i3) * p + c) * kpad + k0 + r;
+        planes[o] = rh;
+        planes[plane + o] = ih;
+        planes[2 * plane + o] = rl;
+        planes[3 * plane + o] = il;
+    }
+}
+
 // Sum the column-range parts of a split final wave (fwd_tc_kernel with
 // g.split > 1) into y, in part order (deterministic).  One thread per
 // (tile, CTA rank, i3 of the span, row).
@@ -765,15 +816,16 @@ __global__ void fwd_split_reduce_kernel(TcGeom g, int64_t tiles, float2* __restr
         const int rank = int(rest % nr);
         const int64_t tt = rest / nr;
         const TcTile tl = tc_tile(g, tt * g.split, uint32_t(rank));
-        const int i1 = tl.i1_0 + row / 32, i2 = tl.i2_0 + row % 32, i3 = tl.i3_0 + i3l;
-        if (i1 >= g.n1 || i2 >= g.n2 || i3 >= g.n3) continue;
+        const int i1 = tl.i1_0 + row / 32, i2 = tl.i2_0 + row % 32, n = tl.i3_0 + i3l;
+        if (i1 >= g.n1 || i2 >= g.n2 || n >= g.nt) continue;
+        const int i3 = n / g.p, c = n - (n / g.p) * g.p;
         float2 acc = make_float2(0.f, 0.f);
         for (int p = 0; p < g.split; ++p) {
             const float2 v = g.ypart[(((tt * g.split + p) * nr + rank) * span + i3l) * TC_ROWS + row];
             acc.x += v.x;
             acc.y += v.y;
         }
-        y[ldy * tl.c + int64_t(tl.k) * nv3 + i1 + int64_t(g.n1) * i2 + pl * i3] = acc;
+        y[ldy * c + int64_t(tl.k) * nv3 + i1 + int64_t(g.n1) * i2 + pl * i3] = acc;
     }
 }
 
