@@ -510,8 +510,8 @@ __global__ void __launch_bounds__(256) adj_split_phi_kernel(const float2* __rest
 
 // U3 planes for the adjoint: [pl][k][slot][n3p] fp16 (i3-contiguous), slot
 // = chunk * 128 + offset of the (j, c) pair inside its chunk; values scaled
-// by AJ_U3_SCALE, 2-term fp16 split, in the 6-plane order of
-// build_bplanes_kernel (-U3i, U3r, U3i hi; the same lo).
+// by AJ_U3_SCALE, 2-term fp16 split, in the 6-plane order
+// (-U3i, U3r, U3i hi; the same lo): the windows [-U3i|U3r] and [U3r|U3i].
 __global__ void build_adj_bplanes_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena,
                                          const int* __restrict__ aslot, int64_t ncols, int q, int n3, int n3p,
                                          int64_t nslots, __half* __restrict__ planes) {

@@ -1,28 +1,29 @@
-// Tensor-core (tcgen05, kind::tf32, 3xTF32 split) forward kernel, complex64.
+// Tensor-core (tcgen05, kind::f16, 2-term fp16 split) forward kernel, complex64.
 //
 // Forward of component k, for one output tile of ROWS = 128 voxel rows
-// (TI1 x TI2 = 4 x 32 of (i1, i2)) times up to 2 x 128 voxels along mode 3:
+// (TI1 x TI2 = 4 x 32 of (i1, i2)) times up to 2 x 128 rows of the N space
+// n = i3 * p + c (voxels along mode 3 times the right-hand sides of the pass):
 //
-//   Y[row, i3] = sum_j sum_r W_j[row, r] U3_j[i3, r],
-//   W_j[row, r] = sum_b V_j[i1, b, r] U2_j[i2, b],  V_j = x_j (U1_j x_1 G_j),
+//   Y[row, n] = sum_j sum_r W_j[row, r] B_j[n, r],
+//   W_j[row, r] = sum_b V_j[i1, b, r] U2_j[i2, b],   V_j = U1_j x_1 G_j,
+//   B_j[i3 p + c, r] = x[j, c] U3_j[i3, r],
 //
 // i.e. one GEMM with K = the packed (j, r) stream of component k
 // (K = sum_j r3_j, no per-column padding) — the reference's stacked_forward
-// (src/matvec.cpp:17-65) with reconstruct's three mode products
-// (src/tensor.cpp:89-120,176-181) restricted to the tile.  The B operand
-// (U3 of every column, concatenated along K) is pre-split at store creation
-// into four fp32 planes {Re hi, Re lo, Im hi, Im lo} (hi = tf32(x),
-// lo = tf32(x - hi)), laid out [plane][k][i3][K] and streamed by TMA
-// (SWIZZLE_32B, 8 K per stage; see build_bplanes_kernel for the 6-plane
-// complex-as-real layout).  The mode-1 products V_j = U1_j x_1 G_j are
-// formed once per store (build_v_kernel; per tile they would be recomputed
-// n2/TI2 x n3/NMMA times).  The A operand W is produced on the fly by 8
-// producer warps (FFMA2 mode-2 products) into the same four-plane split in
-// shared memory (hi = W with the low 13 mantissa bits cleared, lo = W - hi),
-// so no decompressed column is ever written anywhere.  Per 8-wide K step the
-// MMA warp issues 12 tcgen05.mma (M=128, N=NMMA, K=8):
+// (src/matvec.cpp:17-65) with reconstruct's mode products (src/tensor.cpp:
+// 89-120,176-181) restricted to the tile and the rank-1 updates folded into
+// B.  B is built per call (build_xb_kernel) as a scaled 2-term fp16 split
+// in four planes {Re hi, Im hi, Re lo, Im lo} [plane][k][n][K] and streamed
+// by TMA (SWIZZLE_32B, 16 K per stage).  The mode-1 products V_j are formed
+// once per store (build_v_kernel).  The A operand W is produced on the fly
+// by 8 producer warps (FFMA2 mode-2 products, scaled into fp16 range) into
+// the same four-plane split in shared memory, so no decompressed column is
+// ever written anywhere; with p > 1 one W serves every right-hand side.
+// Per 16-wide K step the MMA warp issues 12 tcgen05.mma of N = 256:
 //   Yr += Ar.Br - Ai.Bi,  Yi += Ar.Bi + Ai.Br,  each product as
-//   hi.hi + hi.lo + lo.hi (3xTF32) and the minus sign via the idesc negate-A bit.
+//   hi.hi + hi.lo + lo.hi and the minus sign via the idesc negate-A bit.
+// PAIR: clusters of 2 CTAs run M = 256 cta_group::2 MMAs over two i1
+// blocks, each CTA holding half of the tile's N rows of B.
 //
 // Accuracy: the tensor core's fp32 accumulate truncates, so one TMEM
 // accumulator over the whole K stream (~45 000 terms per component at
@@ -33,22 +34,21 @@
 // global memory (L2-resident, [i3][row] so the fold is coalesced; the CTA
 // owns its tile, so the fold is deterministic); the tile's last chain is
 // added to the running sum on its way to y.  The error is then set by the
-// chain length, not by K.  Keeping the running sum out of TMEM lets a tile
-// span 2 x 128 voxels along mode 3 (all 512 TMEM columns hold [Yr|Yi] of
-// the two halves), so each produced W element feeds twice the MMA work.
+// chain length, not by K.  All 512 TMEM columns hold [Yr|Yi] of the 256-row
+// N span, so each produced W element feeds 256 columns of MMA work.
 //
 // Warp roles (512 threads, 1 CTA / SM, persistent over tiles):
 //   warp 0      TMA producer of the B planes
-//   warp 1      MMA issuer (one elected thread)
+//   warp 1      MMA issuer (one elected thread; the even CTA of a pair)
 //   warp 2      factor loader: per column, bulk-copies {TcDesc, V rows,
 //               U2 rows} of the tile into a 3-deep shared-memory ring
 //   warp 3      TMEM allocator
-//   warps 4-11  A producers (mode-2 W, x_j scale, hi/lo split)
+//   warps 4-11  A producers (mode-2 W, scale, hi/lo split)
 //   warps 12-15 chain fold + epilogue (TMEM -> registers -> y)
-// Pipelines: A/B stage ring (full: 1 TMA arrive+tx + 8 producer-warp
-// arrivals; empty: tcgen05.commit), factor ring (full: bulk-copy tx; empty:
-// 8 producer warps), chain (full: commit after the chain's last K step;
-// free: 4 fold warps).
+// Pipelines: A/B stage ring (full: 1 TMA arrive+tx + the producer-warp
+// arrivals of both CTAs; empty: tcgen05.commit), factor ring (full:
+// bulk-copy tx; empty: 8 producer warps), chain (full: commit after the
+// chain's last K step; free: the fold warps of both CTAs).
 #pragma once
 
 #include <cuda_fp16.h>
@@ -89,8 +89,8 @@ constexpr int TC_A_PLANE = TC_ROWS * 32;     // bytes (128 rows x 16 fp16 = one 
 constexpr int TC_A_STAGE = 4 * TC_A_PLANE;   // 16 KB
 constexpr uint32_t TC_RUN_COL = 256;         // TMEM column of the running sum
 constexpr int TC_SLOT_V = 128;               // byte offset of the V block in a factor slot
-constexpr int TC_BPLANES = 6;                // B planes in HBM: [-U3i, U3r, U3i] x {hi, lo}
-constexpr int TC_FPLANES = 4;                // forward B planes per stage: [U3r, U3i] x {hi, lo}
+constexpr int TC_BPLANES = 6;                // adjoint B planes in HBM: [-U3i, U3r, U3i] x {hi, lo}
+constexpr int TC_FPLANES = 4;                // forward B planes: [Br, Bi] x {hi, lo}
 
 // Per-tensor descriptor of the tensor-core forward (component-major like
 // TDesc).  off_v: float2 offset of the tensor's mode-1 product
@@ -860,33 +860,6 @@ __global__ void build_v_kernel(const TDesc* __restrict__ td, const float2* __res
     }
 }
 
-// ------------------------------------------------- store-side B planes (K6')
-// planes[p][k][i3][K] fp16, K = kofs[k][j] + r, values U3 x TC_U3_SCALE in
-// the order 0: -U3i hi, 1: U3r hi, 2: U3i hi, 3: -U3i lo, 4: U3r lo,
-// 5: U3i lo (2-term fp16 split).  The forward streams planes 1, 2, 4, 5.
-__global__ void build_bplanes_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena,
-                                     const int* __restrict__ kofs, int64_t ncols, int q, int n3, int64_t kpad,
-                                     __half* __restrict__ planes) {
-    const int64_t t = blockIdx.x;  // tensor index k*ncols + j
-    const int k = int(t / ncols);
-    const TDesc d = td[t];
-    const int64_t k0 = kofs[t];
-    const int64_t plane = int64_t(q) * n3 * kpad;
-    for (int e = threadIdx.x; e < n3 * d.r3; e += blockDim.x) {
-        const int i3 = e / d.r3, r = e - i3 * d.r3;
-        const float2 u0 = arena[d.off_u3 + e];
-        const float2 u = make_float2(u0.x * TC_U3_SCALE, u0.y * TC_U3_SCALE);
-        const __half rh = __float2half_rn(u.x), ih = __float2half_rn(u.y);
-        const __half rl = __float2half_rn(u.x - __half2float(rh)), il = __float2half_rn(u.y - __half2float(ih));
-        const int64_t o = (int64_t(k) * n3 + i3) * kpad + k0 + r;
-        planes[o] = __hneg(ih);
-        planes[plane + o] = rh;
-        planes[2 * plane + o] = ih;
-        planes[3 * plane + o] = __hneg(il);
-        planes[4 * plane + o] = rl;
-        planes[5 * plane + o] = il;
-    }
-}
 
 // Per tensor: max over (i1, c) of the 2-norm over b of V[i1, b, c] — a
 // bound on |W[row, c]| / |x_j| because every row of U2 has norm <= 1.
@@ -918,23 +891,6 @@ __global__ void vbound_kernel(const TDesc* __restrict__ td, const TcDesc* __rest
     (void)td;
 }
 
-// wmax = max over (k, j, c) of |x[j, c]| * vbound[k ncols + j] (atomicMax on
-// the bits of non-negative floats: order-free).
-__global__ void wmax_kernel(const float2* __restrict__ x, int64_t ldx, int64_t ncols, int64_t p, int q,
-                            const float* __restrict__ vbound, float* __restrict__ out) {
-    float m = 0.f;
-    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < ncols * p; e += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t j = e % ncols, c = e / ncols;
-        const float2 xv = x[j + ldx * c];
-        const float ax = sqrtf(xv.x * xv.x + xv.y * xv.y);
-        float vb = 0.f;
-        for (int k = 0; k < q; ++k) vb = fmaxf(vb, vbound[int64_t(k) * ncols + j]);
-        m = fmaxf(m, ax * vb * 1.0001f);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned int*>(out), __float_as_uint(m));
-}
 
 // ------------------------------------------------ store-side U2 arena (K6 U2)
 // U2 of every tensor with an odd row stride r2 | 1 and n2 rounded up to TI2
