@@ -792,7 +792,9 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
 void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy,
                     cudaStream_t st, const HostPipe* hp = nullptr) {
     const size_t per_rhs = size_t(TC_FPLANES) * s->q * size_t(s->dims[2]) * s->kpad * sizeof(__half);
-    const int64_t pbmax = std::max<int64_t>(1, std::min<int64_t>(p, int64_t((size_t(4) << 30) / per_rhs)));
+    size_t cap = size_t(4) << 30;  // B-operand budget per pass (TMB_XB_CAP_MB overrides, e.g. for tests)
+    if (const char* e = std::getenv("TMB_XB_CAP_MB")) if (std::atoll(e) > 0) cap = size_t(std::atoll(e)) << 20;
+    const int64_t pbmax = std::max<int64_t>(1, std::min<int64_t>(p, int64_t(cap / per_rhs)));
     for (int64_t c0 = 0; c0 < p; c0 += pbmax) {
         const int64_t pb = std::min<int64_t>(pbmax, p - c0);
         run_forward_pass(s, x + ldx * c0, ldx, pb, y + ldy * c0, ldy, st, hp, c0);

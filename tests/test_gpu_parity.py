@@ -269,6 +269,25 @@ def test_cta_pair_kernels(oracle, product, monkeypatch, dims, q, m, rmin, rmax, 
     assert rel(y2, y1) <= 1e-6 and rel(z2, z1) <= 1e-6
 
 
+def test_forward_rhs_passes(oracle, product, monkeypatch):
+    """The x-in-B forward over several right-hand-side passes (a B-operand
+    budget smaller than one pass of all p), host and device I/O, against
+    the oracle and against the single-pass result."""
+    O, P = oracle, product
+    cc = ragged_store((20, 36, 140), 2, 13, 2, 11, seed=29)
+    ref = O.OracleStore(cc.rounded_c64())
+    ds = P.DeviceStore.from_compressed(cc, "c64")
+    x = cn01(cc.m, 7, 31).astype(np.complex64).astype(np.complex128)
+    y1 = ds.forward(x)
+    monkeypatch.setenv("TMB_XB_CAP_MB", "1")  # ~1 MB: one right-hand side per pass here
+    y2 = ds.forward(x)
+    monkeypatch.delenv("TMB_XB_CAP_MB")
+    y_ref = ref.forward(x)
+    assert rel(y1, y_ref) <= 1e-5
+    assert rel(y2, y_ref) <= 1e-5
+    assert rel(y2, y1) <= 1e-6
+
+
 @pytest.mark.parametrize("chain", ["", "1", "3", "48"])
 def test_tensor_core_long_k(product, monkeypatch, chain):
     """Accumulation over a long K stream (2 500 columns, K ~ 21 000 per
