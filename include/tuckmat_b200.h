@@ -46,6 +46,7 @@ typedef enum {
     TM_CONTRACT_VIOLATION = 1, /* tuckmat::ContractViolation  (errors.hpp:16-19) */
     TM_CAPACITY_ERROR = 2,     /* tuckmat::CapacityError      (errors.hpp:27-30) */
     TM_PARSE_ERROR = 3,        /* tuckmat::ParseError         (errors.hpp:39-45) */
+    TM_SINGULARITY_ERROR = 4,  /* tuckmat::SingularityError   (errors.hpp:21-24) */
     TM_CUDA_ERROR = 6,         /* device / driver failure (no reference analogue) */
     TM_ERROR = 9               /* tuckmat::Error              (errors.hpp:10-13) */
 } tm_status;
@@ -120,6 +121,18 @@ TM_API int tm_aca_forward(tm_store* s, const void* x, int64_t ldx, int64_t xrows
                           int where, void* stream);
 TM_API int tm_aca_adjoint(tm_store* s, const void* phi, int64_t ldphi, int64_t phirows, int64_t p, void* z,
                           int64_t ldz, int where, void* stream);
+
+/* assemble_column (src/scene.cpp:127-150) for a batch of source columns on
+ * the device (complex128), the field evaluation of the GPU compressor:
+ * origin3 / spacing / dims3 the voxel grid, q = 3 (PWC) or 12 (PWL moments),
+ * op = 0 (E-field, src/scene.cpp:84-103) or 1 (H-field, :105-118), k0 the
+ * wavenumber; src a device array of m x 7 doubles {midpoint xyz, unit
+ * direction xyz, weight}; cols a host array of nb column indices; out a
+ * device array of nb x q x n_v complex128 (component-major rows, voxel
+ * f1-fastest).  TM_SINGULARITY_ERROR if an evaluation point hits a source. */
+TM_API int tm_assemble_columns(const double* origin3, double spacing, const int64_t* dims3, int q, int op, double k0,
+                               const double* src, int64_t m, const int64_t* cols, int64_t nb, void* out,
+                               void* stream);
 
 /* Rows of the stored operator at the requested global rows (host array,
  * rows[r] = k*n_v + v, v = i1 + n1*(i2 + n2*i3)): out[r + ldout*j] =

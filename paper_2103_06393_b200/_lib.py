@@ -17,12 +17,14 @@ if os.environ.get("TMB_LIB_VARIANT"):
     LIB_PATH = os.path.join(HERE, "libtuckmat_b200_%s.so" % os.environ["TMB_LIB_VARIANT"])
 
 TM_OK, TM_CONTRACT_VIOLATION, TM_CAPACITY_ERROR, TM_PARSE_ERROR, TM_CUDA_ERROR, TM_ERROR = 0, 1, 2, 3, 6, 9
+TM_SINGULARITY_ERROR = 4
 TM_C64, TM_C128 = 0, 1
 TM_HOST, TM_DEVICE = 0, 1
 
 EXPORTED = [
     "tm_store_create", "tm_store_load_ctc1", "tm_store_load_cta1", "tm_store_destroy", "tm_store_info",
     "tm_forward", "tm_adjoint", "tm_aca_forward", "tm_aca_adjoint", "tm_opcounts", "tm_rows", "tm_last_error",
+    "tm_assemble_columns",
     "tm_launch_count", "tm_version",
 ]
 
@@ -67,6 +69,8 @@ def lib():
             L.tm_aca_adjoint.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp]
             L.tm_opcounts.argtypes = [vp, i64, vp, vp]
             L.tm_rows.argtypes = [vp, vp, i64, vp, i64, i32, vp]
+            L.tm_assemble_columns.argtypes = [vp, ctypes.c_double, vp, i32, i32, ctypes.c_double, vp, i64, vp, i64,
+                                              vp, vp]
             L.tm_last_error.restype = ctypes.c_char_p
             L.tm_launch_count.restype = ctypes.c_int64
             _lib = L

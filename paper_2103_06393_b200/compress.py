@@ -6,10 +6,10 @@ assemble_column (src/scene.cpp:127-150, kernels :84-118) and hosvd
 store straight into HBM (or a CTC1 file, src/io.cpp:121-210).
 
 * Assembly: the E-/H-field kernels evaluated for a batch of columns over all
-  voxel centres in complex128 (q = 3: the reference's point-collocated
-  piecewise-constant column; q = 12: this build's piecewise-linear stand-in,
-  2x2x2 Gauss moments against {1, x~, y~, z~} — the same definition as the
-  oracle's voxel_field).
+  voxel centres in complex128 by a CUDA kernel (tm_assemble_columns; q = 3:
+  the reference's point-collocated piecewise-constant column; q = 12: this
+  build's piecewise-linear stand-in, 2x2x2 Gauss moments against
+  {1, x~, y~, z~} — the same definition as the oracle's voxel_field).
 * HOSVD: per tensor and mode g, the Gram matrix A_g A_g^H of the mode-g
   unfolding (n_g x n_g, cuBLAS zgemm) and its Hermitian eigendecomposition
   (cuSOLVER, batched); squared singular values are the eigenvalues, the
@@ -26,11 +26,9 @@ the concatenated CTC1 tensor payloads, on the device.
 """
 from __future__ import annotations
 
-import math
 
 import numpy as np
 
-_SINGULAR = 1e-12  # kSingularRadius of the reference kernels (src/scene.cpp)
 
 
 def _torch():
@@ -38,60 +36,38 @@ def _torch():
     return torch
 
 
-def voxel_centers(origin, spacing, dims, device):
-    """Voxel centres, f1-fastest (v = i1 + n1 (i2 + n2 i3)), shape (n_v, 3)."""
-    torch = _torch()
-    ax = [torch.arange(int(dims[a]), device=device, dtype=torch.float64) for a in range(3)]
-    i3, i2, i1 = torch.meshgrid(ax[2], ax[1], ax[0], indexing="ij")
-    c = torch.stack([origin[0] + spacing * (i1 + 0.5), origin[1] + spacing * (i2 + 0.5),
-                     origin[2] + spacing * (i3 + 0.5)], dim=-1)
-    return c.reshape(-1, 3)
-
-
-def _kernel(op, k0, src, obs):
-    """Field of sources src (B, 7) at points obs (n, 3) -> (B, n, 3) complex128:
-    efield_kernel (src/scene.cpp:84-103) or hfield_kernel (:105-118)."""
-    torch = _torch()
-    mid, d, w = src[:, None, 0:3], src[:, None, 3:6], src[:, None, 6:7]
-    rv = obs[None, :, :] - mid
-    R = torch.linalg.vector_norm(rv, dim=-1, keepdim=True)
-    if bool((R < _SINGULAR).any()):
-        raise RuntimeError("field kernel: observation point hits the source")
-    rh = rv / R
-    g = torch.polar(1.0 / (4.0 * math.pi * R), -k0 * R)
-    if op == 0:
-        R2 = R * R
-        a = g * torch.complex(k0 * k0 - 1.0 / R2, -k0 / R)
-        b = g * torch.complex(-(k0 * k0) + 3.0 / R2, 3.0 * k0 / R)
-        pr = (rh * d).sum(-1, keepdim=True)
-        return w * (a * d + b * pr * rh)
-    gc = -g * torch.complex(1.0 / R, torch.full_like(R, k0))
-    cr = torch.linalg.cross(rh.expand_as(rv), d.expand_as(rv), dim=-1)
-    return (w * gc) * cr
-
-
 def assemble_columns(scene, cols, device="cuda"):
     """assemble_column (src/scene.cpp:127-150) for the columns `cols`:
-    (len(cols), q, n_v) complex128 on the device, component-major rows."""
+    (len(cols), q, n_v) complex128 on the device, component-major rows —
+    the E-/H-field kernels (src/scene.cpp:84-118) evaluated by the CUDA
+    kernel behind tm_assemble_columns (q = 3: point-collocated PWC column;
+    q = 12: the PWL stand-in's 2x2x2 Gauss moments against {1, x~, y~, z~},
+    the oracle's voxel_field definition).  SingularityError if an evaluation
+    point hits a source."""
+    import ctypes
     torch = _torch()
-    src = torch.as_tensor(np.asarray(scene.sources)[list(cols)], dtype=torch.float64, device=device)
-    cen = voxel_centers(scene.origin, scene.spacing, scene.dims, device)
-    if scene.q == 3:
-        return _kernel(scene.op, scene.k0, src, cen).permute(0, 2, 1).contiguous()
-    if scene.q != 12:
+    from ._lib import lib
+    from .matvec import _check
+    if scene.q not in (3, 12):
         raise ValueError("q must be 3 (PWC) or 12 (PWL stand-in)")
-    off = 0.5 / math.sqrt(3.0)
-    out = torch.zeros((src.shape[0], 12, cen.shape[0]), dtype=torch.complex128, device=device)
-    for gz in (0, 1):
-        for gy in (0, 1):
-            for gx in (0, 1):
-                lx, ly, lz = (off if gx else -off), (off if gy else -off), (off if gz else -off)
-                pt = cen + scene.spacing * torch.tensor([lx, ly, lz], dtype=torch.float64, device=device)
-                f = _kernel(scene.op, scene.k0, src, pt)  # (B, n, 3)
-                phi = (1.0, lx, ly, lz)
-                for c in range(3):
-                    for mu in range(4):
-                        out[:, 4 * c + mu, :] += (0.125 * phi[mu]) * f[:, :, c]
+    cols = np.ascontiguousarray(np.asarray(list(cols), dtype=np.int64).reshape(-1))
+    dev = torch.device(device)
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    nv = int(np.prod(scene.dims))
+    out = torch.empty((cols.size, scene.q, nv), dtype=torch.complex128, device=dev)
+    if cols.size == 0:
+        return out
+    src = torch.as_tensor(np.ascontiguousarray(scene.sources, dtype=np.float64), device=dev)
+    org = (ctypes.c_double * 3)(*[float(v) for v in scene.origin])
+    dims = (ctypes.c_int64 * 3)(*[int(v) for v in scene.dims])
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        for b0 in range(0, cols.size, 65535):
+            cb = np.ascontiguousarray(cols[b0:b0 + 65535])
+            _check(lib().tm_assemble_columns(org, float(scene.spacing), dims, int(scene.q), int(scene.op),
+                                             float(scene.k0), src.data_ptr(), int(src.shape[0]), cb.ctypes.data,
+                                             int(cb.size), out[b0:].data_ptr(), stream))
     return out
 
 

@@ -139,3 +139,101 @@ __global__ void rows_kernel(const TDesc* __restrict__ td, const C* __restrict__ 
 }
 
 }  // namespace tmb
+
+// ------------------------------------------------ column assembly (§8f-1)
+// assemble_column (src/scene.cpp:127-150) on the device, complex128: for
+// each requested source column and every voxel, the E-field (op 0,
+// src/scene.cpp:84-103) or H-field (op 1, :105-118) kernel of the RWG-like
+// edge source {midpoint, unit direction, weight} at the voxel centre (q = 3)
+// or the PWL stand-in's 2 x 2 x 2 Gauss moments against {1, x~, y~, z~}
+// (q = 12; points at +-h / (2 sqrt 3), weights 1/8) — the definitions of
+// the oracle's voxel_field and compress.assemble_columns.  Output
+// out[(b * q + comp) * nv + v], v = i1 + n1 (i2 + n2 i3) (component-major
+// rows, voxel f1-fastest: src/compress.cpp:52-65).  One thread per (voxel,
+// column).  Returns nonzero in *bad when an observation point coincides
+// with a source (the reference's SingularityError, R < 1e-12).
+struct AsmScene {
+    double ox, oy, oz, h, k0;
+    int n1, n2, n3, q, op;
+};
+
+__device__ __forceinline__ void asm_field(const AsmScene& sc, const double* __restrict__ s, double px, double py,
+                                          double pz, double2 (&f)[3], int* __restrict__ bad) {
+    const double rx = px - s[0], ry = py - s[1], rz = pz - s[2];
+    const double R = sqrt(rx * rx + ry * ry + rz * rz);
+    if (R < 1e-12) {
+        atomicExch(bad, 1);
+        f[0] = f[1] = f[2] = make_double2(0.0, 0.0);
+        return;
+    }
+    const double iR = 1.0 / R;
+    const double hx = rx * iR, hy = ry * iR, hz = rz * iR;
+    double sn, cs;
+    sincos(sc.k0 * R, &sn, &cs);
+    const double m = 1.0 / (4.0 * 3.14159265358979323846 * R);
+    const double gr = m * cs, gi = -m * sn;  // g = exp(-i k0 R) / (4 pi R)
+    const double w = s[6], dx = s[3], dy = s[4], dz = s[5];
+    if (sc.op == 0) {
+        const double ar0 = sc.k0 * sc.k0 - iR * iR, ai0 = -sc.k0 * iR;          // a = g (k0^2 - 1/R^2 - i k0/R)
+        const double br0 = -sc.k0 * sc.k0 + 3.0 * iR * iR, bi0 = 3.0 * sc.k0 * iR;  // b = g (-k0^2 + 3/R^2 + 3 i k0/R)
+        const double ar = gr * ar0 - gi * ai0, ai = gr * ai0 + gi * ar0;
+        const double br = gr * br0 - gi * bi0, bi = gr * bi0 + gi * br0;
+        const double pr = hx * dx + hy * dy + hz * dz;
+        const double d[3] = {dx, dy, dz}, hh[3] = {hx, hy, hz};
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            f[c] = make_double2(w * (ar * d[c] + br * pr * hh[c]), w * (ai * d[c] + bi * pr * hh[c]));
+    } else {
+        const double cr = -(gr * iR - gi * sc.k0), ci = -(gr * sc.k0 + gi * iR);  // gc = -g (1/R + i k0)
+        const double x0 = hy * dz - hz * dy, x1 = hz * dx - hx * dz, x2 = hx * dy - hy * dx;  // rh x d
+        f[0] = make_double2(w * cr * x0, w * ci * x0);
+        f[1] = make_double2(w * cr * x1, w * ci * x1);
+        f[2] = make_double2(w * cr * x2, w * ci * x2);
+    }
+}
+
+__global__ void assemble_kernel(AsmScene sc, const double* __restrict__ src, const int64_t* __restrict__ cols,
+                                int64_t nb, double2* __restrict__ out, int* __restrict__ bad) {
+    const int64_t nv = int64_t(sc.n1) * sc.n2 * sc.n3;
+    const int64_t b = blockIdx.y;
+    const double* s = src + 7 * cols[b];
+    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < nv; v += int64_t(gridDim.x) * blockDim.x) {
+        const int i1 = int(v % sc.n1);
+        const int64_t rest = v / sc.n1;
+        const int i2 = int(rest % sc.n2), i3 = int(rest / sc.n2);
+        const double cx = sc.ox + sc.h * (i1 + 0.5), cy = sc.oy + sc.h * (i2 + 0.5), cz = sc.oz + sc.h * (i3 + 0.5);
+        double2* o = out + (b * sc.q) * nv + v;
+        if (sc.q == 3) {
+            double2 f[3];
+            asm_field(sc, s, cx, cy, cz, f, bad);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) o[c * nv] = f[c];
+        } else {
+            double2 acc[12];
+#pragma unroll
+            for (int e = 0; e < 12; ++e) acc[e] = make_double2(0.0, 0.0);
+            const double off = 0.5 / sqrt(3.0);
+#pragma unroll
+            for (int gz = 0; gz < 2; ++gz)
+#pragma unroll
+                for (int gy = 0; gy < 2; ++gy)
+#pragma unroll
+                    for (int gx = 0; gx < 2; ++gx) {
+                        const double lx = gx ? off : -off, ly = gy ? off : -off, lz = gz ? off : -off;
+                        double2 f[3];
+                        asm_field(sc, s, cx + sc.h * lx, cy + sc.h * ly, cz + sc.h * lz, f, bad);
+                        const double phi[4] = {1.0, lx, ly, lz};
+#pragma unroll
+                        for (int c = 0; c < 3; ++c)
+#pragma unroll
+                            for (int mu = 0; mu < 4; ++mu) {
+                                const double wq = 0.125 * phi[mu];
+                                acc[4 * c + mu].x += wq * f[c].x;
+                                acc[4 * c + mu].y += wq * f[c].y;
+                            }
+                    }
+#pragma unroll
+            for (int e = 0; e < 12; ++e) o[e * nv] = acc[e];
+        }
+    }
+}

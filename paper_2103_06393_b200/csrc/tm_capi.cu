@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -1216,6 +1217,50 @@ TM_API int tm_store_info(const tm_store* s, int32_t* q, int64_t* ncols, int64_t*
         if (dtype) *dtype = s->dtype;
         if (m2) *m2 = s->m2;
         if (device_bytes) *device_bytes = s->device_bytes;
+    });
+}
+
+// assemble_column (src/scene.cpp:127-150) for a batch of source columns, on
+// the device, complex128 (the GPU compressor's field evaluation, §8f-1).
+// src: device pointer to m x 7 doubles {midpoint xyz, unit direction xyz,
+// weight}; cols: host array of nb column indices; out: device pointer to nb
+// x q x n_v complex128.  Enqueued on `stream` (NULL = legacy default) and
+// synchronised only for the singularity check.
+TM_API int tm_assemble_columns(const double* origin3, double spacing, const int64_t* dims3, int q, int op, double k0,
+                               const double* src, int64_t m, const int64_t* cols, int64_t nb, void* out,
+                               void* stream) {
+    return guarded([&] {
+        if (!origin3 || !dims3 || (nb > 0 && (!src || !cols || !out))) contract("tm_assemble_columns: null argument");
+        if (q != 3 && q != 12) contract("tm_assemble_columns: q must be 3 (PWC) or 12 (PWL)");
+        if (op != 0 && op != 1) contract("tm_assemble_columns: op must be 0 (E) or 1 (H)");
+        if (!(spacing > 0)) contract("tm_assemble_columns: spacing must be positive");
+        for (int g = 0; g < 3; ++g)
+            if (dims3[g] < 1 || dims3[g] > (int64_t(1) << 30)) contract("tm_assemble_columns: bad grid dimension");
+        for (int64_t b = 0; b < nb; ++b)
+            if (cols[b] < 0 || cols[b] >= m) contract("tm_assemble_columns: column index out of range");
+        if (nb == 0) return;
+        if (nb > 65535) contract("tm_assemble_columns: at most 65535 columns per call");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        AsmScene sc{origin3[0], origin3[1], origin3[2], spacing, k0, int(dims3[0]), int(dims3[1]), int(dims3[2]), q, op};
+        // per-thread scratch reused across calls (a cudaMalloc / cudaFree pair per
+        // call costs more than the kernel for the ACA's one-voxel row batches)
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        static thread_local std::map<int, std::pair<DevBuf, DevBuf>> scratch;
+        DevBuf& cb = scratch[dev].first;
+        DevBuf& bb = scratch[dev].second;
+        int64_t* d_cols = static_cast<int64_t*>(cb.get(size_t(nb) * sizeof(int64_t)));
+        int* d_bad = static_cast<int*>(bb.get(sizeof(int)));
+        CK(cudaMemcpyAsync(d_cols, cols, size_t(nb) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+        const int64_t nv = dims3[0] * dims3[1] * dims3[2];
+        const unsigned gx = unsigned(std::min<int64_t>((nv + 255) / 256, 4096));
+        assemble_kernel<<<dim3(gx, unsigned(nb)), 256, 0, st>>>(sc, src, d_cols, nb, static_cast<double2*>(out), d_bad);
+        launched(cudaSuccess, "assemble_kernel");
+        int hbad = 0;
+        CK(cudaMemcpyAsync(&hbad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (hbad) throw TmError(TM_SINGULARITY_ERROR, "field kernel: observation point hits the source");
     });
 }
 

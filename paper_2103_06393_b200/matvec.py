@@ -52,8 +52,13 @@ class CudaError(Error):
     """Device / driver failure (no reference analogue)."""
 
 
+class SingularityError(Error):
+    """tuckmat::SingularityError (errors.hpp:21-24)."""
+
+
 _ERRS = {_lib.TM_CONTRACT_VIOLATION: ContractViolation, _lib.TM_CAPACITY_ERROR: CapacityError,
-         _lib.TM_PARSE_ERROR: ParseError, _lib.TM_CUDA_ERROR: CudaError}
+         _lib.TM_PARSE_ERROR: ParseError, _lib.TM_CUDA_ERROR: CudaError,
+         _lib.TM_SINGULARITY_ERROR: SingularityError}
 
 
 def _check(st):
