@@ -581,11 +581,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         for (int pl = 0; pl < 4; ++pl) a[pl * TC_A_PLANE / 2] = __float2half_rn(0.f);
                     }
             }
+            // (r2, r3) of the next column are prefetched from the global descriptor table one
+            // column ahead, so the NU dispatch does not wait on the slot's descriptor
+            const int2* rk = reinterpret_cast<const int2*>(&tcd[int64_t(tl.k) * g.ncols].r2);
+            constexpr int kDescStride = int(sizeof(TcDesc) / sizeof(int2));
+            int2 rn = j0 < j1 ? __ldg(rk + int64_t(j0) * kDescStride) : make_int2(0, 0);
             for (int j = j0; j < j1; ++j) {
+                const int r2 = rn.x, r3 = rn.y;
+                if (j + 1 < j1) rn = __ldg(rk + int64_t(j + 1) * kDescStride);
                 TC_TWAIT(g.prof, t_w, (mbar_wait(&ffull[fs], fph)));
                 const unsigned char* slot = sSlot + fs * g.slot_bytes;
-                const int r2 = reinterpret_cast<const TcDesc*>(slot)->r2;
-                const int r3 = reinterpret_cast<const TcDesc*>(slot)->r3;
                 const float2* V = reinterpret_cast<const float2*>(slot + TC_SLOT_V) + i1l;
                 const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
 #define TC_COL(NU)                                                                                             \
