@@ -75,7 +75,7 @@ __host__ __device__ inline float fp16_scale(float amax) {
 }
 
 constexpr int TC_TI1 = 4, TC_TI2 = 32, TC_ROWS = 128;
-constexpr int TC_NST_MAX = 5;   // A/B stages (8 K each)
+constexpr int TC_NST_MAX = 6;   // A/B stages (16 K each; as many as shared memory allows)
 constexpr int TC_JR = 3;        // factor-ring slots
 constexpr int TC_NR = 2;        // tile rows per producer lane (rows i2a + 8 e, e < TC_NR)
 constexpr int TC_NPW = 16 / TC_NR;  // producer warps: 4 i1 rows x (4 / TC_NR) blocks of 8 TC_NR i2
