@@ -288,6 +288,30 @@ def test_forward_rhs_passes(oracle, product, monkeypatch):
     assert rel(y2, y1) <= 1e-6
 
 
+@pytest.mark.parametrize("dims,q,m,rmin,rmax,p", [
+    ((24, 40, 40), 2, 21, 3, 16, 5),      # two right-hand-side pairs + an odd one
+    ((64, 64, 64), 12, 6, 4, 9, 8),       # config-5 grid, four pairs
+    ((9, 70, 20), 1, 70, 1, 13, 2),       # many columns: 64-slot chunks with many short columns
+])
+def test_adjoint_rhs_pairs(oracle, product, monkeypatch, dims, q, m, rmin, rmax, p):
+    """The two-right-hand-side adjoint (adj_tc2_kernel: W once per column for
+    a pair, 64-slot chunks) against the oracle and against the single-RHS
+    kernel (TMB_ADJ_NR1=1)."""
+    O, P = oracle, product
+    cc = ragged_store(dims, q, m, rmin, rmax, seed=13 * m + p)
+    ref = O.OracleStore(cc.rounded_c64())
+    ds = P.DeviceStore.from_compressed(cc, "c64")
+    phi = cn01(cc.rows, p, 41).astype(np.complex64).astype(np.complex128)
+    z2 = ds.adjoint(phi)
+    monkeypatch.setenv("TMB_ADJ_NR1", "1")
+    z1 = ds.adjoint(phi)
+    monkeypatch.delenv("TMB_ADJ_NR1")
+    z_ref = ref.adjoint(phi)
+    assert rel(z2, z_ref) <= 1e-5
+    assert rel(z1, z_ref) <= 1e-5
+    assert rel(z2, z1) <= 1e-6
+
+
 @pytest.mark.parametrize("chain", ["", "1", "3", "48"])
 def test_tensor_core_long_k(product, monkeypatch, chain):
     """Accumulation over a long K stream (2 500 columns, K ~ 21 000 per
