@@ -1,39 +1,49 @@
-// Tensor-core adjoint for pairs of right-hand sides (p >= 2), complex64.
+// Tensor-core adjoint for groups of NR = 2 or 4 right-hand sides (p >= 2), complex64.
 //
 // The single-RHS adjoint (tm_adj_tc.cuh) recomputes its consumers' mode-2
 // product W = V x_2 U2 for every right-hand side.  Here one CTA takes a row
-// tile of TWO right-hand sides c0, c0 + 1: per 64-slot chunk of the (j, c)
-// stream the MMA warp builds Q for both,
-//   [Qi|Qr]_r = Phi_r . [-U3i|U3r] + ...  (N = 128, 6 kind::f16 MMAs per r
-//   and 16 i3, TMEM buffer qb: columns qb 256 + r 128 + [Qi 64 | Qr 64]),
+// tile of NR right-hand sides c0 .. c0 + NR - 1: per chunk of CH = 128 / NR
+// slots of the (j, c) stream the MMA warp builds Q for each,
+//   [Qi|Qr]_r = Phi_r . [-U3i|U3r] + ...  (N = 2 CH, 6 kind::f16 MMAs per r
+//   and 16 i3; TMEM buffer qb: columns qb 256 + r 2 CH + [Qi CH | Qr CH]),
 // and each consumer thread forms W[row, c] once per column and contracts it
-// with both Q — the reference's stacked_adjoint (src/matvec.cpp:67-102)
+// with every Q_r — the reference's stacked_adjoint (src/matvec.cpp:67-102)
 // with the projection form of SURVEY §8 (conj(T) . Phi = conj(W) . (Phi
-// conj(U3))).  The 64-slot chunks use their own packing of the adjoint U3
-// planes (tm_capi.cu: ensure_adj64), whole columns per chunk; TcDesc.pad1 is
-// a column's slot inside its 64-slot chunk.  Everything else (Phi planes,
-// partials, adj_reduce_kernel, split final waves) is the single-RHS path's.
+// conj(U3))).  The CH-slot chunks use their own packing of the adjoint U3
+// planes (tm_capi.cu: ensure_adj_pack), whole columns per chunk; TcDesc.pad1
+// (CH 64) / pad2 (CH 32) is a column's slot inside its chunk.  Everything
+// else (Phi planes, partials, adj_reduce_kernel, split final waves) is the
+// single-RHS path's.  NR = 4 halves the W work again but its N = 64 MMAs
+// read A (4 KB) per 2 KB of B, so the MMA side, not the consumers, bounds it
+// (DESIGN.md §6).
 #pragma once
 
 #include "tm_adj_tc.cuh"
 
 namespace tmb {
 
-constexpr int A2_CH = 64;                          // (j, c) slots per chunk
-constexpr int A2_NST = 3;                          // A/B stages (16 i3 each)
-constexpr int A2_A_STAGE = 2 * AJ_A_STAGE;         // Phi planes of both right-hand sides: 32 KB
-constexpr int A2_B_PLANE = A2_CH * 32;             // 2 KB
-constexpr int A2_B_STAGE = TC_BPLANES * A2_B_PLANE;  // 12 KB
+// NR right-hand sides per CTA (2 or 4): chunks of 128 / NR slots, so the
+// TMEM holds [Qi|Qr] of every right-hand side twice (ping-pong).
+template <int NR>
+struct A2 {
+    static constexpr int CH = 128 / NR;                         // (j, c) slots per chunk
+    static constexpr int NST = NR == 4 ? 2 : 3;                 // A/B stages (16 i3 each)
+    static constexpr int A_STAGE = NR * AJ_A_STAGE;             // Phi planes of the NR right-hand sides
+    static constexpr int B_PLANE = CH * 32;
+    static constexpr int B_STAGE = TC_BPLANES * B_PLANE;
+    static constexpr int RED = 2 * NR * CH * AJ_NPW;            // float2 partial buffer [buf][rhs][col][warp]
+};
 
-// Tile of a pass over right-hand-side pairs: item -> (pair cp, component k,
+// Tile of a pass over right-hand-side groups: item -> (group cp, component k,
 // row tile rt), i2 block fastest as in aj_tile.
+template <int NR>
 __device__ __forceinline__ AjTile aj2_tile(const AjGeom& g, int64_t item) {
     AjTile r;
     const int64_t t = g.tile0 + item / g.split;
     r.part = int(item % g.split);
     const int64_t per_c = int64_t(g.q) * g.nrt;
     const int64_t cp = t / per_c;
-    r.c = int(2 * cp);
+    r.c = int(NR * cp);
     int64_t rem = t - cp * per_c;
     r.k = int(rem / g.nrt);
     r.rt = rem - int64_t(r.k) * g.nrt;
@@ -43,12 +53,13 @@ __device__ __forceinline__ AjTile aj2_tile(const AjGeom& g, int64_t item) {
     return r;
 }
 
-// One column for the consumer thread: W once, then sum_c conj(W) Q_r for both
-// right-hand sides (Q_r: Qi at qaddr + r 128 + s, Qr at + 64).
-template <int NU>
+// One column for the consumer thread: W once, then sum_c conj(W) Q_r for the
+// NR right-hand sides (Q_r: Qi at qaddr + r 2 CH + s, Qr at + CH).
+template <int NU, int NR>
 __device__ __forceinline__ void aj2_consume_column(const float2* __restrict__ V, const float2* __restrict__ U2,
                                                    int r2, int ld2, int r3, int h, int lane, uint32_t qaddr,
-                                                   uint64_t* fempty_s, float2 (&a)[2]) {
+                                                   uint64_t* fempty_s, float2 (&a)[NR]) {
+    constexpr int CH = A2<NR>::CH;
     using namespace sm100;
     uint64_t w[NU];
 #pragma unroll
@@ -66,14 +77,14 @@ __device__ __forceinline__ void aj2_consume_column(const float2* __restrict__ V,
     __syncwarp();
     if (lane == 0) mbar_arrive(fempty_s);
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
+    for (int rr = 0; rr < NR; ++rr) {
         uint32_t qi[NU], qr[NU];
 #pragma unroll
         for (int u = 0; u < NU; ++u) {
             const uint32_t s = (u < NU - 1 || AJ_NH * u + h < r3) ? uint32_t(AJ_NH * u + h) : 0u;
-            const uint32_t q0 = qaddr + uint32_t(rr * 2 * A2_CH) + s;
+            const uint32_t q0 = qaddr + uint32_t(rr * 2 * CH) + s;
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(qi[u]) : "r"(q0));
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(qr[u]) : "r"(q0 + A2_CH));
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(qr[u]) : "r"(q0 + CH));
         }
         tmem_ld_wait();
         float ar = 0.f, ai = 0.f;
@@ -90,19 +101,23 @@ __device__ __forceinline__ void aj2_consume_column(const float2* __restrict__ V,
     }
 }
 
+template <int NR>
 __global__ void __launch_bounds__(AJ_THREADS, 1)
     adj_tc2_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                    const TcDesc* __restrict__ tcd, const float2* __restrict__ varena,
                    const float2* __restrict__ u2arena, const int* __restrict__ nch, const int* __restrict__ cstart,
                    AjGeom g, const float* __restrict__ phimax, float2* __restrict__ part) {
     using namespace sm100;
+    using P = A2<NR>;
+    constexpr int A2_CH = P::CH, A2_NST = P::NST, A2_A_STAGE = P::A_STAGE, A2_B_PLANE = P::B_PLANE,
+                  A2_B_STAGE = P::B_STAGE;
     extern __shared__ __align__(1024) unsigned char a2_smem_raw[];
     unsigned char* sm = a2_smem_raw + ((1024u - (smem_u32(a2_smem_raw) & 1023u)) & 1023u);
     unsigned char* sA = sm;
     unsigned char* sB = sA + A2_NST * A2_A_STAGE;
     unsigned char* sSlot = sB + A2_NST * A2_B_STAGE;
-    float2* red = reinterpret_cast<float2*>(sSlot + TC_JR * g.slot_bytes);  // [2 buf][2 rhs][A2_CH cols][8]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * 2 * A2_CH * AJ_NPW);
+    float2* red = reinterpret_cast<float2*>(sSlot + TC_JR * g.slot_bytes);  // [2 buf][NR rhs][A2_CH cols][8]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + P::RED);
     uint64_t* full = bars;                 // [NST]
     uint64_t* empty = full + A2_NST;       // [NST]
     uint64_t* ffull = empty + A2_NST;      // [JR]
@@ -144,7 +159,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
-                const AjTile tl = aj2_tile(g, t);
+                const AjTile tl = aj2_tile<NR>(g, t);
                 int n0, n1;
                 aj_chunks(g, tl, nch[tl.k], n0, n1);
                 const int arow = int(tl.rt * TC_ROWS);
@@ -155,7 +170,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                         unsigned char* da = sA + s * A2_A_STAGE;
                         unsigned char* db = sB + s * A2_B_STAGE;
 #pragma unroll
-                        for (int rr = 0; rr < 2; ++rr)
+                        for (int rr = 0; rr < NR; ++rr)
 #pragma unroll
                             for (int pl = 0; pl < AJ_APLANES; ++pl)
                                 tma_load_3d(da + (rr * AJ_APLANES + pl) * AJ_A_PLANE, &amap, &full[s], kk * 16, arow,
@@ -177,7 +192,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
             const uint32_t idesc = umma_idesc_f16(TC_ROWS, 2 * A2_CH, false, false);
             uint32_t s = 0, ph = 0, nq = 0;
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
-                const AjTile tl = aj2_tile(g, t);
+                const AjTile tl = aj2_tile<NR>(g, t);
                 int n0, n1;
                 aj_chunks(g, tl, nch[tl.k], n0, n1);
                 for (int n = n0; n < n1; ++n, ++nq) {
@@ -196,7 +211,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                         const uint64_t B1l = umma_smem_desc(b0 + 4 * A2_B_PLANE, 256, 6);
                         const uint32_t acc = kk > 0 ? 1u : 0u;
 #pragma unroll
-                        for (int rr = 0; rr < 2; ++rr) {
+                        for (int rr = 0; rr < NR; ++rr) {
                             uint64_t A[4];
 #pragma unroll
                             for (int pl = 0; pl < 4; ++pl)
@@ -225,7 +240,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
-                const AjTile tl = aj2_tile(g, t);
+                const AjTile tl = aj2_tile<NR>(g, t);
                 const TcDesc* tdk = tcd + int64_t(tl.k) * g.ncols;
                 int n0, n1;
                 aj_chunks(g, tl, nch[tl.k], n0, n1);
@@ -257,18 +272,18 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         const uint32_t lane_addr = uint32_t(i1l * 32) << 16;
         uint32_t fs = 0, fph = 0, nq = 0;
         for (int64_t t = tstart; t < g.t_end; t += tstep) {
-            const AjTile tl = aj2_tile(g, t);
+            const AjTile tl = aj2_tile<NR>(g, t);
             int n0, n1;
             aj_chunks(g, tl, nch[tl.k], n0, n1);
             const int* cs = cstart + int64_t(tl.k) * (g.maxch + 1);
-            float inv_scale[2];
+            float inv_scale[NR];
 #pragma unroll
-            for (int rr = 0; rr < 2; ++rr)
+            for (int rr = 0; rr < NR; ++rr)
                 inv_scale[rr] = 1.f / (aj_phi_scale(phimax[int64_t(tl.c + rr) * g.q + tl.k]) * AJ_U3_SCALE);
             for (int n = n0; n < n1; ++n, ++nq) {
                 const uint32_t qb = nq & 1, qph = (nq >> 1) & 1;
                 const int j0 = cs[n], j1 = cs[n + 1];
-                float2* rb = red + (nq & 1) * 2 * A2_CH * AJ_NPW;  // [rhs][col][warp]
+                float2* rb = red + (nq & 1) * NR * A2_CH * AJ_NPW;  // [rhs][col][warp]
                 mbar_wait(&qfull[qb], qph);
                 tc_fence_after();
                 const uint32_t qbase = tmem + lane_addr + qb * 256u;
@@ -276,12 +291,13 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                     mbar_wait(&ffull[fs], fph);
                     const unsigned char* slot = sSlot + fs * g.slot_bytes;
                     const TcDesc* dd = reinterpret_cast<const TcDesc*>(slot);
-                    const int r2 = dd->r2, r3 = dd->r3, soff = dd->pad1;  // slot inside the 64-slot chunk
+                    // slot inside the chunk: pad1 for 64-slot chunks, pad2 for 32-slot chunks
+                    const int r2 = dd->r2, r3 = dd->r3, soff = NR == 2 ? dd->pad1 : dd->pad2;
                     const float2* V = reinterpret_cast<const float2*>(slot + TC_SLOT_V) + i1l;
                     const float2* U2 = reinterpret_cast<const float2*>(slot + g.u2_off);
-                    float2 a[2];
+                    float2 a[NR];
 #define A2_COL(NU) \
-    aj2_consume_column<NU>(V, U2, (g.debug & 4) ? 0 : r2, r2 | 1, r3, h, lane, qbase + uint32_t(soff), &fempty[fs], a)
+    aj2_consume_column<NU, NR>(V, U2, (g.debug & 4) ? 0 : r2, r2 | 1, r3, h, lane, qbase + uint32_t(soff), &fempty[fs], a)
                     switch ((r3 + AJ_NH - 1) / AJ_NH) {
                         case 1: A2_COL(1); break;
                         case 2: A2_COL(2); break;
@@ -298,7 +314,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                         fph ^= 1;
                     }
 #pragma unroll
-                    for (int rr = 0; rr < 2; ++rr) {
+                    for (int rr = 0; rr < NR; ++rr) {
 #pragma unroll
                         for (int o = 16; o > 0; o >>= 1) {
                             a[rr].x += __shfl_xor_sync(0xffffffffu, a[rr].x, o);
@@ -311,7 +327,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&qfree[qb]);
                 named_bar_sync(1, AJ_NPW * 32);  // all partials of the chunk are in rb
-                for (int e = ctid; e < 2 * (j1 - j0); e += AJ_NPW * 32) {
+                for (int e = ctid; e < NR * (j1 - j0); e += AJ_NPW * 32) {
                     const int rr = e / (j1 - j0), jj = e - rr * (j1 - j0);
                     float sx = 0.f, sy = 0.f;
 #pragma unroll

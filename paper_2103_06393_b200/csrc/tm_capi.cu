@@ -141,15 +141,17 @@ struct tm_store {
     int maxch = 0;
     int64_t nslots = 0;       // slots per component (maxch * 128)
     CUtensorMap adj_bmap{};
-    // right-hand-side pairs (adj_tc2_kernel): the adjoint U3 planes packed in
-    // 64-slot chunks, built on the first adjoint with p >= 2 (ensure_adj64)
-    bool adj64_ok = false;
-    __half* d_aplanes64 = nullptr;
-    int* d_nch64 = nullptr;
-    int* d_cstart64 = nullptr;
-    int maxch64 = 0;
-    int64_t nslots64 = 0;
-    CUtensorMap adj_bmap64{};
+    // right-hand-side groups (adj_tc2_kernel<NR>): the adjoint U3 planes packed
+    // in 128 / NR-slot chunks, built on the first adjoint with p >= 2 (ensure_adj_pack)
+    struct AdjPack {
+        bool ok = false;
+        __half* d_aplanes = nullptr;
+        int* d_nch = nullptr;
+        int* d_cstart = nullptr;
+        int maxch = 0;
+        int64_t nslots = 0;
+        CUtensorMap bmap{};
+    } adjp[2];  // [0]: 64-slot chunks (pairs), [1]: 32-slot chunks (quads)
     int64_t kpad = 0;
     DevBuf xbplanes;        // the forward's per-call B operand (build_xb_kernel)
     size_t xb_zeroed = 0;   // bytes of xbplanes zeroed since allocation
@@ -169,9 +171,11 @@ struct tm_store {
         if (d_varena) cudaFree(d_varena);
         if (d_u2arena) cudaFree(d_u2arena);
         if (d_aplanes) cudaFree(d_aplanes);
-        if (d_aplanes64) cudaFree(d_aplanes64);
-        if (d_nch64) cudaFree(d_nch64);
-        if (d_cstart64) cudaFree(d_cstart64);
+        for (auto& a : adjp) {
+            if (a.d_aplanes) cudaFree(a.d_aplanes);
+            if (a.d_nch) cudaFree(a.d_nch);
+            if (a.d_cstart) cudaFree(a.d_cstart);
+        }
         if (d_nch) cudaFree(d_nch);
         if (d_cstart) cudaFree(d_cstart);
         if (d_desc) cudaFree(d_desc);
@@ -899,10 +903,15 @@ size_t adj_tc_smem(const tm_store* s) {
            size_t(2) * AJ_MAXCOLS * AJ_NPW * sizeof(float2) + (2 * AJ_NST + 2 * TC_JR + 4) * 8 + 16;
 }
 
-// 64-slot chunk packing of the adjoint U3 planes for adj_tc2_kernel (whole
-// columns per chunk, TcDesc.pad1 = slot inside the chunk), built once.
-void ensure_adj64(tm_store* s) {
-    if (s->adj64_ok) return;
+// Chunk packing of the adjoint U3 planes for adj_tc2_kernel<NR> (ch = 128 / NR
+// slots per chunk, whole columns per chunk; TcDesc.pad1 (ch 64) / pad2 (ch 32)
+// = the column's slot inside its chunk), built once per chunk size.  Returns
+// false when some column's r3 exceeds the chunk.
+bool ensure_adj_pack(tm_store* s, int which) {
+    const int ch = which == 0 ? 64 : 32;
+    auto& ap = s->adjp[which];
+    if (ap.ok) return true;
+    if (s->rmax[2] > ch) return false;
     const int64_t ntens = s->ncols * s->q;
     std::vector<TcDesc> tcd(static_cast<size_t>(ntens));
     CK(cudaMemcpy(tcd.data(), s->d_tcd, tcd.size() * sizeof(TcDesc), cudaMemcpyDeviceToHost));
@@ -910,17 +919,17 @@ void ensure_adj64(tm_store* s) {
     std::vector<std::vector<int>> cst(static_cast<size_t>(s->q));
     int maxch = 0;
     for (int k = 0; k < s->q; ++k) {
-        int fill = A2_CH, chunk = -1;
+        int fill = ch, chunk = -1;
         for (int64_t j = 0; j < s->ncols; ++j) {
             const size_t t = static_cast<size_t>(k * s->ncols + j);
             const int r3 = tcd[t].r3;
-            if (fill + r3 > A2_CH || cst[static_cast<size_t>(k)].empty()) {
+            if (fill + r3 > ch || cst[static_cast<size_t>(k)].empty()) {
                 ++chunk;
                 fill = 0;
                 cst[static_cast<size_t>(k)].push_back(int(j));
             }
-            aslot[t] = chunk * A2_CH + fill;
-            tcd[t].pad1 = fill;
+            aslot[t] = chunk * ch + fill;
+            (which == 0 ? tcd[t].pad1 : tcd[t].pad2) = fill;
             fill += r3;
         }
         nch[static_cast<size_t>(k)] = chunk + 1;
@@ -931,29 +940,68 @@ void ensure_adj64(tm_store* s) {
         for (size_t n = 0; n < cst[static_cast<size_t>(k)].size(); ++n)
             cstart[static_cast<size_t>(k) * (maxch + 1) + n] = cst[static_cast<size_t>(k)][n];
     const int64_t n3 = s->dims[2], n3p = (n3 + 7) / 8 * 8;
-    const int64_t nslots = int64_t(maxch) * A2_CH;
+    const int64_t nslots = int64_t(maxch) * ch;
     const size_t abytes = size_t(TC_BPLANES) * s->q * nslots * n3p * sizeof(__half);
-    CK(cudaMalloc(&s->d_aplanes64, abytes));
-    CK(cudaMalloc(&s->d_nch64, nch.size() * sizeof(int)));
-    CK(cudaMalloc(&s->d_cstart64, cstart.size() * sizeof(int)));
-    CK(cudaMemcpy(s->d_nch64, nch.data(), nch.size() * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(s->d_cstart64, cstart.data(), cstart.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&ap.d_aplanes, abytes));
+    CK(cudaMalloc(&ap.d_nch, nch.size() * sizeof(int)));
+    CK(cudaMalloc(&ap.d_cstart, cstart.size() * sizeof(int)));
+    CK(cudaMemcpy(ap.d_nch, nch.data(), nch.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ap.d_cstart, cstart.data(), cstart.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(s->d_tcd, tcd.data(), tcd.size() * sizeof(TcDesc), cudaMemcpyHostToDevice));
-    CK(cudaMemset(s->d_aplanes64, 0, abytes));
+    CK(cudaMemset(ap.d_aplanes, 0, abytes));
     DevBuf as;
     int* d_as = static_cast<int*>(as.get(aslot.size() * sizeof(int)));
     CK(cudaMemcpy(d_as, aslot.data(), aslot.size() * sizeof(int), cudaMemcpyHostToDevice));
     build_adj_bplanes_kernel<<<unsigned(ntens), 256>>>(s->d_desc, static_cast<const float2*>(s->d_arena), d_as,
-                                                       s->ncols, s->q, int(n3), int(n3p), nslots, s->d_aplanes64);
+                                                       s->ncols, s->q, int(n3), int(n3p), nslots, ap.d_aplanes);
     launched(cudaSuccess, "build_adj_bplanes_kernel");
     CK(cudaDeviceSynchronize());
-    s->adj_bmap64 = make_tmap_3d_f16(s->d_aplanes64, uint64_t(n3), uint64_t(nslots), uint64_t(TC_BPLANES * s->q),
-                                     uint64_t(n3p) * 2, uint64_t(nslots) * n3p * 2, 16, A2_CH,
-                                     CU_TENSOR_MAP_SWIZZLE_32B);
-    s->maxch64 = maxch;
-    s->nslots64 = nslots;
+    ap.bmap = make_tmap_3d_f16(ap.d_aplanes, uint64_t(n3), uint64_t(nslots), uint64_t(TC_BPLANES * s->q),
+                               uint64_t(n3p) * 2, uint64_t(nslots) * n3p * 2, 16, uint32_t(ch),
+                               CU_TENSOR_MAP_SWIZZLE_32B);
+    ap.maxch = maxch;
+    ap.nslots = nslots;
     s->device_bytes += int64_t(abytes + (nch.size() + cstart.size()) * sizeof(int));
-    s->adj64_ok = true;
+    ap.ok = true;
+    return true;
+}
+
+// Shared-memory plan of adj_tc2_kernel<NR>.
+template <int NR>
+size_t adj_group_smem(int slot_bytes) {
+    using P = A2<NR>;
+    return 1024 + size_t(P::NST) * (P::A_STAGE + P::B_STAGE) + size_t(TC_JR) * slot_bytes +
+           size_t(P::RED) * sizeof(float2) + (2 * P::NST + 2 * TC_JR + 4) * 8 + 16;
+}
+
+// One pass of adj_tc2_kernel<NR> over right-hand-side groups [grp0, grp0 + ngrp).
+template <int NR>
+void launch_adj_groups(tm_store* s, const AjGeom& g, const CUtensorMap& amap, int64_t grp0, int64_t ngrp,
+                       const float* phimax, float2* part, int nsm, cudaStream_t st) {
+    const auto& ap = s->adjp[NR == 2 ? 0 : 1];
+    AjGeom g2 = g;
+    g2.pair = 0;
+    g2.maxch = ap.maxch;
+    const int64_t tpg = int64_t(g.q) * g.nrt;  // tiles per group
+    g2.ntiles = (grp0 + ngrp) * tpg;
+    const size_t smem2 = adj_group_smem<NR>(g.slot_bytes);
+    if (smem2 > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: shared-memory plan too large");
+    CK(cudaFuncSetAttribute(adj_tc2_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+    const unsigned grid2 = unsigned(std::min<int64_t>(ngrp * tpg, nsm));
+    for (int64_t t0 = grp0 * tpg; t0 < g2.ntiles; t0 += grid2) {
+        const int64_t tiles = std::min<int64_t>(g2.ntiles - t0, int64_t(grid2));
+        g2.split = tiles < int64_t(grid2) ? int(std::max<int64_t>(1, std::min<int64_t>(8, grid2 / tiles))) : 1;
+        g2.tile0 = t0;
+        g2.t_begin = 0;
+        g2.t_end = tiles * g2.split;
+        adj_tc2_kernel<NR><<<grid2, AJ_THREADS, smem2, st>>>(amap, ap.bmap, s->d_tcd, s->d_varena, s->d_u2arena,
+                                                             ap.d_nch, ap.d_cstart, g2, phimax, part);
+        launched(cudaSuccess, "adj_tc2_kernel");
+    }
+}
+
+bool adj_pack_fits(const tm_store* s, int nr, int slot_bytes) {
+    return s->rmax[2] <= 128 / nr && (nr == 4 ? adj_group_smem<4>(slot_bytes) : adj_group_smem<2>(slot_bytes)) <= kSmemMax;
 }
 
 void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, float2* z, int64_t ldz,
@@ -1037,40 +1085,28 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     const int64_t wave = g.pair ? grid / 2 : grid;
     const int64_t tpb = g.nrt >> g.pair;  // tiles per (rhs, component) block
     int64_t bready = hp ? 0 : nblk;
-    // Right-hand-side pairs (adj_tc2_kernel: W once for two right-hand sides);
-    // an odd last right-hand side goes through the single-RHS kernel below.
+    // Right-hand-side groups (adj_tc2_kernel<NR>: W once for NR right-hand
+    // sides): quads first, then a pair; an odd last right-hand side goes
+    // through the single-RHS kernel below.  TMB_ADJ_NR = 1 / 2 / 4 caps NR.
     int64_t tfirst = 0;
     {
-        const char* e = std::getenv("TMB_ADJ_NR1");
-        const int64_t pairs = (e && *e && *e != '0') ? 0 : p / 2;
-        if (pairs > 0) {
-            ensure_adj64(s);
+        int nrmax = 4;
+        if (const char* e = std::getenv("TMB_ADJ_NR")) nrmax = std::atoi(e);
+        if (const char* e = std::getenv("TMB_ADJ_NR1")) if (*e && *e != '0') nrmax = 1;
+        const bool q4 = nrmax >= 4 && p >= 4 && adj_pack_fits(s, 4, g.slot_bytes) && ensure_adj_pack(s, 1);
+        const int64_t quads = q4 ? p / 4 : 0;
+        const bool q2 = nrmax >= 2 && p - 4 * quads >= 2 && adj_pack_fits(s, 2, g.slot_bytes) &&
+                        ensure_adj_pack(s, 0);
+        const int64_t pairs = q2 ? (p - 4 * quads) / 2 : 0;
+        if (quads + pairs > 0) {
             for (; bready < nblk; ++bready) {  // every block of the pass is read by some wave
                 CK(cudaStreamWaitEvent(st, arrived[size_t(bready)], 0));
                 prepare(bready, bready + 1);
             }
-            AjGeom g2 = g;
-            g2.pair = 0;
-            g2.maxch = s->maxch64;
-            g2.ntiles = pairs * g.q * g.nrt;
-            const size_t smem2 = 1024 + size_t(A2_NST) * (A2_A_STAGE + A2_B_STAGE) + size_t(TC_JR) * g.slot_bytes +
-                                 size_t(2) * 2 * A2_CH * AJ_NPW * sizeof(float2) + (2 * A2_NST + 2 * TC_JR + 4) * 8 +
-                                 16;
-            if (smem2 > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: shared-memory plan too large");
-            CK(cudaFuncSetAttribute(adj_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
-            const unsigned grid2 = unsigned(std::min<int64_t>(g2.ntiles, nsm));
-            for (int64_t t0 = 0; t0 < g2.ntiles; t0 += grid2) {
-                const int64_t tiles = std::min<int64_t>(g2.ntiles - t0, int64_t(grid2));
-                g2.split = tiles < int64_t(grid2) ? int(std::max<int64_t>(1, std::min<int64_t>(8, grid2 / tiles))) : 1;
-                g2.tile0 = t0;
-                g2.t_begin = 0;
-                g2.t_end = tiles * g2.split;
-                adj_tc2_kernel<<<grid2, AJ_THREADS, smem2, st>>>(amap, s->adj_bmap64, s->d_tcd, s->d_varena,
-                                                                  s->d_u2arena, s->d_nch64, s->d_cstart64, g2, phimax,
-                                                                  part);
-                launched(cudaSuccess, "adj_tc2_kernel");
-            }
-            tfirst = (2 * pairs) * g.q * tpb;  // the remaining (odd) right-hand side's tiles
+            if (quads > 0) launch_adj_groups<4>(s, g, amap, 0, quads, phimax, part, nsm, st);
+            // pairs start at right-hand side 4 quads = pair index 2 quads
+            if (pairs > 0) launch_adj_groups<2>(s, g, amap, 2 * quads, pairs, phimax, part, nsm, st);
+            tfirst = (4 * quads + 2 * pairs) * g.q * tpb;  // the remaining (odd) right-hand side's tiles
         }
     }
     for (int64_t t0 = tfirst; t0 < g.ntiles; t0 += wave) {  // one launch per wave (see run_forward_tc)

@@ -289,27 +289,32 @@ def test_forward_rhs_passes(oracle, product, monkeypatch):
 
 
 @pytest.mark.parametrize("dims,q,m,rmin,rmax,p", [
-    ((24, 40, 40), 2, 21, 3, 16, 5),      # two right-hand-side pairs + an odd one
-    ((64, 64, 64), 12, 6, 4, 9, 8),       # config-5 grid, four pairs
+    ((24, 40, 40), 2, 21, 3, 16, 5),      # a quad + an odd one (pairs: two + odd)
+    ((64, 64, 64), 12, 6, 4, 9, 8),       # config-5 grid, two quads
     ((9, 70, 20), 1, 70, 1, 13, 2),       # many columns: 64-slot chunks with many short columns
+    ((16, 12, 48), 3, 17, 20, 32, 7),     # r3 up to 32 = a full 32-slot chunk; quad + pair + odd
+    ((8, 8, 64), 2, 9, 33, 40, 6),        # r3 > 32: no quads, three pairs
 ])
 def test_adjoint_rhs_pairs(oracle, product, monkeypatch, dims, q, m, rmin, rmax, p):
-    """The two-right-hand-side adjoint (adj_tc2_kernel: W once per column for
-    a pair, 64-slot chunks) against the oracle and against the single-RHS
-    kernel (TMB_ADJ_NR1=1)."""
+    """The multi-right-hand-side adjoint (adj_tc2_kernel<NR>: W once per
+    column for a quad / pair, 32- / 64-slot chunks) against the oracle and against the single-RHS kernel."""
     O, P = oracle, product
     cc = ragged_store(dims, q, m, rmin, rmax, seed=13 * m + p)
     ref = O.OracleStore(cc.rounded_c64())
     ds = P.DeviceStore.from_compressed(cc, "c64")
     phi = cn01(cc.rows, p, 41).astype(np.complex64).astype(np.complex128)
+    z4 = ds.adjoint(phi)
+    monkeypatch.setenv("TMB_ADJ_NR", "2")
     z2 = ds.adjoint(phi)
-    monkeypatch.setenv("TMB_ADJ_NR1", "1")
+    monkeypatch.setenv("TMB_ADJ_NR", "1")
     z1 = ds.adjoint(phi)
-    monkeypatch.delenv("TMB_ADJ_NR1")
+    monkeypatch.delenv("TMB_ADJ_NR")
     z_ref = ref.adjoint(phi)
+    assert rel(z4, z_ref) <= 1e-5
     assert rel(z2, z_ref) <= 1e-5
     assert rel(z1, z_ref) <= 1e-5
-    assert rel(z2, z1) <= 1e-6
+    for z in (z4, z2):
+        assert rel(z, z1) <= 1e-6
 
 
 @pytest.mark.parametrize("chain", ["", "1", "3", "48"])
