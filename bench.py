@@ -149,6 +149,27 @@ def f16_peak_tflops(torch):
     return best
 
 
+def fp64_peak_tflops(torch):
+    """cuBLAS DGEMM 8192^3 throughput (best of 5): the FP64 roofline
+    denominator of the complex128 (CUDA-core DFMA) kernels."""
+    n = 8192
+    a = torch.randn(n, n, device="cuda", dtype=torch.float64)
+    b = torch.randn(n, n, device="cuda", dtype=torch.float64)
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a @ b
+        e1.record()
+        e1.synchronize()
+        best = max(best, 2 * n ** 3 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    del a, b
+    return best
+
+
 def fp32_peak_tflops(torch, tf32=False):
     """cuBLAS SGEMM 8192^3 throughput (best of 5): plain FP32 (FFMA) or with
     TF32 tensor cores — the roofline denominators the driver does not measure
@@ -373,6 +394,7 @@ def main():
     peaks = measured_peaks()
     fp32_peak = fp32_peak_tflops(torch) if rank == 0 else None
     f16_peak = f16_peak_tflops(torch) if rank == 0 else None
+    fp64_peak = fp64_peak_tflops(torch) if rank == 0 else None
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -477,6 +499,10 @@ def main():
                                          "for the 3-product fp16 split; cuBLAS fp16 GEMM in this run: %.1f TFLOP/s"
                                          % (bf16, f16_peak))
             kernels = ("fwd_tc_kernel", "adj_tc_kernel (+ absmax, adj_split_phi_kernel, adj_reduce_kernel)")
+        elif cfg.dtype == "c128":
+            peak = fp64_peak
+            bound, unit_src = "fp64", "measured here: cuBLAS DGEMM 8192^3 (the c128 kernels run DFMA)"
+            kernels = ("fwd_cc_kernel", "adj_cc_kernel (+ adj_reduce_kernel)")
         else:
             peak = fp32_peak
             bound, unit_src = "fp32-ffma", "measured here: cuBLAS SGEMM 8192^3 without TF32"
@@ -490,6 +516,7 @@ def main():
                 "hbm_bytes_algorithmic": int(compressed_bytes(cfg, ranks[c0:c1]) + (c1 - c0) * cfg.p * 8
                                              + nrows * cfg.p * 8),
                 "hbm_peak_gbs": peaks.get("hbm_gbs"), "fp32_ffma_peak_tflops": round(fp32_peak, 2),
+                "fp64_dgemm_tflops_this_run": round(fp64_peak, 2),
                 "f16_gemm_tflops_this_run": round(f16_peak, 2), "bf16_peak_tflops_measured": peaks.get("bf16_tflops")}
 
     cpu = None
