@@ -437,7 +437,7 @@ def main():
         npdt = np.complex64 if cfg.dtype == "c64" else np.complex128
         xh = torch.from_numpy(np.asfortranarray(x_host[c0:c1]).ravel(order="F")).pin_memory()
         yh = torch.empty(nrows * cfg.p, dtype=cdt).pin_memory()
-        ph = phi.t().contiguous().cpu().pin_memory() if world == 1 else None
+        ph = phi.t().contiguous().cpu().pin_memory()  # every rank reads the whole Phi
         zh = torch.empty((c1 - c0) * cfg.p, dtype=cdt).pin_memory()
         e2e_times = []
         h2d = d2h = 0
@@ -455,18 +455,18 @@ def main():
                 d2h = yh.numel() * yh.element_size() + zh.numel() * zh.element_size()
             else:
                 # sharded public API: host x -> device, forward + NCCL reduce,
-                # y -> host on rank 0; host phi -> device on every rank,
-                # adjoint + all-gather, z -> host
+                # y -> host on rank 0; host phi -> device on every rank (each
+                # over its own PCIe link), adjoint + all-gather, z -> host
                 xd = xh.to(dev, non_blocking=True).reshape(cfg.p, -1).t()
                 y = sh.forward(xd)
                 if rank == 0:
                     yh.copy_(y.t().reshape(-1) if y.dim() == 2 else y, non_blocking=True)
-                pd = phi  # Phi H2D counted below (replicated input)
+                pd = ph.to(dev, non_blocking=True).t()
                 z = sh.adjoint(pd)
                 zf = torch.empty(z.numel(), dtype=cdt).pin_memory()
                 zf.copy_(z.t().reshape(-1) if z.dim() == 2 else z, non_blocking=True)
                 torch.cuda.synchronize()
-                h2d = xh.numel() * xh.element_size()
+                h2d = xh.numel() * xh.element_size() + ph.numel() * ph.element_size()
                 d2h = (yh.numel() * yh.element_size() if rank == 0 else 0) + zf.numel() * zf.element_size()
             torch.cuda.synchronize()
             dt = (time.perf_counter() - t0) * 1e3
@@ -477,7 +477,7 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": tt.item(), "unit": "ms", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
         if world > 1:
-            e2e["note"] = "multi-GPU e2e uses the sharded Python API; Phi is replicated device-resident"
+            e2e["note"] = "multi-GPU e2e uses the sharded Python API; byte counts are rank 0's"
 
     # --- roofline of the dominant kernels (one tensor-core launch per forward;
     # the adjoint is Phi split + tensor-core kernel + partial reduction) ------
