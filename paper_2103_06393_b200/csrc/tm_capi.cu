@@ -535,6 +535,24 @@ tm_store* create_store(const tm_store_desc& d, int device, int dtype, const tmb_
 constexpr size_t kSmemBudget = 100 * 1024;  // 2 CTAs / SM
 constexpr size_t kSmemMax = 227 * 1024;
 
+// Parts per tile for a launch of `tiles` (< one wave of `wave` CTAs) tiles:
+// the split s in [1, smax] that minimises the launch's rounds per part,
+// ceil(tiles s / wave) / s (a 96-tile launch on 148 CTAs: s = 3, two rounds
+// of thirds = 2/3 of a tile; s = 1 leaves 52 CTAs idle for a whole tile).
+int best_split(int64_t tiles, int64_t wave, int smax) {
+    if (tiles <= 0 || tiles >= wave) return 1;
+    int best = 1;
+    double bt = 1.0;
+    for (int sp = 2; sp <= smax; ++sp) {
+        const double t = double((tiles * sp + wave - 1) / wave) / sp;
+        if (t < bt - 1e-9) {
+            bt = t;
+            best = sp;
+        }
+    }
+    return best;
+}
+
 template <typename C, int RM, int CN, int NW, int TI1>
 struct CcPlan {
     static constexpr int ROWS = RM * NW, TI2 = ROWS / TI1, TI3 = 32 * CN;
@@ -690,8 +708,9 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
     CK(cudaFuncSetAttribute(fwd_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     CK(cudaFuncSetAttribute(fwd_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // grid: CTAs; a wave covers `wave` tiles (pair tiles in pair mode)
-    const unsigned grid = g.pair ? unsigned(std::min<int64_t>(2 * g.ntiles, nsm & ~1))
-                                 : unsigned(std::min<int64_t>(g.ntiles, nsm));
+    // (up to 8 parts per tile when there are fewer tiles than SMs: best_split)
+    const unsigned grid = g.pair ? unsigned(std::min<int64_t>(2 * 8 * g.ntiles, nsm & ~1))
+                                 : unsigned(std::min<int64_t>(8 * g.ntiles, nsm));
     const int64_t wave = g.pair ? grid / 2 : grid;
     g.prof = nullptr;
     if (g.debug & 8) {
@@ -734,11 +753,8 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
         const int64_t tiles = std::min<int64_t>(g.ntiles - t0, wave);
         // A final partial wave splits each tile's columns into parts (partial tiles
         // to ypart, summed by fwd_split_reduce_kernel) so the launch fills the GPU.
-        g.split = 1;
-        if (tiles < wave && tiles * 2 <= wave) {
-            g.split = int(std::min<int64_t>({int64_t(8), wave / tiles, std::max<int64_t>(1, s->ncols)}));
-            if (const char* e = std::getenv("TMB_FWD_NOSPLIT")) if (*e && *e != '0') g.split = 1;
-        }
+        g.split = best_split(tiles, wave, int(std::min<int64_t>(8, std::max<int64_t>(1, s->ncols))));
+        if (const char* e = std::getenv("TMB_FWD_NOSPLIT")) if (*e && *e != '0') g.split = 1;
         g.tile0 = t0;
         g.t_begin = 0;
         g.t_end = tiles * g.split;
@@ -987,10 +1003,10 @@ void launch_adj_groups(tm_store* s, const AjGeom& g, const CUtensorMap& amap, in
     const size_t smem2 = adj_group_smem<NR>(g.slot_bytes);
     if (smem2 > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: shared-memory plan too large");
     CK(cudaFuncSetAttribute(adj_tc2_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
-    const unsigned grid2 = unsigned(std::min<int64_t>(ngrp * tpg, nsm));
+    const unsigned grid2 = unsigned(std::min<int64_t>(8 * ngrp * tpg, nsm));
     for (int64_t t0 = grp0 * tpg; t0 < g2.ntiles; t0 += grid2) {
         const int64_t tiles = std::min<int64_t>(g2.ntiles - t0, int64_t(grid2));
-        g2.split = tiles < int64_t(grid2) ? int(std::max<int64_t>(1, std::min<int64_t>(8, grid2 / tiles))) : 1;
+        g2.split = best_split(tiles, int64_t(grid2), 8);
         g2.tile0 = t0;
         g2.t_begin = 0;
         g2.t_end = tiles * g2.split;
@@ -1080,8 +1096,9 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     float2* part = static_cast<float2*>(s->part.get(size_t(s->ncols * p * nred) * sizeof(float2)));
     CK(cudaFuncSetAttribute(adj_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     CK(cudaFuncSetAttribute(adj_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    const unsigned grid = g.pair ? unsigned(std::min<int64_t>(2 * g.ntiles, nsm & ~1))
-                                 : unsigned(std::min<int64_t>(g.ntiles, nsm));
+    // (up to 8 parts per tile when there are fewer tiles than SMs: best_split)
+    const unsigned grid = g.pair ? unsigned(std::min<int64_t>(2 * 8 * g.ntiles, nsm & ~1))
+                                 : unsigned(std::min<int64_t>(8 * g.ntiles, nsm));
     const int64_t wave = g.pair ? grid / 2 : grid;
     const int64_t tpb = g.nrt >> g.pair;  // tiles per (rhs, component) block
     int64_t bready = hp ? 0 : nblk;
@@ -1113,7 +1130,7 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
         const int64_t tiles = std::min<int64_t>(g.ntiles - t0, wave);
         // a final partial wave splits each tile's chunk range into parts so the
         // launch still fills the GPU (partials are per column: no extra reduction)
-        g.split = tiles < wave ? int(std::max<int64_t>(1, std::min<int64_t>(8, wave / tiles))) : 1;
+        g.split = best_split(tiles, wave, 8);
         if (const char* e = std::getenv("TMB_ADJ_NOSPLIT")) if (*e && *e != '0') g.split = 1;
         g.tile0 = t0;
         g.t_begin = 0;
