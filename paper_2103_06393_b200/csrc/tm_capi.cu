@@ -158,6 +158,7 @@ struct tm_store {
     std::mutex mu;
     DevBuf part, xin, yout, wbuf, phiplanes, xplanes, rsum, scal;
     DevBuf ypart;  // partial tiles of a split final wave of the tensor-core forward
+    DevBuf ccpart;  // partial y blocks of a column-split CUDA-core forward (small stores)
 
     int64_t nv() const { return dims[0] * dims[1] * dims[2]; }
     int64_t rows() const { return q * nv(); }
@@ -553,6 +554,8 @@ int best_split(int64_t tiles, int64_t wave, int smax) {
     return best;
 }
 
+int num_sms(int dev);
+
 template <typename C, int RM, int CN, int NW, int TI1>
 struct CcPlan {
     static constexpr int ROWS = RM * NW, TI2 = ROWS / TI1, TI3 = 32 * CN;
@@ -581,28 +584,59 @@ struct CcPlan {
                               std::to_string(g.rmax3) + ") exceed the shared-memory plan of the CUDA-core kernel");
         g.jb = jb;
         smem = slot * jb + red;
-        grid = dim3(unsigned(int64_t(g.nt1) * g.nt2 * nt3), unsigned(s->q), 1);
+        g.ntiles = int(int64_t(g.nt1) * g.nt2 * nt3);
+        g.nsplit = 1;
+        g.part_stride = 0;
+        grid = dim3(unsigned(g.ntiles), unsigned(s->q), 1);
+    }
+    // Small stores (tiles x q x p below two CTAs per SM): split each tile's
+    // column loop into parts so the launch fills the GPU (config 1: 54 CTAs).
+    void split_for(int64_t p, int nsm) {
+        const int64_t ctas = int64_t(g.ntiles) * g.q * std::min<int64_t>(p, 65535);
+        if (ctas >= 2 * int64_t(nsm) || g.ncols < 2) return;
+        g.nsplit = int(std::min<int64_t>({int64_t(16), g.ncols, (2 * int64_t(nsm) + ctas - 1) / ctas}));
+        grid.x = unsigned(int64_t(g.ntiles) * g.nsplit);
     }
 };
 
 template <typename C, int RM, int CN, int NW, int TI1>
-void run_forward_cc(const tm_store* s, const C* x, int64_t ldx, int64_t p, C* y, int64_t ldy, cudaStream_t st) {
+void run_forward_cc(tm_store* s, const C* x, int64_t ldx, int64_t p, C* y, int64_t ldy, cudaStream_t st) {
     CcPlan<C, RM, CN, NW, TI1> plan(s, false);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    plan.split_for(p, num_sms(dev));
     auto kern = fwd_cc_kernel<C, RM, CN, NW, TI1>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan.smem)));
+    const int64_t rows = s->q * s->nv();
     for (int64_t c0 = 0; c0 < p; c0 += 65535) {
         dim3 grid = plan.grid;
-        grid.z = unsigned(std::min<int64_t>(65535, p - c0));
-        kern<<<grid, NW * 32, plan.smem, st>>>(s->d_desc, static_cast<const C*>(s->d_arena), plan.g, x + ldx * c0, ldx,
-                                               y + ldy * c0, ldy);
-        launched(cudaSuccess, "fwd_cc_kernel");
+        const int64_t pc = std::min<int64_t>(65535, p - c0);
+        grid.z = unsigned(pc);
+        if (plan.g.nsplit > 1) {  // partial y per part, then a fixed-order sum
+            CcGeom g = plan.g;
+            g.part_stride = rows * pc;
+            C* yp = static_cast<C*>(s->ccpart.get(size_t(g.nsplit) * size_t(rows * pc) * sizeof(C)));
+            kern<<<grid, NW * 32, plan.smem, st>>>(s->d_desc, static_cast<const C*>(s->d_arena), g, x + ldx * c0,
+                                                   ldx, yp, rows);
+            launched(cudaSuccess, "fwd_cc_kernel");
+            const unsigned rb = unsigned(std::min<int64_t>((rows * pc + 255) / 256, 4096));
+            cc_split_reduce_kernel<C><<<rb, 256, 0, st>>>(yp, g.nsplit, g.part_stride, rows, pc, y + ldy * c0, ldy);
+            launched(cudaSuccess, "cc_split_reduce_kernel");
+        } else {
+            kern<<<grid, NW * 32, plan.smem, st>>>(s->d_desc, static_cast<const C*>(s->d_arena), plan.g, x + ldx * c0,
+                                                   ldx, y + ldy * c0, ldy);
+            launched(cudaSuccess, "fwd_cc_kernel");
+        }
     }
 }
 
 template <typename C, int RM, int CN, int NW, int TI1>
 void run_adjoint_cc(tm_store* s, const C* phi, int64_t ldphi, int64_t p, C* z, int64_t ldz, cudaStream_t st) {
     CcPlan<C, RM, CN, NW, TI1> plan(s, true);
-    const int64_t ntiles = plan.grid.x;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    plan.split_for(p, num_sms(dev));
+    const int64_t ntiles = plan.g.ntiles;
     const int64_t nred = ntiles * s->q;
     C* part = static_cast<C*>(s->part.get(size_t(s->ncols * p * nred) * sizeof(C)));
     auto kern = adj_cc_kernel<C, RM, CN, NW, TI1>;

@@ -36,7 +36,16 @@ struct CcGeom {
     int nt1, nt2;     // tile counts along modes 1 and 2
     int rmax1, rmax2, rmax3;
     int jb;           // columns staged per shared-memory round
+    int ntiles;       // nt1 * nt2 * nt3: blockIdx.x = tile + ntiles * part
+    int nsplit;       // column ranges per tile (> 1 when tiles x q x p < the SMs)
+    int64_t part_stride;  // forward with nsplit > 1: elements between the parts' partial y blocks
 };
+
+// Column range [ja, jz) of split part `part` (contiguous, balanced by count).
+__device__ __forceinline__ void cc_columns(const CcGeom& g, int part, int64_t& ja, int64_t& jz) {
+    ja = g.ncols * part / g.nsplit;
+    jz = g.ncols * (part + 1) / g.nsplit;
+}
 
 // Shared-memory plan (elements of C) for one staged column.
 template <int TI1, int TI2, int TI3>
@@ -140,15 +149,18 @@ __global__ void __launch_bounds__(NW * 32)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* smem = reinterpret_cast<C*>(smem_raw);
 
-    const int t1 = blockIdx.x % g.nt1;
-    const int t2 = (blockIdx.x / g.nt1) % g.nt2;
-    const int t3 = blockIdx.x / (g.nt1 * g.nt2);
+    const int tile = int(blockIdx.x % unsigned(g.ntiles)), part = int(blockIdx.x / unsigned(g.ntiles));
+    const int t1 = tile % g.nt1;
+    const int t2 = (tile / g.nt1) % g.nt2;
+    const int t3 = tile / (g.nt1 * g.nt2);
     const int k = blockIdx.y;
     const int c = blockIdx.z;
     const int i1_0 = t1 * TI1, i2_0 = t2 * TI2, i3_0 = t3 * TI3;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t slot = cc_slot_elems<TI1, TI2, TI3>(g.rmax1, g.rmax2, g.rmax3);
     const C* xc = x + ldx * c;
+    int64_t ja, jz;
+    cc_columns(g, part, ja, jz);
 
     C acc[RM][CN];
 #pragma unroll
@@ -156,8 +168,8 @@ __global__ void __launch_bounds__(NW * 32)
 #pragma unroll
         for (int b = 0; b < CN; ++b) acc[a][b] = cmake<C>(R(0), R(0));
 
-    for (int64_t j0 = 0; j0 < g.ncols; j0 += g.jb) {
-        const int nj = int(g.ncols - j0 < int64_t(g.jb) ? g.ncols - j0 : int64_t(g.jb));
+    for (int64_t j0 = ja; j0 < jz; j0 += g.jb) {
+        const int nj = int(jz - j0 < int64_t(g.jb) ? jz - j0 : int64_t(g.jb));
         cc_stage_chunk<C, TI1, TI2, TI3, NT>(td, arena, g, k, j0, nj, i1_0, i2_0, i3_0, smem, slot,
                                              [&](int64_t j) { return xc[j]; });
         for (int jj = 0; jj < nj; ++jj) {
@@ -181,9 +193,10 @@ __global__ void __launch_bounds__(NW * 32)
         __syncthreads();  // smem is restaged by the next chunk
     }
 
-    // --- epilogue: y[k n_v + i1 + n1 (i2 + n2 i3), c] ---------------------------
+    // --- epilogue: y[k n_v + i1 + n1 (i2 + n2 i3), c] (a split part: its
+    // partial block, summed in part order by cc_split_reduce_kernel) ------------
     const int64_t nv = int64_t(g.n1) * g.n2 * g.n3;
-    C* yc = y + ldy * c + int64_t(k) * nv;
+    C* yc = y + g.part_stride * part + ldy * c + int64_t(k) * nv;
 #pragma unroll
     for (int a = 0; a < RM; ++a) {
         const int row = warp * RM + a;
@@ -212,8 +225,8 @@ __global__ void __launch_bounds__(NW * 32)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* smem = reinterpret_cast<C*>(smem_raw);
 
-    const int ntiles = gridDim.x;
-    const int tile = blockIdx.x;
+    const int ntiles = g.ntiles;
+    const int tile = int(blockIdx.x % unsigned(ntiles)), part_id = int(blockIdx.x / unsigned(ntiles));
     const int t1 = tile % g.nt1;
     const int t2 = (tile / g.nt1) % g.nt2;
     const int t3 = tile / (g.nt1 * g.nt2);
@@ -241,9 +254,11 @@ __global__ void __launch_bounds__(NW * 32)
         }
     }
     const C one = cmake<C>(R(1), R(0));
+    int64_t ja, jz;  // this part's columns (each column's partials come from exactly one part)
+    cc_columns(g, part_id, ja, jz);
 
-    for (int64_t j0 = 0; j0 < g.ncols; j0 += g.jb) {
-        const int nj = int(g.ncols - j0 < int64_t(g.jb) ? g.ncols - j0 : int64_t(g.jb));
+    for (int64_t j0 = ja; j0 < jz; j0 += g.jb) {
+        const int nj = int(jz - j0 < int64_t(g.jb) ? jz - j0 : int64_t(g.jb));
         cc_stage_chunk<C, TI1, TI2, TI3, NT>(td, arena, g, k, j0, nj, i1_0, i2_0, i3_0, smem, slot,
                                              [&](int64_t) { return one; });
         for (int jj = 0; jj < nj; ++jj) {
@@ -285,6 +300,24 @@ __global__ void __launch_bounds__(NW * 32)
         // the next chunk's first __syncthreads (after its loads) orders these
         // reads of `red` before it is rewritten
         static_assert(JBMAX >= 1, "");
+    }
+}
+
+// Forward with split columns: y[row + ldy c] = sum_s yp[s stride + rows c + row],
+// in part order (deterministic).
+template <typename C>
+__global__ void cc_split_reduce_kernel(const C* __restrict__ yp, int nsplit, int64_t stride, int64_t rows, int64_t p,
+                                       C* __restrict__ y, int64_t ldy) {
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * p;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t c = e / rows, r = e - c * rows;
+        C acc = yp[e];
+        for (int sp = 1; sp < nsplit; ++sp) {
+            const C v = yp[sp * stride + e];
+            acc.x += v.x;
+            acc.y += v.y;
+        }
+        y[r + ldy * c] = acc;
     }
 }
 
