@@ -736,6 +736,7 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
                (2 * TC_NST_MAX + 2 * TC_JR + 2) * 8 + 16;
     };
     g.nst = TC_NST_MAX;
+    if (const char* e = std::getenv("TMB_TC_NST")) if (std::atoi(e) >= 2) g.nst = std::min(TC_NST_MAX, std::atoi(e));
     while (g.nst > 2 && smem_for(g.nst) > kSmemMax) --g.nst;
     const size_t smem = smem_for(g.nst);
     if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core forward: shared-memory plan too large");
