@@ -71,6 +71,12 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi takes a moment to start: wait for its first line so a
+            # short timed region is still sampled, then keep only in-region lines
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.02)
+            self.lines = []
         except Exception:
             self.proc = None
 
@@ -81,6 +87,10 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        if not self.lines:  # region shorter than one period: one more sample at its end
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 0.5:
+                time.sleep(0.01)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -332,10 +342,18 @@ def main():
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    # TMB_BENCH_SMOKE_1GPU=1: a functional check of the N > 1 code path on a
+    # one-GPU box (every rank on cuda:0, gloo collectives); never a measurement.
+    smoke1 = os.environ.get("TMB_BENCH_SMOKE_1GPU", "0") == "1"
+    if smoke1:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if smoke1:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     from paper_2103_06393_b200 import DeviceStore, launch_count
     from paper_2103_06393_b200.sharded import ShardedStore, balanced_shards, column_costs
