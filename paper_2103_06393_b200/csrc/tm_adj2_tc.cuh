@@ -37,16 +37,17 @@ struct A2 {
 // Tile of a pass over right-hand-side groups: item -> (group cp, component k,
 // row tile rt), i2 block fastest as in aj_tile.
 template <int NR>
-__device__ __forceinline__ AjTile aj2_tile(const AjGeom& g, int64_t item) {
+__device__ __forceinline__ AjTile aj2_tile(const AjGeom& g, int64_t item, uint32_t rank = 0) {
     AjTile r;
     const int64_t t = g.tile0 + item / g.split;
     r.part = int(item % g.split);
-    const int64_t per_c = int64_t(g.q) * g.nrt;
+    const int64_t tpk = g.nrt >> g.pair;  // (pair) tiles per component
+    const int64_t per_c = int64_t(g.q) * tpk;
     const int64_t cp = t / per_c;
     r.c = int(NR * cp);
     int64_t rem = t - cp * per_c;
-    r.k = int(rem / g.nrt);
-    r.rt = rem - int64_t(r.k) * g.nrt;
+    r.k = int(rem / tpk);
+    r.rt = ((rem - int64_t(r.k) * tpk) << g.pair) + rank;  // a pair tile = row tiles 2 pt, 2 pt + 1
     const int t1 = int(r.rt / g.nt2), t2 = int(r.rt - int64_t(t1) * g.nt2);
     r.i1_0 = t1 * TC_TI1;
     r.i2_0 = t2 * TC_TI2;
@@ -101,7 +102,11 @@ __device__ __forceinline__ void aj2_consume_column(const float2* __restrict__ V,
     }
 }
 
-template <int NR>
+// PAIR: CTA pairs (cta_group::2, M = 256 over two row tiles) as in
+// adj_tc_kernel: each N = 2 CH window [-U3i | U3r] / [U3r | U3i] takes its
+// first CH rows from the even CTA and the rest from the odd one, so a CTA
+// stages 4 of the 6 U3 planes' halves and reads half of B per MMA.
+template <int NR, bool PAIR>
 __global__ void __launch_bounds__(AJ_THREADS, 1)
     adj_tc2_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                    const TcDesc* __restrict__ tcd, const float2* __restrict__ varena,
@@ -110,7 +115,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
     using namespace sm100;
     using P = A2<NR>;
     constexpr int A2_CH = P::CH, A2_NST = P::NST, A2_A_STAGE = P::A_STAGE, A2_B_PLANE = P::B_PLANE,
-                  A2_B_STAGE = P::B_STAGE;
+                  A2_B_STAGE = PAIR ? 4 * P::B_PLANE : P::B_STAGE;
     extern __shared__ __align__(1024) unsigned char a2_smem_raw[];
     unsigned char* sm = a2_smem_raw + ((1024u - (smem_u32(a2_smem_raw) & 1023u)) & 1023u);
     unsigned char* sA = sm;
@@ -127,8 +132,9 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qfree + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t tstart = g.t_begin + blockIdx.x;
-    const int64_t tstep = gridDim.x;
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    const int64_t tstart = g.t_begin + (PAIR ? (blockIdx.x >> 1) : blockIdx.x);
+    const int64_t tstep = PAIR ? (gridDim.x >> 1) : gridDim.x;
     if (threadIdx.x == 0) {
         for (int s = 0; s < A2_NST; ++s) {
             mbar_init(&full[s], 1);
@@ -140,17 +146,23 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&qfull[s], 1);
-            mbar_init(&qfree[s], AJ_NPW);
+            mbar_init(&qfree[s], AJ_NPW * (PAIR ? 2 : 1));  // PAIR: the peer's consumers too
         }
         fence_mbar_init();
     }
-    if (warp == 3) tmem_alloc(tmem_slot, 512);
+    if (warp == 3) {
+        if (PAIR)
+            tmem_alloc_pair(tmem_slot, 512);
+        else
+            tmem_alloc(tmem_slot, 512);
+    }
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&amap);
         tma_prefetch_desc(&bmap);
     }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -159,25 +171,43 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
-                const AjTile tl = aj2_tile<NR>(g, t);
+                const AjTile tl = aj2_tile<NR>(g, t, rank);
                 int n0, n1;
                 aj_chunks(g, tl, nch[tl.k], n0, n1);
                 const int arow = int(tl.rt * TC_ROWS);
                 for (int n = n0; n < n1; ++n) {
                     for (int kk = 0; kk < g.nks; ++kk) {
                         mbar_wait_backoff(&empty[s], ph ^ 1, 64);
-                        mbar_arrive_expect_tx(&full[s], uint32_t(A2_A_STAGE + A2_B_STAGE));
                         unsigned char* da = sA + s * A2_A_STAGE;
                         unsigned char* db = sB + s * A2_B_STAGE;
+                        if (PAIR) {
+                            // both CTAs' bytes complete on the even CTA's barrier
+                            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2u * uint32_t(A2_A_STAGE + A2_B_STAGE));
+                            const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
 #pragma unroll
-                        for (int rr = 0; rr < NR; ++rr)
+                            for (int rr = 0; rr < NR; ++rr)
 #pragma unroll
-                            for (int pl = 0; pl < AJ_APLANES; ++pl)
-                                tma_load_3d(da + (rr * AJ_APLANES + pl) * AJ_A_PLANE, &amap, &full[s], kk * 16, arow,
-                                            (pl * g.p + tl.c + rr) * g.q + tl.k);
+                                for (int pl = 0; pl < AJ_APLANES; ++pl)
+                                    tma_load_3d_pair(da + (rr * AJ_APLANES + pl) * AJ_A_PLANE, &amap, fb, kk * 16,
+                                                     arow, (pl * g.p + tl.c + rr) * g.q + tl.k);
+                            // smem B slots (W1 hi, W2 hi, W1 lo, W2 lo) <- planes rank + {0, 1} (+3 for lo)
 #pragma unroll
-                        for (int pl = 0; pl < TC_BPLANES; ++pl)
-                            tma_load_3d(db + pl * A2_B_PLANE, &bmap, &full[s], kk * 16, n * A2_CH, pl * g.q + tl.k);
+                            for (int sl = 0; sl < 4; ++sl)
+                                tma_load_3d_pair(db + sl * A2_B_PLANE, &bmap, fb, kk * 16, n * A2_CH,
+                                                 (int(rank) + (sl & 1) + 3 * (sl >> 1)) * g.q + tl.k);
+                        } else {
+                            mbar_arrive_expect_tx(&full[s], uint32_t(A2_A_STAGE + A2_B_STAGE));
+#pragma unroll
+                            for (int rr = 0; rr < NR; ++rr)
+#pragma unroll
+                                for (int pl = 0; pl < AJ_APLANES; ++pl)
+                                    tma_load_3d(da + (rr * AJ_APLANES + pl) * AJ_A_PLANE, &amap, &full[s], kk * 16,
+                                                arow, (pl * g.p + tl.c + rr) * g.q + tl.k);
+#pragma unroll
+                            for (int pl = 0; pl < TC_BPLANES; ++pl)
+                                tma_load_3d(db + pl * A2_B_PLANE, &bmap, &full[s], kk * 16, n * A2_CH,
+                                            pl * g.q + tl.k);
+                        }
                         if (++s == A2_NST) {
                             s = 0;
                             ph ^= 1;
@@ -188,11 +218,11 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer
-        if (elect_one()) {
-            const uint32_t idesc = umma_idesc_f16(TC_ROWS, 2 * A2_CH, false, false);
+        if ((!PAIR || rank == 0) && elect_one()) {
+            const uint32_t idesc = umma_idesc_f16(TC_ROWS * (PAIR ? 2 : 1), 2 * A2_CH, false, false);
             uint32_t s = 0, ph = 0, nq = 0;
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
-                const AjTile tl = aj2_tile<NR>(g, t);
+                const AjTile tl = aj2_tile<NR>(g, t, rank);
                 int n0, n1;
                 aj_chunks(g, tl, nch[tl.k], n0, n1);
                 for (int n = n0; n < n1; ++n, ++nq) {
@@ -205,10 +235,11 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                         const uint32_t a0 = smem_u32(sA + s * A2_A_STAGE);
                         const uint32_t b0 = smem_u32(sB + s * A2_B_STAGE);
                         // B windows: [-U3i|U3r] at plane 0 / 3 (hi / lo), [U3r|U3i] at plane 1 / 4
+                        // (PAIR: smem slots 0 / 2 and 1 / 3 of each CTA, half a window each)
                         const uint64_t B2h = umma_smem_desc(b0 + 0 * A2_B_PLANE, 256, 6);
                         const uint64_t B1h = umma_smem_desc(b0 + 1 * A2_B_PLANE, 256, 6);
-                        const uint64_t B2l = umma_smem_desc(b0 + 3 * A2_B_PLANE, 256, 6);
-                        const uint64_t B1l = umma_smem_desc(b0 + 4 * A2_B_PLANE, 256, 6);
+                        const uint64_t B2l = umma_smem_desc(b0 + (PAIR ? 2 : 3) * A2_B_PLANE, 256, 6);
+                        const uint64_t B1l = umma_smem_desc(b0 + (PAIR ? 3 : 4) * A2_B_PLANE, 256, 6);
                         const uint32_t acc = kk > 0 ? 1u : 0u;
 #pragma unroll
                         for (int rr = 0; rr < NR; ++rr) {
@@ -217,20 +248,28 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                             for (int pl = 0; pl < 4; ++pl)
                                 A[pl] = umma_smem_desc(a0 + (rr * AJ_APLANES + pl) * AJ_A_PLANE, 256, 6);
                             const uint32_t qd = tmem + qb * 256u + uint32_t(rr * 2 * A2_CH);
-                            mma_f16(qd, A[0], B2h, idesc, acc);
-                            mma_f16(qd, A[0], B2l, idesc, 1);
-                            mma_f16(qd, A[1], B2h, idesc, 1);
-                            mma_f16(qd, A[2], B1h, idesc, 1);
-                            mma_f16(qd, A[2], B1l, idesc, 1);
-                            mma_f16(qd, A[3], B1h, idesc, 1);
+#define MMA(...) (PAIR ? mma_f16_pair(__VA_ARGS__) : mma_f16(__VA_ARGS__))
+                            MMA(qd, A[0], B2h, idesc, acc);
+                            MMA(qd, A[0], B2l, idesc, 1);
+                            MMA(qd, A[1], B2h, idesc, 1);
+                            MMA(qd, A[2], B1h, idesc, 1);
+                            MMA(qd, A[2], B1l, idesc, 1);
+                            MMA(qd, A[3], B1h, idesc, 1);
+#undef MMA
                         }
-                        mma_commit(&empty[s]);
+                        if (PAIR)
+                            mma_commit_pair(&empty[s]);
+                        else
+                            mma_commit(&empty[s]);
                         if (++s == A2_NST) {
                             s = 0;
                             ph ^= 1;
                         }
                     }
-                    mma_commit(&qfull[qb]);
+                    if (PAIR)
+                        mma_commit_pair(&qfull[qb]);
+                    else
+                        mma_commit(&qfull[qb]);
                 }
             }
         }
@@ -240,7 +279,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
-                const AjTile tl = aj2_tile<NR>(g, t);
+                const AjTile tl = aj2_tile<NR>(g, t, rank);
                 const TcDesc* tdk = tcd + int64_t(tl.k) * g.ncols;
                 int n0, n1;
                 aj_chunks(g, tl, nch[tl.k], n0, n1);
@@ -272,7 +311,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
         const uint32_t lane_addr = uint32_t(i1l * 32) << 16;
         uint32_t fs = 0, fph = 0, nq = 0;
         for (int64_t t = tstart; t < g.t_end; t += tstep) {
-            const AjTile tl = aj2_tile<NR>(g, t);
+            const AjTile tl = aj2_tile<NR>(g, t, rank);
             int n0, n1;
             aj_chunks(g, tl, nch[tl.k], n0, n1);
             const int* cs = cstart + int64_t(tl.k) * (g.maxch + 1);
@@ -325,7 +364,12 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&qfree[qb]);
+                if (lane == 0) {
+                    if (PAIR)
+                        mbar_arrive_cluster(mapa_shared(smem_u32(&qfree[qb]), 0));
+                    else
+                        mbar_arrive(&qfree[qb]);
+                }
                 named_bar_sync(1, AJ_NPW * 32);  // all partials of the chunk are in rb
                 for (int e = ctid; e < NR * (j1 - j0); e += AJ_NPW * 32) {
                     const int rr = e / (j1 - j0), jj = e - rr * (j1 - j0);
@@ -343,7 +387,13 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 3) tmem_dealloc(tmem, 512);
+    if (PAIR) cluster_sync();  // the peer no longer arrives on this CTA's barriers / uses the pair's TMEM
+    if (warp == 3) {
+        if (PAIR)
+            tmem_dealloc_pair(tmem, 512);
+        else
+            tmem_dealloc(tmem, 512);
+    }
 }
 
 }  // namespace tmb

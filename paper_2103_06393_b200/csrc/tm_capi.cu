@@ -1017,11 +1017,12 @@ bool ensure_adj_pack(tm_store* s, int which) {
     return true;
 }
 
-// Shared-memory plan of adj_tc2_kernel<NR>.
+// Shared-memory plan of adj_tc2_kernel<NR, PAIR> (PAIR stages 4 of the 6 U3 planes' halves).
 template <int NR>
-size_t adj_group_smem(int slot_bytes) {
+size_t adj_group_smem(int slot_bytes, bool pair = false) {
     using P = A2<NR>;
-    return 1024 + size_t(P::NST) * (P::A_STAGE + P::B_STAGE) + size_t(TC_JR) * slot_bytes +
+    const size_t bstage = pair ? size_t(4) * P::B_PLANE : size_t(P::B_STAGE);
+    return 1024 + size_t(P::NST) * (P::A_STAGE + bstage) + size_t(TC_JR) * slot_bytes +
            size_t(P::RED) * sizeof(float2) + (2 * P::NST + 2 * TC_JR + 4) * 8 + 16;
 }
 
@@ -1030,29 +1031,54 @@ template <int NR>
 void launch_adj_groups(tm_store* s, const AjGeom& g, const CUtensorMap& amap, int64_t grp0, int64_t ngrp,
                        const float* phimax, float2* part, int nsm, cudaStream_t st) {
     const auto& ap = s->adjp[NR == 2 ? 0 : 1];
-    AjGeom g2 = g;
-    g2.pair = 0;
+    AjGeom g2 = g;  // g.pair: CTA pairs over two row tiles (nrt even), as the single-RHS kernel
     g2.maxch = ap.maxch;
-    const int64_t tpg = int64_t(g.q) * g.nrt;  // tiles per group
+    const int64_t tpg = int64_t(g.q) * (g.nrt >> g2.pair);  // (pair) tiles per group
     g2.ntiles = (grp0 + ngrp) * tpg;
-    const size_t smem2 = adj_group_smem<NR>(g.slot_bytes);
+    const size_t smem2 = adj_group_smem<NR>(g.slot_bytes, g2.pair != 0);
     if (smem2 > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: shared-memory plan too large");
-    CK(cudaFuncSetAttribute(adj_tc2_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
-    const unsigned grid2 = unsigned(std::min<int64_t>(8 * ngrp * tpg, nsm));
-    for (int64_t t0 = grp0 * tpg; t0 < g2.ntiles; t0 += grid2) {
-        const int64_t tiles = std::min<int64_t>(g2.ntiles - t0, int64_t(grid2));
-        g2.split = best_split(tiles, int64_t(grid2), 8);
+    CK(cudaFuncSetAttribute(adj_tc2_kernel<NR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+    CK(cudaFuncSetAttribute(adj_tc2_kernel<NR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+    const unsigned grid2 = g2.pair ? unsigned(std::min<int64_t>(2 * 8 * ngrp * tpg, nsm & ~1))
+                                   : unsigned(std::min<int64_t>(8 * ngrp * tpg, nsm));
+    const int64_t wave = g2.pair ? grid2 / 2 : grid2;
+    for (int64_t t0 = grp0 * tpg; t0 < g2.ntiles; t0 += wave) {
+        const int64_t tiles = std::min<int64_t>(g2.ntiles - t0, wave);
+        g2.split = best_split(tiles, wave, 8);
         g2.tile0 = t0;
         g2.t_begin = 0;
         g2.t_end = tiles * g2.split;
-        adj_tc2_kernel<NR><<<grid2, AJ_THREADS, smem2, st>>>(amap, ap.bmap, s->d_tcd, s->d_varena, s->d_u2arena,
-                                                             ap.d_nch, ap.d_cstart, g2, phimax, part);
-        launched(cudaSuccess, "adj_tc2_kernel");
+        if (g2.pair) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(grid2);
+            cfg.blockDim = dim3(AJ_THREADS);
+            cfg.dynamicSmemBytes = smem2;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            launched(cudaLaunchKernelEx(&cfg, adj_tc2_kernel<NR, true>, amap, ap.bmap,
+                                        static_cast<const TcDesc*>(s->d_tcd), static_cast<const float2*>(s->d_varena),
+                                        static_cast<const float2*>(s->d_u2arena), static_cast<const int*>(ap.d_nch),
+                                        static_cast<const int*>(ap.d_cstart), g2, static_cast<const float*>(phimax),
+                                        part),
+                     "adj_tc2_kernel<pair>");
+        } else {
+            adj_tc2_kernel<NR, false><<<grid2, AJ_THREADS, smem2, st>>>(amap, ap.bmap, s->d_tcd, s->d_varena,
+                                                                        s->d_u2arena, ap.d_nch, ap.d_cstart, g2,
+                                                                        phimax, part);
+            launched(cudaSuccess, "adj_tc2_kernel");
+        }
     }
 }
 
 bool adj_pack_fits(const tm_store* s, int nr, int slot_bytes) {
-    return s->rmax[2] <= 128 / nr && (nr == 4 ? adj_group_smem<4>(slot_bytes) : adj_group_smem<2>(slot_bytes)) <= kSmemMax;
+    return s->rmax[2] <= 128 / nr &&
+           (nr == 4 ? adj_group_smem<4>(slot_bytes) : adj_group_smem<2>(slot_bytes)) <= kSmemMax;
 }
 
 void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, float2* z, int64_t ldz,
