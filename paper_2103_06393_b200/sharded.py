@@ -12,6 +12,12 @@ algorithm has a real exchange step:
   adjoint  z[shard] = Zbc[:, shard]^H phi          -> NCCL all-gather of the
                                                       r-row blocks (m x p total)
 
+An ACA store (Zbc ~ U V^H, aca_forward / aca_adjoint, src/matvec.cpp:150-175)
+shards the r_c U columns with the matching columns of V:
+
+  aca_forward  y = sum_ranks U[:, l] (V[:, l]^H x)  -> reduce, as the forward
+  aca_adjoint  z = sum_ranks V[:, l] (U[:, l]^H phi) -> all-reduce of m2 x p
+
 The class is agnostic of the store type (anything with forward / adjoint /
 rows / ncols), which lets the CPU tests drive the same host logic with gloo.
 """
@@ -79,7 +85,11 @@ class ShardedStore:
         import torch.distributed as dist
 
         xs = x[self.c0:self.c1] if x.shape[0] == self.ncols else x
-        y = self.store.forward(xs)
+        return self._sum(self.store.forward(xs), dst, allreduce)
+
+    def _sum(self, y, dst=0, allreduce=False):
+        import torch.distributed as dist
+
         if self.world > 1:
             # column-major (rows x p) blocks are contiguous as their transpose
             buf = y if y.is_contiguous() else y.t()
@@ -88,6 +98,17 @@ class ShardedStore:
             else:
                 dist.reduce(buf, dst=dst, group=self.group)
         return y
+
+    def aca_forward(self, x, dst=0, allreduce=False):
+        """y = U (V^H x) of an ACA store sharded by U columns (this rank's
+        store holds its U columns and the matching columns of V).  x: (m2 x
+        p), replicated.  The full y on `dst` (every rank with allreduce)."""
+        return self._sum(self.store.aca_forward(x), dst, allreduce)
+
+    def aca_adjoint(self, phi):
+        """z = V (U^H phi) on every rank: the shards' V[:, l] (U[:, l]^H phi)
+        partials (m2 x p each) summed by an all-reduce."""
+        return self._sum(self.store.aca_adjoint(phi), allreduce=True)
 
     def adjoint(self, phi):
         """z = Zbc^H phi on every rank.  phi: (q n_v x p), replicated."""

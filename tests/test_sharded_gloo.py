@@ -1,4 +1,4 @@
-"""Multi-GPU column sharding, host logic on CPU with gloo (world_size 2 and 3).
+"""Multi-GPU column sharding (Tucker and ACA stores), host logic on CPU with gloo (world_size 2 and 3).
 
 Each rank wraps an oracle-backed store over its cost-balanced column shard;
 ShardedStore must reproduce the single-process products: the forward by a
@@ -17,10 +17,11 @@ from conftest import ROOT
 class OracleShard:
     """Store-like wrapper (rows / forward / adjoint on torch CPU tensors)."""
 
-    def __init__(self, cc):
+    def __init__(self, cc, v=None):
         from oracle import oracle as O
         self.st = O.OracleStore(cc)
         self.rows = self.st.rows
+        self.v = v  # ACA: this shard's columns of V (m2 x r)
 
     def forward(self, x):
         import torch
@@ -30,6 +31,14 @@ class OracleShard:
     def adjoint(self, phi):
         import torch
         return torch.from_numpy(np.ascontiguousarray(self.st.adjoint(phi.numpy())))
+
+    def aca_forward(self, x):
+        import torch
+        return torch.from_numpy(np.ascontiguousarray(self.st.aca_forward(self.v, x.numpy())))
+
+    def aca_adjoint(self, phi):
+        import torch
+        return torch.from_numpy(np.ascontiguousarray(self.st.aca_adjoint(self.v, phi.numpy())))
 
 
 def _free_port():
@@ -74,6 +83,17 @@ def _worker(rank, world, port, out_q):
                "z": float(np.linalg.norm(z.numpy() - full.adjoint(phi)) / np.linalg.norm(full.adjoint(phi)))}
         if rank == 0:
             res["y"] = float(np.linalg.norm(y.numpy() - full.forward(x)) / np.linalg.norm(full.forward(x)))
+        # ACA store sharded by U columns with the matching columns of V
+        m2 = 11
+        v = rng.standard_normal((m2, cc.m)) + 1j * rng.standard_normal((m2, cc.m))
+        sha = ShardedStore(OracleShard(sub, np.asfortranarray(v[:, c0:c1])), c0, c1, cc.m, shards=shards)
+        xa = rng.standard_normal((m2, 2)) + 1j * rng.standard_normal((m2, 2))
+        ya = sha.aca_forward(torch.from_numpy(xa), allreduce=True).numpy()
+        za = sha.aca_adjoint(torch.from_numpy(phi)).numpy()
+        ya_ref = full.aca_forward(v, xa)
+        za_ref = full.aca_adjoint(v, phi)
+        res["aca_y"] = float(np.linalg.norm(ya - ya_ref) / np.linalg.norm(ya_ref))
+        res["aca_z"] = float(np.linalg.norm(za - za_ref) / np.linalg.norm(za_ref))
         out_q.put(res)
     finally:
         dist.destroy_process_group()
@@ -94,6 +114,7 @@ def test_sharded_products_gloo(world):
     res = [q.get(timeout=10) for _ in range(world)]
     for r in res:
         assert r["ya"] < 1e-13 and r["z"] < 1e-13
+        assert r["aca_y"] < 1e-13 and r["aca_z"] < 1e-13
         if r["rank"] == 0:
             assert r["y"] < 1e-13
 
