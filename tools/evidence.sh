@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-end evidence on one GPU box: bench lines (c4 with CPU baseline and
-# e2e, the reference arm, c1/c2/c3/c5), the ncu launch list of one forward +
-# adjoint, smoke() and the full-size c4 parity check.  Usage (under gpurun):
+# e2e, the reference arm, c1/c2/c3/c5), the ncu launch list of the bench's
+# timed region (one step; bench.py brackets it with cudaProfilerStart/Stop), smoke() and the full-size c4 parity check.  Usage (under gpurun):
 #   bash tools/evidence.sh TAG      -> gpurun_out/TAG_*
 set -u
 T=${1:-rXX}
@@ -14,7 +14,7 @@ for c in c1 c2 c3 c5; do
   timeout -s KILL 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu >> $O/${T}_bench_configs.jsonl 2>> $O/${T}_bench_configs.err
 done
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
-  --log-file $O/${T}_launches_bench.csv python tools/prof_run.py > $O/${T}_ncu.log 2>&1
+  --log-file $O/${T}_launches_bench.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > $O/${T}_ncu.log 2>&1
 timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/${T}_smoke.log 2>&1
 timeout -s KILL 900 python tools/validate_full.py > $O/${T}_validate_full_c4.json 2> $O/${T}_validate.err
 tail -n 2 $O/${T}_smoke.log
