@@ -540,6 +540,14 @@ def main():
                 "hbm_peak_gbs": peaks.get("hbm_gbs"), "fp32_ffma_peak_tflops": round(fp32_peak, 2),
                 "fp64_dgemm_tflops_this_run": round(fp64_peak, 2),
                 "f16_gemm_tflops_this_run": round(f16_peak, 2), "bf16_peak_tflops_measured": peaks.get("bf16_tflops")}
+        if world > 1:
+            # SURVEY §8d multi-GPU term C_coll / BW_NVLink: the forward's reduce of the
+            # q n_v x p partial y and the adjoint's all-gather of the padded z shards,
+            # against the NVLink 5 per-direction figure (spec, not measured here)
+            cbytes = nrows * cfg.p * 8 + world * max(b - a for a, b in shards) * cfg.p * 8
+            roof["collective"] = {"bytes_per_step": int(cbytes), "nvlink_gbs_spec": 900.0,
+                                  "t_roof_ms": round(cbytes / 900e9 * 1e3, 3),
+                                  "note": "one GPU's compute roofline above is its shard's"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and cpu_pay is not None:
