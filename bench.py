@@ -361,11 +361,11 @@ def main():
 
     from paper_2103_06393_b200 import DeviceStore, launch_count
     from paper_2103_06393_b200.sharded import ShardedStore, balanced_shards, column_costs
-    from paper_2103_06393_b200.workloads import CONFIGS, column_scales, rank_table, synthetic_payload
+    from paper_2103_06393_b200.workloads import CONFIGS, rank_table, synthetic_payload, tensor_scales
 
     cfg = CONFIGS[args.config]
     ranks = rank_table(cfg, SEED)
-    scales = column_scales(cfg, SEED)
+    scales = tensor_scales(cfg, SEED)
     costs = column_costs(cfg.grid, ranks, cfg.p)
     shards = balanced_shards(costs, world)
     c0, c1 = shards[rank]

@@ -22,9 +22,12 @@
  *     exception types (include/tuckmat/errors.hpp:10-48).
  *   - There is no CPU fallback: without a usable sm_100 device every compute
  *     entry point fails with TM_CUDA_ERROR.
- *   - A store is immutable after creation.  Products on one store are
- *     serialised by an internal mutex (they share device work buffers);
- *     products on different stores may run concurrently.
+ *   - A store is immutable after creation.  Products on one store share
+ *     device work buffers: they are serialised on the host by an internal
+ *     mutex and on the device by a per-store completion event (every
+ *     product's stream waits for the previous product's event, whatever
+ *     stream or TM_HOST / TM_DEVICE mode it used).  Products on different
+ *     stores may run concurrently.
  */
 #ifndef TUCKMAT_B200_H
 #define TUCKMAT_B200_H
@@ -89,6 +92,14 @@ TM_API int tm_store_create(const tm_store_desc* desc, int device, int dtype, tm_
  * (replaces load_ctc1 / load_cta1, src/io.cpp:212-230, 249-279). */
 TM_API int tm_store_load_ctc1(const char* path, int device, int dtype, tm_store** out);
 TM_API int tm_store_load_cta1(const char* path, int device, int dtype, tm_store** out);
+
+/* Dense-U ACA store: AcaFactors with `dense_u` set and `tucker_u` empty
+ * (include/tuckmat/aca.hpp:24-41; the `fac.dense_u * w` branches of
+ * aca_forward / aca_adjoint, src/matvec.cpp:158,173).  u: m1 x r, v: m2 x r,
+ * column-major complex128, host pointers (device pointers on `device` with
+ * on_device = 1).  Only tm_aca_forward / tm_aca_adjoint apply to it. */
+TM_API int tm_store_create_dense_aca(const double* u, int64_t m1, const double* v, int64_t m2, int64_t r,
+                                     int on_device, int device, int dtype, tm_store** out);
 
 TM_API int tm_store_destroy(tm_store* s);
 

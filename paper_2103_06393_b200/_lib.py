@@ -22,7 +22,7 @@ TM_C64, TM_C128 = 0, 1
 TM_HOST, TM_DEVICE = 0, 1
 
 EXPORTED = [
-    "tm_store_create", "tm_store_load_ctc1", "tm_store_load_cta1", "tm_store_destroy", "tm_store_info",
+    "tm_store_create", "tm_store_create_dense_aca", "tm_store_load_ctc1", "tm_store_load_cta1", "tm_store_destroy", "tm_store_info",
     "tm_forward", "tm_adjoint", "tm_aca_forward", "tm_aca_adjoint", "tm_opcounts", "tm_rows", "tm_last_error",
     "tm_assemble_columns",
     "tm_launch_count", "tm_version",
@@ -61,6 +61,7 @@ def lib():
             L.tm_store_create.argtypes = [ctypes.POINTER(StoreDesc), i32, i32, ctypes.POINTER(vp)]
             L.tm_store_load_ctc1.argtypes = [ctypes.c_char_p, i32, i32, ctypes.POINTER(vp)]
             L.tm_store_load_cta1.argtypes = [ctypes.c_char_p, i32, i32, ctypes.POINTER(vp)]
+            L.tm_store_create_dense_aca.argtypes = [vp, i64, vp, i64, i64, i32, i32, i32, ctypes.POINTER(vp)]
             L.tm_store_destroy.argtypes = [vp]
             L.tm_store_info.argtypes = [vp, vp, vp, vp, vp, vp, vp]
             L.tm_forward.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp, vp]

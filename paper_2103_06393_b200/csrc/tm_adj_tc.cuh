@@ -509,21 +509,22 @@ __global__ void __launch_bounds__(256) adj_split_phi_kernel(const float2* __rest
 }
 
 // U3 planes for the adjoint: [pl][k][slot][n3p] fp16 (i3-contiguous), slot
-// = chunk * 128 + offset of the (j, c) pair inside its chunk; values scaled
-// by AJ_U3_SCALE, 2-term fp16 split, in the 6-plane order
+// = chunk * 128 + offset of the (j, c) pair inside its chunk; values
+// normalised by 2^-e3 (factor_scale_kernel) and scaled by AJ_U3_SCALE, 2-term fp16 split, in the 6-plane order
 // (-U3i, U3r, U3i hi; the same lo): the windows [-U3i|U3r] and [U3r|U3i].
 __global__ void build_adj_bplanes_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena,
                                          const int* __restrict__ aslot, int64_t ncols, int q, int n3, int n3p,
-                                         int64_t nslots, __half* __restrict__ planes) {
+                                         int64_t nslots, const TcDesc* __restrict__ tcd, __half* __restrict__ planes) {
     const int64_t t = blockIdx.x;
     const int k = int(t / ncols);
     const TDesc d = td[t];
+    const int sc = -fexp_e3(tcd[t].fexp);  // normalised U3 (|u| <= 1), exact
     const int64_t s0 = aslot[t];
     const int64_t plane = int64_t(q) * nslots * n3p;
     for (int e = threadIdx.x; e < n3 * d.r3; e += blockDim.x) {
         const int i3 = e / d.r3, r = e - i3 * d.r3;
         const float2 u0 = arena[d.off_u3 + e];
-        const float2 u = make_float2(u0.x * AJ_U3_SCALE, u0.y * AJ_U3_SCALE);
+        const float2 u = make_float2(ldexpf(u0.x, sc) * AJ_U3_SCALE, ldexpf(u0.y, sc) * AJ_U3_SCALE);
         const __half rh = __float2half_rn(u.x), ih = __float2half_rn(u.y);
         const __half rl = __float2half_rn(u.x - __half2float(rh)), il = __float2half_rn(u.y - __half2float(ih));
         const int64_t o = (int64_t(k) * nslots + s0 + r) * n3p + i3;

@@ -23,7 +23,6 @@
 #include "tm_kernels_tc.cuh"
 #include "tm_adj_tc.cuh"
 #include "tm_adj2_tc.cuh"
-#include "tm_mrhs_tc.cuh"
 #include "tm_tmap.h"
 #include "tm_io_internal.hpp"
 
@@ -123,6 +122,9 @@ struct tm_store {
     void* d_arena = nullptr;
     int64_t arena_elems = 0;
     void* d_v = nullptr;
+    // dense-U ACA store (tm_store_create_dense_aca): U is m1 x r (dims = {m1, 1, 1}, q = 1)
+    bool dense = false;
+    void* d_u = nullptr;
     int64_t device_bytes = 0;
     // tensor-core (tcgen05 3xTF32) forward data: B planes of U3, K offsets
     bool tc_ok = false;
@@ -156,7 +158,10 @@ struct tm_store {
     DevBuf xbplanes;        // the forward's per-call B operand (build_xb_kernel)
     size_t xb_zeroed = 0;   // bytes of xbplanes zeroed since allocation
     std::mutex mu;
-    DevBuf part, xin, yout, wbuf, phiplanes, xplanes, rsum, scal;
+    // completion event of the latest product: products share the work
+    // buffers below, so each one's stream waits for it first (order_after_prev)
+    cudaEvent_t done = nullptr;
+    DevBuf part, xin, yout, wbuf, phiplanes, rsum, scal;
     DevBuf ypart;  // partial tiles of a split final wave of the tensor-core forward
     DevBuf ccpart;  // partial y blocks of a column-split CUDA-core forward (small stores)
 
@@ -164,6 +169,10 @@ struct tm_store {
     int64_t rows() const { return q * nv(); }
     size_t csize() const { return dtype == TM_C64 ? sizeof(float2) : sizeof(double2); }
     ~tm_store() {
+        if (done) {
+            cudaEventSynchronize(done);
+            cudaEventDestroy(done);
+        }
         if (d_kofs) cudaFree(d_kofs);
         if (d_kc) cudaFree(d_kc);
 
@@ -182,10 +191,21 @@ struct tm_store {
         if (d_desc) cudaFree(d_desc);
         if (d_arena) cudaFree(d_arena);
         if (d_v) cudaFree(d_v);
+        if (d_u) cudaFree(d_u);
     }
 };
 
 namespace {
+
+// Device-side ordering of the products on one store.  They share the store's
+// work buffers (B planes, Phi planes, partials, scales), and the host mutex
+// only serialises the enqueue: a TM_DEVICE call returns with its kernels
+// still running.  So every product's stream(s) first wait for the previous
+// product's completion event, and the product records its own at the end —
+// TM_DEVICE calls on different streams and TM_HOST calls on their private
+// streams are serialised on the device too.
+void order_after_prev(tm_store* s, cudaStream_t st) { CK(cudaStreamWaitEvent(st, s->done, 0)); }
+void mark_done(tm_store* s, cudaStream_t st) { CK(cudaEventRecord(s->done, st)); }
 
 // ------------------------------------------------------------ store build --
 // c64 stores run the forward on the tcgen05 3xTF32 kernel (chained TMEM
@@ -240,7 +260,7 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
         u2off += n2p * (d.r2 | 1);
         c.r2 = d.r2;
         c.r3 = d.r3;
-        c.pad0 = c.pad1 = c.pad2 = c.pad3 = 0;
+        c.pad0 = c.pad1 = c.pad2 = c.fexp = 0;
         voff += n1p * d.r2 * d.r3;
     }
     // adjoint chunks: whole columns, at most AJ_CH (j, c) slots each
@@ -284,12 +304,19 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
     CK(cudaMemcpy(s->d_nch, nch.data(), nch.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(s->d_cstart, cstart.data(), cstart.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemset(s->d_aplanes, 0, abytes));
+    CK(cudaMemcpy(s->d_tcd, tcd.data(), tcd.size() * sizeof(TcDesc), cudaMemcpyHostToDevice));
+    // per-tensor power-of-two factor normalisation of the tensor-core operand
+    // copies (non-orthonormal factors stay inside fp16's range)
+    factor_scale_kernel<<<unsigned(ntens), 256>>>(s->d_desc, static_cast<const float2*>(s->d_arena),
+                                                  int(s->dims[1]), int(n3), s->d_tcd);
+    launched(cudaSuccess, "factor_scale_kernel");
     {
         DevBuf as;
         int* d_as = static_cast<int*>(as.get(aslot.size() * sizeof(int)));
         CK(cudaMemcpy(d_as, aslot.data(), aslot.size() * sizeof(int), cudaMemcpyHostToDevice));
         build_adj_bplanes_kernel<<<unsigned(ntens), 256>>>(s->d_desc, static_cast<const float2*>(s->d_arena), d_as,
-                                                           s->ncols, s->q, int(n3), int(n3p), s->nslots, s->d_aplanes);
+                                                           s->ncols, s->q, int(n3), int(n3p), s->nslots, s->d_tcd,
+                                                           s->d_aplanes);
         launched(cudaSuccess, "build_adj_bplanes_kernel");
         CK(cudaDeviceSynchronize());
     }
@@ -299,7 +326,6 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
     s->tca_ok = true;
     CK(cudaMemcpy(s->d_kofs, kofs.data(), kofs.size() * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(s->d_kc, kc.data(), kc.size() * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(s->d_tcd, tcd.data(), tcd.size() * sizeof(TcDesc), cudaMemcpyHostToDevice));
     build_v_kernel<<<unsigned(ntens), 256>>>(s->d_desc, static_cast<const float2*>(s->d_arena), s->d_tcd,
                                              int(s->dims[0]), s->d_varena);
     launched(cudaSuccess, "build_v_kernel");
@@ -518,6 +544,11 @@ tm_store* create_store(const tm_store_desc& d, int device, int dtype, const tmb_
     if (device < 0 || device >= ndev) throw TmError(TM_CUDA_ERROR, "store: no CUDA device " + std::to_string(device));
     DeviceGuard guard(device);
     auto* s = new tm_store;
+    if (cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming) != cudaSuccess) {
+        s->done = nullptr;
+        delete s;
+        throw TmError(TM_CUDA_ERROR, "store: cannot create the completion event");
+    }
     s->device = device;
     s->dtype = dtype;
     s->q = d.q;
@@ -769,7 +800,7 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
     }
     build_xb_kernel<<<unsigned(s->ncols * s->q), 256, 0, st>>>(s->d_desc, static_cast<const float2*>(s->d_arena),
                                                               s->d_kofs, x, ldx, int(p), s->ncols, s->q, g.n3,
-                                                              int64_t(g.nt), s->kpad, wmax, xb);
+                                                              int64_t(g.nt), s->kpad, wmax, s->d_tcd, xb);
     launched(cudaSuccess, "build_xb_kernel");
     const CUtensorMap bmap = make_tmap_3d_f16(xb, uint64_t(s->kpad), uint64_t(g.nt), uint64_t(TC_FPLANES * s->q),
                                               uint64_t(s->kpad) * 2, uint64_t(g.nt) * s->kpad * 2, 16,
@@ -870,63 +901,7 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     }
 }
 
-// Batched multi-RHS forward (tm_mrhs_tc.cuh) for c64 stores at p >= 3,
-// in blocks of MR_P right-hand sides.
-// The older batched forward (tm_mrhs_tc.cuh) only on request: the x-in-B
-// tensor-core forward shares W across right-hand sides itself.
-bool mrhs_ok(const tm_store* s, int64_t p) {
-    const char* e = std::getenv("TMB_USE_MRHS");
-    if (!(e && e[0] == '1')) return false;
-    return s->tc_ok && p >= 3;
-}
-
-void run_forward_mrhs(tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy, cudaStream_t st) {
-    MrGeom g{};
-    g.ncols = s->ncols;
-    g.n1 = int(s->dims[0]);
-    g.n2 = int(s->dims[1]);
-    g.n3 = int(s->dims[2]);
-    g.q = s->q;
-    g.nt2 = (g.n2 + MR_TI2 - 1) / MR_TI2;
-    g.nt3 = (g.n3 + MR_TI3 - 1) / MR_TI3;
-    g.ntiles = int64_t(g.q) * g.n1 * g.nt2 * g.nt3;
-    g.nks = int((s->ncols + 7) / 8);
-    g.chain = tc_chain();
-    g.v_off = 64;
-    g.u2_off = g.v_off + int(round16(uint32_t(TC_TI1 * s->rmax[1] * s->rmax[2] * 8)));
-    g.u3_off = g.u2_off + MR_TI2 * (s->rmax[1] | 1) * 8;
-    g.slot_bytes = (g.u3_off + int(round16(uint32_t(MR_TI3 * s->rmax[2]) * 8u)) + 127) / 128 * 128;
-    const size_t smem = 1024 + size_t(MR_NST) * (MR_A_STAGE + MR_B_STAGE) + size_t(MR_JR) * g.slot_bytes +
-                        size_t(2) * MR_TI2 * MR_WLD * sizeof(float4) + (2 * MR_NST + 2 * MR_JR + 2) * 8 + 16;
-    if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "batched forward: shared-memory plan too large");
-    CK(cudaFuncSetAttribute(fwd_mrhs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    const int64_t mp = (s->ncols + 3) / 4 * 4;
-    float* planes = static_cast<float*>(s->xplanes.get(size_t(TC_BPLANES) * MR_P * mp * sizeof(float)));
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    const unsigned grid = unsigned(std::min<int64_t>(g.ntiles, num_sms(dev)));
-    for (int64_t c0 = 0; c0 < p; c0 += MR_P) {
-        const int pb = int(std::min<int64_t>(MR_P, p - c0));
-        const unsigned sblocks = unsigned(std::min<int64_t>((MR_P * mp + 255) / 256, 4096));
-        mrhs_split_x_kernel<<<sblocks, 256, 0, st>>>(x + ldx * c0, ldx, s->ncols, pb, mp, planes);
-        launched(cudaSuccess, "mrhs_split_x_kernel");
-        const CUtensorMap xmap = make_tmap_3d_f32(planes, uint64_t(mp), uint64_t(MR_P), uint64_t(TC_BPLANES),
-                                                  uint64_t(mp) * 4, uint64_t(MR_P) * mp * 4, 8, MR_P,
-                                                  CU_TENSOR_MAP_SWIZZLE_32B);
-        g.t_begin = 0;
-        g.t_end = g.ntiles;
-        fwd_mrhs_kernel<<<grid, MR_THREADS, smem, st>>>(xmap, s->d_tcd, s->d_varena, s->d_u2arena,
-                                                         static_cast<const float2*>(s->d_arena), g, y + ldy * c0, ldy,
-                                                         pb);
-        launched(cudaSuccess, "fwd_mrhs_kernel");
-    }
-}
-
 void forward_dev(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy, cudaStream_t st) {
-    if (s->tc_ok && !tc_disabled() && mrhs_ok(s, p)) {
-        run_forward_mrhs(s, static_cast<const float2*>(x), ldx, p, static_cast<float2*>(y), ldy, st);
-        return;
-    }
     if (s->tc_ok && !tc_disabled()) {
         run_forward_tc(s, static_cast<const float2*>(x), ldx, p, static_cast<float2*>(y), ldy, st);
         return;
@@ -964,6 +939,8 @@ bool ensure_adj_pack(tm_store* s, int which) {
     if (ap.ok) return true;
     if (s->rmax[2] > ch) return false;
     const int64_t ntens = s->ncols * s->q;
+    // products still in flight read the descriptor table rewritten below
+    CK(cudaEventSynchronize(s->done));
     std::vector<TcDesc> tcd(static_cast<size_t>(ntens));
     CK(cudaMemcpy(tcd.data(), s->d_tcd, tcd.size() * sizeof(TcDesc), cudaMemcpyDeviceToHost));
     std::vector<int> aslot(static_cast<size_t>(ntens), 0), nch(static_cast<size_t>(s->q), 0);
@@ -1004,7 +981,8 @@ bool ensure_adj_pack(tm_store* s, int which) {
     int* d_as = static_cast<int*>(as.get(aslot.size() * sizeof(int)));
     CK(cudaMemcpy(d_as, aslot.data(), aslot.size() * sizeof(int), cudaMemcpyHostToDevice));
     build_adj_bplanes_kernel<<<unsigned(ntens), 256>>>(s->d_desc, static_cast<const float2*>(s->d_arena), d_as,
-                                                       s->ncols, s->q, int(n3), int(n3p), nslots, ap.d_aplanes);
+                                                       s->ncols, s->q, int(n3), int(n3p), nslots, s->d_tcd,
+                                                       ap.d_aplanes);
     launched(cudaSuccess, "build_adj_bplanes_kernel");
     CK(cudaDeviceSynchronize());
     ap.bmap = make_tmap_3d_f16(ap.d_aplanes, uint64_t(n3), uint64_t(nslots), uint64_t(TC_BPLANES * s->q),
@@ -1284,6 +1262,65 @@ void aca_vt_dev(const tm_store* s, const void* t, int64_t p, void* z, int64_t ld
     launched(cudaSuccess, "aca_vt_kernel");
 }
 
+// Dense-U ACA products (aca_forward's `fac.dense_u * w` and aca_adjoint's
+// `fac.dense_u.adjoint() * phi`, src/matvec.cpp:158,173) on the device: the
+// same two reduction kernels as the V side, with U (m1 x r) in V's place.
+void dense_u_times(const tm_store* s, const void* t, int64_t p, void* y, int64_t ldy, cudaStream_t st) {
+    const int64_t m1 = s->dims[0], n = m1 * p;
+    if (n == 0) return;
+    const unsigned blocks = unsigned((n + 255) / 256);
+    if (s->dtype == TM_C64)
+        aca_vt_kernel<float2><<<blocks, 256, 0, st>>>(static_cast<const float2*>(s->d_u), m1, s->ncols,
+                                                      static_cast<const float2*>(t), p, static_cast<float2*>(y), ldy);
+    else
+        aca_vt_kernel<double2><<<blocks, 256, 0, st>>>(static_cast<const double2*>(s->d_u), m1, s->ncols,
+                                                       static_cast<const double2*>(t), p, static_cast<double2*>(y),
+                                                       ldy);
+    launched(cudaSuccess, "aca_vt_kernel<dense U>");
+}
+
+void dense_uh_times(const tm_store* s, const void* phi, int64_t ldphi, int64_t p, void* t, cudaStream_t st) {
+    const int64_t warps = s->ncols * p;
+    if (warps == 0) return;
+    const unsigned blocks = unsigned((warps * 32 + 255) / 256);
+    if (s->dtype == TM_C64)
+        aca_vhx_kernel<float2><<<blocks, 256, 0, st>>>(static_cast<const float2*>(s->d_u), s->dims[0], s->ncols,
+                                                       static_cast<const float2*>(phi), ldphi, p,
+                                                       static_cast<float2*>(t));
+    else
+        aca_vhx_kernel<double2><<<blocks, 256, 0, st>>>(static_cast<const double2*>(s->d_u), s->dims[0], s->ncols,
+                                                        static_cast<const double2*>(phi), ldphi, p,
+                                                        static_cast<double2*>(t));
+    launched(cudaSuccess, "aca_vhx_kernel<dense U>");
+}
+
+// complex128 host or device block -> the store's dtype, into fresh device memory
+void* upload_converted(const tm_store* s, const double* src, int64_t n, bool on_device) {
+    void* dst = nullptr;
+    CK(cudaMalloc(&dst, size_t(std::max<int64_t>(n, 1)) * s->csize()));
+    if (n == 0) return dst;
+    DevBuf st;
+    const double2* d = reinterpret_cast<const double2*>(src);
+    if (!on_device) {
+        void* p = st.get(size_t(n) * sizeof(double2));
+        CK(cudaMemcpy(p, src, size_t(n) * sizeof(double2), cudaMemcpyHostToDevice));
+        d = static_cast<const double2*>(p);
+    }
+    const unsigned grid = unsigned(std::min<int64_t>((n + 255) / 256, 4096));
+    if (s->dtype == TM_C64)
+        convert_kernel<float2><<<grid, 256>>>(d, n, static_cast<float2*>(dst));
+    else
+        convert_kernel<double2><<<grid, 256>>>(d, n, static_cast<double2*>(dst));
+    launched(cudaSuccess, "convert_kernel");
+    CK(cudaDeviceSynchronize());
+    return dst;
+}
+
+void reject_dense(const tm_store* s, const char* what) {
+    if (s->dense)
+        contract(std::string(what) + ": the store holds a dense ACA U (no Tucker columns); use the aca products");
+}
+
 void zero_dev(const tm_store* s, void* y, int64_t rows, int64_t p, int64_t ldy, cudaStream_t st) {
     if (rows * p == 0) return;
     const unsigned blocks = unsigned(std::min<int64_t>((rows * p + 255) / 256, 8192));
@@ -1306,6 +1343,7 @@ void with_host_io(tm_store* s, const void* in, int64_t ldin, int64_t inrows, int
     cudaStream_t st;
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     try {
+        order_after_prev(s, st);
         if (inrows * p > 0)
             CK(cudaMemcpy2DAsync(din, size_t(inrows) * cs, in, size_t(ldin) * cs, size_t(inrows) * cs, size_t(p),
                                  cudaMemcpyHostToDevice, st));
@@ -1313,6 +1351,7 @@ void with_host_io(tm_store* s, const void* in, int64_t ldin, int64_t inrows, int
         if (outrows * p > 0)
             CK(cudaMemcpy2DAsync(out, size_t(ldout) * cs, dout, size_t(outrows) * cs, size_t(outrows) * cs, size_t(p),
                                  cudaMemcpyDeviceToHost, st));
+        mark_done(s, st);
         CK(cudaStreamSynchronize(st));
     } catch (...) {
         cudaStreamSynchronize(st);
@@ -1326,7 +1365,7 @@ void with_host_io(tm_store* s, const void* in, int64_t ldin, int64_t inrows, int
 // kernels block by block (HostPipe).  Returns false when the product does
 // not take the tensor-core path (the caller then uses with_host_io).
 bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy) {
-    if (!(s->tc_ok && !tc_disabled() && !mrhs_ok(s, p))) return false;
+    if (!(s->tc_ok && !tc_disabled())) return false;
     const size_t cs = s->csize();
     void* din = s->xin.get(size_t(std::max<int64_t>(s->ncols * p, 1)) * cs);
     void* dout = s->yout.get(size_t(std::max<int64_t>(s->rows() * p, 1)) * cs);
@@ -1340,6 +1379,8 @@ bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, 
         cudaStreamDestroy(cp);
     };
     try {
+        order_after_prev(s, st);
+        order_after_prev(s, cp);
         CK(cudaMemcpy2DAsync(din, size_t(s->ncols) * cs, x, size_t(ldx) * cs, size_t(s->ncols) * cs, size_t(p),
                              cudaMemcpyHostToDevice, st));
         HostPipe hp;
@@ -1347,6 +1388,7 @@ bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, 
         hp.host = y;
         hp.ldhost = ldy;
         run_forward_tc(s, static_cast<const float2*>(din), s->ncols, p, static_cast<float2*>(dout), s->rows(), st, &hp);
+        mark_done(s, st);
         CK(cudaStreamSynchronize(st));
         CK(cudaStreamSynchronize(cp));
     } catch (...) {
@@ -1372,6 +1414,8 @@ bool adjoint_host_pipelined(tm_store* s, const void* phi, int64_t ldphi, int64_t
         cudaStreamDestroy(cp);
     };
     try {
+        order_after_prev(s, st);
+        order_after_prev(s, cp);
         HostPipe hp;
         hp.copy = cp;
         hp.host = const_cast<void*>(phi);
@@ -1379,6 +1423,7 @@ bool adjoint_host_pipelined(tm_store* s, const void* phi, int64_t ldphi, int64_t
         run_adjoint_tc(s, static_cast<const float2*>(din), s->rows(), p, static_cast<float2*>(dout), s->ncols, st, &hp);
         CK(cudaMemcpy2DAsync(z, size_t(ldz) * cs, dout, size_t(s->ncols) * cs, size_t(s->ncols) * cs, size_t(p),
                              cudaMemcpyDeviceToHost, st));
+        mark_done(s, st);
         CK(cudaStreamSynchronize(st));
     } catch (...) {
         done();
@@ -1415,6 +1460,40 @@ TM_API int tm_store_create(const tm_store_desc* desc, int device, int dtype, tm_
     return guarded([&] {
         if (!desc || !out) contract("tm_store_create: null argument");
         *out = create_store(*desc, device, dtype);
+    });
+}
+
+TM_API int tm_store_create_dense_aca(const double* u, int64_t m1, const double* v, int64_t m2, int64_t r,
+                                     int on_device, int device, int dtype, tm_store** out) {
+    return guarded([&] {
+        if (!out) contract("tm_store_create_dense_aca: null argument");
+        if (dtype != TM_C64 && dtype != TM_C128) contract("store: dtype must be TM_C64 or TM_C128");
+        if (m1 < 1 || m2 < 1 || r < 0) contract("store: dense ACA needs m1, m2 >= 1 and r >= 0");
+        if (r > 0 && (!u || !v)) contract("store: dense ACA needs U and V");
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev)
+            throw TmError(TM_CUDA_ERROR, "store: no CUDA device " + std::to_string(device));
+        DeviceGuard guard(device);
+        auto* s = new tm_store;
+        try {
+            CK(cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming));
+            s->device = device;
+            s->dtype = dtype;
+            s->dense = true;
+            s->q = 1;
+            s->ncols = r;
+            s->dims[0] = m1;
+            s->dims[1] = s->dims[2] = 1;
+            s->m2 = m2;
+            s->d_u = upload_converted(s, u, m1 * r, on_device != 0);
+            s->d_v = upload_converted(s, v, m2 * r, on_device != 0);
+            s->device_bytes = (m1 + m2) * r * int64_t(s->csize());
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        *out = s;
     });
 }
 
@@ -1488,6 +1567,7 @@ TM_API int tm_rows(tm_store* s, const int64_t* rows, int64_t nrows, void* out, i
                    void* stream) {
     return guarded([&] {
         if (!s) contract("null store");
+        reject_dense(s, "tm_rows");
         if (nrows < 0) contract("negative row count");
         if (where != TM_HOST && where != TM_DEVICE) contract("where must be TM_HOST or TM_DEVICE");
         if (nrows > 0 && (!rows || !out)) contract("null rows or output pointer");
@@ -1506,6 +1586,7 @@ TM_API int tm_rows(tm_store* s, const int64_t* rows, int64_t nrows, void* out, i
             own = true;
         }
         try {
+            order_after_prev(s, st);
             int64_t* d_rows = static_cast<int64_t*>(s->wbuf.get(size_t(nrows) * sizeof(int64_t)));
             CK(cudaMemcpyAsync(d_rows, rows, size_t(nrows) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
             void* dout = where == TM_DEVICE ? out : s->yout.get(size_t(nrows * s->ncols) * cs);
@@ -1523,6 +1604,7 @@ TM_API int tm_rows(tm_store* s, const int64_t* rows, int64_t nrows, void* out, i
             if (where == TM_HOST)
                 CK(cudaMemcpy2DAsync(out, size_t(ldout) * cs, dout, size_t(nrows) * cs, size_t(nrows) * cs,
                                      size_t(s->ncols), cudaMemcpyDeviceToHost, st));
+            mark_done(s, st);
             CK(cudaStreamSynchronize(st));
         } catch (...) {
             if (own) {
@@ -1547,15 +1629,18 @@ TM_API int tm_forward(tm_store* s, const void* x, int64_t ldx, int64_t xrows, in
                       int where, void* stream, int64_t* ops) {
     return guarded([&] {
         if (!s) contract("null store");
+        reject_dense(s, "forward");
         if (xrows != s->ncols)
             contract("forward: x has " + std::to_string(xrows) + " rows, expected m = " + std::to_string(s->ncols));
         check_common(s, p, ldx, xrows, ldy, s->rows(), where, x, y);
         std::lock_guard<std::mutex> lock(s->mu);
         DeviceGuard guard(s->device);
         if (p > 0) {
-            if (where == TM_DEVICE)
+            if (where == TM_DEVICE) {
+                order_after_prev(s, static_cast<cudaStream_t>(stream));
                 forward_dev(s, x, ldx, p, y, ldy, static_cast<cudaStream_t>(stream));
-            else if (!forward_host_pipelined(s, x, ldx, p, y, ldy))
+                mark_done(s, static_cast<cudaStream_t>(stream));
+            } else if (!forward_host_pipelined(s, x, ldx, p, y, ldy))
                 with_host_io(s, x, ldx, xrows, p, y, ldy, s->rows(),
                              [&](void* din, int64_t ldi, void* dout, int64_t ldo, cudaStream_t st) {
                                  forward_dev(s, din, ldi, p, dout, ldo, st);
@@ -1572,6 +1657,7 @@ TM_API int tm_adjoint(tm_store* s, const void* phi, int64_t ldphi, int64_t phiro
                       int where, void* stream, int64_t* ops) {
     return guarded([&] {
         if (!s) contract("null store");
+        reject_dense(s, "adjoint");
         if (phirows != s->rows())
             contract("adjoint: phi has " + std::to_string(phirows) + " rows, expected q*n_v = " +
                      std::to_string(s->rows()));
@@ -1579,9 +1665,11 @@ TM_API int tm_adjoint(tm_store* s, const void* phi, int64_t ldphi, int64_t phiro
         std::lock_guard<std::mutex> lock(s->mu);
         DeviceGuard guard(s->device);
         if (p > 0 && s->ncols > 0) {
-            if (where == TM_DEVICE)
+            if (where == TM_DEVICE) {
+                order_after_prev(s, static_cast<cudaStream_t>(stream));
                 adjoint_dev(s, phi, ldphi, p, z, ldz, static_cast<cudaStream_t>(stream));
-            else if (!adjoint_host_pipelined(s, phi, ldphi, p, z, ldz))
+                mark_done(s, static_cast<cudaStream_t>(stream));
+            } else if (!adjoint_host_pipelined(s, phi, ldphi, p, z, ldz))
                 with_host_io(s, phi, ldphi, phirows, p, z, ldz, s->ncols,
                              [&](void* din, int64_t ldi, void* dout, int64_t ldo, cudaStream_t st) {
                                  adjoint_dev(s, din, ldi, p, dout, ldo, st);
@@ -1612,15 +1700,21 @@ TM_API int tm_aca_forward(tm_store* s, const void* x, int64_t ldx, int64_t xrows
             }
             void* w = s->wbuf.get(size_t(s->ncols * p) * s->csize());
             aca_vhx_dev(s, xin, ldi, p, w, st);
-            forward_dev(s, w, s->ncols, p, yout, ldo, st);
+            if (s->dense)
+                dense_u_times(s, w, p, yout, ldo, st);
+            else
+                forward_dev(s, w, s->ncols, p, yout, ldo, st);
         };
-        if (where == TM_DEVICE)
+        if (where == TM_DEVICE) {
+            order_after_prev(s, static_cast<cudaStream_t>(stream));
             body(x, ldx, y, ldy, static_cast<cudaStream_t>(stream));
-        else
+            mark_done(s, static_cast<cudaStream_t>(stream));
+        } else {
             with_host_io(s, x, ldx, xrows, p, y, ldy, s->rows(),
                          [&](void* din, int64_t ldi, void* dout, int64_t ldo, cudaStream_t st) {
                              body(din, ldi, dout, ldo, st);
                          });
+        }
     });
 }
 
@@ -1642,16 +1736,22 @@ TM_API int tm_aca_adjoint(tm_store* s, const void* phi, int64_t ldphi, int64_t p
                 return;
             }
             void* t = s->wbuf.get(size_t(s->ncols * p) * s->csize());
-            adjoint_dev(s, pin, ldi, p, t, s->ncols, st);
+            if (s->dense)
+                dense_uh_times(s, pin, ldi, p, t, st);
+            else
+                adjoint_dev(s, pin, ldi, p, t, s->ncols, st);
             aca_vt_dev(s, t, p, zout, ldo, st);
         };
-        if (where == TM_DEVICE)
+        if (where == TM_DEVICE) {
+            order_after_prev(s, static_cast<cudaStream_t>(stream));
             body(phi, ldphi, z, ldz, static_cast<cudaStream_t>(stream));
-        else
+            mark_done(s, static_cast<cudaStream_t>(stream));
+        } else {
             with_host_io(s, phi, ldphi, phirows, p, z, ldz, s->m2,
                          [&](void* din, int64_t ldi, void* dout, int64_t ldo, cudaStream_t st) {
                              body(din, ldi, dout, ldo, st);
                          });
+        }
     });
 }
 

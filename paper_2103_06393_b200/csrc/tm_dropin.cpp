@@ -1,15 +1,18 @@
 // C++ drop-in of the reference matvec API on top of the C ABI
 // (include/tuckmat_b200/tuckmat.hpp).  Host glue only: flatten the
 // reference value types into a tm_store_desc, keep the device store cached
-// by object identity, convert MultiVector blocks to the store precision and
+// by content (a hash of the factors), convert MultiVector blocks to the store precision and
 // map status codes back onto the reference exception types.
 #include "../../include/tuckmat_b200/tuckmat.hpp"
 
+#include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
-#include <map>
+#include <cstring>
+#include <list>
 #include <mutex>
-#include <tuple>
+#include <thread>
 
 #include "tm_io_internal.hpp"
 
@@ -104,10 +107,28 @@ tm_store* make_store(int q, Index ncols, const Dims3& dims,
     return h;
 }
 
-// ---- identity cache ------------------------------------------------------
-using Key = std::tuple<const void*, const void*, Index, int, Index, Index, Index, int, int>;
+// ---- content-keyed store cache -------------------------------------------
+// The reference's value types are immutable and passed by const& on every
+// call (src/matvec.cpp:132-175), so the drop-in keeps the device store it
+// built for a given CONTENT: the key is a 64-bit hash of every tensor's
+// ranks and payload (and V), plus shape, dtype and device.  An object whose
+// address is reused for different data (a loop that rebuilds its factors)
+// hashes differently and gets a fresh store; identical content in another
+// object reuses the store.  Least-recently-used eviction bounds the device
+// memory held ($TUCKMAT_STORE_CACHE stores, default 4).
+struct Key {
+    std::uint64_t hash;
+    Index ncols, m2;
+    int q, dtype, device, kind;
+    Index d0, d1, d2;
+    bool operator==(const Key& o) const {
+        return hash == o.hash && ncols == o.ncols && m2 == o.m2 && q == o.q && dtype == o.dtype &&
+               device == o.device && kind == o.kind && d0 == o.d0 && d1 == o.d1 && d2 == o.d2;
+    }
+};
+
 std::mutex g_mu;
-std::map<Key, std::shared_ptr<tm_store>> g_cache;
+std::list<std::pair<Key, std::shared_ptr<tm_store>>> g_cache;  // front = most recently used
 int g_dtype = TM_C128;
 int g_device = -1;
 
@@ -117,12 +138,76 @@ int current_device() {
     return 0;
 }
 
+std::size_t cache_capacity() {
+    if (const char* e = std::getenv("TUCKMAT_STORE_CACHE")) {
+        const long v = std::atol(e);
+        if (v >= 0) return std::size_t(v);
+    }
+    return 4;
+}
+
+inline std::uint64_t mix(std::uint64_t h, std::uint64_t w) {
+    h ^= w + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+    return h * 0xBF58476D1CE4E5B9ull;
+}
+
+std::uint64_t hash_words(std::uint64_t h, const void* p, std::size_t bytes) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    std::size_t i = 0;
+    for (; i + 8 <= bytes; i += 8) {
+        std::uint64_t w;
+        std::memcpy(&w, b + i, 8);
+        h = mix(h, w);
+    }
+    std::uint64_t tail = 0;
+    std::memcpy(&tail, b + i, bytes - i);
+    return mix(h, tail ^ bytes);
+}
+
+std::uint64_t hash_tensor(const TuckerTensor& tt) {
+    std::uint64_t h = 0x12345678ull;
+    for (int g = 0; g < 3; ++g) h = mix(h, std::uint64_t(tt.core.dim(g + 1)) | (std::uint64_t(tt.factors[g].rows()) << 32));
+    h = hash_words(h, tt.core.data(), sizeof(Complex) * std::size_t(tt.core.size()));
+    for (int g = 0; g < 3; ++g) h = hash_words(h, tt.factors[g].data(), sizeof(Complex) * std::size_t(tt.factors[g].size()));
+    return h;
+}
+
+// Hash of ncols x q tensors, computed per tensor on a few threads (a
+// config-4 store is 6 GB of complex128) and combined in tensor order.
+std::uint64_t hash_columns(int q, Index ncols, const std::function<const TuckerTensor&(Index, int)>& at) {
+    const Index nt = ncols * q;
+    std::vector<std::uint64_t> ht(static_cast<std::size_t>(nt));
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const unsigned nth = nt > 64 ? hw : 1;
+    std::atomic<Index> next{0};
+    auto work = [&]() {
+        for (;;) {
+            const Index t0 = next.fetch_add(16);
+            if (t0 >= nt) return;
+            for (Index t = t0; t < std::min(nt, t0 + 16); ++t) ht[std::size_t(t)] = hash_tensor(at(t / q, int(t % q)));
+        }
+    };
+    std::vector<std::thread> pool;
+    for (unsigned i = 1; i < nth; ++i) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+    std::uint64_t h = mix(0xC0FFEEull, std::uint64_t(nt));
+    for (std::uint64_t v : ht) h = mix(h, v);
+    return h;
+}
+
 std::shared_ptr<tm_store> cached(const Key& key, const std::function<tm_store*()>& make) {
     std::lock_guard<std::mutex> lock(g_mu);
-    auto it = g_cache.find(key);
-    if (it != g_cache.end()) return it->second;
+    for (auto it = g_cache.begin(); it != g_cache.end(); ++it)
+        if (it->first == key) {
+            g_cache.splice(g_cache.begin(), g_cache, it);
+            return g_cache.front().second;
+        }
     std::shared_ptr<tm_store> s(make(), [](tm_store* p) { tm_store_destroy(p); });
-    g_cache.emplace(key, s);
+    const std::size_t cap = cache_capacity();
+    if (cap == 0) return s;  // caching disabled: the store lives as long as the call
+    g_cache.emplace_front(key, s);
+    while (g_cache.size() > cap) g_cache.pop_back();  // in-flight users keep their shared_ptr
     return s;
 }
 
@@ -200,51 +285,57 @@ MultiVector aca_adj(tm_store* s, int dtype, const MultiVector& phi) {
     });
 }
 
-Key key_of(const CompressedCoupling& cc) {
-    return Key(&cc, cc.columns.data(), cc.m, cc.q, cc.grid_dims[0], cc.grid_dims[1], cc.grid_dims[2], g_dtype,
-               current_device());
+Key key_of(int kind, int q, Index ncols, const Dims3& dims, Index m2, std::uint64_t h) {
+    return Key{h, ncols, m2, q, g_dtype, current_device(), kind, dims[0], dims[1], dims[2]};
 }
 
-Key key_of(const AcaFactors& f) {
-    return Key(&f, f.tucker_u.data(), f.rank(), f.q, f.grid_dims[0], f.grid_dims[1], f.grid_dims[2], g_dtype,
-               current_device());
+std::shared_ptr<tm_store> store_of(const TuckerColumns& z) {
+    const std::uint64_t h = hash_columns(z.q, z.ncols, z.tensor);
+    return cached(key_of(0, z.q, z.ncols, z.grid_dims, 0, h),
+                  [&] { return make_store(z.q, z.ncols, z.grid_dims, z.tensor, nullptr, g_dtype, current_device()); });
 }
 
 std::shared_ptr<tm_store> store_of(const CompressedCoupling& cc) {
     if (static_cast<Index>(cc.columns.size()) != cc.m) throw ContractViolation("CompressedCoupling: columns != m");
-    return cached(key_of(cc), [&] {
-        return make_store(
-            cc.q, cc.m, cc.grid_dims,
-            [&](Index j, int k) -> const TuckerTensor& {
-                return cc.columns[static_cast<std::size_t>(j)][static_cast<std::size_t>(k)];
-            },
-            nullptr, g_dtype, current_device());
-    });
+    for (const auto& col : cc.columns)
+        if (static_cast<int>(col.size()) != cc.q) throw ContractViolation("CompressedCoupling: column with wrong component count");
+    TuckerColumns z;
+    z.tensor = [&](Index j, int k) -> const TuckerTensor& {
+        return cc.columns[static_cast<std::size_t>(j)][static_cast<std::size_t>(k)];
+    };
+    z.ncols = cc.m;
+    z.q = cc.q;
+    z.grid_dims = cc.grid_dims;
+    return store_of(z);
 }
 
 std::shared_ptr<tm_store> store_of(const AcaFactors& f) {
-    return cached(key_of(f), [&] {
-        return make_store(
-            f.q, f.rank(), f.grid_dims,
-            [&](Index l, int k) -> const TuckerTensor& {
-                return f.tucker_u[static_cast<std::size_t>(k)][static_cast<std::size_t>(l)];
-            },
-            &f.v, g_dtype, current_device());
-    });
+    auto at = [&](Index l, int k) -> const TuckerTensor& {
+        return f.tucker_u[static_cast<std::size_t>(k)][static_cast<std::size_t>(l)];
+    };
+    if (static_cast<int>(f.tucker_u.size()) != f.q) throw ContractViolation("AcaFactors: tucker_u needs q rows");
+    for (const auto& row : f.tucker_u)
+        if (static_cast<Index>(row.size()) != f.rank()) throw ContractViolation("AcaFactors: tucker_u rows need r_c tensors");
+    std::uint64_t h = hash_columns(f.q, f.rank(), at);
+    h = hash_words(h, f.v.data(), sizeof(Complex) * std::size_t(f.v.size()));
+    return cached(key_of(1, f.q, f.rank(), f.grid_dims, f.v.rows(), h),
+                  [&] { return make_store(f.q, f.rank(), f.grid_dims, at, &f.v, g_dtype, current_device()); });
 }
 
-// Dense-U ACA products (aca_forward's `fac.dense_u * w` branch,
-// src/matvec.cpp:158,173): small host GEMMs, as in the reference.
-MultiVector host_gemm(const Matrix& a, bool conj_a, const MultiVector& b) {
-    const Index m = conj_a ? a.cols() : a.rows(), k = conj_a ? a.rows() : a.cols();
-    MultiVector c(m, b.cols());
-    for (Index j = 0; j < b.cols(); ++j)
-        for (Index i = 0; i < m; ++i) {
-            Complex s = 0;
-            for (Index l = 0; l < k; ++l) s += (conj_a ? std::conj(a(l, i)) : a(i, l)) * b(l, j);
-            c(i, j) = s;
-        }
-    return c;
+// AcaFactors with a dense U (aca_forward / aca_adjoint's `fac.dense_u`
+// branches, src/matvec.cpp:158,173): a dense-U device store.
+std::shared_ptr<tm_store> dense_store_of(const AcaFactors& f) {
+    if (f.dense_u.cols() != f.v.cols()) throw ContractViolation("AcaFactors: dense_u and v column counts differ");
+    std::uint64_t h = hash_words(0xDE05Eull, f.dense_u.data(), sizeof(Complex) * std::size_t(f.dense_u.size()));
+    h = hash_words(h, f.v.data(), sizeof(Complex) * std::size_t(f.v.size()));
+    const Dims3 d{f.dense_u.rows(), 1, 1};
+    return cached(key_of(2, 1, f.rank(), d, f.v.rows(), h), [&] {
+        tm_store* st = nullptr;
+        check(tm_store_create_dense_aca(reinterpret_cast<const double*>(f.dense_u.data()), f.dense_u.rows(),
+                                        reinterpret_cast<const double*>(f.v.data()), f.v.rows(), f.rank(), 0,
+                                        current_device(), g_dtype, &st));
+        return st;
+    });
 }
 
 }  // namespace
@@ -270,16 +361,16 @@ MultiVector stacked_forward(const TuckerColumns& z, const MultiVector& x, int, O
     if (x.rows() != z.ncols)
         throw ContractViolation("stacked_forward: x has " + std::to_string(x.rows()) + " rows, expected " +
                                 std::to_string(z.ncols));
-    b200::DeviceStore s(z, g_dtype, current_device());
-    return fwd(s.handle(), g_dtype, x, ops);
+    auto s = store_of(z);
+    return fwd(s.get(), g_dtype, x, ops);
 }
 
 MultiVector stacked_adjoint(const TuckerColumns& z, const MultiVector& x, int, OpCounts* ops) {
     if (x.rows() != z.rows())
         throw ContractViolation("stacked_adjoint: x has " + std::to_string(x.rows()) + " rows, expected " +
                                 std::to_string(z.rows()));
-    b200::DeviceStore s(z, g_dtype, current_device());
-    return adj(s.handle(), g_dtype, x, ops);
+    auto s = store_of(z);
+    return adj(s.get(), g_dtype, x, ops);
 }
 
 namespace {
@@ -307,8 +398,8 @@ Complex element(const TuckerTensor& tt, Index i1, Index i2, Index i3) {
     z.q = 1;
     z.grid_dims = d;
     z.tensor = [&](Index, int) -> const TuckerTensor& { return tt; };
-    b200::DeviceStore s(z, g_dtype, current_device());
-    return store_row(s.handle(), g_dtype, i1 + d[0] * (i2 + d[1] * i3), 1)[0];
+    auto s = store_of(z);
+    return store_row(s.get(), g_dtype, i1 + d[0] * (i2 + d[1] * i3), 1)[0];
 }
 
 MultiVector row_of_compressed_u(const AcaFactors& fac, Index i) {
@@ -325,8 +416,7 @@ MultiVector aca_forward(const AcaFactors& fac, const MultiVector& x, int) {
     if (x.rows() != fac.cols())
         throw ContractViolation("aca_forward: x has " + std::to_string(x.rows()) + " rows, expected " +
                                 std::to_string(fac.cols()));
-    if (!fac.compressed()) return host_gemm(fac.dense_u, false, host_gemm(fac.v, true, x));
-    auto s = store_of(fac);
+    auto s = fac.compressed() ? store_of(fac) : dense_store_of(fac);
     return aca_fwd(s.get(), g_dtype, x);
 }
 
@@ -334,8 +424,7 @@ MultiVector aca_adjoint(const AcaFactors& fac, const MultiVector& phi, int) {
     if (phi.rows() != fac.rows())
         throw ContractViolation("aca_adjoint: phi has " + std::to_string(phi.rows()) + " rows, expected " +
                                 std::to_string(fac.rows()));
-    if (!fac.compressed()) return host_gemm(fac.v, false, host_gemm(fac.dense_u, true, phi));
-    auto s = store_of(fac);
+    auto s = fac.compressed() ? store_of(fac) : dense_store_of(fac);
     return aca_adj(s.get(), g_dtype, phi);
 }
 

@@ -105,8 +105,11 @@ struct TcDesc {
     int64_t off_v;
     int64_t off_u2;
     int64_t off_u3;  // float2 offset of U3t (n3 x r3 row-major) in the store arena
-    int32_t r2, r3, pad0, pad1, pad2, pad3;
+    int32_t r2, r3, pad0, pad1, pad2;
+    int32_t fexp;    // factor normalisation exponents (factor_scale_kernel): e2 in bits 0-7, e3 in 8-15 (signed)
 };
+__host__ __device__ inline int fexp_e2(int32_t f) { return int(int8_t(f & 0xff)); }
+__host__ __device__ inline int fexp_e3(int32_t f) { return int(int8_t((f >> 8) & 0xff)); }
 static_assert(sizeof(TcDesc) % 16 == 0, "TcDesc is bulk-copied (16-byte granularity)");
 
 struct TcGeom {
@@ -773,17 +776,18 @@ __global__ void xmax_kernel(const float2* __restrict__ x, int64_t ldx, int64_t n
 // The forward's B operand for a pass of p right-hand sides:
 // B[k][n = i3 p + c][K = kofs[k][j] + r] = sb x[j, c] U3_j[i3, r] as a 2-term
 // fp16 split in 4 planes [Re hi, Im hi, Re lo, Im lo][q][nt][kpad] (sb =
-// fp16_scale(max |x|); |U3| <= 1).  x_j rides in B so the producers' A
+// fp16_scale(max |x|); U3 normalised by 2^-e3 so |U3| <= 1, factor_scale_kernel).  x_j rides in B so the producers' A
 // operand is x-free and, with p > 1, W = V x_2 U2 is produced once for all
 // right-hand sides (they share the tile's N space).  One block per tensor.
 __global__ void build_xb_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena,
                                 const int* __restrict__ kofs, const float2* __restrict__ x, int64_t ldx, int p,
                                 int64_t ncols, int q, int n3, int64_t nt, int64_t kpad, const float* __restrict__ xmax,
-                                __half* __restrict__ planes) {
+                                const TcDesc* __restrict__ tcd, __half* __restrict__ planes) {
     const int64_t t = blockIdx.x;  // tensor index k*ncols + j
     const int k = int(t / ncols);
     const int64_t j = t - int64_t(k) * ncols;
     const TDesc d = td[t];
+    const int e3 = fexp_e3(tcd[t].fexp);
     const int64_t k0 = kofs[t];
     const int64_t plane = int64_t(q) * nt * kpad;
     const float sb = fp16_scale(*xmax);
@@ -791,7 +795,8 @@ __global__ void build_xb_kernel(const TDesc* __restrict__ td, const float2* __re
         const int c = e / (n3 * d.r3);
         const int rem = e - c * (n3 * d.r3);
         const int i3 = rem / d.r3, r = rem - i3 * d.r3;
-        const float2 u = arena[d.off_u3 + rem];
+        const float2 u0 = arena[d.off_u3 + rem];
+        const float2 u = make_float2(ldexpf(u0.x, -e3), ldexpf(u0.y, -e3));  // normalised U3 (|u| <= 1), exact
         const float2 xv = x[j + ldx * c];
         const float br = (xv.x * u.x - xv.y * u.y) * sb, bi = (xv.x * u.y + xv.y * u.x) * sb;
         const __half rh = __float2half_rn(br), ih = __float2half_rn(bi);
@@ -847,6 +852,7 @@ __global__ void build_v_kernel(const TDesc* __restrict__ td, const float2* __res
     const int r23 = d.r2 * d.r3;
     const int n1p = (n1 + 3) & ~3;
     float2* out = varena + tcd[t].off_v;
+    const int ev = fexp_e2(tcd[t].fexp) + fexp_e3(tcd[t].fexp);  // V carries the factors' normalisation
     for (int e = threadIdx.x; e < n1p * r23; e += blockDim.x) {
         const int i1 = e / r23, bc = e - i1 * r23;
         double vr = 0.0, vi = 0.0;
@@ -859,7 +865,7 @@ __global__ void build_v_kernel(const TDesc* __restrict__ td, const float2* __res
                 vi += double(ua.x) * ga.y + double(ua.y) * ga.x;
             }
         }
-        const float fr = float(vr), fi = float(vi);
+        const float fr = float(ldexp(vr, ev)), fi = float(ldexp(vi, ev));
         const int b = bc % d.r2, c = bc / d.r2;  // bc = b + r2 c (core order)
         out[int64_t(i1 >> 2) * 4 * r23 + int64_t(c + d.r3 * b) * 4 + (i1 & 3)] = make_float2(fr, fi);
     }
@@ -867,7 +873,8 @@ __global__ void build_v_kernel(const TDesc* __restrict__ td, const float2* __res
 
 
 // Per tensor: max over (i1, c) of the 2-norm over b of V[i1, b, c] — a
-// bound on |W[row, c]| / |x_j| because every row of U2 has norm <= 1.
+// bound on |W[row, c]| / |x_j| because every row of the normalised U2 has
+// norm <= 1 (factor_scale_kernel).
 __global__ void vbound_kernel(const TDesc* __restrict__ td, const TcDesc* __restrict__ tcd,
                               const float2* __restrict__ varena, int n1, float* __restrict__ vbound) {
     const int64_t t = blockIdx.x;
@@ -907,9 +914,62 @@ __global__ void build_u2_kernel(const TDesc* __restrict__ td, const float2* __re
     const int ld2 = d.r2 | 1;
     const int n2p = (n2 + TC_TI2 - 1) / TC_TI2 * TC_TI2;
     float2* out = u2arena + tcd[t].off_u2;
+    const int e2 = fexp_e2(tcd[t].fexp);
     for (int e = threadIdx.x; e < n2p * ld2; e += blockDim.x) {
         const int i2 = e / ld2, b = e - i2 * ld2;
-        out[e] = (i2 < n2 && b < d.r2) ? arena[d.off_u2 + int64_t(i2) * d.r2 + b] : make_float2(0.f, 0.f);
+        const float2 u = (i2 < n2 && b < d.r2) ? arena[d.off_u2 + int64_t(i2) * d.r2 + b] : make_float2(0.f, 0.f);
+        out[e] = make_float2(ldexpf(u.x, -e2), ldexpf(u.y, -e2));  // normalised U2 (row norms <= 1), exact
+    }
+}
+
+// ---------------------------------------- factor normalisation (per tensor)
+// The tensor-core operands rely on two bounds that hold for the reference's
+// orthonormal factors: |U3| <= 1 (fp16 scale of the B planes) and U2 row
+// norms <= 1 (the |W| bound behind the A scale).  A valid store need not be
+// orthonormal (proj/src/io.cpp:131-139 checks ranks only): T = G x1 U1 x2 U2
+// x3 U3 is unchanged by U3 -> U3 2^-e3, U2 -> U2 2^-e2, V = U1 x1 G -> V
+// 2^(e2+e3), and powers of two are exact.  Per tensor: e3 = the binary
+// exponent of max |U3| and e2 that of the largest U2 row norm (frexp: the
+// normalised maxima fall in [1/2, 1)), packed into TcDesc::fexp.
+__global__ void factor_scale_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena, int n2, int n3,
+                                    TcDesc* __restrict__ tcd) {
+    const int64_t t = blockIdx.x;
+    const TDesc d = td[t];
+    float m3 = 0.f, m2 = 0.f;
+    for (int e = threadIdx.x; e < n3 * d.r3; e += blockDim.x) {
+        const float2 u = arena[d.off_u3 + e];
+        m3 = fmaxf(m3, sqrtf(u.x * u.x + u.y * u.y));
+    }
+    for (int i2 = threadIdx.x; i2 < n2; i2 += blockDim.x) {
+        float s2 = 0.f;
+        for (int b = 0; b < d.r2; ++b) {
+            const float2 u = arena[d.off_u2 + int64_t(i2) * d.r2 + b];
+            s2 += u.x * u.x + u.y * u.y;
+        }
+        m2 = fmaxf(m2, sqrtf(s2) * 1.0001f);  // margin for the fp32 norm's rounding
+    }
+    __shared__ float r3[32], r2[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        m3 = fmaxf(m3, __shfl_xor_sync(0xffffffffu, m3, o));
+        m2 = fmaxf(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        r3[threadIdx.x >> 5] = m3;
+        r2[threadIdx.x >> 5] = m2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+            m3 = fmaxf(m3, r3[w]);
+            m2 = fmaxf(m2, r2[w]);
+        }
+        int e3 = 0, e2 = 0;
+        if (m3 > 0.f) frexpf(m3, &e3);
+        if (m2 > 0.f) frexpf(m2, &e2);
+        e3 = max(-100, min(100, e3));
+        e2 = max(-100, min(100, e2));
+        tcd[t].fexp = (e2 & 0xff) | ((e3 & 0xff) << 8);
     }
 }
 

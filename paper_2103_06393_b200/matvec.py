@@ -157,6 +157,19 @@ class DeviceStore:
         return cls(h, int(device))
 
     @classmethod
+    def dense_aca(cls, u, v, dtype="c64", device=0):
+        """AcaFactors with a dense U (m1 x r) and V (m2 x r): only aca_forward /
+        aca_adjoint apply (src/matvec.cpp:158,173), on the device."""
+        un = np.asfortranarray(np.asarray(u, dtype=np.complex128))
+        vn = np.asfortranarray(np.asarray(v, dtype=np.complex128))
+        if un.ndim != 2 or vn.ndim != 2 or un.shape[1] != vn.shape[1]:
+            raise ContractViolation("dense ACA: U and V need the same column count")
+        h = ctypes.c_void_p()
+        _check(lib().tm_store_create_dense_aca(un.ctypes.data, un.shape[0], vn.ctypes.data, vn.shape[0], un.shape[1],
+                                               0, int(device), _DT[dtype], ctypes.byref(h)))
+        return cls(h, int(device))
+
+    @classmethod
     def from_compressed(cls, cc, dtype="c64", device=0):
         """From any object with grid_dims, q, ranks, payload (and v for ACA)."""
         return cls.from_arrays(cc.grid_dims, cc.q, cc.ranks, cc.payload, dtype, device, getattr(cc, "v", None))
@@ -252,6 +265,7 @@ class DeviceStore:
         td = _torch_dtype(self.dtype)
         if x.device.type != "cuda" or x.device.index != self.device:
             raise ContractViolation(f"input is on {x.device}, store is on cuda:{self.device}")
+        x_in = x
         squeeze = x.dim() == 1
         if squeeze:
             x = x.reshape(-1, 1)
@@ -267,9 +281,29 @@ class DeviceStore:
             x = x.t().contiguous().t()
         inrows, p = x.shape
         ldx = x.stride(1) if p > 1 else max(inrows, 1)
-        if out is None:
+        own_out = out is None
+        if own_out:
             out = torch.empty((p, outrows), dtype=td, device=x.device).t()
+        else:  # a caller's buffer: exact shape, dtype, device and column-major layout
+            o2 = out.reshape(-1, 1) if out.dim() == 1 else out
+            if (o2.dim() != 2 or tuple(o2.shape) != (outrows, p) or out.dtype != td
+                    or out.device != x.device or o2.stride(0) != 1 or (p > 1 and o2.stride(1) < outrows)):
+                raise ContractViolation(
+                    f"out must be a column-major {td} tensor of shape ({outrows}, {p}) on {x.device}, got "
+                    f"{tuple(out.shape)} {out.dtype} strides {tuple(out.stride())} on {out.device}")
+            out = o2
         ldo = out.stride(1) if p > 1 else max(outrows, 1)
+        if stream is not None:
+            # work enqueued on a caller's stream: it first waits for torch's
+            # current stream (where x was produced and temporaries were
+            # allocated), and the allocator must not recycle those
+            # temporaries before the caller's stream is done with them
+            ext = torch.cuda.ExternalStream(stream, device=x.device)
+            ext.wait_stream(torch.cuda.current_stream(x.device))
+            if x.data_ptr() != x_in.data_ptr():
+                x.record_stream(ext)
+            if own_out:
+                out.record_stream(ext)
         st = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
         o = np.zeros(2, np.int64)
         args = [self.handle, x.data_ptr(), ldx, inrows, p, out.data_ptr(), ldo, TM_DEVICE, st]

@@ -356,17 +356,18 @@ def test_tensor_core_long_k(product, monkeypatch, chain):
     ((9, 20, 70), 1, 11, 3, 16, 40),      # rank-16 factors, two RHS blocks (32 + 8)
 ])
 def test_batched_forward(oracle, product, monkeypatch, dims, q, m, rmin, rmax, p):
-    """Batched multi-RHS forward (fwd_mrhs_kernel: T decompressed once per tile,
-    T.X on tcgen05) vs the oracle and vs the per-RHS tensor-core forward."""
+    """Batched multi-RHS forward (one pass: W shared by all p right-hand
+    sides in the N space) vs the oracle and vs one-RHS passes (the B-operand
+    budget TMB_XB_CAP_MB=1 forces a pass per right-hand side)."""
     O, P = oracle, product
     cc = ragged_store(dims, q, m, rmin, rmax, seed=11 * m + p)
     ref = O.OracleStore(cc.rounded_c64())
     ds = P.DeviceStore.from_compressed(cc, "c64")
     x = cn01(m, p, 21).astype(np.complex64).astype(np.complex128)
     y_b = ds.forward(x)
-    monkeypatch.setenv("TMB_DISABLE_MRHS", "1")
+    monkeypatch.setenv("TMB_XB_CAP_MB", "1")
     y_s = ds.forward(x)
-    monkeypatch.delenv("TMB_DISABLE_MRHS")
+    monkeypatch.delenv("TMB_XB_CAP_MB")
     y_ref = ref.forward(x)
     assert rel(y_b, y_ref) <= 1e-5
     assert rel(y_s, y_ref) <= 1e-5
