@@ -107,6 +107,11 @@ TM_API int tm_store_destroy(tm_store* s);
 TM_API int tm_store_info(const tm_store* s, int32_t* q, int64_t* ncols, int64_t* dims3, int32_t* dtype,
                          int64_t* m2, int64_t* device_bytes);
 
+/* Which kernels the store's products run: 1 = tcgen05 tensor-core kernels
+ * (c64 stores with every rank <= 32 whose factor slots fit the shared-memory
+ * plan), 0 = CUDA-core kernels (c128, larger ranks, TMB_DISABLE_TC=1). */
+TM_API int tm_store_kernels(const tm_store* s, int32_t* forward_tc, int32_t* adjoint_tc);
+
 /*
  * Y = Zbc X  — forward(cc, x, workers, ops) (src/matvec.cpp:132-138) and
  * stacked_forward (src/matvec.cpp:17-65).  x: xrows x p (xrows must equal
@@ -157,6 +162,47 @@ TM_API int tm_rows(tm_store* s, const int64_t* rows, int64_t nrows, void* out, i
 /* Exact OpCounts of one product at p right-hand sides, without running it
  * (reconstruct_madds, src/matvec.cpp:10-15; accumulate term :51,95). */
 TM_API int tm_opcounts(const tm_store* s, int64_t p, int64_t* decompress_madds, int64_t* accumulate_madds);
+
+/* ------------------------------------------------------------ multi-GPU --
+ * Column sharding over the GPUs of one box, driven by
+ * one host thread through a single-process NCCL communicator
+ * (ncclCommInitAll).  Replaces the reference's worker pool over columns
+ * (parallel_for, src/parallel.cpp:13-48; stacked_forward's per-worker
+ * partials summed serially, src/matvec.cpp:30-38,58-59): each GPU holds a
+ * contiguous, cost-balanced column range (all q components) as a regular
+ * store; the forward's partial y is reduced to the root GPU (devices[0]) per
+ * component as soon as every GPU has finished that component, overlapping
+ * the later components' waves; the adjoint broadcasts Phi and gathers the
+ * rows of z (no reduction: rows are independent, src/matvec.cpp:78-96).
+ * ACA stores shard U with the matching columns of V.  NCCL is loaded at run
+ * time by tm_comm_init (the copy already in the process, $TMB_NCCL_LIB, or
+ * libnccl.so.2).  A device list that repeats a device makes an EMULATED
+ * communicator (collectives as device-local copies / adds): a functional
+ * check of the sharded orchestration on one GPU, not a measurement. */
+typedef struct tm_comm tm_comm;
+typedef struct tm_sharded tm_sharded;
+
+TM_API int tm_comm_init(int ndev, const int* devices, tm_comm** out);
+TM_API int tm_comm_finalize(tm_comm* comm);
+TM_API int tm_comm_info(const tm_comm* comm, int32_t* ndev, int32_t* emulated);
+
+/* desc as for tm_store_create, host payload / V only; shard d lives on
+ * devices[d].  ranges (optional, 2 * nshards) receives each shard's [c0, c1). */
+TM_API int tm_sharded_create(const tm_store_desc* desc, tm_comm* comm, int dtype, tm_sharded** out);
+TM_API int tm_sharded_destroy(tm_sharded* s);
+TM_API int tm_sharded_info(const tm_sharded* s, int32_t* nshards, int64_t* ranges, int64_t* device_bytes);
+
+/* As tm_forward / tm_adjoint / tm_aca_*; with TM_DEVICE the inputs and
+ * outputs live on devices[0] and the work is ordered after / before
+ * `stream` (a cudaStream_t of devices[0]). */
+TM_API int tm_sharded_forward(tm_sharded* s, const void* x, int64_t ldx, int64_t xrows, int64_t p, void* y,
+                              int64_t ldy, int where, void* stream, int64_t* ops);
+TM_API int tm_sharded_adjoint(tm_sharded* s, const void* phi, int64_t ldphi, int64_t phirows, int64_t p, void* z,
+                              int64_t ldz, int where, void* stream, int64_t* ops);
+TM_API int tm_sharded_aca_forward(tm_sharded* s, const void* x, int64_t ldx, int64_t xrows, int64_t p, void* y,
+                                  int64_t ldy, int where, void* stream);
+TM_API int tm_sharded_aca_adjoint(tm_sharded* s, const void* phi, int64_t ldphi, int64_t phirows, int64_t p,
+                                  void* z, int64_t ldz, int where, void* stream);
 
 /* Thread-local message of the last failed call on this thread. */
 TM_API const char* tm_last_error(void);

@@ -238,6 +238,44 @@ MultiVector adjoint(const DeviceStore& s, const MultiVector& phi, OpCounts* ops 
 MultiVector aca_forward(const DeviceStore& s, const MultiVector& x);
 MultiVector aca_adjoint(const DeviceStore& s, const MultiVector& phi);
 
+// Multi-GPU: the columns sharded over the GPUs of one box (tm_comm_* /
+// tm_sharded_*, tuckmat_b200.h); products take and return host blocks.
+class Communicator {
+public:
+    explicit Communicator(const std::vector<int>& devices);
+    ~Communicator();
+    Communicator(const Communicator&) = delete;
+    Communicator& operator=(const Communicator&) = delete;
+    tm_comm* handle() const { return h_; }
+
+private:
+    tm_comm* h_ = nullptr;
+};
+
+class ShardedStore {
+public:
+    ShardedStore(const CompressedCoupling& cc, Communicator& comm, int dtype = TM_C128);
+    ShardedStore(const AcaFactors& fac, Communicator& comm, int dtype = TM_C128);
+    ~ShardedStore();
+    ShardedStore(const ShardedStore&) = delete;
+    ShardedStore& operator=(const ShardedStore&) = delete;
+    tm_sharded* handle() const { return h_; }
+    int dtype() const { return dtype_; }
+    Index rows() const { return rows_; }
+    Index cols() const { return cols_; }
+    Index m2() const { return m2_; }
+
+private:
+    tm_sharded* h_ = nullptr;
+    int dtype_ = TM_C128;
+    Index rows_ = 0, cols_ = 0, m2_ = 0;
+};
+
+MultiVector forward(const ShardedStore& s, const MultiVector& x, OpCounts* ops = nullptr);
+MultiVector adjoint(const ShardedStore& s, const MultiVector& phi, OpCounts* ops = nullptr);
+MultiVector aca_forward(const ShardedStore& s, const MultiVector& x);
+MultiVector aca_adjoint(const ShardedStore& s, const MultiVector& phi);
+
 }  // namespace b200
 }  // namespace tuckmat
 

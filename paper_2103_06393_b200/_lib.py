@@ -22,9 +22,11 @@ TM_C64, TM_C128 = 0, 1
 TM_HOST, TM_DEVICE = 0, 1
 
 EXPORTED = [
-    "tm_store_create", "tm_store_create_dense_aca", "tm_store_load_ctc1", "tm_store_load_cta1", "tm_store_destroy", "tm_store_info",
+    "tm_store_create", "tm_store_create_dense_aca", "tm_store_load_ctc1", "tm_store_load_cta1", "tm_store_destroy", "tm_store_info", "tm_store_kernels",
     "tm_forward", "tm_adjoint", "tm_aca_forward", "tm_aca_adjoint", "tm_opcounts", "tm_rows", "tm_last_error",
     "tm_assemble_columns",
+    "tm_comm_init", "tm_comm_finalize", "tm_comm_info", "tm_sharded_create", "tm_sharded_destroy", "tm_sharded_info",
+    "tm_sharded_forward", "tm_sharded_adjoint", "tm_sharded_aca_forward", "tm_sharded_aca_adjoint",
     "tm_launch_count", "tm_version",
 ]
 
@@ -61,9 +63,12 @@ def lib():
             L.tm_store_create.argtypes = [ctypes.POINTER(StoreDesc), i32, i32, ctypes.POINTER(vp)]
             L.tm_store_load_ctc1.argtypes = [ctypes.c_char_p, i32, i32, ctypes.POINTER(vp)]
             L.tm_store_load_cta1.argtypes = [ctypes.c_char_p, i32, i32, ctypes.POINTER(vp)]
-            L.tm_store_create_dense_aca.argtypes = [vp, i64, vp, i64, i64, i32, i32, i32, ctypes.POINTER(vp)]
+            if hasattr(L, "tm_store_create_dense_aca"):  # (older A/B variants lack the newer entry points)
+                L.tm_store_create_dense_aca.argtypes = [vp, i64, vp, i64, i64, i32, i32, i32, ctypes.POINTER(vp)]
             L.tm_store_destroy.argtypes = [vp]
             L.tm_store_info.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+            if hasattr(L, "tm_store_kernels"):
+                L.tm_store_kernels.argtypes = [vp, vp, vp]
             L.tm_forward.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp, vp]
             L.tm_adjoint.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp, vp]
             L.tm_aca_forward.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp]
@@ -72,6 +77,17 @@ def lib():
             L.tm_rows.argtypes = [vp, vp, i64, vp, i64, i32, vp]
             L.tm_assemble_columns.argtypes = [vp, ctypes.c_double, vp, i32, i32, ctypes.c_double, vp, i64, vp, i64,
                                               vp, vp]
+            if hasattr(L, "tm_comm_init"):
+                L.tm_comm_init.argtypes = [i32, vp, ctypes.POINTER(vp)]
+                L.tm_comm_finalize.argtypes = [vp]
+                L.tm_comm_info.argtypes = [vp, vp, vp]
+                L.tm_sharded_create.argtypes = [ctypes.POINTER(StoreDesc), vp, i32, ctypes.POINTER(vp)]
+                L.tm_sharded_destroy.argtypes = [vp]
+                L.tm_sharded_info.argtypes = [vp, vp, vp, vp]
+                L.tm_sharded_forward.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp, vp]
+                L.tm_sharded_adjoint.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp, vp]
+                L.tm_sharded_aca_forward.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp]
+                L.tm_sharded_aca_adjoint.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp]
             L.tm_last_error.restype = ctypes.c_char_p
             L.tm_launch_count.restype = ctypes.c_int64
             _lib = L

@@ -69,7 +69,7 @@ def build(force=False, verbose=False, ptxas_verbose=False):
         _run(cmd, verbose)
         objs.append(obj)
     tmp = OUT + ".tmp"
-    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lpthread"], verbose)
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl", "-lpthread"], verbose)
     shutil.move(tmp, OUT)
     return OUT
 

@@ -106,7 +106,7 @@ __device__ __forceinline__ void aj2_consume_column(const float2* __restrict__ V,
 // adj_tc_kernel: each N = 2 CH window [-U3i | U3r] / [U3r | U3i] takes its
 // first CH rows from the even CTA and the rest from the odd one, so a CTA
 // stages 4 of the 6 U3 planes' halves and reads half of B per MMA.
-template <int NR, bool PAIR>
+template <int NR, bool PAIR, bool BIG = false>  // BIG: r3 > 16 (see adj_tc_kernel)
 __global__ void __launch_bounds__(AJ_THREADS, 1)
     adj_tc2_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                    const TcDesc* __restrict__ tcd, const float2* __restrict__ varena,
@@ -337,15 +337,36 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                     float2 a[NR];
 #define A2_COL(NU) \
     aj2_consume_column<NU, NR>(V, U2, (g.debug & 4) ? 0 : r2, r2 | 1, r3, h, lane, qbase + uint32_t(soff), &fempty[fs], a)
-                    switch ((r3 + AJ_NH - 1) / AJ_NH) {
-                        case 1: A2_COL(1); break;
-                        case 2: A2_COL(2); break;
-                        case 3: A2_COL(3); break;
-                        case 4: A2_COL(4); break;
-                        case 5: A2_COL(5); break;
-                        case 6: A2_COL(6); break;
-                        case 7: A2_COL(7); break;
-                        default: A2_COL(8); break;
+                    if constexpr (BIG) {
+                        switch ((r3 + AJ_NH - 1) / AJ_NH) {
+                            case 1: A2_COL(1); break;
+                            case 2: A2_COL(2); break;
+                            case 3: A2_COL(3); break;
+                            case 4: A2_COL(4); break;
+                            case 5: A2_COL(5); break;
+                            case 6: A2_COL(6); break;
+                            case 7: A2_COL(7); break;
+                            case 8: A2_COL(8); break;
+                            case 9: A2_COL(9); break;
+                            case 10: A2_COL(10); break;
+                            case 11: A2_COL(11); break;
+                            case 12: A2_COL(12); break;
+                            case 13: A2_COL(13); break;
+                            case 14: A2_COL(14); break;
+                            case 15: A2_COL(15); break;
+                            default: A2_COL(16); break;
+                        }
+                    } else {
+                        switch ((r3 + AJ_NH - 1) / AJ_NH) {
+                            case 1: A2_COL(1); break;
+                            case 2: A2_COL(2); break;
+                            case 3: A2_COL(3); break;
+                            case 4: A2_COL(4); break;
+                            case 5: A2_COL(5); break;
+                            case 6: A2_COL(6); break;
+                            case 7: A2_COL(7); break;
+                            default: A2_COL(8); break;
+                        }
                     }
 #undef A2_COL
                     if (++fs == TC_JR) {

@@ -169,7 +169,11 @@ __device__ __forceinline__ float2 aj_consume_column(const float2* __restrict__ V
     return make_float2(ar, ai);
 }
 
-template <bool PAIR>
+// NSTX: A/B stage count override (0 = AJ_NST / AJ_NST2); 2 for stores whose
+// rank-(r2, r3) factor slots leave no room for the default ring.
+// BIG: stores with r3 > 16 (up to TC_RMAX = 32), a separate instantiation so
+// the r3 <= 16 kernels keep their register budget.
+template <bool PAIR, int NSTX = 0, bool BIG = false>
 __global__ void __launch_bounds__(AJ_THREADS, 1)
     adj_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                   const TcDesc* __restrict__ tcd, const float2* __restrict__ varena,
@@ -181,7 +185,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
     // PAIR: the M = 256 MMA takes B rows [0, 128) of each N = 256 window from
     // the even CTA and [128, 256) from the odd one: the even CTA holds planes
     // (-U3i, U3r), the odd one (U3r, U3i), hi and lo — 4 planes per stage.
-    constexpr int NST = PAIR ? AJ_NST2 : AJ_NST;
+    constexpr int NST = NSTX ? NSTX : (PAIR ? AJ_NST2 : AJ_NST);
     constexpr int BSTAGE = PAIR ? 4 * AJ_B_PLANE : AJ_B_STAGE;
     unsigned char* sA = sm;
     unsigned char* sB = sA + NST * AJ_A_STAGE;
@@ -388,15 +392,36 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                     float2 a;
 #define AJ_COL(NU) \
     a = aj_consume_column<NU>(V, U2, (g.debug & 4) ? 0 : r2, r2 | 1, r3, h, lane, qbase + uint32_t(soff), &fempty[fs])
-                    switch ((r3 + AJ_NH - 1) / AJ_NH) {
-                        case 1: AJ_COL(1); break;
-                        case 2: AJ_COL(2); break;
-                        case 3: AJ_COL(3); break;
-                        case 4: AJ_COL(4); break;
-                        case 5: AJ_COL(5); break;
-                        case 6: AJ_COL(6); break;
-                        case 7: AJ_COL(7); break;
-                        default: AJ_COL(8); break;
+                    if constexpr (BIG) {
+                        switch ((r3 + AJ_NH - 1) / AJ_NH) {
+                            case 1: AJ_COL(1); break;
+                            case 2: AJ_COL(2); break;
+                            case 3: AJ_COL(3); break;
+                            case 4: AJ_COL(4); break;
+                            case 5: AJ_COL(5); break;
+                            case 6: AJ_COL(6); break;
+                            case 7: AJ_COL(7); break;
+                            case 8: AJ_COL(8); break;
+                            case 9: AJ_COL(9); break;
+                            case 10: AJ_COL(10); break;
+                            case 11: AJ_COL(11); break;
+                            case 12: AJ_COL(12); break;
+                            case 13: AJ_COL(13); break;
+                            case 14: AJ_COL(14); break;
+                            case 15: AJ_COL(15); break;
+                            default: AJ_COL(16); break;
+                        }
+                    } else {
+                        switch ((r3 + AJ_NH - 1) / AJ_NH) {
+                            case 1: AJ_COL(1); break;
+                            case 2: AJ_COL(2); break;
+                            case 3: AJ_COL(3); break;
+                            case 4: AJ_COL(4); break;
+                            case 5: AJ_COL(5); break;
+                            case 6: AJ_COL(6); break;
+                            case 7: AJ_COL(7); break;
+                            default: AJ_COL(8); break;
+                        }
                     }
 #undef AJ_COL
                     if (++fs == TC_JR) {

@@ -93,6 +93,18 @@ __global__ void aca_vt_kernel(const C* __restrict__ v, int64_t m2, int64_t rc, c
     z[i + ldz * c] = cmake<C>(R(sx), R(sy));
 }
 
+// y[i] += x[i] (the emulated communicator's reduce, tm_shard.cuh)
+template <typename C>
+__global__ void add_kernel(C* __restrict__ y, const C* __restrict__ x, int64_t n) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        C a = y[i];
+        const C b = x[i];
+        a.x += b.x;
+        a.y += b.y;
+        y[i] = a;
+    }
+}
+
 // y(:, c) = 0 for a (rows x p) block with leading dimension ldy.
 template <typename C>
 __global__ void zero_kernel(C* __restrict__ y, int64_t rows, int64_t p, int64_t ldy) {

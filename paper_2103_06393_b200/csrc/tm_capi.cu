@@ -9,7 +9,9 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <fstream>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -68,6 +70,18 @@ struct DeviceGuard {
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+        o.p = nullptr;
+        o.bytes = 0;
+    }
+    void release() {  // on the device that owns the buffer
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
     void* get(size_t need) {
         if (need > bytes) {
             if (p) cudaFree(p);
@@ -104,6 +118,9 @@ int guarded(F&& f) {
 }
 
 int64_t align2(int64_t v) { return (v + 1) & ~int64_t(1); }
+
+constexpr size_t kSmemBudget = 100 * 1024;  // 2 CTAs / SM
+constexpr size_t kSmemMax = 227 * 1024;
 
 }  // namespace
 
@@ -233,6 +250,14 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
     if (s->dtype != TM_C64 || s->ncols == 0 || major != 10) return;
     if (s->rmax[0] > TC_RMAX || s->rmax[1] > TC_RMAX || s->rmax[2] > TC_RMAX) return;
     if (s->dims[2] < 16) return;
+    {  // the forward's worst-case plan (single CTA, two 128-voxel i3 halves) must fit
+        const int u2_off = TC_SLOT_V + int(round16(uint32_t(TC_TI1 * s->rmax[1] * s->rmax[2] * 8)));
+        const size_t slot = size_t((u2_off + TC_TI2 * (s->rmax[1] | 1) * 8 + 127) / 128 * 128);
+        const int nst_min = s->rmax[2] > 16 ? 3 : 2;
+        const size_t need = 1024 + size_t(nst_min) * (TC_A_STAGE + 2 * TC_FPLANES * TC_NMAX * 32) + TC_JR * slot +
+                            (2 * TC_NST_MAX + 2 * TC_JR + 2) * 8 + 16;
+        if (need > kSmemMax) return;  // ranks too large for the factor ring: CUDA-core kernels
+    }
     const int64_t ntens = s->ncols * s->q;
     std::vector<int> kofs(static_cast<size_t>(ntens)), kc(static_cast<size_t>(s->q), 0);
     for (int k = 0; k < s->q; ++k) {
@@ -564,8 +589,6 @@ tm_store* create_store(const tm_store_desc& d, int device, int dtype, const tmb_
 }
 
 // ------------------------------------------------------------ kernel plan --
-constexpr size_t kSmemBudget = 100 * 1024;  // 2 CTAs / SM
-constexpr size_t kSmemMax = 227 * 1024;
 
 // Parts per tile for a launch of `tiles` (< one wave of `wave` CTAs) tiles:
 // the split s in [1, smax] that minimises the launch's rounds per part,
@@ -714,9 +737,13 @@ int num_sms(int dev) {
 // host while later waves compute; the adjoint copies Phi in block by block
 // ahead of the waves that need it (tm_forward / tm_adjoint with TM_HOST).
 struct HostPipe {
-    cudaStream_t copy = nullptr;
+    cudaStream_t copy = nullptr;  // nullptr: no host copies (only the block hook)
     void* host = nullptr;  // forward: y (out); adjoint: phi (in)
     int64_t ldhost = 0;
+    // forward: called (on the host, while enqueueing) once components [k0, k1)
+    // of right-hand sides [c0, c0 + pb) are complete on `st` — the sharded
+    // store's per-component reduce hangs off it (tm_shard.cuh)
+    std::function<void(int64_t k0, int64_t k1, int64_t c0, int64_t pb, cudaStream_t st)> block_done;
 };
 
 // One pass of the tensor-core forward over pb right-hand sides: the B
@@ -766,13 +793,19 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
         return 1024 + size_t(nst) * (TC_A_STAGE + g.b_stage) + size_t(TC_JR) * g.slot_bytes +
                (2 * TC_NST_MAX + 2 * TC_JR + 2) * 8 + 16;
     };
+    // a column opens up to ceil((15 + r3) / 16) A stages at once: 2 for r3 <= 16, 3 up to TC_RMAX
+    const int nst_min = s->rmax[2] > 16 ? 3 : 2;
     g.nst = TC_NST_MAX;
     if (const char* e = std::getenv("TMB_TC_NST")) if (std::atoi(e) >= 2) g.nst = std::min(TC_NST_MAX, std::atoi(e));
-    while (g.nst > 2 && smem_for(g.nst) > kSmemMax) --g.nst;
+    g.nst = std::max(g.nst, nst_min);
+    while (g.nst > nst_min && smem_for(g.nst) > kSmemMax) --g.nst;
     const size_t smem = smem_for(g.nst);
     if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core forward: shared-memory plan too large");
-    CK(cudaFuncSetAttribute(fwd_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    CK(cudaFuncSetAttribute(fwd_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const bool big = s->rmax[2] > 16;  // the r3 <= 32 instantiations
+    auto kfpair = big ? fwd_tc_kernel<true, true> : fwd_tc_kernel<true>;
+    auto kfsingle = big ? fwd_tc_kernel<false, true> : fwd_tc_kernel<false>;
+    CK(cudaFuncSetAttribute(kfsingle, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CK(cudaFuncSetAttribute(kfpair, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // grid: CTAs; a wave covers `wave` tiles (pair tiles in pair mode)
     // (up to 8 parts per tile when there are fewer tiles than SMs: best_split)
     const unsigned grid = g.pair ? unsigned(std::min<int64_t>(2 * 8 * g.ntiles, nsm & ~1))
@@ -841,14 +874,14 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            launched(cudaLaunchKernelEx(&cfg, fwd_tc_kernel<true>, bmap, static_cast<const TcDesc*>(s->d_tcd),
+            launched(cudaLaunchKernelEx(&cfg, kfpair, bmap, static_cast<const TcDesc*>(s->d_tcd),
                                         static_cast<const float2*>(s->d_varena),
                                         static_cast<const float2*>(s->d_u2arena), static_cast<const int*>(s->d_kc),
                                         static_cast<const int*>(s->d_kofs), g, x, ldx, y, ldy, rsum,
                                         static_cast<const float*>(wmax)),
                      "fwd_tc_kernel<pair>");
         } else {
-            fwd_tc_kernel<false><<<grid, TC_THREADS, smem, st>>>(bmap, s->d_tcd, s->d_varena, s->d_u2arena,
+            kfsingle<<<grid, TC_THREADS, smem, st>>>(bmap, s->d_tcd, s->d_varena, s->d_u2arena,
                                                                   s->d_kc, s->d_kofs, g, x, ldx, y, ldy, rsum, wmax);
             launched(cudaSuccess, "fwd_tc_kernel");
         }
@@ -859,7 +892,8 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
             launched(cudaSuccess, "fwd_split_reduce_kernel");
         }
         const int64_t bnow = (t0 + tiles) / tpb;
-        if (hp && bnow > bdone) {
+        if (hp && hp->block_done && bnow > bdone) hp->block_done(bdone, bnow, hc0, p, st);
+        if (hp && hp->copy && bnow > bdone) {
             cudaEvent_t ev;
             CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
             CK(cudaEventRecord(ev, st));
@@ -870,8 +904,8 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
                     CK(cudaMemcpyAsync(static_cast<float2*>(hp->host) + hp->ldhost * (hc0 + c) + k * nv,
                                        y + ldy * c + k * nv, size_t(nv) * sizeof(float2), cudaMemcpyDeviceToHost,
                                        hp->copy));
-            bdone = bnow;
         }
+        if (hp) bdone = std::max(bdone, bnow);
     }
     if (g.prof) {  // wait profile: mean cycles per recording thread, per role
         unsigned long long h[32];
@@ -901,11 +935,21 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     }
 }
 
-void forward_dev(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy, cudaStream_t st) {
+void forward_dev(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy, cudaStream_t st,
+                 const HostPipe* hook = nullptr) {
     if (s->tc_ok && !tc_disabled()) {
-        run_forward_tc(s, static_cast<const float2*>(x), ldx, p, static_cast<float2*>(y), ldy, st);
+        run_forward_tc(s, static_cast<const float2*>(x), ldx, p, static_cast<float2*>(y), ldy, st, hook);
         return;
     }
+    struct AtEnd {  // the CUDA-core kernels finish every component at once
+        const HostPipe* h;
+        const tm_store* s;
+        int64_t p;
+        cudaStream_t st;
+        ~AtEnd() noexcept(false) {
+            if (h && h->block_done && std::uncaught_exceptions() == 0) h->block_done(0, s->q, 0, p, st);
+        }
+    } at_end{hook, s, p, st};
     const int cn = pick_cn(s->dims[2]);
     if (s->dtype == TM_C64) {
         auto X = static_cast<const float2*>(x);
@@ -922,12 +966,17 @@ void forward_dev(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, in
     }
 }
 
-size_t adj_tc_smem(const tm_store* s) {
+// Shared-memory plan of adj_tc_kernel with `nst` A/B stages (the default
+// ring, or 2 stages for stores with large rank-(r2, r3) factor slots).
+size_t adj_tc_smem(const tm_store* s, int nst = AJ_NST) {
     const int u2_off = TC_SLOT_V + int(round16(uint32_t(TC_TI1 * s->rmax[1] * s->rmax[2] * 8)));
     const int slot = (u2_off + TC_TI2 * (s->rmax[1] | 1) * 8 + 127) / 128 * 128;
-    return 1024 + size_t(AJ_NST) * (AJ_A_STAGE + AJ_B_STAGE) + size_t(TC_JR) * slot +
-           size_t(2) * AJ_MAXCOLS * AJ_NPW * sizeof(float2) + (2 * AJ_NST + 2 * TC_JR + 4) * 8 + 16;
+    return 1024 + size_t(nst) * (AJ_A_STAGE + AJ_B_STAGE) + size_t(TC_JR) * slot +
+           size_t(2) * AJ_MAXCOLS * AJ_NPW * sizeof(float2) + (2 * nst + 2 * TC_JR + 4) * 8 + 16;
 }
+
+// The smallest tensor-core adjoint plan fits (2-stage ring)
+bool adj_tc_fits(const tm_store* s) { return adj_tc_smem(s, 2) <= kSmemMax; }
 
 // Chunk packing of the adjoint U3 planes for adj_tc2_kernel<NR> (ch = 128 / NR
 // slots per chunk, whole columns per chunk; TcDesc.pad1 (ch 64) / pad2 (ch 32)
@@ -1015,8 +1064,11 @@ void launch_adj_groups(tm_store* s, const AjGeom& g, const CUtensorMap& amap, in
     g2.ntiles = (grp0 + ngrp) * tpg;
     const size_t smem2 = adj_group_smem<NR>(g.slot_bytes, g2.pair != 0);
     if (smem2 > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: shared-memory plan too large");
-    CK(cudaFuncSetAttribute(adj_tc2_kernel<NR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
-    CK(cudaFuncSetAttribute(adj_tc2_kernel<NR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+    const bool big = s->rmax[2] > 16;  // the r3 <= 32 instantiations
+    auto k2pair = big ? adj_tc2_kernel<NR, true, true> : adj_tc2_kernel<NR, true>;
+    auto k2single = big ? adj_tc2_kernel<NR, false, true> : adj_tc2_kernel<NR, false>;
+    CK(cudaFuncSetAttribute(k2single, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+    CK(cudaFuncSetAttribute(k2pair, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
     const unsigned grid2 = g2.pair ? unsigned(std::min<int64_t>(2 * 8 * ngrp * tpg, nsm & ~1))
                                    : unsigned(std::min<int64_t>(8 * ngrp * tpg, nsm));
     const int64_t wave = g2.pair ? grid2 / 2 : grid2;
@@ -1039,14 +1091,14 @@ void launch_adj_groups(tm_store* s, const AjGeom& g, const CUtensorMap& amap, in
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            launched(cudaLaunchKernelEx(&cfg, adj_tc2_kernel<NR, true>, amap, ap.bmap,
+            launched(cudaLaunchKernelEx(&cfg, k2pair, amap, ap.bmap,
                                         static_cast<const TcDesc*>(s->d_tcd), static_cast<const float2*>(s->d_varena),
                                         static_cast<const float2*>(s->d_u2arena), static_cast<const int*>(ap.d_nch),
                                         static_cast<const int*>(ap.d_cstart), g2, static_cast<const float*>(phimax),
                                         part),
                      "adj_tc2_kernel<pair>");
         } else {
-            adj_tc2_kernel<NR, false><<<grid2, AJ_THREADS, smem2, st>>>(amap, ap.bmap, s->d_tcd, s->d_varena,
+            k2single<<<grid2, AJ_THREADS, smem2, st>>>(amap, ap.bmap, s->d_tcd, s->d_varena,
                                                                         s->d_u2arena, ap.d_nch, ap.d_cstart, g2,
                                                                         phimax, part);
             launched(cudaSuccess, "adj_tc2_kernel");
@@ -1088,10 +1140,14 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
         const char* dbg = std::getenv("TMB_TC_DEBUG");
         g.debug = dbg ? std::atoi(dbg) : 0;
     }
-    const int nst = g.pair ? AJ_NST2 : AJ_NST;
     const size_t bstage = g.pair ? size_t(4) * AJ_B_PLANE : size_t(AJ_B_STAGE);
-    const size_t smem = 1024 + size_t(nst) * (AJ_A_STAGE + bstage) + size_t(TC_JR) * g.slot_bytes +
-                        size_t(2) * AJ_MAXCOLS * AJ_NPW * sizeof(float2) + (2 * nst + 2 * TC_JR + 4) * 8 + 16;
+    auto smem_for = [&](int nst) {
+        return 1024 + size_t(nst) * (AJ_A_STAGE + bstage) + size_t(TC_JR) * g.slot_bytes +
+               size_t(2) * AJ_MAXCOLS * AJ_NPW * sizeof(float2) + (2 * nst + 2 * TC_JR + 4) * 8 + 16;
+    };
+    // the default ring, or a 2-stage ring when large factor slots leave no room for it
+    const bool small_ring = smem_for(g.pair ? AJ_NST2 : AJ_NST) > kSmemMax;
+    const size_t smem = smem_for(small_ring ? 2 : (g.pair ? AJ_NST2 : AJ_NST));
     if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core adjoint: shared-memory plan too large");
     // Phi -> scaled 2-term fp16 planes (per call)
     g.nks = (g.n3 + 15) / 16;
@@ -1133,8 +1189,13 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
                                               CU_TENSOR_MAP_SWIZZLE_32B);
     const int64_t nred = g.nrt * g.q;
     float2* part = static_cast<float2*>(s->part.get(size_t(s->ncols * p * nred) * sizeof(float2)));
-    CK(cudaFuncSetAttribute(adj_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    CK(cudaFuncSetAttribute(adj_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const bool big = s->rmax[2] > 16;  // the r3 <= 32 instantiations
+    auto kpair = big ? (small_ring ? adj_tc_kernel<true, 2, true> : adj_tc_kernel<true, 0, true>)
+                     : (small_ring ? adj_tc_kernel<true, 2> : adj_tc_kernel<true>);
+    auto ksingle = big ? (small_ring ? adj_tc_kernel<false, 2, true> : adj_tc_kernel<false, 0, true>)
+                       : (small_ring ? adj_tc_kernel<false, 2> : adj_tc_kernel<false>);
+    CK(cudaFuncSetAttribute(ksingle, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CK(cudaFuncSetAttribute(kpair, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // (up to 8 parts per tile when there are fewer tiles than SMs: best_split)
     const unsigned grid = g.pair ? unsigned(std::min<int64_t>(2 * 8 * g.ntiles, nsm & ~1))
                                  : unsigned(std::min<int64_t>(8 * g.ntiles, nsm));
@@ -1192,14 +1253,14 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            launched(cudaLaunchKernelEx(&cfg, adj_tc_kernel<true>, amap, s->adj_bmap,
+            launched(cudaLaunchKernelEx(&cfg, kpair, amap, s->adj_bmap,
                                         static_cast<const TcDesc*>(s->d_tcd), static_cast<const float2*>(s->d_varena),
                                         static_cast<const float2*>(s->d_u2arena), static_cast<const int*>(s->d_nch),
                                         static_cast<const int*>(s->d_cstart), g, static_cast<const float*>(phimax),
                                         part),
                      "adj_tc_kernel<pair>");
         } else {
-            adj_tc_kernel<false><<<grid, AJ_THREADS, smem, st>>>(amap, s->adj_bmap, s->d_tcd, s->d_varena,
+            ksingle<<<grid, AJ_THREADS, smem, st>>>(amap, s->adj_bmap, s->d_tcd, s->d_varena,
                                                                   s->d_u2arena, s->d_nch, s->d_cstart, g, phimax,
                                                                   part);
             launched(cudaSuccess, "adj_tc_kernel");
@@ -1214,7 +1275,7 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
 
 void adjoint_dev(tm_store* s, const void* phi, int64_t ldphi, int64_t p, void* z, int64_t ldz, cudaStream_t st) {
     if (s->ncols == 0 || p == 0) return;
-    if (s->tca_ok && !tc_disabled() && adj_tc_smem(s) <= kSmemMax && int64_t(p) * s->q <= 65535) {
+    if (s->tca_ok && !tc_disabled() && adj_tc_fits(s) && int64_t(p) * s->q <= 65535) {
         run_adjoint_tc(s, static_cast<const float2*>(phi), ldphi, p, static_cast<float2*>(z), ldz, st);
         return;
     }
@@ -1400,7 +1461,7 @@ bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, 
 }
 
 bool adjoint_host_pipelined(tm_store* s, const void* phi, int64_t ldphi, int64_t p, void* z, int64_t ldz) {
-    if (!(s->tca_ok && !tc_disabled() && adj_tc_smem(s) <= kSmemMax && int64_t(p) * s->q <= 65535)) return false;
+    if (!(s->tca_ok && !tc_disabled() && adj_tc_fits(s) && int64_t(p) * s->q <= 65535)) return false;
     const size_t cs = s->csize();
     void* din = s->xin.get(size_t(std::max<int64_t>(s->rows() * p, 1)) * cs);
     void* dout = s->yout.get(size_t(std::max<int64_t>(s->ncols * p, 1)) * cs);
@@ -1516,6 +1577,15 @@ TM_API int tm_store_info(const tm_store* s, int32_t* q, int64_t* ncols, int64_t*
         if (dtype) *dtype = s->dtype;
         if (m2) *m2 = s->m2;
         if (device_bytes) *device_bytes = s->device_bytes;
+    });
+}
+
+TM_API int tm_store_kernels(const tm_store* s, int32_t* forward_tc, int32_t* adjoint_tc) {
+    return guarded([&] {
+        if (!s) contract("null store");
+        const bool off = tc_disabled();
+        if (forward_tc) *forward_tc = (s->tc_ok && !off) ? 1 : 0;
+        if (adjoint_tc) *adjoint_tc = (s->tca_ok && !off && adj_tc_fits(s)) ? 1 : 0;
     });
 }
 
@@ -1756,6 +1826,8 @@ TM_API int tm_aca_adjoint(tm_store* s, const void* phi, int64_t ldphi, int64_t p
 }
 
 }  // extern "C"
+
+#include "tm_shard.cuh"
 
 // Streaming CTC1 / CTA1 ingest (tm_io.cpp): `d` carries the ranks (and V),
 // the payload comes chunk by chunk from `fill`.

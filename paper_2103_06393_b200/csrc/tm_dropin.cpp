@@ -80,9 +80,11 @@ void append_tensor(Flat& f, const TuckerTensor& tt, const Dims3& dims) {
     for (int g = 0; g < 3; ++g) put(tt.factors[g].data(), tt.factors[g].size());
 }
 
-tm_store* make_store(int q, Index ncols, const Dims3& dims,
-                     const std::function<const TuckerTensor&(Index, int)>& at, const Matrix* v, int dtype,
-                     int device) {
+// Flattens the columns (and V) into a tm_store_desc and hands it to `create`
+// (tm_store_create or tm_sharded_create).
+template <typename Create>
+void with_desc(int q, Index ncols, const Dims3& dims, const std::function<const TuckerTensor&(Index, int)>& at,
+               const Matrix* v, Create create) {
     Flat f;
     for (Index j = 0; j < ncols; ++j)
         for (int k = 0; k < q; ++k) append_tensor(f, at(j, k), dims);
@@ -102,8 +104,14 @@ tm_store* make_store(int q, Index ncols, const Dims3& dims,
         d.v = vbuf.data();
         d.m2 = v->rows();
     }
+    create(d);
+}
+
+tm_store* make_store(int q, Index ncols, const Dims3& dims,
+                     const std::function<const TuckerTensor&(Index, int)>& at, const Matrix* v, int dtype,
+                     int device) {
     tm_store* h = nullptr;
-    check(tm_store_create(&d, device, dtype, &h));
+    with_desc(q, ncols, dims, at, v, [&](const tm_store_desc& d) { check(tm_store_create(&d, device, dtype, &h)); });
     return h;
 }
 
@@ -547,6 +555,75 @@ MultiVector adjoint(const DeviceStore& s, const MultiVector& phi, OpCounts* ops)
 }
 MultiVector aca_forward(const DeviceStore& s, const MultiVector& x) { return aca_fwd(s.handle(), s.dtype(), x); }
 MultiVector aca_adjoint(const DeviceStore& s, const MultiVector& phi) { return aca_adj(s.handle(), s.dtype(), phi); }
+
+// ---- multi-GPU ---------------------------------------------------------
+Communicator::Communicator(const std::vector<int>& devices) {
+    check(tm_comm_init(int(devices.size()), devices.data(), &h_));
+}
+Communicator::~Communicator() {
+    if (h_) tm_comm_finalize(h_);
+}
+
+ShardedStore::ShardedStore(const CompressedCoupling& cc, Communicator& comm, int dtype) : dtype_(dtype) {
+    with_desc(
+        cc.q, cc.m, cc.grid_dims,
+        [&](Index j, int k) -> const TuckerTensor& {
+            return cc.columns[static_cast<std::size_t>(j)][static_cast<std::size_t>(k)];
+        },
+        nullptr, [&](const tm_store_desc& d) { check(tm_sharded_create(&d, comm.handle(), dtype, &h_)); });
+    rows_ = cc.rows();
+    cols_ = cc.m;
+}
+
+ShardedStore::ShardedStore(const AcaFactors& f, Communicator& comm, int dtype) : dtype_(dtype) {
+    if (!f.compressed()) throw ContractViolation("ShardedStore: AcaFactors needs a Tucker-compressed U");
+    with_desc(
+        f.q, f.rank(), f.grid_dims,
+        [&](Index l, int k) -> const TuckerTensor& {
+            return f.tucker_u[static_cast<std::size_t>(k)][static_cast<std::size_t>(l)];
+        },
+        &f.v, [&](const tm_store_desc& d) { check(tm_sharded_create(&d, comm.handle(), dtype, &h_)); });
+    rows_ = f.rows();
+    cols_ = f.rank();
+    m2_ = f.cols();
+}
+
+ShardedStore::~ShardedStore() {
+    if (h_) tm_sharded_destroy(h_);
+}
+
+MultiVector forward(const ShardedStore& s, const MultiVector& x, OpCounts* ops) {
+    std::int64_t o[2] = {0, 0};
+    MultiVector y = run(nullptr, s.dtype(), x, s.rows(), [&](const void* in, Index ldi, void* out, Index ldo) {
+        return tm_sharded_forward(s.handle(), in, ldi, x.rows(), x.cols(), out, ldo, TM_HOST, nullptr, o);
+    });
+    if (ops) {
+        ops->decompress_madds += o[0];
+        ops->accumulate_madds += o[1];
+    }
+    return y;
+}
+MultiVector adjoint(const ShardedStore& s, const MultiVector& phi, OpCounts* ops) {
+    std::int64_t o[2] = {0, 0};
+    MultiVector z = run(nullptr, s.dtype(), phi, s.cols(), [&](const void* in, Index ldi, void* out, Index ldo) {
+        return tm_sharded_adjoint(s.handle(), in, ldi, phi.rows(), phi.cols(), out, ldo, TM_HOST, nullptr, o);
+    });
+    if (ops) {
+        ops->decompress_madds += o[0];
+        ops->accumulate_madds += o[1];
+    }
+    return z;
+}
+MultiVector aca_forward(const ShardedStore& s, const MultiVector& x) {
+    return run(nullptr, s.dtype(), x, s.rows(), [&](const void* in, Index ldi, void* out, Index ldo) {
+        return tm_sharded_aca_forward(s.handle(), in, ldi, x.rows(), x.cols(), out, ldo, TM_HOST, nullptr);
+    });
+}
+MultiVector aca_adjoint(const ShardedStore& s, const MultiVector& phi) {
+    return run(nullptr, s.dtype(), phi, s.m2(), [&](const void* in, Index ldi, void* out, Index ldo) {
+        return tm_sharded_aca_adjoint(s.handle(), in, ldi, phi.rows(), phi.cols(), out, ldo, TM_HOST, nullptr);
+    });
+}
 
 }  // namespace b200
 }  // namespace tuckmat

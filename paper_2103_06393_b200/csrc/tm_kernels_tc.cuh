@@ -84,7 +84,7 @@ constexpr int TC_PW0 = 4;       // first producer warp
 constexpr int TC_FW0 = TC_PW0 + TC_NPW;   // first fold / epilogue warp
 constexpr int TC_THREADS = (TC_FW0 + 4) * 32;
 constexpr int TC_NMAX = 128;    // i3 per tile (N per MMA)
-constexpr int TC_RMAX = 16;     // rank bound of the tensor-core path
+constexpr int TC_RMAX = 32;     // rank bound of the tensor-core path (forward: up to 3 A stages per column)
 constexpr int TC_A_PLANE = TC_ROWS * 32;     // bytes (128 rows x 16 fp16 = one K16 stage)
 constexpr int TC_A_STAGE = 4 * TC_A_PLANE;   // 16 KB
 constexpr uint32_t TC_RUN_COL = 256;         // TMEM column of the running sum
@@ -239,7 +239,7 @@ __device__ __forceinline__ void ring_ahead(const ARing& r, uint32_t i, uint32_t 
 // rows, U2 by the NU values of c), then the scaled fp16 hi/lo split of W
 // into its K slots of the A ring.  A warp's 2-byte plane stores cover 8 rows
 // x 4 consecutive K slots (8 bytes of each 32-byte K-major row, swizzled):
-// conflict-free, one wavefront.  NU = ceil(r3/4).
+// conflict-free, one wavefront.  NU = ceil(r3/4) <= 8 (r3 <= TC_RMAX = 32).
 template <int NU, bool PAIR>
 __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, const float2* __restrict__ U2, int r2,
                                                   int ld2, int r3, int hq, int i2a, float wsc, uint64_t* fempty_s,
@@ -283,22 +283,21 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
     for (int e = 0; e < TC_NR; ++e)
 #pragma unroll
         for (int u = 0; u < NU; ++u) asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(w[e][u]) : "l"(sc2));
-    // wait for every stage (16 K) this column opens (at most two: r3 <= 16)
+    // wait for every stage (16 K) this column opens: kpos + r3 <= 15 + 32,
+    // so at most three (two while r3 <= 16); the ring holds nst >= 3 stages
     const uint32_t kend = ring.kpos + uint32_t(r3);
     if (ring.kpos == 0) mbar_wait(&empty[ring.st], ring.ph ^ 1u);
-    if (kend > 16) {
-        uint32_t s, ph;
-        ring_ahead(ring, 1, nst, s, ph);
-        mbar_wait(&empty[s], ph ^ 1u);
-    }
-    uint32_t s1, ph1;
+    uint32_t s1, ph1, s2, ph2;
     ring_ahead(ring, 1, nst, s1, ph1);
+    ring_ahead(ring, 2, nst, s2, ph2);
+    if (kend > 16) mbar_wait(&empty[s1], ph1 ^ 1u);
+    if (NU > 4 && kend > 32) mbar_wait(&empty[s2], ph2 ^ 1u);
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
         const int c = TC_NH * u + hq;
         if (u < NU - 1 || c < r3) {
             const uint32_t K = ring.kpos + uint32_t(c);
-            const uint32_t s = K < 16 ? ring.st : s1;
+            const uint32_t s = K < 16 ? ring.st : (NU <= 4 || K < 32 ? s1 : s2);
             unsigned char* st = sA + s * TC_A_STAGE;
 #pragma unroll
             for (int e = 0; e < TC_NR; ++e) {
@@ -312,22 +311,32 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
             }
         }
     }
-    if (kend >= 16) {  // the current stage is complete (and maybe the next one too, kend == 32 is impossible)
+    if (kend >= 16) {  // the current stage is complete (and with r3 > 16 maybe the next one too)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-            if (PAIR)
+            if (PAIR) {
                 mbar_arrive_cluster(mapa_shared(smem_u32(&full[ring.st]), 0));  // the even CTA issues the MMAs
-            else
+                if (NU > 4 && kend >= 32) mbar_arrive_cluster(mapa_shared(smem_u32(&full[s1]), 0));
+            } else {
                 mbar_arrive(&full[ring.st]);
+                if (NU > 4 && kend >= 32) mbar_arrive(&full[s1]);
+            }
         }
-        ring.st = s1;
-        ring.ph = ph1;
+        if (NU > 4 && kend >= 32) {
+            ring.st = s2;
+            ring.ph = ph2;
+        } else {
+            ring.st = s1;
+            ring.ph = ph1;
+        }
     }
     ring.kpos = kend & 15u;
 }
 
-template <bool PAIR>
+// BIG: stores with r3 > 16 (up to TC_RMAX = 32); the default instantiation
+// keeps the r3 <= 16 dispatch (fewer registers, smaller code).
+template <bool PAIR, bool BIG = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap bmap, const TcDesc* __restrict__ tcd,
                   const float2* __restrict__ varena, const float2* __restrict__ u2arena, const int* __restrict__ kc,
@@ -541,7 +550,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
         }
     } else if (warp >= TC_PW0 && warp < TC_FW0) {
-        static_assert(TC_NH * 4 >= TC_RMAX, "producer switch covers ceil(TC_RMAX / TC_NH)");
+        static_assert(TC_NH * 8 >= TC_RMAX, "producer switch covers ceil(TC_RMAX / TC_NH)");
         // ------------------------------------------------------ A producers
         // warp pw: i1 = pw / (4 / NR) (warp-uniform), rows i2 in a block of 8 NR;
         // lane: row lane rl in [0, 8) (rows i2a = block base + rl, + 8 e for
@@ -599,11 +608,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #define TC_COL(NU)                                                                                             \
     tc_produce_column<NU, PAIR>(V, U2, (g.debug & 1) ? 0 : r2, r2 | 1, r3, hq, i2a, g.wsc, &fempty[fs], empty, full, sA, \
                           rowbase, xorv, lane, nst, ring)
-                switch ((r3 + TC_NH - 1) / TC_NH) {
-                    case 1: TC_COL(1); break;
-                    case 2: TC_COL(2); break;
-                    case 3: TC_COL(3); break;
-                    default: TC_COL(4); break;
+                if constexpr (BIG) {
+                    switch ((r3 + TC_NH - 1) / TC_NH) {
+                        case 1: TC_COL(1); break;
+                        case 2: TC_COL(2); break;
+                        case 3: TC_COL(3); break;
+                        case 4: TC_COL(4); break;
+                        case 5: TC_COL(5); break;
+                        case 6: TC_COL(6); break;
+                        case 7: TC_COL(7); break;
+                        default: TC_COL(8); break;
+                    }
+                } else {
+                    switch ((r3 + TC_NH - 1) / TC_NH) {
+                        case 1: TC_COL(1); break;
+                        case 2: TC_COL(2); break;
+                        case 3: TC_COL(3); break;
+                        default: TC_COL(4); break;
+                    }
                 }
 #undef TC_COL
                 if (++fs == TC_JR) {

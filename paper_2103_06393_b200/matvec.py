@@ -233,6 +233,14 @@ class DeviceStore:
             raise ContractViolation("element: index out of range")
         return self.row_block([k * self.num_voxels + i1 + n1 * (i2 + n2 * i3)])[0, j]
 
+    def kernel_paths(self):
+        """{'forward': 'tcgen05' | 'cuda-core', 'adjoint': ...} for this store."""
+        f = ctypes.c_int32()
+        a = ctypes.c_int32()
+        _check(lib().tm_store_kernels(self.handle, ctypes.byref(f), ctypes.byref(a)))
+        name = {1: "tcgen05", 0: "cuda-core"}
+        return {"forward": name[f.value], "adjoint": name[a.value]}
+
     def opcounts(self, p=1):
         """Exact OpCounts of one product at p right-hand sides (matvec.cpp:10-15,50-51)."""
         dec = ctypes.c_int64()

@@ -2,7 +2,7 @@
 a C++ program written against the reference API (forward, adjoint,
 stacked_forward / stacked_adjoint over TuckerColumns, element,
 aca_forward / aca_adjoint with Tucker and dense U, row_of_compressed_u,
-load_ctc1 / load_cta1) runs on the committed golden fixtures and its outputs
+load_ctc1 / load_cta1, and the multi-GPU ShardedStore) runs on the committed golden fixtures and its outputs
 are compared with the golden arrays (the oracle's, pinned to the reference
 by tests/test_ref_pin_cpu.py) at 1e-12 (the drop-in's default is complex128).
 It also rebuilds a CompressedCoupling with different values at the same
@@ -71,6 +71,16 @@ int main(int argc, char** argv) {
     wr(o + "/yd.bin", aca_forward(dense, rd(o + "/dx.bin", 40, 2)));
     wr(o + "/zd.bin", aca_adjoint(dense, rd(o + "/dp.bin", 300, 2)));
 
+    // the columns sharded over an (emulated, one-GPU) two-shard communicator
+    {
+        b200::Communicator comm({0, 0});
+        b200::ShardedStore ss(cc, comm);
+        wr(o + "/ysh.bin", forward(ss, x));
+        wr(o + "/zsh.bin", adjoint(ss, phi));
+        b200::ShardedStore sa(fac, comm);
+        wr(o + "/yash.bin", aca_forward(sa, xa));
+    }
+
     // the same stack slot, different contents each iteration
     for (int it = 0; it < 3; ++it) {
         CompressedCoupling c2 = cc;
@@ -133,5 +143,8 @@ def test_cpp_dropin_values(product, oracle, tmp_path):
     assert rel(_r(tmp_path / "row.bin", 1, fac.rank)[0], want) <= 1e-12
     assert rel(_r(tmp_path / "yd.bin", 300, 2), du @ (dv.conj().T @ dx)) <= 1e-12
     assert rel(_r(tmp_path / "zd.bin", 40, 2), dv @ (du.conj().T @ dp)) <= 1e-12
+    assert rel(_r(tmp_path / "ysh.bin", rows, 8), ld("loop8_y.npy")) <= 1e-12
+    assert rel(_r(tmp_path / "zsh.bin", m, 8), ld("loop8_z.npy")) <= 1e-12
+    assert rel(_r(tmp_path / "yash.bin", fac.rows, 4), ld("aca8_y.npy")) <= 1e-12
     for it in range(3):
         assert rel(_r(tmp_path / f"yit{it}.bin", rows, 8), (it + 1) * ld("loop8_y.npy")) <= 1e-12

@@ -504,3 +504,33 @@ def test_device_inputs_with_lazy_conjugation(oracle, product):
     assert rel(h(ds.forward(-x)), -h(ds.forward(x))) <= 1e-15
     phi = torch.from_numpy(cn01(cc.rows, 1, 2)).cuda()
     assert rel(h(ds.adjoint(phi.conj())), h(ds.adjoint(phi.conj().resolve_conj()))) <= 1e-15
+
+
+@pytest.mark.parametrize("dims,q,m,hi,p", [
+    ((48, 40, 96), 3, 12, (20, 20, 20), 1),     # one rank-20 tensor among ranks <= 12
+    ((40, 36, 140), 2, 9, (24, 18, 24), 3),     # r2 != r3, two i3 halves
+    ((36, 33, 64), 3, 7, (8, 12, 32), 2),        # r3 = 32: a column spans three 16-K stages
+    ((64, 64, 64), 12, 6, (16, 17, 17), 5),     # just past the old rank-16 bound, quads + single adjoint
+])
+def test_ranks_above_16_stay_on_tensor_cores(oracle, product, dims, q, m, hi, p):
+    """Ranks up to 32 run on tcgen05 (the reference accepts any 1 <= r <= n,
+    src/io.cpp:131-139): one or more high-rank tensors in a ragged store."""
+    O, P = oracle, product
+    base = ragged_store(dims, q, m, 2, 12, seed=sum(dims) + p)
+    rng = np.random.default_rng(7)
+    tens = [base.tensor(j, k) for j in range(m) for k in range(q)]
+    for t in (1, (m * q) // 2, m * q - 1):  # replace three tensors by high-rank ones
+        rk = [min(hi[g], dims[g]) for g in range(3)]
+        core = rng.standard_normal(rk) + 1j * rng.standard_normal(rk)
+        us = [np.linalg.qr(rng.standard_normal((dims[g], rk[g])) + 1j * rng.standard_normal((dims[g], rk[g])))[0]
+              for g in range(3)]
+        tens[t] = (np.asfortranarray(core), *[np.asfortranarray(u) for u in us])
+    ranks, payload = O.pack_tensors(tens)
+    cc = O.Compressed(dims, q, m, ranks.reshape(m, q, 3), payload)
+    ds = P.DeviceStore.from_compressed(cc, "c64")
+    assert ds.kernel_paths() == {"forward": "tcgen05", "adjoint": "tcgen05"}
+    ref = O.OracleStore(cc.rounded_c64())
+    x = cn01(m, p, 3).astype(np.complex64).astype(np.complex128)
+    phi = cn01(cc.rows, p, 4).astype(np.complex64).astype(np.complex128)
+    assert rel(ds.forward(x), ref.forward(x)) <= 1e-5
+    assert rel(ds.adjoint(phi), ref.adjoint(phi)) <= 1e-5
