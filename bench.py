@@ -212,11 +212,57 @@ def fp32_peak_tflops(torch, tf32=False):
 
 
 # ------------------------------------------------------------- CPU reference --
-def cpu_sample(cfg, ranks, host_payload_fn, x_full, phi_full, ncols_sample, workers):
-    """Time the restated reference (oracle/, src/matvec.cpp:17-102) forward +
-    adjoint on the first `ncols_sample` columns with `workers` host threads,
-    and scale to the whole store by the algorithmic madd count."""
+def ref_store(kind, cfg, ranks, payload, v=None, tmpdir=None):
+    """The CPU store of the reference arm / cpu_baseline: the reference itself
+    (oracle/_ref: proj/src compiled unchanged, kind "reference") when it was
+    built, else the restatement (oracle/, kind "port").  ACA stores go
+    through the reference's own CTA1 loader."""
     from oracle import oracle as O
+    nc = np.asarray(ranks).shape[0]
+    if kind == "reference":
+        from oracle import ref as R
+        if v is None:
+            return R.RefCC.from_compressed(O.Compressed(cfg.grid, cfg.q, nc, ranks, payload))
+        path = os.path.join(tmpdir, "store.cta1")
+        O.save_cta1(path, O.Aca(cfg.grid, cfg.q, ranks, payload, v), 1.0, 0)
+        return R.RefAca.load_cta1(path)
+    if v is None:
+        return O.OracleStore(O.Compressed(cfg.grid, cfg.q, nc, ranks, payload))
+
+    class _PortAca:  # aca_forward / aca_adjoint of the restatement (oracle.py)
+        def __init__(self):
+            self.fac = O.Aca(cfg.grid, cfg.q, ranks, payload, v)
+
+        def aca_forward(self, x, w):
+            return O.aca_forward(self.fac, x, w)
+
+        def aca_adjoint(self, phi, w):
+            return O.aca_adjoint(self.fac, phi, w)
+    return _PortAca()
+
+
+def ref_kind():
+    try:
+        from oracle import ref as R
+        return "reference" if R.available() else "port"
+    except Exception:
+        return "port"
+
+
+def full_cpu_pair(cfg):
+    """Configs whose whole reference product pair takes seconds on the host
+    are timed in full; the large ones (c4, c5) through the bounded sample."""
+    from paper_2103_06393_b200.sharded import column_costs
+    from paper_2103_06393_b200.workloads import rank_table
+    return float(column_costs(cfg.grid, rank_table(cfg, SEED), cfg.p).sum()) < 5e10
+
+
+def cpu_sample(cfg, ranks, host_payload_fn, x_full, phi_full, ncols_sample, workers, kind="port", fixed=None):
+    """Time the reference's forward + adjoint (src/matvec.cpp:17-102) on the
+    first `ncols_sample` columns with `workers` host threads, and scale to the
+    whole store by the algorithmic madd count.  With `fixed` (the forward's
+    fixed partial-sum cost from an earlier two-point call) one round of W
+    columns is timed per call (the reference arm's timed steps)."""
     from paper_2103_06393_b200.sharded import column_costs
 
     from paper_2103_06393_b200.workloads import tensor_offsets
@@ -226,7 +272,7 @@ def cpu_sample(cfg, ranks, host_payload_fn, x_full, phi_full, ncols_sample, work
 
     def timed_forward(nc):
         off = tensor_offsets(cfg.grid, ranks[:nc])
-        st = O.OracleStore(O.Compressed(cfg.grid, cfg.q, nc, ranks[:nc], pay[: int(off[-1])]))
+        st = ref_store(kind, cfg, ranks[:nc], pay[: int(off[-1])])
         t0 = time.perf_counter()
         st.forward(np.asfortranarray(x_full[:nc]), workers)
         return time.perf_counter() - t0, st
@@ -237,17 +283,40 @@ def cpu_sample(cfg, ranks, host_payload_fn, x_full, phi_full, ncols_sample, work
     # the difference is one round of column work at full thread occupancy.
     W = workers
     n1, n2 = min(W, ncols_sample), min(2 * W, ncols_sample)
-    ta, _ = timed_forward(n1)
-    tb, st = timed_forward(n2)
-    ca, cb = costs[:n1].sum(), costs[:n2].sum()
-    rate = (cb - ca) / max(tb - ta, 1e-9) if n2 > n1 else ca / ta  # madds per second, all workers
+    ta, st = timed_forward(n1)
+    ca = costs[:n1].sum()
+    if fixed is None:
+        tb, st = timed_forward(n2)
+        cb = costs[:n2].sum()
+        rate = (cb - ca) / max(tb - ta, 1e-9) if n2 > n1 else ca / ta  # madds per second, all workers
+        fixed = max(ta - ca / rate, 0.0)
+    else:
+        cb = ca
+        rate = ca / max(ta - fixed, 1e-9)
     fwd_full = ta + (costs.sum() - ca) / rate
-    fixed = max(ta - ca / rate, 0.0)
     t1 = time.perf_counter()
     st.adjoint(phi_full, workers)
     t2 = time.perf_counter()
     scale = float(costs.sum() / cb)
     return {"fwd_s": fwd_full, "adj_s": (t2 - t1) * scale, "scale": scale, "fwd_fixed_s": fixed}
+
+
+def cpu_full(cfg, ranks, payload, v, x, phi, workers, kind, repeats=1):
+    """The whole reference product pair (forward + adjoint, or the ACA pair)
+    timed with wall clock as run_matvec_bench does (src/experiments.cpp:530-535)."""
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        st = ref_store(kind, cfg, ranks, payload, v, td)
+        tf, ta = [], []
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            st.aca_forward(x, workers) if v is not None else st.forward(x, workers)
+            t1 = time.perf_counter()
+            st.aca_adjoint(phi, workers) if v is not None else st.adjoint(phi, workers)
+            t2 = time.perf_counter()
+            tf.append(t1 - t0)
+            ta.append(t2 - t1)
+    return {"fwd_s": statistics.median(tf), "adj_s": statistics.median(ta)}
 
 
 def cpu_workers(cfg, ncols_cap):
@@ -264,46 +333,94 @@ def cpu_workers(cfg, ncols_cap):
     return max(1, min(nproc, budget, ncols_cap))
 
 
+def full_measurement(cfg):
+    """The committed full-size measurement of the reference on the GPU box's
+    host (tools/cpu_reference.py -> profiles/r02_cpu_full.jsonl), if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_cpu_full.jsonl")) as f:
+            for ln in f:
+                d = json.loads(ln)
+                if d.get("config") == cfg.name:
+                    return d
+    except (OSError, ValueError):
+        pass
+    return None
+
+
+def config_dict(cfg, world):
+    """The workload description both arms print (same dict: same_config)."""
+    from paper_2103_06393_b200.workloads import rank_table
+    gb = compressed_bytes(cfg, rank_table(cfg, SEED)) / 1e9
+    return {"workload": cfg.name, "grid": list(cfg.grid), "q": cfg.q, "m": cfg.m, "p": cfg.p,
+            "aca_m2": cfg.aca_m2 or None, "parallelism": f"column-shard x{world}",
+            "l2": "inputs larger than L2 (compressed store %.2f GB c64 + derived tensor-core operands)" % gb
+            if gb >= 0.2 else "L2 flushed between timed steps (512 MB write outside the step events; store %.3f GB)"
+            % gb}
+
+
 # --------------------------------------------------------------------- main --
 def run_reference(args):
-    """--impl reference: the reference's own CPU matvec path (restated in
-    oracle/, Eigen unavailable) on the host cores, same config / metric."""
+    """--impl reference: the reference's own CPU matvec path on the host cores
+    (oracle/_ref, proj/src compiled unchanged; the restatement oracle/ only if
+    that was not built), same config / metric as the GPU arm.  Small configs
+    run whole; config 4 / 5 run the bounded sample and extrapolate, with the
+    model's error against a committed full-size run reported beside it."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    from paper_2103_06393_b200.workloads import CONFIGS, column_scales, rank_table
-    from oracle import oracle as O
+    from paper_2103_06393_b200.workloads import CONFIGS, rank_table, synthetic_v, tensor_scales
 
     cfg = CONFIGS[args.config]
+    kind = ref_kind()
     ranks = rank_table(cfg, SEED)
-    scales = column_scales(cfg, SEED)
+    scales = tensor_scales(cfg, SEED)
     nrows = cfg.q * int(np.prod(cfg.grid))
-    W = cpu_workers(cfg, 32)
+    full = full_cpu_pair(cfg)
+    W = cpu_workers(cfg, 64 if full else 32)
     ncs = args.cpu_cols or 2 * W
-    x = cn01(cfg.m, cfg.p, SEED).astype(np.complex64).astype(np.complex128)
-    phi = np.asfortranarray(cn01(nrows, cfg.p, SEED + 1).astype(np.complex64).astype(np.complex128))
-
-    def host_payload(nc):
-        return _numpy_synthetic(cfg, ranks[:nc], scales[:nc], SEED)
-
+    rnd = (lambda a: a.astype(np.complex64).astype(np.complex128)) if cfg.dtype == "c64" else (lambda a: a)
+    x = rnd(cn01(cfg.aca_m2 or cfg.m, cfg.p, SEED))
+    phi = np.asfortranarray(rnd(cn01(nrows, cfg.p, SEED + 1)))
     times = []
-    for s in range(args.warmup + args.steps):
-        r = cpu_sample(cfg, ranks, host_payload, x, phi, ncs, W)
-        if s >= args.warmup:
-            times.append((r["fwd_s"] + r["adj_s"]) * 1e3)
+    if full:
+        pay = _numpy_synthetic(cfg, ranks, scales, SEED)
+        v = rnd(synthetic_v(cfg, SEED)) if cfg.aca_m2 else None
+        for s in range(args.warmup + args.steps):
+            r = cpu_full(cfg, ranks, pay, v, x, phi, W, kind)
+            if s >= args.warmup:
+                times.append((r["fwd_s"] + r["adj_s"]) * 1e3)
+        sample = f"the whole product pair ({cfg.m} columns x {cfg.q} components, p = {cfg.p}) with {W} worker threads"
+    else:
+        pay = _numpy_synthetic(cfg, ranks[:ncs], scales[:ncs], SEED)
+        fixed = None
+        for s in range(args.warmup + args.steps):
+            # warm-up steps calibrate the forward's fixed partial-sum cost (W and 2W
+            # columns); each timed step then runs one round of W columns
+            r = cpu_sample(cfg, ranks, lambda nc: pay, x, phi, ncs, W, kind, None if s < args.warmup else fixed)
+            if s < args.warmup:
+                fixed = r["fwd_fixed_s"] if fixed is None else min(fixed, r["fwd_fixed_s"])
+            else:
+                times.append((r["fwd_s"] + r["adj_s"]) * 1e3)
+        sample = (f"per step the forward on {W} of {cfg.m} columns (all q={cfg.q} components) with {W} workers, "
+                  f"extrapolated as the fixed partial-sum cost (calibrated on {W} and {ncs} columns in the warm-up "
+                  f"steps) + per-round rate; the adjoint on {W} columns scaled by the madd count")
     ms = statistics.median(times)
     line = {
-        "impl": "reference", "metric": metric_name(cfg), "value": ms, "unit": "ms", "n_gpus": 0,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "c128 (restated reference; c64-rounded factors)",
-        "data": "synthetic", "config": {"workload": cfg.name, "p": cfg.p, "m": cfg.m, "q": cfg.q,
-                                        "grid": list(cfg.grid)},
-        "cpu_baseline": {"value": ms, "unit": "ms", "cores": W, "kind": "port",
-                         "sample": f"forward timed on {W} and {ncs} of {cfg.m} columns (all q={cfg.q} components) "
-                                   f"with {W} workers (fixed partial-sum cost + per-round rate), adjoint on {ncs} "
-                                   f"columns scaled by the madd count"},
-        "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": metric_name(cfg), "value": round(ms, 1), "unit": "ms", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "c128 (the reference's arithmetic; c64-rounded factors)", "data": "synthetic",
+        "config": config_dict(cfg, world),
+        "cpu_baseline": {"value": round(ms, 1), "unit": "ms", "cores": W, "kind": kind, "sample": sample},
+        "e2e": {"value": round(ms, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "extrapolated": not full,
     }
+    fm = full_measurement(cfg)
+    if fm:
+        line["full_size_measurement"] = {"pair_ms": round(fm["pair_s"] * 1e3, 1), "workers": fm["workers"],
+                                         "cpu": fm.get("cpu"), "source": "profiles/r02_cpu_full.jsonl",
+                                         "sample_model_rel_error": (fm.get("sample_model") or {}).get(
+                                             "rel_error_vs_full")}
     print(json.dumps(line), flush=True)
 
 
@@ -312,8 +429,10 @@ def _numpy_synthetic(cfg, ranks, scales, seed):
     CPU legs without a GPU-generated payload)."""
     import torch
     from paper_2103_06393_b200.workloads import synthetic_payload
-    pay, _ = synthetic_payload(cfg.grid, ranks, scales, seed, device="cpu")
-    return pay.to(torch.complex64).to(torch.complex128).cpu().numpy()
+    pay, _ = synthetic_payload(cfg.grid, ranks, scales, seed + 1000, device="cpu")
+    if cfg.dtype == "c64":
+        pay = pay.to(torch.complex64).to(torch.complex128)
+    return pay.cpu().numpy()
 
 
 def cn01(rows, cols, seed):
@@ -361,12 +480,14 @@ def main():
 
     from paper_2103_06393_b200 import DeviceStore, launch_count
     from paper_2103_06393_b200.sharded import ShardedStore, balanced_shards, column_costs
-    from paper_2103_06393_b200.workloads import CONFIGS, rank_table, synthetic_payload, tensor_scales
+    from paper_2103_06393_b200.workloads import CONFIGS, rank_table, synthetic_payload, synthetic_v, tensor_scales
 
     cfg = CONFIGS[args.config]
     ranks = rank_table(cfg, SEED)
     scales = tensor_scales(cfg, SEED)
     costs = column_costs(cfg.grid, ranks, cfg.p)
+    aca = bool(cfg.aca_m2)  # ACA configs: aca_forward / aca_adjoint (src/matvec.cpp:150-175), V included
+    v_all = synthetic_v(cfg, SEED) if aca else None
     shards = balanced_shards(costs, world)
     c0, c1 = shards[rank]
     nrows = cfg.q * int(np.prod(cfg.grid))
@@ -375,36 +496,40 @@ def main():
     # --- store: seeded synthetic payload generated on the device, packed once --
     t_build = time.perf_counter()
     pay, _ = synthetic_payload(cfg.grid, ranks[c0:c1], scales[c0:c1], SEED + 1000 + c0, device=dev)
-    store = DeviceStore.from_arrays(cfg.grid, cfg.q, ranks[c0:c1], pay, cfg.dtype, local)
+    store = DeviceStore.from_arrays(cfg.grid, cfg.q, ranks[c0:c1], pay, cfg.dtype, local,
+                                    v=v_all[:, c0:c1] if aca else None)
     cpu_pay = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        W = cpu_workers(cfg, 32)
-        ncs = min(args.cpu_cols or 2 * W, c1 - c0)
-        from paper_2103_06393_b200.workloads import tensor_offsets
-        off = tensor_offsets(cfg.grid, ranks[:ncs])
-        cpu_pay = pay[: int(off[-1])].to(cdt).to(torch.complex128).cpu().numpy()
+        if full_cpu_pair(cfg):
+            cpu_pay = pay.to(cdt).to(torch.complex128).cpu().numpy()
+        else:
+            W = cpu_workers(cfg, 32)
+            ncs = min(args.cpu_cols or 2 * W, c1 - c0)
+            from paper_2103_06393_b200.workloads import tensor_offsets
+            off = tensor_offsets(cfg.grid, ranks[:ncs])
+            cpu_pay = pay[: int(off[-1])].to(cdt).to(torch.complex128).cpu().numpy()
     del pay
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t_build
     sh = ShardedStore(store, c0, c1, cfg.m, shards=shards)
 
     # --- inputs: CN(0,1), seeded (x: numpy, Phi: device RNG) ---------------------
-    x_host = cn01(cfg.m, cfg.p, SEED).astype(np.complex64 if cfg.dtype == "c64" else np.complex128)
+    x_host = cn01(cfg.aca_m2 or cfg.m, cfg.p, SEED).astype(np.complex64 if cfg.dtype == "c64" else np.complex128)
     x = torch.from_numpy(np.ascontiguousarray(x_host.T)).to(dev).t()
     g = torch.Generator(device=dev)
     g.manual_seed(SEED + 1)
     phi = (torch.randn((cfg.p, nrows), dtype=cdt, device=dev, generator=g)).t()
-    xs = x[c0:c1]
+    xs = x if aca else x[c0:c1]
 
     stream = torch.cuda.current_stream(dev)
 
     def step(ev=None):
         if ev:
             ev[0].record(stream)
-        y = sh.forward(xs)
+        y = sh.aca_forward(xs) if aca else sh.forward(xs)
         if ev:
             ev[1].record(stream)
-        z = sh.adjoint(phi)
+        z = sh.aca_adjoint(phi) if aca else sh.adjoint(phi)
         if ev:
             ev[2].record(stream)
         return y, z
@@ -430,8 +555,14 @@ def main():
     l0 = launch_count()
     t_all0 = torch.cuda.Event(enable_timing=True)
     t_all1 = torch.cuda.Event(enable_timing=True)
+    # stores smaller than L2 (126 MB): flush L2 between timed steps (a 512 MB
+    # write, outside the per-step events) so each step re-reads its operands
+    flush = compressed_bytes(cfg, ranks) < (200 << 20)
+    fbuf = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if flush else None
     t_all0.record(stream)
     for s in range(args.steps):
+        if flush:
+            fbuf.fill_(s & 0xFF)
         step(evs[s])
     t_all1.record(stream)
     torch.cuda.synchronize()
@@ -448,6 +579,11 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, fwd_med, adj_med = t.tolist()
+    if flush:  # the per-step events exclude the L2 flushes
+        tt = torch.tensor([sum(f + a for f, a in zip(fwd_ms, adj_ms))], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = tt.item()
     ms_per_step = total_ms / args.steps
 
     # --- e2e through the public API with host buffers ---------------------------
@@ -457,10 +593,12 @@ def main():
         from paper_2103_06393_b200._lib import TM_HOST, lib
         from paper_2103_06393_b200.matvec import _check
         npdt = np.complex64 if cfg.dtype == "c64" else np.complex128
-        xh = torch.from_numpy(np.asfortranarray(x_host[c0:c1]).ravel(order="F")).pin_memory()
+        xin = x_host if aca else x_host[c0:c1]
+        xh = torch.from_numpy(np.asfortranarray(xin).ravel(order="F")).pin_memory()
         yh = torch.empty(nrows * cfg.p, dtype=cdt).pin_memory()
         ph = phi.t().contiguous().cpu().pin_memory()  # every rank reads the whole Phi
-        zh = torch.empty((c1 - c0) * cfg.p, dtype=cdt).pin_memory()
+        zrows = cfg.aca_m2 if aca else c1 - c0
+        zh = torch.empty(zrows * cfg.p, dtype=cdt).pin_memory()
         e2e_times = []
         h2d = d2h = 0
         for s in range(1 + args.e2e_steps):
@@ -468,7 +606,14 @@ def main():
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            if world == 1:
+            if world == 1 and aca:
+                _check(lib().tm_aca_forward(store.handle, xh.data_ptr(), cfg.aca_m2, cfg.aca_m2, cfg.p, yh.data_ptr(),
+                                            nrows, TM_HOST, None))
+                _check(lib().tm_aca_adjoint(store.handle, ph.data_ptr(), nrows, nrows, cfg.p, zh.data_ptr(),
+                                            cfg.aca_m2, TM_HOST, None))
+                h2d = xh.numel() * xh.element_size() + ph.numel() * ph.element_size()
+                d2h = yh.numel() * yh.element_size() + zh.numel() * zh.element_size()
+            elif world == 1:
                 _check(lib().tm_forward(store.handle, xh.data_ptr(), c1 - c0, c1 - c0, cfg.p, yh.data_ptr(), nrows,
                                         TM_HOST, None, None))
                 _check(lib().tm_adjoint(store.handle, ph.data_ptr(), nrows, nrows, cfg.p, zh.data_ptr(), c1 - c0,
@@ -480,11 +625,11 @@ def main():
                 # y -> host on rank 0; host phi -> device on every rank (each
                 # over its own PCIe link), adjoint + all-gather, z -> host
                 xd = xh.to(dev, non_blocking=True).reshape(cfg.p, -1).t()
-                y = sh.forward(xd)
+                y = sh.aca_forward(xd) if aca else sh.forward(xd)
                 if rank == 0:
                     yh.copy_(y.t().reshape(-1) if y.dim() == 2 else y, non_blocking=True)
                 pd = ph.to(dev, non_blocking=True).t()
-                z = sh.adjoint(pd)
+                z = sh.aca_adjoint(pd) if aca else sh.adjoint(pd)
                 zf = torch.empty(z.numel(), dtype=cdt).pin_memory()
                 zf.copy_(z.t().reshape(-1) if z.dim() == 2 else z, non_blocking=True)
                 torch.cuda.synchronize()
@@ -505,6 +650,8 @@ def main():
     # the adjoint is Phi split + tensor-core kernel + partial reduction) ------
     dec, acc = store.opcounts(cfg.p)
     flops = 8.0 * (dec + acc)  # OpCounts x 8 real flops per complex madd (this rank's shard)
+    if aca:  # + the V side of one ACA product (V^H x or V t): m2 r_c p madds
+        flops += 8.0 * cfg.aca_m2 * (c1 - c0) * cfg.p
     tc = cfg.dtype == "c64" and os.environ.get("TMB_DISABLE_TC", "0") != "1"
     roof = None
     if rank == 0:
@@ -551,16 +698,32 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and cpu_pay is not None:
-        W = cpu_workers(cfg, 32)
-        ncs = min(args.cpu_cols or 2 * W, c1 - c0)
+        kind = ref_kind()
         phi_h = np.asfortranarray(phi.cpu().numpy().astype(np.complex128))
-        r = cpu_sample(cfg, ranks, lambda nc: cpu_pay, x_host.astype(np.complex128), phi_h, ncs, W)
-        cpu = {"value": round((r["fwd_s"] + r["adj_s"]) * 1e3, 1), "unit": "ms", "cores": W, "kind": "port",
-               "sample": f"forward timed on {W} and {ncs} of {cfg.m} columns (all {cfg.q} components) with {W} "
-                         f"worker threads, extrapolated as fixed partial-sum cost + per-round rate; adjoint on "
-                         f"{ncs} columns scaled x{r['scale']:.1f} by the madd count",
-               "fwd_fixed_ms": round(r["fwd_fixed_s"] * 1e3, 1),
-               "forward_ms": round(r["fwd_s"] * 1e3, 1), "adjoint_ms": round(r["adj_s"] * 1e3, 1)}
+        if full_cpu_pair(cfg):
+            W = cpu_workers(cfg, 64)
+            v64 = v_all.astype(np.complex64).astype(np.complex128) if aca and cfg.dtype == "c64" else v_all
+            r = cpu_full(cfg, ranks, cpu_pay, v64, x_host.astype(np.complex128), phi_h, W, kind)
+            sample = (f"the whole product pair ({cfg.m} columns x {cfg.q} components, p = {cfg.p}"
+                      + (", through aca_forward / aca_adjoint" if aca else "") + f") with {W} worker threads")
+            extra = {}
+        else:
+            W = cpu_workers(cfg, 32)
+            ncs = min(args.cpu_cols or 2 * W, c1 - c0)
+            r = cpu_sample(cfg, ranks, lambda nc: cpu_pay, x_host.astype(np.complex128), phi_h, ncs, W, kind)
+            sample = (f"forward timed on {W} and {ncs} of {cfg.m} columns (all {cfg.q} components) with {W} worker "
+                      f"threads, extrapolated as fixed partial-sum cost + per-round rate; adjoint on {ncs} columns "
+                      f"scaled x{r['scale']:.1f} by the madd count")
+            extra = {"extrapolated": True, "fwd_fixed_ms": round(r["fwd_fixed_s"] * 1e3, 1)}
+            fm = full_measurement(cfg)
+            if fm:
+                extra["full_size_measurement"] = {"pair_ms": round(fm["pair_s"] * 1e3, 1), "workers": fm["workers"],
+                                                  "source": "profiles/r02_cpu_full.jsonl",
+                                                  "sample_model_rel_error": (fm.get("sample_model") or {}).get(
+                                                      "rel_error_vs_full")}
+        cpu = {"value": round((r["fwd_s"] + r["adj_s"]) * 1e3, 1), "unit": "ms", "cores": W, "kind": kind,
+               "sample": sample, "forward_ms": round(r["fwd_s"] * 1e3, 1), "adjoint_ms": round(r["adj_s"] * 1e3, 1),
+               **extra}
 
     if rank == 0:
         line = {
@@ -568,9 +731,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
             "data": "synthetic (seeded Tucker store with the config's shape and rank distribution)",
-            "config": {"workload": cfg.name, "grid": list(cfg.grid), "q": cfg.q, "m": cfg.m, "p": cfg.p,
-                       "parallelism": f"column-shard x{world}", "l2": "inputs larger than L2 (store %.2f GB)"
-                       % (store.device_bytes * world / 1e9)},
+            "config": config_dict(cfg, world),
+            "device_store_gb": round(store.device_bytes * world / 1e9, 2),
             "forward_ms": round(fwd_med, 3), "adjoint_ms": round(adj_med, 3),
             "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "store_build_s": round(t_build, 2),
