@@ -18,8 +18,15 @@ store straight into HBM (or a CTC1 file, src/io.cpp:121-210).
   eigenvectors and the core is T x_1 U1^H x_2 U2^H x_3 U3^H.  Singular
   vectors differ from an SVD's by a phase per column, which changes no
   product (the factors only enter through U diag G U^H-type contractions).
-  The Gram route squares the condition number; with eps >= 1e-8 the kept
-  spectrum lies far above fp64's resolution of it.
+  The Gram route squares the condition number: its eigenvalues resolve
+  squared singular values only to ~1e-16 lambda_max, and the subspace path's
+  discarded energy (trace - kept eigenvalues) to the ulp of the trace.  That
+  is ample for eps >= 1e-6 (budget eps^2/3 |T|^2 >= 3e-13 |T|^2); below it
+  (the reference experiments' default eps 1e-8, include/tuckmat/
+  experiments.hpp:48) the budget would sit at rounding level, so the
+  singular values and vectors come from a batched SVD of the unfolding
+  itself and the discarded energy is summed from the smallest singular
+  values up, exactly as the reference does (src/tensor.cpp:155-163).
 
 The result is the reference's CompressedCoupling layout: ranks (m, q, 3) and
 the concatenated CTC1 tensor payloads, on the device.
@@ -143,6 +150,20 @@ def _ranked_eigh(gram, budget, kmax=32, iters=2):
     return vecs, ranks
 
 
+def _ranked_svd(a, budget):
+    """Truncation rank and left singular vectors of a batch of unfoldings a
+    (B, n, N) from their thin SVD: the reference's rule summed directly from
+    the smallest squared singular values (src/tensor.cpp:155-163).  Returns
+    (vecs, ranks) in _ranked_eigh's convention (ascending order: the last r
+    columns are the leading singular vectors)."""
+    torch = _torch()
+    u, sv, _ = torch.linalg.svd(a, full_matrices=False)  # sv descending
+    k = sv.shape[-1]
+    small = torch.cumsum((sv * sv).flip(-1), dim=-1)  # energy of the t smallest
+    keep_small = (small <= budget[:, None]).sum(-1)
+    return list(u.flip(-1).unbind(0)), torch.clamp(k - keep_small, min=1)
+
+
 def hosvd_batch(t, eps):
     """Truncated HOSVD of a batch of tensors t (B, n3, n2, n1) complex128
     (f1-fastest): list of (core (r1, r2, r3) f1-fastest as a torch tensor of
@@ -158,6 +179,9 @@ def hosvd_batch(t, eps):
     facs = []
     for mode in (1, 2, 3):
         a = _unfold(t, mode)
+        if eps < 1e-6:  # budget near rounding level of the Gram route: SVD of the unfolding
+            facs.append(_ranked_svd(a, budget))
+            continue
         gram = a @ a.conj().transpose(1, 2)
         facs.append(_ranked_eigh(gram, budget))
     out = []
