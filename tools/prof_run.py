@@ -20,13 +20,12 @@ def main():
     args = ap.parse_args()
     import torch
     from paper_2103_06393_b200 import DeviceStore
-    from paper_2103_06393_b200.workloads import CONFIGS, column_scales, rank_table, synthetic_payload
+    from paper_2103_06393_b200.workloads import CONFIGS, bench_store_arrays
     if args.cc:
         os.environ["TMB_DISABLE_TC"] = "1"
     cfg = CONFIGS[args.config]
     m = args.cols or cfg.m
-    ranks = rank_table(cfg, 1234)[:m]
-    pay, _ = synthetic_payload(cfg.grid, ranks, column_scales(cfg, 1234)[:m], 2234, device="cuda")
+    ranks, pay = bench_store_arrays(cfg, 1234, 0, m)  # bench.py's store (its first m columns)
     s = DeviceStore.from_arrays(cfg.grid, cfg.q, ranks, pay, cfg.dtype, 0)
     del pay
     rows = cfg.q * int(np.prod(cfg.grid))

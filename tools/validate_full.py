@@ -33,12 +33,10 @@ def main():
     args = ap.parse_args()
     import torch
     from paper_2103_06393_b200 import DeviceStore
-    from paper_2103_06393_b200.workloads import CONFIGS, column_scales, rank_table, synthetic_payload, tensor_offsets
+    from paper_2103_06393_b200.workloads import CONFIGS, bench_store_arrays, tensor_offsets
 
     cfg = CONFIGS[args.config]
-    ranks = rank_table(cfg, 1234)
-    scales = column_scales(cfg, 1234)
-    pay, _ = synthetic_payload(cfg.grid, ranks, scales, 1234 + 1000, device="cuda")
+    ranks, pay = bench_store_arrays(cfg, 1234)  # exactly bench.py's store
     pay64 = pay.to(torch.complex64).to(torch.complex128)  # the c64 store's values, exactly
     s64 = DeviceStore.from_arrays(cfg.grid, cfg.q, ranks, pay, "c64", 0)
     s128 = DeviceStore.from_arrays(cfg.grid, cfg.q, ranks, pay64, "c128", 0)
