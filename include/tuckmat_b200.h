@@ -125,6 +125,14 @@ TM_API int tm_store_kernels(const tm_store* s, int32_t* forward_tc, int32_t* adj
 TM_API int tm_forward(tm_store* s, const void* x, int64_t ldx, int64_t xrows, int64_t p, void* y, int64_t ldy,
                       int where, void* stream, int64_t* ops);
 
+/* The forward restricted to components [k0, k1): rows k n_v .. (k+1) n_v - 1 of
+ * y for k in the range are written, the other rows untouched; device
+ * pointers, enqueued on `stream`.  Lets a one-process-per-GPU driver reduce
+ * component k of the partial y while component k + 1 computes
+ * (sharded.py). */
+TM_API int tm_forward_components(tm_store* s, const void* x, int64_t ldx, int64_t xrows, int64_t p, void* y,
+                                 int64_t ldy, int32_t k0, int32_t k1, void* stream);
+
 /* Z = Zbc^H Phi — adjoint(cc, phi, workers, ops) (src/matvec.cpp:140-148)
  * and stacked_adjoint (src/matvec.cpp:67-102).  phi: q*n_v x p, z: ncols x p. */
 TM_API int tm_adjoint(tm_store* s, const void* phi, int64_t ldphi, int64_t phirows, int64_t p, void* z,

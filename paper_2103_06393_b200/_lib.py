@@ -23,7 +23,7 @@ TM_HOST, TM_DEVICE = 0, 1
 
 EXPORTED = [
     "tm_store_create", "tm_store_create_dense_aca", "tm_store_load_ctc1", "tm_store_load_cta1", "tm_store_destroy", "tm_store_info", "tm_store_kernels",
-    "tm_forward", "tm_adjoint", "tm_aca_forward", "tm_aca_adjoint", "tm_opcounts", "tm_rows", "tm_last_error",
+    "tm_forward", "tm_forward_components", "tm_adjoint", "tm_aca_forward", "tm_aca_adjoint", "tm_opcounts", "tm_rows", "tm_last_error",
     "tm_assemble_columns",
     "tm_comm_init", "tm_comm_finalize", "tm_comm_info", "tm_sharded_create", "tm_sharded_destroy", "tm_sharded_info",
     "tm_sharded_forward", "tm_sharded_adjoint", "tm_sharded_aca_forward", "tm_sharded_aca_adjoint",
@@ -71,6 +71,8 @@ def lib():
                 L.tm_store_kernels.argtypes = [vp, vp, vp]
             L.tm_forward.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp, vp]
             L.tm_adjoint.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp, vp]
+            if hasattr(L, "tm_forward_components"):
+                L.tm_forward_components.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, i32, vp]
             L.tm_aca_forward.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp]
             L.tm_aca_adjoint.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp]
             L.tm_opcounts.argtypes = [vp, i64, vp, vp]

@@ -654,8 +654,11 @@ struct CcPlan {
 };
 
 template <typename C, int RM, int CN, int NW, int TI1>
-void run_forward_cc(tm_store* s, const C* x, int64_t ldx, int64_t p, C* y, int64_t ldy, cudaStream_t st) {
+void run_forward_cc(tm_store* s, const C* x, int64_t ldx, int64_t p, C* y, int64_t ldy, cudaStream_t st, int kb,
+                    int ke) {
     CcPlan<C, RM, CN, NW, TI1> plan(s, false);
+    plan.g.k0 = kb;
+    plan.grid.y = unsigned(ke - kb);
     int dev = 0;
     CK(cudaGetDevice(&dev));
     plan.split_for(p, num_sms(dev));
@@ -674,7 +677,8 @@ void run_forward_cc(tm_store* s, const C* x, int64_t ldx, int64_t p, C* y, int64
                                                    ldx, yp, rows);
             launched(cudaSuccess, "fwd_cc_kernel");
             const unsigned rb = unsigned(std::min<int64_t>((rows * pc + 255) / 256, 4096));
-            cc_split_reduce_kernel<C><<<rb, 256, 0, st>>>(yp, g.nsplit, g.part_stride, rows, pc, y + ldy * c0, ldy);
+            cc_split_reduce_kernel<C><<<rb, 256, 0, st>>>(yp, g.nsplit, g.part_stride, rows, pc, y + ldy * c0, ldy,
+                                                          int64_t(kb) * s->nv(), int64_t(ke - kb) * s->nv());
             launched(cudaSuccess, "cc_split_reduce_kernel");
         } else {
             kern<<<grid, NW * 32, plan.smem, st>>>(s->d_desc, static_cast<const C*>(s->d_arena), plan.g, x + ldx * c0,
@@ -751,7 +755,7 @@ struct HostPipe {
 // tiles span the N space n = i3 * pb + c, so W is produced once for all
 // right-hand sides of the pass.
 void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy,
-                      cudaStream_t st, const HostPipe* hp, int64_t hc0) {
+                      cudaStream_t st, const HostPipe* hp, int64_t hc0, int kb, int ke) {
     TcGeom g{};
     g.ncols = s->ncols;
     g.n1 = int(s->dims[0]);
@@ -831,9 +835,9 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
         CK(cudaMemsetAsync(xb, 0, ms->xbplanes.bytes, st));
         ms->xb_zeroed = ms->xbplanes.bytes;
     }
-    build_xb_kernel<<<unsigned(s->ncols * s->q), 256, 0, st>>>(s->d_desc, static_cast<const float2*>(s->d_arena),
-                                                              s->d_kofs, x, ldx, int(p), s->ncols, s->q, g.n3,
-                                                              int64_t(g.nt), s->kpad, wmax, s->d_tcd, xb);
+    build_xb_kernel<<<unsigned(s->ncols * (ke - kb)), 256, 0, st>>>(
+        s->d_desc, static_cast<const float2*>(s->d_arena), s->d_kofs, x, ldx, int(p), s->ncols, s->q, g.n3,
+        int64_t(g.nt), s->kpad, wmax, s->d_tcd, xb, int64_t(kb) * s->ncols);
     launched(cudaSuccess, "build_xb_kernel");
     const CUtensorMap bmap = make_tmap_3d_f16(xb, uint64_t(s->kpad), uint64_t(g.nt), uint64_t(TC_FPLANES * s->q),
                                               uint64_t(s->kpad) * 2, uint64_t(g.nt) * s->kpad * 2, 16,
@@ -846,10 +850,11 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
     // config-4 forward, measured).
     const int64_t tpb = g.ntiles / g.q;  // tiles per component (all right-hand sides of the pass)
     const int64_t nv = s->nv();
-    int64_t bdone = 0;
+    int64_t bdone = kb;
     const int span = g.nmma * g.nh3;
-    for (int64_t t0 = 0; t0 < g.ntiles; t0 += wave) {
-        const int64_t tiles = std::min<int64_t>(g.ntiles - t0, wave);
+    const int64_t tend = int64_t(ke) * tpb;  // components [kb, ke): tiles [kb tpb, ke tpb)
+    for (int64_t t0 = int64_t(kb) * tpb; t0 < tend; t0 += wave) {
+        const int64_t tiles = std::min<int64_t>(tend - t0, wave);
         // A final partial wave splits each tile's columns into parts (partial tiles
         // to ypart, summed by fwd_split_reduce_kernel) so the launch fills the GPU.
         g.split = best_split(tiles, wave, int(std::min<int64_t>(8, std::max<int64_t>(1, s->ncols))));
@@ -924,21 +929,23 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
 // The tensor-core forward: passes of up to pbmax right-hand sides (the B
 // operand of a pass is 4 q n3 kpad fp16 per right-hand side).
 void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy,
-                    cudaStream_t st, const HostPipe* hp = nullptr) {
+                    cudaStream_t st, const HostPipe* hp = nullptr, int kb = 0, int ke = -1) {
+    if (ke < 0) ke = s->q;
     const size_t per_rhs = size_t(TC_FPLANES) * s->q * size_t(s->dims[2]) * s->kpad * sizeof(__half);
     size_t cap = size_t(4) << 30;  // B-operand budget per pass (TMB_XB_CAP_MB overrides, e.g. for tests)
     if (const char* e = std::getenv("TMB_XB_CAP_MB")) if (std::atoll(e) > 0) cap = size_t(std::atoll(e)) << 20;
     const int64_t pbmax = std::max<int64_t>(1, std::min<int64_t>(p, int64_t(cap / per_rhs)));
     for (int64_t c0 = 0; c0 < p; c0 += pbmax) {
         const int64_t pb = std::min<int64_t>(pbmax, p - c0);
-        run_forward_pass(s, x + ldx * c0, ldx, pb, y + ldy * c0, ldy, st, hp, c0);
+        run_forward_pass(s, x + ldx * c0, ldx, pb, y + ldy * c0, ldy, st, hp, c0, kb, ke);
     }
 }
 
 void forward_dev(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy, cudaStream_t st,
-                 const HostPipe* hook = nullptr) {
+                 const HostPipe* hook = nullptr, int kb = 0, int ke = -1) {
+    if (ke < 0) ke = s->q;
     if (s->tc_ok && !tc_disabled()) {
-        run_forward_tc(s, static_cast<const float2*>(x), ldx, p, static_cast<float2*>(y), ldy, st, hook);
+        run_forward_tc(s, static_cast<const float2*>(x), ldx, p, static_cast<float2*>(y), ldy, st, hook, kb, ke);
         return;
     }
     struct AtEnd {  // the CUDA-core kernels finish every component at once
@@ -947,22 +954,23 @@ void forward_dev(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, in
         int64_t p;
         cudaStream_t st;
         ~AtEnd() noexcept(false) {
-            if (h && h->block_done && std::uncaught_exceptions() == 0) h->block_done(0, s->q, 0, p, st);
+            if (h && h->block_done && std::uncaught_exceptions() == 0) h->block_done(kb, ke, 0, p, st);
         }
-    } at_end{hook, s, p, st};
+        int kb, ke;
+    } at_end{hook, s, p, st, kb, ke};
     const int cn = pick_cn(s->dims[2]);
     if (s->dtype == TM_C64) {
         auto X = static_cast<const float2*>(x);
         auto Y = static_cast<float2*>(y);
-        if (cn == 4) run_forward_cc<float2, 8, 4, 8, 8>(s, X, ldx, p, Y, ldy, st);
-        else if (cn == 2) run_forward_cc<float2, 8, 2, 8, 8>(s, X, ldx, p, Y, ldy, st);
-        else run_forward_cc<float2, 8, 1, 8, 8>(s, X, ldx, p, Y, ldy, st);
+        if (cn == 4) run_forward_cc<float2, 8, 4, 8, 8>(s, X, ldx, p, Y, ldy, st, kb, ke);
+        else if (cn == 2) run_forward_cc<float2, 8, 2, 8, 8>(s, X, ldx, p, Y, ldy, st, kb, ke);
+        else run_forward_cc<float2, 8, 1, 8, 8>(s, X, ldx, p, Y, ldy, st, kb, ke);
     } else {
         auto X = static_cast<const double2*>(x);
         auto Y = static_cast<double2*>(y);
-        if (cn == 4) run_forward_cc<double2, 4, 4, 8, 8>(s, X, ldx, p, Y, ldy, st);
-        else if (cn == 2) run_forward_cc<double2, 4, 2, 8, 8>(s, X, ldx, p, Y, ldy, st);
-        else run_forward_cc<double2, 4, 1, 8, 8>(s, X, ldx, p, Y, ldy, st);
+        if (cn == 4) run_forward_cc<double2, 4, 4, 8, 8>(s, X, ldx, p, Y, ldy, st, kb, ke);
+        else if (cn == 2) run_forward_cc<double2, 4, 2, 8, 8>(s, X, ldx, p, Y, ldy, st, kb, ke);
+        else run_forward_cc<double2, 4, 1, 8, 8>(s, X, ldx, p, Y, ldy, st, kb, ke);
     }
 }
 
@@ -1719,6 +1727,26 @@ TM_API int tm_forward(tm_store* s, const void* x, int64_t ldx, int64_t xrows, in
         if (ops) {
             ops[0] += s->dec_madds;
             ops[1] += s->ncols * s->q * s->nv() * p;
+        }
+    });
+}
+
+TM_API int tm_forward_components(tm_store* s, const void* x, int64_t ldx, int64_t xrows, int64_t p, void* y,
+                                 int64_t ldy, int32_t k0, int32_t k1, void* stream) {
+    return guarded([&] {
+        if (!s) contract("null store");
+        reject_dense(s, "forward");
+        if (xrows != s->ncols)
+            contract("forward: x has " + std::to_string(xrows) + " rows, expected m = " + std::to_string(s->ncols));
+        if (k0 < 0 || k1 > s->q || k0 > k1) contract("tm_forward_components: component range out of range");
+        check_common(s, p, ldx, xrows, ldy, s->rows(), TM_DEVICE, x, y);
+        std::lock_guard<std::mutex> lock(s->mu);
+        DeviceGuard guard(s->device);
+        if (p > 0 && k1 > k0) {
+            cudaStream_t st = static_cast<cudaStream_t>(stream);
+            order_after_prev(s, st);
+            forward_dev(s, x, ldx, p, y, ldy, st, nullptr, k0, k1);
+            mark_done(s, st);
         }
     });
 }

@@ -39,6 +39,7 @@ struct CcGeom {
     int ntiles;       // nt1 * nt2 * nt3: blockIdx.x = tile + ntiles * part
     int nsplit;       // column ranges per tile (> 1 when tiles x q x p < the SMs)
     int64_t part_stride;  // forward with nsplit > 1: elements between the parts' partial y blocks
+    int k0;               // forward: first component (blockIdx.y = k - k0; tm_forward_components)
 };
 
 // Column range [ja, jz) of split part `part` (contiguous, balanced by count).
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(NW * 32)
     const int t1 = tile % g.nt1;
     const int t2 = (tile / g.nt1) % g.nt2;
     const int t3 = tile / (g.nt1 * g.nt2);
-    const int k = blockIdx.y;
+    const int k = g.k0 + int(blockIdx.y);
     const int c = blockIdx.z;
     const int i1_0 = t1 * TI1, i2_0 = t2 * TI2, i3_0 = t3 * TI3;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -307,13 +308,16 @@ __global__ void __launch_bounds__(NW * 32)
 // in part order (deterministic).
 template <typename C>
 __global__ void cc_split_reduce_kernel(const C* __restrict__ yp, int nsplit, int64_t stride, int64_t rows, int64_t p,
-                                       C* __restrict__ y, int64_t ldy) {
-    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * p;
+                                       C* __restrict__ y, int64_t ldy, int64_t r0 = 0, int64_t nr = -1) {
+    // rows [r0, r0 + nr) of each column (all rows when nr < 0)
+    if (nr < 0) nr = rows;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nr * p;
          e += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t c = e / rows, r = e - c * rows;
-        C acc = yp[e];
+        const int64_t c = e / nr, r = r0 + (e - c * nr);
+        const int64_t ei = r + rows * c;
+        C acc = yp[ei];
         for (int sp = 1; sp < nsplit; ++sp) {
-            const C v = yp[sp * stride + e];
+            const C v = yp[sp * stride + ei];
             acc.x += v.x;
             acc.y += v.y;
         }

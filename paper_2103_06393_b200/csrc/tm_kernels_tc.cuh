@@ -804,8 +804,8 @@ __global__ void xmax_kernel(const float2* __restrict__ x, int64_t ldx, int64_t n
 __global__ void build_xb_kernel(const TDesc* __restrict__ td, const float2* __restrict__ arena,
                                 const int* __restrict__ kofs, const float2* __restrict__ x, int64_t ldx, int p,
                                 int64_t ncols, int q, int n3, int64_t nt, int64_t kpad, const float* __restrict__ xmax,
-                                const TcDesc* __restrict__ tcd, __half* __restrict__ planes) {
-    const int64_t t = blockIdx.x;  // tensor index k*ncols + j
+                                const TcDesc* __restrict__ tcd, __half* __restrict__ planes, int64_t t0 = 0) {
+    const int64_t t = t0 + blockIdx.x;  // tensor index k*ncols + j (t0: first tensor of a component range)
     const int k = int(t / ncols);
     const int64_t j = t - int64_t(k) * ncols;
     const TDesc d = td[t];

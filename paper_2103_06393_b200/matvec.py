@@ -323,6 +323,29 @@ class DeviceStore:
             ops["accumulate_madds"] = ops.get("accumulate_madds", 0) + int(o[1])
         return out[:, 0] if squeeze else out
 
+    def forward_components(self, x, k0, k1, out, stream=None):
+        """Device forward restricted to components [k0, k1): rows k n_v ..
+        (k + 1) n_v - 1 of `out` (column-major, rows x p) for k in the range;
+        the other rows are untouched (tm_forward_components)."""
+        import torch
+        td = _torch_dtype(self.dtype)
+        if x.device.type != "cuda" or x.device.index != self.device:
+            raise ContractViolation(f"input is on {x.device}, store is on cuda:{self.device}")
+        x = x.reshape(-1, 1) if x.dim() == 1 else x
+        x = x.to(td).resolve_conj().resolve_neg()
+        if x.stride(0) != 1 or (x.shape[1] > 1 and x.stride(1) < x.shape[0]):
+            x = x.t().contiguous().t()
+        o2 = out.reshape(-1, 1) if out.dim() == 1 else out
+        inrows, p = x.shape
+        if (tuple(o2.shape) != (self.rows, p) or out.dtype != td or out.device != x.device or o2.stride(0) != 1
+                or (p > 1 and o2.stride(1) < self.rows)):
+            raise ContractViolation(f"out must be a column-major {td} tensor of shape ({self.rows}, {p}) on {x.device}")
+        st = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
+        _check(lib().tm_forward_components(self.handle, x.data_ptr(), x.stride(1) if p > 1 else max(inrows, 1),
+                                           inrows, p, o2.data_ptr(), o2.stride(1) if p > 1 else self.rows, int(k0),
+                                           int(k1), st))
+        return out
+
     def forward(self, x, ops=None):
         """Y = Zbc X (forward, src/matvec.cpp:132-138)."""
         return self._call(lib().tm_forward, x, self.rows, ops, True)

@@ -78,14 +78,40 @@ class ShardedStore:
     def rows(self):
         return self.store.rows
 
-    def forward(self, x, dst=0, allreduce=False):
+    def forward(self, x, dst=0, allreduce=False, groups=4):
         """y = Zbc x.  x: (ncols x p) on this rank's device (the full block or
         just this shard's rows).  Returns the full y on `dst` (or every rank
-        with allreduce=True); other ranks get their partial."""
+        with allreduce=True); other ranks get their partial.
+
+        With N > 1 and a device store the forward runs in `groups` component
+        groups (tm_forward_components) and each group's rows of the partial y
+        are reduced asynchronously as soon as the group is done, so the
+        reduce of group g overlaps the computation of group g + 1 (only the
+        last group's reduce is exposed)."""
+        xs = x[self.c0:self.c1] if x.shape[0] == self.ncols else x
+        if self.world == 1 or not hasattr(self.store, "forward_components") or groups <= 1:
+            return self._sum(self.store.forward(xs), dst, allreduce)
+        import torch
         import torch.distributed as dist
 
-        xs = x[self.c0:self.c1] if x.shape[0] == self.ncols else x
-        return self._sum(self.store.forward(xs), dst, allreduce)
+        squeeze = xs.dim() == 1
+        x2 = xs.reshape(-1, 1) if squeeze else xs
+        q, nv, p = self.store.q, self.store.num_voxels, x2.shape[1]
+        dt = torch.complex64 if self.store.np_dtype == np.complex64 else torch.complex128
+        y = torch.empty((p, q * nv), dtype=dt, device=x2.device).t()
+        bounds = [round(q * g / groups) for g in range(groups + 1)]
+        handles = []
+        for k0, k1 in zip(bounds, bounds[1:]):
+            if k1 <= k0:
+                continue
+            self.store.forward_components(x2, k0, k1, y)
+            for c in range(p):  # rows [k0 nv, k1 nv) of column c: contiguous
+                seg = y.t()[c, k0 * nv:k1 * nv]
+                handles.append(dist.all_reduce(seg, group=self.group, async_op=True) if allreduce else
+                               dist.reduce(seg, dst=dst, group=self.group, async_op=True))
+        for h in handles:
+            h.wait()
+        return y[:, 0] if squeeze else y
 
     def _sum(self, y, dst=0, allreduce=False):
         import torch.distributed as dist
