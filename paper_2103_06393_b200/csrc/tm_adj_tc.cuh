@@ -1,4 +1,4 @@
-// Tensor-core (tcgen05, kind::tf32, 3xTF32 split) adjoint kernel, complex64.
+// Tensor-core (tcgen05, kind::f16, 2-term fp16 split) adjoint kernel, complex64.
 //
 // The reference's stacked_adjoint (src/matvec.cpp:67-102) forms, per column
 // j and component k, z_j += vec(T_jk)^H Phi_k.  With T_jk[row, i3] =

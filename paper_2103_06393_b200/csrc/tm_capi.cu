@@ -143,7 +143,7 @@ struct tm_store {
     bool dense = false;
     void* d_u = nullptr;
     int64_t device_bytes = 0;
-    // tensor-core (tcgen05 3xTF32) forward data: B planes of U3, K offsets
+    // tensor-core (tcgen05 fp16-split) forward data: V / U2 operand copies, K offsets
     bool tc_ok = false;
     int* d_kofs = nullptr;   // [q*ncols] component-major K offset of each tensor
     int* d_kc = nullptr;     // [q] K extent of each component
@@ -225,7 +225,7 @@ void order_after_prev(tm_store* s, cudaStream_t st) { CK(cudaStreamWaitEvent(st,
 void mark_done(tm_store* s, cudaStream_t st) { CK(cudaEventRecord(s->done, st)); }
 
 // ------------------------------------------------------------ store build --
-// c64 stores run the forward on the tcgen05 3xTF32 kernel (chained TMEM
+// c64 stores run the forward on the tcgen05 fp16-split kernel (chained TMEM
 // accumulation, tm_kernels_tc.cuh) whenever the store qualifies;
 // TMB_DISABLE_TC=1 forces the CUDA-core kernel (used by the tests to check
 // one against the other).

@@ -114,3 +114,20 @@ def test_device_out_validation(product):
                 torch.empty((cc.rows, 2), dtype=torch.complex64)):                     # host tensor
         with pytest.raises(P.ContractViolation):
             ds.forward_into(x, bad)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_empty_store_and_empty_blocks(oracle, product, dtype):
+    """A store with no columns (the reference's stacked_forward with
+    ncols = 0 returns zeros, src/matvec.cpp:28-38), and p = 0 blocks."""
+    O, P = oracle, product
+    cc = O.Compressed((6, 5, 17), 3, 0, np.zeros((0, 3, 3), np.int32), np.zeros(0, np.complex128))
+    ds = P.DeviceStore.from_compressed(cc, dtype)
+    y = ds.forward(np.zeros((0, 2)))
+    assert y.shape == (ds.rows, 2) and not np.any(y)
+    z = ds.adjoint(np.ones((ds.rows, 2)))
+    assert z.shape == (0, 2)
+    full = ragged_store((6, 5, 17), 3, 4, 1, 4, seed=2)
+    d2 = P.DeviceStore.from_compressed(full, dtype)
+    assert d2.forward(np.zeros((4, 0))).shape == (d2.rows, 0)
+    assert d2.adjoint(np.zeros((d2.rows, 0))).shape == (4, 0)

@@ -223,7 +223,7 @@ def test_aca_products(oracle, product, dtype):
     ((9, 70, 20), 2, 40, 1, 13, 3),      # many short chains, ragged ranks from 1
 ])
 def test_tensor_core_forward(oracle, product, monkeypatch, dims, q, m, rmin, rmax, p):
-    """tcgen05 3xTF32 forward and adjoint (c64, the default c64 path) vs the
+    """tcgen05 fp16-split forward and adjoint (c64, the default c64 path) vs the
     oracle and vs the CUDA-core kernels (TMB_DISABLE_TC=1)."""
     O, P = oracle, product
     cc = ragged_store(dims, q, m, rmin, rmax, seed=7 * m + q)
