@@ -254,7 +254,7 @@ def full_cpu_pair(cfg):
     are timed in full; the large ones (c4, c5) through the bounded sample."""
     from paper_2103_06393_b200.sharded import column_costs
     from paper_2103_06393_b200.workloads import rank_table
-    return float(column_costs(cfg.grid, rank_table(cfg, SEED), cfg.p).sum()) < 5e10
+    return float(column_costs(cfg.grid, rank_table(cfg, SEED), cfg.p).sum()) < 2e11
 
 
 def cpu_sample(cfg, ranks, host_payload_fn, x_full, phi_full, ncols_sample, workers, kind="port", fixed=None):
