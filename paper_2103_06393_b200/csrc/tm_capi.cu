@@ -237,9 +237,12 @@ bool tc_disabled() {
 int tc_chain() {
     const char* e = std::getenv("TMB_TC_CHAIN");
     const int v = e ? std::atoi(e) : 0;
-    // 24 stages x 6 truncating MMAs per accumulator: 2.9e-6 at config 4
-    // (8: 1.2e-6, 16: 2.0e-6, 32: 3.9e-6, 48: 5.8e-6 — tools/validate_full.py)
-    return v > 0 ? v : 24;
+    // 32 stages x 6 truncating MMAs per accumulator: 3.7e-6 at config 4 (the
+    // physics-rank store; 24: 2.8e-6, 48: 5.4e-6 — tools/validate_full.py
+    // --chains, profiles/r02i_tune.jsonl); each fold moves the 256 KB
+    // accumulator through red.global.add, so longer chains cost less (24 -> 32:
+    // -3.5 % forward time per SM clock, same box)
+    return v > 0 ? v : 32;
 }
 
 // B planes of the tensor-core forward (see tm_kernels_tc.cuh), built once.

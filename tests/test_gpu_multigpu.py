@@ -85,12 +85,18 @@ def test_forward_components(oracle, product):
         y = torch.full((2, ds.rows), 7.0 + 0j, dtype=td, device="cuda").t()
         ds.forward_components(x, 3, 8, y)
         torch.cuda.synchronize()
-        assert torch.equal(y[3 * nv:8 * nv], full[3 * nv:8 * nv])
+        # (the waves of a component range split their final partial wave
+        # differently, so the c64 partial sums may round differently)
+        tol = 1e-6 if dtype == "c64" else 1e-14
+
+        def trel(a, b):
+            return float(torch.linalg.vector_norm((a - b).reshape(-1)) / torch.linalg.vector_norm(b.reshape(-1)))
+        assert trel(y[3 * nv:8 * nv], full[3 * nv:8 * nv]) <= tol
         assert bool((y[:3 * nv] == 7.0).all()) and bool((y[8 * nv:] == 7.0).all())
         for k0, k1 in ((0, 4), (4, 9), (9, 12)):
             ds.forward_components(x, k0, k1, y)
         torch.cuda.synchronize()
-        assert torch.equal(y, full)
+        assert trel(y, full) <= tol
 
 
 def _overlap_worker(rank, world, port, path, out):
