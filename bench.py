@@ -283,17 +283,18 @@ def cpu_sample(cfg, ranks, host_payload_fn, x_full, phi_full, ncols_sample, work
     # the difference is one round of column work at full thread occupancy.
     W = workers
     n1, n2 = min(W, ncols_sample), min(2 * W, ncols_sample)
-    ta, st = timed_forward(n1)
-    ca = costs[:n1].sum()
     if fixed is None:
+        ta, _ = timed_forward(n1)
+        ca = costs[:n1].sum()
         tb, st = timed_forward(n2)
         cb = costs[:n2].sum()
         rate = (cb - ca) / max(tb - ta, 1e-9) if n2 > n1 else ca / ta  # madds per second, all workers
         fixed = max(ta - ca / rate, 0.0)
-    else:
-        cb = ca
-        rate = ca / max(ta - fixed, 1e-9)
-    fwd_full = ta + (costs.sum() - ca) / rate
+    else:  # two rounds of W columns against the calibrated fixed cost
+        tb, st = timed_forward(n2)
+        cb = costs[:n2].sum()
+        rate = cb / max(tb - fixed, 1e-9)
+    fwd_full = fixed + costs.sum() / rate
     t1 = time.perf_counter()
     st.adjoint(phi_full, workers)
     t2 = time.perf_counter()
@@ -392,18 +393,20 @@ def run_reference(args):
         sample = f"the whole product pair ({cfg.m} columns x {cfg.q} components, p = {cfg.p}) with {W} worker threads"
     else:
         pay = _numpy_synthetic(cfg, ranks[:ncs], scales[:ncs], SEED)
-        fixed = None
+        fixed, fixes = None, []
         for s in range(args.warmup + args.steps):
             # warm-up steps calibrate the forward's fixed partial-sum cost (W and 2W
             # columns); each timed step then runs one round of W columns
             r = cpu_sample(cfg, ranks, lambda nc: pay, x, phi, ncs, W, kind, None if s < args.warmup else fixed)
             if s < args.warmup:
-                fixed = r["fwd_fixed_s"] if fixed is None else min(fixed, r["fwd_fixed_s"])
+                fixes.append(r["fwd_fixed_s"])
+                fixed = statistics.median(fixes)
             else:
                 times.append((r["fwd_s"] + r["adj_s"]) * 1e3)
-        sample = (f"per step the forward on {W} of {cfg.m} columns (all q={cfg.q} components) with {W} workers, "
-                  f"extrapolated as the fixed partial-sum cost (calibrated on {W} and {ncs} columns in the warm-up "
-                  f"steps) + per-round rate; the adjoint on {W} columns scaled by the madd count")
+        sample = (f"per step the forward on {ncs} of {cfg.m} columns (all q={cfg.q} components, two rounds of {W} "
+                  f"worker threads), extrapolated as the fixed partial-sum cost (median of the warm-up steps' "
+                  f"two-point fits on {W} and {ncs} columns) + the per-round rate; the adjoint on {ncs} columns "
+                  f"scaled by the madd count")
     ms = statistics.median(times)
     line = {
         "impl": "reference", "metric": metric_name(cfg), "value": round(ms, 1), "unit": "ms", "n_gpus": 0,
