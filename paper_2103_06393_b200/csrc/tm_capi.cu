@@ -25,7 +25,6 @@
 #include "tm_kernels_tc.cuh"
 #include "tm_adj_tc.cuh"
 #include "tm_adj2_tc.cuh"
-#include "tm_k3_tc.cuh"
 #include "tm_tmap.h"
 #include "tm_io_internal.hpp"
 
@@ -945,86 +944,9 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     }
 }
 
-// The K3 forward (tm_k3_tc.cuh: T decompressed once per tile on CUDA cores,
-// Y += T X on tcgen05) for many right-hand sides: p >= TMB_K3_PMIN (default
-// 16), ranks r3 <= 16; TMB_K3=0 disables it.
-bool k3_ok(const tm_store* s, int64_t p) {
-    if (!s->tc_ok || tc_disabled() || s->rmax[2] > 16) return false;
-    {  // at least a 3-slot factor ring next to the A / B stages
-        const int u2 = TC_SLOT_V + int(round16(uint32_t(TC_TI1 * s->rmax[1] * s->rmax[2] * 8)));
-        const size_t slot = size_t((u2 + TC_TI2 * (s->rmax[1] | 1) * 8 + K3_NI3 * s->rmax[2] * 8 + 127) / 128 * 128);
-        if (1024 + size_t(K3_NST) * (K3_A_STAGE + K3_B_STAGE) + 3 * slot + 512 > kSmemMax) return false;
-    }
-    if (const char* e = std::getenv("TMB_K3")) if (*e == '0') return false;
-    int64_t pmin = 16;
-    if (const char* e = std::getenv("TMB_K3_PMIN")) if (std::atoll(e) > 0) pmin = std::atoll(e);
-    return p >= pmin;
-}
-
-void run_forward_k3(tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy, cudaStream_t st) {
-    K3Geom g{};
-    g.ncols = s->ncols;
-    g.n1 = int(s->dims[0]);
-    g.n2 = int(s->dims[1]);
-    g.n3 = int(s->dims[2]);
-    g.q = s->q;
-    g.nt1 = (g.n1 + TC_TI1 - 1) / TC_TI1;
-    g.nt2 = (g.n2 + TC_TI2 - 1) / TC_TI2;
-    g.nt3 = (g.n3 + K3_NI3 - 1) / K3_NI3;
-    g.ntiles = int64_t(g.q) * g.nt1 * g.nt2 * g.nt3;
-    g.rmax2 = s->rmax[1];
-    g.rmax3 = s->rmax[2];
-    g.u2_off = TC_SLOT_V + int(round16(uint32_t(TC_TI1 * g.rmax2 * g.rmax3 * 8)));
-    g.u3_off = g.u2_off + TC_TI2 * (g.rmax2 | 1) * 8;
-    g.slot_bytes = (g.u3_off + K3_NI3 * g.rmax3 * 8 + 127) / 128 * 128;
-    g.nks = int((s->ncols + 15) / 16);
-    g.chain = tc_chain();
-    // |T| <= r3 max|W| (normalised factors: |U3| <= 1): the fp16 scale of T
-    g.sa = fp16_scale(float(g.rmax3) * s->vmax * 1.0001f);
-    auto smem_for = [&](int jr) {
-        return 1024 + size_t(K3_NST) * (K3_A_STAGE + K3_B_STAGE) + size_t(jr) * g.slot_bytes +
-               (2 * K3_NST + 2 * K3_JR_MAX + 2) * 8 + 16;
-    };
-    g.jr = K3_JR_MAX;
-    if (const char* e = std::getenv("TMB_K3_JR")) if (std::atoi(e) >= 2) g.jr = std::min(K3_JR_MAX, std::atoi(e));
-    while (g.jr > 2 && smem_for(g.jr) > kSmemMax) --g.jr;
-    const size_t smem = smem_for(g.jr);
-    if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "K3 forward: shared-memory plan too large");
-    CK(cudaFuncSetAttribute(fwd_k3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    const unsigned grid = unsigned(std::min<int64_t>(g.ntiles, num_sms(dev)));
-    float* rsum = static_cast<float*>(s->rsum.get(size_t(grid) * K3_YCOLS * TC_ROWS * sizeof(float)));
-    const int64_t kpad = (s->ncols + 15) / 16 * 16;
-    __half* planes = static_cast<__half*>(s->xbplanes.get(size_t(4) * 2 * K3_P * kpad * sizeof(__half)));
-    float* xmax = static_cast<float*>(s->scal.get(2 * sizeof(float))) + 1;
-    for (int64_t c0 = 0; c0 < p; c0 += K3_P) {
-        const int pb = int(std::min<int64_t>(K3_P, p - c0));
-        CK(cudaMemsetAsync(xmax, 0, sizeof(float), st));
-        xmax_kernel<<<unsigned(std::min<int64_t>((s->ncols * pb + 255) / 256, 1184)), 256, 0, st>>>(
-            x + ldx * c0, ldx, s->ncols, pb, xmax);
-        launched(cudaSuccess, "xmax_kernel");
-        k3_xplanes_kernel<<<unsigned(std::min<int64_t>((K3_P * kpad + 255) / 256, 4096)), 256, 0, st>>>(
-            x + ldx * c0, ldx, s->ncols, pb, kpad, xmax, planes);
-        launched(cudaSuccess, "k3_xplanes_kernel");
-        const CUtensorMap xmap = make_tmap_3d_f16(planes, uint64_t(kpad), uint64_t(2 * K3_P), 4, uint64_t(kpad) * 2,
-                                                  uint64_t(2 * K3_P) * kpad * 2, 16, 2 * K3_P,
-                                                  CU_TENSOR_MAP_SWIZZLE_32B);
-        g.p = pb;
-        fwd_k3_kernel<<<grid, K3_THREADS, smem, st>>>(xmap, s->d_tcd, s->d_varena, s->d_u2arena,
-                                                      static_cast<const float2*>(s->d_arena), g, y + ldy * c0, ldy,
-                                                      rsum, xmax);
-        launched(cudaSuccess, "fwd_k3_kernel");
-    }
-}
-
 void forward_dev(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy, cudaStream_t st,
                  const HostPipe* hook = nullptr, int kb = 0, int ke = -1) {
     if (ke < 0) ke = s->q;
-    if (!hook && kb == 0 && ke == s->q && k3_ok(s, p)) {
-        run_forward_k3(s, static_cast<const float2*>(x), ldx, p, static_cast<float2*>(y), ldy, st);
-        return;
-    }
     if (s->tc_ok && !tc_disabled()) {
         run_forward_tc(s, static_cast<const float2*>(x), ldx, p, static_cast<float2*>(y), ldy, st, hook, kb, ke);
         return;
@@ -1515,7 +1437,7 @@ void with_host_io(tm_store* s, const void* in, int64_t ldin, int64_t inrows, int
 // kernels block by block (HostPipe).  Returns false when the product does
 // not take the tensor-core path (the caller then uses with_host_io).
 bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy) {
-    if (!(s->tc_ok && !tc_disabled()) || k3_ok(s, p)) return false;
+    if (!(s->tc_ok && !tc_disabled())) return false;
     const size_t cs = s->csize();
     void* din = s->xin.get(size_t(std::max<int64_t>(s->ncols * p, 1)) * cs);
     void* dout = s->yout.get(size_t(std::max<int64_t>(s->rows() * p, 1)) * cs);

@@ -534,30 +534,3 @@ def test_ranks_above_16_stay_on_tensor_cores(oracle, product, dims, q, m, hi, p)
     phi = cn01(cc.rows, p, 4).astype(np.complex64).astype(np.complex128)
     assert rel(ds.forward(x), ref.forward(x)) <= 1e-5
     assert rel(ds.adjoint(phi), ref.adjoint(phi)) <= 1e-5
-
-
-@pytest.mark.parametrize("dims,q,m,rmin,rmax,p", [
-    ((64, 64, 64), 12, 40, 4, 9, 32),     # config-5 shape, one 32-RHS pass
-    ((21, 40, 37), 3, 19, 1, 13, 16),     # ragged, n1 / n2 / n3 not multiples of the tile, m not of 16
-    ((9, 33, 70), 2, 35, 3, 16, 40),      # rank-16 factors, two passes (32 + 8)
-    ((16, 32, 8), 1, 100, 2, 5, 20),      # many columns: several accumulation chains per tile
-])
-def test_k3_forward(oracle, product, monkeypatch, dims, q, m, rmin, rmax, p):
-    """The K3 batched forward (T decompressed once per tile on CUDA cores,
-    Y += T X on tcgen05; the default for p >= 16) vs the oracle and vs the
-    x-in-B forward (TMB_K3=0)."""
-    O, P = oracle, product
-    cc = ragged_store(dims, q, m, rmin, rmax, seed=7 * m + p)
-    ref = O.OracleStore(cc.rounded_c64())
-    ds = P.DeviceStore.from_compressed(cc, "c64")
-    x = cn01(m, p, 17).astype(np.complex64).astype(np.complex128)
-    monkeypatch.setenv("TMB_TC_CHAIN", "3")  # short chains: exercise the fold
-    y3 = ds.forward(x)
-    monkeypatch.delenv("TMB_TC_CHAIN")
-    y3b = ds.forward(x)
-    monkeypatch.setenv("TMB_K3", "0")
-    yb = ds.forward(x)
-    monkeypatch.delenv("TMB_K3")
-    yo = ref.forward(x)
-    assert rel(y3, yo) <= 1e-5 and rel(y3b, yo) <= 1e-5 and rel(yb, yo) <= 1e-5
-    assert rel(ds.forward(x[:, :1]), yo[:, :1]) <= 1e-5  # p = 1 stays on the x-in-B forward
