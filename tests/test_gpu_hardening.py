@@ -131,3 +131,25 @@ def test_empty_store_and_empty_blocks(oracle, product, dtype):
     d2 = P.DeviceStore.from_compressed(full, dtype)
     assert d2.forward(np.zeros((4, 0))).shape == (d2.rows, 0)
     assert d2.adjoint(np.zeros((d2.rows, 0))).shape == (4, 0)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_many_columns(oracle, product, dtype):
+    """70 000 columns (more than a 16-bit grid dimension, long K streams and
+    many adjoint chunks) on a small grid: forward / adjoint vs the oracle."""
+    O, P = oracle, product
+    rng = np.random.default_rng(0)
+    m, q, dims = 70000, 1, (4, 4, 16)
+    ranks = rng.integers(1, 3, size=(m, q, 3)).astype(np.int32)
+    from paper_2103_06393_b200.workloads import synthetic_payload
+    pay, _ = synthetic_payload(dims, ranks, np.exp(-rng.random(m) * 3), 5, device="cpu")
+    cc = O.Compressed(dims, q, m, ranks, pay.numpy())
+    ds = P.DeviceStore.from_compressed(cc, dtype)
+    ref = O.OracleStore(cc.rounded_c64() if dtype == "c64" else cc)
+    x = cn01(m, 2, 1)
+    phi = cn01(cc.rows, 2, 2)
+    if dtype == "c64":
+        x, phi = _c64(x), _c64(phi)
+    tol = 1e-5 if dtype == "c64" else 1e-12
+    assert rel(ds.forward(x), ref.forward(x, 8)) <= tol
+    assert rel(ds.adjoint(phi), ref.adjoint(phi, 8)) <= tol
