@@ -112,6 +112,8 @@ __device__ __forceinline__ void cc_stage_chunk(const TDesc* __restrict__ td, con
             C acc = zero;
             const C* gp = G + int64_t(bc) * d.r1;
             const C* up = s.u1 + i1l * d.r1;
+            // independent core loads in flight (L2 latency, not FMA, bounds this loop)
+#pragma unroll 4
             for (int a = 0; a < d.r1; ++a) cfma(acc, up[a], __ldg(reinterpret_cast<const C*>(gp + a)));
             s.v[e] = acc;
         }
@@ -129,6 +131,7 @@ __device__ __forceinline__ void cc_stage_chunk(const TDesc* __restrict__ td, con
             C acc = zero;
             const C* vp = s.v + i1l * r23 + d.r2 * c;
             const C* up = s.u2 + i2l * d.r2;
+#pragma unroll 4
             for (int b = 0; b < d.r2; ++b) cfma(acc, vp[b], up[b]);
             s.w[e] = cmul(acc, sj);
         }
