@@ -45,6 +45,53 @@ def balanced_shards(costs, world, align=1):
     return [(bounds[i], bounds[i + 1]) for i in range(world)]
 
 
+def row_pieces(comp_costs, n1, world, align=8, min_rows=8):
+    """Row (voxel-slab) sharding, the alternative of SURVEY §8e: the q * n1
+    (component, i1) slabs of the output are cut into `world` contiguous
+    ranges of near-equal cost (a slab of component k costs comp_costs[k] / n1:
+    every stage of the product is linear in the i1 rows).  Cuts inside a
+    component fall on multiples of `align` rows and leave at least
+    `min_rows` rows on both sides (a piece is a Tucker store on the sub-grid
+    i1 in [a, b), so it needs b - a >= r1 of its tensors); otherwise they
+    move to the nearer component boundary.  Returns, per shard, a list of
+    pieces (k, a, b) — component k, i1 rows [a, b)."""
+    cc = np.asarray(comp_costs, np.float64)
+    q = len(cc)
+    n1 = int(n1)
+    step = max(int(align), 1)
+    lo = max(int(min_rows), step)
+    pref = np.concatenate([[0.0], np.cumsum(cc)])
+    cuts = [0]
+    for s in range(1, world):
+        target = pref[-1] * s / world
+        k = int(np.clip(np.searchsorted(pref, target, side="right") - 1, 0, q - 1))
+        frac = (target - pref[k]) / cc[k] if cc[k] > 0 else 0.0
+        loc = int(round(frac * n1 / step)) * step
+        if loc < lo or n1 - loc < lo:
+            loc = 0 if frac < 0.5 else n1
+        cuts.append(max(cuts[-1], min(k * n1 + loc, q * n1)))
+    cuts.append(q * n1)
+    out = []
+    for s in range(world):
+        r0, r1 = cuts[s], cuts[s + 1]
+        pcs = []
+        while r0 < r1:
+            k = r0 // n1
+            e = min(r1, (k + 1) * n1)
+            pcs.append((k, r0 - k * n1, e - k * n1))
+            r0 = e
+        out.append(pcs)
+    return out
+
+
+def component_costs(dims, ranks, p=1):
+    """Per-component madds of one product: sum_j reconstruct_madds + m n_v p."""
+    r = np.asarray(ranks, np.int64)
+    n1, n2, n3 = (int(d) for d in dims)
+    dec = n1 * r[..., 0] * r[..., 1] * r[..., 2] + n1 * n2 * r[..., 1] * r[..., 2] + n1 * n2 * n3 * r[..., 2]
+    return dec.sum(axis=0) + r.shape[0] * n1 * n2 * n3 * p
+
+
 def column_costs(dims, ranks, p=1):
     """Per-column madds of one product: sum_k reconstruct_madds + q n_v p."""
     r = np.asarray(ranks, np.int64)
