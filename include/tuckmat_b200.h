@@ -190,6 +190,19 @@ TM_API int tm_opcounts(const tm_store* s, int64_t p, int64_t* decompress_madds, 
 typedef struct tm_comm tm_comm;
 typedef struct tm_sharded tm_sharded;
 
+/* Partition modes of a sharded store.  TM_SHARD_COLUMNS: as above.
+ * TM_SHARD_ROWS: row (voxel-slab) sharding, the alternative of SURVEY §8e —
+ * the q * n1 (component, i1) slabs of the output are cut into one contiguous
+ * cost-balanced range per GPU (cuts inside a component on multiples of 8 i1
+ * rows, at least max r1 rows per piece); each (component k, i1 rows [a, b))
+ * piece is a one-component store on the sub-grid (b - a) x n2 x n3 with all
+ * columns (U1 rows sliced: the same operator restricted to those voxels).
+ * The forward has no reduction (each GPU copies its rows of y into the
+ * output, peer to peer for a device output); the adjoint reads only its
+ * GPU's rows of Phi and reduces the m x p partial z (ACA: m2 x p).  Every
+ * GPU holds ~1/N of the store and of Phi. */
+typedef enum { TM_SHARD_COLUMNS = 0, TM_SHARD_ROWS = 1 } tm_shard_mode;
+
 TM_API int tm_comm_init(int ndev, const int* devices, tm_comm** out);
 TM_API int tm_comm_finalize(tm_comm* comm);
 TM_API int tm_comm_info(const tm_comm* comm, int32_t* ndev, int32_t* emulated);
@@ -197,8 +210,17 @@ TM_API int tm_comm_info(const tm_comm* comm, int32_t* ndev, int32_t* emulated);
 /* desc as for tm_store_create, host payload / V only; shard d lives on
  * devices[d].  ranges (optional, 2 * nshards) receives each shard's [c0, c1). */
 TM_API int tm_sharded_create(const tm_store_desc* desc, tm_comm* comm, int dtype, tm_sharded** out);
+TM_API int tm_sharded_create_mode(const tm_store_desc* desc, tm_comm* comm, int dtype, int mode, tm_sharded** out);
 TM_API int tm_sharded_destroy(tm_sharded* s);
+/* ranges: columns mode [c0, c1) per shard; rows mode the shard's slab range
+ * [r0, r1) of global slab indices k * n1 + i1. */
 TM_API int tm_sharded_info(const tm_sharded* s, int32_t* nshards, int64_t* ranges, int64_t* device_bytes);
+/* Rows mode: the pieces (4 int64 each: shard index, k, a, b), in shard order. */
+TM_API int tm_sharded_pieces(const tm_sharded* s, int32_t* npieces, int64_t* pieces);
+/* The row partition rule on its own (host only, no device needed): ndev + 1
+ * cut points over [0, q * n1) from per-component costs. */
+TM_API int tm_shard_row_cuts(int32_t q, int64_t n1, int32_t ndev, int64_t align, int64_t min_rows,
+                             const double* comp_costs, int64_t* cuts);
 
 /* As tm_forward / tm_adjoint / tm_aca_*; with TM_DEVICE the inputs and
  * outputs live on devices[0] and the work is ordered after / before

@@ -238,8 +238,9 @@ MultiVector adjoint(const DeviceStore& s, const MultiVector& phi, OpCounts* ops 
 MultiVector aca_forward(const DeviceStore& s, const MultiVector& x);
 MultiVector aca_adjoint(const DeviceStore& s, const MultiVector& phi);
 
-// Multi-GPU: the columns sharded over the GPUs of one box (tm_comm_* /
-// tm_sharded_*, tuckmat_b200.h); products take and return host blocks.
+// Multi-GPU: the store sharded over the GPUs of one box (tm_comm_* /
+// tm_sharded_*, tuckmat_b200.h) by columns (TM_SHARD_COLUMNS) or by row
+// slabs (TM_SHARD_ROWS); products take and return host blocks.
 class Communicator {
 public:
     explicit Communicator(const std::vector<int>& devices);
@@ -254,8 +255,9 @@ private:
 
 class ShardedStore {
 public:
-    ShardedStore(const CompressedCoupling& cc, Communicator& comm, int dtype = TM_C128);
-    ShardedStore(const AcaFactors& fac, Communicator& comm, int dtype = TM_C128);
+    ShardedStore(const CompressedCoupling& cc, Communicator& comm, int dtype = TM_C128,
+                 int mode = TM_SHARD_COLUMNS);
+    ShardedStore(const AcaFactors& fac, Communicator& comm, int dtype = TM_C128, int mode = TM_SHARD_COLUMNS);
     ~ShardedStore();
     ShardedStore(const ShardedStore&) = delete;
     ShardedStore& operator=(const ShardedStore&) = delete;

@@ -20,6 +20,7 @@ TM_OK, TM_CONTRACT_VIOLATION, TM_CAPACITY_ERROR, TM_PARSE_ERROR, TM_CUDA_ERROR, 
 TM_SINGULARITY_ERROR = 4
 TM_C64, TM_C128 = 0, 1
 TM_HOST, TM_DEVICE = 0, 1
+TM_SHARD_COLUMNS, TM_SHARD_ROWS = 0, 1
 
 EXPORTED = [
     "tm_store_create", "tm_store_create_dense_aca", "tm_store_load_ctc1", "tm_store_load_cta1", "tm_store_destroy", "tm_store_info", "tm_store_kernels",
@@ -27,6 +28,7 @@ EXPORTED = [
     "tm_assemble_columns",
     "tm_comm_init", "tm_comm_finalize", "tm_comm_info", "tm_sharded_create", "tm_sharded_destroy", "tm_sharded_info",
     "tm_sharded_forward", "tm_sharded_adjoint", "tm_sharded_aca_forward", "tm_sharded_aca_adjoint",
+    "tm_sharded_create_mode", "tm_sharded_pieces", "tm_shard_row_cuts",
     "tm_launch_count", "tm_version",
 ]
 
@@ -90,6 +92,9 @@ def lib():
                 L.tm_sharded_adjoint.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp, vp]
                 L.tm_sharded_aca_forward.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp]
                 L.tm_sharded_aca_adjoint.argtypes = [vp, vp, i64, i64, i64, vp, i64, i32, vp]
+                L.tm_sharded_create_mode.argtypes = [ctypes.POINTER(StoreDesc), vp, i32, i32, ctypes.POINTER(vp)]
+                L.tm_sharded_pieces.argtypes = [vp, vp, vp]
+                L.tm_shard_row_cuts.argtypes = [i32, i64, i32, i64, i64, vp, vp]
             L.tm_last_error.restype = ctypes.c_char_p
             L.tm_launch_count.restype = ctypes.c_int64
             _lib = L

@@ -564,25 +564,25 @@ Communicator::~Communicator() {
     if (h_) tm_comm_finalize(h_);
 }
 
-ShardedStore::ShardedStore(const CompressedCoupling& cc, Communicator& comm, int dtype) : dtype_(dtype) {
+ShardedStore::ShardedStore(const CompressedCoupling& cc, Communicator& comm, int dtype, int mode) : dtype_(dtype) {
     with_desc(
         cc.q, cc.m, cc.grid_dims,
         [&](Index j, int k) -> const TuckerTensor& {
             return cc.columns[static_cast<std::size_t>(j)][static_cast<std::size_t>(k)];
         },
-        nullptr, [&](const tm_store_desc& d) { check(tm_sharded_create(&d, comm.handle(), dtype, &h_)); });
+        nullptr, [&](const tm_store_desc& d) { check(tm_sharded_create_mode(&d, comm.handle(), dtype, mode, &h_)); });
     rows_ = cc.rows();
     cols_ = cc.m;
 }
 
-ShardedStore::ShardedStore(const AcaFactors& f, Communicator& comm, int dtype) : dtype_(dtype) {
+ShardedStore::ShardedStore(const AcaFactors& f, Communicator& comm, int dtype, int mode) : dtype_(dtype) {
     if (!f.compressed()) throw ContractViolation("ShardedStore: AcaFactors needs a Tucker-compressed U");
     with_desc(
         f.q, f.rank(), f.grid_dims,
         [&](Index l, int k) -> const TuckerTensor& {
             return f.tucker_u[static_cast<std::size_t>(k)][static_cast<std::size_t>(l)];
         },
-        &f.v, [&](const tm_store_desc& d) { check(tm_sharded_create(&d, comm.handle(), dtype, &h_)); });
+        &f.v, [&](const tm_store_desc& d) { check(tm_sharded_create_mode(&d, comm.handle(), dtype, mode, &h_)); });
     rows_ = f.rows();
     cols_ = f.rank();
     m2_ = f.cols();

@@ -16,6 +16,16 @@
 // forward reduces the partial y as above, the adjoint reduces the m2 x p
 // partial V t.
 //
+// Row (voxel-slab) sharding, the alternative of SURVEY §8e (TM_SHARD_ROWS):
+// the q * n1 (component, i1) slabs of the output are cut into one
+// contiguous, cost-balanced range per GPU; a GPU holds each (component k,
+// i1 rows [a, b)) piece of its range as a regular one-component store on the
+// sub-grid (b - a) x n2 x n3 with all m columns (U1 rows sliced — the same
+// operator restricted to those voxels).  The forward needs no reduction:
+// each piece writes its rows of y (a strided copy from the piece's
+// sub-grid layout, peer-to-peer for a device y on the root); the adjoint
+// reads only its rows of Phi and reduces the m x p partial z (a few KB).
+//
 // A communicator whose device list repeats a device is EMULATED: the
 // collectives become device-local copies and adds on the root's stream.
 // That lets the sharded orchestration (column split, per-shard stores,
@@ -40,12 +50,22 @@ struct tm_comm {
 };
 
 struct tm_sharded {
-    tm_comm* comm = nullptr;
+    tm_comm* comm = nullptr;  // products use its NCCL communicators
+    std::vector<int> devices;  // own copy: destroying the store never touches the communicator
+    int mode = TM_SHARD_COLUMNS;
     int dtype = TM_C64;
     int q = 0;
     int64_t ncols = 0, dims[3] = {0, 0, 0}, m2 = 0;
-    std::vector<int64_t> c0, c1;
-    std::vector<tm_store*> shards;
+    std::vector<int64_t> c0, c1;  // columns: shard d's columns; rows: its (k n1 + i1) slab range
+    std::vector<tm_store*> shards;  // columns mode: one store per device
+    struct Piece {                   // rows mode: component k, i1 rows [a, b) on device index d
+        size_t d = 0;
+        int k = 0;
+        int64_t a = 0, b = 0;
+        tm_store* st = nullptr;
+        DevBuf ybuf, pbuf, tbuf;  // piece output y, gathered Phi, partial adjoint
+    };
+    std::vector<Piece> pieces;
     std::vector<cudaStream_t> cst, mst;  // per shard: compute and communication streams
     std::vector<cudaEvent_t> done;       // per shard: end of the latest sharded product
     std::vector<DevBuf> xbuf, ybuf, zbuf;
@@ -54,25 +74,34 @@ struct tm_sharded {
     int64_t nv() const { return dims[0] * dims[1] * dims[2]; }
     int64_t rows() const { return q * nv(); }
     size_t csize() const { return dtype == TM_C64 ? sizeof(float2) : sizeof(double2); }
-    int dev(size_t d) const { return comm->devices[d]; }
+    int dev(size_t d) const { return devices[d]; }
+    size_t ndev() const { return devices.size(); }
+    const tm_store* any_store() const { return mode == TM_SHARD_ROWS ? pieces.front().st : shards.front(); }
     ~tm_sharded() {
-        for (size_t d = 0; d < shards.size(); ++d) {
-            cudaSetDevice(dev(d));
-            if (done.size() > d && done[d]) {
+        for (size_t d = 0; d < done.size(); ++d)
+            if (done[d]) {
+                cudaSetDevice(dev(d));
                 cudaEventSynchronize(done[d]);
-                cudaEventDestroy(done[d]);
             }
-            if (cst.size() > d && cst[d]) cudaStreamDestroy(cst[d]);
-            if (mst.size() > d && mst[d]) cudaStreamDestroy(mst[d]);
-            xbuf[d].release();
-            ybuf[d].release();
-            zbuf[d].release();
-            if (shards[d]) delete shards[d];
+        for (Piece& pc : pieces) {
+            cudaSetDevice(dev(pc.d));
+            if (pc.st) delete pc.st;
+            pc.ybuf.release();
+            pc.pbuf.release();
+            pc.tbuf.release();
         }
-        if (!shards.empty()) {
-            cudaSetDevice(dev(0));
-            zgather.release();
+        for (size_t d = 0; d < ndev(); ++d) {
+            cudaSetDevice(dev(d));
+            if (d < done.size() && done[d]) cudaEventDestroy(done[d]);
+            if (d < cst.size() && cst[d]) cudaStreamDestroy(cst[d]);
+            if (d < mst.size() && mst[d]) cudaStreamDestroy(mst[d]);
+            if (d < xbuf.size()) xbuf[d].release();
+            if (d < ybuf.size()) ybuf[d].release();
+            if (d < zbuf.size()) zbuf[d].release();
+            if (d < shards.size() && shards[d]) delete shards[d];
         }
+        cudaSetDevice(dev(0));
+        zgather.release();
     }
 };
 
@@ -192,7 +221,7 @@ struct RedUnit {
 // communication streams.
 void reduce_units(tm_sharded* S, std::vector<RedUnit>& units, const std::vector<void*>& out,
                   const std::vector<int64_t>& ld) {
-    const size_t nd = S->shards.size();
+    const size_t nd = S->ndev();
     const size_t cs = S->csize();
     for (RedUnit& u : units) {
         if (S->comm->emulated || nd == 1) {
@@ -443,6 +472,294 @@ void sharded_adjoint(tm_sharded* S, const void* phi, int64_t ldphi, int64_t p, v
     }
 }
 
+// ------------------------------------------------------------ row sharding --
+
+// Cut points (global slab index k n1 + i1) of the row partition: `nd`
+// contiguous ranges of near-equal cost (a slab of component k costs
+// cc[k] / n1); cuts inside a component on multiples of `align` rows leaving
+// >= min_rows rows on both sides, else at the nearer component boundary.
+// Bit-for-bit the same rule as sharded.py:row_pieces (tests compare them).
+std::vector<int64_t> row_cuts(const std::vector<double>& cc, int64_t n1, int nd, int64_t align, int64_t min_rows) {
+    const int q = int(cc.size());
+    const int64_t step = std::max<int64_t>(align, 1), lo = std::max<int64_t>(min_rows, step);
+    std::vector<double> pre(size_t(q) + 1, 0.0);
+    for (int k = 0; k < q; ++k) pre[size_t(k) + 1] = pre[size_t(k)] + cc[size_t(k)];
+    std::vector<int64_t> cuts{0};
+    for (int s = 1; s < nd; ++s) {
+        const double target = pre[size_t(q)] * s / nd;
+        int k = int(std::upper_bound(pre.begin(), pre.end(), target) - pre.begin()) - 1;
+        k = std::min(std::max(k, 0), q - 1);
+        const double frac = cc[size_t(k)] > 0 ? (target - pre[size_t(k)]) / cc[size_t(k)] : 0.0;
+        int64_t loc = int64_t(std::nearbyint(frac * double(n1) / double(step))) * step;  // round half to even
+        if (loc < lo || n1 - loc < lo) loc = frac < 0.5 ? 0 : n1;
+        cuts.push_back(std::max(cuts.back(), std::min<int64_t>(int64_t(k) * n1 + loc, int64_t(q) * n1)));
+    }
+    cuts.push_back(int64_t(q) * n1);
+    return cuts;
+}
+
+// Per-component madds of one product (reconstruct_madds, src/matvec.cpp:10-15,
+// plus the accumulate term at p = 1), exact in int64.
+std::vector<double> component_costs(const tm_store_desc& d) {
+    const int64_t n1 = d.dims[0], n2 = d.dims[1], n3 = d.dims[2];
+    std::vector<double> cc(size_t(d.q), 0.0);
+    for (int k = 0; k < d.q; ++k) {
+        int64_t c = 0;
+        for (int64_t j = 0; j < d.ncols; ++j) {
+            const int32_t* r = d.ranks + 3 * (j * d.q + k);
+            c += n1 * r[0] * r[1] * r[2] + n1 * n2 * r[1] * r[2] + n1 * n2 * n3 * r[2] + n1 * n2 * n3;
+        }
+        cc[size_t(k)] = double(c);
+    }
+    return cc;
+}
+
+// The piece (component k, i1 rows [a, b)) of a host store as a one-component
+// store on the sub-grid (b - a) x n2 x n3: every column's tensor (j, k) with
+// U1 restricted to rows [a, b) (col-major n1 x r1 -> (b - a) x r1).
+tm_store* create_piece_store(const tm_store_desc& d, const std::vector<int64_t>& toff, int k, int64_t a, int64_t b,
+                             int device, int dtype) {
+    const int64_t n1 = d.dims[0], n2 = d.dims[1], n3 = d.dims[2], m = d.ncols, h = b - a;
+    std::vector<int32_t> rk(size_t(3 * std::max<int64_t>(m, 1)));
+    int64_t total = 0;
+    for (int64_t j = 0; j < m; ++j) {
+        const int32_t* r = d.ranks + 3 * (j * d.q + k);
+        if (r[0] > h)
+            contract("row sharding: a piece of " + std::to_string(h) + " i1 rows is below tucker rank r1 = " +
+                     std::to_string(r[0]));
+        for (int g = 0; g < 3; ++g) rk[size_t(3 * j + g)] = r[g];
+        total += int64_t(r[0]) * r[1] * r[2] + h * r[0] + n2 * r[1] + n3 * r[2];
+    }
+    std::vector<double> pay(size_t(2 * std::max<int64_t>(total, 1)));
+    double* o = pay.data();
+    for (int64_t j = 0; j < m; ++j) {
+        const int32_t* r = d.ranks + 3 * (j * d.q + k);
+        const double* src = d.payload + 2 * toff[size_t(j * d.q + k)];
+        const int64_t core = int64_t(r[0]) * r[1] * r[2];
+        std::memcpy(o, src, size_t(2 * core) * sizeof(double));
+        o += 2 * core;
+        for (int c = 0; c < r[0]; ++c) {
+            std::memcpy(o, src + 2 * (core + c * n1 + a), size_t(2 * h) * sizeof(double));
+            o += 2 * h;
+        }
+        const int64_t rest = n2 * r[1] + n3 * r[2];
+        std::memcpy(o, src + 2 * (core + n1 * r[0]), size_t(2 * rest) * sizeof(double));
+        o += 2 * rest;
+    }
+    tm_store_desc sd = d;
+    sd.q = 1;
+    sd.dims[0] = h;
+    sd.ranks = rk.data();
+    sd.payload = pay.data();
+    return create_store(sd, device, dtype);
+}
+
+void build_row_pieces(tm_sharded* S, const tm_store_desc& d, int dtype) {
+    const int nd = int(S->ndev());
+    const int64_t n1 = d.dims[0];
+    int32_t r1max = 1;
+    for (int64_t i = 0; i < d.ncols * d.q; ++i) r1max = std::max(r1max, d.ranks[3 * i]);
+    const int64_t align = 2 * 4;  // the CTA-pair tile height of the tensor-core kernels (i1 rows)
+    const std::vector<int64_t> cuts =
+        row_cuts(component_costs(d), n1, nd, align, (int64_t(r1max) + align - 1) / align * align);
+    std::vector<int64_t> toff(size_t(d.ncols * d.q) + 1, 0);
+    for (int64_t i = 0; i < d.ncols * d.q; ++i) {
+        const int32_t* r = d.ranks + 3 * i;
+        toff[size_t(i) + 1] = toff[size_t(i)] + int64_t(r[0]) * r[1] * r[2] + d.dims[0] * r[0] +
+                              d.dims[1] * r[1] + d.dims[2] * r[2];
+    }
+    S->pieces.reserve(size_t(d.q + nd));
+    for (int s = 0; s < nd; ++s) {
+        S->c0.push_back(cuts[size_t(s)]);
+        S->c1.push_back(cuts[size_t(s) + 1]);
+        for (int64_t r0 = cuts[size_t(s)]; r0 < cuts[size_t(s) + 1];) {
+            const int k = int(r0 / n1);
+            const int64_t e = std::min(cuts[size_t(s) + 1], int64_t(k + 1) * n1);
+            S->pieces.emplace_back();
+            tm_sharded::Piece& pc = S->pieces.back();
+            pc.d = size_t(s);
+            pc.k = k;
+            pc.a = r0 - int64_t(k) * n1;
+            pc.b = e - int64_t(k) * n1;
+            pc.st = create_piece_store(d, toff, k, pc.a, pc.b, S->dev(size_t(s)), dtype);
+            r0 = e;
+        }
+    }
+}
+
+// rows [a, b) of component k, right-hand side c: out (n1-pitched, full grid)
+// <-> piece (h-pitched, sub-grid); n2 n3 rows of h elements.
+void slab_copy(const tm_sharded* S, void* dst, size_t dpitch, const void* src, size_t spitch, int64_t h,
+               cudaMemcpyKind kind, cudaStream_t st) {
+    const size_t cs = S->csize();
+    CK(cudaMemcpy2DAsync(dst, dpitch * cs, src, spitch * cs, size_t(h) * cs, size_t(S->dims[1] * S->dims[2]), kind,
+                         st));
+}
+
+// Forward (aca: aca_forward) over the row pieces: every device reads the
+// whole input, each piece computes its rows of y on the sub-grid and copies
+// them into y (host, or device memory on the root — peer to peer).
+void rows_forward(tm_sharded* S, const void* x, int64_t ldx, int64_t xrows, int64_t p, void* y, int64_t ldy,
+                  bool host, cudaStream_t caller, bool aca) {
+    const size_t nd = S->ndev(), cs = S->csize();
+    cudaEvent_t in_ready = nullptr;
+    if (!host) {
+        DeviceGuard g(S->dev(0));
+        CK(cudaEventCreateWithFlags(&in_ready, cudaEventDisableTiming));
+        CK(cudaEventRecord(in_ready, caller));
+    }
+    std::vector<void*> xd(nd, nullptr);
+    for (size_t d = 0; d < nd; ++d) {
+        DeviceGuard g(S->dev(d));
+        CK(cudaStreamWaitEvent(S->cst[d], S->done[d], 0));
+        if (!host) CK(cudaStreamWaitEvent(S->cst[d], in_ready, 0));
+        xd[d] = S->xbuf[d].get(size_t(std::max<int64_t>(xrows * p, 1)) * cs);
+        if (xrows * p > 0)
+            CK(cudaMemcpy2DAsync(xd[d], size_t(xrows) * cs, x, size_t(ldx) * cs, size_t(xrows) * cs, size_t(p),
+                                 host ? cudaMemcpyHostToDevice : cudaMemcpyDefault, S->cst[d]));
+    }
+    const int64_t nv = S->nv(), n1 = S->dims[0];
+    for (tm_sharded::Piece& pc : S->pieces) {
+        const size_t d = pc.d;
+        DeviceGuard g(S->dev(d));
+        tm_store* st = pc.st;
+        const int64_t h = pc.b - pc.a, rp = st->rows();
+        void* yt = pc.ybuf.get(size_t(std::max<int64_t>(rp * p, 1)) * cs);
+        order_after_prev(st, S->cst[d]);
+        if (st->ncols == 0) {
+            zero_dev(st, yt, rp, p, rp, S->cst[d]);
+        } else if (aca) {
+            void* w = st->wbuf.get(size_t(st->ncols * p) * cs);
+            aca_vhx_dev(st, xd[d], xrows, p, w, S->cst[d]);
+            forward_dev(st, w, st->ncols, p, yt, rp, S->cst[d]);
+        } else {
+            forward_dev(st, xd[d], xrows, p, yt, rp, S->cst[d]);
+        }
+        mark_done(st, S->cst[d]);
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, S->cst[d]));
+        CK(cudaStreamWaitEvent(S->mst[d], ev, 0));
+        CK(cudaEventDestroy(ev));
+        for (int64_t c = 0; c < p; ++c)
+            slab_copy(S, static_cast<char*>(y) + size_t(c * ldy + pc.k * nv + pc.a) * cs, size_t(n1),
+                      static_cast<const char*>(yt) + size_t(c * rp) * cs, size_t(h), h,
+                      host ? cudaMemcpyDeviceToHost : cudaMemcpyDefault, S->mst[d]);
+    }
+    for (size_t d = 0; d < nd; ++d) {
+        DeviceGuard g(S->dev(d));
+        // done[d]: this device's compute (cst) and copies (mst)
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, S->cst[d]));
+        CK(cudaStreamWaitEvent(S->mst[d], ev, 0));
+        CK(cudaEventDestroy(ev));
+        CK(cudaEventRecord(S->done[d], S->mst[d]));
+    }
+    DeviceGuard g(S->dev(0));
+    if (in_ready) CK(cudaEventDestroy(in_ready));
+    if (host) {
+        for (size_t d = 0; d < nd; ++d) CK(cudaEventSynchronize(S->done[d]));
+    } else {
+        for (size_t d = 0; d < nd; ++d) CK(cudaStreamWaitEvent(caller, S->done[d], 0));
+    }
+}
+
+// Adjoint (aca: aca_adjoint) over the row pieces: each piece reads its rows
+// of Phi, the pieces of a device sum their m x p (ACA: r_c x p, then V t,
+// m2 x p) partials, and the devices' partials are reduced to the root.
+void rows_adjoint(tm_sharded* S, const void* phi, int64_t ldphi, int64_t p, void* z, int64_t ldz, bool host,
+                  cudaStream_t caller, bool aca) {
+    const size_t nd = S->ndev(), cs = S->csize();
+    const int64_t nv = S->nv(), n1 = S->dims[0], tr = S->ncols, outrows = aca ? S->m2 : S->ncols;
+    cudaEvent_t in_ready = nullptr;
+    if (!host) {
+        DeviceGuard g(S->dev(0));
+        CK(cudaEventCreateWithFlags(&in_ready, cudaEventDisableTiming));
+        CK(cudaEventRecord(in_ready, caller));
+    }
+    std::vector<void*> out(nd, nullptr);
+    std::vector<int64_t> ld(nd, outrows);
+    std::vector<bool> first(nd, true);
+    std::vector<tm_store*> any(nd, nullptr);
+    for (size_t d = 0; d < nd; ++d) {
+        DeviceGuard g(S->dev(d));
+        CK(cudaStreamWaitEvent(S->cst[d], S->done[d], 0));
+        if (!host) CK(cudaStreamWaitEvent(S->cst[d], in_ready, 0));
+    }
+    for (tm_sharded::Piece& pc : S->pieces) {
+        const size_t d = pc.d;
+        DeviceGuard g(S->dev(d));
+        tm_store* st = pc.st;
+        const int64_t h = pc.b - pc.a, rp = st->rows();
+        void* pt = pc.pbuf.get(size_t(std::max<int64_t>(rp * p, 1)) * cs);
+        for (int64_t c = 0; c < p; ++c)
+            slab_copy(S, static_cast<char*>(pt) + size_t(c * rp) * cs, size_t(h),
+                      static_cast<const char*>(phi) + size_t(c * ldphi + pc.k * nv + pc.a) * cs, size_t(n1), h,
+                      host ? cudaMemcpyHostToDevice : cudaMemcpyDefault, S->cst[d]);
+        void* acc = S->zbuf[d].get(size_t(std::max<int64_t>(tr * p, 1)) * cs);
+        void* t = first[d] ? acc : pc.tbuf.get(size_t(std::max<int64_t>(tr * p, 1)) * cs);
+        order_after_prev(st, S->cst[d]);
+        if (tr > 0) adjoint_dev(st, pt, rp, p, t, tr, S->cst[d]);
+        mark_done(st, S->cst[d]);
+        if (!first[d]) add_into(S, acc, t, tr * p, S->cst[d]);
+        first[d] = false;
+        any[d] = st;
+    }
+    for (size_t d = 0; d < nd; ++d) {
+        DeviceGuard g(S->dev(d));
+        void* acc = S->zbuf[d].get(size_t(std::max<int64_t>(tr * p, 1)) * cs);
+        if (first[d] && tr * p > 0) CK(cudaMemsetAsync(acc, 0, size_t(tr * p) * cs, S->cst[d]));  // no pieces here
+        if (aca) {
+            void* zp = S->ybuf[d].get(size_t(std::max<int64_t>(outrows * p, 1)) * cs);
+            if (any[d])
+                aca_vt_dev(any[d], acc, p, zp, outrows, S->cst[d]);
+            else if (outrows * p > 0)
+                CK(cudaMemsetAsync(zp, 0, size_t(outrows * p) * cs, S->cst[d]));
+            out[d] = zp;
+        } else {
+            out[d] = acc;
+        }
+    }
+    RedUnit u{0, outrows, 0, p, {}};
+    for (size_t d = 0; d < nd; ++d) {
+        DeviceGuard g(S->dev(d));
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, S->cst[d]));
+        u.ev.push_back(ev);
+    }
+    std::vector<RedUnit> units{u};
+    reduce_units(S, units, out, ld);
+    {
+        DeviceGuard g(S->dev(0));
+        if (outrows * p > 0)
+            CK(cudaMemcpy2DAsync(z, size_t(ldz) * cs, out[0], size_t(outrows) * cs, size_t(outrows) * cs, size_t(p),
+                                 host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, S->mst[0]));
+    }
+    for (size_t d = 0; d < nd; ++d) {
+        DeviceGuard g(S->dev(d));
+        CK(cudaEventRecord(S->done[d], S->comm->emulated || nd == 1 ? S->mst[0] : S->mst[d]));
+        CK(cudaEventDestroy(units[0].ev[d]));
+    }
+    DeviceGuard g(S->dev(0));
+    if (in_ready) CK(cudaEventDestroy(in_ready));
+    if (host) {
+        for (size_t d = 0; d < nd; ++d) CK(cudaEventSynchronize(S->done[d]));
+    } else {
+        CK(cudaStreamWaitEvent(caller, S->done[0], 0));
+    }
+}
+
+void add_ops(const tm_sharded* S, int64_t p, int64_t* ops) {
+    auto one = [&](const tm_store* st) {
+        ops[0] += st->dec_madds;
+        ops[1] += st->ncols * st->q * st->nv() * p;
+    };
+    for (const tm_store* st : S->shards) one(st);
+    for (const tm_sharded::Piece& pc : S->pieces) one(pc.st);
+}
+
 }  // namespace
 
 extern "C" {
@@ -461,6 +778,17 @@ TM_API int tm_comm_init(int ndev, const int* devices, tm_comm** out) {
         if (!c->emulated) {
             c->comms.assign(size_t(ndev), nullptr);
             NCK(nccl().CommInitAll(c->comms.data(), ndev, devices));
+            // peer access for the row-sharded products' direct slab copies (NVLink)
+            for (int i = 0; i < ndev; ++i)
+                for (int j = 0; j < ndev; ++j) {
+                    int can = 0;
+                    if (i == j || cudaDeviceCanAccessPeer(&can, devices[i], devices[j]) != cudaSuccess || !can)
+                        continue;
+                    DeviceGuard g(devices[i]);
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+                    else CK(e);
+                }
         }
         *out = c.release();
     });
@@ -478,9 +806,11 @@ TM_API int tm_comm_info(const tm_comm* c, int32_t* ndev, int32_t* emulated) {
     });
 }
 
-TM_API int tm_sharded_create(const tm_store_desc* desc, tm_comm* comm, int dtype, tm_sharded** out) {
+TM_API int tm_sharded_create_mode(const tm_store_desc* desc, tm_comm* comm, int dtype, int mode, tm_sharded** out) {
     return guarded([&] {
         if (!desc || !comm || !out) contract("tm_sharded_create: null argument");
+        if (mode != TM_SHARD_COLUMNS && mode != TM_SHARD_ROWS)
+            contract("tm_sharded_create: mode must be TM_SHARD_COLUMNS or TM_SHARD_ROWS");
         if (desc->payload_on_device || desc->v_on_device)
             contract("tm_sharded_create: payload and V must be host arrays (each shard uploads its own columns)");
         const tm_store_desc& d = *desc;
@@ -495,11 +825,30 @@ TM_API int tm_sharded_create(const tm_store_desc* desc, tm_comm* comm, int dtype
         const int nd = int(comm->devices.size());
         auto S = std::make_unique<tm_sharded>();
         S->comm = comm;
+        S->devices = comm->devices;
+        S->mode = mode;
         S->dtype = dtype;
         S->q = d.q;
         S->ncols = d.ncols;
         S->m2 = d.v ? d.m2 : 0;
         for (int g = 0; g < 3; ++g) S->dims[g] = d.dims[g];
+        S->cst.assign(size_t(nd), nullptr);
+        S->mst.assign(size_t(nd), nullptr);
+        S->done.assign(size_t(nd), nullptr);
+        S->xbuf.resize(size_t(nd));
+        S->ybuf.resize(size_t(nd));
+        S->zbuf.resize(size_t(nd));
+        for (int s = 0; s < nd; ++s) {
+            DeviceGuard g(comm->devices[size_t(s)]);
+            CK(cudaStreamCreateWithFlags(&S->cst[size_t(s)], cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&S->mst[size_t(s)], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&S->done[size_t(s)], cudaEventDisableTiming));
+        }
+        if (mode == TM_SHARD_ROWS) {
+            build_row_pieces(S.get(), d, dtype);
+            *out = S.release();
+            return;
+        }
         const std::vector<int64_t> b = balanced_bounds(d, nd);
         // payload offset (complex scalars) of each column
         std::vector<int64_t> col_off(size_t(d.ncols) + 1, 0);
@@ -512,12 +861,6 @@ TM_API int tm_sharded_create(const tm_store_desc* desc, tm_comm* comm, int dtype
             col_off[size_t(j) + 1] = col_off[size_t(j)] + sz;
         }
         S->shards.assign(size_t(nd), nullptr);
-        S->cst.assign(size_t(nd), nullptr);
-        S->mst.assign(size_t(nd), nullptr);
-        S->done.assign(size_t(nd), nullptr);
-        S->xbuf.resize(size_t(nd));
-        S->ybuf.resize(size_t(nd));
-        S->zbuf.resize(size_t(nd));
         for (int s = 0; s < nd; ++s) {
             S->c0.push_back(b[size_t(s)]);
             S->c1.push_back(b[size_t(s) + 1]);
@@ -527,12 +870,36 @@ TM_API int tm_sharded_create(const tm_store_desc* desc, tm_comm* comm, int dtype
             sd.payload = d.payload + 2 * col_off[size_t(b[size_t(s)])];
             if (d.v) sd.v = d.v + 2 * d.m2 * b[size_t(s)];  // V's columns of this shard (column-major)
             S->shards[size_t(s)] = create_store(sd, comm->devices[size_t(s)], dtype);
-            DeviceGuard g(comm->devices[size_t(s)]);
-            CK(cudaStreamCreateWithFlags(&S->cst[size_t(s)], cudaStreamNonBlocking));
-            CK(cudaStreamCreateWithFlags(&S->mst[size_t(s)], cudaStreamNonBlocking));
-            CK(cudaEventCreateWithFlags(&S->done[size_t(s)], cudaEventDisableTiming));
         }
         *out = S.release();
+    });
+}
+
+TM_API int tm_sharded_create(const tm_store_desc* desc, tm_comm* comm, int dtype, tm_sharded** out) {
+    return tm_sharded_create_mode(desc, comm, dtype, TM_SHARD_COLUMNS, out);
+}
+
+TM_API int tm_shard_row_cuts(int32_t q, int64_t n1, int32_t ndev, int64_t align, int64_t min_rows,
+                             const double* comp_costs, int64_t* cuts) {
+    return guarded([&] {
+        if (q < 1 || n1 < 1 || ndev < 1 || !comp_costs || !cuts) contract("tm_shard_row_cuts: bad argument");
+        const std::vector<int64_t> c =
+            row_cuts(std::vector<double>(comp_costs, comp_costs + q), n1, ndev, align, min_rows);
+        std::copy(c.begin(), c.end(), cuts);
+    });
+}
+
+TM_API int tm_sharded_pieces(const tm_sharded* s, int32_t* npieces, int64_t* pieces) {
+    return guarded([&] {
+        if (!s) contract("null sharded store");
+        if (npieces) *npieces = int32_t(s->pieces.size());
+        if (pieces)
+            for (size_t i = 0; i < s->pieces.size(); ++i) {
+                pieces[4 * i] = int64_t(s->pieces[i].d);
+                pieces[4 * i + 1] = s->pieces[i].k;
+                pieces[4 * i + 2] = s->pieces[i].a;
+                pieces[4 * i + 3] = s->pieces[i].b;
+            }
     });
 }
 
@@ -543,15 +910,16 @@ TM_API int tm_sharded_destroy(tm_sharded* s) {
 TM_API int tm_sharded_info(const tm_sharded* s, int32_t* nshards, int64_t* ranges, int64_t* device_bytes) {
     return guarded([&] {
         if (!s) contract("null sharded store");
-        if (nshards) *nshards = int32_t(s->shards.size());
+        if (nshards) *nshards = int32_t(s->ndev());
         int64_t bytes = 0;
-        for (size_t d = 0; d < s->shards.size(); ++d) {
+        for (size_t d = 0; d < s->ndev(); ++d) {
             if (ranges) {
                 ranges[2 * d] = s->c0[d];
                 ranges[2 * d + 1] = s->c1[d];
             }
-            bytes += s->shards[d]->device_bytes;
+            if (d < s->shards.size()) bytes += s->shards[d]->device_bytes;
         }
+        for (const tm_sharded::Piece& pc : s->pieces) bytes += pc.st->device_bytes;
         if (device_bytes) *device_bytes = bytes;
     });
 }
@@ -562,9 +930,11 @@ TM_API int tm_sharded_forward(tm_sharded* S, const void* x, int64_t ldx, int64_t
         if (!S) contract("null sharded store");
         if (xrows != S->ncols)
             contract("forward: x has " + std::to_string(xrows) + " rows, expected m = " + std::to_string(S->ncols));
-        check_common(S->shards[0], p, ldx, xrows, ldy, S->rows(), where, x, y);
+        check_common(S->any_store(), p, ldx, xrows, ldy, S->rows(), where, x, y);
         std::lock_guard<std::mutex> lock(S->mu);
-        if (p > 0)
+        if (p > 0 && S->mode == TM_SHARD_ROWS)
+            rows_forward(S, x, ldx, xrows, p, y, ldy, where == TM_HOST, static_cast<cudaStream_t>(stream), false);
+        else if (p > 0)
             sharded_sum(S, x, ldx, xrows, p, y, ldy, S->rows(), where == TM_HOST, static_cast<cudaStream_t>(stream),
                         false, [](tm_store* st, const void* xd, int64_t n, int64_t pp, void* yd, int64_t ld,
                                   cudaStream_t cs, const HostPipe* hp) {
@@ -573,11 +943,7 @@ TM_API int tm_sharded_forward(tm_sharded* S, const void* x, int64_t ldx, int64_t
                             else
                                 zero_dev(st, yd, st->rows(), pp, ld, cs);
                         });
-        if (ops)
-            for (tm_store* st : S->shards) {
-                ops[0] += st->dec_madds;
-                ops[1] += st->ncols * st->q * st->nv() * p;
-            }
+        if (ops) add_ops(S, p, ops);
     });
 }
 
@@ -588,15 +954,13 @@ TM_API int tm_sharded_adjoint(tm_sharded* S, const void* phi, int64_t ldphi, int
         if (phirows != S->rows())
             contract("adjoint: phi has " + std::to_string(phirows) + " rows, expected q*n_v = " +
                      std::to_string(S->rows()));
-        check_common(S->shards[0], p, ldphi, phirows, ldz, S->ncols, where, phi, z);
+        check_common(S->any_store(), p, ldphi, phirows, ldz, S->ncols, where, phi, z);
         std::lock_guard<std::mutex> lock(S->mu);
-        if (p > 0 && S->ncols > 0)
+        if (p > 0 && S->ncols > 0 && S->mode == TM_SHARD_ROWS)
+            rows_adjoint(S, phi, ldphi, p, z, ldz, where == TM_HOST, static_cast<cudaStream_t>(stream), false);
+        else if (p > 0 && S->ncols > 0)
             sharded_adjoint(S, phi, ldphi, p, z, ldz, where == TM_HOST, static_cast<cudaStream_t>(stream));
-        if (ops)
-            for (tm_store* st : S->shards) {
-                ops[0] += st->dec_madds;
-                ops[1] += st->ncols * st->q * st->nv() * p;
-            }
+        if (ops) add_ops(S, p, ops);
     });
 }
 
@@ -607,9 +971,11 @@ TM_API int tm_sharded_aca_forward(tm_sharded* S, const void* x, int64_t ldx, int
         if (!S->m2) contract("aca_forward: store carries no ACA V factor");
         if (xrows != S->m2)
             contract("aca_forward: x has " + std::to_string(xrows) + " rows, expected " + std::to_string(S->m2));
-        check_common(S->shards[0], p, ldx, xrows, ldy, S->rows(), where, x, y);
+        check_common(S->any_store(), p, ldx, xrows, ldy, S->rows(), where, x, y);
         std::lock_guard<std::mutex> lock(S->mu);
-        if (p > 0)
+        if (p > 0 && S->mode == TM_SHARD_ROWS)
+            rows_forward(S, x, ldx, xrows, p, y, ldy, where == TM_HOST, static_cast<cudaStream_t>(stream), true);
+        else if (p > 0)
             sharded_sum(S, x, ldx, xrows, p, y, ldy, S->rows(), where == TM_HOST, static_cast<cudaStream_t>(stream),
                         true, [](tm_store* st, const void* xd, int64_t n, int64_t pp, void* yd, int64_t ld,
                                  cudaStream_t cs, const HostPipe* hp) {
@@ -632,9 +998,11 @@ TM_API int tm_sharded_aca_adjoint(tm_sharded* S, const void* phi, int64_t ldphi,
         if (phirows != S->rows())
             contract("aca_adjoint: phi has " + std::to_string(phirows) + " rows, expected " +
                      std::to_string(S->rows()));
-        check_common(S->shards[0], p, ldphi, phirows, ldz, S->m2, where, phi, z);
+        check_common(S->any_store(), p, ldphi, phirows, ldz, S->m2, where, phi, z);
         std::lock_guard<std::mutex> lock(S->mu);
-        if (p > 0)
+        if (p > 0 && S->mode == TM_SHARD_ROWS)
+            rows_adjoint(S, phi, ldphi, p, z, ldz, where == TM_HOST, static_cast<cudaStream_t>(stream), true);
+        else if (p > 0)
             sharded_sum(S, phi, ldphi, phirows, p, z, ldz, S->m2, where == TM_HOST,
                         static_cast<cudaStream_t>(stream), true,
                         [](tm_store* st, const void* pd, int64_t n, int64_t pp, void* zd, int64_t ld, cudaStream_t cs,

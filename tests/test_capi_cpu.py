@@ -177,3 +177,27 @@ def test_cpp_dropin_compiles_and_validates(product, tmp_path):
         assert r.returncode == 0, r.stdout + r.stderr
     else:
         assert r.returncode == 5 and "device error" in r.stdout  # no CPU fallback
+
+
+def test_row_partition_rule_matches_python(product):
+    """tm_shard_row_cuts (the C ABI's row-sharding partition) and
+    sharded.row_pieces implement the same rule: identical cuts on random
+    component costs, grid heights, device counts, alignments and minimum
+    piece heights; every piece honours the alignment / minimum-height rule."""
+    from paper_2103_06393_b200.multigpu import row_cuts
+    from paper_2103_06393_b200.sharded import row_pieces
+    rng = np.random.default_rng(0)
+    for _ in range(500):
+        q, n1, nd = int(rng.integers(1, 14)), int(rng.integers(1, 300)), int(rng.integers(1, 10))
+        cc = rng.random(q) * float(rng.choice([1.0, 1e6, 1e12]))
+        al, mr = int(rng.choice([1, 4, 8])), int(rng.integers(1, 40))
+        cuts = row_cuts(cc, n1, nd, al, mr)
+        pcs = row_pieces(cc, n1, nd, al, mr)
+        want = np.cumsum([0] + [sum(b - a for _, a, b in p) for p in pcs])
+        assert list(cuts) == list(want)
+        assert cuts[0] == 0 and cuts[-1] == q * n1 and np.all(np.diff(cuts) >= 0)
+        for p in pcs:
+            for k, a, b in p:
+                for e in (a, b):  # a cut inside a component: aligned, >= max(min_rows, align) from both ends
+                    if 0 < e < n1:
+                        assert e % al == 0 and min(e, n1 - e) >= max(mr, al)

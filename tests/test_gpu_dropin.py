@@ -2,7 +2,7 @@
 a C++ program written against the reference API (forward, adjoint,
 stacked_forward / stacked_adjoint over TuckerColumns, element,
 aca_forward / aca_adjoint with Tucker and dense U, row_of_compressed_u,
-load_ctc1 / load_cta1, and the multi-GPU ShardedStore) runs on the committed golden fixtures and its outputs
+load_ctc1 / load_cta1, and the multi-GPU ShardedStore by columns and by rows) runs on the committed golden fixtures and its outputs
 are compared with the golden arrays (the oracle's, pinned to the reference
 by tests/test_ref_pin_cpu.py) at 1e-12 (the drop-in's default is complex128).
 It also rebuilds a CompressedCoupling with different values at the same
@@ -79,6 +79,13 @@ int main(int argc, char** argv) {
         wr(o + "/zsh.bin", adjoint(ss, phi));
         b200::ShardedStore sa(fac, comm);
         wr(o + "/yash.bin", aca_forward(sa, xa));
+        // row (voxel-slab) sharding
+        b200::ShardedStore sr(cc, comm, TM_C128, TM_SHARD_ROWS);
+        wr(o + "/ysr.bin", forward(sr, x));
+        wr(o + "/zsr.bin", adjoint(sr, phi));
+        b200::ShardedStore sar(fac, comm, TM_C128, TM_SHARD_ROWS);
+        wr(o + "/yasr.bin", aca_forward(sar, xa));
+        wr(o + "/zasr.bin", aca_adjoint(sar, pa));
     }
 
     // the same stack slot, different contents each iteration
@@ -146,5 +153,9 @@ def test_cpp_dropin_values(product, oracle, tmp_path):
     assert rel(_r(tmp_path / "ysh.bin", rows, 8), ld("loop8_y.npy")) <= 1e-12
     assert rel(_r(tmp_path / "zsh.bin", m, 8), ld("loop8_z.npy")) <= 1e-12
     assert rel(_r(tmp_path / "yash.bin", fac.rows, 4), ld("aca8_y.npy")) <= 1e-12
+    assert rel(_r(tmp_path / "ysr.bin", rows, 8), ld("loop8_y.npy")) <= 1e-12
+    assert rel(_r(tmp_path / "zsr.bin", m, 8), ld("loop8_z.npy")) <= 1e-12
+    assert rel(_r(tmp_path / "yasr.bin", fac.rows, 4), ld("aca8_y.npy")) <= 1e-12
+    assert rel(_r(tmp_path / "zasr.bin", fac.cols, 4), ld("aca8_z.npy")) <= 1e-12
     for it in range(3):
         assert rel(_r(tmp_path / f"yit{it}.bin", rows, 8), (it + 1) * ld("loop8_y.npy")) <= 1e-12

@@ -1,5 +1,5 @@
-"""Multi-GPU column sharding at the C ABI (tm_comm_* / tm_sharded_*) on the
-one GPU of the test box: a real single-rank NCCL communicator ([0]) and an
+"""Multi-GPU sharding at the C ABI (tm_comm_* / tm_sharded_*), by columns and
+by row slabs (TM_SHARD_ROWS), on the one GPU of the test box: a real single-rank NCCL communicator ([0]) and an
 emulated three-shard communicator ([0, 0, 0]: the collectives become
 device-local copies / adds, every other part of the sharded path — cost-
 balanced column split, per-shard stores, per-component completion events,
@@ -19,19 +19,33 @@ def _r(a, dtype):
     return a.astype(np.complex64).astype(np.complex128) if dtype == "c64" else a
 
 
+def _check_pieces(ss, cc, ndev):
+    """rows mode: the pieces tile the q * n1 slabs in shard order."""
+    n1 = cc.grid_dims[0]
+    got = [(k * n1 + a, k * n1 + b) for _, k, a, b in ss.pieces]
+    assert got[0][0] == 0 and got[-1][1] == cc.q * n1
+    assert all(x[1] == y[0] for x, y in zip(got, got[1:]))
+    assert [d for d, *_ in ss.pieces] == sorted(d for d, *_ in ss.pieces)
+    assert all(0 <= d < ndev for d, *_ in ss.pieces)
+
+
+@pytest.mark.parametrize("mode", ["columns", "rows"])
 @pytest.mark.parametrize("devices", [[0], [0, 0, 0]])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("dims,q,m,p", [((16, 12, 40), 3, 17, 1), ((64, 64, 64), 12, 10, 3), ((9, 5, 7), 1, 2, 2)])
-def test_sharded_products(oracle, product, devices, dtype, dims, q, m, p):
+def test_sharded_products(oracle, product, mode, devices, dtype, dims, q, m, p):
     import torch
     from paper_2103_06393_b200.multigpu import Comm, ShardedDeviceStore
     O = oracle
     cc = ragged_store(dims, q, m, 2, 9, seed=m + q)
     comm = Comm(devices)
     assert comm.emulated == (len(set(devices)) != len(devices))
-    ss = ShardedDeviceStore.from_compressed(comm, cc, dtype)
+    ss = ShardedDeviceStore.from_compressed(comm, cc, dtype, mode=mode)
     rng = ss.shard_ranges
-    assert rng[0][0] == 0 and rng[-1][1] == m and all(a[1] == b[0] for a, b in zip(rng, rng[1:]))
+    end = m if mode == "columns" else q * dims[0]
+    assert rng[0][0] == 0 and rng[-1][1] == end and all(a[1] == b[0] for a, b in zip(rng, rng[1:]))
+    if mode == "rows":
+        _check_pieces(ss, cc, len(devices))
     ref = O.OracleStore(cc.rounded_c64() if dtype == "c64" else cc)
     x = _r(cn01(m, p, 1), dtype)
     phi = _r(cn01(cc.rows, p, 2), dtype)
@@ -54,8 +68,9 @@ def test_sharded_products(oracle, product, devices, dtype, dims, q, m, p):
         assert rel(z.cpu().numpy(), zo) <= TOL[dtype]
 
 
+@pytest.mark.parametrize("mode", ["columns", "rows"])
 @pytest.mark.parametrize("devices", [[0], [0, 0]])
-def test_sharded_aca(oracle, product, devices):
+def test_sharded_aca(oracle, product, devices, mode):
     from paper_2103_06393_b200.multigpu import Comm, ShardedDeviceStore
     O = oracle
     cc = ragged_store((20, 18, 30), 3, 9, 2, 6, seed=4)
@@ -63,11 +78,46 @@ def test_sharded_aca(oracle, product, devices):
     v = rng.standard_normal((23, 9)) + 1j * rng.standard_normal((23, 9))
     fac = O.Aca(cc.grid_dims, cc.q, cc.ranks, cc.payload, v)
     comm = Comm(devices)
-    ss = ShardedDeviceStore.from_arrays(comm, fac.grid_dims, fac.q, fac.ranks, fac.payload, "c128", v=v)
+    ss = ShardedDeviceStore.from_arrays(comm, fac.grid_dims, fac.q, fac.ranks, fac.payload, "c128", v=v, mode=mode)
     x = cn01(23, 2, 5)
     phi = cn01(fac.rows, 2, 6)
     assert rel(ss.aca_forward(x), O.aca_forward(fac, x)) <= 1e-12
     assert rel(ss.aca_adjoint(phi), O.aca_adjoint(fac, phi)) <= 1e-12
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0, 0, 0]])
+def test_row_sharding_slabs_inside_components(oracle, product, devices):
+    """Row sharding whose cuts fall inside components (a 64-row grid, q = 3,
+    low ranks: pieces of 8..56 i1 rows), c64 on the tensor cores: host and
+    strided device I/O, OpCounts equal to the unsharded store's, a device
+    with several pieces (partial adjoints summed on the device)."""
+    import torch
+    from paper_2103_06393_b200.multigpu import Comm, ShardedDeviceStore
+    O = oracle
+    cc = ragged_store((64, 40, 256), 3, 12, 1, 6, seed=21)
+    comm = Comm(devices)
+    ss = ShardedDeviceStore.from_compressed(comm, cc, "c64", mode="rows")
+    _check_pieces(ss, cc, len(devices))
+    assert any(0 < a or b < 64 for _, _, a, b in ss.pieces)  # some cut inside a component
+    ref = O.OracleStore(cc.rounded_c64())
+    x = _r(cn01(cc.m, 3, 1), "c64")
+    phi = _r(cn01(cc.rows, 3, 2), "c64")
+    ops = {}
+    assert rel(ss.forward(x, ops), ref.forward(x)) <= 1e-5
+    d = ref.opcounts(3)
+    assert ops["decompress_madds"] == d[0] and ops["accumulate_madds"] == d[1]
+    assert rel(ss.adjoint(phi), ref.adjoint(phi)) <= 1e-5
+    xd = torch.from_numpy(np.ascontiguousarray(x.T)).to(torch.complex64).cuda().t()
+    pbig = torch.zeros((3, cc.rows + 7), dtype=torch.complex64, device="cuda")
+    pbig[:, :cc.rows] = torch.from_numpy(np.ascontiguousarray(phi.T)).to(torch.complex64).cuda()
+    pd = pbig.t()[:cc.rows]  # leading dimension rows + 7
+    y = torch.full((3, cc.rows + 5), 9.0 + 0j, dtype=torch.complex64, device="cuda").t()[:cc.rows]
+    z = torch.empty((3, cc.m + 2), dtype=torch.complex64, device="cuda").t()[:cc.m]
+    ss.forward_into(xd, y)
+    ss.adjoint_into(pd, z)
+    torch.cuda.synchronize()
+    assert rel(y.cpu().numpy(), ref.forward(x)) <= 1e-5
+    assert rel(z.cpu().numpy(), ref.adjoint(phi)) <= 1e-5
 
 
 def test_forward_components(oracle, product):
