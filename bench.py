@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-cols", type=int, default=0, help="columns in the CPU sample (0 = auto)")
+    ap.add_argument("--shard", default="rows", choices=["rows", "columns"],
+                    help="N > 1: row-slab pieces (SURVEY §8e, no forward reduction) or column ranges")
     return ap.parse_args()
 
 
@@ -348,12 +350,13 @@ def full_measurement(cfg):
     return None
 
 
-def config_dict(cfg, world):
+def config_dict(cfg, world, shard="rows"):
     """The workload description both arms print (same dict: same_config)."""
     from paper_2103_06393_b200.workloads import rank_table
     gb = compressed_bytes(cfg, rank_table(cfg, SEED)) / 1e9
     return {"workload": cfg.name, "grid": list(cfg.grid), "q": cfg.q, "m": cfg.m, "p": cfg.p,
-            "aca_m2": cfg.aca_m2 or None, "parallelism": f"column-shard x{world}",
+            "aca_m2": cfg.aca_m2 or None,
+            "parallelism": f"row-slab-shard x{world}" if world > 1 and shard == "rows" else f"column-shard x{world}",
             "l2": "inputs larger than L2 (compressed store %.2f GB c64 + derived tensor-core operands)" % gb
             if gb >= 0.2 else "L2 flushed between timed steps (512 MB write outside the step events; store %.3f GB)"
             % gb}
@@ -413,7 +416,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None,
         "dtype": "c128 (the reference's arithmetic; c64-rounded factors)", "data": "synthetic",
-        "config": config_dict(cfg, world),
+        "config": config_dict(cfg, world, args.shard),
         "cpu_baseline": {"value": round(ms, 1), "unit": "ms", "cores": W, "kind": kind, "sample": sample},
         "e2e": {"value": round(ms, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "extrapolated": not full,
@@ -449,12 +452,12 @@ def cn01(rows, cols, seed):
     return np.asfortranarray(a)
 
 
-def compressed_bytes(cfg, ranks):
+def compressed_bytes(cfg, ranks, n1=None):
     """Bytes of the compressed store proper (cores + factors, c64): the
     roofline's B_alg term, without the derived tensor-core
-    operand copies."""
+    operand copies.  n1: the grid height of a row-slab piece."""
     r = np.asarray(ranks, np.int64).reshape(-1, 3)
-    n1, n2, n3 = cfg.grid
+    n1, n2, n3 = (cfg.grid[0] if n1 is None else n1), cfg.grid[1], cfg.grid[2]
     scalars = (r[:, 0] * r[:, 1] * r[:, 2] + n1 * r[:, 0] + n2 * r[:, 1] + n3 * r[:, 2]).sum()
     return int(scalars) * (8 if cfg.dtype == "c64" else 16)
 
@@ -486,7 +489,8 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
 
     from paper_2103_06393_b200 import DeviceStore, launch_count
-    from paper_2103_06393_b200.sharded import ShardedStore, balanced_shards, column_costs
+    from paper_2103_06393_b200.sharded import (RowShardedStore, ShardedStore, balanced_shards, column_costs,
+                                               component_costs, row_pieces, slice_payload_rows)
     from paper_2103_06393_b200.workloads import CONFIGS, rank_table, synthetic_payload, synthetic_v, tensor_scales
 
     cfg = CONFIGS[args.config]
@@ -495,16 +499,36 @@ def main():
     costs = column_costs(cfg.grid, ranks, cfg.p)
     aca = bool(cfg.aca_m2)  # ACA configs: aca_forward / aca_adjoint (src/matvec.cpp:150-175), V included
     v_all = synthetic_v(cfg, SEED) if aca else None
+    rows_mode = world > 1 and args.shard == "rows"
     shards = balanced_shards(costs, world)
-    c0, c1 = shards[rank]
+    c0, c1 = (0, cfg.m) if rows_mode else shards[rank]  # rows mode: every rank holds all columns of its pieces
     nrows = cfg.q * int(np.prod(cfg.grid))
     cdt = torch.complex64 if cfg.dtype == "c64" else torch.complex128
 
     # --- store: seeded synthetic payload generated on the device, packed once --
     t_build = time.perf_counter()
-    pay, _ = synthetic_payload(cfg.grid, ranks[c0:c1], scales[c0:c1], SEED + 1000 + c0, device=dev)
-    store = DeviceStore.from_arrays(cfg.grid, cfg.q, ranks[c0:c1], pay, cfg.dtype, local,
-                                    v=v_all[:, c0:c1] if aca else None)
+    if rows_mode:
+        # this rank's (component, i1-slab) pieces, each a one-component store on
+        # its sub-grid with every column (sharded.row_pieces / slice_payload_rows)
+        r1max = int(ranks[..., 0].max())
+        layout = row_pieces(component_costs(cfg.grid, ranks, cfg.p), cfg.grid[0], world, align=8,
+                            min_rows=8 * ((r1max + 7) // 8))
+        pieces = []
+        for k, a, b in layout[rank]:
+            rk = np.ascontiguousarray(ranks[:, k:k + 1, :])
+            payk, _ = synthetic_payload(cfg.grid, rk, scales[:, k:k + 1], SEED + 1000 + 7 * k, device=dev)
+            payp = slice_payload_rows(cfg.grid, rk, payk, a, b)
+            del payk
+            pieces.append((k, a, b, DeviceStore.from_arrays((b - a, cfg.grid[1], cfg.grid[2]), 1, rk, payp, cfg.dtype,
+                                                            local, v=v_all if aca else None)))
+            del payp
+        part_stores = [st for *_, st in pieces]
+        store = part_stores[0] if part_stores else None
+    else:
+        pay, _ = synthetic_payload(cfg.grid, ranks[c0:c1], scales[c0:c1], SEED + 1000 + c0, device=dev)
+        store = DeviceStore.from_arrays(cfg.grid, cfg.q, ranks[c0:c1], pay, cfg.dtype, local,
+                                        v=v_all[:, c0:c1] if aca else None)
+        part_stores = [store]
     cpu_pay = None
     if rank == 0 and world == 1 and not args.no_cpu:
         if full_cpu_pair(cfg):
@@ -515,10 +539,14 @@ def main():
             from paper_2103_06393_b200.workloads import tensor_offsets
             off = tensor_offsets(cfg.grid, ranks[:ncs])
             cpu_pay = pay[: int(off[-1])].to(cdt).to(torch.complex128).cpu().numpy()
-    del pay
+    if not rows_mode:
+        del pay
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t_build
-    sh = ShardedStore(store, c0, c1, cfg.m, shards=shards)
+    if rows_mode:
+        sh = RowShardedStore(pieces, cfg.grid, cfg.q, cfg.m, layout, m2=cfg.aca_m2 or 0)
+    else:
+        sh = ShardedStore(store, c0, c1, cfg.m, shards=shards)
 
     # --- inputs: CN(0,1), seeded (x: numpy, Phi: device RNG) ---------------------
     x_host = cn01(cfg.aca_m2 or cfg.m, cfg.p, SEED).astype(np.complex64 if cfg.dtype == "c64" else np.complex128)
@@ -653,9 +681,17 @@ def main():
         if world > 1:
             e2e["note"] = "multi-GPU e2e uses the sharded Python API; byte counts are rank 0's"
 
+    sb = torch.tensor([float(sum(st.device_bytes for st in part_stores))], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(sb, op=dist.ReduceOp.SUM)
+    store_bytes_all = sb.item()
+
     # --- roofline of the dominant kernels (one tensor-core launch per forward;
     # the adjoint is Phi split + tensor-core kernel + partial reduction) ------
-    dec, acc = store.opcounts(cfg.p)
+    dec = acc = 0
+    for st in part_stores:
+        d_, a_ = st.opcounts(cfg.p)
+        dec, acc = dec + d_, acc + a_
     flops = 8.0 * (dec + acc)  # OpCounts x 8 real flops per complex madd (this rank's shard)
     if aca:  # + the V side of one ACA product (V^H x or V t): m2 r_c p madds
         flops += 8.0 * cfg.aca_m2 * (c1 - c0) * cfg.p
@@ -690,7 +726,9 @@ def main():
                 "algorithmic_flops_per_launch": flops,
                 "adjoint": {"kernel": kernels[1], "achieved": round(aa, 2), "frac": round(aa / peak, 4)},
                 "hbm_bytes_algorithmic": int(compressed_bytes(cfg, ranks[c0:c1]) + (c1 - c0) * cfg.p * 8
-                                             + nrows * cfg.p * 8),
+                                             + nrows * cfg.p * 8) if not rows_mode else
+                int(sum(compressed_bytes(cfg, ranks[:, k], n1=b - a) for k, a, b in layout[rank])
+                    + cfg.m * cfg.p * 8 + sum(st.rows for st in part_stores) * cfg.p * 8),
                 "hbm_peak_gbs": peaks.get("hbm_gbs"), "fp32_ffma_peak_tflops": round(fp32_peak, 2),
                 "fp64_dgemm_tflops_this_run": round(fp64_peak, 2),
                 "f16_gemm_tflops_this_run": round(f16_peak, 2), "bf16_peak_tflops_measured": peaks.get("bf16_tflops")}
@@ -698,7 +736,10 @@ def main():
             # SURVEY §8d multi-GPU term C_coll / BW_NVLink: the forward's reduce of the
             # q n_v x p partial y and the adjoint's all-gather of the padded z shards,
             # against the NVLink 5 per-direction figure (spec, not measured here)
-            cbytes = nrows * cfg.p * 8 + world * max(b - a for a, b in shards) * cfg.p * 8
+            if rows_mode:  # pieces' rows of y to rank 0 + all-reduce of the m x p partial z
+                cbytes = nrows * cfg.p * 8 * (world - 1) // world + 2 * (cfg.aca_m2 or cfg.m) * cfg.p * 8
+            else:
+                cbytes = nrows * cfg.p * 8 + world * max(b - a for a, b in shards) * cfg.p * 8
             roof["collective"] = {"bytes_per_step": int(cbytes), "nvlink_gbs_spec": 900.0,
                                   "t_roof_ms": round(cbytes / 900e9 * 1e3, 3),
                                   "note": "one GPU's compute roofline above is its shard's"}
@@ -738,8 +779,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
             "data": "synthetic (seeded Tucker store with the config's shape and rank distribution)",
-            "config": config_dict(cfg, world),
-            "device_store_gb": round(store.device_bytes * world / 1e9, 2),
+            "config": config_dict(cfg, world, args.shard),
+            "device_store_gb": round(store_bytes_all / 1e9, 2),
             "forward_ms": round(fwd_med, 3), "adjoint_ms": round(adj_med, 3),
             "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "store_build_s": round(t_build, 2),

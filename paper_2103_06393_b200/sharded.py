@@ -1,4 +1,4 @@
-"""Column sharding of a Tucker store across GPUs (one process per GPU).
+"""Column and row sharding of a Tucker store across GPUs (one process per GPU).
 
 The reference parallelises products over columns with host threads
 (stacked_forward's per-worker partials, src/matvec.cpp:28-59; stacked_adjoint's
@@ -18,7 +18,14 @@ shards the r_c U columns with the matching columns of V:
   aca_forward  y = sum_ranks U[:, l] (V[:, l]^H x)  -> reduce, as the forward
   aca_adjoint  z = sum_ranks V[:, l] (U[:, l]^H phi) -> all-reduce of m2 x p
 
-The class is agnostic of the store type (anything with forward / adjoint /
+Row (voxel-slab) sharding, the alternative of SURVEY §8e (RowShardedStore,
+row_pieces, slice_payload_rows): each rank owns cost-balanced (component,
+i1-slab) pieces of the output rows, each a store on its sub-grid with every
+column; the forward needs no reduction (the pieces' rows of y are sent to the
+destination rank), the adjoint reads only the rank's rows of Phi and
+all-reduces the m x p partial z.
+
+The classes are agnostic of the store type (anything with forward / adjoint /
 rows / ncols), which lets the CPU tests drive the same host logic with gloo.
 """
 from __future__ import annotations
@@ -201,3 +208,150 @@ class ShardedStore:
         parts = [full[r * self.max_cols: r * self.max_cols + (b - a)] for r, (a, b) in enumerate(self.shards)]
         out = torch.cat(parts, 0)
         return out[:, 0] if squeeze else out
+
+
+def slice_payload_rows(dims, ranks, payload, a, b):
+    """The payload of one-component tensors (`ranks`: (ncols, 1, 3), CTC1 layout
+    `payload`, numpy or torch) restricted to the i1 rows [a, b): core and
+    U2 / U3 unchanged, U1 (n1 x r1, column-major) -> (b - a) x r1.  The
+    tensors then describe the same operator on the sub-grid (b - a, n2, n3)."""
+    r = np.asarray(ranks, np.int64).reshape(-1, 3)
+    n1, n2, n3 = (int(d) for d in dims)
+    h = int(b) - int(a)
+    if np.any(r[:, 0] > h):
+        raise ValueError(f"a slab of {h} i1 rows is below a tensor's rank r1 = {int(r[:, 0].max())}")
+    core = r[:, 0] * r[:, 1] * r[:, 2]
+    size = core + n1 * r[:, 0] + n2 * r[:, 1] + n3 * r[:, 2]
+    off = np.concatenate([[0], np.cumsum(size)])[:-1]
+    # source segments per tensor: core, r1 column pieces of U1, then U2 + U3
+    nseg = 2 + r[:, 0]
+    t_of = np.repeat(np.arange(len(r)), nseg)
+    pos = np.arange(int(nseg.sum())) - np.repeat(np.cumsum(nseg) - nseg, nseg)  # segment index inside its tensor
+    o, c0, r1 = off[t_of], core[t_of], r[t_of, 0]
+    is_core, is_tail = pos == 0, pos == nseg[t_of] - 1
+    start = np.where(is_core, o, np.where(is_tail, o + c0 + n1 * r1, o + c0 + (pos - 1) * n1 + int(a)))
+    length = np.where(is_core, c0, np.where(is_tail, n2 * r[t_of, 1] + n3 * r[t_of, 2], h))
+    total = int(length.sum())
+    idx = np.repeat(start - (np.cumsum(length) - length), length) + np.arange(total)
+    if hasattr(payload, "device"):  # torch
+        import torch
+        return payload[torch.from_numpy(idx).to(payload.device)]
+    return np.asarray(payload)[idx]
+
+
+class RowShardedStore:
+    """One rank's row-slab pieces (the alternative of SURVEY §8e; the C-ABI
+    counterpart is TM_SHARD_ROWS) plus the collectives that assemble the
+    products.  `pieces`: this rank's [(k, a, b, store)], each store a
+    one-component store on the sub-grid (b - a, n2, n3) with every column
+    (slice_payload_rows); `layout`: every rank's [(k, a, b)] lists
+    (row_pieces).  The forward has no reduction: each rank sends its pieces'
+    rows of y to `dst` (or every rank, allreduce=True); the adjoint reads only
+    this rank's rows of Phi and all-reduces the m x p partial z."""
+
+    def __init__(self, pieces, dims, q, ncols, layout, group=None, m2=0):
+        import torch.distributed as dist
+
+        self.pieces = [(int(k), int(a), int(b), st) for k, a, b, st in pieces]
+        self.dims = tuple(int(d) for d in dims)
+        self.q, self.ncols, self.m2 = int(q), int(ncols), int(m2)
+        self.layout = [[tuple(int(v) for v in pc) for pc in lst] for lst in layout]
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.nv = int(np.prod(self.dims))
+
+    @property
+    def rows(self):
+        return self.q * self.nv
+
+    def _slab(self, t, k, a, b):
+        """(p, n2 n3, b - a) view of rows [k n_v, (k + 1) n_v), i1 in [a, b) of a
+        column-major (rows x p) tensor."""
+        n1, n2, n3 = self.dims
+        tt = t.t()[:, k * self.nv:(k + 1) * self.nv]
+        return tt.reshape(tt.shape[0], n2 * n3, n1)[:, :, a:b]
+
+    def _assemble(self, outs, p, dtype, device, dst, allreduce):
+        import torch
+        import torch.distributed as dist
+
+        y = torch.zeros((p, self.rows), dtype=dtype, device=device).t()
+        for (k, a, b, _), yk in zip(self.pieces, outs):
+            self._slab(y, k, a, b).copy_(yk.t().reshape(p, -1, b - a))
+        if self.world == 1:
+            return y
+        if allreduce:  # rows are disjoint: the sum is the assembly
+            dist.all_reduce(y.t(), group=self.group)
+            return y
+        nccl = dist.get_backend(self.group) == "nccl"
+        stage = (lambda t: t) if nccl else (lambda t: t.cpu())  # gloo point-to-point: host tensors
+        ops, recv = [], []
+        if self.rank == dst:
+            for r, lst in enumerate(self.layout):
+                if r == dst:
+                    continue
+                for k, a, b in lst:
+                    buf = stage(torch.empty((p, (b - a) * self.nv // self.dims[0]), dtype=dtype, device=device))
+                    ops.append(dist.P2POp(dist.irecv, buf, r, self.group))
+                    recv.append((k, a, b, buf))
+        else:
+            for (k, a, b, _), yk in zip(self.pieces, outs):
+                ops.append(dist.P2POp(dist.isend, stage(yk.t().contiguous()), dst, self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        for k, a, b, buf in recv:
+            self._slab(y, k, a, b).copy_(buf.to(device).reshape(p, -1, b - a))
+        return y
+
+    def _forward(self, x, dst, allreduce, aca):
+        import torch
+
+        squeeze = x.dim() == 1
+        x2 = x.reshape(-1, 1) if squeeze else x
+        outs = [(st.aca_forward(x2) if aca else st.forward(x2)) for *_, st in self.pieces]
+        outs = [o.reshape(-1, 1) if o.dim() == 1 else o for o in outs]
+        dtype = outs[0].dtype if outs else (x2.dtype if x2.is_complex() else torch.complex128)
+        y = self._assemble(outs, x2.shape[1], dtype, x2.device, dst, allreduce)
+        return y[:, 0] if squeeze else y
+
+    def forward(self, x, dst=0, allreduce=False):
+        """y = Zbc x (x: m x p, replicated): the full y on `dst` (every rank
+        with allreduce=True); other ranks get their own rows only."""
+        return self._forward(x, dst, allreduce, False)
+
+    def aca_forward(self, x, dst=0, allreduce=False):
+        """y = U (V^H x) (x: m2 x p, replicated; every piece store holds V)."""
+        return self._forward(x, dst, allreduce, True)
+
+    def _adjoint(self, phi, aca):
+        import torch
+        import torch.distributed as dist
+
+        squeeze = phi.dim() == 1
+        ph = phi.reshape(-1, 1) if squeeze else phi
+        p = ph.shape[1]
+        z = None
+        for k, a, b, st in self.pieces:
+            pk = self._slab(ph, k, a, b).reshape(p, -1).t()  # contiguous copy of this piece's rows
+            zk = st.aca_adjoint(pk) if aca else st.adjoint(pk)
+            zk = zk.reshape(-1, 1) if zk.dim() == 1 else zk
+            z = zk.clone() if z is None else z + zk
+        if z is None:
+            n = self.m2 if aca else self.ncols
+            z = torch.zeros((n, p), dtype=ph.dtype, device=ph.device)
+        if self.world > 1:
+            zt = z.t().contiguous()
+            dist.all_reduce(zt, group=self.group)
+            z = zt.t()
+        return z[:, 0] if squeeze else z
+
+    def adjoint(self, phi):
+        """z = Zbc^H phi on every rank (phi: q n_v x p, replicated; each rank
+        reads only its rows)."""
+        return self._adjoint(phi, False)
+
+    def aca_adjoint(self, phi):
+        """z = V (U^H phi) on every rank."""
+        return self._adjoint(phi, True)
