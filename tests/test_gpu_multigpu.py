@@ -192,3 +192,15 @@ def test_sharded_forward_overlaps_component_reduces(oracle, product, tmp_path):
     y = np.load(out)
     x = cn01(cc.m, 2, 9).astype(np.complex64).astype(np.complex128)
     assert rel(y, O.OracleStore(cc.rounded_c64()).forward(x)) <= 1e-5
+
+
+@pytest.mark.parametrize("mode", ["columns", "rows"])
+def test_sharded_empty_store(oracle, product, mode):
+    """A store with no columns, sharded (src/matvec.cpp:28-38: zeros out)."""
+    from paper_2103_06393_b200.multigpu import Comm, ShardedDeviceStore
+    O = oracle
+    cc = O.Compressed((16, 5, 17), 3, 0, np.zeros((0, 3, 3), np.int32), np.zeros(0, np.complex128))
+    ss = ShardedDeviceStore.from_compressed(Comm([0, 0]), cc, "c64", mode=mode)
+    y = ss.forward(np.zeros((0, 2)))
+    assert y.shape == (cc.rows, 2) and not np.any(y)
+    assert ss.adjoint(np.ones((cc.rows, 2))).shape == (0, 2)
