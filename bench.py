@@ -259,24 +259,54 @@ def full_cpu_pair(cfg):
     return float(column_costs(cfg.grid, rank_table(cfg, SEED), cfg.p).sum()) < 2e11
 
 
+def sample_columns(cfg, ranks, n):
+    """The CPU legs' column sample: the n columns whose per-column madd count is
+    closest to the median, in column order.  A sample of near-equal columns
+    keeps the W workers of the timed rounds equally busy, as the whole store's
+    thousands of columns do under the reference's dynamic column queue
+    (src/matvec.cpp:34,40-42); the first n columns (ranks varying 9-12 at
+    config 4) left workers idle at the end of every round and overestimated
+    the adjoint by ~25 %."""
+    from paper_2103_06393_b200.sharded import column_costs
+    costs = column_costs(cfg.grid, ranks, cfg.p)
+    n = min(int(n), len(costs))
+    return np.sort(np.argsort(np.abs(costs - np.median(costs)), kind="stable")[:n])
+
+
+def column_payload(cfg, ranks, payload, cols):
+    """The payload slices of columns `cols` (all q components each), concatenated
+    (numpy or torch payload of the whole store, [col][comp] tensor order)."""
+    from paper_2103_06393_b200.workloads import tensor_offsets
+    off = tensor_offsets(cfg.grid, ranks)
+    q = cfg.q
+    parts = [payload[int(off[j * q]):int(off[(j + 1) * q])] for j in cols]
+    if isinstance(payload, np.ndarray):
+        return np.concatenate(parts)
+    import torch
+    return torch.cat(parts)
+
+
 def cpu_sample(cfg, ranks, host_payload_fn, x_full, phi_full, ncols_sample, workers, kind="port", fixed=None):
-    """Time the reference's forward + adjoint (src/matvec.cpp:17-102) on the
-    first `ncols_sample` columns with `workers` host threads, and scale to the
-    whole store by the algorithmic madd count.  With `fixed` (the forward's
-    fixed partial-sum cost from an earlier two-point call) one round of W
-    columns is timed per call (the reference arm's timed steps)."""
+    """Time the reference's forward + adjoint (src/matvec.cpp:17-102) on a
+    balanced sample of `ncols_sample` columns (sample_columns) with `workers`
+    host threads, and scale to the whole store by the algorithmic madd count.
+    host_payload_fn(sel) returns the payload of columns `sel`.  With `fixed`
+    (the forward's fixed partial-sum cost from an earlier two-point call) one
+    round of W columns is timed per call (the reference arm's timed steps)."""
     from paper_2103_06393_b200.sharded import column_costs
 
     from paper_2103_06393_b200.workloads import tensor_offsets
 
-    pay = host_payload_fn(ncols_sample)  # complex128 (already c64-rounded values)
-    costs = column_costs(cfg.grid, ranks, cfg.p)
+    sel = sample_columns(cfg, ranks, ncols_sample)
+    pay = host_payload_fn(sel)  # complex128 (already c64-rounded values)
+    costs_all = column_costs(cfg.grid, ranks, cfg.p)
+    rs, costs, xs = ranks[sel], costs_all[sel], x_full[sel]
 
     def timed_forward(nc):
-        off = tensor_offsets(cfg.grid, ranks[:nc])
-        st = ref_store(kind, cfg, ranks[:nc], pay[: int(off[-1])])
+        off = tensor_offsets(cfg.grid, rs[:nc])
+        st = ref_store(kind, cfg, rs[:nc], pay[: int(off[-1])])
         t0 = time.perf_counter()
-        st.forward(np.asfortranarray(x_full[:nc]), workers)
+        st.forward(np.asfortranarray(xs[:nc]), workers)
         return time.perf_counter() - t0, st
 
     # stacked_forward with W workers = a fixed cost (zeroing and serially
@@ -296,11 +326,11 @@ def cpu_sample(cfg, ranks, host_payload_fn, x_full, phi_full, ncols_sample, work
         tb, st = timed_forward(n2)
         cb = costs[:n2].sum()
         rate = cb / max(tb - fixed, 1e-9)
-    fwd_full = fixed + costs.sum() / rate
+    fwd_full = fixed + costs_all.sum() / rate
     t1 = time.perf_counter()
     st.adjoint(phi_full, workers)
     t2 = time.perf_counter()
-    scale = float(costs.sum() / cb)
+    scale = float(costs_all.sum() / cb)
     return {"fwd_s": fwd_full, "adj_s": (t2 - t1) * scale, "scale": scale, "fwd_fixed_s": fixed}
 
 
@@ -395,18 +425,19 @@ def run_reference(args):
                 times.append((r["fwd_s"] + r["adj_s"]) * 1e3)
         sample = f"the whole product pair ({cfg.m} columns x {cfg.q} components, p = {cfg.p}) with {W} worker threads"
     else:
-        pay = _numpy_synthetic(cfg, ranks[:ncs], scales[:ncs], SEED)
+        sel = sample_columns(cfg, ranks, ncs)
+        pay = _numpy_synthetic(cfg, ranks[sel], scales[sel], SEED)
         fixed, fixes = None, []
         for s in range(args.warmup + args.steps):
             # warm-up steps calibrate the forward's fixed partial-sum cost (W and 2W
             # columns); each timed step then runs one round of W columns
-            r = cpu_sample(cfg, ranks, lambda nc: pay, x, phi, ncs, W, kind, None if s < args.warmup else fixed)
+            r = cpu_sample(cfg, ranks, lambda sel_: pay, x, phi, ncs, W, kind, None if s < args.warmup else fixed)
             if s < args.warmup:
                 fixes.append(r["fwd_fixed_s"])
                 fixed = statistics.median(fixes)
             else:
                 times.append((r["fwd_s"] + r["adj_s"]) * 1e3)
-        sample = (f"per step the forward on {ncs} of {cfg.m} columns (all q={cfg.q} components, two rounds of {W} "
+        sample = (f"per step the forward on {ncs} of {cfg.m} columns (the median-cost ones, all q={cfg.q} components, two rounds of {W} "
                   f"worker threads), extrapolated as the fixed partial-sum cost (median of the warm-up steps' "
                   f"two-point fits on {W} and {ncs} columns) + the per-round rate; the adjoint on {ncs} columns "
                   f"scaled by the madd count")
@@ -536,9 +567,8 @@ def main():
         else:
             W = cpu_workers(cfg, 32)
             ncs = min(args.cpu_cols or 2 * W, c1 - c0)
-            from paper_2103_06393_b200.workloads import tensor_offsets
-            off = tensor_offsets(cfg.grid, ranks[:ncs])
-            cpu_pay = pay[: int(off[-1])].to(cdt).to(torch.complex128).cpu().numpy()
+            sel = sample_columns(cfg, ranks, ncs)
+            cpu_pay = column_payload(cfg, ranks, pay, sel).to(cdt).to(torch.complex128).cpu().numpy()
     if not rows_mode:
         del pay
     torch.cuda.synchronize()
@@ -758,8 +788,8 @@ def main():
         else:
             W = cpu_workers(cfg, 32)
             ncs = min(args.cpu_cols or 2 * W, c1 - c0)
-            r = cpu_sample(cfg, ranks, lambda nc: cpu_pay, x_host.astype(np.complex128), phi_h, ncs, W, kind)
-            sample = (f"forward timed on {W} and {ncs} of {cfg.m} columns (all {cfg.q} components) with {W} worker "
+            r = cpu_sample(cfg, ranks, lambda sel_: cpu_pay, x_host.astype(np.complex128), phi_h, ncs, W, kind)
+            sample = (f"forward timed on {W} and {ncs} of {cfg.m} columns (the median-cost ones, all {cfg.q} components) with {W} worker "
                       f"threads, extrapolated as fixed partial-sum cost + per-round rate; adjoint on {ncs} columns "
                       f"scaled x{r['scale']:.1f} by the madd count")
             extra = {"extrapolated": True, "fwd_fixed_ms": round(r["fwd_fixed_s"] * 1e3, 1)}

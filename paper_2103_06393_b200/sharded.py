@@ -233,10 +233,10 @@ def slice_payload_rows(dims, ranks, payload, a, b):
     length = np.where(is_core, c0, np.where(is_tail, n2 * r[t_of, 1] + n3 * r[t_of, 2], h))
     total = int(length.sum())
     idx = np.repeat(start - (np.cumsum(length) - length), length) + np.arange(total)
-    if hasattr(payload, "device"):  # torch
-        import torch
-        return payload[torch.from_numpy(idx).to(payload.device)]
-    return np.asarray(payload)[idx]
+    if isinstance(payload, np.ndarray):
+        return payload[idx]
+    import torch  # a torch tensor (the bench slices its device payload)
+    return payload[torch.from_numpy(idx).to(payload.device)]
 
 
 class RowShardedStore:

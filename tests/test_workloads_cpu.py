@@ -1,6 +1,7 @@
 """Benchmark workload definitions (BASELINE.json configs) on CPU."""
 import numpy as np
 
+from conftest import ROOT
 from paper_2103_06393_b200.sharded import column_costs
 from paper_2103_06393_b200.workloads import CONFIGS, rank_table, synthetic_payload, tensor_offsets
 
@@ -58,3 +59,29 @@ def test_synthetic_payload_layout_cpu(oracle):
         core, u1, u2, u3 = oracle.split_tensor(cfg.grid, ranks.reshape(-1, 3)[i], p[off[i]:off[i + 1]])
         for u in (u1, u2, u3):
             assert np.linalg.norm(u.conj().T @ u - np.eye(u.shape[1])) < 1e-12
+
+
+def test_cpu_sample_columns_are_balanced_and_cover_the_payload():
+    """The CPU legs' column sample (bench.sample_columns): n distinct columns
+    in order, per-column madds within a narrow band around the median; and
+    bench.column_payload returns exactly those columns' tensors."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench as B
+    from paper_2103_06393_b200.sharded import column_costs
+    from paper_2103_06393_b200.workloads import CONFIGS, rank_table, tensor_offsets
+    cfg = CONFIGS["c4"]
+    ranks = rank_table(cfg, 1234)
+    costs = column_costs(cfg.grid, ranks, cfg.p)
+    sel = B.sample_columns(cfg, ranks, 32)
+    assert len(set(sel.tolist())) == 32 and np.all(np.diff(sel) > 0)
+    med = np.median(costs)
+    assert np.abs(costs[sel] - med).max() <= np.abs(costs - med).max() * 0.1
+    small = CONFIGS["c1"]
+    r1 = rank_table(small, 1234)
+    off = tensor_offsets(small.grid, r1)
+    pay = np.arange(off[-1]).astype(np.complex128)
+    sel1 = B.sample_columns(small, r1, 5)
+    got = B.column_payload(small, r1, pay, sel1)
+    want = np.concatenate([pay[off[j * small.q]:off[(j + 1) * small.q]] for j in sel1])
+    assert np.array_equal(got, want)

@@ -105,10 +105,8 @@ def main():
         # the sample model bench.py's reference arm uses (W and 2W columns, adjoint scaled)
         if v is None:
             ncs = min(2 * W, cfg.m)
-            from paper_2103_06393_b200.workloads import tensor_offsets
-            off = tensor_offsets(cfg.grid, ranks[:ncs])
-            samp = B.cpu_sample(cfg, ranks, lambda nc: host[: int(off[-1])], x, np.asfortranarray(phi), ncs, W,
-                                kind="reference")
+            samp = B.cpu_sample(cfg, ranks, lambda sel: B.column_payload(cfg, ranks, host, sel), x,
+                                np.asfortranarray(phi), ncs, W, kind="reference")
             pred = samp["fwd_s"] + samp["adj_s"]
             line["sample_model"] = {"columns": ncs, "forward_s": round(samp["fwd_s"], 3),
                                     "adjoint_s": round(samp["adj_s"], 3), "pair_s": round(pred, 3),
