@@ -290,9 +290,11 @@ def cpu_sample(cfg, ranks, host_payload_fn, x_full, phi_full, ncols_sample, work
     """Time the reference's forward + adjoint (src/matvec.cpp:17-102) on a
     balanced sample of `ncols_sample` columns (sample_columns) with `workers`
     host threads, and scale to the whole store by the algorithmic madd count.
-    host_payload_fn(sel) returns the payload of columns `sel`.  With `fixed`
-    (the forward's fixed partial-sum cost from an earlier two-point call) one
-    round of W columns is timed per call (the reference arm's timed steps)."""
+    host_payload_fn(sel) returns the payload of columns `sel`.  Both products
+    are modelled as a fixed per-call cost + rounds of W columns at a constant
+    rate, fitted on W and 2W columns; with `fixed` ({"fwd": s, "adj": s} from
+    earlier calls) only the 2W-column store is timed (the reference arm's
+    timed steps)."""
     from paper_2103_06393_b200.sharded import column_costs
 
     from paper_2103_06393_b200.workloads import tensor_offsets
@@ -309,29 +311,42 @@ def cpu_sample(cfg, ranks, host_payload_fn, x_full, phi_full, ncols_sample, work
         st.forward(np.asfortranarray(xs[:nc]), workers)
         return time.perf_counter() - t0, st
 
+    def timed_adjoint(st):
+        t0 = time.perf_counter()
+        st.adjoint(phi_full, workers)
+        return time.perf_counter() - t0
+
     # stacked_forward with W workers = a fixed cost (zeroing and serially
     # summing the W rows x p partials, src/matvec.cpp:30-38,58-59) + rounds of
-    # W columns in parallel.  Time W and 2W columns with the same W workers:
-    # the difference is one round of column work at full thread occupancy.
+    # W columns in parallel; stacked_adjoint = a fixed per-call cost (the
+    # q n_v x p Phi block handed over, the output) + rounds of W columns.  Time
+    # W and 2W columns with the same W workers: the difference is one round of
+    # column work at full thread occupancy.
+    def fit(ta, tb, ca, cb, fx):
+        if fx is not None:  # two rounds of W columns against the calibrated fixed cost
+            rate = cb / max(tb - fx, 1e-9)
+            return rate, fx
+        rate = (cb - ca) / max(tb - ta, 1e-9) if cb > ca else cb / tb  # madds per second, all workers
+        return rate, max(ta - ca / rate, 0.0)
+
     W = workers
     n1, n2 = min(W, ncols_sample), min(2 * W, ncols_sample)
+    ca, cb = costs[:n1].sum(), costs[:n2].sum()
     if fixed is None:
-        ta, _ = timed_forward(n1)
-        ca = costs[:n1].sum()
+        ta, st_a = timed_forward(n1)
         tb, st = timed_forward(n2)
-        cb = costs[:n2].sum()
-        rate = (cb - ca) / max(tb - ta, 1e-9) if n2 > n1 else ca / ta  # madds per second, all workers
-        fixed = max(ta - ca / rate, 0.0)
-    else:  # two rounds of W columns against the calibrated fixed cost
+        aa, ab = timed_adjoint(st_a), timed_adjoint(st)
+        del st_a
+        rf, ff = fit(ta, tb, ca, cb, None)
+        ra, fa = fit(aa, ab, ca, cb, None)
+    else:
         tb, st = timed_forward(n2)
-        cb = costs[:n2].sum()
-        rate = cb / max(tb - fixed, 1e-9)
-    fwd_full = fixed + costs_all.sum() / rate
-    t1 = time.perf_counter()
-    st.adjoint(phi_full, workers)
-    t2 = time.perf_counter()
-    scale = float(costs_all.sum() / cb)
-    return {"fwd_s": fwd_full, "adj_s": (t2 - t1) * scale, "scale": scale, "fwd_fixed_s": fixed}
+        ab = timed_adjoint(st)
+        rf, ff = fit(None, tb, ca, cb, fixed["fwd"])
+        ra, fa = fit(None, ab, ca, cb, fixed["adj"])
+    total = costs_all.sum()
+    return {"fwd_s": ff + total / rf, "adj_s": fa + total / ra, "scale": float(total / cb), "fwd_fixed_s": ff,
+            "adj_fixed_s": fa}
 
 
 def cpu_full(cfg, ranks, payload, v, x, phi, workers, kind, repeats=1):
@@ -427,20 +442,21 @@ def run_reference(args):
     else:
         sel = sample_columns(cfg, ranks, ncs)
         pay = _numpy_synthetic(cfg, ranks[sel], scales[sel], SEED)
-        fixed, fixes = None, []
+        fixed, fixes, afixes = None, [], []
         for s in range(args.warmup + args.steps):
             # warm-up steps calibrate the forward's fixed partial-sum cost (W and 2W
             # columns); each timed step then runs one round of W columns
             r = cpu_sample(cfg, ranks, lambda sel_: pay, x, phi, ncs, W, kind, None if s < args.warmup else fixed)
             if s < args.warmup:
                 fixes.append(r["fwd_fixed_s"])
-                fixed = statistics.median(fixes)
+                afixes.append(r["adj_fixed_s"])
+                fixed = {"fwd": statistics.median(fixes), "adj": statistics.median(afixes)}
             else:
                 times.append((r["fwd_s"] + r["adj_s"]) * 1e3)
         sample = (f"per step the forward on {ncs} of {cfg.m} columns (the median-cost ones, all q={cfg.q} components, two rounds of {W} "
-                  f"worker threads), extrapolated as the fixed partial-sum cost (median of the warm-up steps' "
-                  f"two-point fits on {W} and {ncs} columns) + the per-round rate; the adjoint on {ncs} columns "
-                  f"scaled by the madd count")
+                  f"worker threads) and the adjoint on the same {ncs} columns, each extrapolated as its fixed "
+                  f"per-call cost (median of the warm-up steps' two-point fits on {W} and {ncs} columns) + the "
+                  f"per-round rate x the store's madd count")
     ms = statistics.median(times)
     line = {
         "impl": "reference", "metric": metric_name(cfg), "value": round(ms, 1), "unit": "ms", "n_gpus": 0,
@@ -790,9 +806,10 @@ def main():
             ncs = min(args.cpu_cols or 2 * W, c1 - c0)
             r = cpu_sample(cfg, ranks, lambda sel_: cpu_pay, x_host.astype(np.complex128), phi_h, ncs, W, kind)
             sample = (f"forward timed on {W} and {ncs} of {cfg.m} columns (the median-cost ones, all {cfg.q} components) with {W} worker "
-                      f"threads, extrapolated as fixed partial-sum cost + per-round rate; adjoint on {ncs} columns "
-                      f"scaled x{r['scale']:.1f} by the madd count")
-            extra = {"extrapolated": True, "fwd_fixed_ms": round(r["fwd_fixed_s"] * 1e3, 1)}
+                      f"threads, and the adjoint likewise, each extrapolated as a fixed per-call cost + the per-round rate "
+                      f"(two-point fit on {W} and {ncs} columns) x the store's madd count")
+            extra = {"extrapolated": True, "fwd_fixed_ms": round(r["fwd_fixed_s"] * 1e3, 1),
+                     "adj_fixed_ms": round(r["adj_fixed_s"] * 1e3, 1)}
             fm = full_measurement(cfg)
             if fm:
                 extra["full_size_measurement"] = {"pair_ms": round(fm["pair_s"] * 1e3, 1), "workers": fm["workers"],

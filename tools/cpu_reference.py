@@ -57,6 +57,8 @@ def main():
     ap.add_argument("--repeats", type=int, default=3)
     ap.add_argument("--out", default="gpurun_out/cpu_full.jsonl")
     ap.add_argument("--workers", type=int, default=0)
+    ap.add_argument("--sample-only", default="",
+                    help="skip the full run: compare the sample model with the full measurement in this jsonl file")
     args = ap.parse_args()
     import torch
     import bench as B
@@ -87,6 +89,9 @@ def main():
             phi = r64(cn01(rows, cfg.p, SEED + 1))
             reps = 1 if name == "c4" else args.repeats
             tf, ta = [], []
+            if args.sample_only:
+                prev = [json.loads(ln) for ln in open(args.sample_only) if json.loads(ln)["config"] == cfg.name]
+                tf, ta, reps = [prev[-1]["forward_s"]], [prev[-1]["adjoint_s"]], 0
             for _ in range(reps):
                 s = time.perf_counter()
                 y = ref.aca_forward(x, W) if v is not None else ref.forward(x, W)
@@ -100,15 +105,18 @@ def main():
         line = {"config": cfg.name, "kind": "reference", "impl": "oracle/_ref (proj/src compiled unchanged)",
                 "forward_s": round(statistics.median(tf), 3), "adjoint_s": round(statistics.median(ta), 3),
                 "pair_s": round(statistics.median(tf) + statistics.median(ta), 3), "repeats": reps,
+                "full_from": args.sample_only or "this run",
                 "forward_runs_s": [round(t, 3) for t in tf], "adjoint_runs_s": [round(t, 3) for t in ta],
                 "workers": W, "nproc": os.cpu_count(), "cpu": cpu_model(), "store_build_s": round(t_build, 1)}
-        # the sample model bench.py's reference arm uses (W and 2W columns, adjoint scaled)
+        # the sample model of bench.py's CPU legs (W and 2W median-cost columns, two-point fits)
         if v is None:
             ncs = min(2 * W, cfg.m)
             samp = B.cpu_sample(cfg, ranks, lambda sel: B.column_payload(cfg, ranks, host, sel), x,
                                 np.asfortranarray(phi), ncs, W, kind="reference")
             pred = samp["fwd_s"] + samp["adj_s"]
             line["sample_model"] = {"columns": ncs, "forward_s": round(samp["fwd_s"], 3),
+                                    "fwd_fixed_s": round(float(samp["fwd_fixed_s"]), 3),
+                                    "adj_fixed_s": round(float(samp.get("adj_fixed_s", 0.0)), 3),
                                     "adjoint_s": round(samp["adj_s"], 3), "pair_s": round(pred, 3),
                                     "rel_error_vs_full": round(pred / line["pair_s"] - 1.0, 4)}
         print(json.dumps(line), flush=True)
