@@ -152,6 +152,11 @@ struct tm_store {
     TcDesc* d_tcd = nullptr;  // [q*ncols] tensor-core descriptors
     float2* d_varena = nullptr;  // mode-1 products V = U1 x_1 G
     float2* d_u2arena = nullptr;  // U2 with odd row strides
+    // W arena (W = V x_2 U2 as the forward's fp16-split A operand, built when it
+    // fits the memory budget: the forward then runs without producer warps)
+    __half* d_warena = nullptr;
+    int64_t warena_rows = 0;
+    CUtensorMap warena_map{};
     // tensor-core adjoint: chunk-aligned, i3-contiguous U3 planes
     bool tca_ok = false;
     __half* d_aplanes = nullptr;
@@ -197,6 +202,7 @@ struct tm_store {
         if (d_tcd) cudaFree(d_tcd);
         if (d_varena) cudaFree(d_varena);
         if (d_u2arena) cudaFree(d_u2arena);
+        if (d_warena) cudaFree(d_warena);
         if (d_aplanes) cudaFree(d_aplanes);
         for (auto& a : adjp) {
             if (a.d_aplanes) cudaFree(a.d_aplanes);
@@ -243,6 +249,43 @@ int tc_chain() {
     // accumulator through red.global.add, so longer chains cost less (24 -> 32:
     // -3.5 % forward time per SM clock, same box)
     return v > 0 ? v : 32;
+}
+
+bool warena_disabled() {
+    const char* e = std::getenv("TMB_WARENA");
+    return e && *e == '0';
+}
+
+// The W arena: W = V x_2 U2 of every tensor as the forward's fp16-split A
+// operand, precomputed once (build_warena_kernel) when it fits
+// $TMB_WARENA_GB (default 24 GB) and half of the free device memory — small
+// and medium grids (configs 2, 3, 5: 0.7 / 1.1 / 2.6 GB), not config 4
+// (~220 GB).  The forward then streams A by TMA like B, with no producer
+// warps; the adjoint keeps the V arena.  TMB_WARENA=0 disables it.
+void build_warena(tm_store* s) {
+    if (warena_disabled() || s->ncols == 0) return;
+    const int nt1 = int((s->dims[0] + TC_TI1 - 1) / TC_TI1), nt2 = int((s->dims[1] + TC_TI2 - 1) / TC_TI2);
+    const int64_t rows_pad = int64_t(nt1) * nt2 * TC_ROWS;
+    const size_t bytes = size_t(4) * s->q * size_t(rows_pad) * size_t(s->kpad) * sizeof(__half);
+    double cap_gb = 24.0;
+    if (const char* e = std::getenv("TMB_WARENA_GB")) cap_gb = std::atof(e);
+    size_t freeb = 0, total = 0;
+    CK(cudaMemGetInfo(&freeb, &total));
+    if (double(bytes) > cap_gb * 1e9 || bytes > freeb / 2 || nt1 * nt2 > 65535 || rows_pad >= (int64_t(1) << 31))
+        return;
+    CK(cudaMalloc(&s->d_warena, bytes));
+    CK(cudaMemset(s->d_warena, 0, bytes));
+    const int64_t ntens = s->ncols * s->q;
+    build_warena_kernel<<<dim3(unsigned(ntens), unsigned(nt1 * nt2)), TC_ROWS>>>(
+        s->d_tcd, s->d_varena, s->d_u2arena, s->d_kofs, s->ncols, s->q, int(s->dims[0]), int(s->dims[1]), nt2,
+        rows_pad, s->kpad, fp16_scale(s->vmax * 1.0001f), s->d_warena);
+    launched(cudaSuccess, "build_warena_kernel");
+    CK(cudaDeviceSynchronize());
+    s->warena_rows = rows_pad;
+    s->warena_map = make_tmap_3d_f16(s->d_warena, uint64_t(s->kpad), uint64_t(rows_pad), uint64_t(4 * s->q),
+                                     uint64_t(s->kpad) * 2, uint64_t(rows_pad) * s->kpad * 2, 16, TC_ROWS,
+                                     CU_TENSOR_MAP_SWIZZLE_32B);
+    s->device_bytes += int64_t(bytes);
 }
 
 // B planes of the tensor-core forward (see tm_kernels_tc.cuh), built once.
@@ -371,6 +414,7 @@ void build_tc(tm_store* s, const std::vector<TDesc>& desc) {
     }
     s->device_bytes += int64_t(vbytes + u2bytes + abytes + tcd.size() * sizeof(TcDesc) + (kofs.size() + kc.size()) * sizeof(int));
     s->tc_ok = true;
+    build_warena(s);
 }
 
 void build_store(tm_store* s, const tm_store_desc& d, const tmb_io::PayloadFill* fill = nullptr) {
@@ -796,12 +840,14 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
         const char* dbg = std::getenv("TMB_TC_DEBUG");
         g.debug = dbg ? std::atoi(dbg) : 0;
     }
+    // W arena (build_warena): A by TMA, no producers and no factor slots
+    const bool wa = s->d_warena && !warena_disabled();
     auto smem_for = [&](int nst) {
-        return 1024 + size_t(nst) * (TC_A_STAGE + g.b_stage) + size_t(TC_JR) * g.slot_bytes +
+        return 1024 + size_t(nst) * (TC_A_STAGE + g.b_stage) + (wa ? 0 : size_t(TC_JR) * g.slot_bytes) +
                (2 * TC_NST_MAX + 2 * TC_JR + 2) * 8 + 16;
     };
     // a column opens up to ceil((15 + r3) / 16) A stages at once: 2 for r3 <= 16, 3 up to TC_RMAX
-    const int nst_min = s->rmax[2] > 16 ? 3 : 2;
+    const int nst_min = (s->rmax[2] > 16 && !wa) ? 3 : 2;
     g.nst = TC_NST_MAX;
     if (const char* e = std::getenv("TMB_TC_NST")) if (std::atoi(e) >= 2) g.nst = std::min(TC_NST_MAX, std::atoi(e));
     g.nst = std::max(g.nst, nst_min);
@@ -809,8 +855,8 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
     const size_t smem = smem_for(g.nst);
     if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "tensor-core forward: shared-memory plan too large");
     const bool big = s->rmax[2] > 16;  // the r3 <= 32 instantiations
-    auto kfpair = big ? fwd_tc_kernel<true, true> : fwd_tc_kernel<true>;
-    auto kfsingle = big ? fwd_tc_kernel<false, true> : fwd_tc_kernel<false>;
+    auto kfpair = wa ? fwd_tc_kernel<true, false, true> : (big ? fwd_tc_kernel<true, true> : fwd_tc_kernel<true>);
+    auto kfsingle = wa ? fwd_tc_kernel<false, false, true> : (big ? fwd_tc_kernel<false, true> : fwd_tc_kernel<false>);
     CK(cudaFuncSetAttribute(kfsingle, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     CK(cudaFuncSetAttribute(kfpair, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // grid: CTAs; a wave covers `wave` tiles (pair tiles in pair mode)
@@ -882,14 +928,16 @@ void run_forward_pass(const tm_store* s, const float2* x, int64_t ldx, int64_t p
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            launched(cudaLaunchKernelEx(&cfg, kfpair, bmap, static_cast<const TcDesc*>(s->d_tcd),
+            launched(cudaLaunchKernelEx(&cfg, kfpair, bmap, wa ? s->warena_map : bmap,
+                                        static_cast<const TcDesc*>(s->d_tcd),
                                         static_cast<const float2*>(s->d_varena),
                                         static_cast<const float2*>(s->d_u2arena), static_cast<const int*>(s->d_kc),
                                         static_cast<const int*>(s->d_kofs), g, x, ldx, y, ldy, rsum,
                                         static_cast<const float*>(wmax)),
                      "fwd_tc_kernel<pair>");
         } else {
-            kfsingle<<<grid, TC_THREADS, smem, st>>>(bmap, s->d_tcd, s->d_varena, s->d_u2arena,
+            kfsingle<<<grid, TC_THREADS, smem, st>>>(bmap, wa ? s->warena_map : bmap, s->d_tcd, s->d_varena,
+                                                     s->d_u2arena,
                                                                   s->d_kc, s->d_kofs, g, x, ldx, y, ldy, rsum, wmax);
             launched(cudaSuccess, "fwd_tc_kernel");
         }
@@ -1595,7 +1643,7 @@ TM_API int tm_store_kernels(const tm_store* s, int32_t* forward_tc, int32_t* adj
     return guarded([&] {
         if (!s) contract("null store");
         const bool off = tc_disabled();
-        if (forward_tc) *forward_tc = (s->tc_ok && !off) ? 1 : 0;
+        if (forward_tc) *forward_tc = (s->tc_ok && !off) ? (s->d_warena && !warena_disabled() ? 2 : 1) : 0;
         if (adjoint_tc) *adjoint_tc = (s->tca_ok && !off && adj_tc_fits(s)) ? 1 : 0;
     });
 }

@@ -201,9 +201,20 @@ __host__ __device__ inline TcTile tc_tile(const TcGeom& g, int64_t item, uint32_
 
 // Column range [j0, j1) of a work item and its packed-K range [ka, kb) in
 // the component's K stream (kofs: component-major K offsets, kc: K per
-// component); the item runs stages [ka / 16, ceil(kb / 16)).
+// component); the item runs stages [ka / 16, ceil(kb / 16)).  WA (the
+// W-arena forward): parts are cut at stage boundaries instead (j0 / j1 unused).
+template <bool WA = false>
 __device__ __forceinline__ void tc_range(const TcGeom& g, const TcTile& tl, const int* __restrict__ kofs,
                                          const int* __restrict__ kc, int& j0, int& j1, uint32_t& ka, uint32_t& kb) {
+    if (WA && g.split > 1) {
+        const uint32_t kk = uint32_t(kc[tl.k]), ns = (kk + 15u) >> 4;
+        const uint32_t s0 = uint32_t(uint64_t(ns) * tl.part / g.split);
+        const uint32_t s1 = uint32_t(uint64_t(ns) * (tl.part + 1) / g.split);
+        j0 = j1 = 0;
+        ka = s0 * 16u;
+        kb = s1 == ns ? kk : s1 * 16u;
+        return;
+    }
     if (g.split == 1) {  // the common case: the whole column stream
         j0 = 0;
         j1 = int(g.ncols);
@@ -336,9 +347,15 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
 
 // BIG: stores with r3 > 16 (up to TC_RMAX = 32); the default instantiation
 // keeps the r3 <= 16 dispatch (fewer registers, smaller code).
-template <bool PAIR, bool BIG = false>
+// WA: the A operand W = V x_2 U2 comes precomputed from the store's W arena
+// by TMA (build_warena_kernel; stores whose W fits the memory budget) — no
+// producer warps, no factor ring; the tile's K range is cut at stage
+// boundaries for split items (a column's r3 slots may straddle parts: the
+// sum over K is linear).
+template <bool PAIR, bool BIG = false, bool WA = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    fwd_tc_kernel(const __grid_constant__ CUtensorMap bmap, const TcDesc* __restrict__ tcd,
+    fwd_tc_kernel(const __grid_constant__ CUtensorMap bmap, const __grid_constant__ CUtensorMap amap,
+                  const TcDesc* __restrict__ tcd,
                   const float2* __restrict__ varena, const float2* __restrict__ u2arena, const int* __restrict__ kc,
                   const int* __restrict__ kofs, TcGeom g, const float2* __restrict__ x, int64_t ldx, float2* __restrict__ y, int64_t ldy,
                   float2* __restrict__ rsum, const float* __restrict__ wmax) {
@@ -351,7 +368,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     unsigned char* sA = sm;
     unsigned char* sB = sA + nst * TC_A_STAGE;
     unsigned char* sSlot = sB + nst * g.b_stage;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sSlot + TC_JR * g.slot_bytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sSlot + (WA ? 0 : TC_JR * g.slot_bytes));  // WA: no factor ring
     uint64_t* full = bars;                 // [nst]
     uint64_t* empty = full + TC_NST_MAX;   // [nst]
     uint64_t* ffull = empty + TC_NST_MAX;  // [JR]
@@ -370,7 +387,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int64_t tstep = PAIR ? (gridDim.x >> 1) : gridDim.x;
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < nst; ++s) {
-            mbar_init(&full[s], 1 + TC_NPW * (PAIR ? 2 : 1));
+            mbar_init(&full[s], WA ? 1 : 1 + TC_NPW * (PAIR ? 2 : 1));
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < TC_JR; ++s) {
@@ -406,13 +423,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             rec = true;
             uint32_t s = 0, ph = 0;
             const int plane_bytes = g.nmma * 32;
+            // WA: the tile's A rows in the W arena (tile-major: [i1 / 4][i2 / 32][128 rows])
+            constexpr uint32_t a_bytes = WA ? uint32_t(TC_A_STAGE) : 0u;
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
                 const TcTile tl = tc_tile(g, t, rank);
                 int j0, j1;
                 uint32_t ka, kb;
-                tc_range(g, tl, kofs, kc, j0, j1, ka, kb);
+                tc_range<WA>(g, tl, kofs, kc, j0, j1, ka, kb);
+                const int arow = ((tl.i1_0 / TC_TI1) * g.nt2 + tl.i2_0 / TC_TI2) * TC_ROWS;
                 for (int kk = int(ka >> 4); kk < int((kb + 15) >> 4); ++kk) {
                     TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(&empty[s], ph ^ 1, 128)));
+                    if constexpr (WA) {  // A: this CTA's 128 rows x 16 K of the 4 W planes
+                        unsigned char* da = sA + s * TC_A_STAGE;
+                        if (PAIR) {
+                            const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+#pragma unroll
+                            for (int pl = 0; pl < 4; ++pl)
+                                tma_load_3d_pair(da + pl * TC_A_PLANE, &amap, fb, kk * 16, arow, pl * g.q + tl.k);
+                        } else {
+#pragma unroll
+                            for (int pl = 0; pl < 4; ++pl)
+                                tma_load_3d(da + pl * TC_A_PLANE, &amap, &full[s], kk * 16, arow, pl * g.q + tl.k);
+                        }
+                    }
                     if (PAIR) {
                         // each CTA loads its half of the i3 span (B rows [rank nmma, +nmma) of the
                         // M = 256 MMA); the bytes of both halves complete on rank 0's barrier
@@ -420,7 +453,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             if (g.debug & 2)
                                 mbar_arrive(&full[s]);
                             else
-                                mbar_arrive_expect_tx(&full[s], 2u * uint32_t(g.b_stage));
+                                mbar_arrive_expect_tx(&full[s], 2u * (uint32_t(g.b_stage) + a_bytes));
                         }
                         if (!(g.debug & 2)) {
                             unsigned char* dst = sB + s * g.b_stage;
@@ -433,7 +466,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     } else if (g.debug & 2) {
                         mbar_arrive(&full[s]);
                     } else {
-                        mbar_arrive_expect_tx(&full[s], uint32_t(g.b_stage));
+                        mbar_arrive_expect_tx(&full[s], uint32_t(g.b_stage) + a_bytes);
                         unsigned char* dst = sB + s * g.b_stage;
                         // smem plane pl = (Br hi, Bi hi, Br lo, Bi lo) holds both halves of the
                         // tile's N rows contiguously ([pl][hh][nmma rows])
@@ -467,7 +500,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const TcTile tl = tc_tile(g, t, rank);
                 int j0, j1;
                 uint32_t ka, kb;
-                tc_range(g, tl, kofs, kc, j0, j1, ka, kb);
+                tc_range<WA>(g, tl, kofs, kc, j0, j1, ka, kb);
                 const int nks = int((kb + 15) >> 4) - int(ka >> 4);
                 int cpos = 0;  // stage position inside the current chain
                 for (int kk = 0; kk < nks; ++kk) {
@@ -519,7 +552,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #undef MMA
 #undef COMMIT
         __syncwarp();
-    } else if (warp == 2) {
+    } else if (warp == 2 && !WA) {
         // ---------------------------------------------------- factor loader
         if (elect_one()) {
             rec = true;
@@ -549,7 +582,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 }
             }
         }
-    } else if (warp >= TC_PW0 && warp < TC_FW0) {
+    } else if (!WA && warp >= TC_PW0 && warp < TC_FW0) {
         static_assert(TC_NH * 8 >= TC_RMAX, "producer switch covers ceil(TC_RMAX / TC_NH)");
         // ------------------------------------------------------ A producers
         // warp pw: i1 = pw / (4 / NR) (warp-uniform), rows i2 in a block of 8 NR;
@@ -679,7 +712,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const TcTile tl = tc_tile(g, t, rank);
             int j0, j1;
             uint32_t ka, kb;
-            tc_range(g, tl, kofs, kc, j0, j1, ka, kb);
+            tc_range<WA>(g, tl, kofs, kc, j0, j1, ka, kb);
             const int nks = int((kb + 15) >> 4) - int(ka >> 4);
             const int nch = (nks + g.chain - 1) / g.chain;
             const int ei1 = tl.i1_0 + quarter, ei2 = tl.i2_0 + lane;
@@ -705,6 +738,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 }
                 yp[ldy * c + pl * i3] = v;
             };
+            if (WA && nch == 0) {
+                // an empty K range (a split item of the W-arena forward with fewer
+                // K stages than parts): its partial tile is zero
+                if (part_out)
+                    for (int nl = 0; nl < span; ++nl) put(nl, make_float2(0.f, 0.f));
+                continue;
+            }
             for (int ch = 0; ch < nch; ++ch, ++gch) {
                 TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(cfull, gch & 1, 256)));
                 tc_fence_after();
@@ -941,6 +981,47 @@ __global__ void build_u2_kernel(const TDesc* __restrict__ td, const float2* __re
         const int i2 = e / ld2, b = e - i2 * ld2;
         const float2 u = (i2 < n2 && b < d.r2) ? arena[d.off_u2 + int64_t(i2) * d.r2 + b] : make_float2(0.f, 0.f);
         out[e] = make_float2(ldexpf(u.x, -e2), ldexpf(u.y, -e2));  // normalised U2 (row norms <= 1), exact
+    }
+}
+
+// ------------------------------------------ store-side W arena (WA forward)
+// W = V x_2 U2 of every tensor, scaled by the forward's A scale wsc and split
+// into the A operand's 4 fp16 planes, for stores whose W fits the memory
+// budget (build_warena, tm_capi.cu): [plane][k][row][kpad] fp16 with rows
+// tile-major ([i1 / 4][i2 / 32][i1 % 4][i2 % 32], TC_ROWS per tile) and K the
+// component's packed column stream.  The arithmetic is the producer warps'
+// (tc_produce_column: FFMA2 complex multiply-adds over b in order, the wsc
+// multiply, f16_split2), so the A tiles are the same bits.  One block per
+// (tensor, row tile), one thread per row.
+__global__ void build_warena_kernel(const TcDesc* __restrict__ tcd, const float2* __restrict__ varena,
+                                    const float2* __restrict__ u2arena, const int* __restrict__ kofs, int64_t ncols,
+                                    int q, int n1, int n2, int nt2, int64_t rows_pad, int64_t kpad, float wsc,
+                                    __half* __restrict__ wa) {
+    using namespace sm100;
+    const int64_t t = blockIdx.x;  // component-major tensor index k ncols + j
+    const int k = int(t / ncols);
+    const int tile = int(blockIdx.y), t1 = tile / nt2, t2 = tile - t1 * nt2;
+    const int row = int(threadIdx.x);  // i2 + 32 i1 inside the tile
+    const int i1 = t1 * TC_TI1 + row / TC_TI2, i2 = t2 * TC_TI2 + row % TC_TI2;
+    if (i1 >= n1 || i2 >= n2) return;  // padding rows stay zero (the arena is cleared)
+    const TcDesc d = tcd[t];
+    const int r2 = d.r2, r3 = d.r3;
+    const float2* V = varena + d.off_v + int64_t(i1 / TC_TI1) * TC_TI1 * r2 * r3 + (i1 % TC_TI1);
+    const float2* U = u2arena + d.off_u2 + int64_t(i2) * (r2 | 1);
+    const int64_t plane = int64_t(q) * rows_pad * kpad;
+    unsigned short* o = reinterpret_cast<unsigned short*>(wa) + (int64_t(k) * rows_pad + int64_t(tile) * TC_ROWS + row) * kpad +
+                        kofs[t];
+    const uint64_t sc2 = f2_pack(wsc, wsc);
+    for (int c = 0; c < r3; ++c) {
+        uint64_t w = 0;
+        for (int b = 0; b < r2; ++b) cfma2v(w, V[(c + r3 * b) * TC_TI1], U[b]);
+        asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(w) : "l"(sc2));
+        uint32_t hi, lo;
+        f16_split2(w, hi, lo);
+        o[c] = static_cast<unsigned short>(hi);                  // Re hi
+        o[plane + c] = static_cast<unsigned short>(lo);          // Re lo
+        o[2 * plane + c] = static_cast<unsigned short>(hi >> 16);  // Im hi
+        o[3 * plane + c] = static_cast<unsigned short>(lo >> 16);  // Im lo
     }
 }
 

@@ -512,7 +512,8 @@ def test_device_inputs_with_lazy_conjugation(oracle, product):
     ((36, 33, 64), 3, 7, (8, 12, 32), 2),        # r3 = 32: a column spans three 16-K stages
     ((64, 64, 64), 12, 6, (16, 17, 17), 5),     # just past the old rank-16 bound, quads + single adjoint
 ])
-def test_ranks_above_16_stay_on_tensor_cores(oracle, product, dims, q, m, hi, p):
+@pytest.mark.parametrize("warena", ["on", "off"])
+def test_ranks_above_16_stay_on_tensor_cores(oracle, product, dims, q, m, hi, p, warena, monkeypatch):
     """Ranks up to 32 run on tcgen05 (the reference accepts any 1 <= r <= n,
     src/io.cpp:131-139): one or more high-rank tensors in a ragged store."""
     O, P = oracle, product
@@ -528,7 +529,11 @@ def test_ranks_above_16_stay_on_tensor_cores(oracle, product, dims, q, m, hi, p)
     ranks, payload = O.pack_tensors(tens)
     cc = O.Compressed(dims, q, m, ranks.reshape(m, q, 3), payload)
     ds = P.DeviceStore.from_compressed(cc, "c64")
-    assert ds.kernel_paths() == {"forward": "tcgen05", "adjoint": "tcgen05"}
+    kp = ds.kernel_paths()
+    assert kp["forward"] == "tcgen05+warena" and kp["adjoint"] == "tcgen05"
+    if warena == "off":  # the producer-warp forward (the BIG instantiation for r3 > 16)
+        monkeypatch.setenv("TMB_WARENA", "0")
+        assert ds.kernel_paths()["forward"] == "tcgen05"
     ref = O.OracleStore(cc.rounded_c64())
     x = cn01(m, p, 3).astype(np.complex64).astype(np.complex128)
     phi = cn01(cc.rows, p, 4).astype(np.complex64).astype(np.complex128)

@@ -1,0 +1,61 @@
+"""The W-arena forward (fwd_tc_kernel<..., WA>): for stores whose W = U1 x1 G
+x2 U2 fits the memory budget, the A operand is precomputed once
+(build_warena_kernel) and streamed by TMA — no producer warps.  Checked
+against the oracle and against the producer-warp forward of the same store
+(TMB_WARENA=0 switches a store back at run time), over ragged ranks, grids
+whose n2 is not a multiple of 32, one and many right-hand sides, split final
+waves (cut at K-stage boundaries) and CTA pairs; and the budget switch."""
+import numpy as np
+import pytest
+
+from conftest import rel
+from helpers import cn01, ragged_store
+
+pytestmark = pytest.mark.gpu
+
+
+def _c64(a):
+    return a.astype(np.complex64).astype(np.complex128)
+
+
+@pytest.mark.parametrize("dims,q,m,rlo,rhi,p", [
+    ((16, 12, 40), 3, 17, 2, 9, 1),       # single-CTA tiles, n2 < 32
+    ((64, 64, 64), 12, 10, 2, 9, 3),      # q = 12, three right-hand sides
+    ((48, 40, 256), 3, 23, 4, 12, 1),     # CTA pairs (256-voxel i3 span), n2 = 40
+    ((40, 36, 140), 2, 9, 10, 16, 2),     # two i3 halves
+    ((24, 32, 64), 3, 300, 1, 6, 40),     # many columns and right-hand sides
+    ((8, 8, 16), 1, 2, 1, 3, 1),          # tiny
+])
+def test_warena_forward_matches_oracle_and_producer_path(oracle, product, dims, q, m, rlo, rhi, p, monkeypatch):
+    O, P = oracle, product
+    cc = ragged_store(dims, q, m, rlo, rhi, seed=m + q + p)
+    ds = P.DeviceStore.from_compressed(cc, "c64")
+    assert ds.kernel_paths()["forward"] == "tcgen05+warena"
+    ref = O.OracleStore(cc.rounded_c64())
+    x = _c64(cn01(m, p, 11))
+    yo = ref.forward(x)
+    yw = ds.forward(x)
+    assert rel(yw, yo) <= 1e-5
+    monkeypatch.setenv("TMB_WARENA", "0")
+    assert ds.kernel_paths()["forward"] == "tcgen05"
+    yp = ds.forward(x)
+    assert rel(yp, yo) <= 1e-5
+    # the same A bits: the two forwards differ only where final-wave splits differ
+    assert rel(yw, yp) <= 1e-6
+    monkeypatch.delenv("TMB_WARENA")
+    assert rel(ds.forward(x), yw) == 0.0  # deterministic
+
+
+def test_warena_budget(oracle, product, monkeypatch):
+    """A store whose W arena exceeds $TMB_WARENA_GB keeps the producer path;
+    TMB_WARENA=0 at build time builds none."""
+    P = product
+    cc = ragged_store((32, 32, 64), 3, 8, 2, 6, seed=5)
+    monkeypatch.setenv("TMB_WARENA_GB", "0.000001")
+    assert P.DeviceStore.from_compressed(cc, "c64").kernel_paths()["forward"] == "tcgen05"
+    monkeypatch.delenv("TMB_WARENA_GB")
+    monkeypatch.setenv("TMB_WARENA", "0")
+    ds = P.DeviceStore.from_compressed(cc, "c64")
+    monkeypatch.delenv("TMB_WARENA")
+    assert ds.kernel_paths()["forward"] == "tcgen05"
+    assert P.DeviceStore.from_compressed(cc, "c64").kernel_paths()["forward"] == "tcgen05+warena"
