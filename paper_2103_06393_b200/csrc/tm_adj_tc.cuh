@@ -86,6 +86,11 @@ struct AjGeom {
     int split;       // work items per tile in this launch (chunk ranges; > 1 only for a final partial wave)
     int64_t tile0;   // first tile of this launch: item t is tile tile0 + t / split, part t % split
     int64_t t_begin, t_end;  // item range of this launch
+    // W arena of the adjoint (WA kernels): W = V x_2 U2 per (component, row
+    // tile, packed K slot, row), float2, [k][row tile][wkpad][128 rows]
+    const float2* wadj;
+    const int* kofs;  // component-major K offset of each tensor (the forward's packing)
+    int64_t wkpad;
 };
 
 struct AjTile {
@@ -169,11 +174,48 @@ __device__ __forceinline__ float2 aj_consume_column(const float2* __restrict__ V
     return make_float2(ar, ai);
 }
 
+// aj_consume_column for the W-arena kernels: W[row, c] comes precomputed
+// ([c][128 rows] float2 in the factor slot, bulk-copied from the adjoint W
+// arena: the same normalised V x_2 U2 bits the consumers would compute), then
+// the same contraction with Q.
+template <int NU>
+__device__ __forceinline__ float2 aj_consume_column_w(const float2* __restrict__ Wc, int r3, int h, int row,
+                                                      int lane, uint32_t qaddr, uint64_t* fempty_s) {
+    using namespace sm100;
+    float2 w[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        const int c = AJ_NH * u + h;
+        w[u] = (u < NU - 1 || c < r3) ? Wc[c * TC_ROWS + row] : make_float2(0.f, 0.f);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(fempty_s);
+    uint32_t qi[NU], qr[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        const uint32_t sl = (u < NU - 1 || AJ_NH * u + h < r3) ? uint32_t(AJ_NH * u + h) : 0u;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(qi[u]) : "r"(qaddr + sl));
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(qr[u]) : "r"(qaddr + AJ_CH + sl));
+    }
+    tmem_ld_wait();
+    float ar = 0.f, ai = 0.f;
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        if (u < NU - 1 || AJ_NH * u + h < r3) {
+            const float qre = __uint_as_float(qr[u]), qim = __uint_as_float(qi[u]);
+            ar = fmaf(w[u].x, qre, fmaf(w[u].y, qim, ar));
+            ai = fmaf(w[u].x, qim, fmaf(-w[u].y, qre, ai));
+        }
+    }
+    return make_float2(ar, ai);
+}
+
 // NSTX: A/B stage count override (0 = AJ_NST / AJ_NST2); 2 for stores whose
 // rank-(r2, r3) factor slots leave no room for the default ring.
 // BIG: stores with r3 > 16 (up to TC_RMAX = 32), a separate instantiation so
 // the r3 <= 16 kernels keep their register budget.
-template <bool PAIR, int NSTX = 0, bool BIG = false>
+// WA: W from the adjoint W arena (r3 <= 16 stores whose arena fits the budget).
+template <bool PAIR, int NSTX = 0, bool BIG = false, bool WA = false>
 __global__ void __launch_bounds__(AJ_THREADS, 1)
     adj_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                   const TcDesc* __restrict__ tcd, const float2* __restrict__ varena,
@@ -346,6 +388,14 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                     mbar_wait_backoff(&fempty[s], ph ^ 1, 64);
                     const TcDesc d = tdk[j];
                     unsigned char* slot = sSlot + s * g.slot_bytes;
+                    if constexpr (WA) {  // the column's W tile: r3 x 128 rows, contiguous in the arena
+                        const uint32_t bw = uint32_t(d.r3) * TC_ROWS * 8u;
+                        const int64_t kof = g.kofs[int64_t(tl.k) * g.ncols + j];
+                        mbar_arrive_expect_tx(&ffull[s], uint32_t(sizeof(TcDesc)) + bw);
+                        bulk_g2s(slot, tdk + j, uint32_t(sizeof(TcDesc)), &ffull[s]);
+                        bulk_g2s(slot + TC_SLOT_V,
+                                 g.wadj + ((int64_t(tl.k) * g.nrt + tl.rt) * g.wkpad + kof) * TC_ROWS, bw, &ffull[s]);
+                    } else {
                     const uint32_t r23 = uint32_t(d.r2 * d.r3);
                     const uint32_t ld2 = uint32_t(d.r2 | 1);
                     const uint32_t bv = round16(uint32_t(TC_TI1) * r23 * 8u);
@@ -354,6 +404,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                     bulk_g2s(slot, tdk + j, uint32_t(sizeof(TcDesc)), &ffull[s]);
                     bulk_g2s(slot + TC_SLOT_V, varena + d.off_v + int64_t(tl.i1_0) * r23, bv, &ffull[s]);
                     bulk_g2s(slot + g.u2_off, u2arena + d.off_u2 + int64_t(tl.i2_0) * ld2, b2, &ffull[s]);
+                    }
                     if (++s == TC_JR) {
                         s = 0;
                         ph ^= 1;
@@ -392,7 +443,21 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                     float2 a;
 #define AJ_COL(NU) \
     a = aj_consume_column<NU>(V, U2, (g.debug & 4) ? 0 : r2, r2 | 1, r3, h, lane, qbase + uint32_t(soff), &fempty[fs])
-                    if constexpr (BIG) {
+#define AJ_COLW(NU)                                                                                                   \
+    a = aj_consume_column_w<NU>(reinterpret_cast<const float2*>(slot + TC_SLOT_V), r3, h, i1l * 32 + lane, lane,   \
+                                qbase + uint32_t(soff), &fempty[fs])
+                    if constexpr (WA) {
+                        switch ((r3 + AJ_NH - 1) / AJ_NH) {
+                            case 1: AJ_COLW(1); break;
+                            case 2: AJ_COLW(2); break;
+                            case 3: AJ_COLW(3); break;
+                            case 4: AJ_COLW(4); break;
+                            case 5: AJ_COLW(5); break;
+                            case 6: AJ_COLW(6); break;
+                            case 7: AJ_COLW(7); break;
+                            default: AJ_COLW(8); break;
+                        }
+                    } else if constexpr (BIG) {
                         switch ((r3 + AJ_NH - 1) / AJ_NH) {
                             case 1: AJ_COL(1); break;
                             case 2: AJ_COL(2); break;
@@ -424,6 +489,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                         }
                     }
 #undef AJ_COL
+#undef AJ_COLW
                     if (++fs == TC_JR) {
                         fs = 0;
                         fph ^= 1;

@@ -155,6 +155,7 @@ struct tm_store {
     // W arena (W = V x_2 U2 as the forward's fp16-split A operand, built when it
     // fits the memory budget: the forward then runs without producer warps)
     __half* d_warena = nullptr;
+    float2* d_wadj = nullptr;  // the adjoint's W arena (fp32 W, r3 <= 16 stores)
     int64_t warena_rows = 0;
     CUtensorMap warena_map{};
     // tensor-core adjoint: chunk-aligned, i3-contiguous U3 planes
@@ -203,6 +204,7 @@ struct tm_store {
         if (d_varena) cudaFree(d_varena);
         if (d_u2arena) cudaFree(d_u2arena);
         if (d_warena) cudaFree(d_warena);
+        if (d_wadj) cudaFree(d_wadj);
         if (d_aplanes) cudaFree(d_aplanes);
         for (auto& a : adjp) {
             if (a.d_aplanes) cudaFree(a.d_aplanes);
@@ -267,25 +269,29 @@ void build_warena(tm_store* s) {
     const int nt1 = int((s->dims[0] + TC_TI1 - 1) / TC_TI1), nt2 = int((s->dims[1] + TC_TI2 - 1) / TC_TI2);
     const int64_t rows_pad = int64_t(nt1) * nt2 * TC_ROWS;
     const size_t bytes = size_t(4) * s->q * size_t(rows_pad) * size_t(s->kpad) * sizeof(__half);
+    // the adjoint's arena (same size, fp32 float2) when its W tiles fit the factor ring (r3 <= 16)
+    const size_t abytes = s->rmax[2] <= 16 ? bytes : 0;
     double cap_gb = 24.0;
     if (const char* e = std::getenv("TMB_WARENA_GB")) cap_gb = std::atof(e);
     size_t freeb = 0, total = 0;
     CK(cudaMemGetInfo(&freeb, &total));
-    if (double(bytes) > cap_gb * 1e9 || bytes > freeb / 2 || nt1 * nt2 > 65535 || rows_pad >= (int64_t(1) << 31))
+    if (double(bytes + abytes) > cap_gb * 1e9 || bytes + abytes > freeb / 2 || nt1 * nt2 > 65535 ||
+        rows_pad >= (int64_t(1) << 31))
         return;
     CK(cudaMalloc(&s->d_warena, bytes));
     CK(cudaMemset(s->d_warena, 0, bytes));
+    if (abytes) CK(cudaMalloc(&s->d_wadj, abytes));  // every slot a column reads is written below
     const int64_t ntens = s->ncols * s->q;
     build_warena_kernel<<<dim3(unsigned(ntens), unsigned(nt1 * nt2)), TC_ROWS>>>(
         s->d_tcd, s->d_varena, s->d_u2arena, s->d_kofs, s->ncols, s->q, int(s->dims[0]), int(s->dims[1]), nt2,
-        rows_pad, s->kpad, fp16_scale(s->vmax * 1.0001f), s->d_warena);
+        rows_pad, s->kpad, fp16_scale(s->vmax * 1.0001f), s->d_warena, s->d_wadj);
     launched(cudaSuccess, "build_warena_kernel");
     CK(cudaDeviceSynchronize());
     s->warena_rows = rows_pad;
     s->warena_map = make_tmap_3d_f16(s->d_warena, uint64_t(s->kpad), uint64_t(rows_pad), uint64_t(4 * s->q),
                                      uint64_t(s->kpad) * 2, uint64_t(rows_pad) * s->kpad * 2, 16, TC_ROWS,
                                      CU_TENSOR_MAP_SWIZZLE_32B);
-    s->device_bytes += int64_t(bytes);
+    s->device_bytes += int64_t(bytes + abytes);
 }
 
 // B planes of the tensor-core forward (see tm_kernels_tc.cuh), built once.
@@ -1194,6 +1200,14 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     g.rmax3 = s->rmax[2];
     g.u2_off = TC_SLOT_V + int(round16(uint32_t(TC_TI1 * g.rmax2 * g.rmax3 * 8)));
     g.slot_bytes = (g.u2_off + TC_TI2 * (g.rmax2 | 1) * 8 + 127) / 128 * 128;
+    // W arena (build_warena): the consumers read W tiles (r3 x 128 float2) instead of forming V x_2 U2
+    const bool wa = s->d_wadj && !warena_disabled() && s->rmax[2] <= 16;
+    if (wa) {
+        g.slot_bytes = (TC_SLOT_V + g.rmax3 * TC_ROWS * 8 + 127) / 128 * 128;
+        g.wadj = s->d_wadj;
+        g.kofs = s->d_kofs;
+        g.wkpad = s->kpad;
+    }
     g.maxch = s->maxch;
     {
         const char* dbg = std::getenv("TMB_TC_DEBUG");
@@ -1249,10 +1263,12 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     const int64_t nred = g.nrt * g.q;
     float2* part = static_cast<float2*>(s->part.get(size_t(s->ncols * p * nred) * sizeof(float2)));
     const bool big = s->rmax[2] > 16;  // the r3 <= 32 instantiations
-    auto kpair = big ? (small_ring ? adj_tc_kernel<true, 2, true> : adj_tc_kernel<true, 0, true>)
-                     : (small_ring ? adj_tc_kernel<true, 2> : adj_tc_kernel<true>);
-    auto ksingle = big ? (small_ring ? adj_tc_kernel<false, 2, true> : adj_tc_kernel<false, 0, true>)
-                       : (small_ring ? adj_tc_kernel<false, 2> : adj_tc_kernel<false>);
+    auto kpair = wa ? (small_ring ? adj_tc_kernel<true, 2, false, true> : adj_tc_kernel<true, 0, false, true>)
+                    : big ? (small_ring ? adj_tc_kernel<true, 2, true> : adj_tc_kernel<true, 0, true>)
+                          : (small_ring ? adj_tc_kernel<true, 2> : adj_tc_kernel<true>);
+    auto ksingle = wa ? (small_ring ? adj_tc_kernel<false, 2, false, true> : adj_tc_kernel<false, 0, false, true>)
+                      : big ? (small_ring ? adj_tc_kernel<false, 2, true> : adj_tc_kernel<false, 0, true>)
+                            : (small_ring ? adj_tc_kernel<false, 2> : adj_tc_kernel<false>);
     CK(cudaFuncSetAttribute(ksingle, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     CK(cudaFuncSetAttribute(kpair, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // (up to 8 parts per tile when there are fewer tiles than SMs: best_split)
@@ -1644,7 +1660,8 @@ TM_API int tm_store_kernels(const tm_store* s, int32_t* forward_tc, int32_t* adj
         if (!s) contract("null store");
         const bool off = tc_disabled();
         if (forward_tc) *forward_tc = (s->tc_ok && !off) ? (s->d_warena && !warena_disabled() ? 2 : 1) : 0;
-        if (adjoint_tc) *adjoint_tc = (s->tca_ok && !off && adj_tc_fits(s)) ? 1 : 0;
+        if (adjoint_tc)
+            *adjoint_tc = (s->tca_ok && !off && adj_tc_fits(s)) ? (s->d_wadj && !warena_disabled() ? 2 : 1) : 0;
     });
 }
 

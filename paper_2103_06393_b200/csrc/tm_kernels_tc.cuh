@@ -992,11 +992,13 @@ __global__ void build_u2_kernel(const TDesc* __restrict__ td, const float2* __re
 // component's packed column stream.  The arithmetic is the producer warps'
 // (tc_produce_column: FFMA2 complex multiply-adds over b in order, the wsc
 // multiply, f16_split2), so the A tiles are the same bits.  One block per
-// (tensor, row tile), one thread per row.
+// (tensor, row tile), one thread per row.  wadj (optional): the adjoint's W
+// arena, the unscaled fp32 W as float2 [k][row tile][kpad][128 rows] (a
+// column's r3 x 128 block is contiguous; the adjoint consumers' own bits).
 __global__ void build_warena_kernel(const TcDesc* __restrict__ tcd, const float2* __restrict__ varena,
                                     const float2* __restrict__ u2arena, const int* __restrict__ kofs, int64_t ncols,
                                     int q, int n1, int n2, int nt2, int64_t rows_pad, int64_t kpad, float wsc,
-                                    __half* __restrict__ wa) {
+                                    __half* __restrict__ wa, float2* __restrict__ wadj) {
     using namespace sm100;
     const int64_t t = blockIdx.x;  // component-major tensor index k ncols + j
     const int k = int(t / ncols);
@@ -1015,6 +1017,7 @@ __global__ void build_warena_kernel(const TcDesc* __restrict__ tcd, const float2
     for (int c = 0; c < r3; ++c) {
         uint64_t w = 0;
         for (int b = 0; b < r2; ++b) cfma2v(w, V[(c + r3 * b) * TC_TI1], U[b]);
+        if (wadj) wadj[((int64_t(k) * gridDim.y + tile) * kpad + kofs[t] + c) * TC_ROWS + row] = f2_unpack(w);
         asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(w) : "l"(sc2));
         uint32_t hi, lo;
         f16_split2(w, hi, lo);

@@ -241,7 +241,7 @@ class DeviceStore:
         a = ctypes.c_int32()
         _check(lib().tm_store_kernels(self.handle, ctypes.byref(f), ctypes.byref(a)))
         name = {2: "tcgen05+warena", 1: "tcgen05", 0: "cuda-core"}
-        return {"forward": name[f.value], "adjoint": name[a.value]}
+        return {"forward": name[f.value], "adjoint": name[a.value]}  # adjoint 2: W tiles from the arena
 
     def opcounts(self, p=1):
         """Exact OpCounts of one product at p right-hand sides (matvec.cpp:10-15,50-51)."""

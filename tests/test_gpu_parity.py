@@ -530,10 +530,10 @@ def test_ranks_above_16_stay_on_tensor_cores(oracle, product, dims, q, m, hi, p,
     cc = O.Compressed(dims, q, m, ranks.reshape(m, q, 3), payload)
     ds = P.DeviceStore.from_compressed(cc, "c64")
     kp = ds.kernel_paths()
-    assert kp["forward"] == "tcgen05+warena" and kp["adjoint"] == "tcgen05"
+    assert kp["forward"] == "tcgen05+warena" and kp["adjoint"] in ("tcgen05", "tcgen05+warena")
     if warena == "off":  # the producer-warp forward (the BIG instantiation for r3 > 16)
         monkeypatch.setenv("TMB_WARENA", "0")
-        assert ds.kernel_paths()["forward"] == "tcgen05"
+        assert ds.kernel_paths() == {"forward": "tcgen05", "adjoint": "tcgen05"}
     ref = O.OracleStore(cc.rounded_c64())
     x = cn01(m, p, 3).astype(np.complex64).astype(np.complex128)
     phi = cn01(cc.rows, p, 4).astype(np.complex64).astype(np.complex128)

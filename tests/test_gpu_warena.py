@@ -1,6 +1,7 @@
-"""The W-arena forward (fwd_tc_kernel<..., WA>): for stores whose W = U1 x1 G
-x2 U2 fits the memory budget, the A operand is precomputed once
-(build_warena_kernel) and streamed by TMA — no producer warps.  Checked
+"""The W arena (fwd_tc_kernel<..., WA>, adj_tc_kernel<..., WA>): for stores
+whose W = U1 x1 G x2 U2 fits the memory budget, the forward's A operand is
+precomputed once (build_warena_kernel) and streamed by TMA — no producer
+warps — and the adjoint's consumers read fp32 W tiles instead of forming them.  Checked
 against the oracle and against the producer-warp forward of the same store
 (TMB_WARENA=0 switches a store back at run time), over ragged ranks, grids
 whose n2 is not a multiple of 32, one and many right-hand sides, split final
@@ -26,24 +27,28 @@ def _c64(a):
     ((24, 32, 64), 3, 300, 1, 6, 40),     # many columns and right-hand sides
     ((8, 8, 16), 1, 2, 1, 3, 1),          # tiny
 ])
-def test_warena_forward_matches_oracle_and_producer_path(oracle, product, dims, q, m, rlo, rhi, p, monkeypatch):
+def test_warena_products_match_oracle_and_producer_path(oracle, product, dims, q, m, rlo, rhi, p, monkeypatch):
     O, P = oracle, product
     cc = ragged_store(dims, q, m, rlo, rhi, seed=m + q + p)
     ds = P.DeviceStore.from_compressed(cc, "c64")
-    assert ds.kernel_paths()["forward"] == "tcgen05+warena"
+    assert ds.kernel_paths() == {"forward": "tcgen05+warena", "adjoint": "tcgen05+warena"}
     ref = O.OracleStore(cc.rounded_c64())
     x = _c64(cn01(m, p, 11))
-    yo = ref.forward(x)
-    yw = ds.forward(x)
-    assert rel(yw, yo) <= 1e-5
+    phi = _c64(cn01(cc.rows, p, 12))
+    yo, zo = ref.forward(x), ref.adjoint(phi)
+    yw, zw = ds.forward(x), ds.adjoint(phi)
+    assert rel(yw, yo) <= 1e-5 and rel(zw, zo) <= 1e-5
     monkeypatch.setenv("TMB_WARENA", "0")
-    assert ds.kernel_paths()["forward"] == "tcgen05"
-    yp = ds.forward(x)
-    assert rel(yp, yo) <= 1e-5
-    # the same A bits: the two forwards differ only where final-wave splits differ
+    assert ds.kernel_paths() == {"forward": "tcgen05", "adjoint": "tcgen05"}
+    yp, zp = ds.forward(x), ds.adjoint(phi)
+    assert rel(yp, yo) <= 1e-5 and rel(zp, zo) <= 1e-5
+    # the same W bits: the forwards differ only where final-wave splits differ;
+    # the adjoint consumers read exactly the W they would have computed
     assert rel(yw, yp) <= 1e-6
+    if p == 1:
+        assert rel(zw, zp) == 0.0
     monkeypatch.delenv("TMB_WARENA")
-    assert rel(ds.forward(x), yw) == 0.0  # deterministic
+    assert rel(ds.forward(x), yw) == 0.0 and rel(ds.adjoint(phi), zw) == 0.0  # deterministic
 
 
 def test_warena_budget(oracle, product, monkeypatch):
