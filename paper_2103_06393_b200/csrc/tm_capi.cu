@@ -1200,7 +1200,11 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     g.rmax3 = s->rmax[2];
     g.u2_off = TC_SLOT_V + int(round16(uint32_t(TC_TI1 * g.rmax2 * g.rmax3 * 8)));
     g.slot_bytes = (g.u2_off + TC_TI2 * (g.rmax2 | 1) * 8 + 127) / 128 * 128;
-    // W arena (build_warena): the consumers read W tiles (r3 x 128 float2) instead of forming V x_2 U2
+    // the right-hand-side-group kernels form W themselves (with W tiles from the
+    // arena they measured slower: twice the bytes per column, larger slots)
+    const int slot_groups = g.slot_bytes;
+    // W arena (build_warena): the single-RHS consumers read W tiles (r3 x 128 float2)
+    // instead of forming V x_2 U2
     const bool wa = s->d_wadj && !warena_disabled() && s->rmax[2] <= 16;
     if (wa) {
         g.slot_bytes = (TC_SLOT_V + g.rmax3 * TC_ROWS * 8 + 127) / 128 * 128;
@@ -1285,9 +1289,12 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
         int nrmax = 4;
         if (const char* e = std::getenv("TMB_ADJ_NR")) nrmax = std::atoi(e);
         if (const char* e = std::getenv("TMB_ADJ_NR1")) if (*e && *e != '0') nrmax = 1;
-        const bool q4 = nrmax >= 4 && p >= 4 && adj_pack_fits(s, 4, g.slot_bytes) && ensure_adj_pack(s, 1);
+        AjGeom gg = g;  // the group kernels' geometry: V / U2 factor slots, no W arena
+        gg.slot_bytes = slot_groups;
+        gg.wadj = nullptr;
+        const bool q4 = nrmax >= 4 && p >= 4 && adj_pack_fits(s, 4, gg.slot_bytes) && ensure_adj_pack(s, 1);
         const int64_t quads = q4 ? p / 4 : 0;
-        const bool q2 = nrmax >= 2 && p - 4 * quads >= 2 && adj_pack_fits(s, 2, g.slot_bytes) &&
+        const bool q2 = nrmax >= 2 && p - 4 * quads >= 2 && adj_pack_fits(s, 2, gg.slot_bytes) &&
                         ensure_adj_pack(s, 0);
         const int64_t pairs = q2 ? (p - 4 * quads) / 2 : 0;
         if (quads + pairs > 0) {
@@ -1295,9 +1302,9 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
                 CK(cudaStreamWaitEvent(st, arrived[size_t(bready)], 0));
                 prepare(bready, bready + 1);
             }
-            if (quads > 0) launch_adj_groups<4>(s, g, amap, 0, quads, phimax, part, nsm, st);
+            if (quads > 0) launch_adj_groups<4>(s, gg, amap, 0, quads, phimax, part, nsm, st);
             // pairs start at right-hand side 4 quads = pair index 2 quads
-            if (pairs > 0) launch_adj_groups<2>(s, g, amap, 2 * quads, pairs, phimax, part, nsm, st);
+            if (pairs > 0) launch_adj_groups<2>(s, gg, amap, 2 * quads, pairs, phimax, part, nsm, st);
             tfirst = (4 * quads + 2 * pairs) * g.q * tpb;  // the remaining (odd) right-hand side's tiles
         }
     }
