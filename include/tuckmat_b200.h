@@ -110,11 +110,12 @@ TM_API int tm_store_info(const tm_store* s, int32_t* q, int64_t* ncols, int64_t*
 /* Which kernels the store's products run: 1 = tcgen05 tensor-core kernels
  * (c64 stores with every rank <= 32 whose factor slots fit the shared-memory
  * plan), 0 = CUDA-core kernels (c128, larger ranks, TMB_DISABLE_TC=1);
- * 2 = tcgen05 with W = U1 x_1 G x_2 U2 from the store's precomputed W arena
- * (forward: the fp16-split A operand by TMA, no producer warps; single
- * right-hand-side adjoint passes, for r3 <= 16: fp32 W tiles for the
- * consumers), built when it fits
- * $TMB_WARENA_GB (default 24) and half the free memory; TMB_WARENA=0 off. */
+ * forward 2 = tcgen05 with its A operand (W = U1 x_1 G x_2 U2 as fp16
+ * splits) streamed from the store's precomputed W arena, no producer warps;
+ * adjoint 3 = the adjoint as one tcgen05 GEMM on the transposed arena,
+ * G = conj(W)^T Phi, then z = sum conj(U3) G.  The arenas are built when the
+ * whole store's fit $TMB_WARENA_GB (default 24) and half the free memory;
+ * TMB_WARENA=0 (both) / TMB_ADJ_GEMM=0 (the GEMM adjoint) switch them off. */
 TM_API int tm_store_kernels(const tm_store* s, int32_t* forward_tc, int32_t* adjoint_tc);
 
 /*

@@ -86,11 +86,6 @@ struct AjGeom {
     int split;       // work items per tile in this launch (chunk ranges; > 1 only for a final partial wave)
     int64_t tile0;   // first tile of this launch: item t is tile tile0 + t / split, part t % split
     int64_t t_begin, t_end;  // item range of this launch
-    // W arena of the adjoint (WA kernels): W = V x_2 U2 per (component, row
-    // tile, packed K slot, row), float2, [k][row tile][wkpad][128 rows]
-    const float2* wadj;
-    const int* kofs;  // component-major K offset of each tensor (the forward's packing)
-    int64_t wkpad;
 };
 
 struct AjTile {
@@ -174,48 +169,11 @@ __device__ __forceinline__ float2 aj_consume_column(const float2* __restrict__ V
     return make_float2(ar, ai);
 }
 
-// aj_consume_column for the W-arena kernels: W[row, c] comes precomputed
-// ([c][128 rows] float2 in the factor slot, bulk-copied from the adjoint W
-// arena: the same normalised V x_2 U2 bits the consumers would compute), then
-// the same contraction with Q.
-template <int NU>
-__device__ __forceinline__ float2 aj_consume_column_w(const float2* __restrict__ Wc, int r3, int h, int row,
-                                                      int lane, uint32_t qaddr, uint64_t* fempty_s) {
-    using namespace sm100;
-    float2 w[NU];
-#pragma unroll
-    for (int u = 0; u < NU; ++u) {
-        const int c = AJ_NH * u + h;
-        w[u] = (u < NU - 1 || c < r3) ? Wc[c * TC_ROWS + row] : make_float2(0.f, 0.f);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(fempty_s);
-    uint32_t qi[NU], qr[NU];
-#pragma unroll
-    for (int u = 0; u < NU; ++u) {
-        const uint32_t sl = (u < NU - 1 || AJ_NH * u + h < r3) ? uint32_t(AJ_NH * u + h) : 0u;
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(qi[u]) : "r"(qaddr + sl));
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(qr[u]) : "r"(qaddr + AJ_CH + sl));
-    }
-    tmem_ld_wait();
-    float ar = 0.f, ai = 0.f;
-#pragma unroll
-    for (int u = 0; u < NU; ++u) {
-        if (u < NU - 1 || AJ_NH * u + h < r3) {
-            const float qre = __uint_as_float(qr[u]), qim = __uint_as_float(qi[u]);
-            ar = fmaf(w[u].x, qre, fmaf(w[u].y, qim, ar));
-            ai = fmaf(w[u].x, qim, fmaf(-w[u].y, qre, ai));
-        }
-    }
-    return make_float2(ar, ai);
-}
-
 // NSTX: A/B stage count override (0 = AJ_NST / AJ_NST2); 2 for stores whose
 // rank-(r2, r3) factor slots leave no room for the default ring.
 // BIG: stores with r3 > 16 (up to TC_RMAX = 32), a separate instantiation so
 // the r3 <= 16 kernels keep their register budget.
-// WA: W from the adjoint W arena (r3 <= 16 stores whose arena fits the budget).
-template <bool PAIR, int NSTX = 0, bool BIG = false, bool WA = false>
+template <bool PAIR, int NSTX = 0, bool BIG = false>
 __global__ void __launch_bounds__(AJ_THREADS, 1)
     adj_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                   const TcDesc* __restrict__ tcd, const float2* __restrict__ varena,
@@ -388,14 +346,6 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                     mbar_wait_backoff(&fempty[s], ph ^ 1, 64);
                     const TcDesc d = tdk[j];
                     unsigned char* slot = sSlot + s * g.slot_bytes;
-                    if constexpr (WA) {  // the column's W tile: r3 x 128 rows, contiguous in the arena
-                        const uint32_t bw = uint32_t(d.r3) * TC_ROWS * 8u;
-                        const int64_t kof = g.kofs[int64_t(tl.k) * g.ncols + j];
-                        mbar_arrive_expect_tx(&ffull[s], uint32_t(sizeof(TcDesc)) + bw);
-                        bulk_g2s(slot, tdk + j, uint32_t(sizeof(TcDesc)), &ffull[s]);
-                        bulk_g2s(slot + TC_SLOT_V,
-                                 g.wadj + ((int64_t(tl.k) * g.nrt + tl.rt) * g.wkpad + kof) * TC_ROWS, bw, &ffull[s]);
-                    } else {
                     const uint32_t r23 = uint32_t(d.r2 * d.r3);
                     const uint32_t ld2 = uint32_t(d.r2 | 1);
                     const uint32_t bv = round16(uint32_t(TC_TI1) * r23 * 8u);
@@ -404,7 +354,6 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                     bulk_g2s(slot, tdk + j, uint32_t(sizeof(TcDesc)), &ffull[s]);
                     bulk_g2s(slot + TC_SLOT_V, varena + d.off_v + int64_t(tl.i1_0) * r23, bv, &ffull[s]);
                     bulk_g2s(slot + g.u2_off, u2arena + d.off_u2 + int64_t(tl.i2_0) * ld2, b2, &ffull[s]);
-                    }
                     if (++s == TC_JR) {
                         s = 0;
                         ph ^= 1;
@@ -443,21 +392,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                     float2 a;
 #define AJ_COL(NU) \
     a = aj_consume_column<NU>(V, U2, (g.debug & 4) ? 0 : r2, r2 | 1, r3, h, lane, qbase + uint32_t(soff), &fempty[fs])
-#define AJ_COLW(NU)                                                                                                   \
-    a = aj_consume_column_w<NU>(reinterpret_cast<const float2*>(slot + TC_SLOT_V), r3, h, i1l * 32 + lane, lane,   \
-                                qbase + uint32_t(soff), &fempty[fs])
-                    if constexpr (WA) {
-                        switch ((r3 + AJ_NH - 1) / AJ_NH) {
-                            case 1: AJ_COLW(1); break;
-                            case 2: AJ_COLW(2); break;
-                            case 3: AJ_COLW(3); break;
-                            case 4: AJ_COLW(4); break;
-                            case 5: AJ_COLW(5); break;
-                            case 6: AJ_COLW(6); break;
-                            case 7: AJ_COLW(7); break;
-                            default: AJ_COLW(8); break;
-                        }
-                    } else if constexpr (BIG) {
+                    if constexpr (BIG) {
                         switch ((r3 + AJ_NH - 1) / AJ_NH) {
                             case 1: AJ_COL(1); break;
                             case 2: AJ_COL(2); break;
@@ -489,7 +424,6 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                         }
                     }
 #undef AJ_COL
-#undef AJ_COLW
                     if (++fs == TC_JR) {
                         fs = 0;
                         fph ^= 1;
@@ -625,6 +559,100 @@ __global__ void build_adj_bplanes_kernel(const TDesc* __restrict__ td, const flo
         planes[3 * plane + o] = __hneg(il);
         planes[4 * plane + o] = rl;
         planes[5 * plane + o] = il;
+    }
+}
+
+// ------------------------------------------------ adjoint as one GEMM (W arena)
+// For stores with the transposed W arena (build_warena): G = conj(W)^T Phi on
+// the forward arena kernel (fwd_tc_kernel<..., WA, ADJ>), then z from G here.
+//
+// Phi as the GEMM's K-major B operand: [plane][k][n = i3 p + c][row] fp16,
+// rows tile-major (the arena's order) and contiguous, scaled per component by
+// fp16_scale(max over the component's right-hand sides of max(|re|, |im|))
+// (absmax_kernel's per-(rhs, component) maxima), split hi / lo.  One block per
+// (row tile, n, k); thread t -> (i1 = i1_0 + t % 4, i2 = i2_0 + t / 4), so four
+// threads read 32 contiguous bytes of Phi.
+__global__ void adjg_split_phi_kernel(const float2* __restrict__ phi, int64_t ldphi, int n1, int n2, int n3, int p,
+                                      int q, int nt2, int64_t R, int64_t nt, const float* __restrict__ phimax,
+                                      __half* __restrict__ planes) {
+    using namespace sm100;
+    const int tile = int(blockIdx.x);
+    const int64_t n = blockIdx.y;
+    const int k = int(blockIdx.z);
+    const int i3 = int(n / p), c = int(n - int64_t(i3) * p);
+    const int t1 = tile / nt2, t2 = tile - t1 * nt2;
+    const int t = int(threadIdx.x);
+    const int i1 = t1 * TC_TI1 + (t & 3), i2 = t2 * TC_TI2 + (t >> 2);
+    float m = 0.f;
+    for (int cc = 0; cc < p; ++cc) m = fmaxf(m, phimax[int64_t(cc) * q + k]);
+    const float sc = fp16_scale(m);
+    float2 v = make_float2(0.f, 0.f);
+    if (i1 < n1 && i2 < n2) {
+        const int64_t nv = int64_t(n1) * n2 * n3;
+        v = phi[ldphi * c + int64_t(k) * nv + i1 + int64_t(n1) * (i2 + int64_t(n2) * i3)];
+    }
+    uint32_t hi, lo;
+    f16_split2(f2_pack(v.x * sc, v.y * sc), hi, lo);
+    const int64_t pl = int64_t(q) * nt * R;
+    unsigned short* o = reinterpret_cast<unsigned short*>(planes) + (int64_t(k) * nt + n) * R + int64_t(tile) * TC_ROWS +
+                        (t & 3) * TC_TI2 + (t >> 2);
+    // the B plane order of the forward kernel: Re hi, Im hi, Re lo, Im lo
+    o[0] = static_cast<unsigned short>(hi);
+    o[pl] = static_cast<unsigned short>(hi >> 16);
+    o[2 * pl] = static_cast<unsigned short>(lo);
+    o[3 * pl] = static_cast<unsigned short>(lo >> 16);
+}
+
+// z[j, c] = sum_k inv_k sum_r sum_i3 conj(U3n_jk[i3, r]) G[k][i3 p + c][kofs_jk + r]
+// (U3n = U3 2^-e3 undoes the arena's normalisation W 2^e3; inv_k the W and
+// Phi scales).  One block per column j; thread (c, i3 group) with the r3
+// slots innermost (contiguous in G); the i3 groups are summed in a fixed
+// order: bitwise reproducible.
+__global__ void adjg_contract_kernel(const float2* __restrict__ G, int64_t gslots, int64_t nt, int p, int q,
+                                     int64_t ncols, int n3, const TcDesc* __restrict__ tcd,
+                                     const float2* __restrict__ arena, const int* __restrict__ kofs,
+                                     const float* __restrict__ phimax, float wsc, float2* __restrict__ z,
+                                     int64_t ldz) {
+    __shared__ float2 red[256];
+    const int64_t j = blockIdx.x;
+    const int tid = int(threadIdx.x);
+    for (int c0 = 0; c0 < p; c0 += 256) {
+        const int pc = min(p - c0, 256), ng = 256 / pc;
+        const int c = c0 + tid % pc, gi = tid / pc;
+        float ar = 0.f, ai = 0.f;
+        if (gi < ng) {
+            for (int k = 0; k < q; ++k) {
+                float m = 0.f;
+                for (int cc = 0; cc < p; ++cc) m = fmaxf(m, phimax[int64_t(cc) * q + k]);
+                const int64_t t = int64_t(k) * ncols + j;
+                const TcDesc d = tcd[t];
+                const float sk = ldexpf(1.f, -fexp_e3(d.fexp)) / (wsc * fp16_scale(m));
+                const float2* u3 = arena + d.off_u3;  // n3 x r3, row-major
+                const float2* gk = G + int64_t(k) * nt * gslots + kofs[t];
+                float kr = 0.f, ki = 0.f;
+                for (int i3 = gi; i3 < n3; i3 += ng) {
+                    const float2* gr = gk + (int64_t(i3) * p + c) * gslots;
+                    for (int r = 0; r < d.r3; ++r) {
+                        const float2 u = u3[i3 * d.r3 + r], gv = gr[r];
+                        kr += u.x * gv.x + u.y * gv.y;  // conj(u) gv
+                        ki += u.x * gv.y - u.y * gv.x;
+                    }
+                }
+                ar += kr * sk;
+                ai += ki * sk;
+            }
+        }
+        red[tid] = make_float2(ar, ai);
+        __syncthreads();
+        if (tid < pc) {
+            float sr = 0.f, si = 0.f;
+            for (int g2 = 0; g2 < ng; ++g2) {
+                sr += red[g2 * pc + tid].x;
+                si += red[g2 * pc + tid].y;
+            }
+            z[j + ldz * (c0 + tid)] = make_float2(sr, si);
+        }
+        __syncthreads();
     }
 }
 

@@ -155,7 +155,12 @@ struct tm_store {
     // W arena (W = V x_2 U2 as the forward's fp16-split A operand, built when it
     // fits the memory budget: the forward then runs without producer warps)
     __half* d_warena = nullptr;
-    float2* d_wadj = nullptr;  // the adjoint's W arena (fp32 W, r3 <= 16 stores)
+    // the adjoint GEMM (run_adjoint_gemm): the arena transposed, [plane][k][slot][row]
+    __half* d_wt = nullptr;
+    int64_t wt_kpadt = 0;  // slots per component, a multiple of 256 (CTA-pair slot tiles)
+    int* d_kcr = nullptr;  // [q] the GEMM's K extent (rows) per component
+    CUtensorMap wt_map{};
+    DevBuf gbuf, phit;     // per call: G and the row-contiguous Phi planes
     int64_t warena_rows = 0;
     CUtensorMap warena_map{};
     // tensor-core adjoint: chunk-aligned, i3-contiguous U3 planes
@@ -204,7 +209,8 @@ struct tm_store {
         if (d_varena) cudaFree(d_varena);
         if (d_u2arena) cudaFree(d_u2arena);
         if (d_warena) cudaFree(d_warena);
-        if (d_wadj) cudaFree(d_wadj);
+        if (d_wt) cudaFree(d_wt);
+        if (d_kcr) cudaFree(d_kcr);
         if (d_aplanes) cudaFree(d_aplanes);
         for (auto& a : adjp) {
             if (a.d_aplanes) cudaFree(a.d_aplanes);
@@ -258,6 +264,12 @@ bool warena_disabled() {
     return e && *e == '0';
 }
 
+// TMB_ADJ_GEMM=0: no adjoint GEMM on the W arena (the consumer-warp adjoint instead)
+bool adjg_disabled() {
+    const char* e = std::getenv("TMB_ADJ_GEMM");
+    return e && *e == '0';
+}
+
 // The W arena: W = V x_2 U2 of every tensor as the forward's fp16-split A
 // operand, precomputed once (build_warena_kernel) when it fits
 // $TMB_WARENA_GB (default 24 GB) and half of the free device memory — small
@@ -269,29 +281,40 @@ void build_warena(tm_store* s) {
     const int nt1 = int((s->dims[0] + TC_TI1 - 1) / TC_TI1), nt2 = int((s->dims[1] + TC_TI2 - 1) / TC_TI2);
     const int64_t rows_pad = int64_t(nt1) * nt2 * TC_ROWS;
     const size_t bytes = size_t(4) * s->q * size_t(rows_pad) * size_t(s->kpad) * sizeof(__half);
-    // the adjoint's arena (same size, fp32 float2) when its W tiles fit the factor ring (r3 <= 16)
-    const size_t abytes = s->rmax[2] <= 16 ? bytes : 0;
+    // the adjoint GEMM's transposed arena (slots padded to CTA-pair tiles of 256)
+    const int64_t kpadt = (s->kpad + 255) / 256 * 256;
+    const size_t tbytes = adjg_disabled() ? 0 : size_t(4) * s->q * size_t(kpadt) * size_t(rows_pad) * sizeof(__half);
     double cap_gb = 24.0;
     if (const char* e = std::getenv("TMB_WARENA_GB")) cap_gb = std::atof(e);
     size_t freeb = 0, total = 0;
     CK(cudaMemGetInfo(&freeb, &total));
-    if (double(bytes + abytes) > cap_gb * 1e9 || bytes + abytes > freeb / 2 || nt1 * nt2 > 65535 ||
+    if (double(bytes + tbytes) > cap_gb * 1e9 || bytes + tbytes > freeb / 2 || nt1 * nt2 > 65535 ||
         rows_pad >= (int64_t(1) << 31))
         return;
     CK(cudaMalloc(&s->d_warena, bytes));
     CK(cudaMemset(s->d_warena, 0, bytes));
-    if (abytes) CK(cudaMalloc(&s->d_wadj, abytes));  // every slot a column reads is written below
+    if (tbytes) {
+        CK(cudaMalloc(&s->d_wt, tbytes));
+        CK(cudaMemset(s->d_wt, 0, tbytes));
+        std::vector<int> kcr(static_cast<size_t>(s->q), int(rows_pad));
+        CK(cudaMalloc(&s->d_kcr, kcr.size() * sizeof(int)));
+        CK(cudaMemcpy(s->d_kcr, kcr.data(), kcr.size() * sizeof(int), cudaMemcpyHostToDevice));
+        s->wt_kpadt = kpadt;
+        s->wt_map = make_tmap_3d_f16(s->d_wt, uint64_t(rows_pad), uint64_t(kpadt), uint64_t(4 * s->q),
+                                     uint64_t(rows_pad) * 2, uint64_t(kpadt) * rows_pad * 2, 16, TC_ROWS,
+                                     CU_TENSOR_MAP_SWIZZLE_32B);
+    }
     const int64_t ntens = s->ncols * s->q;
     build_warena_kernel<<<dim3(unsigned(ntens), unsigned(nt1 * nt2)), TC_ROWS>>>(
         s->d_tcd, s->d_varena, s->d_u2arena, s->d_kofs, s->ncols, s->q, int(s->dims[0]), int(s->dims[1]), nt2,
-        rows_pad, s->kpad, fp16_scale(s->vmax * 1.0001f), s->d_warena, s->d_wadj);
+        rows_pad, s->kpad, fp16_scale(s->vmax * 1.0001f), s->d_warena, s->d_wt, kpadt);
     launched(cudaSuccess, "build_warena_kernel");
     CK(cudaDeviceSynchronize());
     s->warena_rows = rows_pad;
     s->warena_map = make_tmap_3d_f16(s->d_warena, uint64_t(s->kpad), uint64_t(rows_pad), uint64_t(4 * s->q),
                                      uint64_t(s->kpad) * 2, uint64_t(rows_pad) * s->kpad * 2, 16, TC_ROWS,
                                      CU_TENSOR_MAP_SWIZZLE_32B);
-    s->device_bytes += int64_t(bytes + abytes);
+    s->device_bytes += int64_t(bytes + tbytes);
 }
 
 // B planes of the tensor-core forward (see tm_kernels_tc.cuh), built once.
@@ -1200,18 +1223,6 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     g.rmax3 = s->rmax[2];
     g.u2_off = TC_SLOT_V + int(round16(uint32_t(TC_TI1 * g.rmax2 * g.rmax3 * 8)));
     g.slot_bytes = (g.u2_off + TC_TI2 * (g.rmax2 | 1) * 8 + 127) / 128 * 128;
-    // the right-hand-side-group kernels form W themselves (with W tiles from the
-    // arena they measured slower: twice the bytes per column, larger slots)
-    const int slot_groups = g.slot_bytes;
-    // W arena (build_warena): the single-RHS consumers read W tiles (r3 x 128 float2)
-    // instead of forming V x_2 U2
-    const bool wa = s->d_wadj && !warena_disabled() && s->rmax[2] <= 16;
-    if (wa) {
-        g.slot_bytes = (TC_SLOT_V + g.rmax3 * TC_ROWS * 8 + 127) / 128 * 128;
-        g.wadj = s->d_wadj;
-        g.kofs = s->d_kofs;
-        g.wkpad = s->kpad;
-    }
     g.maxch = s->maxch;
     {
         const char* dbg = std::getenv("TMB_TC_DEBUG");
@@ -1267,12 +1278,10 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     const int64_t nred = g.nrt * g.q;
     float2* part = static_cast<float2*>(s->part.get(size_t(s->ncols * p * nred) * sizeof(float2)));
     const bool big = s->rmax[2] > 16;  // the r3 <= 32 instantiations
-    auto kpair = wa ? (small_ring ? adj_tc_kernel<true, 2, false, true> : adj_tc_kernel<true, 0, false, true>)
-                    : big ? (small_ring ? adj_tc_kernel<true, 2, true> : adj_tc_kernel<true, 0, true>)
-                          : (small_ring ? adj_tc_kernel<true, 2> : adj_tc_kernel<true>);
-    auto ksingle = wa ? (small_ring ? adj_tc_kernel<false, 2, false, true> : adj_tc_kernel<false, 0, false, true>)
-                      : big ? (small_ring ? adj_tc_kernel<false, 2, true> : adj_tc_kernel<false, 0, true>)
-                            : (small_ring ? adj_tc_kernel<false, 2> : adj_tc_kernel<false>);
+    auto kpair = big ? (small_ring ? adj_tc_kernel<true, 2, true> : adj_tc_kernel<true, 0, true>)
+                     : (small_ring ? adj_tc_kernel<true, 2> : adj_tc_kernel<true>);
+    auto ksingle = big ? (small_ring ? adj_tc_kernel<false, 2, true> : adj_tc_kernel<false, 0, true>)
+                       : (small_ring ? adj_tc_kernel<false, 2> : adj_tc_kernel<false>);
     CK(cudaFuncSetAttribute(ksingle, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     CK(cudaFuncSetAttribute(kpair, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // (up to 8 parts per tile when there are fewer tiles than SMs: best_split)
@@ -1289,12 +1298,9 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
         int nrmax = 4;
         if (const char* e = std::getenv("TMB_ADJ_NR")) nrmax = std::atoi(e);
         if (const char* e = std::getenv("TMB_ADJ_NR1")) if (*e && *e != '0') nrmax = 1;
-        AjGeom gg = g;  // the group kernels' geometry: V / U2 factor slots, no W arena
-        gg.slot_bytes = slot_groups;
-        gg.wadj = nullptr;
-        const bool q4 = nrmax >= 4 && p >= 4 && adj_pack_fits(s, 4, gg.slot_bytes) && ensure_adj_pack(s, 1);
+        const bool q4 = nrmax >= 4 && p >= 4 && adj_pack_fits(s, 4, g.slot_bytes) && ensure_adj_pack(s, 1);
         const int64_t quads = q4 ? p / 4 : 0;
-        const bool q2 = nrmax >= 2 && p - 4 * quads >= 2 && adj_pack_fits(s, 2, gg.slot_bytes) &&
+        const bool q2 = nrmax >= 2 && p - 4 * quads >= 2 && adj_pack_fits(s, 2, g.slot_bytes) &&
                         ensure_adj_pack(s, 0);
         const int64_t pairs = q2 ? (p - 4 * quads) / 2 : 0;
         if (quads + pairs > 0) {
@@ -1302,9 +1308,9 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
                 CK(cudaStreamWaitEvent(st, arrived[size_t(bready)], 0));
                 prepare(bready, bready + 1);
             }
-            if (quads > 0) launch_adj_groups<4>(s, gg, amap, 0, quads, phimax, part, nsm, st);
+            if (quads > 0) launch_adj_groups<4>(s, g, amap, 0, quads, phimax, part, nsm, st);
             // pairs start at right-hand side 4 quads = pair index 2 quads
-            if (pairs > 0) launch_adj_groups<2>(s, gg, amap, 2 * quads, pairs, phimax, part, nsm, st);
+            if (pairs > 0) launch_adj_groups<2>(s, g, amap, 2 * quads, pairs, phimax, part, nsm, st);
             tfirst = (4 * quads + 2 * pairs) * g.q * tpb;  // the remaining (odd) right-hand side's tiles
         }
     }
@@ -1355,8 +1361,118 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
     launched(cudaSuccess, "adj_reduce_kernel");
 }
 
+// The adjoint of a W-arena store as one GEMM per pass of right-hand sides:
+// G = conj(W)^T Phi on fwd_tc_kernel<PAIR, false, true, true> (A = the
+// transposed arena, B = Phi as row-contiguous fp16 planes from
+// adjg_split_phi_kernel; M = slot tiles, N = (i3, c), K = rows), then
+// adjg_contract_kernel applies U3 and the scales.  The MACs are the forward
+// arena kernel's (rows x n3 p x slots), with no consumer warps.
+void run_adjoint_gemm(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, float2* z, int64_t ldz,
+                      cudaStream_t st) {
+    const int n1 = int(s->dims[0]), n2 = int(s->dims[1]), n3 = int(s->dims[2]);
+    const int nt1r = (n1 + TC_TI1 - 1) / TC_TI1, nt2r = (n2 + TC_TI2 - 1) / TC_TI2;
+    const int64_t R = int64_t(nt1r) * nt2r * TC_ROWS, nv = s->nv(), kt = s->wt_kpadt;
+    // passes of pb right-hand sides: G (q n3 pb kt float2) and the Phi planes (4 q n3 pb R fp16) within budget
+    const size_t per_rhs = std::max(size_t(s->q) * n3 * kt * sizeof(float2), size_t(4) * s->q * n3 * R * 2);
+    const int64_t pbmax = std::max<int64_t>(1, std::min<int64_t>({p, int64_t((size_t(2) << 30) / per_rhs),
+                                                                   int64_t(65535 / n3)}));
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const int nsm = num_sms(dev);
+    float* phimax = static_cast<float*>(s->scal.get(size_t(pbmax * s->q + 2) * sizeof(float))) + 2;
+    for (int64_t c0 = 0; c0 < p; c0 += pbmax) {
+        const int64_t pb = std::min<int64_t>(pbmax, p - c0);
+        const float2* ph = phi + ldphi * c0;
+        const int64_t nt = int64_t(n3) * pb;
+        CK(cudaMemsetAsync(phimax, 0, size_t(pb * s->q) * sizeof(float), st));
+        absmax_kernel<<<dim3(148, unsigned(pb * s->q)), 256, 0, st>>>(ph, ldphi, nv, s->q, 0, phimax);
+        launched(cudaSuccess, "absmax_kernel");
+        __half* planes = static_cast<__half*>(s->phit.get(size_t(4) * s->q * nt * R * sizeof(__half)));
+        adjg_split_phi_kernel<<<dim3(unsigned(nt1r * nt2r), unsigned(nt), unsigned(s->q)), TC_ROWS, 0, st>>>(
+            ph, ldphi, n1, n2, n3, int(pb), s->q, nt2r, R, nt, phimax, planes);
+        launched(cudaSuccess, "adjg_split_phi_kernel");
+        TcGeom g{};
+        g.ncols = s->ncols;
+        g.n1 = n1;
+        g.n2 = n2;
+        g.n3 = n3;
+        g.q = s->q;
+        g.p = int(pb);
+        g.nt = int(nt);
+        g.nmma = std::min(TC_NMAX, (g.nt + 15) / 16 * 16);
+        g.nh3 = g.nt > TC_NMAX ? 2 : 1;
+        g.nt3 = (g.nt + g.nmma * g.nh3 - 1) / (g.nmma * g.nh3);
+        g.nt1 = int(kt / TC_ROWS);  // slot tiles play the forward's i1 blocks (nt2 = 1)
+        g.nt2 = 1;
+        g.pair = (g.nmma == TC_NMAX && g.nh3 == 2 && g.nt1 % 2 == 0 && nsm >= 2) ? 1 : 0;
+        if (g.pair) g.nt1 /= 2;
+        g.ntiles = int64_t(g.q) * g.nt3 * g.nt2 * g.nt1;
+        g.b_stage = (g.pair ? 1 : g.nh3) * TC_FPLANES * g.nmma * 32;
+        g.chain = tc_chain();
+        g.gslots = kt;
+        g.split = 1;
+        auto smem_for = [&](int nst) {
+            return 1024 + size_t(nst) * (TC_A_STAGE + g.b_stage) + (2 * TC_NST_MAX + 2 * TC_JR + 2) * 8 + 16;
+        };
+        g.nst = TC_NST_MAX;
+        while (g.nst > 2 && smem_for(g.nst) > kSmemMax) --g.nst;
+        const size_t smem = smem_for(g.nst);
+        auto kpair = fwd_tc_kernel<true, false, true, true>;
+        auto ksingle = fwd_tc_kernel<false, false, true, true>;
+        CK(cudaFuncSetAttribute(ksingle, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        CK(cudaFuncSetAttribute(kpair, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        const unsigned grid = g.pair ? unsigned(std::min<int64_t>(2 * g.ntiles, nsm & ~1))
+                                     : unsigned(std::min<int64_t>(g.ntiles, nsm));
+        const int64_t wave = g.pair ? grid / 2 : grid;
+        float2* rsum =
+            static_cast<float2*>(s->rsum.get(size_t(grid) * g.nmma * g.nh3 * TC_ROWS * sizeof(float2)));
+        float2* G = static_cast<float2*>(s->gbuf.get(size_t(s->q) * nt * kt * sizeof(float2)));
+        const CUtensorMap bmap = make_tmap_3d_f16(planes, uint64_t(R), uint64_t(nt), uint64_t(TC_FPLANES * s->q),
+                                                  uint64_t(R) * 2, uint64_t(nt) * R * 2, 16, uint32_t(g.nmma),
+                                                  CU_TENSOR_MAP_SWIZZLE_32B);
+        for (int64_t t0 = 0; t0 < g.ntiles; t0 += wave) {  // one launch per wave (see run_forward_pass)
+            const int64_t tiles = std::min<int64_t>(g.ntiles - t0, wave);
+            g.tile0 = t0;
+            g.t_begin = 0;
+            g.t_end = tiles;
+            if (g.pair) {
+                cudaLaunchConfig_t cfg{};
+                cfg.gridDim = dim3(grid);
+                cfg.blockDim = dim3(TC_THREADS);
+                cfg.dynamicSmemBytes = smem;
+                cfg.stream = st;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = 2;
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                launched(cudaLaunchKernelEx(&cfg, kpair, bmap, s->wt_map, static_cast<const TcDesc*>(s->d_tcd),
+                                            static_cast<const float2*>(s->d_varena),
+                                            static_cast<const float2*>(s->d_u2arena), static_cast<const int*>(s->d_kcr),
+                                            static_cast<const int*>(s->d_kofs), g, static_cast<const float2*>(nullptr),
+                                            int64_t(0), G, int64_t(0), rsum, static_cast<const float*>(phimax)),
+                         "fwd_tc_kernel<pair, adjoint GEMM>");
+            } else {
+                ksingle<<<grid, TC_THREADS, smem, st>>>(bmap, s->wt_map, s->d_tcd, s->d_varena, s->d_u2arena,
+                                                        s->d_kcr, s->d_kofs, g, nullptr, 0, G, 0, rsum, phimax);
+                launched(cudaSuccess, "fwd_tc_kernel<adjoint GEMM>");
+            }
+        }
+        adjg_contract_kernel<<<unsigned(s->ncols), 256, 0, st>>>(
+            G, kt, nt, int(pb), s->q, s->ncols, n3, s->d_tcd, static_cast<const float2*>(s->d_arena), s->d_kofs,
+            phimax, fp16_scale(s->vmax * 1.0001f), z + ldz * c0, ldz);
+        launched(cudaSuccess, "adjg_contract_kernel");
+    }
+}
+
 void adjoint_dev(tm_store* s, const void* phi, int64_t ldphi, int64_t p, void* z, int64_t ldz, cudaStream_t st) {
     if (s->ncols == 0 || p == 0) return;
+    if (s->d_wt && !warena_disabled() && !adjg_disabled() && !tc_disabled()) {
+        run_adjoint_gemm(s, static_cast<const float2*>(phi), ldphi, p, static_cast<float2*>(z), ldz, st);
+        return;
+    }
     if (s->tca_ok && !tc_disabled() && adj_tc_fits(s) && int64_t(p) * s->q <= 65535) {
         run_adjoint_tc(s, static_cast<const float2*>(phi), ldphi, p, static_cast<float2*>(z), ldz, st);
         return;
@@ -1544,6 +1660,7 @@ bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, 
 
 bool adjoint_host_pipelined(tm_store* s, const void* phi, int64_t ldphi, int64_t p, void* z, int64_t ldz) {
     if (!(s->tca_ok && !tc_disabled() && adj_tc_fits(s) && int64_t(p) * s->q <= 65535)) return false;
+    if (s->d_wt && !warena_disabled() && !adjg_disabled()) return false;  // the adjoint GEMM (adjoint_dev)
     const size_t cs = s->csize();
     void* din = s->xin.get(size_t(std::max<int64_t>(s->rows() * p, 1)) * cs);
     void* dout = s->yout.get(size_t(std::max<int64_t>(s->ncols * p, 1)) * cs);
@@ -1668,7 +1785,9 @@ TM_API int tm_store_kernels(const tm_store* s, int32_t* forward_tc, int32_t* adj
         const bool off = tc_disabled();
         if (forward_tc) *forward_tc = (s->tc_ok && !off) ? (s->d_warena && !warena_disabled() ? 2 : 1) : 0;
         if (adjoint_tc)
-            *adjoint_tc = (s->tca_ok && !off && adj_tc_fits(s)) ? (s->d_wadj && !warena_disabled() ? 2 : 1) : 0;
+            *adjoint_tc = (s->d_wt && !warena_disabled() && !adjg_disabled() && !off) ? 3
+                          : (s->tca_ok && !off && adj_tc_fits(s)) ? 1
+                                                                  : 0;
     });
 }
 

@@ -130,6 +130,7 @@ struct TcGeom {
     int chain;                  // K stages per TMEM accumulation chain
     int debug;                  // diagnostics (TMB_TC_DEBUG): 1 = no mode-2 work, 2 = no B loads
     int pair;                   // 1: CTA-pair kernel (cta_group::2, M = 256), nt1 counts pairs of i1 blocks
+    int64_t gslots;             // ADJ: slots per component in the G buffer ([k][n][slot])
     unsigned long long* prof;   // diagnostics (TMB_TC_DEBUG & 8, builds with -DTMB_TC_PROFILE): per-role wait cycles
     int split;                  // work items per tile in this launch (column ranges; > 1 only in a final
                                 // partial wave, whose items write partial tiles to ypart)
@@ -352,7 +353,13 @@ __device__ __forceinline__ void tc_produce_column(const float2* __restrict__ V, 
 // producer warps, no factor ring; the tile's K range is cut at stage
 // boundaries for split items (a column's r3 slots may straddle parts: the
 // sum over K is linear).
-template <bool PAIR, bool BIG = false, bool WA = false>
+// ADJ (with WA): the adjoint of a W-arena store as one GEMM, G = conj(W)^T Phi
+// (M = the packed (j, r3) slots of a component, N = (i3, c), K = rows): A =
+// the transposed arena, B = Phi as row-contiguous fp16 planes, the MMA signs
+// of a conjugated A, and the epilogue writes raw G (adjg_contract_kernel
+// finishes z).  The tile map reuses the forward's with nt2 = 1: "i1 block" =
+// slot tile.
+template <bool PAIR, bool BIG = false, bool WA = false, bool ADJ = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap bmap, const __grid_constant__ CUtensorMap amap,
                   const TcDesc* __restrict__ tcd,
@@ -494,6 +501,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int span = g.nmma * g.nh3;
             const uint32_t id_p = umma_idesc_f16(TC_ROWS * (PAIR ? 2 : 1), span, false, false);
             const uint32_t id_n = umma_idesc_f16(TC_ROWS * (PAIR ? 2 : 1), span, true, false);
+            // Yr += Ar Br -/+ Ai Bi, Yi += Ar Bi +/- Ai Br: the lower signs for the adjoint
+            // GEMM's conjugated A (ADJ)
+            const uint32_t id_aibi = ADJ ? id_p : id_n, id_aibr = ADJ ? id_n : id_p;
             const int plane_b = (PAIR ? span / 2 : span) * 32;  // one smem B plane (this CTA's i3 rows)
             uint32_t s = 0, ph = 0, gch = 0;
             for (int64_t t = tstart; t < g.t_end; t += tstep) {
@@ -527,15 +537,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     MMA(yr, A[0], Brh, id_p, acc);
                     MMA(yr, A[0], Brl, id_p, 1);
                     MMA(yr, A[1], Brh, id_p, 1);
-                    MMA(yr, A[2], Bih, id_n, 1);
-                    MMA(yr, A[2], Bil, id_n, 1);
-                    MMA(yr, A[3], Bih, id_n, 1);
+                    MMA(yr, A[2], Bih, id_aibi, 1);
+                    MMA(yr, A[2], Bil, id_aibi, 1);
+                    MMA(yr, A[3], Bih, id_aibi, 1);
                     MMA(yi, A[0], Bih, id_p, acc);
                     MMA(yi, A[0], Bil, id_p, 1);
                     MMA(yi, A[1], Bih, id_p, 1);
-                    MMA(yi, A[2], Brh, id_p, 1);
-                    MMA(yi, A[2], Brl, id_p, 1);
-                    MMA(yi, A[3], Brh, id_p, 1);
+                    MMA(yi, A[2], Brh, id_aibr, 1);
+                    MMA(yi, A[2], Brl, id_aibr, 1);
+                    MMA(yi, A[3], Brh, id_aibr, 1);
                     COMMIT(&empty[s]);
                     if (++s == nst) {
                         s = 0;
@@ -706,7 +716,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int span = g.nmma * g.nh3;
         float4* rs = reinterpret_cast<float4*>(rsum) + int64_t(blockIdx.x) * (span / 2) * TC_ROWS + row;
         const int64_t nv3 = int64_t(g.n1) * g.n2 * g.n3;
-        const float inv = 1.f / (g.wsc * fp16_scale(*wmax));  // exact power of two (W scale x B scale)
+        // exact power of two (W scale x B scale); the adjoint GEMM writes raw G
+        const float inv = ADJ ? 1.f : 1.f / (g.wsc * fp16_scale(*wmax));
         uint32_t gch = 0;
         for (int64_t t = tstart; t < g.t_end; t += tstep) {
             const TcTile tl = tc_tile(g, t, rank);
@@ -719,12 +730,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             // split items write their partial tile to ypart ([item][rank][i3][row]); the wave's
             // reduce kernel sums the parts into y in a fixed order
             const bool part_out = g.split > 1;
-            const bool eok = part_out || (ei1 < g.n1 && ei2 < g.n2);
-            float2* yp = part_out ? g.ypart + ((t * (1 + g.pair) + int64_t(rank)) * span) * TC_ROWS + row
-                                  : y + int64_t(tl.k) * nv3 + ei1 + int64_t(g.n1) * ei2;
+            const bool eok = ADJ || part_out || (ei1 < g.n1 && ei2 < g.n2);
+            float2* yp = ADJ ? y + int64_t(tl.k) * g.nt * g.gslots + int64_t(tl.i1_0 / TC_TI1) * TC_ROWS + row
+                         : part_out ? g.ypart + ((t * (1 + g.pair) + int64_t(rank)) * span) * TC_ROWS + row
+                                    : y + int64_t(tl.k) * nv3 + ei1 + int64_t(g.n1) * ei2;
             const int64_t pl = int64_t(g.n1) * g.n2;
             // output of tile column nl (N row n = i3_0 + nl = i3 * p + c)
             auto put = [&](int nl, float2 v) {
+                if (ADJ) {  // G[k][n][slot]: a warp's 32 slots are contiguous
+                    const int n = tl.i3_0 + nl;
+                    if (n < g.nt) yp[int64_t(n) * g.gslots] = v;
+                    return;
+                }
                 if (part_out) {
                     yp[int64_t(TC_ROWS) * nl] = v;
                     return;
@@ -992,13 +1009,13 @@ __global__ void build_u2_kernel(const TDesc* __restrict__ td, const float2* __re
 // component's packed column stream.  The arithmetic is the producer warps'
 // (tc_produce_column: FFMA2 complex multiply-adds over b in order, the wsc
 // multiply, f16_split2), so the A tiles are the same bits.  One block per
-// (tensor, row tile), one thread per row.  wadj (optional): the adjoint's W
-// arena, the unscaled fp32 W as float2 [k][row tile][kpad][128 rows] (a
-// column's r3 x 128 block is contiguous; the adjoint consumers' own bits).
+// (tensor, row tile), one thread per row.  wt (optional): the same planes
+// transposed, [plane][k][slot < kpadt][row] (the adjoint GEMM's K-major A:
+// M = the packed (j, r3) slots, K = rows).
 __global__ void build_warena_kernel(const TcDesc* __restrict__ tcd, const float2* __restrict__ varena,
                                     const float2* __restrict__ u2arena, const int* __restrict__ kofs, int64_t ncols,
                                     int q, int n1, int n2, int nt2, int64_t rows_pad, int64_t kpad, float wsc,
-                                    __half* __restrict__ wa, float2* __restrict__ wadj) {
+                                    __half* __restrict__ wa, __half* __restrict__ wt, int64_t kpadt) {
     using namespace sm100;
     const int64_t t = blockIdx.x;  // component-major tensor index k ncols + j
     const int k = int(t / ncols);
@@ -1017,7 +1034,6 @@ __global__ void build_warena_kernel(const TcDesc* __restrict__ tcd, const float2
     for (int c = 0; c < r3; ++c) {
         uint64_t w = 0;
         for (int b = 0; b < r2; ++b) cfma2v(w, V[(c + r3 * b) * TC_TI1], U[b]);
-        if (wadj) wadj[((int64_t(k) * gridDim.y + tile) * kpad + kofs[t] + c) * TC_ROWS + row] = f2_unpack(w);
         asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(w) : "l"(sc2));
         uint32_t hi, lo;
         f16_split2(w, hi, lo);
@@ -1025,6 +1041,15 @@ __global__ void build_warena_kernel(const TcDesc* __restrict__ tcd, const float2
         o[plane + c] = static_cast<unsigned short>(lo);          // Re lo
         o[2 * plane + c] = static_cast<unsigned short>(hi >> 16);  // Im hi
         o[3 * plane + c] = static_cast<unsigned short>(lo >> 16);  // Im lo
+        if (wt) {  // the adjoint GEMM's A operand: [plane][k][slot][row], rows contiguous
+            const int64_t tp = int64_t(q) * kpadt * rows_pad;
+            unsigned short* ot = reinterpret_cast<unsigned short*>(wt) +
+                                 (int64_t(k) * kpadt + kofs[t] + c) * rows_pad + int64_t(tile) * TC_ROWS + row;
+            ot[0] = static_cast<unsigned short>(hi);
+            ot[tp] = static_cast<unsigned short>(lo);
+            ot[2 * tp] = static_cast<unsigned short>(hi >> 16);
+            ot[3 * tp] = static_cast<unsigned short>(lo >> 16);
+        }
     }
 }
 

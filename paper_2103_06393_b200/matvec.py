@@ -234,13 +234,14 @@ class DeviceStore:
         return self.row_block([k * self.num_voxels + i1 + n1 * (i2 + n2 * i3)])[0, j]
 
     def kernel_paths(self):
-        """{'forward': 'tcgen05+warena' | 'tcgen05' | 'cuda-core', 'adjoint': ...}
-        for this store ('tcgen05+warena': the forward's A operand from the
-        precomputed W arena, no producer warps)."""
+        """{'forward': 'tcgen05+warena' | 'tcgen05' | 'cuda-core', 'adjoint':
+        'tcgen05+gemm' | 'tcgen05' | 'cuda-core'} for this
+        store ('tcgen05+warena': the forward's A operand from the precomputed W
+        arena; 'tcgen05+gemm': the adjoint as one GEMM on the transposed arena)."""
         f = ctypes.c_int32()
         a = ctypes.c_int32()
         _check(lib().tm_store_kernels(self.handle, ctypes.byref(f), ctypes.byref(a)))
-        name = {2: "tcgen05+warena", 1: "tcgen05", 0: "cuda-core"}
+        name = {3: "tcgen05+gemm", 2: "tcgen05+warena", 1: "tcgen05", 0: "cuda-core"}
         return {"forward": name[f.value], "adjoint": name[a.value]}  # adjoint 2: W tiles from the arena
 
     def opcounts(self, p=1):

@@ -1,7 +1,8 @@
-"""The W arena (fwd_tc_kernel<..., WA>, adj_tc_kernel<..., WA>): for stores
-whose W = U1 x1 G x2 U2 fits the memory budget, the forward's A operand is
-precomputed once (build_warena_kernel) and streamed by TMA — no producer
-warps — and the adjoint's consumers read fp32 W tiles instead of forming them.  Checked
+"""The W arena (fwd_tc_kernel<..., WA>): for stores whose W = U1 x1 G x2 U2
+fits the memory budget, the forward's A operand is precomputed once
+(build_warena_kernel) and streamed by TMA — no producer warps — and the
+adjoint runs as one GEMM, G = conj(W)^T Phi on the transposed arena
+(fwd_tc_kernel<..., WA, ADJ>), then z = sum conj(U3) G (adjg_contract_kernel).  Checked
 against the oracle and against the producer-warp forward of the same store
 (TMB_WARENA=0 switches a store back at run time), over ragged ranks, grids
 whose n2 is not a multiple of 32, one and many right-hand sides, split final
@@ -31,7 +32,7 @@ def test_warena_products_match_oracle_and_producer_path(oracle, product, dims, q
     O, P = oracle, product
     cc = ragged_store(dims, q, m, rlo, rhi, seed=m + q + p)
     ds = P.DeviceStore.from_compressed(cc, "c64")
-    assert ds.kernel_paths() == {"forward": "tcgen05+warena", "adjoint": "tcgen05+warena"}
+    assert ds.kernel_paths() == {"forward": "tcgen05+warena", "adjoint": "tcgen05+gemm"}
     ref = O.OracleStore(cc.rounded_c64())
     x = _c64(cn01(m, p, 11))
     phi = _c64(cn01(cc.rows, p, 12))
@@ -42,13 +43,16 @@ def test_warena_products_match_oracle_and_producer_path(oracle, product, dims, q
     assert ds.kernel_paths() == {"forward": "tcgen05", "adjoint": "tcgen05"}
     yp, zp = ds.forward(x), ds.adjoint(phi)
     assert rel(yp, yo) <= 1e-5 and rel(zp, zo) <= 1e-5
-    # the same W bits: the forwards differ only where final-wave splits differ;
-    # the adjoint consumers read exactly the W they would have computed
-    assert rel(yw, yp) <= 1e-6
-    if p == 1:
-        assert rel(zw, zp) == 0.0
+    # the same W bits: the forwards differ only where final-wave splits differ
+    print(f"forward {rel(yw, yo):.2e} / {rel(yp, yo):.2e}, adjoint gemm {rel(zw, zo):.2e} / consumers {rel(zp, zo):.2e}")
+    assert rel(yw, yp) <= 1e-6 and rel(zw, zp) <= 1e-5
     monkeypatch.delenv("TMB_WARENA")
     assert rel(ds.forward(x), yw) == 0.0 and rel(ds.adjoint(phi), zw) == 0.0  # deterministic
+    # TMB_ADJ_GEMM=0: the consumer-warp adjoint (forming W) on an arena store
+    monkeypatch.setenv("TMB_ADJ_GEMM", "0")
+    assert ds.kernel_paths() == {"forward": "tcgen05+warena", "adjoint": "tcgen05"}
+    za = ds.adjoint(phi)
+    assert rel(za, zo) <= 1e-5 and rel(za, zp) == 0.0
 
 
 def test_warena_budget(oracle, product, monkeypatch):
