@@ -1432,9 +1432,17 @@ void run_adjoint_gemm(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, 
                                                   CU_TENSOR_MAP_SWIZZLE_32B);
         for (int64_t t0 = 0; t0 < g.ntiles; t0 += wave) {  // one launch per wave (see run_forward_pass)
             const int64_t tiles = std::min<int64_t>(g.ntiles - t0, wave);
+            // a final partial wave splits each tile's K (row) stages into parts:
+            // partial G tiles to ypart, summed in part order by adjg_split_reduce_kernel
+            g.split = best_split(tiles, wave, 8);
+            if (const char* e = std::getenv("TMB_ADJ_NOSPLIT")) if (*e && *e != '0') g.split = 1;
             g.tile0 = t0;
             g.t_begin = 0;
-            g.t_end = tiles;
+            g.t_end = tiles * g.split;
+            g.ypart = nullptr;
+            if (g.split > 1)
+                g.ypart = static_cast<float2*>(s->ypart.get(size_t(tiles) * g.split * (1 + g.pair) * g.nmma * g.nh3 *
+                                                            TC_ROWS * sizeof(float2)));
             if (g.pair) {
                 cudaLaunchConfig_t cfg{};
                 cfg.gridDim = dim3(grid);
@@ -1458,6 +1466,12 @@ void run_adjoint_gemm(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, 
                 ksingle<<<grid, TC_THREADS, smem, st>>>(bmap, s->wt_map, s->d_tcd, s->d_varena, s->d_u2arena,
                                                         s->d_kcr, s->d_kofs, g, nullptr, 0, G, 0, rsum, phimax);
                 launched(cudaSuccess, "fwd_tc_kernel<adjoint GEMM>");
+            }
+            if (g.split > 1) {
+                const int64_t n = tiles * (1 + g.pair) * g.nmma * g.nh3 * TC_ROWS;
+                adjg_split_reduce_kernel<<<unsigned(std::min<int64_t>((n + 255) / 256, 4096)), 256, 0, st>>>(g, tiles,
+                                                                                                           G);
+                launched(cudaSuccess, "adjg_split_reduce_kernel");
             }
         }
         adjg_contract_kernel<<<unsigned(s->ncols), 256, 0, st>>>(

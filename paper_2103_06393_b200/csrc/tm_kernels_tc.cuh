@@ -731,19 +731,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             // reduce kernel sums the parts into y in a fixed order
             const bool part_out = g.split > 1;
             const bool eok = ADJ || part_out || (ei1 < g.n1 && ei2 < g.n2);
-            float2* yp = ADJ ? y + int64_t(tl.k) * g.nt * g.gslots + int64_t(tl.i1_0 / TC_TI1) * TC_ROWS + row
-                         : part_out ? g.ypart + ((t * (1 + g.pair) + int64_t(rank)) * span) * TC_ROWS + row
-                                    : y + int64_t(tl.k) * nv3 + ei1 + int64_t(g.n1) * ei2;
+            float2* yp = part_out ? g.ypart + ((t * (1 + g.pair) + int64_t(rank)) * span) * TC_ROWS + row
+                         : ADJ    ? y + int64_t(tl.k) * g.nt * g.gslots + int64_t(tl.i1_0 / TC_TI1) * TC_ROWS + row
+                                  : y + int64_t(tl.k) * nv3 + ei1 + int64_t(g.n1) * ei2;
             const int64_t pl = int64_t(g.n1) * g.n2;
             // output of tile column nl (N row n = i3_0 + nl = i3 * p + c)
             auto put = [&](int nl, float2 v) {
+                if (part_out) {
+                    yp[int64_t(TC_ROWS) * nl] = v;
+                    return;
+                }
                 if (ADJ) {  // G[k][n][slot]: a warp's 32 slots are contiguous
                     const int n = tl.i3_0 + nl;
                     if (n < g.nt) yp[int64_t(n) * g.gslots] = v;
-                    return;
-                }
-                if (part_out) {
-                    yp[int64_t(TC_ROWS) * nl] = v;
                     return;
                 }
                 const int n = tl.i3_0 + nl;
@@ -915,6 +915,33 @@ __global__ void fwd_split_reduce_kernel(TcGeom g, int64_t tiles, float2* __restr
             acc.y += v.y;
         }
         y[ldy * c + int64_t(tl.k) * nv3 + i1 + int64_t(g.n1) * i2 + pl * i3] = acc;
+    }
+}
+
+// The same for the adjoint GEMM's split final wave (fwd_tc_kernel<.., ADJ>,
+// parts = K-stage ranges of the rows): the parts of each (slot tile, n) are
+// summed in part order into G[k][n][slot].
+__global__ void adjg_split_reduce_kernel(TcGeom g, int64_t tiles, float2* __restrict__ G) {
+    const int span = g.nmma * g.nh3;
+    const int nr = 1 + g.pair;
+    const int64_t total = tiles * nr * span * TC_ROWS;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int row = int(e % TC_ROWS);
+        int64_t rest = e / TC_ROWS;
+        const int i3l = int(rest % span);
+        rest /= span;
+        const int rank = int(rest % nr);
+        const int64_t tt = rest / nr;
+        const TcTile tl = tc_tile(g, tt * g.split, uint32_t(rank));
+        const int n = tl.i3_0 + i3l;
+        if (n >= g.nt) continue;
+        float2 acc = make_float2(0.f, 0.f);
+        for (int p = 0; p < g.split; ++p) {
+            const float2 v = g.ypart[(((tt * g.split + p) * nr + rank) * span + i3l) * TC_ROWS + row];
+            acc.x += v.x;
+            acc.y += v.y;
+        }
+        G[(int64_t(tl.k) * g.nt + n) * g.gslots + int64_t(tl.i1_0 / TC_TI1) * TC_ROWS + row] = acc;
     }
 }
 

@@ -48,6 +48,11 @@ def test_warena_products_match_oracle_and_producer_path(oracle, product, dims, q
     assert rel(yw, yp) <= 1e-6 and rel(zw, zp) <= 1e-5
     monkeypatch.delenv("TMB_WARENA")
     assert rel(ds.forward(x), yw) == 0.0 and rel(ds.adjoint(phi), zw) == 0.0  # deterministic
+    # the adjoint GEMM's final partial wave split into row (K-stage) parts vs unsplit
+    monkeypatch.setenv("TMB_ADJ_NOSPLIT", "1")
+    zn = ds.adjoint(phi)
+    monkeypatch.delenv("TMB_ADJ_NOSPLIT")
+    assert rel(zn, zo) <= 1e-5 and rel(zn, zw) <= 1e-6
     # TMB_ADJ_GEMM=0: the consumer-warp adjoint (forming W) on an arena store
     monkeypatch.setenv("TMB_ADJ_GEMM", "0")
     assert ds.kernel_paths() == {"forward": "tcgen05+warena", "adjoint": "tcgen05"}
