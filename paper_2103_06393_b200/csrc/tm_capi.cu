@@ -25,6 +25,7 @@
 #include "tm_kernels_tc.cuh"
 #include "tm_adj_tc.cuh"
 #include "tm_adj2_tc.cuh"
+#include "tm_k3w_tc.cuh"
 #include "tm_tmap.h"
 #include "tm_io_internal.hpp"
 
@@ -163,6 +164,15 @@ struct tm_store {
     DevBuf gbuf, phit;     // per call: G and the row-contiguous Phi planes
     int64_t warena_rows = 0;
     CUtensorMap warena_map{};
+    // K3W (tm_k3w_tc.cuh, many right-hand sides on a W-arena store): per-slot
+    // U3S / descriptor tables and the unswizzled W-plane map, built on first use
+    __half* d_k3pa = nullptr;      // the W arena's fp16 planes on K3W's padded slot stream
+    __half* d_k3b1 = nullptr;      // GEMM1's B operand per (component, stage, i3 block)
+    uint32_t* d_k3flag = nullptr;  // [q][kpad8 / 16] column-end bits per stage
+    int* d_k3kc = nullptr;         // [q] padded slots per component
+    int* d_k3gend = nullptr;       // [q][nks] W stages needed through each GEMM2 stage
+    int64_t k3_kpad8 = 0;
+    CUtensorMap k3_wmap{};
     // tensor-core adjoint: chunk-aligned, i3-contiguous U3 planes
     bool tca_ok = false;
     __half* d_aplanes = nullptr;
@@ -210,6 +220,11 @@ struct tm_store {
         if (d_u2arena) cudaFree(d_u2arena);
         if (d_warena) cudaFree(d_warena);
         if (d_wt) cudaFree(d_wt);
+        if (d_k3pa) cudaFree(d_k3pa);
+        if (d_k3b1) cudaFree(d_k3b1);
+        if (d_k3flag) cudaFree(d_k3flag);
+        if (d_k3kc) cudaFree(d_k3kc);
+        if (d_k3gend) cudaFree(d_k3gend);
         if (d_kcr) cudaFree(d_kcr);
         if (d_aplanes) cudaFree(d_aplanes);
         for (auto& a : adjp) {
@@ -1021,9 +1036,182 @@ void run_forward_tc(const tm_store* s, const float2* x, int64_t ldx, int64_t p, 
     }
 }
 
+// K3W (tm_k3w_tc.cuh): the batched forward of a W-arena store at the
+// algorithmic cost (T decompressed once per tile from the arena on CUDA
+// cores, Y += T X on tcgen05), for p >= TMB_K3_PMIN (default 16) right-hand
+// sides and r3 <= 16; TMB_K3=0 disables it (the x-in-B arena forward).
+bool k3w_ok(const tm_store* s, int64_t p) {
+    if (!s->d_warena || warena_disabled() || tc_disabled() || s->rmax[2] > 16 || s->ncols >= (int64_t(1) << 25))
+        return false;
+    if (const char* e = std::getenv("TMB_K3")) if (*e == '0') return false;
+    int64_t pmin = 16;
+    if (const char* e = std::getenv("TMB_K3_PMIN")) if (std::atoll(e) > 0) pmin = std::atoll(e);
+    return p >= pmin;
+}
+
+void ensure_k3w(tm_store* s, cudaStream_t st) {
+    if (s->d_k3pa) return;
+    const int64_t n3 = s->dims[2], m = s->ncols;
+    const int nt3 = int((n3 + K3_NI3 - 1) / K3_NI3);
+    // K3W's slot stream (tm_k3w_tc.cuh): columns back to back, at most two
+    // overlapping a 16-slot stage; flags per stage: bit 0 half 1 present,
+    // bit 1 it ends in the stage, bit 2 half 0 continues the previous stage
+    std::vector<int> poff(size_t(s->q * m)), kc8(size_t(s->q));
+    std::vector<std::vector<uint32_t>> flags(size_t(s->q));
+    std::vector<std::vector<int2>> sdesc(size_t(s->q));
+    std::vector<std::vector<int>> cends(size_t(s->q), std::vector<int>(size_t(m)));  // stage where column j ends
+    int64_t kpad8 = 16;
+    for (int k = 0; k < s->q; ++k) {
+        int64_t pos = 0;
+        auto& fk = flags[size_t(k)];
+        auto& dk = sdesc[size_t(k)];
+        auto& cend = cends[size_t(k)];
+        std::vector<int> over;  // columns overlapping each stage so far
+        auto stage_at = [&](size_t stg) {
+            if (stg >= fk.size()) {
+                fk.resize(stg + 1, 0u);
+                dk.resize(stg + 1, make_int2(-1, -1));
+                over.resize(stg + 1, 0);
+            }
+        };
+        for (int64_t j = 0; j < m; ++j) {
+            const int r3 = s->ranks[size_t((j * s->q + k) * 3 + 2)];
+            size_t s0 = size_t(pos / 16);
+            stage_at(s0);
+            if (over[s0] == 2) {  // a third column would overlap the stage: start the next one
+                pos = int64_t(s0 + 1) * 16;
+                s0 = size_t(pos / 16);
+                stage_at(s0);
+            }
+            const int64_t end = pos + r3 - 1;
+            const size_t s1 = size_t(end / 16);
+            const int t = int(k * m + j);
+            if (over[s0] == 0) {
+                dk[s0].x = t;  // half 0: ends in this stage (it starts at slot 0)
+            } else {
+                dk[s0].y = t;  // half 1
+                fk[s0] |= 1u;
+                if (s1 == s0) fk[s0] |= 2u;
+            }
+            ++over[s0];
+            if (s1 > s0) {  // continues as half 0 of the next stage
+                stage_at(s1);
+                dk[s1].x = t;
+                fk[s1] |= 4u;
+                over[s1] = 1;
+            }
+            cend[size_t(j)] = int(s1);
+            poff[size_t(t)] = int(pos);
+            pos = end + 1;
+        }
+        kc8[size_t(k)] = int(pos);
+        kpad8 = std::max<int64_t>(kpad8, (pos + 15) / 16 * 16);
+    }
+    if (kpad8 >= (int64_t(1) << 30)) throw TmError(TM_CAPACITY_ERROR, "K3W: slot stream too long");
+    const int64_t nstg = kpad8 / 16;
+    // gend[k][kk]: the W stages through the one where column 16 (kk + 1) - 1 ends
+    const int64_t nks = (m + 15) / 16;
+    std::vector<int> gend(size_t(s->q * nks), 0);
+    for (int k = 0; k < s->q; ++k)
+        for (int64_t kk = 0; kk < nks; ++kk)
+            gend[size_t(k * nks + kk)] = cends[size_t(k)][size_t(std::min<int64_t>(16 * (kk + 1), m) - 1)] + 1;
+    std::vector<uint32_t> fl(size_t(s->q * nstg), 0u);
+    std::vector<int2> sd(size_t(s->q * nstg), make_int2(-1, -1));
+    for (int k = 0; k < s->q; ++k) {
+        std::copy(flags[size_t(k)].begin(), flags[size_t(k)].end(), fl.begin() + k * nstg);
+        std::copy(sdesc[size_t(k)].begin(), sdesc[size_t(k)].end(), sd.begin() + k * nstg);
+    }
+    const uint64_t rows_pad = uint64_t(s->warena_rows), kp = uint64_t(kpad8);
+    const size_t pab = size_t(4) * s->q * rows_pad * kp * sizeof(__half);
+    const size_t b1b = size_t(s->q) * size_t(nstg) * size_t(nt3) * K3_B1_BYTES;
+    int* d_poff = nullptr;
+    int2* d_sd = nullptr;
+    CK(cudaMalloc(&s->d_k3pa, pab));
+    CK(cudaMalloc(&s->d_k3b1, b1b));
+    CK(cudaMalloc(&s->d_k3flag, fl.size() * sizeof(uint32_t)));
+    CK(cudaMalloc(&s->d_k3kc, kc8.size() * sizeof(int)));
+    CK(cudaMalloc(&s->d_k3gend, gend.size() * sizeof(int)));
+    CK(cudaMemcpy(s->d_k3gend, gend.data(), gend.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&d_poff, poff.size() * sizeof(int)));
+    CK(cudaMalloc(&d_sd, sd.size() * sizeof(int2)));
+    s->device_bytes += int64_t(pab + b1b + fl.size() * 4 + kc8.size() * 4);
+    s->k3_kpad8 = kpad8;
+    CK(cudaMemcpy(s->d_k3flag, fl.data(), fl.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(s->d_k3kc, kc8.data(), kc8.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_poff, poff.data(), poff.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_sd, sd.data(), sd.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    CK(cudaMemsetAsync(s->d_k3pa, 0, pab, st));
+    build_k3w_pa_kernel<<<unsigned(s->q * m), 256, 0, st>>>(s->d_desc, s->d_kofs, d_poff, m, s->q, s->d_warena,
+                                                           int64_t(rows_pad), s->kpad, kpad8, s->d_k3pa);
+    launched(cudaSuccess, "build_k3w_pa_kernel");
+    build_k3w_b1_kernel<<<unsigned(s->q * nstg * nt3), 256, 0, st>>>(
+        s->d_desc, s->d_tcd, static_cast<const float2*>(s->d_arena), d_sd, d_poff, int(n3), nt3, nstg, s->d_k3b1);
+    launched(cudaSuccess, "build_k3w_b1_kernel");
+    CK(cudaStreamSynchronize(st));
+    CK(cudaFree(d_poff));
+    CK(cudaFree(d_sd));
+    s->k3_wmap = make_tmap_3d_f16(s->d_k3pa, kp, rows_pad, uint64_t(4 * s->q), kp * 2, rows_pad * kp * 2, 16, TC_ROWS,
+                                  CU_TENSOR_MAP_SWIZZLE_32B);
+}
+
+void run_forward_k3w(tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy, cudaStream_t st) {
+    ensure_k3w(s, st);
+    K3Geom g{};
+    g.ncols = s->ncols;
+    g.n1 = int(s->dims[0]);
+    g.n2 = int(s->dims[1]);
+    g.n3 = int(s->dims[2]);
+    g.q = s->q;
+    g.nt1 = (g.n1 + TC_TI1 - 1) / TC_TI1;
+    g.nt2 = (g.n2 + TC_TI2 - 1) / TC_TI2;
+    g.nt3 = (g.n3 + K3_NI3 - 1) / K3_NI3;
+    g.ntiles = int64_t(g.q) * g.nt1 * g.nt2 * g.nt3;
+    g.nks = int((s->ncols + 15) / 16);
+    g.chain = tc_chain();
+    // |T| <= r3 max |arena| < r3 2^14 (|U3 2^-e3| <= 1): T 2^-ceil(log2 r3) stays below 2^14
+    int lr = 0;
+    while ((1 << lr) < s->rmax[2]) ++lr;
+    // D1 = 2^12 wsc T (B1 carries U3 2^12): tsc takes it below 2^14, the epilogue undoes wsc x tsc x sb
+    g.tsc = ldexpf(1.f, -12 - lr);
+    g.wsc = fp16_scale(s->vmax * 1.0001f) * TC_U3_SCALE;
+    const size_t smem = 1024 + size_t(K3_NST) * (K3_A_STAGE + K3_B_STAGE) + size_t(K3_NWS) * K3_W_STAGE +
+                        (2 * K3_NST + 2 * K3_NWS + 2 * K3_ND1 + 2) * 8 + 16;
+    if (smem > kSmemMax) throw TmError(TM_CAPACITY_ERROR, "K3W forward: shared-memory plan too large");
+    CK(cudaFuncSetAttribute(fwd_k3w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const unsigned grid = unsigned(std::min<int64_t>(g.ntiles, num_sms(dev)));
+    float* rsum = static_cast<float*>(s->rsum.get(size_t(grid) * K3_YCOLS * TC_ROWS * sizeof(float)));
+    const int64_t kpad = (s->ncols + 15) / 16 * 16;
+    __half* planes = static_cast<__half*>(s->xbplanes.get(size_t(4) * 2 * K3_P * kpad * sizeof(__half)));
+    float* xmax = static_cast<float*>(s->scal.get(2 * sizeof(float))) + 1;
+    for (int64_t c0 = 0; c0 < p; c0 += K3_P) {
+        const int pb = int(std::min<int64_t>(K3_P, p - c0));
+        CK(cudaMemsetAsync(xmax, 0, sizeof(float), st));
+        xmax_kernel<<<unsigned(std::min<int64_t>((s->ncols * pb + 255) / 256, 1184)), 256, 0, st>>>(
+            x + ldx * c0, ldx, s->ncols, pb, xmax);
+        launched(cudaSuccess, "xmax_kernel");
+        k3_xplanes_kernel<<<unsigned(std::min<int64_t>((K3_P * kpad + 255) / 256, 4096)), 256, 0, st>>>(
+            x + ldx * c0, ldx, s->ncols, pb, kpad, xmax, planes);
+        launched(cudaSuccess, "k3_xplanes_kernel");
+        const CUtensorMap xmap = make_tmap_3d_f16(planes, uint64_t(kpad), uint64_t(2 * K3_P), 4, uint64_t(kpad) * 2,
+                                                  uint64_t(2 * K3_P) * kpad * 2, 16, 2 * K3_P,
+                                                  CU_TENSOR_MAP_SWIZZLE_32B);
+        g.p = pb;
+        fwd_k3w_kernel<<<grid, K3_THREADS, smem, st>>>(xmap, s->k3_wmap, s->d_k3b1, s->d_k3kc, s->d_k3flag,
+                                                       s->k3_kpad8 / 16, s->d_k3gend, g, y + ldy * c0, ldy, rsum,
+                                                       xmax);
+        launched(cudaSuccess, "fwd_k3w_kernel");
+    }
+}
+
 void forward_dev(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy, cudaStream_t st,
                  const HostPipe* hook = nullptr, int kb = 0, int ke = -1) {
     if (ke < 0) ke = s->q;
+    if (!hook && kb == 0 && ke == s->q && k3w_ok(s, p)) {
+        run_forward_k3w(s, static_cast<const float2*>(x), ldx, p, static_cast<float2*>(y), ldy, st);
+        return;
+    }
     if (s->tc_ok && !tc_disabled()) {
         run_forward_tc(s, static_cast<const float2*>(x), ldx, p, static_cast<float2*>(y), ldy, st, hook, kb, ke);
         return;
@@ -1638,7 +1826,7 @@ void with_host_io(tm_store* s, const void* in, int64_t ldin, int64_t inrows, int
 // kernels block by block (HostPipe).  Returns false when the product does
 // not take the tensor-core path (the caller then uses with_host_io).
 bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy) {
-    if (!(s->tc_ok && !tc_disabled())) return false;
+    if (!(s->tc_ok && !tc_disabled()) || k3w_ok(s, p)) return false;
     const size_t cs = s->csize();
     void* din = s->xin.get(size_t(std::max<int64_t>(s->ncols * p, 1)) * cs);
     void* dout = s->yout.get(size_t(std::max<int64_t>(s->rows() * p, 1)) * cs);
