@@ -172,7 +172,7 @@ struct tm_store {
     int* d_k3kc = nullptr;         // [q] padded slots per component
     int* d_k3gend = nullptr;       // [q][nks] W stages needed through each GEMM2 stage
     int64_t k3_kpad8 = 0;
-    CUtensorMap k3_wmap{};
+
     // tensor-core adjoint: chunk-aligned, i3-contiguous U3 planes
     bool tca_ok = false;
     __half* d_aplanes = nullptr;
@@ -1142,7 +1142,8 @@ void ensure_k3w(tm_store* s, cudaStream_t st) {
     CK(cudaMemcpy(d_sd, sd.data(), sd.size() * sizeof(int2), cudaMemcpyHostToDevice));
     CK(cudaMemsetAsync(s->d_k3pa, 0, pab, st));
     build_k3w_pa_kernel<<<unsigned(s->q * m), 256, 0, st>>>(s->d_desc, s->d_kofs, d_poff, m, s->q, s->d_warena,
-                                                           int64_t(rows_pad), s->kpad, kpad8, s->d_k3pa);
+                                                           int64_t(rows_pad), s->kpad, nstg,
+                                                           reinterpret_cast<unsigned char*>(s->d_k3pa));
     launched(cudaSuccess, "build_k3w_pa_kernel");
     build_k3w_b1_kernel<<<unsigned(s->q * nstg * nt3), 256, 0, st>>>(
         s->d_desc, s->d_tcd, static_cast<const float2*>(s->d_arena), d_sd, d_poff, int(n3), nt3, nstg, s->d_k3b1);
@@ -1150,8 +1151,6 @@ void ensure_k3w(tm_store* s, cudaStream_t st) {
     CK(cudaStreamSynchronize(st));
     CK(cudaFree(d_poff));
     CK(cudaFree(d_sd));
-    s->k3_wmap = make_tmap_3d_f16(s->d_k3pa, kp, rows_pad, uint64_t(4 * s->q), kp * 2, rows_pad * kp * 2, 16, TC_ROWS,
-                                  CU_TENSOR_MAP_SWIZZLE_32B);
 }
 
 void run_forward_k3w(tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy, cudaStream_t st) {
@@ -1198,7 +1197,7 @@ void run_forward_k3w(tm_store* s, const float2* x, int64_t ldx, int64_t p, float
                                                   uint64_t(2 * K3_P) * kpad * 2, 16, 2 * K3_P,
                                                   CU_TENSOR_MAP_SWIZZLE_32B);
         g.p = pb;
-        fwd_k3w_kernel<<<grid, K3_THREADS, smem, st>>>(xmap, s->k3_wmap, s->d_k3b1, s->d_k3kc, s->d_k3flag,
+        fwd_k3w_kernel<<<grid, K3_THREADS, smem, st>>>(xmap, reinterpret_cast<const unsigned char*>(s->d_k3pa), s->d_k3b1, s->d_k3kc, s->d_k3flag,
                                                        s->k3_kpad8 / 16, s->d_k3gend, g, y + ldy * c0, ldy, rsum,
                                                        xmax);
         launched(cudaSuccess, "fwd_k3w_kernel");

@@ -17,13 +17,15 @@
 // that would be the third starts the next stage).  Half 0 of a stage is its
 // first column, which ends in the stage (it may have started in the previous
 // one: a straddler), half 1 the second, which may continue into the next
-// stage as that stage's half 0; the converters add the two partials.  GEMM1 per stage: A1 = the stage's W planes (TMA, SW32), B1 = a
-// per-store block-diagonal table ([k][stage][i3 block] 4 fp16 planes of 16 n
+// stage as that stage's half 0; the converters add the two partials.
+// GEMM1 per stage: A1 = the stage's W planes (one bulk copy of a pre-swizzled
+// 16 KB block), B1 = a per-store block-diagonal table ([k][stage][i3 block] 4 fp16 planes of 16 n
 // x 16 slots: n = half c x 8 + i3 x 2 + (Tr, Ti); the column of half c; U3
-// 2^-e3 x 2^12 as the fp16 split; bulk-copied) — 6 tcgen05.mma (M = 128,
-// N = 16): D1 = Wr B1a + Wi B1b, each as hi.hi + hi.lo + lo.hi, into one of
-// 8 TMEM buffers of 16 columns.  Converter warps read D1 (tcgen05.ld), scale
-// and split T into the A operand of GEMM2 at K position j % 16 (4 M = 128
+// 2^-e3 x 2^12 as the fp16 split; bulk-copied) — 4 tcgen05.mma (M = 128):
+// D1 = Wr B1a + Wi B1b as hi.hi + hi.lo + lo.hi, the hi planes of W against
+// [B hi ; B lo] in one N = 32 MMA each (the hi.lo terms land in columns
+// 16-31), into one of 8 TMEM buffers of 32 columns.  Converter warps read
+// D1 (tcgen05.ld), scale and split T into the A operand of GEMM2 at K position j % 16 (4 M = 128
 // blocks, one per i3 of the tile).  GEMM2 is the earlier K3 design: B = X as
 // fp16-split planes [Xr | Xi], [-Xi | Xr] (N = 64), 6 tcgen05.mma per i3
 // block per 16 columns, [Yr | Yi] += Tr [Xr | Xi] + Ti [-Xi | Xr]; chained
@@ -33,7 +35,7 @@
 //   warp 0      TMA producer of the X planes (B of GEMM2)
 //   warp 1      MMA issuer (GEMM1 per stage, GEMM2 per 16 columns)
 //   warp 2      loader of the W stages (A1 planes by TMA, B1 block by bulk copy)
-//   warp 3      TMEM allocator (512 columns: GEMM2 accumulator 256, D1 8 x 16)
+//   warp 3      TMEM allocator (512 columns: GEMM2 accumulator 256, D1 8 x 32)
 //   warps 4-11  converters: warps 4-7 even stages, 8-11 odd stages (D1 -> A2)
 //   warps 12-15 chain fold + epilogue
 #pragma once
@@ -55,7 +57,7 @@ constexpr int K3_A_STAGE = K3_NI3 * K3_A_BLOCK;  // 64 KB
 constexpr int K3_B_PLANE = 2 * K3_P * 32;        // 64 rows x 16 fp16
 constexpr int K3_B_STAGE = 4 * K3_B_PLANE;       // [Xr|Xi] hi, [-Xi|Xr] hi, [Xr|Xi] lo, [-Xi|Xr] lo
 constexpr int K3_YCOLS = K3_NI3 * 2 * K3_P;      // TMEM columns of the GEMM2 accumulator
-constexpr int K3_ND1 = 8;                        // D1 (GEMM1 output) TMEM buffers of 16 columns
+constexpr int K3_ND1 = 8;                        // D1 (GEMM1 output) TMEM buffers of 32 columns (hi and lo halves)
 constexpr int K3_TCOLS = 512;                    // TMEM allocation
 constexpr int K3_THREADS = 16 * 32;
 // W stage: A1 = 4 planes [128 rows][16 slots] fp16 (SW32), then B1 = 4 planes [16 n][16 slots] fp16 (SW32)
@@ -103,7 +105,7 @@ __device__ __forceinline__ void mbar_arrive_n(uint64_t* bar, uint32_t n) {
 }
 
 __global__ void __launch_bounds__(K3_THREADS, 1)
-    fwd_k3w_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
+    fwd_k3w_kernel(const __grid_constant__ CUtensorMap xmap, const unsigned char* __restrict__ patab,
                    const __half* __restrict__ b1tab, const int* __restrict__ kc,
                    const uint32_t* __restrict__ sflag, int64_t nstg, const int* __restrict__ gend, K3Geom g, float2* __restrict__ y, int64_t ldy,
                    float* __restrict__ rsum, const float* __restrict__ xmax) {
@@ -149,7 +151,6 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
     fence_proxy_async_smem();
     if (warp == 3) tmem_alloc(tmem_slot, K3_TCOLS);
     if (warp == 0 && lane == 0) tma_prefetch_desc(&xmap);
-    if (warp == 2 && lane == 0) tma_prefetch_desc(&wmap);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -179,6 +180,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
         if (elect_one()) {
             const uint32_t id2 = umma_idesc_f16(TC_ROWS, 2 * K3_P, false, false);
             const uint32_t id1 = umma_idesc_f16(TC_ROWS, 16, false, false);
+            const uint32_t id1w = umma_idesc_f16(TC_ROWS, 32, false, false);
             uint32_t s = 0, ph = 0, gch = 0;
             uint32_t sg = 0;  // W stages issued (all tiles): W ring slot sg % K3_NWS, D1 buffer sg % K3_ND1
             for (int64_t t = tstart; t < g.ntiles; t += tstep) {
@@ -203,26 +205,29 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                         const uint64_t Bal = umma_smem_desc(b0 + K3_B1_PLANE, 256, 6);
                         const uint64_t Bbh = umma_smem_desc(b0 + 2 * K3_B1_PLANE, 256, 6);
                         const uint64_t Bbl = umma_smem_desc(b0 + 3 * K3_B1_PLANE, 256, 6);
-                        const uint32_t d = tD1 + db * 16u;
-                        // D1 = Wr B1a + Wi B1b (Tr = Wr U3r - Wi U3i, Ti = Wr U3i + Wi U3r in B1's columns)
-                        mma_f16(d, Arh, Bah, id1, 0);
-                        mma_f16(d, Arh, Bal, id1, 1);
+                        const uint32_t d = tD1 + db * 32u;
+                        // D1 = Wr B1a + Wi B1b (Tr = Wr U3r - Wi U3i, Ti = Wr U3i + Wi U3r in B1's
+                        // columns): the hi planes of A meet [B hi ; B lo] in one N = 32 MMA (columns
+                        // 16-31 take the hi.lo terms; the converters add the halves), so each A
+                        // plane is read once
+                        mma_f16(d, Arh, Bah, id1w, 0);
                         mma_f16(d, Arl, Bah, id1, 1);
-                        mma_f16(d, Aih, Bbh, id1, 1);
-                        mma_f16(d, Aih, Bbl, id1, 1);
+                        mma_f16(d, Aih, Bbh, id1w, 1);
                         mma_f16(d, Ail, Bbh, id1, 1);
+                        (void)Bal;
+                        (void)Bbl;
                         mma_commit(&wempty[ws]);
                         mma_commit(&dfull[db]);
                         ++snext;
                         ++sg;
                     }
                 };
-                int gnext = ge[0];
                 int cpos = 0;
                 for (int kk = 0; kk < g.nks; ++kk) {
-                    const int need = gnext;
-                    if (kk + 1 < g.nks) gnext = ge[kk + 1];
-                    gemm1_until(need);  // every W stage holding a column of GEMM2 stage kk
+                    // GEMM1 of every W stage holding a column of GEMM2 stages kk and kk + 1,
+                    // issued before GEMM2 kk: the tensor pipe runs in order, so the converters
+                    // fill stage kk + 1 while GEMM2 kk executes (the A ring holds two stages)
+                    gemm1_until(ge[kk + 1 < g.nks ? kk + 1 : kk]);
                     if (cpos == 0) {
                         mbar_wait(cfree, (gch & 1) ^ 1);  // the previous chain has been folded
                         tc_fence_after();
@@ -262,9 +267,6 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                         cpos = 0;
                         ++gch;
                     }
-                    // look ahead one GEMM2 stage (the A ring holds two): the converters fill
-                    // stage kk + 1 while GEMM2 runs on stage kk
-                    gemm1_until(gnext);
                 }
             }
         }
@@ -276,15 +278,14 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
             for (int64_t t = tstart; t < g.ntiles; t += tstep) {
                 const K3Tile tl = k3_tile(g, t);
                 const int nws = (kc[tl.k] + 15) >> 4;
-                const int row0 = ((tl.i1_0 / TC_TI1) * g.nt2 + tl.i2_0 / TC_TI2) * TC_ROWS;
+                const int rt = (tl.i1_0 / TC_TI1) * g.nt2 + tl.i2_0 / TC_TI2;  // row tile
+                const unsigned char* pa = patab + (int64_t(tl.k) * g.nt1 * g.nt2 + rt) * nstg * (4 * K3_A_PLANE);
                 const __half* b1 = b1tab + ((int64_t(tl.k) * nstg) * g.nt3 + tl.i3_0 / K3_NI3) * (K3_B1_BYTES / 2);
                 for (int kk = 0; kk < nws; ++kk) {
                     mbar_wait_backoff(&wempty[s], ph ^ 1, 64);
                     mbar_arrive_expect_tx(&wfull[s], uint32_t(4 * K3_A_PLANE + K3_B1_BYTES));
                     unsigned char* dst = sW + s * K3_W_STAGE;
-#pragma unroll
-                    for (int pl = 0; pl < 4; ++pl)
-                        tma_load_3d(dst + pl * K3_A_PLANE, &wmap, &wfull[s], kk * 16, row0, pl * g.q + tl.k);
+                    bulk_g2s(dst, pa + int64_t(kk) * (4 * K3_A_PLANE), uint32_t(4 * K3_A_PLANE), &wfull[s]);
                     bulk_g2s(dst + K3_W_B1, b1 + int64_t(kk) * g.nt3 * (K3_B1_BYTES / 2), uint32_t(K3_B1_BYTES),
                              &wfull[s]);
                     if (++s == K3_NWS) {
@@ -337,18 +338,24 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                 mbar_wait(&dfull[db], dph);
                 tc_fence_after();
                 uint32_t v[16];
-                tmem_ld16(tD1 + lane_addr + db * 16u, v);
+                uint32_t vl[16];
+                tmem_ld16(tD1 + lane_addr + db * 32u, v);
+                tmem_ld16(tD1 + lane_addr + db * 32u + 16u, vl);  // the hi.lo terms
                 if (f & 4u) {
                     // half 0 continues the previous stage's half 1 (a column straddling the
                     // boundary): add that partial (complete, as GEMM1 commits in order)
-                    uint32_t w8[8];
-                    tmem_ld8(tD1 + lane_addr + dbp * 16u + 8u, w8);
+                    uint32_t w8[8], x8[8];
+                    tmem_ld8(tD1 + lane_addr + dbp * 32u + 8u, w8);
+                    tmem_ld8(tD1 + lane_addr + dbp * 32u + 24u, x8);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) + __uint_as_float(w8[e]));
+                    for (int e = 0; e < 8; ++e)
+                        v[e] = __float_as_uint(__uint_as_float(v[e]) + (__uint_as_float(w8[e]) + __uint_as_float(x8[e])));
                 } else {
                     tmem_ld_wait();
                 }
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) + __uint_as_float(vl[e]));
                 tc_fence_before();
                 __syncwarp();
                 // a D1 buffer is released by its own stage's converters and by the next stage's
@@ -527,8 +534,11 @@ __global__ void k3_xplanes_kernel(const float2* __restrict__ x, int64_t ldx, int
 // Per-store tables of K3W (built on first use, tm_capi.cu ensure_k3w) on
 // K3W's padded slot stream (column j of component k at slot poff[t], t = k m
 // + j, taking 8 slots if r3 <= 8 else 16; a stage holds one or two columns):
-//   pa[plane][k][row][kpad8] — the W arena's four fp16 planes moved to the
-//     padded slots (build_k3w_pa_kernel; padding zero by the caller's memset);
+//   pa[k][row tile][stage][plane][128 rows x 32 B] — the W arena's four fp16
+//     planes on K3W's slot stream, each (row tile, stage) block one
+//     contiguous 16 KB A operand, pre-swizzled for SW32 K-major (byte row 32
+//     + ((slot 2) ^ ((row & 4) << 2))), loaded by one bulk copy
+//     (build_k3w_pa_kernel; padding zero by the caller's memset);
 //   b1[k][stage][i3 block][4 planes][16 n][16 slots] — GEMM1's B operand,
 //     pre-swizzled for SW32 K-major (byte n 32 + ((slot 2) ^ ((n & 4) << 2))):
 //     n = c 8 + l 2 + part for the column of half c (stage desc sd: the
@@ -539,19 +549,23 @@ __global__ void k3_xplanes_kernel(const float2* __restrict__ x, int64_t ldx, int
 //     U3r) for Ti, U3 = U3_t[i3, r] 2^-e3 2^12 (build_k3w_b1_kernel).
 __global__ void build_k3w_pa_kernel(const TDesc* __restrict__ td, const int* __restrict__ kofs,
                                     const int* __restrict__ poff, int64_t ncols, int q, const __half* __restrict__ wa,
-                                    int64_t rows_pad, int64_t kpad, int64_t kpad8, __half* __restrict__ pa) {
+                                    int64_t rows_pad, int64_t kpad, int64_t nstg, unsigned char* __restrict__ pa) {
     const int64_t t = blockIdx.x;
     const int k = int(t / ncols);
     const int r3 = td[t].r3;
     const int64_t k0 = kofs[t], p0 = poff[t];
-    const int64_t plane = int64_t(q) * rows_pad * kpad, plane8 = int64_t(q) * rows_pad * kpad8;
+    const int64_t plane = int64_t(q) * rows_pad * kpad, nrt = rows_pad / TC_ROWS;
     for (int64_t e = threadIdx.x; e < rows_pad * r3; e += blockDim.x) {
         const int64_t row = e / r3;
         const int r = int(e - row * r3);
         const int64_t src = (int64_t(k) * rows_pad + row) * kpad + k0 + r;
-        const int64_t dst = (int64_t(k) * rows_pad + row) * kpad8 + p0 + r;
+        const int64_t slot = p0 + r, rt = row / TC_ROWS;
+        const uint32_t rr = uint32_t(row % TC_ROWS), sl = uint32_t(slot % 16);
+        unsigned char* blk = pa + ((int64_t(k) * nrt + rt) * nstg + slot / 16) * (4 * K3_A_PLANE);
+        const uint32_t off = rr * 32u + ((sl * 2u) ^ ((rr & 4u) << 2));
 #pragma unroll
-        for (int pl = 0; pl < 4; ++pl) pa[pl * plane8 + dst] = wa[pl * plane + src];
+        for (int pl = 0; pl < 4; ++pl)
+            *reinterpret_cast<__half*>(blk + pl * K3_A_PLANE + off) = wa[pl * plane + src];
     }
 }
 
