@@ -36,7 +36,7 @@
 //   warp 1      MMA issuer (GEMM1 per stage, GEMM2 per 16 columns)
 //   warp 2      loader of the W stages (A1 planes by TMA, B1 block by bulk copy)
 //   warp 3      TMEM allocator (512 columns: GEMM2 accumulator 256, D1 8 x 32)
-//   warps 4-11  converters: warps 4-7 even stages, 8-11 odd stages (D1 -> A2)
+//   warps 4-11  converters (D1 -> A2): lane quarter w & 3, i3 pair (w - 4) >> 2
 //   warps 12-15 chain fold + epilogue
 #pragma once
 
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < K3_NST; ++s) {
-            mbar_init(&full[s], 1 + 4 * 16);  // X TMA + 4 converter warps per column of the stage
+            mbar_init(&full[s], 1 + 8 * 16);  // X TMA + 8 converter warps per column of the stage
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < K3_NWS; ++s) {
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
         }
         for (int s = 0; s < K3_ND1; ++s) {
             mbar_init(&dfull[s], 1);
-            mbar_init(&dempty[s], 8);  // the stage's converters and the next stage's
+            mbar_init(&dempty[s], 16);  // the stage's 8 converter warps and the next stage's
         }
         mbar_init(cfull, 1);
         mbar_init(cfree, 4);
@@ -297,65 +297,62 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
         }
     } else if (warp >= TC_PW0 && warp < TC_PW0 + 8) {
         // ------------------------------------------------------- converters
-        // group grp = warps 4-7 / 8-11 takes the W stages sg = grp (mod 2);
-        // warp (w & 3) reads TMEM lane quarter w & 3: row = i2 + 32 i1 of the tile
+        // every converter warp takes every W stage: warp w reads TMEM lane quarter
+        // w & 3 (row = i2 + 32 i1 of the tile) and converts the i3 pair 2 grp,
+        // 2 grp + 1 (grp = (w - 4) >> 2); completed columns are buffered in
+        // registers and stored 4 K positions at a time (one 64-bit store per
+        // i3 and plane)
         const int grp = (warp - TC_PW0) >> 2, quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const uint32_t rowbase = uint32_t(row) * 32u, xorv = (uint32_t(row) & 4u) << 2;
-        const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+        const uint32_t lane_addr = (uint32_t(quarter * 32) << 16) + uint32_t(4 * grp);
         const float tsc = g.tsc;
-        uint32_t sg = 0;       // W stages of all tiles so far (both groups)
+        uint32_t sg = 0;       // W stages of all tiles so far
         uint32_t tseq = 0;     // tiles so far: GEMM2 stage sequence = tseq nks + j / 16
+        // [i3 of the pair][plane]: a shift register of the last 4 columns' fp16 values
+        // (ba: the older two, bb: the newer two; a new column enters at the top of bb)
+        uint32_t ba[2][4], bb[2][4];
+#pragma unroll
+        for (int l = 0; l < 2; ++l)
+#pragma unroll
+            for (int pl = 0; pl < 4; ++pl) ba[l][pl] = bb[l][pl] = 0u;
         for (int64_t t = tstart; t < g.ntiles; t += tstep, ++tseq) {
             const K3Tile tl = k3_tile(g, t);
             const int nws = (kc[tl.k] + 15) >> 4;
             const uint32_t* fl = sflag + int64_t(tl.k) * nstg;
-            // the stages' column counts 32 at a time (lane l: stage base + l) and their
-            // exclusive prefix (first column of each stage) by a warp scan
-            int cnt = 0, jfirst = 0, carry = 0;
+            int j = 0;           // next column to complete
+            uint32_t fnext = fl[0];
             for (int kk = 0; kk < nws; ++kk, ++sg) {
-                if ((kk & 31) == 0) {
-                    // columns ending in stage kk + lane: half 0 always, half 1 if present and ending
-                    cnt = 0;
-                    if (kk + lane < nws) {
-                        const uint32_t f = fl[kk + lane];
-                        cnt = 1 + ((f & 3u) == 3u ? 1 : 0);
-                    }
-                    int incl = cnt;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= o) incl += v;
-                    }
-                    jfirst = carry + incl - cnt;
-                    carry += __shfl_sync(0xffffffffu, incl, 31);
-                }
-                const int nc = __shfl_sync(0xffffffffu, cnt, kk & 31);  // columns ending here (1 or 2)
-                const int jc = __shfl_sync(0xffffffffu, jfirst, kk & 31);
-                if (int(sg & 1u) != grp) continue;
-                const uint32_t f = fl[kk];
+                const uint32_t f = fnext;
+                if (kk + 1 < nws) fnext = fl[kk + 1];
                 const uint32_t db = sg % K3_ND1, dph = (sg / K3_ND1) & 1u, dbp = (sg + K3_ND1 - 1) % K3_ND1;
                 mbar_wait(&dfull[db], dph);
                 tc_fence_after();
-                uint32_t v[16];
-                uint32_t vl[16];
-                tmem_ld16(tD1 + lane_addr + db * 32u, v);
-                tmem_ld16(tD1 + lane_addr + db * 32u + 16u, vl);  // the hi.lo terms
+                // this warp's columns of D1: half c at 8 c + 4 grp + (2 l + part), hi.lo terms + 16
+                uint32_t h0[4], h1[4], g0[4], g1[4];
+                tmem_ld4(tD1 + lane_addr + db * 32u, h0);
+                tmem_ld4(tD1 + lane_addr + db * 32u + 8u, h1);
+                tmem_ld4(tD1 + lane_addr + db * 32u + 16u, g0);
+                tmem_ld4(tD1 + lane_addr + db * 32u + 24u, g1);
+                float t0[4], t1[4];
                 if (f & 4u) {
                     // half 0 continues the previous stage's half 1 (a column straddling the
                     // boundary): add that partial (complete, as GEMM1 commits in order)
-                    uint32_t w8[8], x8[8];
-                    tmem_ld8(tD1 + lane_addr + dbp * 32u + 8u, w8);
-                    tmem_ld8(tD1 + lane_addr + dbp * 32u + 24u, x8);
+                    uint32_t p0[4], p1[4];
+                    tmem_ld4(tD1 + lane_addr + dbp * 32u + 8u, p0);
+                    tmem_ld4(tD1 + lane_addr + dbp * 32u + 24u, p1);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        v[e] = __float_as_uint(__uint_as_float(v[e]) + (__uint_as_float(w8[e]) + __uint_as_float(x8[e])));
+                    for (int e = 0; e < 4; ++e)
+                        t0[e] = __uint_as_float(h0[e]) + __uint_as_float(g0[e]) +
+                                (__uint_as_float(p0[e]) + __uint_as_float(p1[e]));
                 } else {
                     tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) t0[e] = __uint_as_float(h0[e]) + __uint_as_float(g0[e]);
                 }
 #pragma unroll
-                for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) + __uint_as_float(vl[e]));
+                for (int e = 0; e < 4; ++e) t1[e] = __uint_as_float(h1[e]) + __uint_as_float(g1[e]);
                 tc_fence_before();
                 __syncwarp();
                 // a D1 buffer is released by its own stage's converters and by the next stage's
@@ -363,46 +360,47 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                     mbar_arrive(&dempty[db]);
                     if (sg > 0) mbar_arrive(&dempty[dbp]);
                 }
-                // the stage's columns into the GEMM2 stage(s) of columns jc, jc + 1: a pair in one
-                // GEMM2 stage at an even K position shares one 32-bit store per plane
-                const bool pair32 = nc == 2 && (jc & 1) == 0;
-                for (int c = 0; c < nc; c += pair32 ? 2 : 1) {
-                    const int j = jc + c;
-                    const uint32_t aseq = tseq * uint32_t(g.nks) + uint32_t(j >> 4);
-                    const uint32_t as = aseq % K3_NST, aph = (aseq / K3_NST) & 1u;
-                    const uint32_t ks = uint32_t(j) & 15u;
-                    mbar_wait(&empty[as], aph ^ 1u);
-                    unsigned char* st = sA + as * K3_A_STAGE + rowbase + ((ks * 2u) ^ xorv);
+                const int nc = 1 + ((f & 3u) == 3u ? 1 : 0);  // columns ending here: half 0, half 1 if it ends
 #pragma unroll
-                    for (int l = 0; l < K3_NI3; ++l) {
-                        // half c of D1: (Tr, Ti) of i3 l at columns 8c + 2l, 8c + 2l + 1
-                        const uint32_t vr = c ? v[8 + 2 * l] : v[2 * l], vi = c ? v[9 + 2 * l] : v[2 * l + 1];
-                        uint32_t hi0, lo0;
-                        f16_split2(f2_pack(__uint_as_float(vr) * tsc, __uint_as_float(vi) * tsc), hi0, lo0);
-                        if (pair32) {
-                            uint32_t hi1, lo1;
-                            f16_split2(f2_pack(__uint_as_float(v[8 + 2 * l]) * tsc, __uint_as_float(v[9 + 2 * l]) * tsc),
-                                       hi1, lo1);
-                            uint32_t* w = reinterpret_cast<uint32_t*>(st + l * K3_A_BLOCK);
-                            w[0] = __byte_perm(hi0, hi1, 0x5410);                  // re hi (K = ks, ks + 1)
-                            w[K3_A_PLANE / 4] = __byte_perm(lo0, lo1, 0x5410);     // re lo
-                            w[2 * K3_A_PLANE / 4] = __byte_perm(hi0, hi1, 0x7632); // im hi
-                            w[3 * K3_A_PLANE / 4] = __byte_perm(lo0, lo1, 0x7632); // im lo
-                        } else {
-                            unsigned short* h = reinterpret_cast<unsigned short*>(st + l * K3_A_BLOCK);
-                            h[0] = static_cast<unsigned short>(hi0);                         // re hi
-                            h[K3_A_PLANE / 2] = static_cast<unsigned short>(lo0);            // re lo
-                            h[2 * K3_A_PLANE / 2] = static_cast<unsigned short>(hi0 >> 16);  // im hi
-                            h[3 * K3_A_PLANE / 2] = static_cast<unsigned short>(lo0 >> 16);  // im lo
-                        }
+                for (int c = 0; c < 2; ++c) {
+                    if (c >= nc) break;
+                    const float* tv = c ? t1 : t0;
+                    const uint32_t ks = uint32_t(j) & 15u, sub = ks & 3u;
+#pragma unroll
+                    for (int l = 0; l < 2; ++l) {
+                        uint32_t hi, lo;
+                        f16_split2(f2_pack(tv[2 * l] * tsc, tv[2 * l + 1] * tsc), hi, lo);
+                        // shift in: (ba, bb) <- (ba.hi16 bb.lo16, bb.hi16 new)
+#pragma unroll
+                        for (int pl = 0; pl < 4; ++pl) ba[l][pl] = __byte_perm(ba[l][pl], bb[l][pl], 0x5432);
+                        bb[l][0] = __byte_perm(bb[l][0], hi, 0x5432);  // re hi
+                        bb[l][1] = __byte_perm(bb[l][1], lo, 0x5432);  // re lo
+                        bb[l][2] = __byte_perm(bb[l][2], hi, 0x7632);  // im hi
+                        bb[l][3] = __byte_perm(bb[l][3], lo, 0x7632);  // im lo
                     }
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
+                    const bool last = j == int(g.ncols) - 1;
+                    if (sub == 3u || last) {
+                        // flush K positions ks & ~3 .. ks into the GEMM2 stage of column j
+                        const uint32_t aseq = tseq * uint32_t(g.nks) + uint32_t(j >> 4);
+                        const uint32_t as = aseq % K3_NST, aph = (aseq / K3_NST) & 1u;
+                        mbar_wait(&empty[as], aph ^ 1u);
+                        unsigned char* st = sA + as * K3_A_STAGE + rowbase + (((ks & ~3u) * 2u) ^ xorv);
+                        // the register holds columns (ks & ~3) .. ks in its top sub + 1 positions
+                        const uint32_t drop = 16u * (3u - sub);
+#pragma unroll
+                        for (int l = 0; l < 2; ++l)
+#pragma unroll
+                            for (int pl = 0; pl < 4; ++pl) {
+                                uint64_t v64 = (uint64_t(bb[l][pl]) << 32) | ba[l][pl];
+                                if (drop) v64 >>= drop;  // a tile's last, partial group
+                                *reinterpret_cast<uint64_t*>(st + (2 * grp + l) * K3_A_BLOCK + pl * K3_A_PLANE) = v64;
+                            }
+                        fence_proxy_async_smem();
+                        __syncwarp();
                         // a tile's last column also stands in for the missing columns of its stage
-                        const int nw = pair32 ? 2 : 1;
-                        mbar_arrive_n(&full[as], j + nw == int(g.ncols) ? 16u - ks : uint32_t(nw));
+                        if (lane == 0) mbar_arrive_n(&full[as], last ? 16u - (ks & ~3u) : 4u);
                     }
+                    ++j;
                 }
             }
         }
