@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
         }
         for (int s = 0; s < K3_ND1; ++s) {
             mbar_init(&dfull[s], 1);
-            mbar_init(&dempty[s], 16);  // the stage's 8 converter warps and the next stage's
+            mbar_init(&dempty[s], 8);  // the stage's 8 converter warps
         }
         mbar_init(cfull, 1);
         mbar_init(cfree, 4);
@@ -322,44 +322,42 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
             const uint32_t* fl = sflag + int64_t(tl.k) * nstg;
             int j = 0;           // next column to complete
             uint32_t fnext = fl[0];
+            // D1 of stage kk is loaded while stage kk - 1 is converted (software pipelining);
+            // this warp's columns: half c at 8 c + 4 grp + (2 l + part), the hi.lo terms at + 16
+            uint32_t cur[16];
+            auto load_d1 = [&](uint32_t sgx) {
+                const uint32_t dbx = sgx % K3_ND1;
+                mbar_wait(&dfull[dbx], (sgx / K3_ND1) & 1u);
+                tc_fence_after();
+                const uint32_t ta = tD1 + lane_addr + dbx * 32u;
+                tmem_ld4(ta, *reinterpret_cast<uint32_t(*)[4]>(&cur[0]));
+                tmem_ld4(ta + 8u, *reinterpret_cast<uint32_t(*)[4]>(&cur[4]));
+                tmem_ld4(ta + 16u, *reinterpret_cast<uint32_t(*)[4]>(&cur[8]));
+                tmem_ld4(ta + 24u, *reinterpret_cast<uint32_t(*)[4]>(&cur[12]));
+            };
+            load_d1(sg);
+            float t1prev[4] = {0.f, 0.f, 0.f, 0.f};  // the previous stage's half 1 (a straddler's head)
             for (int kk = 0; kk < nws; ++kk, ++sg) {
                 const uint32_t f = fnext;
                 if (kk + 1 < nws) fnext = fl[kk + 1];
-                const uint32_t db = sg % K3_ND1, dph = (sg / K3_ND1) & 1u, dbp = (sg + K3_ND1 - 1) % K3_ND1;
-                mbar_wait(&dfull[db], dph);
-                tc_fence_after();
-                // this warp's columns of D1: half c at 8 c + 4 grp + (2 l + part), hi.lo terms + 16
-                uint32_t h0[4], h1[4], g0[4], g1[4];
-                tmem_ld4(tD1 + lane_addr + db * 32u, h0);
-                tmem_ld4(tD1 + lane_addr + db * 32u + 8u, h1);
-                tmem_ld4(tD1 + lane_addr + db * 32u + 16u, g0);
-                tmem_ld4(tD1 + lane_addr + db * 32u + 24u, g1);
+                tmem_ld_wait_regs(cur);
                 float t0[4], t1[4];
-                if (f & 4u) {
-                    // half 0 continues the previous stage's half 1 (a column straddling the
-                    // boundary): add that partial (complete, as GEMM1 commits in order)
-                    uint32_t p0[4], p1[4];
-                    tmem_ld4(tD1 + lane_addr + dbp * 32u + 8u, p0);
-                    tmem_ld4(tD1 + lane_addr + dbp * 32u + 24u, p1);
-                    tmem_ld_wait();
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        t0[e] = __uint_as_float(h0[e]) + __uint_as_float(g0[e]) +
-                                (__uint_as_float(p0[e]) + __uint_as_float(p1[e]));
-                } else {
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) t0[e] = __uint_as_float(h0[e]) + __uint_as_float(g0[e]);
+                for (int e = 0; e < 4; ++e) {
+                    t0[e] = __uint_as_float(cur[e]) + __uint_as_float(cur[8 + e]);
+                    t1[e] = __uint_as_float(cur[4 + e]) + __uint_as_float(cur[12 + e]);
                 }
-#pragma unroll
-                for (int e = 0; e < 4; ++e) t1[e] = __uint_as_float(h1[e]) + __uint_as_float(g1[e]);
                 tc_fence_before();
                 __syncwarp();
-                // a D1 buffer is released by its own stage's converters and by the next stage's
-                if (lane == 0) {
-                    mbar_arrive(&dempty[db]);
-                    if (sg > 0) mbar_arrive(&dempty[dbp]);
+                if (lane == 0) mbar_arrive(&dempty[sg % K3_ND1]);
+                if (kk + 1 < nws) load_d1(sg + 1);
+                if (f & 4u) {
+                    // half 0 continues the previous stage's half 1 (a column straddling the boundary)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) t0[e] += t1prev[e];
                 }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) t1prev[e] = t1[e];
                 const int nc = 1 + ((f & 3u) == 3u ? 1 : 0);  // columns ending here: half 0, half 1 if it ends
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
