@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
             uint32_t s = 0, ph = 0;
             for (int64_t t = tstart; t < g.ntiles; t += tstep)
                 for (int kk = 0; kk < g.nks; ++kk) {
-                    mbar_wait_backoff(&empty[s], ph ^ 1, 128);
+                    mbar_wait_backoff(&empty[s], ph ^ 1, 512);
                     mbar_arrive_expect_tx(&full[s], uint32_t(K3_B_STAGE));
                     unsigned char* dst = sB + s * K3_B_STAGE;
 #pragma unroll
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                 const unsigned char* pa = patab + (int64_t(tl.k) * g.nt1 * g.nt2 + rt) * nstg * (4 * K3_A_PLANE);
                 const __half* b1 = b1tab + ((int64_t(tl.k) * nstg) * g.nt3 + tl.i3_0 / K3_NI3) * (K3_B1_BYTES / 2);
                 for (int kk = 0; kk < nws; ++kk) {
-                    mbar_wait_backoff(&wempty[s], ph ^ 1, 64);
+                    mbar_wait_backoff(&wempty[s], ph ^ 1, 128);
                     mbar_arrive_expect_tx(&wfull[s], uint32_t(4 * K3_A_PLANE + K3_B1_BYTES));
                     unsigned char* dst = sW + s * K3_W_STAGE;
                     bulk_g2s(dst, pa + int64_t(kk) * (4 * K3_A_PLANE), uint32_t(4 * K3_A_PLANE), &wfull[s]);
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
             const int ei1 = tl.i1_0 + quarter, ei2 = tl.i2_0 + lane;
             const bool eok = ei1 < g.n1 && ei2 < g.n2;
             for (int ch = 0; ch < nch; ++ch, ++gch) {
-                mbar_wait_backoff(cfull, gch & 1, 256);
+                mbar_wait_backoff(cfull, gch & 1, 1024);
                 tc_fence_after();
                 const bool last = ch == nch - 1;
                 for (int l = 0; l < K3_NI3; ++l)

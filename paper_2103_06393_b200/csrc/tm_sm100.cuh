@@ -96,9 +96,11 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
     const uint32_t a = smem_u32(bar);
     if (mbar_try<CLUSTER>(a, parity)) return;
     const uint64_t t0 = globaltimer_ns();
+    uint32_t n = 0;
     while (!mbar_try<CLUSTER>(a, parity)) {
         __nanosleep(ns);
-        if (globaltimer_ns() - t0 > 20000000000ull) __trap();
+        // the clock is read only every 256 polls
+        if ((++n & 0xFFu) == 0 && globaltimer_ns() - t0 > 20000000000ull) __trap();
     }
 }
 
