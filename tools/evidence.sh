@@ -24,3 +24,8 @@ for k in fwd_tc_kernel adj_tc_kernel; do
 done
 tail -n 2 $O/${T}_smoke.log
 cut -c1-160 $O/${T}_bench_c4.jsonl $O/${T}_bench_configs.jsonl
+# config 5: the K3W batched forward and the adjoint GEMM on the W arena, ncu --set full
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on --profile-from-start off \
+  -k regex:fwd_k3w -c 1 -f -o $O/${T}_ncu_c5_k3w python tools/prof_run.py --config c5 > $O/${T}_ncu_c5_k3w.log 2>&1
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on --profile-from-start off \
+  -k regex:fwd_tc_kernel -c 1 -f -o $O/${T}_ncu_c5_adjgemm python tools/prof_run.py --config c5 > $O/${T}_ncu_c5_adjgemm.log 2>&1
