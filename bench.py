@@ -775,6 +775,14 @@ def main():
                                          "for the 3-product fp16 split; cuBLAS fp16 GEMM in this run: %.1f TFLOP/s"
                                          % (bf16, f16_peak))
             kernels = ("fwd_tc_kernel", "adj_tc_kernel (+ absmax, adj_split_phi_kernel, adj_reduce_kernel)")
+            paths = part_stores[0].kernel_paths() if part_stores else {}
+            if paths.get("forward") == "tcgen05+warena":  # the W arena (DESIGN §3 / §4)
+                k3w = cfg.p >= int(os.environ.get("TMB_K3_PMIN", "16")) and os.environ.get("TMB_K3", "1") != "0"
+                kernels = ("fwd_k3w_kernel (K3W: GEMM1 T = W U3^T + GEMM2 Y += T X)" if k3w
+                           else "fwd_tc_kernel (A operand from the W arena)", kernels[1])
+            if paths.get("adjoint") == "tcgen05+gemm":
+                kernels = (kernels[0], "fwd_tc_kernel<ADJ> (G = conj(W)^T Phi on the transposed W arena; "
+                                       "+ adjg_split_phi_kernel, adjg_contract_kernel)")
         elif cfg.dtype == "c128":
             peak = fp64_peak
             bound, unit_src = "fp64", "measured here: cuBLAS DGEMM 8192^3 (the c128 kernels run DFMA)"
