@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                 const int arow = int(tl.rt * TC_ROWS);
                 for (int n = n0; n < n1; ++n) {
                     for (int kk = 0; kk < g.nks; ++kk) {
-                        mbar_wait_backoff(&empty[s], ph ^ 1, 64);
+                        mbar_wait_backoff(&empty[s], ph ^ 1, TC_BACKOFF_ADJ);
                         unsigned char* da = sA + s * A2_A_STAGE;
                         unsigned char* db = sB + s * A2_B_STAGE;
                         if (PAIR) {
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(AJ_THREADS, 1)
                 aj_chunks(g, tl, nch[tl.k], n0, n1);
                 const int* cs = cstart + int64_t(tl.k) * (g.maxch + 1);
                 for (int64_t j = cs[n0]; j < cs[n1]; ++j) {
-                    mbar_wait_backoff(&fempty[s], ph ^ 1, 64);
+                    mbar_wait_backoff(&fempty[s], ph ^ 1, TC_BACKOFF_ADJ);
                     const TcDesc d = tdk[j];
                     unsigned char* slot = sSlot + s * g.slot_bytes;
                     const uint32_t r23 = uint32_t(d.r2 * d.r3);

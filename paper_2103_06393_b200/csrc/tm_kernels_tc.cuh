@@ -75,6 +75,22 @@ __host__ __device__ inline float fp16_scale(float amax) {
 }
 
 constexpr int TC_TI1 = 4, TC_TI2 = 32, TC_ROWS = 128;
+// Back-off (ns between barrier polls) of the warp roles that wait off the
+// critical path — the B-plane TMA warp, the factor loader and the chain fold —
+// so that their polling takes fewer issue slots from the producer / consumer
+// warps sharing their SM sub-partitions.
+#ifndef TC_BACKOFF_TMA
+#define TC_BACKOFF_TMA 128
+#endif
+#ifndef TC_BACKOFF_LD
+#define TC_BACKOFF_LD 128
+#endif
+#ifndef TC_BACKOFF_FOLD
+#define TC_BACKOFF_FOLD 256
+#endif
+#ifndef TC_BACKOFF_ADJ
+#define TC_BACKOFF_ADJ 64
+#endif
 constexpr int TC_NST_MAX = 6;   // A/B stages (16 K each; as many as shared memory allows)
 constexpr int TC_JR = 3;        // factor-ring slots
 constexpr int TC_NR = 2;        // tile rows per producer lane (rows i2a + 8 e, e < TC_NR)
@@ -439,7 +455,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 tc_range<WA>(g, tl, kofs, kc, j0, j1, ka, kb);
                 const int arow = ((tl.i1_0 / TC_TI1) * g.nt2 + tl.i2_0 / TC_TI2) * TC_ROWS;
                 for (int kk = int(ka >> 4); kk < int((kb + 15) >> 4); ++kk) {
-                    TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(&empty[s], ph ^ 1, 128)));
+                    TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(&empty[s], ph ^ 1, TC_BACKOFF_TMA)));
                     if constexpr (WA) {  // A: this CTA's 128 rows x 16 K of the 4 W planes
                         unsigned char* da = sA + s * TC_A_STAGE;
                         if (PAIR) {
@@ -574,7 +590,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 uint32_t ka, kb;
                 tc_range(g, tl, kofs, kc, j0, j1, ka, kb);
                 for (int j = j0; j < j1; ++j) {
-                    TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(&fempty[s], ph ^ 1, 128)));
+                    TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(&fempty[s], ph ^ 1, TC_BACKOFF_LD)));
                     const TcDesc d = tdk[j];
                     unsigned char* slot = sSlot + s * g.slot_bytes;
                     const uint32_t r23 = uint32_t(d.r2 * d.r3);
@@ -763,7 +779,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 continue;
             }
             for (int ch = 0; ch < nch; ++ch, ++gch) {
-                TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(cfull, gch & 1, 256)));
+                TC_TWAIT(g.prof, t_w, (mbar_wait_backoff(cfull, gch & 1, TC_BACKOFF_FOLD)));
                 tc_fence_after();
                 const bool last = ch == nch - 1;
                 for (int hh = 0; hh < g.nh3; ++hh)
