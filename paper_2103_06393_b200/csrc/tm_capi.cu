@@ -1153,7 +1153,8 @@ void ensure_k3w(tm_store* s, cudaStream_t st) {
     CK(cudaFree(d_sd));
 }
 
-void run_forward_k3w(tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy, cudaStream_t st) {
+void run_forward_k3w(tm_store* s, const float2* x, int64_t ldx, int64_t p, float2* y, int64_t ldy, cudaStream_t st,
+                     const HostPipe* hp = nullptr) {
     ensure_k3w(s, st);
     K3Geom g{};
     g.ncols = s->ncols;
@@ -1197,10 +1198,32 @@ void run_forward_k3w(tm_store* s, const float2* x, int64_t ldx, int64_t p, float
                                                   uint64_t(2 * K3_P) * kpad * 2, 16, 2 * K3_P,
                                                   CU_TENSOR_MAP_SWIZZLE_32B);
         g.p = pb;
-        fwd_k3w_kernel<<<grid, K3_THREADS, smem, st>>>(xmap, reinterpret_cast<const unsigned char*>(s->d_k3pa), s->d_k3b1, s->d_k3kc, s->d_k3flag,
-                                                       s->k3_kpad8 / 16, s->d_k3gend, g, y + ldy * c0, ldy, rsum,
-                                                       xmax);
-        launched(cudaSuccess, "fwd_k3w_kernel");
+        // TM_HOST (hp->copy): one launch per component, each component's y block copied
+        // out on the copy stream while the next one computes (tiles are component-major)
+        const bool pipe = hp && hp->copy;
+        const int nl = pipe ? g.q : 1;
+        const int64_t tpl = g.ntiles / nl;
+        for (int l = 0; l < nl; ++l) {
+            K3Geom gl = g;
+            gl.tile0 = int64_t(l) * tpl;
+            gl.ntiles = tpl;
+            fwd_k3w_kernel<<<unsigned(std::min<int64_t>(tpl, grid)), K3_THREADS, smem, st>>>(
+                xmap, reinterpret_cast<const unsigned char*>(s->d_k3pa), s->d_k3b1, s->d_k3kc, s->d_k3flag,
+                s->k3_kpad8 / 16, s->d_k3gend, gl, y + ldy * c0, ldy, rsum, xmax);
+            launched(cudaSuccess, "fwd_k3w_kernel");
+            if (pipe) {
+                const int64_t nv = s->nv();
+                cudaEvent_t ev;
+                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                CK(cudaEventRecord(ev, st));
+                CK(cudaStreamWaitEvent(hp->copy, ev, 0));
+                CK(cudaEventDestroy(ev));
+                CK(cudaMemcpy2DAsync(static_cast<float2*>(hp->host) + hp->ldhost * c0 + int64_t(l) * nv,
+                                     size_t(hp->ldhost) * sizeof(float2), y + ldy * c0 + int64_t(l) * nv,
+                                     size_t(ldy) * sizeof(float2), size_t(nv) * sizeof(float2), size_t(pb),
+                                     cudaMemcpyDeviceToHost, hp->copy));
+            }
+        }
     }
 }
 
@@ -1825,7 +1848,7 @@ void with_host_io(tm_store* s, const void* in, int64_t ldin, int64_t inrows, int
 // kernels block by block (HostPipe).  Returns false when the product does
 // not take the tensor-core path (the caller then uses with_host_io).
 bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy) {
-    if (!(s->tc_ok && !tc_disabled()) || k3w_ok(s, p)) return false;
+    if (!(s->tc_ok && !tc_disabled())) return false;
     const size_t cs = s->csize();
     void* din = s->xin.get(size_t(std::max<int64_t>(s->ncols * p, 1)) * cs);
     void* dout = s->yout.get(size_t(std::max<int64_t>(s->rows() * p, 1)) * cs);
@@ -1847,7 +1870,12 @@ bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, 
         hp.copy = cp;
         hp.host = y;
         hp.ldhost = ldy;
-        run_forward_tc(s, static_cast<const float2*>(din), s->ncols, p, static_cast<float2*>(dout), s->rows(), st, &hp);
+        if (k3w_ok(s, p))
+            run_forward_k3w(s, static_cast<const float2*>(din), s->ncols, p, static_cast<float2*>(dout), s->rows(), st,
+                            &hp);
+        else
+            run_forward_tc(s, static_cast<const float2*>(din), s->ncols, p, static_cast<float2*>(dout), s->rows(), st,
+                           &hp);
         mark_done(s, st);
         CK(cudaStreamSynchronize(st));
         CK(cudaStreamSynchronize(cp));

@@ -72,7 +72,8 @@ struct K3Geom {
     int n1, n2, n3, q;
     int nt1, nt2, nt3;
     int p;             // right-hand sides of this pass (<= K3_P)
-    int64_t ntiles;
+    int64_t ntiles;    // tiles of this launch: tile0 .. tile0 + ntiles - 1
+    int64_t tile0;
     int nks;           // GEMM2 K stages per tile = ceil(ncols / 16)
     int chain;         // K stages per TMEM accumulation chain
     float tsc;         // power of two taking D1 (W-arena x U3 units) into fp16 range
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
             uint32_t s = 0, ph = 0, gch = 0;
             uint32_t sg = 0;  // W stages issued (all tiles): W ring slot sg % K3_NWS, D1 buffer sg % K3_ND1
             for (int64_t t = tstart; t < g.ntiles; t += tstep) {
-                const K3Tile tl = k3_tile(g, t);
+                const K3Tile tl = k3_tile(g, g.tile0 + t);
                 // gend[k][kk]: W stages up to the last one holding a column of GEMM2 stage kk
                 const int* ge = gend + int64_t(tl.k) * g.nks;
                 int snext = 0;
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
         if (elect_one()) {
             uint32_t s = 0, ph = 0;
             for (int64_t t = tstart; t < g.ntiles; t += tstep) {
-                const K3Tile tl = k3_tile(g, t);
+                const K3Tile tl = k3_tile(g, g.tile0 + t);
                 const int nws = (kc[tl.k] + 15) >> 4;
                 const int rt = (tl.i1_0 / TC_TI1) * g.nt2 + tl.i2_0 / TC_TI2;  // row tile
                 const unsigned char* pa = patab + (int64_t(tl.k) * g.nt1 * g.nt2 + rt) * nstg * (4 * K3_A_PLANE);
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
 #pragma unroll
             for (int pl = 0; pl < 4; ++pl) ba[l][pl] = bb[l][pl] = 0u;
         for (int64_t t = tstart; t < g.ntiles; t += tstep, ++tseq) {
-            const K3Tile tl = k3_tile(g, t);
+            const K3Tile tl = k3_tile(g, g.tile0 + t);
             const int nws = (kc[tl.k] + 15) >> 4;
             const uint32_t* fl = sflag + int64_t(tl.k) * nstg;
             int j = 0;           // next column to complete
@@ -418,7 +419,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
         const float inv = 1.f / (g.wsc * g.tsc * fp16_scale(*xmax));
         uint32_t gch = 0;
         for (int64_t t = tstart; t < g.ntiles; t += tstep) {
-            const K3Tile tl = k3_tile(g, t);
+            const K3Tile tl = k3_tile(g, g.tile0 + t);
             const int ei1 = tl.i1_0 + quarter, ei2 = tl.i2_0 + lane;
             const bool eok = ei1 < g.n1 && ei2 < g.n2;
             for (int ch = 0; ch < nch; ++ch, ++gch) {
