@@ -489,6 +489,23 @@ __global__ void absmax_kernel(const float2* __restrict__ phi, int64_t ldphi, int
     if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned int*>(out + b), __float_as_uint(m));
 }
 
+// max |Phi| of component k for every right-hand side c of the pass (out[c q +
+// k], the per-component form of absmax_kernel used when Phi arrives from the
+// host component by component).
+__global__ void absmax_comp_kernel(const float2* __restrict__ phi, int64_t ldphi, int64_t nv, int q, int k,
+                                   float* __restrict__ out) {
+    const int64_t c = blockIdx.y;
+    const float2* src = phi + ldphi * c + int64_t(k) * nv;
+    float m = 0.f;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nv; e += int64_t(gridDim.x) * blockDim.x) {
+        const float2 v = src[e];
+        m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned int*>(out + c * q + k), __float_as_uint(m));
+}
+
 // Phi (c64, [c][k n_v + v]) -> scaled 2-term fp16 planes [pl][c][k][row-tile
 // order][n3p] (n3p = n3 rounded up to 8 for the TMA row pitch), pl = re hi,
 // re lo, im hi, im lo; tile rows are (i2 + 32 i1) of the (TI1 x TI2) row
@@ -574,11 +591,11 @@ __global__ void build_adj_bplanes_kernel(const TDesc* __restrict__ td, const flo
 // threads read 32 contiguous bytes of Phi.
 __global__ void adjg_split_phi_kernel(const float2* __restrict__ phi, int64_t ldphi, int n1, int n2, int n3, int p,
                                       int q, int nt2, int64_t R, int64_t nt, const float* __restrict__ phimax,
-                                      __half* __restrict__ planes) {
+                                      __half* __restrict__ planes, int k0) {
     using namespace sm100;
     const int tile = int(blockIdx.x);
     const int64_t n = blockIdx.y;
-    const int k = int(blockIdx.z);
+    const int k = k0 + int(blockIdx.z);  // components [k0, k0 + gridDim.z)
     const int i3 = int(n / p), c = int(n - int64_t(i3) * p);
     const int t1 = tile / nt2, t2 = tile - t1 * nt2;
     const int t = int(threadIdx.x);

@@ -1578,7 +1578,7 @@ void run_adjoint_tc(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, fl
 // adjg_contract_kernel applies U3 and the scales.  The MACs are the forward
 // arena kernel's (rows x n3 p x slots), with no consumer warps.
 void run_adjoint_gemm(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, float2* z, int64_t ldz,
-                      cudaStream_t st) {
+                      cudaStream_t st, const HostPipe* hp = nullptr) {
     const int n1 = int(s->dims[0]), n2 = int(s->dims[1]), n3 = int(s->dims[2]);
     const int nt1r = (n1 + TC_TI1 - 1) / TC_TI1, nt2r = (n2 + TC_TI2 - 1) / TC_TI2;
     const int64_t R = int64_t(nt1r) * nt2r * TC_ROWS, nv = s->nv(), kt = s->wt_kpadt;
@@ -1595,12 +1595,40 @@ void run_adjoint_gemm(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, 
         const float2* ph = phi + ldphi * c0;
         const int64_t nt = int64_t(n3) * pb;
         CK(cudaMemsetAsync(phimax, 0, size_t(pb * s->q) * sizeof(float), st));
-        absmax_kernel<<<dim3(148, unsigned(pb * s->q)), 256, 0, st>>>(ph, ldphi, nv, s->q, 0, phimax);
-        launched(cudaSuccess, "absmax_kernel");
         __half* planes = static_cast<__half*>(s->phit.get(size_t(4) * s->q * nt * R * sizeof(__half)));
-        adjg_split_phi_kernel<<<dim3(unsigned(nt1r * nt2r), unsigned(nt), unsigned(s->q)), TC_ROWS, 0, st>>>(
-            ph, ldphi, n1, n2, n3, int(pb), s->q, nt2r, R, nt, phimax, planes);
-        launched(cudaSuccess, "adjg_split_phi_kernel");
+        // TM_HOST (hp->copy): Phi arrives component by component on the copy stream and
+        // each component's absmax and split run once it is in, ahead of the GEMM waves
+        // that read it (split_upto); otherwise all components at once
+        const bool pipe = hp && hp->copy;
+        std::vector<cudaEvent_t> arrived;
+        int ksplit = 0;
+        auto split_upto = [&](int kend) {
+            for (; ksplit < kend; ++ksplit) {
+                CK(cudaStreamWaitEvent(st, arrived[size_t(ksplit)], 0));
+                absmax_comp_kernel<<<dim3(148, unsigned(pb)), 256, 0, st>>>(ph, ldphi, nv, s->q, ksplit, phimax);
+                launched(cudaSuccess, "absmax_comp_kernel");
+                adjg_split_phi_kernel<<<dim3(unsigned(nt1r * nt2r), unsigned(nt), 1u), TC_ROWS, 0, st>>>(
+                    ph, ldphi, n1, n2, n3, int(pb), s->q, nt2r, R, nt, phimax, planes, ksplit);
+                launched(cudaSuccess, "adjg_split_phi_kernel");
+            }
+        };
+        if (pipe) {
+            arrived.resize(size_t(s->q));
+            for (int k = 0; k < s->q; ++k) {
+                CK(cudaMemcpy2DAsync(const_cast<float2*>(ph) + int64_t(k) * nv, size_t(ldphi) * sizeof(float2),
+                                     static_cast<const float2*>(hp->host) + hp->ldhost * c0 + int64_t(k) * nv,
+                                     size_t(hp->ldhost) * sizeof(float2), size_t(nv) * sizeof(float2), size_t(pb),
+                                     cudaMemcpyHostToDevice, hp->copy));
+                CK(cudaEventCreateWithFlags(&arrived[size_t(k)], cudaEventDisableTiming));
+                CK(cudaEventRecord(arrived[size_t(k)], hp->copy));
+            }
+        } else {
+            absmax_kernel<<<dim3(148, unsigned(pb * s->q)), 256, 0, st>>>(ph, ldphi, nv, s->q, 0, phimax);
+            launched(cudaSuccess, "absmax_kernel");
+            adjg_split_phi_kernel<<<dim3(unsigned(nt1r * nt2r), unsigned(nt), unsigned(s->q)), TC_ROWS, 0, st>>>(
+                ph, ldphi, n1, n2, n3, int(pb), s->q, nt2r, R, nt, phimax, planes, 0);
+            launched(cudaSuccess, "adjg_split_phi_kernel");
+        }
         TcGeom g{};
         g.ncols = s->ncols;
         g.n1 = n1;
@@ -1653,6 +1681,7 @@ void run_adjoint_gemm(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, 
             if (g.split > 1)
                 g.ypart = static_cast<float2*>(s->ypart.get(size_t(tiles) * g.split * (1 + g.pair) * g.nmma * g.nh3 *
                                                             TC_ROWS * sizeof(float2)));
+            if (pipe) split_upto(int((t0 + tiles - 1) / (g.ntiles / g.q)) + 1);  // the components this wave reads
             if (g.pair) {
                 cudaLaunchConfig_t cfg{};
                 cfg.gridDim = dim3(grid);
@@ -1684,10 +1713,12 @@ void run_adjoint_gemm(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, 
                 launched(cudaSuccess, "adjg_split_reduce_kernel");
             }
         }
+        if (pipe) split_upto(s->q);
         adjg_contract_kernel<<<unsigned(s->ncols), 256, 0, st>>>(
             G, kt, nt, int(pb), s->q, s->ncols, n3, s->d_tcd, static_cast<const float2*>(s->d_arena), s->d_kofs,
             phimax, fp16_scale(s->vmax * 1.0001f), z + ldz * c0, ldz);
         launched(cudaSuccess, "adjg_contract_kernel");
+        for (auto ev : arrived) CK(cudaEventDestroy(ev));
     }
 }
 
@@ -1888,8 +1919,8 @@ bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, 
 }
 
 bool adjoint_host_pipelined(tm_store* s, const void* phi, int64_t ldphi, int64_t p, void* z, int64_t ldz) {
-    if (!(s->tca_ok && !tc_disabled() && adj_tc_fits(s) && int64_t(p) * s->q <= 65535)) return false;
-    if (s->d_wt && !warena_disabled() && !adjg_disabled()) return false;  // the adjoint GEMM (adjoint_dev)
+    const bool gemm = s->d_wt && !warena_disabled() && !adjg_disabled() && !tc_disabled();  // adjoint_dev's choice
+    if (!gemm && !(s->tca_ok && !tc_disabled() && adj_tc_fits(s) && int64_t(p) * s->q <= 65535)) return false;
     const size_t cs = s->csize();
     void* din = s->xin.get(size_t(std::max<int64_t>(s->rows() * p, 1)) * cs);
     void* dout = s->yout.get(size_t(std::max<int64_t>(s->ncols * p, 1)) * cs);
@@ -1909,7 +1940,12 @@ bool adjoint_host_pipelined(tm_store* s, const void* phi, int64_t ldphi, int64_t
         hp.copy = cp;
         hp.host = const_cast<void*>(phi);
         hp.ldhost = ldphi;
-        run_adjoint_tc(s, static_cast<const float2*>(din), s->rows(), p, static_cast<float2*>(dout), s->ncols, st, &hp);
+        if (gemm)
+            run_adjoint_gemm(s, static_cast<const float2*>(din), s->rows(), p, static_cast<float2*>(dout), s->ncols, st,
+                             &hp);
+        else
+            run_adjoint_tc(s, static_cast<const float2*>(din), s->rows(), p, static_cast<float2*>(dout), s->ncols, st,
+                           &hp);
         CK(cudaMemcpy2DAsync(z, size_t(ldz) * cs, dout, size_t(s->ncols) * cs, size_t(s->ncols) * cs, size_t(p),
                              cudaMemcpyDeviceToHost, st));
         mark_done(s, st);
