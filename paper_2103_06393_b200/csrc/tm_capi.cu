@@ -1878,10 +1878,15 @@ void with_host_io(tm_store* s, const void* in, int64_t ldin, int64_t inrows, int
 // TM_HOST products on the tensor-core path: host I/O overlapped with the
 // kernels block by block (HostPipe).  Returns false when the product does
 // not take the tensor-core path (the caller then uses with_host_io).
-bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy) {
+// `xrows` / `prep`: the ACA forward copies its x (m2 rows) in and forms w = V^H x
+// on the device first (prep returns the device input of the column products).
+bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, void* y, int64_t ldy,
+                            int64_t xrows = -1,
+                            const std::function<const void*(const void*, cudaStream_t)>& prep = nullptr) {
     if (!(s->tc_ok && !tc_disabled())) return false;
+    if (xrows < 0) xrows = s->ncols;
     const size_t cs = s->csize();
-    void* din = s->xin.get(size_t(std::max<int64_t>(s->ncols * p, 1)) * cs);
+    void* din = s->xin.get(size_t(std::max<int64_t>(xrows * p, 1)) * cs);
     void* dout = s->yout.get(size_t(std::max<int64_t>(s->rows() * p, 1)) * cs);
     cudaStream_t st, cp;
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -1895,18 +1900,17 @@ bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, 
     try {
         order_after_prev(s, st);
         order_after_prev(s, cp);
-        CK(cudaMemcpy2DAsync(din, size_t(s->ncols) * cs, x, size_t(ldx) * cs, size_t(s->ncols) * cs, size_t(p),
+        CK(cudaMemcpy2DAsync(din, size_t(xrows) * cs, x, size_t(ldx) * cs, size_t(xrows) * cs, size_t(p),
                              cudaMemcpyHostToDevice, st));
+        const float2* xin = static_cast<const float2*>(prep ? prep(din, st) : din);
         HostPipe hp;
         hp.copy = cp;
         hp.host = y;
         hp.ldhost = ldy;
         if (k3w_ok(s, p))
-            run_forward_k3w(s, static_cast<const float2*>(din), s->ncols, p, static_cast<float2*>(dout), s->rows(), st,
-                            &hp);
+            run_forward_k3w(s, xin, s->ncols, p, static_cast<float2*>(dout), s->rows(), st, &hp);
         else
-            run_forward_tc(s, static_cast<const float2*>(din), s->ncols, p, static_cast<float2*>(dout), s->rows(), st,
-                           &hp);
+            run_forward_tc(s, xin, s->ncols, p, static_cast<float2*>(dout), s->rows(), st, &hp);
         mark_done(s, st);
         CK(cudaStreamSynchronize(st));
         CK(cudaStreamSynchronize(cp));
@@ -1918,9 +1922,14 @@ bool forward_host_pipelined(tm_store* s, const void* x, int64_t ldx, int64_t p, 
     return true;
 }
 
-bool adjoint_host_pipelined(tm_store* s, const void* phi, int64_t ldphi, int64_t p, void* z, int64_t ldz) {
+// `zrows` / `post`: the ACA adjoint maps the column products t to z = V t (m2
+// rows) on the device before the copy out (post returns the device z).
+bool adjoint_host_pipelined(tm_store* s, const void* phi, int64_t ldphi, int64_t p, void* z, int64_t ldz,
+                            int64_t zrows = -1,
+                            const std::function<void*(void*, cudaStream_t)>& post = nullptr) {
     const bool gemm = s->d_wt && !warena_disabled() && !adjg_disabled() && !tc_disabled();  // adjoint_dev's choice
     if (!gemm && !(s->tca_ok && !tc_disabled() && adj_tc_fits(s) && int64_t(p) * s->q <= 65535)) return false;
+    if (zrows < 0) zrows = s->ncols;
     const size_t cs = s->csize();
     void* din = s->xin.get(size_t(std::max<int64_t>(s->rows() * p, 1)) * cs);
     void* dout = s->yout.get(size_t(std::max<int64_t>(s->ncols * p, 1)) * cs);
@@ -1946,7 +1955,8 @@ bool adjoint_host_pipelined(tm_store* s, const void* phi, int64_t ldphi, int64_t
         else
             run_adjoint_tc(s, static_cast<const float2*>(din), s->rows(), p, static_cast<float2*>(dout), s->ncols, st,
                            &hp);
-        CK(cudaMemcpy2DAsync(z, size_t(ldz) * cs, dout, size_t(s->ncols) * cs, size_t(s->ncols) * cs, size_t(p),
+        void* zdev = post ? post(dout, st) : dout;
+        CK(cudaMemcpy2DAsync(z, size_t(ldz) * cs, zdev, size_t(zrows) * cs, size_t(zrows) * cs, size_t(p),
                              cudaMemcpyDeviceToHost, st));
         mark_done(s, st);
         CK(cudaStreamSynchronize(st));
@@ -2266,7 +2276,12 @@ TM_API int tm_aca_forward(tm_store* s, const void* x, int64_t ldx, int64_t xrows
             order_after_prev(s, static_cast<cudaStream_t>(stream));
             body(x, ldx, y, ldy, static_cast<cudaStream_t>(stream));
             mark_done(s, static_cast<cudaStream_t>(stream));
-        } else {
+        } else if (s->dense || s->ncols == 0 ||
+                   !forward_host_pipelined(s, x, ldx, p, y, ldy, s->m2, [&](const void* xin, cudaStream_t st) {
+                       void* w = s->wbuf.get(size_t(s->ncols * p) * s->csize());
+                       aca_vhx_dev(s, xin, s->m2, p, w, st);
+                       return static_cast<const void*>(w);
+                   })) {
             with_host_io(s, x, ldx, xrows, p, y, ldy, s->rows(),
                          [&](void* din, int64_t ldi, void* dout, int64_t ldo, cudaStream_t st) {
                              body(din, ldi, dout, ldo, st);
@@ -2303,7 +2318,12 @@ TM_API int tm_aca_adjoint(tm_store* s, const void* phi, int64_t ldphi, int64_t p
             order_after_prev(s, static_cast<cudaStream_t>(stream));
             body(phi, ldphi, z, ldz, static_cast<cudaStream_t>(stream));
             mark_done(s, static_cast<cudaStream_t>(stream));
-        } else {
+        } else if (s->dense || s->ncols == 0 ||
+                   !adjoint_host_pipelined(s, phi, ldphi, p, z, ldz, s->m2, [&](void* t, cudaStream_t st) {
+                       void* zd = s->ypart.get(size_t(s->m2 * p) * s->csize());
+                       aca_vt_dev(s, t, p, zd, s->m2, st);
+                       return zd;
+                   })) {
             with_host_io(s, phi, ldphi, phirows, p, z, ldz, s->m2,
                          [&](void* din, int64_t ldi, void* dout, int64_t ldo, cudaStream_t st) {
                              body(din, ldi, dout, ldo, st);
