@@ -11,30 +11,34 @@
 //   GEMM1  T_j[row, i3] = sum_r W_j[row, r] U3_j[i3, r]   (K = slots, N = 16)
 //   GEMM2  Y[row, i3, :] += sum_j T_j[row, i3] X[j, :]     (K = columns)
 //
-// Slot stream.  K3W runs on its own padded copy of the W arena's fp16-split
-// A planes ([plane][k][row][kpad8], built once per store): columns are packed
-// back to back except that at most two columns overlap a K16 stage (a column
-// that would be the third starts the next stage).  Half 0 of a stage is its
-// first column, which ends in the stage (it may have started in the previous
-// one: a straddler), half 1 the second, which may continue into the next
-// stage as that stage's half 0; the converters add the two partials.
-// GEMM1 per stage: A1 = the stage's W planes (one bulk copy of a pre-swizzled
-// 16 KB block), B1 = a per-store block-diagonal table ([k][stage][i3 block] 4 fp16 planes of 16 n
-// x 16 slots: n = half c x 8 + i3 x 2 + (Tr, Ti); the column of half c; U3
-// 2^-e3 x 2^12 as the fp16 split; bulk-copied) — 4 tcgen05.mma (M = 128):
-// D1 = Wr B1a + Wi B1b as hi.hi + hi.lo + lo.hi, the hi planes of W against
-// [B hi ; B lo] in one N = 32 MMA each (the hi.lo terms land in columns
-// 16-31), into one of 8 TMEM buffers of 32 columns.  Converter warps read
-// D1 (tcgen05.ld), scale and split T into the A operand of GEMM2 at K position j % 16 (4 M = 128
-// blocks, one per i3 of the tile).  GEMM2 is the earlier K3 design: B = X as
-// fp16-split planes [Xr | Xi], [-Xi | Xr] (N = 64), 6 tcgen05.mma per i3
-// block per 16 columns, [Yr | Yi] += Tr [Xr | Xi] + Ti [-Xi | Xr]; chained
-// accumulation folded into a per-CTA L2 running sum.
+// Slot stream.  K3W runs on its own copy of the W arena's fp16-split A planes
+// (pre-swizzled 16 KB blocks [k][row tile][stage], built once per store):
+// columns are packed back to back except that at most two columns overlap a
+// K16 stage (a column that would be the third starts the next stage).  Half 0
+// of a stage is its first column, which ends in the stage (it may have
+// started in the previous one: a straddler), half 1 the second, which may
+// continue into the next stage as that stage's half 0; the converters add
+// the two partials.
+// GEMM1 per stage: A1 = the stage's W planes (one bulk copy), B1 = a
+// per-store block-diagonal table ([k][stage][i3 block], 4 fp16 planes of
+// 16 n x 16 slots: n = half c x 8 + i3 x 2 + (Tr, Ti) for the column of half
+// c; U3 2^-e3 x 2^12 as the fp16 split; bulk-copied) — 4 tcgen05.mma
+// (M = 128): D1 = Wr B1a + Wi B1b as hi.hi + hi.lo + lo.hi, the hi planes of
+// W against [B hi ; B lo] in one N = 32 MMA each (the hi.lo terms land in
+// columns 16-31), into one of 8 TMEM buffers of 32 columns.  Converter warps
+// read D1 (tcgen05.ld), scale and split T, and store it 4 columns at a time
+// into the A operand of GEMM2 at K position j % 16 (4 M = 128 blocks, one per
+// i3 of the tile).  GEMM2: B = X as fp16-split planes [Xr | Xi], [-Xi | Xr]
+// (N = 64) by TMA, 6 tcgen05.mma per i3 block per 16 columns, [Yr | Yi] +=
+// Tr [Xr | Xi] + Ti [-Xi | Xr]; chained accumulation folded into a per-CTA
+// L2 running sum.  The MMA thread issues the GEMM1s of GEMM2 stage kk + 1
+// before GEMM2 kk (the tensor pipe runs in order), so the converters fill one
+// A stage while GEMM2 runs on the other.
 //
 // Warp roles (512 threads, 1 CTA / SM, persistent over tiles):
 //   warp 0      TMA producer of the X planes (B of GEMM2)
 //   warp 1      MMA issuer (GEMM1 per stage, GEMM2 per 16 columns)
-//   warp 2      loader of the W stages (A1 planes by TMA, B1 block by bulk copy)
+//   warp 2      loader of the W stages (A1 and B1 blocks by bulk copy)
 //   warp 3      TMEM allocator (512 columns: GEMM2 accumulator 256, D1 8 x 32)
 //   warps 4-11  converters (D1 -> A2): lane quarter w & 3, i3 pair (w - 4) >> 2
 //   warps 12-15 chain fold + epilogue
