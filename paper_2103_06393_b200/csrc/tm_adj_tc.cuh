@@ -600,8 +600,17 @@ __global__ void adjg_split_phi_kernel(const float2* __restrict__ phi, int64_t ld
     const int t1 = tile / nt2, t2 = tile - t1 * nt2;
     const int t = int(threadIdx.x);
     const int i1 = t1 * TC_TI1 + (t & 3), i2 = t2 * TC_TI2 + (t >> 2);
+    // the component's scale: max over the pass's right-hand sides, reduced by the block
+    // (one load per thread instead of p)
+    __shared__ float wmx[TC_ROWS / 32];
     float m = 0.f;
-    for (int cc = 0; cc < p; ++cc) m = fmaxf(m, phimax[int64_t(cc) * q + k]);
+    for (int cc = t; cc < p; cc += TC_ROWS) m = fmaxf(m, phimax[int64_t(cc) * q + k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((t & 31) == 0) wmx[t >> 5] = m;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < TC_ROWS / 32; ++w) m = fmaxf(m, wmx[w]);
     const float sc = fp16_scale(m);
     float2 v = make_float2(0.f, 0.f);
     if (i1 < n1 && i2 < n2) {
@@ -625,10 +634,20 @@ __global__ void adjg_split_phi_kernel(const float2* __restrict__ phi, int64_t ld
 // Phi scales).  One block per column j; thread (c, i3 group) with the r3
 // slots innermost (contiguous in G); the i3 groups are summed in a fixed
 // order: bitwise reproducible.
+// kmax[k] = max over the pass's right-hand sides c of phimax[c q + k] (the
+// component's Phi scale, read by adjg_contract_kernel).
+__global__ void phimax_k_kernel(const float* __restrict__ phimax, int p, int q, float* __restrict__ kmax) {
+    for (int k = int(threadIdx.x); k < q; k += int(blockDim.x)) {
+        float m = 0.f;
+        for (int c = 0; c < p; ++c) m = fmaxf(m, phimax[int64_t(c) * q + k]);
+        kmax[k] = m;
+    }
+}
+
 __global__ void adjg_contract_kernel(const float2* __restrict__ G, int64_t gslots, int64_t nt, int p, int q,
                                      int64_t ncols, int n3, const TcDesc* __restrict__ tcd,
                                      const float2* __restrict__ arena, const int* __restrict__ kofs,
-                                     const float* __restrict__ phimax, float wsc, float2* __restrict__ z,
+                                     const float* __restrict__ kmax, float wsc, float2* __restrict__ z,
                                      int64_t ldz) {
     __shared__ float2 red[256];
     const int64_t j = blockIdx.x;
@@ -639,8 +658,7 @@ __global__ void adjg_contract_kernel(const float2* __restrict__ G, int64_t gslot
         float ar = 0.f, ai = 0.f;
         if (gi < ng) {
             for (int k = 0; k < q; ++k) {
-                float m = 0.f;
-                for (int cc = 0; cc < p; ++cc) m = fmaxf(m, phimax[int64_t(cc) * q + k]);
+                const float m = kmax[k];
                 const int64_t t = int64_t(k) * ncols + j;
                 const TcDesc d = tcd[t];
                 const float sk = ldexpf(1.f, -fexp_e3(d.fexp)) / (wsc * fp16_scale(m));

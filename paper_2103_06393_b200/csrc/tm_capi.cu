@@ -162,6 +162,7 @@ struct tm_store {
     int* d_kcr = nullptr;  // [q] the GEMM's K extent (rows) per component
     CUtensorMap wt_map{};
     DevBuf gbuf, phit;     // per call: G and the row-contiguous Phi planes
+    DevBuf gkmax;          // per call: the components' Phi scales (phimax_k_kernel)
     int64_t warena_rows = 0;
     CUtensorMap warena_map{};
     // K3W (tm_k3w_tc.cuh, many right-hand sides on a W-arena store): per-slot
@@ -1714,9 +1715,12 @@ void run_adjoint_gemm(tm_store* s, const float2* phi, int64_t ldphi, int64_t p, 
             }
         }
         if (pipe) split_upto(s->q);
+        float* kmax = static_cast<float*>(s->gkmax.get(size_t(s->q) * sizeof(float)));
+        phimax_k_kernel<<<1, 256, 0, st>>>(phimax, int(pb), s->q, kmax);
+        launched(cudaSuccess, "phimax_k_kernel");
         adjg_contract_kernel<<<unsigned(s->ncols), 256, 0, st>>>(
             G, kt, nt, int(pb), s->q, s->ncols, n3, s->d_tcd, static_cast<const float2*>(s->d_arena), s->d_kofs,
-            phimax, fp16_scale(s->vmax * 1.0001f), z + ldz * c0, ldz);
+            kmax, fp16_scale(s->vmax * 1.0001f), z + ldz * c0, ldz);
         launched(cudaSuccess, "adjg_contract_kernel");
         for (auto ev : arrived) CK(cudaEventDestroy(ev));
     }
