@@ -63,7 +63,9 @@ constexpr int K3_B_STAGE = 4 * K3_B_PLANE;       // [Xr|Xi] hi, [-Xi|Xr] hi, [Xr
 constexpr int K3_YCOLS = K3_NI3 * 2 * K3_P;      // TMEM columns of the GEMM2 accumulator
 constexpr int K3_ND1 = 8;                        // D1 (GEMM1 output) TMEM buffers of 32 columns (hi and lo halves)
 constexpr int K3_TCOLS = 512;                    // TMEM allocation
-constexpr int K3_THREADS = 16 * 32;
+constexpr int K3_CI = 2;                         // i3 per converter warp (1: 16 converter warps, measured slower)
+constexpr int K3_NCW = 4 * (K3_NI3 / K3_CI);     // converter warps (TMEM lane quarter x i3 group)
+constexpr int K3_THREADS = (8 + K3_NCW) * 32;
 // W stage: A1 = 4 planes [128 rows][16 slots] fp16 (SW32), then B1 = 4 planes [16 n][16 slots] fp16 (SW32)
 constexpr int K3_B1_PLANE = 16 * 32;
 constexpr int K3_B1_BYTES = 4 * K3_B1_PLANE;     // 2 KB
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < K3_NST; ++s) {
-            mbar_init(&full[s], 1 + 8 * 16);  // X TMA + 8 converter warps per column of the stage
+            mbar_init(&full[s], 1 + K3_NCW * 16);  // X TMA + every converter warp per column of the stage
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < K3_NWS; ++s) {
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
         }
         for (int s = 0; s < K3_ND1; ++s) {
             mbar_init(&dfull[s], 1);
-            mbar_init(&dempty[s], 8);  // the stage's 8 converter warps
+            mbar_init(&dempty[s], K3_NCW);  // the stage's converter warps
         }
         mbar_init(cfull, 1);
         mbar_init(cfree, 4);
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                 }
             }
         }
-    } else if (warp >= TC_PW0 && warp < TC_PW0 + 8) {
+    } else if (warp >= TC_PW0 && warp < TC_PW0 + K3_NCW) {
         // ------------------------------------------------------- converters
         // every converter warp takes every W stage: warp w reads TMEM lane quarter
         // w & 3 (row = i2 + 32 i1 of the tile) and converts the i3 pair 2 grp,
@@ -310,15 +312,15 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
         const int grp = (warp - TC_PW0) >> 2, quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const uint32_t rowbase = uint32_t(row) * 32u, xorv = (uint32_t(row) & 4u) << 2;
-        const uint32_t lane_addr = (uint32_t(quarter * 32) << 16) + uint32_t(4 * grp);
+        const uint32_t lane_addr = (uint32_t(quarter * 32) << 16) + uint32_t(2 * K3_CI * grp);
         const float tsc = g.tsc;
         uint32_t sg = 0;       // W stages of all tiles so far
         uint32_t tseq = 0;     // tiles so far: GEMM2 stage sequence = tseq nks + j / 16
         // [i3 of the pair][plane]: a shift register of the last 4 columns' fp16 values
         // (ba: the older two, bb: the newer two; a new column enters at the top of bb)
-        uint32_t ba[2][4], bb[2][4];
+        uint32_t ba[K3_CI][4], bb[K3_CI][4];
 #pragma unroll
-        for (int l = 0; l < 2; ++l)
+        for (int l = 0; l < K3_CI; ++l)
 #pragma unroll
             for (int pl = 0; pl < 4; ++pl) ba[l][pl] = bb[l][pl] = 0u;
         for (int64_t t = tstart; t < g.ntiles; t += tstep, ++tseq) {
@@ -328,29 +330,34 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
             int j = 0;           // next column to complete
             uint32_t fnext = fl[0];
             // D1 of stage kk is loaded while stage kk - 1 is converted (software pipelining);
-            // this warp's columns: half c at 8 c + 4 grp + (2 l + part), the hi.lo terms at + 16
-            uint32_t cur[16];
+            // this warp's columns: half c at 8 c + 2 K3_CI grp + (2 l + part), the hi.lo terms
+            // at + 16; cur = [half 0 | half 1 | half 0 hi.lo | half 1 hi.lo], NW words each
+            constexpr int NW = 2 * K3_CI;
+            uint32_t cur[4 * NW];
             auto load_d1 = [&](uint32_t sgx) {
                 const uint32_t dbx = sgx % K3_ND1;
                 mbar_wait(&dfull[dbx], (sgx / K3_ND1) & 1u);
                 tc_fence_after();
                 const uint32_t ta = tD1 + lane_addr + dbx * 32u;
-                tmem_ld4(ta, *reinterpret_cast<uint32_t(*)[4]>(&cur[0]));
-                tmem_ld4(ta + 8u, *reinterpret_cast<uint32_t(*)[4]>(&cur[4]));
-                tmem_ld4(ta + 16u, *reinterpret_cast<uint32_t(*)[4]>(&cur[8]));
-                tmem_ld4(ta + 24u, *reinterpret_cast<uint32_t(*)[4]>(&cur[12]));
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {  // columns + 0, 8, 16, 24
+                    if constexpr (NW == 4)
+                        tmem_ld4(ta + 8u * q4, *reinterpret_cast<uint32_t(*)[4]>(&cur[NW * q4]));
+                    else
+                        tmem_ld2(ta + 8u * q4, *reinterpret_cast<uint32_t(*)[2]>(&cur[NW * q4]));
+                }
             };
             load_d1(sg);
-            float t1prev[4] = {0.f, 0.f, 0.f, 0.f};  // the previous stage's half 1 (a straddler's head)
+            float t1prev[NW] = {};  // the previous stage's half 1 (a straddler's head)
             for (int kk = 0; kk < nws; ++kk, ++sg) {
                 const uint32_t f = fnext;
                 if (kk + 1 < nws) fnext = fl[kk + 1];
                 tmem_ld_wait_regs(cur);
-                float t0[4], t1[4];
+                float t0[NW], t1[NW];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    t0[e] = __uint_as_float(cur[e]) + __uint_as_float(cur[8 + e]);
-                    t1[e] = __uint_as_float(cur[4 + e]) + __uint_as_float(cur[12 + e]);
+                for (int e = 0; e < NW; ++e) {
+                    t0[e] = __uint_as_float(cur[e]) + __uint_as_float(cur[2 * NW + e]);
+                    t1[e] = __uint_as_float(cur[NW + e]) + __uint_as_float(cur[3 * NW + e]);
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -359,10 +366,10 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                 if (f & 4u) {
                     // half 0 continues the previous stage's half 1 (a column straddling the boundary)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) t0[e] += t1prev[e];
+                    for (int e = 0; e < NW; ++e) t0[e] += t1prev[e];
                 }
 #pragma unroll
-                for (int e = 0; e < 4; ++e) t1prev[e] = t1[e];
+                for (int e = 0; e < NW; ++e) t1prev[e] = t1[e];
                 const int nc = 1 + ((f & 3u) == 3u ? 1 : 0);  // columns ending here: half 0, half 1 if it ends
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
@@ -370,7 +377,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                     const float* tv = c ? t1 : t0;
                     const uint32_t ks = uint32_t(j) & 15u, sub = ks & 3u;
 #pragma unroll
-                    for (int l = 0; l < 2; ++l) {
+                    for (int l = 0; l < K3_CI; ++l) {
                         uint32_t hi, lo;
                         f16_split2(f2_pack(tv[2 * l] * tsc, tv[2 * l + 1] * tsc), hi, lo);
                         // shift in: (ba, bb) <- (ba.hi16 bb.lo16, bb.hi16 new)
@@ -391,12 +398,12 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                         // the register holds columns (ks & ~3) .. ks in its top sub + 1 positions
                         const uint32_t drop = 16u * (3u - sub);
 #pragma unroll
-                        for (int l = 0; l < 2; ++l)
+                        for (int l = 0; l < K3_CI; ++l)
 #pragma unroll
                             for (int pl = 0; pl < 4; ++pl) {
                                 uint64_t v64 = (uint64_t(bb[l][pl]) << 32) | ba[l][pl];
                                 if (drop) v64 >>= drop;  // a tile's last, partial group
-                                *reinterpret_cast<uint64_t*>(st + (2 * grp + l) * K3_A_BLOCK + pl * K3_A_PLANE) = v64;
+                                *reinterpret_cast<uint64_t*>(st + (K3_CI * grp + l) * K3_A_BLOCK + pl * K3_A_PLANE) = v64;
                             }
                         fence_proxy_async_smem();
                         __syncwarp();
@@ -407,7 +414,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                 }
             }
         }
-    } else if (warp >= TC_PW0 + 8) {
+    } else if (warp >= TC_PW0 + K3_NCW) {
         // ------------------------------------------ chain fold + epilogue
         // Running sum of the tile: rsum[blockIdx.x][col / 4][row] as float4
         // (4 consecutive TMEM columns), L2-resident; the first chain stores,
