@@ -190,6 +190,9 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
             const uint32_t id1w = umma_idesc_f16(TC_ROWS, 32, false, false);
             uint32_t s = 0, ph = 0, gch = 0;
             uint32_t sg = 0;  // W stages issued (all tiles): W ring slot sg % K3_NWS, D1 buffer sg % K3_ND1
+            const uint64_t wdesc0 = umma_smem_desc(smem_u32(sW), 256, 6);
+            const uint64_t adesc0 = umma_smem_desc(smem_u32(sA), 256, 6);
+            const uint64_t bdesc0 = umma_smem_desc(smem_u32(sB), 256, 6);
             for (int64_t t = tstart; t < g.ntiles; t += tstep) {
                 const K3Tile tl = k3_tile(g, g.tile0 + t);
                 // gend[k][kk]: W stages up to the last one holding a column of GEMM2 stage kk
@@ -203,15 +206,14 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                         mbar_wait(&wfull[ws], wph);
                         mbar_wait(&dempty[db], dph ^ 1u);
                         tc_fence_after();
-                        const uint32_t a0 = smem_u32(sW + ws * K3_W_STAGE), b0 = a0 + K3_W_B1;
-                        const uint64_t Arh = umma_smem_desc(a0, 256, 6);
-                        const uint64_t Arl = umma_smem_desc(a0 + K3_A_PLANE, 256, 6);
-                        const uint64_t Aih = umma_smem_desc(a0 + 2 * K3_A_PLANE, 256, 6);
-                        const uint64_t Ail = umma_smem_desc(a0 + 3 * K3_A_PLANE, 256, 6);
-                        const uint64_t Bah = umma_smem_desc(b0, 256, 6);
-                        const uint64_t Bal = umma_smem_desc(b0 + K3_B1_PLANE, 256, 6);
-                        const uint64_t Bbh = umma_smem_desc(b0 + 2 * K3_B1_PLANE, 256, 6);
-                        const uint64_t Bbl = umma_smem_desc(b0 + 3 * K3_B1_PLANE, 256, 6);
+                        // descriptors: the start-address field is addr >> 4 (< 2^14 for shared
+                        // memory), so an offset is a plain add to the slot's base descriptor
+                        const uint64_t Arh = wdesc0 + uint64_t(ws) * (K3_W_STAGE >> 4);
+                        const uint64_t Arl = Arh + (K3_A_PLANE >> 4);
+                        const uint64_t Aih = Arh + (2 * K3_A_PLANE >> 4);
+                        const uint64_t Ail = Arh + (3 * K3_A_PLANE >> 4);
+                        const uint64_t Bah = Arh + (K3_W_B1 >> 4);
+                        const uint64_t Bbh = Bah + (2 * K3_B1_PLANE >> 4);
                         const uint32_t d = tD1 + db * 32u;
                         // D1 = Wr B1a + Wi B1b (Tr = Wr U3r - Wi U3i, Ti = Wr U3i + Wi U3r in B1's
                         // columns): the hi planes of A meet [B hi ; B lo] in one N = 32 MMA (columns
@@ -221,8 +223,6 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                         mma_f16(d, Arl, Bah, id1, 1);
                         mma_f16(d, Aih, Bbh, id1w, 1);
                         mma_f16(d, Ail, Bbh, id1, 1);
-                        (void)Bal;
-                        (void)Bbl;
                         mma_commit(&wempty[ws]);
                         mma_commit(&dfull[db]);
                         ++snext;
@@ -241,20 +241,17 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                     }
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
-                    const uint32_t a0 = smem_u32(sA + s * K3_A_STAGE);
-                    const uint32_t b0 = smem_u32(sB + s * K3_B_STAGE);
-                    const uint64_t Bah = umma_smem_desc(b0, 256, 6);
-                    const uint64_t Bbh = umma_smem_desc(b0 + K3_B_PLANE, 256, 6);
-                    const uint64_t Bal = umma_smem_desc(b0 + 2 * K3_B_PLANE, 256, 6);
-                    const uint64_t Bbl = umma_smem_desc(b0 + 3 * K3_B_PLANE, 256, 6);
+                    const uint64_t Bah = bdesc0 + uint64_t(s) * (K3_B_STAGE >> 4);
+                    const uint64_t Bbh = Bah + (K3_B_PLANE >> 4);
+                    const uint64_t Bal = Bah + (2 * K3_B_PLANE >> 4);
+                    const uint64_t Bbl = Bah + (3 * K3_B_PLANE >> 4);
                     const uint32_t acc = cpos > 0 ? 1u : 0u;
 #pragma unroll
                     for (int l = 0; l < K3_NI3; ++l) {
-                        const uint32_t ab = a0 + l * K3_A_BLOCK;
-                        const uint64_t Arh = umma_smem_desc(ab, 256, 6);
-                        const uint64_t Arl = umma_smem_desc(ab + K3_A_PLANE, 256, 6);
-                        const uint64_t Aih = umma_smem_desc(ab + 2 * K3_A_PLANE, 256, 6);
-                        const uint64_t Ail = umma_smem_desc(ab + 3 * K3_A_PLANE, 256, 6);
+                        const uint64_t Arh = adesc0 + uint64_t(s) * (K3_A_STAGE >> 4) + uint64_t(l) * (K3_A_BLOCK >> 4);
+                        const uint64_t Arl = Arh + (K3_A_PLANE >> 4);
+                        const uint64_t Aih = Arh + (2 * K3_A_PLANE >> 4);
+                        const uint64_t Ail = Arh + (3 * K3_A_PLANE >> 4);
                         const uint32_t d = tmem + uint32_t(l * 2 * K3_P);
                         // [Yr | Yi] += Tr [Xr | Xi] + Ti [-Xi | Xr], each as hi.hi + hi.lo + lo.hi
                         mma_f16(d, Arh, Bah, id2, acc);
