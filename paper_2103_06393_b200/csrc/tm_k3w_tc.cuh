@@ -230,11 +230,15 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                     }
                 };
                 int cpos = 0;
+                const int last = g.nks - 1;
+                int gnext = ge[min(1, last)];  // gend one GEMM2 stage ahead, loaded a stage early
                 for (int kk = 0; kk < g.nks; ++kk) {
+                    const int need = gnext;
+                    gnext = ge[min(kk + 2, last)];
                     // GEMM1 of every W stage holding a column of GEMM2 stages kk and kk + 1,
                     // issued before GEMM2 kk: the tensor pipe runs in order, so the converters
                     // fill stage kk + 1 while GEMM2 kk executes (the A ring holds two stages)
-                    gemm1_until(ge[kk + 1 < g.nks ? kk + 1 : kk]);
+                    gemm1_until(need);
                     if (cpos == 0) {
                         mbar_wait(cfree, (gch & 1) ^ 1);  // the previous chain has been folded
                         tc_fence_after();
